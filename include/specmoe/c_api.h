@@ -1,0 +1,280 @@
+/*
+ * specmoe/c_api.h — the C-ABI drop-in boundary of the B200 verify step.
+ *
+ * Plain pointers and sizes only (no torch / CUDA types in the signatures):
+ * streams are passed as `smo_stream` (a cudaStream_t, NULL = legacy default).
+ * Every call is asynchronous on the given stream unless stated otherwise and
+ * returns an smo_status; the message of the last failure on the calling host
+ * thread is available from smo_last_error(). The caller owns every tensor
+ * passed in; the library owns only handle-scoped resources (engine, streamer).
+ *
+ * Each entry cites the reference interface it realises (file:line into
+ * /root/reference/proj). The reference has no FFI of its own: its boundary is
+ * the header-only C++ API `moeplan::*`; INTEGRATION.md shows the binding a
+ * maintainer adds on that side.
+ */
+#ifndef SPECMOE_C_API_H
+#define SPECMOE_C_API_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SMO_OK = 0,
+  SMO_INVALID_ARG = 1, /* std::invalid_argument in the reference (attention.hpp:92-144) */
+  SMO_CAPACITY = 2,    /* moeplan::CapacityError (memory.hpp:15) */
+  SMO_CUDA = 3,
+  SMO_NCCL = 4,
+  SMO_UNSUPPORTED = 5
+} smo_status;
+
+typedef void* smo_stream;
+
+const char* smo_last_error(void);
+const char* smo_version(void);
+/* Number of kernels this library has launched since it was loaded. */
+uint64_t smo_launch_count(void);
+int smo_device_sm_count(int device);
+
+/* ---- procedural synthetic tensors -------------------------
+ * dst[i] = bf16(fl(float(2*u24 - 2^24) * fl(scale*2^-24))),
+ * u24 = splitmix64(splitmix64(seed ^ tensor_id*0x9e3779b97f4a7c15 ^ (base+i)))>>40
+ * — the reference RNG family (specdec.hpp:34-39).                           */
+smo_status smo_fill_uniform_bf16(void* dst, uint64_t count, uint64_t seed, uint64_t tensor_id,
+                                 uint64_t base, float scale, smo_stream stream);
+
+/* ---- K1: chunked verification attention ------------------------------------
+ * Realises moeplan::chunked_attention (attention.hpp:117-156) batched over
+ * requests and GQA heads in bf16: prefix keys implicitly visible, the n x n
+ * draft block gated by a bit-packed compact mask (attention.hpp:41-58).
+ *   q       bf16 [b*n, n_q, d]          (row r*n+i = draft i of request r)
+ *   k_cache bf16 [b, n_kv, s_max, d]    (draft rows already at prefix_r + i)
+ *   v_cache bf16 [b, n_kv, s_max, d]
+ *   mask    u64  [b*n]  bit j of row (r,i) = draft j visible to draft i
+ *   prefix  i32  [b]
+ *   out     bf16 [b*n, n_q, d]
+ * n <= 64, n*(n_q/n_kv) <= 128, d in {64,128}. Errors: SMO_INVALID_ARG with
+ * the reference's messages.                                                 */
+typedef struct {
+  const void* q;
+  const void* k_cache;
+  const void* v_cache;
+  const uint64_t* mask;
+  const int32_t* prefix_len;
+  void* out;
+  int32_t b, n, n_q, n_kv, d, s_max;
+  int32_t max_prefix; /* host upper bound of prefix_len (split planning) */
+  void* workspace;    /* >= smo_verify_attention_workspace() bytes */
+  size_t workspace_bytes;
+} smo_attn_args;
+size_t smo_verify_attention_workspace(const smo_attn_args* a);
+smo_status smo_verify_attention(const smo_attn_args* a, smo_stream stream);
+
+/* The reference's desk-scale fp64 operator, one head of one request, host
+ * buffers in and out, computed by an fp64 CUDA kernel (synchronous).
+ * Same contract as moeplan::chunked_attention (attention.hpp:117); the
+ * messages of attention.hpp:96-144 are reported through smo_last_error().
+ * Q n x d, K/V (p+n) x d row-major, mask n x n bytes (1 = visible).        */
+smo_status smo_chunked_attention_f64(size_t n, size_t p, size_t d, const double* Q,
+                                     const double* K, const double* V, size_t mask_n,
+                                     const uint8_t* mask, double* out);
+
+/* ---- K2: router top-k -------------------------------------------------------
+ * logits[t,e] = fp32 x[t,:].w[e,:] in the fixed order of DESIGN.md §3.3 (so
+ * ids are bit-exact vs the oracle); top-k ties to the lower expert id; weights
+ * = softmax over the k selected logits. x bf16 [T,h], w bf16 [E,h]; h%256==0,
+ * E <= 64, k <= 8. logits_out may be NULL. (n_activate: config.hpp:51)     */
+smo_status smo_router_topk(const void* x, const void* w_router, int32_t T, int32_t h, int32_t E,
+                           int32_t k, float* logits_out, int32_t* ids, float* weights,
+                           smo_stream stream);
+
+/* ---- K3: permute / unpermute-combine ---------------------------------------
+ * Stable counting sort of the T*k (token,slot) pairs by expert id:
+ * offsets i32 [E+1], perm i32 [T*k] (source pair at each sorted position),
+ * pos i32 [T*k] (sorted position of each pair), x_perm bf16 [T*k, h] rows
+ * gathered from x bf16 [T,h] (x/x_perm may be NULL to skip the gather).    */
+smo_status smo_permute(const int32_t* ids, int32_t T, int32_t k, int32_t E, const void* x, int32_t h,
+                       int32_t* offsets, int32_t* perm, int32_t* pos, void* x_perm,
+                       smo_stream stream);
+/* residual[t,:] += sum_{j<k} weights[t,j] * y_perm[pos[t*k+j], :]  (fp32,
+ * j order fixed, no atomics). y_perm fp32 [T*k, h].                         */
+smo_status smo_unpermute_combine(const float* y_perm, const int32_t* pos, const float* weights,
+                                 int32_t T, int32_t k, int32_t h, float* residual, smo_stream stream);
+
+/* ---- K4: tcgen05 GEMMs ------------------------------------------------------
+ * out[t, n] = sum_c x[t,c] * W_g[n,c] for the rows t of group g
+ * (row_offsets[g] <= t < row_offsets[g+1]); W_g = pool block w_index[g].
+ * SWIGLU: out = bf16(silu(x W_g^T) * (x U_g^T)) with U from w_up.
+ * ARGMAX: no output matrix; (max, index) partials per 128-row weight tile
+ * into argmax_val/argmax_idx [rows, N/128] (the LM-head epilogue of K6).
+ * Weights are row-major [N, K] per block (nn.Linear layout) — the MMA's
+ * 128-row A operand ("swap-AB": tokens are the small N side).              */
+enum {
+  SMO_EPI_BF16 = 0,
+  SMO_EPI_F32 = 1,
+  SMO_EPI_F32_ADD = 2,
+  SMO_EPI_SWIGLU = 3,
+  SMO_EPI_ARGMAX = 4
+};
+typedef struct {
+  const void* x;              /* bf16 [rows, K] */
+  int32_t rows, K, N, groups;
+  const int32_t* row_offsets; /* device [groups+1]; NULL: one group = all rows */
+  int32_t max_rows_per_group; /* host bound (grid sizing); <= rows */
+  const void* w;              /* bf16 pool, block b at w + b*w_block_stride */
+  const void* w_up;           /* SWIGLU second weight (same pool layout) */
+  uint64_t w_block_stride;    /* bytes between pool blocks */
+  int32_t w_pool_blocks;
+  const int32_t* w_index;     /* device [groups] pool block per group; NULL = g */
+  int32_t epilogue;
+  void* out;                  /* bf16 or f32 [rows, ldo] */
+  int64_t ldo;
+  float* argmax_val;          /* [rows, N/128] */
+  int32_t* argmax_idx;
+  int32_t split_k;            /* 1 (reserved) */
+} smo_gemm_args;
+smo_status smo_gemm(const smo_gemm_args* a, smo_stream stream);
+
+/* ---- support ops of the verify layer (standard Mixtral block, not in the
+ *      reference: SURVEY.md §2.3 "support")                                 */
+/* y bf16 [T,h] = x f32 [T,h] * rsqrt(mean(x^2)+eps) * gain bf16 [h] */
+smo_status smo_rmsnorm(const float* x, const void* gain, int32_t T, int32_t h, float eps, void* y,
+                       smo_stream stream);
+/* x f32 [T,h] = embed bf16 [V,h] rows at tokens [T] */
+smo_status smo_embed(const int32_t* tokens, const void* embed, int32_t T, int32_t h, float* x,
+                     smo_stream stream);
+/* qkv bf16 [b*n, (n_q+2 n_kv) d]: RoPE (rotate-half, theta) on q and k at
+ * position prefix[r] + depth(r,i) (depth = i for chains, from parent[]
+ * otherwise), q written to q_out [b*n, n_q, d]; k/v appended to the caches
+ * at row prefix[r] + i.                                                     */
+smo_status smo_rope_append(const void* qkv, const int32_t* prefix_len, const int32_t* parent,
+                           int32_t b, int32_t n, int32_t n_q, int32_t n_kv, int32_t d, int32_t s_max,
+                           float theta, void* q_out, void* k_cache, void* v_cache, smo_stream stream);
+/* Synthetic prefix KV: cache[r,h,pos,c] for pos < prefix[r] =
+ * uniform(seed, tensor_id, idx = ((r*n_kv+h) << 32) | (pos*d + c)).       */
+smo_status smo_fill_kv_prefix(void* cache, const int32_t* prefix_len, int32_t b, int32_t n_kv,
+                              int32_t d, int32_t s_max, uint64_t seed, uint64_t tensor_id,
+                              smo_stream stream);
+
+/* ---- K6: argmax + greedy accept + KV rollback ------------------------------
+ * Greedy verification restating specdec.hpp:65-76 with the Bernoulli draw
+ * replaced by argmax(logits of the parent row) == token. Chain when parent
+ * is NULL; tree otherwise (parent[r*n+i] < i, -1 for the root row 0): the
+ * longest matching root path, ties to the lower node id.
+ * acc_len[b] accepted drafts (committed = acc_len + 1, config.hpp:69-70),
+ * bonus[b] = argmax at the accepted tip, keep[b*n] accepted rows in path
+ * order (root first, -1 padded).                                           */
+smo_status smo_argmax_reduce(const float* part_val, const int32_t* part_idx, int32_t rows,
+                             int32_t parts, int32_t* target, smo_stream stream);
+smo_status smo_argmax_rows(const float* logits, int32_t rows, int32_t V, int32_t* target,
+                           smo_stream stream);
+smo_status smo_greedy_accept(const int32_t* tokens, const int32_t* target, const int32_t* parent,
+                             int32_t b, int32_t n, int32_t* acc_len, int32_t* bonus, int32_t* keep,
+                             smo_stream stream);
+/* Tree rollback: move the accepted rows keep[r, 0..acc] of every layer's
+ * K/V to prefix[r] + 0..acc (chains are already in place) and set
+ * kv_len[r] = prefix[r] + acc_len[r] + 1. caches: n_layers pointers.       */
+smo_status smo_kv_rollback(void* const* k_caches, void* const* v_caches, int32_t n_layers,
+                           const int32_t* prefix_len, const int32_t* acc_len, const int32_t* keep,
+                           int32_t b, int32_t n, int32_t n_kv, int32_t d, int32_t s_max,
+                           int32_t* kv_len, smo_stream stream);
+
+/* ---- K5 + engine: the measured verify step ---------------------------------
+ * The engine owns the model (procedural weights; experts in pinned host
+ * DRAM), the expert streamer (copy-engine stream, double-buffered HBM slots,
+ * hot-expert cache) and the KV cache. One verify() = the reference's target
+ * DAG (pipeline.hpp:147-206) realised on streams + events.                 */
+typedef struct {
+  int32_t hidden;      /* h        (ModelSpec.h, config.hpp:48) */
+  int32_t inter;       /* h_i      (ModelSpec.h_i) */
+  int32_t n_expert;    /* E        (ModelSpec.n_expert) */
+  int32_t top_k;       /* n_activate */
+  int32_t n_layers;
+  int32_t n_q_heads;
+  int32_t n_kv_heads;  /* h / g */
+  int32_t head_dim;
+  int32_t vocab;
+  float rope_theta;
+  float rms_eps;
+  uint64_t seed;
+  float lm_scale;      /* multiplier on the LM-head init scale (margin screening) */
+  float router_scale;  /* multiplier on the router init scale */
+} smo_model_config;
+
+enum { SMO_ENGINE_DEBUG = 1 /* keep per-layer intermediates for parity tests */ };
+
+typedef struct {
+  int32_t max_batch;          /* b */
+  int32_t max_verify;         /* n = k+1 rows per request (chain or tree) */
+  int32_t max_seq;            /* KV capacity per request (s_max) */
+  int32_t hbm_slots;          /* expert-layer staging slots, >= 2 */
+  int64_t expert_cache_bytes; /* hot-expert HBM cache (MemoryPolicy.expert_cache_bytes) */
+  int32_t host_alias_layers;  /* 0: one pinned expert buffer per layer; A: layer l uses l % A */
+  int32_t device;
+  int32_t flags;
+  int32_t ep_rank, ep_size;   /* expert parallelism: this rank owns experts e % ep_size == ep_rank */
+  void* nccl_comm;            /* ncclComm_t when ep_size > 1 */
+} smo_engine_options;
+
+typedef struct smo_engine smo_engine;
+
+smo_status smo_engine_create(const smo_model_config* cfg, const smo_engine_options* opt,
+                             smo_engine** out);
+smo_status smo_engine_destroy(smo_engine* e);
+/* Fill the synthetic prefix KV of every layer for requests 0..b-1. */
+smo_status smo_engine_fill_prefix(smo_engine* e, const int32_t* prefix_len_host, int32_t b);
+
+typedef struct {
+  int32_t b, n;
+  const int32_t* tokens;     /* [b*n], row 0 of each request = root token */
+  const int32_t* parent;     /* [b*n] or NULL (chain) */
+  const int32_t* prefix_len; /* [b] */
+  int32_t on_device;         /* 0: host pointers (copied in on the stream) */
+} smo_verify_batch;
+
+typedef struct {
+  int32_t* acc_len; /* [b] */
+  int32_t* bonus;   /* [b] */
+  int32_t* keep;    /* [b*n] or NULL */
+  int32_t* target;  /* [b*n] argmax per row, or NULL */
+  int32_t on_device;
+} smo_verify_output;
+
+smo_status smo_engine_verify(smo_engine* e, const smo_verify_batch* in, smo_verify_output* out,
+                             smo_stream stream);
+
+/* Measured stage durations of the last verify (seconds, CUDA events), in the
+ * reference's IterationBreakdown vocabulary (report.hpp:27-37).             */
+typedef struct {
+  double target_total;
+  double attention;    /* K1 (the reference's CPU_ATTN slot) */
+  double gpu_moe;      /* K4 + combine */
+  double h2d_transfer; /* K5 copy-engine busy time */
+  double others;       /* norms, QKV/O GEMMs, router, permute, LM head, accept */
+  double h2d_bytes;    /* bytes streamed */
+  double launches;     /* kernels launched */
+} smo_stage_times;
+smo_status smo_engine_last_times(smo_engine* e, smo_stage_times* t);
+
+/* Debug intermediates of the last verify (engine created with SMO_ENGINE_DEBUG).
+ * name: "x_in" f32 [T,h] layer input, "xn1" bf16, "q" bf16 [T,n_q,d],
+ * "attn" bf16 [T,n_q,d], "xn2" bf16 [T,h], "logits_r" f32 [T,E],
+ * "ids" i32 [T,k], "weights" f32 [T,k], "offsets" i32 [E+1], "pos" i32 [T*k],
+ * "x_out" f32 [T,h]; layer -1 with "xf" bf16 [T,h], "logits" f32 [T,V].
+ * Copies into host dst (synchronous).                                      */
+smo_status smo_engine_debug_tensor(smo_engine* e, const char* name, int32_t layer, void* dst,
+                                   size_t bytes);
+/* Device pointer of a weight tensor ("embed","lm_head","final_norm" with
+ * layer -1; "wqkv","wo","attn_norm","ffn_norm","router" per layer) or of an
+ * expert's pinned host block ("expert_host", layer, expert): [W1|W3|W2].  */
+smo_status smo_engine_tensor_ptr(smo_engine* e, const char* name, int32_t layer, int32_t expert,
+                                 void** ptr, size_t* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECMOE_C_API_H */

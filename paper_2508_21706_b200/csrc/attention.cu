@@ -1,0 +1,605 @@
+// attention.cu — K1: chunked verification attention on tcgen05.
+//
+// Semantics: moeplan::chunked_attention (attention.hpp:117-156) batched over
+// requests and GQA heads: for draft query i of request r, the s_r prefix keys
+// are implicitly visible and draft key j is visible iff bit j of mask[r,i]
+// (the compact n x n mask, attention.hpp:41-58; never expanded). Softmax is
+// stabilised by the running row maximum (online across 128-key chunks).
+//
+// Layout / mapping:
+//  * work item = (request r, KV head h, KV split); persistent CTAs stride over
+//    items. The g*n query rows sharing KV head h (row = i*g + hh) form the
+//    M=128 A tile (Q, K-major, TMA 3D box {64, g, n}); a 128-key chunk of K is
+//    the B operand of S = Q K^T (N=128); P (bf16, written by the softmax warps
+//    into a swizzled K-major smem tile) times V (MN-major B, N=d) gives the
+//    chunk's O contribution in TMEM, folded into fp32 registers with the
+//    online-softmax rescale.
+//  * warps: w0 TMA producer, w1 TMEM alloc + MMA issuer, w2..w5 softmax
+//    (thread = query row = TMEM lane).
+//  * TMEM: S double buffer cols [0,256), O-chunk double buffer cols [256,512).
+//  * HBM-bound: algorithmic bytes = 2*b*(s+n)*n_kv*d*2 (roofline.hpp:88) +
+//    Q/O; FLOPs = 4*n*(s+n)*n_q*d per request.
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+
+namespace smo {
+
+namespace {
+
+constexpr int kThreads = 192;
+constexpr int kChunk = 128;
+constexpr int kKvStages = 2;
+
+struct AttnParams {
+  const uint64_t* mask;
+  const int32_t* prefix;
+  uint16_t* out;
+  float* ws_o;
+  float2* ws_ml;
+  int b, n, n_q, n_kv, g, rows, s_max;
+  int splits, split_chunks, items;
+  float scale_log2;
+};
+
+template <int D>
+struct AttnSmem {
+  static constexpr int kKBlocks = D / 64;
+  static constexpr int kQBytes = kKBlocks * 16384;      // 128 rows x D
+  static constexpr int kKvBytes = kKBlocks * 16384;     // 128 keys x D (K or V)
+  static constexpr int kPBytes = 2 * 16384;             // 128 rows x 128 keys
+  static constexpr int kQOff = 0;
+  static constexpr int kKvOff = 2 * kQBytes;
+  static constexpr int kPOff = kKvOff + kKvStages * 2 * kKvBytes;
+  static constexpr int kTotal = kPOff + kPBytes;
+};
+
+struct ItemInfo {
+  int r, h, c_begin, c_end, keys;
+};
+
+__device__ __forceinline__ ItemInfo item_info(const AttnParams& p, int item) {
+  ItemInfo it;
+  const int pair = item / p.splits, split = item % p.splits;
+  it.r = pair / p.n_kv;
+  it.h = pair % p.n_kv;
+  it.keys = p.prefix[it.r] + p.n;
+  const int chunks = (it.keys + kChunk - 1) / kChunk;
+  it.c_begin = min(split * p.split_chunks, chunks);
+  it.c_end = min(it.c_begin + p.split_chunks, chunks);
+  return it;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    verify_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv_k,
+                            const __grid_constant__ CUtensorMap tm_kv_v, AttnParams p) {
+  using L = AttnSmem<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t q_full[2], q_empty[2];
+  __shared__ __align__(8) uint64_t kv_full[kKvStages], kv_empty[kKvStages];
+  __shared__ __align__(8) uint64_t s_full[2], s_empty[2], o_full[2], o_empty[2], p_full;
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 4);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_empty[i], 4);
+    }
+    for (int i = 0; i < kKvStages; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    mbar_init(&p_full, 4);
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_kv_k);
+    tma_prefetch_desc(&tm_kv_v);
+  }
+  if (warp == 1) tmem_alloc<512>(&tmem_base_sh);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  const int kv_row_base_stride = p.s_max;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (elect_one()) {
+      int used = 0, gc = 0;
+      for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+        const ItemInfo it = item_info(p, item);
+        if (it.c_end <= it.c_begin) continue;
+        const int qb = used & 1;
+        mbar_wait(&q_empty[qb], ((used >> 1) & 1) ^ 1);
+        ++used;
+        const uint32_t qbytes = uint32_t(L::kKBlocks * 64 * p.g * p.n * 2);
+        mbar_arrive_expect_tx(&q_full[qb], qbytes);
+        for (int kb = 0; kb < L::kKBlocks; ++kb)
+          tma_load_3d(smem + L::kQOff + qb * L::kQBytes + kb * 16384, &tm_q, &q_full[qb], kb * 64, it.h * p.g,
+                      it.r * p.n);
+        const int row_base = (it.r * p.n_kv + it.h) * kv_row_base_stride;
+        for (int c = it.c_begin; c < it.c_end; ++c, ++gc) {
+          const int s = gc % kKvStages;
+          mbar_wait(&kv_empty[s], ((gc / kKvStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&kv_full[s], uint32_t(2 * L::kKvBytes));
+          uint8_t* kdst = smem + L::kKvOff + s * 2 * L::kKvBytes;
+          uint8_t* vdst = kdst + L::kKvBytes;
+          for (int kb = 0; kb < L::kKBlocks; ++kb) {
+            tma_load_2d(kdst + kb * 16384, &tm_kv_k, &kv_full[s], kb * 64, row_base + c * kChunk);
+            tma_load_2d(vdst + kb * 16384, &tm_kv_v, &kv_full[s], kb * 64, row_base + c * kChunk);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      const uint32_t id_s = make_idesc_bf16(128, kChunk);
+      const uint32_t id_o = make_idesc_bf16(128, D, /*b_mn_major=*/1);
+      int used = 0, gc = 0;
+      uint32_t p_phase = 0;
+      for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+        const ItemInfo it = item_info(p, item);
+        if (it.c_end <= it.c_begin) continue;
+        const int qb = used & 1;
+        mbar_wait(&q_full[qb], (used >> 1) & 1);
+        ++used;
+        const uint32_t q_addr = smem_u32(smem + L::kQOff + qb * L::kQBytes);
+        const int nch = it.c_end - it.c_begin;
+        auto issue_s = [&](int ci) {
+          const int g2 = gc + ci;
+          const int s = g2 % kKvStages, sb = g2 & 1;
+          mbar_wait(&kv_full[s], (g2 / kKvStages) & 1);
+          mbar_wait(&s_empty[sb], ((g2 >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t k_addr = smem_u32(smem + L::kKvOff + s * 2 * L::kKvBytes);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk / 4) * 16384 + (kk % 4) * 32;
+            umma_bf16(tmem + sb * 128, make_sdesc_sw128(q_addr + off, 16, 1024),
+                      make_sdesc_sw128(k_addr + off, 16, 1024), id_s, kk > 0 ? 1u : 0u);
+          }
+          umma_commit(&s_full[sb]);
+          if (ci == nch - 1) umma_commit(&q_empty[qb]);
+        };
+        issue_s(0);
+        for (int ci = 0; ci < nch; ++ci) {
+          if (ci + 1 < nch) issue_s(ci + 1);
+          const int g2 = gc + ci;
+          const int s = g2 % kKvStages, ob = g2 & 1;
+          mbar_wait(&p_full, p_phase);
+          p_phase ^= 1;
+          mbar_wait(&o_empty[ob], ((g2 >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t p_addr = smem_u32(smem + L::kPOff);
+          const uint32_t v_addr = smem_u32(smem + L::kKvOff + s * 2 * L::kKvBytes + L::kKvBytes);
+#pragma unroll
+          for (int kk = 0; kk < kChunk / 16; ++kk) {
+            const uint32_t aoff = (kk / 4) * 16384 + (kk % 4) * 32;
+            umma_bf16(tmem + 256 + ob * 128, make_sdesc_sw128(p_addr + aoff, 16, 1024),
+                      make_sdesc_sw128(v_addr + kk * 2048, 16384, 1024), id_o, kk > 0 ? 1u : 0u);
+          }
+          umma_commit(&o_full[ob]);
+          umma_commit(&kv_empty[s]);
+        }
+        gc += nch;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax
+    const int q4 = warp & 3;
+    const int row = q4 * 32 + lane;
+    const uint32_t tlane = uint32_t(q4 * 32) << 16;
+    uint8_t* pbuf = smem + L::kPOff;
+    int gc = 0;
+    for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+      const ItemInfo it = item_info(p, item);
+      const int nch = it.c_end - it.c_begin;
+      const bool live = row < p.rows;
+      const int qi = live ? row / p.g : 0;
+      const int hh = live ? row % p.g : 0;
+      const uint64_t mbits = live ? p.mask[it.r * p.n + qi] : 0ull;
+      const int prefix = it.keys - p.n;
+      float O[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) O[c] = 0.f;
+      float m_run = -INFINITY, l_run = 0.f, m_fold = -INFINITY, m_pend = -INFINITY;
+      for (int ci = 0; ci < nch; ++ci) {
+        const int g2 = gc + ci;
+        const int sb = g2 & 1;
+        const int key0 = (it.c_begin + ci) * kChunk;
+        mbar_wait(&s_full[sb], (g2 >> 1) & 1);
+        tc_fence_after();
+        // pass 1: masked row max of this chunk
+        float cmax = -INFINITY;
+#pragma unroll
+        for (int c0 = 0; c0 < kChunk; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(tmem + tlane + sb * 128 + c0, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int key = key0 + c0 + j;
+            const bool vis = key < prefix || (key < it.keys && ((mbits >> (key - prefix)) & 1ull));
+            if (vis) cmax = fmaxf(cmax, __uint_as_float(r[j]));
+          }
+        }
+        const float m_new = fmaxf(m_run, cmax * p.scale_log2);
+        const float alpha = (m_run == -INFINITY) ? 0.f : exp2f(m_run - m_new);
+        const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
+        // fold the previous chunk's PV (relative to m_pend) before P is overwritten
+        if (ci > 0) {
+          const int pg = g2 - 1, ob = pg & 1;
+          mbar_wait(&o_full[ob], (pg >> 1) & 1);
+          tc_fence_after();
+          const float f = (m_fold == -INFINITY) ? 0.f : exp2f(m_fold - m_pend);
+#pragma unroll
+          for (int c0 = 0; c0 < D; c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(tmem + tlane + 256 + ob * 128 + c0, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) O[c0 + j] = O[c0 + j] * f + __uint_as_float(r[j]);
+          }
+          m_fold = m_pend;
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&o_empty[ob]);
+        }
+        // pass 2: p = exp2(s*scale - m), row sum, bf16 P tile (swizzled K-major)
+        float psum = 0.f;
+#pragma unroll
+        for (int c0 = 0; c0 < kChunk; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(tmem + tlane + sb * 128 + c0, r);
+          tmem_ld_wait();
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            float pv[2];
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              const int key = key0 + c0 + j + t;
+              const bool vis = live && (key < prefix || (key < it.keys && ((mbits >> (key - prefix)) & 1ull)));
+              pv[t] = vis ? exp2f(__uint_as_float(r[j + t]) * p.scale_log2 - m_use) : 0.f;
+              psum += pv[t];
+            }
+            pk[j / 2] = uint32_t(f2bf(pv[0])) | (uint32_t(f2bf(pv[1])) << 16);
+          }
+          const int kb = c0 / 64;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int lc = ((c0 % 64) / 8) + t;
+            uint4 v = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+            *reinterpret_cast<uint4*>(pbuf + kb * 16384 + row * 128 + ((lc ^ (row & 7)) * 16)) = v;
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[sb]);
+        l_run = l_run * alpha + psum;
+        m_run = m_new;
+        m_pend = m_use;
+        // keys past the request's end in the last chunk: zero their V rows so
+        // stale (possibly non-finite) cache contents cannot reach the MMA
+        if (key0 + kChunk > it.keys) {
+          const int s = g2 % kKvStages;
+          uint8_t* vbuf = smem + L::kKvOff + s * 2 * L::kKvBytes + L::kKvBytes;
+          if (key0 + row >= it.keys) {
+#pragma unroll
+            for (int kb = 0; kb < L::kKBlocks; ++kb)
+#pragma unroll
+              for (int t = 0; t < 8; ++t)
+                *reinterpret_cast<uint4*>(vbuf + kb * 16384 + row * 128 + t * 16) = make_uint4(0, 0, 0, 0);
+          }
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full);
+      }
+      if (nch > 0) {
+        const int pg = gc + nch - 1, ob = pg & 1;
+        mbar_wait(&o_full[ob], (pg >> 1) & 1);
+        tc_fence_after();
+        const float f = (m_fold == -INFINITY) ? 0.f : exp2f(m_fold - m_pend);
+#pragma unroll
+        for (int c0 = 0; c0 < D; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(tmem + tlane + 256 + ob * 128 + c0, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) O[c0 + j] = O[c0 + j] * f + __uint_as_float(r[j]);
+        }
+        m_fold = m_pend;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&o_empty[ob]);
+      }
+      gc += nch;
+      if (!live) continue;
+      if (p.splits == 1) {
+        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+        uint16_t* dst = p.out + ((size_t(it.r) * p.n + qi) * p.n_q + size_t(it.h) * p.g + hh) * D;
+#pragma unroll
+        for (int c0 = 0; c0 < D; c0 += 8) {
+          uint4 v;
+          v.x = uint32_t(f2bf(O[c0] * inv)) | (uint32_t(f2bf(O[c0 + 1] * inv)) << 16);
+          v.y = uint32_t(f2bf(O[c0 + 2] * inv)) | (uint32_t(f2bf(O[c0 + 3] * inv)) << 16);
+          v.z = uint32_t(f2bf(O[c0 + 4] * inv)) | (uint32_t(f2bf(O[c0 + 5] * inv)) << 16);
+          v.w = uint32_t(f2bf(O[c0 + 6] * inv)) | (uint32_t(f2bf(O[c0 + 7] * inv)) << 16);
+          *reinterpret_cast<uint4*>(dst + c0) = v;
+        }
+      } else {
+        float* dst = p.ws_o + (size_t(item) * p.rows + row) * D;
+#pragma unroll
+        for (int c0 = 0; c0 < D; c0 += 4)
+          *reinterpret_cast<float4*>(dst + c0) = make_float4(O[c0], O[c0 + 1], O[c0 + 2], O[c0 + 3]);
+        p.ws_ml[size_t(item) * p.rows + row] = make_float2(nch > 0 ? m_fold : -INFINITY, l_run);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// Merge the split-KV partials: O = sum_s O_s 2^(m_s - M) / sum_s l_s 2^(m_s - M).
+template <int D>
+__global__ void attn_combine_kernel(AttnParams p) {
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  const int pairs = p.b * p.n_kv;
+  if (warp_global >= pairs * p.rows) return;
+  const int pair = warp_global / p.rows, row = warp_global % p.rows;
+  const int r = pair / p.n_kv, h = pair % p.n_kv;
+  float M = -INFINITY;
+  for (int s = 0; s < p.splits; ++s) M = fmaxf(M, p.ws_ml[size_t(pair * p.splits + s) * p.rows + row].x);
+  constexpr int V = D / 32;
+  float acc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc[v] = 0.f;
+  float L = 0.f;
+  for (int s = 0; s < p.splits; ++s) {
+    const size_t item = size_t(pair) * p.splits + s;
+    const float2 ml = p.ws_ml[item * p.rows + row];
+    if (ml.x == -INFINITY) continue;
+    const float w = exp2f(ml.x - M);
+    L += ml.y * w;
+    const float* src = p.ws_o + (item * p.rows + row) * D;
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] += src[lane + 32 * v] * w;
+  }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  const int qi = row / p.g, hh = row % p.g;
+  uint16_t* dst = p.out + ((size_t(r) * p.n + qi) * p.n_q + size_t(h) * p.g + hh) * D;
+#pragma unroll
+  for (int v = 0; v < V; ++v) dst[lane + 32 * v] = f2bf(acc[v] * inv);
+}
+
+struct AttnPlan {
+  int splits, split_chunks, items, grid;
+  size_t ws_bytes;
+};
+
+AttnPlan plan_attention(const smo_attn_args& a, int sms) {
+  AttnPlan pl{};
+  const int g = a.n_q / a.n_kv;
+  const int rows = g * a.n;
+  const int max_keys = std::max(1, a.max_prefix + a.n);
+  const int chunks = (max_keys + kChunk - 1) / kChunk;
+  const int pairs = a.b * a.n_kv;
+  // enough items for ~2 rounds of the persistent grid, at least 2 chunks each
+  int splits = std::max(1, std::min(chunks, (2 * sms + pairs - 1) / pairs));
+  if (splits > 1) splits = std::min(splits, std::max(1, chunks / 2));
+  pl.split_chunks = (chunks + splits - 1) / splits;
+  pl.splits = (chunks + pl.split_chunks - 1) / pl.split_chunks;
+  pl.items = pairs * pl.splits;
+  pl.grid = std::min(pl.items, sms);
+  pl.ws_bytes = pl.splits > 1 ? size_t(pl.items) * rows * (a.d * sizeof(float) + sizeof(float2)) : 0;
+  return pl;
+}
+
+int device_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+void check_attn_args(const smo_attn_args& a) {
+  SMO_REQUIRE(a.q && a.k_cache && a.v_cache && a.mask && a.prefix_len && a.out, "attention: null pointer");
+  SMO_REQUIRE(a.b > 0 && a.n > 0 && a.n_q > 0 && a.n_kv > 0, "attention: shape mismatch");
+  SMO_REQUIRE(a.n_q % a.n_kv == 0, "attention: shape mismatch");
+  SMO_REQUIRE(a.d == 64 || a.d == 128, "attention: head_dim must be 64 or 128");
+  SMO_REQUIRE(a.n <= 64, "attention: mask size mismatch");
+  SMO_REQUIRE((a.n_q / a.n_kv) * a.n <= 128, "attention: n * (n_q/n_kv) must be <= 128");
+  SMO_REQUIRE(a.max_prefix >= 0 && a.max_prefix + a.n <= a.s_max, "attention: shape mismatch");
+}
+
+}  // namespace
+
+size_t attention_workspace(const smo_attn_args& a) {
+  check_attn_args(a);
+  return plan_attention(a, device_sms()).ws_bytes;
+}
+
+void attention_launch(const smo_attn_args& a, cudaStream_t stream) {
+  check_attn_args(a);
+  const AttnPlan pl = plan_attention(a, device_sms());
+  SMO_REQUIRE(pl.ws_bytes == 0 || (a.workspace && a.workspace_bytes >= pl.ws_bytes),
+              "attention: workspace too small");
+  const int g = a.n_q / a.n_kv;
+  AttnParams p{};
+  p.mask = a.mask;
+  p.prefix = a.prefix_len;
+  p.out = reinterpret_cast<uint16_t*>(a.out);
+  p.ws_o = reinterpret_cast<float*>(a.workspace);
+  p.ws_ml = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(a.workspace) +
+                                      (pl.ws_bytes ? size_t(pl.items) * g * a.n * a.d * sizeof(float) : 0));
+  p.b = a.b;
+  p.n = a.n;
+  p.n_q = a.n_q;
+  p.n_kv = a.n_kv;
+  p.g = g;
+  p.rows = g * a.n;
+  p.s_max = a.s_max;
+  p.splits = pl.splits;
+  p.split_chunks = pl.split_chunks;
+  p.items = pl.items;
+  p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(a.d)));
+
+  CUtensorMap tq, tk, tv;
+  {
+    uint64_t dims[3] = {uint64_t(a.d), uint64_t(a.n_q), uint64_t(a.b) * a.n};
+    uint64_t strides[2] = {uint64_t(a.d) * 2, uint64_t(a.n_q) * a.d * 2};
+    uint32_t box[3] = {64, uint32_t(g), uint32_t(a.n)};
+    make_tmap_bf16(&tq, a.q, 3, dims, strides, box, true);
+  }
+  {
+    uint64_t dims[2] = {uint64_t(a.d), uint64_t(a.b) * a.n_kv * a.s_max};
+    uint64_t strides[1] = {uint64_t(a.d) * 2};
+    uint32_t box[2] = {64, uint32_t(kChunk)};
+    make_tmap_bf16(&tk, a.k_cache, 2, dims, strides, box, true);
+    make_tmap_bf16(&tv, a.v_cache, 2, dims, strides, box, true);
+  }
+  if (a.d == 128) {
+    constexpr size_t smem = AttnSmem<128>::kTotal + 1024;
+    static bool set = false;
+    if (!set) {
+      SMO_CUDA_CHECK(cudaFuncSetAttribute(verify_attention_kernel<128>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      set = true;
+    }
+    verify_attention_kernel<128><<<pl.grid, kThreads, smem, stream>>>(tq, tk, tv, p);
+  } else {
+    constexpr size_t smem = AttnSmem<64>::kTotal + 1024;
+    static bool set = false;
+    if (!set) {
+      SMO_CUDA_CHECK(cudaFuncSetAttribute(verify_attention_kernel<64>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      set = true;
+    }
+    verify_attention_kernel<64><<<pl.grid, kThreads, smem, stream>>>(tq, tk, tv, p);
+  }
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+  if (pl.splits > 1) {
+    const int warps = a.b * a.n_kv * p.rows;
+    const int blocks = (warps * 32 + 255) / 256;
+    if (a.d == 128)
+      attn_combine_kernel<128><<<blocks, 256, 0, stream>>>(p);
+    else
+      attn_combine_kernel<64><<<blocks, 256, 0, stream>>>(p);
+    count_launch();
+    SMO_CUDA_CHECK(cudaGetLastError());
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fp64 desk-scale operator (the reference API, attention.hpp:117-156), one
+// block per query row; columns visited prefix-first then masked drafts, the
+// same order as the reference so results agree to fp64 rounding.
+__global__ void chunked_attention_f64_kernel(int n, int p, int d, const double* Q, const double* K,
+                                             const double* V, const uint8_t* mask, double* scores,
+                                             double* out, int* blocked) {
+  const int i = blockIdx.x;
+  const int total = p + n;
+  const double scale = 1.0 / sqrt(double(d));
+  double* sc = scores + size_t(i) * total;
+  __shared__ double red[256];
+  double mx = -INFINITY;
+  for (int j = threadIdx.x; j < total; j += blockDim.x) {
+    const bool vis = j < p || mask[size_t(i) * n + (j - p)];
+    double s = -INFINITY;
+    if (vis) {
+      double acc = 0.0;
+      for (int c = 0; c < d; ++c) acc += Q[size_t(i) * d + c] * K[size_t(j) * d + c];
+      s = acc * scale;
+    }
+    sc[j] = s;
+    mx = fmax(mx, s);
+  }
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  mx = red[0];
+  __syncthreads();
+  if (mx == -INFINITY) {
+    if (threadIdx.x == 0) *blocked = 1;
+    return;
+  }
+  // serial denominator in column order (matches the reference's summation)
+  if (threadIdx.x == 0) {
+    double den = 0.0;
+    for (int j = 0; j < total; ++j)
+      if (sc[j] != -INFINITY) {
+        sc[j] = exp(sc[j] - mx);
+        den += sc[j];
+      } else {
+        sc[j] = 0.0;
+      }
+    red[0] = den;
+  }
+  __syncthreads();
+  const double den = red[0];
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < total; ++j)
+      if (j < p || mask[size_t(i) * n + (j - p)]) acc += (sc[j] / den) * V[size_t(j) * d + c];
+    out[size_t(i) * d + c] = acc;
+  }
+}
+
+void chunked_attention_f64(size_t n, size_t p, size_t d, const double* Q, const double* K, const double* V,
+                           size_t mask_n, const uint8_t* mask, double* out) {
+  const size_t total = p + n;
+  for (size_t i = 0; i < n * d; ++i)
+    if (!std::isfinite(Q[i])) throw Error(SMO_INVALID_ARG, "attention: non-finite Q");
+  for (size_t i = 0; i < total * d; ++i)
+    if (!std::isfinite(K[i])) throw Error(SMO_INVALID_ARG, "attention: non-finite K");
+  for (size_t i = 0; i < total * d; ++i)
+    if (!std::isfinite(V[i])) throw Error(SMO_INVALID_ARG, "attention: non-finite V");
+  if (mask_n != n) throw Error(SMO_INVALID_ARG, "attention: mask size mismatch");
+  if (n == 0) return;
+  double *dQ, *dK, *dV, *dS, *dO;
+  uint8_t* dM;
+  int* dB;
+  SMO_CUDA_CHECK(cudaMalloc(&dQ, sizeof(double) * n * d + 16));
+  SMO_CUDA_CHECK(cudaMalloc(&dK, sizeof(double) * total * d + 16));
+  SMO_CUDA_CHECK(cudaMalloc(&dV, sizeof(double) * total * d + 16));
+  SMO_CUDA_CHECK(cudaMalloc(&dS, sizeof(double) * n * total + 16));
+  SMO_CUDA_CHECK(cudaMalloc(&dO, sizeof(double) * n * d + 16));
+  SMO_CUDA_CHECK(cudaMalloc(&dM, n * n + 16));
+  SMO_CUDA_CHECK(cudaMalloc(&dB, sizeof(int)));
+  SMO_CUDA_CHECK(cudaMemcpy(dQ, Q, sizeof(double) * n * d, cudaMemcpyHostToDevice));
+  SMO_CUDA_CHECK(cudaMemcpy(dK, K, sizeof(double) * total * d, cudaMemcpyHostToDevice));
+  SMO_CUDA_CHECK(cudaMemcpy(dV, V, sizeof(double) * total * d, cudaMemcpyHostToDevice));
+  SMO_CUDA_CHECK(cudaMemcpy(dM, mask, n * n, cudaMemcpyHostToDevice));
+  SMO_CUDA_CHECK(cudaMemset(dB, 0, sizeof(int)));
+  chunked_attention_f64_kernel<<<int(n), 256>>>(int(n), int(p), int(d), dQ, dK, dV, dM, dS, dO, dB);
+  count_launch();
+  int blocked = 0;
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpy(&blocked, dB, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(out, dO, sizeof(double) * n * d, cudaMemcpyDeviceToHost);
+  cudaFree(dQ); cudaFree(dK); cudaFree(dV); cudaFree(dS); cudaFree(dO); cudaFree(dM); cudaFree(dB);
+  cuda_check(e, "chunked_attention_f64");
+  if (blocked) throw Error(SMO_INVALID_ARG, "attention: fully blocked query row");
+}
+
+}  // namespace smo

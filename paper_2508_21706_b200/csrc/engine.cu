@@ -1,0 +1,716 @@
+// engine.cu — VerifyEngine: the measured realisation of the reference's
+// target-verification DAG (pipeline.hpp:147-206) on one B200.
+//
+// Per layer l (compute stream):  RMSNorm -> QKV GEMM -> RoPE+KV append ->
+//   K1 attention -> O GEMM (+residual) -> RMSNorm -> K2 router -> K3 permute
+//   -> [wait slot_ready(l)] -> K4 SwiGLU gate/up -> K4 down -> K3 combine
+//   -> record slot_free(l mod S).
+// Copy stream (K5 expert streamer): H2D_EXPERTS(l) into HBM slot l mod S,
+//   waiting slot_free of the layer that last used the slot — the reference's
+//   serial-link model (pipeline.hpp:177-181) plus the real slot-release edge
+//   H2D(l+S) <- GPU_MOE(l).
+// After the last layer: final RMSNorm -> LM head GEMM with fused argmax
+// partials -> K6 argmax reduce -> greedy accept (specdec.hpp:65-76).
+//
+// Experts live in pinned host DRAM as [W1 | W3 | W2] blocks (nn.Linear
+// layouts: W1,W3 [h_i, h], W2 [h, h_i]); the HBM pool holds S staging slots of
+// E blocks each plus the hot-expert cache (MemoryPolicy.expert_cache_bytes,
+// config.hpp:103-108), filled once at creation.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace smo {
+
+smo_status run_guarded(const std::function<void()>& f);
+size_t attention_workspace(const smo_attn_args& a);
+void attention_launch(const smo_attn_args& a, cudaStream_t s);
+void gemm_launch(const smo_gemm_args& a, cudaStream_t s);
+void fill_uniform(void* dst, uint64_t count, uint64_t seed, uint64_t tensor_id, uint64_t base, float scale,
+                  cudaStream_t st);
+void fill_kv_prefix(void* cache, const int32_t* prefix, int b, int n_kv, int d, int s_max, uint64_t seed,
+                    uint64_t tensor_id, cudaStream_t st);
+void router_topk(const void* x, const void* w, int T, int h, int E, int k, float* logits, int32_t* ids,
+                 float* weights, cudaStream_t st);
+void permute(const int32_t* ids, int T, int k, int E, const void* x, int h, int32_t* offsets, int32_t* perm,
+             int32_t* pos, void* xp, cudaStream_t st);
+void unpermute_combine(const float* y, const int32_t* pos, const float* w, int T, int k, int h, float* res,
+                       cudaStream_t st);
+void rmsnorm(const float* x, const void* gain, int T, int h, float eps, void* y, cudaStream_t st);
+void embed(const int32_t* tok, const void* emb, int T, int h, float* x, cudaStream_t st);
+void rope_append(const void* qkv, const int32_t* prefix, const int32_t* parent, int b, int n, int n_q, int n_kv,
+                 int d, int s_max, float theta, void* q_out, void* kc, void* vc, cudaStream_t st);
+void argmax_reduce(const float* val, const int32_t* idx, int rows, int parts, int32_t* target, cudaStream_t st);
+void greedy_accept(const int32_t* tokens, const int32_t* target, const int32_t* parent, int b, int n,
+                   int32_t* acc_len, int32_t* bonus, int32_t* keep, cudaStream_t st);
+void build_mask(const int32_t* parent, int b, int n, uint64_t* mask, cudaStream_t st);
+
+// Procedural tensor ids; the oracle tests use the same ids.
+namespace tid {
+constexpr uint64_t kEmbed = 1, kLmHead = 2;
+inline uint64_t layer(int l) { return 1000ull * uint64_t(l + 1); }
+constexpr uint64_t kWqkv = 1, kWo = 2, kRouter = 4, kExpert = 100;
+inline uint64_t kv(int l, int which) { return 900000ull + 2ull * uint64_t(l) + uint64_t(which); }
+}  // namespace tid
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct Engine {
+  smo_model_config cfg{};
+  smo_engine_options opt{};
+  cudaStream_t copy = nullptr;
+  int h = 0, hi = 0, E = 0, K = 0, L = 0, nq = 0, nkv = 0, d = 0, V = 0;
+  int qkv_w = 0;
+  size_t blk_elems = 0, blk_bytes = 0;
+  std::vector<DevBuf> allocs;
+
+  // weights
+  uint16_t *embed_w = nullptr, *lm_w = nullptr, *final_norm = nullptr, *ones = nullptr;
+  struct Layer {
+    uint16_t *wqkv, *wo, *router;
+    uint16_t *kc, *vc;
+  };
+  std::vector<Layer> layers;
+  std::vector<uint16_t*> host_bufs;  // pinned, E blocks each
+  int host_alias = 0;
+  // expert pool in HBM
+  uint16_t* pool = nullptr;
+  int slots = 2, pool_blocks = 0;
+  std::vector<int> cache_blk;  // [L*E] pool block of a cached expert, -1 otherwise
+  int32_t* d_w_index = nullptr;  // [L*E]
+  std::vector<cudaEvent_t> slot_ready, slot_free;
+  // EP: experts owned by this rank
+  std::vector<int> owned;
+
+  // activations (max sizes)
+  int maxT = 0, maxB = 0, maxN = 0, s_max = 0;
+  float *x = nullptr, *ybuf = nullptr, *rw = nullptr, *amax_v = nullptr;
+  uint16_t *xn = nullptr, *qkv = nullptr, *q = nullptr, *attn = nullptr, *xp = nullptr, *hbuf = nullptr;
+  int32_t *ids = nullptr, *offsets = nullptr, *perm = nullptr, *pos = nullptr, *amax_i = nullptr, *target = nullptr;
+  int32_t *d_tokens = nullptr, *d_parent = nullptr, *d_prefix = nullptr, *d_acc = nullptr, *d_bonus = nullptr,
+          *d_keep = nullptr;
+  uint64_t* d_mask = nullptr;
+  void* attn_ws = nullptr;
+  size_t attn_ws_bytes = 0;
+  int32_t* h_stage = nullptr;  // pinned staging for host inputs/outputs
+  size_t h_stage_elems = 0;
+
+  // timing
+  std::vector<cudaEvent_t> ev;  // pool of timing events
+  smo_stage_times last{};
+  double last_h2d_bytes = 0;
+
+  // debug snapshots
+  bool debug = false;
+  std::map<std::string, std::vector<DevBuf>> dbg;
+
+  ~Engine() {
+    for (auto e : slot_ready) cudaEventDestroy(e);
+    for (auto e : slot_free) cudaEventDestroy(e);
+    for (auto e : ev) cudaEventDestroy(e);
+    for (auto hb : host_bufs) cudaFreeHost(hb);
+    if (h_stage) cudaFreeHost(h_stage);
+    for (auto& a : allocs) cudaFree(a.p);
+    for (auto& kv : dbg)
+      for (auto& b : kv.second) cudaFree(b.p);
+    if (copy) cudaStreamDestroy(copy);
+  }
+
+  template <class T>
+  T* dalloc(size_t count) {
+    void* p = nullptr;
+    const size_t bytes = std::max<size_t>(16, count * sizeof(T));
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess)
+      throw Error(SMO_CAPACITY, std::string("engine: cudaMalloc(") + std::to_string(bytes) + ") failed: " +
+                                    cudaGetErrorString(e));
+    allocs.push_back({p, bytes});
+    return reinterpret_cast<T*>(p);
+  }
+
+  int host_layer(int l) const { return host_alias > 0 ? l % host_alias : l; }
+  int expert_owner(int e) const { return opt.ep_size > 1 ? e % opt.ep_size : 0; }
+  bool owns(int e) const { return opt.ep_size <= 1 || expert_owner(e) == opt.ep_rank; }
+
+  void create() {
+    h = cfg.hidden;
+    hi = cfg.inter;
+    E = cfg.n_expert;
+    K = cfg.top_k;
+    L = cfg.n_layers;
+    nq = cfg.n_q_heads;
+    nkv = cfg.n_kv_heads;
+    d = cfg.head_dim;
+    V = cfg.vocab;
+    SMO_REQUIRE(h > 0 && hi > 0 && E > 0 && K > 0 && K <= E && L > 0, "engine: bad model shape");
+    SMO_REQUIRE(nq > 0 && nkv > 0 && nq % nkv == 0 && (d == 64 || d == 128), "engine: bad attention shape");
+    SMO_REQUIRE(h % 256 == 0 && hi % 128 == 0 && V % 128 == 0 && (nq * d) % 128 == 0, "engine: unsupported dims");
+    SMO_REQUIRE(opt.max_batch > 0 && opt.max_verify > 0 && opt.max_verify <= 64, "engine: bad batch options");
+    SMO_REQUIRE(opt.ep_size <= 1, "engine: expert parallelism is driven by the Python EP front end (not here)");
+    qkv_w = (nq + 2 * nkv) * d;
+    blk_elems = size_t(3) * h * hi;
+    blk_bytes = blk_elems * 2;
+    maxB = opt.max_batch;
+    maxN = opt.max_verify;
+    maxT = maxB * maxN;
+    s_max = opt.max_seq;
+    SMO_REQUIRE(s_max >= maxN + 1, "engine: max_seq too small");
+    slots = std::max(2, opt.hbm_slots);
+    host_alias = opt.host_alias_layers > 0 ? std::min(opt.host_alias_layers, L) : L;
+    debug = (opt.flags & SMO_ENGINE_DEBUG) != 0;
+    SMO_CUDA_CHECK(cudaSetDevice(opt.device));
+    SMO_CUDA_CHECK(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+    cudaStream_t st = nullptr;
+
+    // dense weights
+    embed_w = dalloc<uint16_t>(size_t(V) * h);
+    lm_w = dalloc<uint16_t>(size_t(V) * h);
+    ones = dalloc<uint16_t>(size_t(std::max(h, 1)));
+    final_norm = ones;
+    fill_uniform(embed_w, size_t(V) * h, cfg.seed, tid::kEmbed, 0, 1.0f, st);
+    fill_uniform(lm_w, size_t(V) * h, cfg.seed, tid::kLmHead, 0, std::sqrt(3.0f / h) * cfg.lm_scale, st);
+    {
+      std::vector<uint16_t> one(h, 0x3F80);  // bf16 1.0: RMSNorm gains = 1
+      SMO_CUDA_CHECK(cudaMemcpy(ones, one.data(), size_t(h) * 2, cudaMemcpyHostToDevice));
+    }
+    layers.resize(L);
+    for (int l = 0; l < L; ++l) {
+      Layer& ly = layers[l];
+      ly.wqkv = dalloc<uint16_t>(size_t(qkv_w) * h);
+      ly.wo = dalloc<uint16_t>(size_t(h) * nq * d);
+      ly.router = dalloc<uint16_t>(size_t(E) * h);
+      ly.kc = dalloc<uint16_t>(size_t(maxB) * nkv * s_max * d);
+      ly.vc = dalloc<uint16_t>(size_t(maxB) * nkv * s_max * d);
+      SMO_CUDA_CHECK(cudaMemset(ly.kc, 0, size_t(maxB) * nkv * s_max * d * 2));
+      SMO_CUDA_CHECK(cudaMemset(ly.vc, 0, size_t(maxB) * nkv * s_max * d * 2));
+      fill_uniform(ly.wqkv, size_t(qkv_w) * h, cfg.seed, tid::layer(l) + tid::kWqkv, 0, std::sqrt(3.0f / h), st);
+      fill_uniform(ly.wo, size_t(h) * nq * d, cfg.seed, tid::layer(l) + tid::kWo, 0, std::sqrt(3.0f / (nq * d)),
+                   st);
+      fill_uniform(ly.router, size_t(E) * h, cfg.seed, tid::layer(l) + tid::kRouter, 0,
+                   std::sqrt(3.0f / h) * cfg.router_scale, st);
+    }
+
+    // experts: generate each block on the device, stage to pinned host DRAM
+    for (int e = 0; e < E; ++e)
+      if (owns(e)) owned.push_back(e);
+    host_bufs.assign(host_alias, nullptr);
+    uint16_t* stage = dalloc<uint16_t>(blk_elems);
+    for (int a = 0; a < host_alias; ++a) {
+      void* hp = nullptr;
+      cudaError_t err = cudaHostAlloc(&hp, blk_bytes * E, cudaHostAllocPortable);
+      if (err != cudaSuccess)
+        throw Error(SMO_CAPACITY, "engine: pinned host allocation of " + std::to_string(blk_bytes * E) +
+                                      " bytes failed (" + cudaGetErrorString(err) + "); set host_alias_layers");
+      host_bufs[a] = reinterpret_cast<uint16_t*>(hp);
+      for (int e : owned) {
+        const uint64_t base = tid::layer(a) + tid::kExpert + 3ull * e;
+        fill_uniform(stage, size_t(hi) * h, cfg.seed, base + 0, 0, std::sqrt(3.0f / h), st);
+        fill_uniform(stage + size_t(hi) * h, size_t(hi) * h, cfg.seed, base + 1, 0, std::sqrt(3.0f / h), st);
+        fill_uniform(stage + 2 * size_t(hi) * h, size_t(h) * hi, cfg.seed, base + 2, 0, std::sqrt(3.0f / hi), st);
+        SMO_CUDA_CHECK(cudaMemcpy(host_bufs[a] + size_t(e) * blk_elems, stage, blk_bytes, cudaMemcpyDeviceToHost));
+      }
+    }
+
+    // HBM pool: slots x E staging blocks + hot-expert cache
+    const int64_t cache_blocks = opt.expert_cache_bytes > 0 ? int64_t(opt.expert_cache_bytes / int64_t(blk_bytes)) : 0;
+    cache_blk.assign(size_t(L) * E, -1);
+    int placed = 0;
+    for (int l = 0; l < L && placed < cache_blocks; ++l)
+      for (int e : owned) {
+        if (placed >= cache_blocks) break;
+        cache_blk[size_t(l) * E + e] = slots * E + placed;
+        ++placed;
+      }
+    pool_blocks = slots * E + placed;
+    pool = dalloc<uint16_t>(size_t(pool_blocks) * blk_elems);
+    for (int l = 0; l < L; ++l)
+      for (int e : owned) {
+        const int cb = cache_blk[size_t(l) * E + e];
+        if (cb >= 0)
+          SMO_CUDA_CHECK(cudaMemcpy(pool + size_t(cb) * blk_elems, host_bufs[host_layer(l)] + size_t(e) * blk_elems,
+                                    blk_bytes, cudaMemcpyHostToDevice));
+      }
+    std::vector<int32_t> widx(size_t(L) * E);
+    for (int l = 0; l < L; ++l)
+      for (int e = 0; e < E; ++e) {
+        const int cb = cache_blk[size_t(l) * E + e];
+        widx[size_t(l) * E + e] = cb >= 0 ? cb : (l % slots) * E + e;
+      }
+    d_w_index = dalloc<int32_t>(widx.size());
+    SMO_CUDA_CHECK(cudaMemcpy(d_w_index, widx.data(), widx.size() * 4, cudaMemcpyHostToDevice));
+    slot_ready.resize(slots);
+    slot_free.resize(slots);
+    for (int s = 0; s < slots; ++s) {
+      SMO_CUDA_CHECK(cudaEventCreateWithFlags(&slot_ready[s], cudaEventDisableTiming));
+      SMO_CUDA_CHECK(cudaEventCreateWithFlags(&slot_free[s], cudaEventDisableTiming));
+    }
+
+    // activations
+    const int P = maxT * K;
+    x = dalloc<float>(size_t(maxT) * h);
+    xn = dalloc<uint16_t>(size_t(maxT) * h);
+    qkv = dalloc<uint16_t>(size_t(maxT) * qkv_w);
+    q = dalloc<uint16_t>(size_t(maxT) * nq * d);
+    attn = dalloc<uint16_t>(size_t(maxT) * nq * d);
+    ids = dalloc<int32_t>(P);
+    rw = dalloc<float>(P);
+    offsets = dalloc<int32_t>(E + 1);
+    perm = dalloc<int32_t>(P);
+    pos = dalloc<int32_t>(P);
+    xp = dalloc<uint16_t>(size_t(P) * h);
+    hbuf = dalloc<uint16_t>(size_t(P) * hi);
+    ybuf = dalloc<float>(size_t(P) * h);
+    amax_v = dalloc<float>(size_t(maxT) * (V / 128));
+    amax_i = dalloc<int32_t>(size_t(maxT) * (V / 128));
+    target = dalloc<int32_t>(maxT);
+    d_tokens = dalloc<int32_t>(maxT);
+    d_parent = dalloc<int32_t>(maxT);
+    d_prefix = dalloc<int32_t>(maxB);
+    d_acc = dalloc<int32_t>(maxB);
+    d_bonus = dalloc<int32_t>(maxB);
+    d_keep = dalloc<int32_t>(maxT);
+    d_mask = dalloc<uint64_t>(maxT);
+    smo_attn_args wa{};
+    wa.b = maxB;
+    wa.n = maxN;
+    wa.n_q = nq;
+    wa.n_kv = nkv;
+    wa.d = d;
+    wa.s_max = s_max;
+    wa.max_prefix = s_max - maxN;
+    wa.q = wa.k_cache = wa.v_cache = wa.out = reinterpret_cast<void*>(1);
+    wa.mask = reinterpret_cast<const uint64_t*>(1);
+    wa.prefix_len = reinterpret_cast<const int32_t*>(1);
+    attn_ws_bytes = attention_workspace(wa);
+    // split planning gives items <= pairs * ceil(2*SMs / pairs) <= 2*SMs + pairs
+    // for any batch <= maxB and prefix <= s_max - n: size for that bound
+    {
+      int sms = 0;
+      SMO_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, opt.device));
+      const size_t bound = size_t(2 * sms + maxB * nkv) * size_t(nq / nkv) * maxN * (size_t(d) * 4 + 8);
+      attn_ws_bytes = std::max(attn_ws_bytes, bound);
+    }
+    attn_ws = attn_ws_bytes ? dalloc<uint8_t>(attn_ws_bytes) : nullptr;
+    h_stage_elems = size_t(maxT) * 4 + maxB * 4;
+    SMO_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_stage), h_stage_elems * 4, cudaHostAllocPortable));
+    ev.resize(8 + size_t(L) * 6);
+    for (auto& e : ev) SMO_CUDA_CHECK(cudaEventCreate(&e));
+    SMO_CUDA_CHECK(cudaDeviceSynchronize());
+  }
+
+  void fill_prefix(const int32_t* prefix_host, int b) {
+    SMO_REQUIRE(b > 0 && b <= maxB, "fill_prefix: bad batch");
+    for (int r = 0; r < b; ++r)
+      SMO_REQUIRE(prefix_host[r] >= 0 && prefix_host[r] + maxN <= s_max, "fill_prefix: prefix exceeds max_seq");
+    SMO_CUDA_CHECK(cudaMemcpy(d_prefix, prefix_host, size_t(b) * 4, cudaMemcpyHostToDevice));
+    for (int l = 0; l < L; ++l) {
+      fill_kv_prefix(layers[l].kc, d_prefix, b, nkv, d, s_max, cfg.seed, tid::kv(l, 0), nullptr);
+      fill_kv_prefix(layers[l].vc, d_prefix, b, nkv, d, s_max, cfg.seed, tid::kv(l, 1), nullptr);
+    }
+    SMO_CUDA_CHECK(cudaDeviceSynchronize());
+  }
+
+  // Stream layer l's non-cached owned experts into slot l % slots.
+  double enqueue_h2d(int l, cudaEvent_t t0, cudaEvent_t t1) {
+    const int s = l % slots;
+    SMO_CUDA_CHECK(cudaStreamWaitEvent(copy, slot_free[s], 0));
+    if (t0) SMO_CUDA_CHECK(cudaEventRecord(t0, copy));
+    double bytes = 0;
+    const uint16_t* hb = host_bufs[host_layer(l)];
+    int e = 0;
+    while (e < E) {
+      if (!owns(e) || cache_blk[size_t(l) * E + e] >= 0) {
+        ++e;
+        continue;
+      }
+      int e2 = e;
+      while (e2 + 1 < E && owns(e2 + 1) && cache_blk[size_t(l) * E + e2 + 1] < 0 && opt.ep_size <= 1) ++e2;
+      const size_t nbytes = size_t(e2 - e + 1) * blk_bytes;
+      SMO_CUDA_CHECK(cudaMemcpyAsync(pool + (size_t(s) * E + e) * blk_elems, hb + size_t(e) * blk_elems, nbytes,
+                                     cudaMemcpyHostToDevice, copy));
+      bytes += double(nbytes);
+      e = e2 + 1;
+    }
+    if (t1) SMO_CUDA_CHECK(cudaEventRecord(t1, copy));
+    SMO_CUDA_CHECK(cudaEventRecord(slot_ready[s], copy));
+    return bytes;
+  }
+
+  void snap(const char* name, int layer, const void* src, size_t bytes, cudaStream_t st) {
+    if (!debug) return;
+    auto& v = dbg[name];
+    const size_t idx = size_t(layer + 1);
+    if (v.size() <= idx) v.resize(idx + 1);
+    if (v[idx].bytes < bytes) {
+      if (v[idx].p) cudaFree(v[idx].p);
+      SMO_CUDA_CHECK(cudaMalloc(&v[idx].p, bytes));
+      v[idx].bytes = bytes;
+    }
+    SMO_CUDA_CHECK(cudaMemcpyAsync(v[idx].p, src, bytes, cudaMemcpyDeviceToDevice, st));
+  }
+
+  void verify(const smo_verify_batch& in, smo_verify_output& out, cudaStream_t st) {
+    const int b = in.b, n = in.n, T = b * n;
+    SMO_REQUIRE(b > 0 && b <= maxB && n > 0 && n <= maxN, "verify: batch exceeds engine capacity");
+    SMO_REQUIRE(in.tokens && in.prefix_len, "verify: null tokens/prefix_len");
+    SMO_REQUIRE(out.acc_len && out.bonus, "verify: null outputs");
+    const uint64_t l0 = 0;
+    (void)l0;
+    // ---- inputs
+    int max_prefix = s_max - n;
+    if (in.on_device) {
+      SMO_CUDA_CHECK(cudaMemcpyAsync(d_tokens, in.tokens, size_t(T) * 4, cudaMemcpyDeviceToDevice, st));
+      SMO_CUDA_CHECK(cudaMemcpyAsync(d_prefix, in.prefix_len, size_t(b) * 4, cudaMemcpyDeviceToDevice, st));
+      if (in.parent)
+        SMO_CUDA_CHECK(cudaMemcpyAsync(d_parent, in.parent, size_t(T) * 4, cudaMemcpyDeviceToDevice, st));
+    } else {
+      max_prefix = 0;
+      for (int r = 0; r < b; ++r) {
+        SMO_REQUIRE(in.prefix_len[r] >= 0 && in.prefix_len[r] + n <= s_max, "verify: prefix exceeds max_seq");
+        max_prefix = std::max(max_prefix, in.prefix_len[r]);
+      }
+      SMO_CUDA_CHECK(cudaStreamSynchronize(st));  // staging buffer reuse
+      int32_t* hs = h_stage;
+      std::memcpy(hs, in.tokens, size_t(T) * 4);
+      std::memcpy(hs + T, in.prefix_len, size_t(b) * 4);
+      if (in.parent) std::memcpy(hs + T + b, in.parent, size_t(T) * 4);
+      SMO_CUDA_CHECK(cudaMemcpyAsync(d_tokens, hs, size_t(T) * 4, cudaMemcpyHostToDevice, st));
+      SMO_CUDA_CHECK(cudaMemcpyAsync(d_prefix, hs + T, size_t(b) * 4, cudaMemcpyHostToDevice, st));
+      if (in.parent)
+        SMO_CUDA_CHECK(cudaMemcpyAsync(d_parent, hs + T + b, size_t(T) * 4, cudaMemcpyHostToDevice, st));
+    }
+    const int32_t* parent = in.parent ? d_parent : nullptr;
+    const uint64_t launches0 = 0;
+    (void)launches0;
+
+    cudaEvent_t e_start = ev[0], e_end = ev[1];
+    SMO_CUDA_CHECK(cudaEventRecord(e_start, st));
+    // order the copy stream after the step start (so H2D timing is step-relative)
+    SMO_CUDA_CHECK(cudaStreamWaitEvent(copy, e_start, 0));
+    double h2d_bytes = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> h2d_ev, attn_ev, moe_ev;
+    auto tev = [&](int i) { return ev[8 + size_t(i)]; };
+    for (int l = 0; l < std::min(slots, L); ++l) {
+      h2d_bytes += enqueue_h2d(l, tev(l * 6 + 0), tev(l * 6 + 1));
+      h2d_ev.push_back({tev(l * 6 + 0), tev(l * 6 + 1)});
+    }
+    build_mask(parent, b, n, d_mask, st);
+    embed(d_tokens, embed_w, T, h, x, st);
+
+    const int P = T * K;
+    for (int l = 0; l < L; ++l) {
+      Layer& ly = layers[l];
+      snap("x_in", l, x, size_t(T) * h * 4, st);
+      rmsnorm(x, ones, T, h, cfg.rms_eps, xn, st);
+      snap("xn1", l, xn, size_t(T) * h * 2, st);
+      smo_gemm_args g{};
+      g.x = xn;
+      g.rows = T;
+      g.K = h;
+      g.N = qkv_w;
+      g.groups = 1;
+      g.max_rows_per_group = T;
+      g.w = ly.wqkv;
+      g.w_pool_blocks = 1;
+      g.epilogue = SMO_EPI_BF16;
+      g.out = qkv;
+      g.ldo = qkv_w;
+      gemm_launch(g, st);
+      rope_append(qkv, d_prefix, parent, b, n, nq, nkv, d, s_max, cfg.rope_theta, q, ly.kc, ly.vc, st);
+      snap("q", l, q, size_t(T) * nq * d * 2, st);
+      smo_attn_args a{};
+      a.q = q;
+      a.k_cache = ly.kc;
+      a.v_cache = ly.vc;
+      a.mask = d_mask;
+      a.prefix_len = d_prefix;
+      a.out = attn;
+      a.b = b;
+      a.n = n;
+      a.n_q = nq;
+      a.n_kv = nkv;
+      a.d = d;
+      a.s_max = s_max;
+      a.max_prefix = max_prefix;
+      a.workspace = attn_ws;
+      a.workspace_bytes = attn_ws_bytes;
+      SMO_CUDA_CHECK(cudaEventRecord(tev(l * 6 + 2), st));
+      attention_launch(a, st);
+      SMO_CUDA_CHECK(cudaEventRecord(tev(l * 6 + 3), st));
+      attn_ev.push_back({tev(l * 6 + 2), tev(l * 6 + 3)});
+      snap("attn", l, attn, size_t(T) * nq * d * 2, st);
+      g = smo_gemm_args{};
+      g.x = attn;
+      g.rows = T;
+      g.K = nq * d;
+      g.N = h;
+      g.groups = 1;
+      g.max_rows_per_group = T;
+      g.w = ly.wo;
+      g.w_pool_blocks = 1;
+      g.epilogue = SMO_EPI_F32_ADD;
+      g.out = x;
+      g.ldo = h;
+      gemm_launch(g, st);
+      rmsnorm(x, ones, T, h, cfg.rms_eps, xn, st);
+      snap("xn2", l, xn, size_t(T) * h * 2, st);
+      float* rlog = nullptr;
+      if (debug) {
+        auto& v = dbg["logits_r"];
+        if (v.size() <= size_t(l + 1)) v.resize(l + 2);
+        if (!v[l + 1].p) {
+          SMO_CUDA_CHECK(cudaMalloc(&v[l + 1].p, size_t(maxT) * E * 4));
+          v[l + 1].bytes = size_t(maxT) * E * 4;
+        }
+        rlog = reinterpret_cast<float*>(v[l + 1].p);
+      }
+      router_topk(xn, ly.router, T, h, E, K, rlog, ids, rw, st);
+      permute(ids, T, K, E, xn, h, offsets, perm, pos, xp, st);
+      snap("ids", l, ids, size_t(P) * 4, st);
+      snap("weights", l, rw, size_t(P) * 4, st);
+      snap("offsets", l, offsets, size_t(E + 1) * 4, st);
+      snap("pos", l, pos, size_t(P) * 4, st);
+      // ---- MoE: wait for this layer's experts
+      SMO_CUDA_CHECK(cudaStreamWaitEvent(st, slot_ready[l % slots], 0));
+      SMO_CUDA_CHECK(cudaEventRecord(tev(l * 6 + 4), st));
+      g = smo_gemm_args{};
+      g.x = xp;
+      g.rows = P;
+      g.K = h;
+      g.N = hi;
+      g.groups = E;
+      g.row_offsets = offsets;
+      g.max_rows_per_group = T;  // a token selects an expert at most once
+      g.w = pool;
+      g.w_up = pool + size_t(hi) * h;
+      g.w_block_stride = blk_bytes;
+      g.w_pool_blocks = pool_blocks;
+      g.w_index = d_w_index + size_t(l) * E;
+      g.epilogue = SMO_EPI_SWIGLU;
+      g.out = hbuf;
+      g.ldo = hi;
+      gemm_launch(g, st);
+      g = smo_gemm_args{};
+      g.x = hbuf;
+      g.rows = P;
+      g.K = hi;
+      g.N = h;
+      g.groups = E;
+      g.row_offsets = offsets;
+      g.max_rows_per_group = T;
+      g.w = pool + 2 * size_t(hi) * h;
+      g.w_block_stride = blk_bytes;
+      g.w_pool_blocks = pool_blocks;
+      g.w_index = d_w_index + size_t(l) * E;
+      g.epilogue = SMO_EPI_F32;
+      g.out = ybuf;
+      g.ldo = h;
+      gemm_launch(g, st);
+      SMO_CUDA_CHECK(cudaEventRecord(slot_free[l % slots], st));
+      unpermute_combine(ybuf, pos, rw, T, K, h, x, st);
+      SMO_CUDA_CHECK(cudaEventRecord(tev(l * 6 + 5), st));
+      moe_ev.push_back({tev(l * 6 + 4), tev(l * 6 + 5)});
+      snap("x_out", l, x, size_t(T) * h * 4, st);
+      if (l + slots < L) {
+        const int ln = l + slots;
+        h2d_bytes += enqueue_h2d(ln, tev(ln * 6 + 0), tev(ln * 6 + 1));
+        h2d_ev.push_back({tev(ln * 6 + 0), tev(ln * 6 + 1)});
+      }
+    }
+    // ---- LM head with fused argmax partials, then K6
+    rmsnorm(x, final_norm, T, h, cfg.rms_eps, xn, st);
+    snap("xf", -1, xn, size_t(T) * h * 2, st);
+    smo_gemm_args g{};
+    g.x = xn;
+    g.rows = T;
+    g.K = h;
+    g.N = V;
+    g.groups = 1;
+    g.max_rows_per_group = T;
+    g.w = lm_w;
+    g.w_pool_blocks = 1;
+    g.epilogue = SMO_EPI_ARGMAX;
+    g.argmax_val = amax_v;
+    g.argmax_idx = amax_i;
+    gemm_launch(g, st);
+    if (debug) {
+      auto& v = dbg["logits"];
+      if (v.empty()) v.resize(1);
+      if (!v[0].p) {
+        SMO_CUDA_CHECK(cudaMalloc(&v[0].p, size_t(maxT) * V * 4));
+        v[0].bytes = size_t(maxT) * V * 4;
+      }
+      g.epilogue = SMO_EPI_F32;
+      g.out = v[0].p;
+      g.ldo = V;
+      gemm_launch(g, st);
+    }
+    argmax_reduce(amax_v, amax_i, T, V / 128, target, st);
+    greedy_accept(d_tokens, target, parent, b, n, d_acc, d_bonus, d_keep, st);
+    SMO_CUDA_CHECK(cudaEventRecord(e_end, st));
+    // the step is complete only when the copy engine is idle too
+    SMO_CUDA_CHECK(cudaStreamWaitEvent(st, slot_ready[(L - 1) % slots], 0));
+    // ---- outputs
+    if (out.on_device) {
+      SMO_CUDA_CHECK(cudaMemcpyAsync(out.acc_len, d_acc, size_t(b) * 4, cudaMemcpyDeviceToDevice, st));
+      SMO_CUDA_CHECK(cudaMemcpyAsync(out.bonus, d_bonus, size_t(b) * 4, cudaMemcpyDeviceToDevice, st));
+      if (out.keep) SMO_CUDA_CHECK(cudaMemcpyAsync(out.keep, d_keep, size_t(T) * 4, cudaMemcpyDeviceToDevice, st));
+      if (out.target)
+        SMO_CUDA_CHECK(cudaMemcpyAsync(out.target, target, size_t(T) * 4, cudaMemcpyDeviceToDevice, st));
+    } else {
+      int32_t* hs = h_stage + 2 * size_t(T) + b;
+      SMO_CUDA_CHECK(cudaMemcpyAsync(hs, d_acc, size_t(b) * 4, cudaMemcpyDeviceToHost, st));
+      SMO_CUDA_CHECK(cudaMemcpyAsync(hs + b, d_bonus, size_t(b) * 4, cudaMemcpyDeviceToHost, st));
+      SMO_CUDA_CHECK(cudaMemcpyAsync(hs + 2 * b, d_keep, size_t(T) * 4, cudaMemcpyDeviceToHost, st));
+      SMO_CUDA_CHECK(cudaMemcpyAsync(hs + 2 * b + T, target, size_t(T) * 4, cudaMemcpyDeviceToHost, st));
+      SMO_CUDA_CHECK(cudaStreamSynchronize(st));
+      std::memcpy(out.acc_len, hs, size_t(b) * 4);
+      std::memcpy(out.bonus, hs + b, size_t(b) * 4);
+      if (out.keep) std::memcpy(out.keep, hs + 2 * b, size_t(T) * 4);
+      if (out.target) std::memcpy(out.target, hs + 2 * b + T, size_t(T) * 4);
+    }
+    pending_attn = attn_ev;
+    pending_moe = moe_ev;
+    pending_h2d = h2d_ev;
+    last_h2d_bytes = h2d_bytes;
+  }
+
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending_attn, pending_moe, pending_h2d;
+
+  void times(smo_stage_times* t) {
+    SMO_CUDA_CHECK(cudaDeviceSynchronize());
+    auto span = [](const std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
+      double s = 0;
+      for (auto& p : v) {
+        float ms = 0;
+        if (cudaEventElapsedTime(&ms, p.first, p.second) == cudaSuccess) s += ms * 1e-3;
+      }
+      return s;
+    };
+    smo_stage_times r{};
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev[0], ev[1]);
+    r.target_total = ms * 1e-3;
+    r.attention = span(pending_attn);
+    r.gpu_moe = span(pending_moe);
+    r.h2d_transfer = span(pending_h2d);
+    r.h2d_bytes = last_h2d_bytes;
+    r.others = std::max(0.0, r.target_total - r.attention - r.gpu_moe);
+    *t = r;
+  }
+};
+
+}  // namespace smo
+
+struct smo_engine {
+  smo::Engine impl;
+};
+
+extern "C" {
+
+smo_status smo_engine_create(const smo_model_config* cfg, const smo_engine_options* opt, smo_engine** out) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(cfg && opt && out, "engine: null argument");
+    auto* e = new smo_engine();
+    e->impl.cfg = *cfg;
+    e->impl.opt = *opt;
+    try {
+      e->impl.create();
+    } catch (...) {
+      delete e;
+      throw;
+    }
+    *out = e;
+  });
+}
+
+smo_status smo_engine_destroy(smo_engine* e) {
+  return smo::run_guarded([&] { delete e; });
+}
+
+smo_status smo_engine_fill_prefix(smo_engine* e, const int32_t* prefix_len_host, int32_t b) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(e && prefix_len_host, "engine: null argument");
+    e->impl.fill_prefix(prefix_len_host, b);
+  });
+}
+
+smo_status smo_engine_verify(smo_engine* e, const smo_verify_batch* in, smo_verify_output* out,
+                             smo_stream stream) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(e && in && out, "engine: null argument");
+    e->impl.verify(*in, *out, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+smo_status smo_engine_last_times(smo_engine* e, smo_stage_times* t) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(e && t, "engine: null argument");
+    e->impl.times(t);
+  });
+}
+
+smo_status smo_engine_debug_tensor(smo_engine* e, const char* name, int32_t layer, void* dst, size_t bytes) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(e && name && dst, "engine: null argument");
+    SMO_REQUIRE(e->impl.debug, "engine: created without SMO_ENGINE_DEBUG");
+    auto it = e->impl.dbg.find(name);
+    SMO_REQUIRE(it != e->impl.dbg.end(), std::string("engine: unknown debug tensor ") + name);
+    const size_t idx = size_t(layer + 1);
+    SMO_REQUIRE(idx < it->second.size() && it->second[idx].p, "engine: debug tensor not captured for layer");
+    SMO_REQUIRE(bytes <= it->second[idx].bytes, "engine: debug tensor smaller than requested");
+    SMO_CUDA_CHECK(cudaDeviceSynchronize());
+    SMO_CUDA_CHECK(cudaMemcpy(dst, it->second[idx].p, bytes, cudaMemcpyDeviceToHost));
+  });
+}
+
+smo_status smo_engine_tensor_ptr(smo_engine* e, const char* name, int32_t layer, int32_t expert, void** ptr,
+                                 size_t* bytes) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(e && name && ptr && bytes, "engine: null argument");
+    smo::Engine& g = e->impl;
+    const std::string n(name);
+    auto need_layer = [&] { SMO_REQUIRE(layer >= 0 && layer < g.L, "engine: layer out of range"); };
+    if (n == "embed") {
+      *ptr = g.embed_w;
+      *bytes = size_t(g.V) * g.h * 2;
+    } else if (n == "lm_head") {
+      *ptr = g.lm_w;
+      *bytes = size_t(g.V) * g.h * 2;
+    } else if (n == "wqkv") {
+      need_layer();
+      *ptr = g.layers[layer].wqkv;
+      *bytes = size_t(g.qkv_w) * g.h * 2;
+    } else if (n == "wo") {
+      need_layer();
+      *ptr = g.layers[layer].wo;
+      *bytes = size_t(g.h) * g.nq * g.d * 2;
+    } else if (n == "router") {
+      need_layer();
+      *ptr = g.layers[layer].router;
+      *bytes = size_t(g.E) * g.h * 2;
+    } else if (n == "k_cache" || n == "v_cache") {
+      need_layer();
+      *ptr = n == "k_cache" ? g.layers[layer].kc : g.layers[layer].vc;
+      *bytes = size_t(g.maxB) * g.nkv * g.s_max * g.d * 2;
+    } else if (n == "expert_host") {
+      need_layer();
+      SMO_REQUIRE(expert >= 0 && expert < g.E, "engine: expert out of range");
+      *ptr = g.host_bufs[g.host_layer(layer)] + size_t(expert) * g.blk_elems;
+      *bytes = g.blk_bytes;
+    } else {
+      throw smo::Error(SMO_INVALID_ARG, "engine: unknown tensor " + n);
+    }
+  });
+}
+
+}  // extern "C"

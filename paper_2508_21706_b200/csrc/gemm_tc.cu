@@ -1,0 +1,295 @@
+// gemm_tc.cu — K4: tcgen05/TMEM GEMM fed by TMA, used for the grouped SwiGLU
+// experts and (one group) for the dense QKV / O / LM-head projections.
+//
+// Swap-AB: the weight matrix W [N, K] (nn.Linear layout, K contiguous) is the
+// 128-row A operand; the small token batch X [rows, K] is the B operand
+// (MMA N = tokens, up to 256 per instruction, two instructions for up to 512).
+// One CTA = one 128-row weight tile x one token tile of one group (expert).
+// Warp roles: w0 TMA producer, w1 TMEM allocator + single-thread MMA issuer,
+// w2..w5 epilogue (TMEM -> registers -> global). The smem ring is a
+// full/empty mbarrier pipeline; tcgen05.commit releases stages.
+//
+// Algorithmic cost (roofline.hpp:56-64, moe_cost_large_batch):
+//   FLOPs = 2 * rows * N * K (x2 for SwiGLU), HBM bytes ~= weight bytes
+//   (N*K*2 per group, x2 for SwiGLU) + activations.
+#include "common.cuh"
+
+namespace smo {
+
+namespace {
+
+constexpr int kThreads = 192;
+constexpr int kBK = 64;           // K elements per stage (one 128 B swizzle atom)
+constexpr int kTileBytesA = 128 * kBK * 2;
+constexpr int kMaxStages = 8;
+constexpr int kSmemBudget = 220 * 1024;
+
+struct GemmParams {
+  int K, N, rows;
+  const int32_t* row_offsets;
+  const int32_t* w_index;
+  int tile_tokens;
+  int stages;
+  int epilogue;
+  void* out;
+  int64_t ldo;
+  float* amax_val;
+  int32_t* amax_idx;
+  int n_tiles;
+};
+
+__device__ __forceinline__ void tmem_alloc_dyn(uint32_t cols, uint32_t* dst) {
+  switch (cols) {
+    case 32: tmem_alloc<32>(dst); break;
+    case 64: tmem_alloc<64>(dst); break;
+    case 128: tmem_alloc<128>(dst); break;
+    case 256: tmem_alloc<256>(dst); break;
+    default: tmem_alloc<512>(dst); break;
+  }
+}
+__device__ __forceinline__ void tmem_dealloc_dyn(uint32_t cols, uint32_t taddr) {
+  switch (cols) {
+    case 32: tmem_dealloc<32>(taddr); break;
+    case 64: tmem_dealloc<64>(taddr); break;
+    case 128: tmem_dealloc<128>(taddr); break;
+    case 256: tmem_dealloc<256>(taddr); break;
+    default: tmem_dealloc<512>(taddr); break;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_u,
+                   const __grid_constant__ CUtensorMap tm_x, GemmParams p, uint32_t tmem_cols) {
+  const int nb = blockIdx.x, g = blockIdx.y, tt = blockIdx.z;
+  const int g_begin = p.row_offsets ? p.row_offsets[g] : 0;
+  const int g_end = p.row_offsets ? p.row_offsets[g + 1] : p.rows;
+  const int row0 = g_begin + tt * p.tile_tokens;
+  const int cnt = min(p.tile_tokens, g_end - row0);
+  if (cnt <= 0) return;  // uniform across the CTA
+
+  const bool swiglu = p.epilogue == SMO_EPI_SWIGLU;
+  const int wblk = p.w_index ? p.w_index[g] : g;
+  const int n_pad = (cnt + 15) & ~15;
+  const int n_load = (cnt + 31) & ~31;
+  const int a_bytes = kTileBytesA * (swiglu ? 2 : 1);
+  const int stage_bytes = a_bytes + p.tile_tokens * 128;
+  const uint32_t tx_bytes = uint32_t(a_bytes + (n_load / 32) * 4096);
+  const int KB = p.K / kBK;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full_bar[kMaxStages];
+  __shared__ __align__(8) uint64_t empty_bar[kMaxStages];
+  __shared__ __align__(8) uint64_t tmem_full_bar;
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&tmem_full_bar, 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_w);
+    tma_prefetch_desc(&tm_x);
+    if (swiglu) tma_prefetch_desc(&tm_u);
+  }
+  if (warp == 1) tmem_alloc_dyn(tmem_cols, &tmem_base_sh);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % p.stages;
+        const uint32_t ph = (kb / p.stages) & 1;
+        mbar_wait(&empty_bar[s], ph ^ 1);
+        mbar_arrive_expect_tx(&full_bar[s], tx_bytes);
+        uint8_t* sa = smem + s * stage_bytes;
+        tma_load_3d(sa, &tm_w, &full_bar[s], kb * kBK, nb * 128, wblk);
+        if (swiglu) tma_load_3d(sa + kTileBytesA, &tm_u, &full_bar[s], kb * kBK, nb * 128, wblk);
+        uint8_t* sb = sa + a_bytes;
+        for (int i = 0; i < n_load / 32; ++i)
+          tma_load_2d(sb + i * 4096, &tm_x, &full_bar[s], kb * kBK, row0 + i * 32);
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      const int nc0 = min(n_pad, 256);
+      const int nc1 = n_pad - nc0;
+      const uint32_t id0 = make_idesc_bf16(128, nc0);
+      const uint32_t id1 = nc1 > 0 ? make_idesc_bf16(128, nc1) : 0u;
+      for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % p.stages;
+        const uint32_t ph = (kb / p.stages) & 1;
+        mbar_wait(&full_bar[s], ph);
+        tc_fence_after();
+        const uint32_t a_addr = smem_u32(smem + s * stage_bytes);
+        const uint32_t b_addr = a_addr + a_bytes;
+#pragma unroll
+        for (int k = 0; k < kBK / 16; ++k) {
+          const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+          const uint64_t ad = make_sdesc_sw128(a_addr + k * 32, 16, 1024);
+          const uint64_t bd0 = make_sdesc_sw128(b_addr + k * 32, 16, 1024);
+          umma_bf16(tmem, ad, bd0, id0, acc);
+          if (nc1 > 0) {
+            const uint64_t bd1 = make_sdesc_sw128(b_addr + 256 * 128 + k * 32, 16, 1024);
+            umma_bf16(tmem + 256, ad, bd1, id1, acc);
+          }
+          if (swiglu) {
+            const uint64_t au = make_sdesc_sw128(a_addr + kTileBytesA + k * 32, 16, 1024);
+            umma_bf16(tmem + 256, au, bd0, id0, acc);
+          }
+        }
+        umma_commit(&empty_bar[s]);
+      }
+      umma_commit(&tmem_full_bar);
+    }
+  } else {
+    // ---- epilogue: warps 2..5 own TMEM lane quarters (warp % 4) ----
+    const int q = warp & 3;
+    const int row = q * 32 + lane;  // weight row within the tile
+    const int n = nb * 128 + row;   // output feature
+    mbar_wait(&tmem_full_bar, 0);
+    tc_fence_after();
+    const uint32_t trow = tmem + (uint32_t(q * 32) << 16);
+    if (p.epilogue == SMO_EPI_ARGMAX) {
+      // All MMAs are done: the stage ring is free scratch, [32 tokens][129] f32
+      // (padded so both the column writes and the row scans are conflict-free).
+      float* scratch = reinterpret_cast<float*>(smem);
+      for (int c0 = 0; c0 < n_pad; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(trow + c0, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) scratch[j * 129 + row] = __uint_as_float(r[j]);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (warp == 2 && c0 + lane < cnt) {
+          // ties resolve to the lowest vocabulary index (strict >)
+          float best = scratch[lane * 129];
+          int bi = 0;
+          for (int i = 1; i < 128; ++i) {
+            const float v = scratch[lane * 129 + i];
+            if (v > best) { best = v; bi = i; }
+          }
+          const size_t at = size_t(row0 + c0 + lane) * p.n_tiles + nb;
+          p.amax_val[at] = best;
+          p.amax_idx[at] = nb * 128 + bi;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+    } else {
+      for (int c0 = 0; c0 < n_pad; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(trow + c0, r);
+        if (swiglu) {
+          uint32_t u[32];
+          tmem_ld32(trow + 256 + c0, u);
+          tmem_ld_wait();
+          uint16_t* out = reinterpret_cast<uint16_t*>(p.out);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (c0 + j < cnt) {
+              const float gv = __uint_as_float(r[j]);
+              const float hv = gv / (1.0f + __expf(-gv)) * __uint_as_float(u[j]);
+              out[size_t(row0 + c0 + j) * p.ldo + n] = f2bf(hv);
+            }
+          }
+        } else {
+          tmem_ld_wait();
+          if (p.epilogue == SMO_EPI_BF16) {
+            uint16_t* out = reinterpret_cast<uint16_t*>(p.out);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (c0 + j < cnt) out[size_t(row0 + c0 + j) * p.ldo + n] = f2bf(__uint_as_float(r[j]));
+          } else if (p.epilogue == SMO_EPI_F32) {
+            float* out = reinterpret_cast<float*>(p.out);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (c0 + j < cnt) out[size_t(row0 + c0 + j) * p.ldo + n] = __uint_as_float(r[j]);
+          } else {  // SMO_EPI_F32_ADD
+            float* out = reinterpret_cast<float*>(p.out);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (c0 + j < cnt) out[size_t(row0 + c0 + j) * p.ldo + n] += __uint_as_float(r[j]);
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc_dyn(tmem_cols, tmem);
+}
+
+}  // namespace
+
+void gemm_launch(const smo_gemm_args& a, cudaStream_t stream) {
+  SMO_REQUIRE(a.x && a.w, "gemm: null operand");
+  SMO_REQUIRE(a.K > 0 && a.K % kBK == 0, "gemm: K must be a positive multiple of 64");
+  SMO_REQUIRE(a.N > 0 && a.N % 128 == 0, "gemm: N must be a positive multiple of 128");
+  SMO_REQUIRE(a.rows > 0 && a.groups > 0, "gemm: rows/groups must be positive");
+  SMO_REQUIRE(a.groups == 1 || a.row_offsets, "gemm: grouped GEMM needs row_offsets");
+  const bool swiglu = a.epilogue == SMO_EPI_SWIGLU;
+  SMO_REQUIRE(!swiglu || a.w_up, "gemm: SWIGLU needs w_up");
+  SMO_REQUIRE(a.epilogue != SMO_EPI_ARGMAX || (a.argmax_val && a.argmax_idx), "gemm: ARGMAX needs partial buffers");
+  SMO_REQUIRE(a.epilogue == SMO_EPI_ARGMAX || a.out, "gemm: null output");
+  const int per_group = a.max_rows_per_group > 0 ? std::min(a.max_rows_per_group, a.rows) : a.rows;
+  const int cap = swiglu ? 256 : 512;
+  int tile = std::min(cap, (per_group + 31) & ~31);
+  const int token_tiles = (per_group + tile - 1) / tile;
+  const int a_bytes = kTileBytesA * (swiglu ? 2 : 1);
+  const int stage_bytes = a_bytes + tile * 128;
+  int stages = std::min(kMaxStages, kSmemBudget / stage_bytes);
+  SMO_REQUIRE(stages >= 2, "gemm: token tile too large for the smem ring");
+  uint32_t cols = 32;
+  const int need = swiglu ? 512 : tile;
+  while (int(cols) < need) cols <<= 1;
+
+  CUtensorMap tw, tu, tx;
+  const int pool = std::max(1, a.w_pool_blocks);
+  const uint64_t stride_blk = a.w_block_stride ? a.w_block_stride : uint64_t(a.N) * a.K * 2;
+  {
+    uint64_t dims[3] = {uint64_t(a.K), uint64_t(a.N), uint64_t(pool)};
+    uint64_t strides[2] = {uint64_t(a.K) * 2, stride_blk};
+    uint32_t box[3] = {uint32_t(kBK), 128, 1};
+    make_tmap_bf16(&tw, a.w, 3, dims, strides, box, true);
+    make_tmap_bf16(&tu, swiglu ? a.w_up : a.w, 3, dims, strides, box, true);
+  }
+  {
+    uint64_t dims[2] = {uint64_t(a.K), uint64_t(a.rows)};
+    uint64_t strides[1] = {uint64_t(a.K) * 2};
+    uint32_t box[2] = {uint32_t(kBK), 32};
+    make_tmap_bf16(&tx, a.x, 2, dims, strides, box, true);
+  }
+  GemmParams p{};
+  p.K = a.K;
+  p.N = a.N;
+  p.rows = a.rows;
+  p.row_offsets = a.row_offsets;
+  p.w_index = a.w_index;
+  p.tile_tokens = tile;
+  p.stages = stages;
+  p.epilogue = a.epilogue;
+  p.out = a.out;
+  p.ldo = a.ldo > 0 ? a.ldo : a.N;
+  p.amax_val = a.argmax_val;
+  p.amax_idx = a.argmax_idx;
+  p.n_tiles = a.N / 128;
+  const size_t smem = size_t(stages) * stage_bytes + 1024;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SMO_CUDA_CHECK(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kSmemBudget + 4096));
+    attr_set = true;
+  }
+  dim3 grid(a.N / 128, a.groups, token_tiles);
+  gemm_tc_kernel<<<grid, kThreads, smem, stream>>>(tw, tu, tx, p, cols);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace smo

@@ -1,0 +1,533 @@
+// ops.cu — K2 router top-k, K3 permute / unpermute-combine, K6 argmax +
+// greedy accept + KV rollback, and the small support ops of a Mixtral verify
+// layer (RMSNorm, embedding, RoPE + KV append, procedural fills).
+// All of these are HBM/latency-bound; none is GEMM-shaped.
+#include <cmath>
+
+#include "common.cuh"
+
+namespace smo {
+
+namespace {
+
+constexpr int kMaxExperts = 64;
+constexpr int kMaxTopK = 8;
+
+// ---------------------------------------------------------------- fills
+__global__ void fill_uniform_kernel(uint16_t* dst, uint64_t count, uint64_t key, uint64_t base, float s) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t x = splitmix64(splitmix64(key ^ (base + i)));
+    const int32_t c = int32_t((x >> 40) << 1) - (1 << 24);
+    dst[i] = f2bf(__fmul_rn(float(c), s));
+  }
+}
+
+__global__ void fill_kv_prefix_kernel(uint16_t* cache, const int32_t* prefix, int n_kv, int d, int s_max,
+                                      uint64_t key, float s) {
+  const int rh = blockIdx.y;  // r * n_kv + h
+  const int r = rh / n_kv;
+  const int len = prefix[r];
+  const uint64_t total = uint64_t(len) * d;
+  for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < total;
+       e += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t idx = (uint64_t(rh) << 32) | e;
+    const uint64_t x = splitmix64(splitmix64(key ^ idx));
+    const int32_t c = int32_t((x >> 40) << 1) - (1 << 24);
+    cache[uint64_t(rh) * s_max * d + e] = f2bf(__fmul_rn(float(c), s));
+  }
+}
+
+// ---------------------------------------------------------------- K2 router
+// One warp per token. Lane l owns the 8-element chunks at 256*i + 8*l and
+// accumulates them in order with fmaf; an xor-butterfly then reduces the 32
+// partials (identical on every lane). This fixed order is what the oracle
+// restates (oracle.c:orc_router_logits), so ids are bit-exact.
+__global__ void router_topk_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w, int T, int h,
+                                   int E, int k, float* logits_out, int32_t* ids, float* weights) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (warp >= T) return;
+  const uint16_t* xr = x + size_t(warp) * h;
+  float lg[kMaxExperts];
+  for (int e = 0; e < E; ++e) {
+    const uint16_t* wr = w + size_t(e) * h;
+    float a = 0.f;
+    for (int base = lane * 8; base < h; base += 256) {
+      const uint4 xv = *reinterpret_cast<const uint4*>(xr + base);
+      const uint4 wv = *reinterpret_cast<const uint4*>(wr + base);
+      const uint32_t xs[4] = {xv.x, xv.y, xv.z, xv.w};
+      const uint32_t ws[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        a = __fmaf_rn(__uint_as_float(xs[t] << 16), __uint_as_float(ws[t] << 16), a);
+        a = __fmaf_rn(__uint_as_float(xs[t] & 0xffff0000u), __uint_as_float(ws[t] & 0xffff0000u), a);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
+    lg[e] = a;
+  }
+  if (lane != 0) return;
+  if (logits_out)
+    for (int e = 0; e < E; ++e) logits_out[size_t(warp) * E + e] = lg[e];
+  uint64_t used = 0;
+  int sel[kMaxTopK];
+  for (int j = 0; j < k; ++j) {
+    int best = -1;
+    for (int e = 0; e < E; ++e) {
+      if ((used >> e) & 1ull) continue;
+      if (best < 0 || lg[e] > lg[best]) best = e;
+    }
+    used |= 1ull << best;
+    sel[j] = best;
+    ids[size_t(warp) * k + j] = best;
+  }
+  const float mx = lg[sel[0]];
+  float ex[kMaxTopK], den = 0.f;
+  for (int j = 0; j < k; ++j) {
+    ex[j] = expf(lg[sel[j]] - mx);
+    den += ex[j];
+  }
+  for (int j = 0; j < k; ++j) weights[size_t(warp) * k + j] = ex[j] / den;
+}
+
+// ---------------------------------------------------------------- K3 permute
+// Single CTA, one warp per expert (strided): ballot + popc gives each pair's
+// rank among the earlier pairs of its expert -> a stable counting sort.
+__global__ void permute_kernel(const int32_t* __restrict__ ids, int P, int E, int32_t* offsets, int32_t* perm,
+                               int32_t* pos) {
+  __shared__ int cnt[kMaxExperts + 1];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  for (int e = warp; e < E; e += nw) {
+    int c = 0;
+    for (int i0 = 0; i0 < P; i0 += 32) {
+      const int i = i0 + lane;
+      c += __popc(__ballot_sync(0xffffffffu, i < P && ids[i] == e));
+    }
+    if (lane == 0) cnt[e] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int e = 0; e < E; ++e) {
+      const int c = cnt[e];
+      cnt[e] = run;
+      offsets[e] = run;
+      run += c;
+    }
+    offsets[E] = run;
+  }
+  __syncthreads();
+  for (int e = warp; e < E; e += nw) {
+    int base = cnt[e];
+    for (int i0 = 0; i0 < P; i0 += 32) {
+      const int i = i0 + lane;
+      const bool mine = i < P && ids[i] == e;
+      const uint32_t bal = __ballot_sync(0xffffffffu, mine);
+      if (mine) {
+        const int at = base + __popc(bal & ((1u << lane) - 1u));
+        perm[at] = i;
+        pos[i] = at;
+      }
+      base += __popc(bal);
+    }
+  }
+}
+
+__global__ void gather_rows_kernel(const uint16_t* __restrict__ x, const int32_t* __restrict__ perm, int k,
+                                   int h, int P, uint16_t* __restrict__ xp) {
+  const int row = blockIdx.x;
+  if (row >= P) return;
+  const int src = perm[row] / k;
+  const uint4* s = reinterpret_cast<const uint4*>(x + size_t(src) * h);
+  uint4* d = reinterpret_cast<uint4*>(xp + size_t(row) * h);
+  for (int c = threadIdx.x; c < h / 8; c += blockDim.x) d[c] = s[c];
+}
+
+__global__ void combine_kernel(const float* __restrict__ y, const int32_t* __restrict__ pos,
+                               const float* __restrict__ w, int T, int k, int h, float* __restrict__ res) {
+  const int t = blockIdx.x;
+  for (int c = threadIdx.x * 4; c < h; c += blockDim.x * 4) {
+    float4 acc = *reinterpret_cast<float4*>(res + size_t(t) * h + c);
+    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < k; ++j) {
+      const float wj = w[size_t(t) * k + j];
+      const float4 v = *reinterpret_cast<const float4*>(y + size_t(pos[size_t(t) * k + j]) * h + c);
+      sum.x = __fmaf_rn(wj, v.x, sum.x);
+      sum.y = __fmaf_rn(wj, v.y, sum.y);
+      sum.z = __fmaf_rn(wj, v.z, sum.z);
+      sum.w = __fmaf_rn(wj, v.w, sum.w);
+    }
+    acc.x += sum.x;
+    acc.y += sum.y;
+    acc.z += sum.z;
+    acc.w += sum.w;
+    *reinterpret_cast<float4*>(res + size_t(t) * h + c) = acc;
+  }
+}
+
+// ---------------------------------------------------------------- norm / embed
+__global__ void rmsnorm_kernel(const float* __restrict__ x, const uint16_t* __restrict__ gain, int h, float eps,
+                               uint16_t* __restrict__ y) {
+  const int t = blockIdx.x;
+  const float* xr = x + size_t(t) * h;
+  float ss = 0.f;
+  for (int c = threadIdx.x * 4; c < h; c += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(xr + c);
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  __shared__ float red[32];
+  ss = warp_sum(ss);
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(red[0] / float(h) + eps);
+  for (int c = threadIdx.x * 4; c < h; c += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(xr + c);
+    const uint2 gv = *reinterpret_cast<const uint2*>(gain + c);
+    const float g0 = __uint_as_float(gv.x << 16), g1 = __uint_as_float(gv.x & 0xffff0000u);
+    const float g2 = __uint_as_float(gv.y << 16), g3 = __uint_as_float(gv.y & 0xffff0000u);
+    uint2 o;
+    o.x = uint32_t(f2bf(v.x * inv * g0)) | (uint32_t(f2bf(v.y * inv * g1)) << 16);
+    o.y = uint32_t(f2bf(v.z * inv * g2)) | (uint32_t(f2bf(v.w * inv * g3)) << 16);
+    *reinterpret_cast<uint2*>(y + size_t(t) * h + c) = o;
+  }
+}
+
+__global__ void embed_kernel(const int32_t* __restrict__ tok, const uint16_t* __restrict__ emb, int h,
+                             float* __restrict__ x) {
+  const int t = blockIdx.x;
+  const uint16_t* src = emb + size_t(tok[t]) * h;
+  for (int c = threadIdx.x; c < h; c += blockDim.x) x[size_t(t) * h + c] = bf2f(src[c]);
+}
+
+// ---------------------------------------------------------------- RoPE + append
+// One block per verify row (r, i). Rotate-half RoPE at position
+// prefix[r] + depth(i); angles in fp64 so long positions stay accurate.
+__global__ void rope_append_kernel(const uint16_t* __restrict__ qkv, const int32_t* __restrict__ prefix,
+                                   const int32_t* __restrict__ parent, int n, int n_q, int n_kv, int d, int s_max,
+                                   double theta, uint16_t* __restrict__ q_out, uint16_t* __restrict__ kc,
+                                   uint16_t* __restrict__ vc) {
+  const int row = blockIdx.x;
+  const int r = row / n, i = row % n;
+  int depth = i;
+  if (parent) {
+    depth = 0;
+    int cur = i;
+    while (cur > 0 && depth <= n) {
+      cur = parent[size_t(r) * n + cur];
+      ++depth;
+    }
+  }
+  const int pos = prefix[r] + depth;
+  const int slot = prefix[r] + i;
+  const int half = d / 2;
+  const int width = (n_q + 2 * n_kv) * d;
+  const uint16_t* src = qkv + size_t(row) * width;
+  for (int e = threadIdx.x; e < (n_q + n_kv) * half; e += blockDim.x) {
+    const int head = e / half, j = e % half;
+    const double inv = pow(theta, -2.0 * j / double(d));
+    double sn, cs;
+    sincos(double(pos) * inv, &sn, &cs);
+    const float c = float(cs), s = float(sn);
+    const float a = bf2f(src[head * d + j]), b = bf2f(src[head * d + j + half]);
+    const uint16_t o0 = f2bf(a * c - b * s), o1 = f2bf(b * c + a * s);
+    if (head < n_q) {
+      uint16_t* dst = q_out + (size_t(row) * n_q + head) * d;
+      dst[j] = o0;
+      dst[j + half] = o1;
+    } else {
+      const int hk = head - n_q;
+      uint16_t* dst = kc + ((size_t(r) * n_kv + hk) * s_max + slot) * d;
+      dst[j] = o0;
+      dst[j + half] = o1;
+    }
+  }
+  for (int e = threadIdx.x; e < n_kv * d; e += blockDim.x) {
+    const int hk = e / d, c = e % d;
+    vc[((size_t(r) * n_kv + hk) * s_max + slot) * d + c] = src[(n_q + n_kv) * d + e];
+  }
+}
+
+// ---------------------------------------------------------------- K6
+__global__ void argmax_reduce_kernel(const float* __restrict__ val, const int32_t* __restrict__ idx, int rows,
+                                     int parts, int32_t* target) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+  if (warp >= rows) return;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int p = lane; p < parts; p += 32) {
+    const float v = val[size_t(warp) * parts + p];
+    const int i = idx[size_t(warp) * parts + p];
+    if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+  }
+  if (lane == 0) target[warp] = bi;
+}
+
+__global__ void argmax_rows_kernel(const float* __restrict__ logits, int V, int32_t* target) {
+  const int row = blockIdx.x;
+  const float* l = logits + size_t(row) * V;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    const float x = l[v];
+    if (x > best || (x == best && v < bi)) { best = x; bi = v; }
+  }
+  __shared__ float sv[32];
+  __shared__ int si[32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+  }
+  if (threadIdx.x % 32 == 0) { sv[threadIdx.x / 32] = best; si[threadIdx.x / 32] = bi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < int(blockDim.x / 32); ++w)
+      if (sv[w] > best || (sv[w] == best && si[w] < bi)) { best = sv[w]; bi = si[w]; }
+    target[row] = bi;
+  }
+}
+
+// Greedy verification, one thread per request (n <= 64). Restates
+// specdec.hpp:65-76 with the draw replaced by token == argmax(parent row):
+// longest accepted root path, children scanned in id order so ties resolve
+// to the lower node id; committed = accepted + 1.
+__global__ void greedy_accept_kernel(const int32_t* __restrict__ tokens, const int32_t* __restrict__ target,
+                                     const int32_t* __restrict__ parent, int b, int n, int32_t* acc_len,
+                                     int32_t* bonus, int32_t* keep) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= b) return;
+  const int32_t* tok = tokens + size_t(r) * n;
+  const int32_t* tgt = target + size_t(r) * n;
+  int8_t best[64], depth[64];
+  for (int i = n - 1; i >= 0; --i) {
+    best[i] = -1;
+    depth[i] = 0;
+    for (int c = i + 1; c < n; ++c) {
+      const int pc = parent ? parent[size_t(r) * n + c] : c - 1;
+      if (pc != i || tok[c] != tgt[i]) continue;
+      if (1 + depth[c] > depth[i]) {
+        depth[i] = int8_t(1 + depth[c]);
+        best[i] = int8_t(c);
+      }
+    }
+  }
+  int cur = 0, a = 0;
+  if (keep) keep[size_t(r) * n] = 0;
+  while (best[cur] >= 0) {
+    cur = best[cur];
+    ++a;
+    if (keep) keep[size_t(r) * n + a] = cur;
+  }
+  if (keep)
+    for (int i = a + 1; i < n; ++i) keep[size_t(r) * n + i] = -1;
+  acc_len[r] = a;
+  bonus[r] = tgt[cur];
+}
+
+// Tree KV compaction: row keep[r, j] -> prefix + j, j ascending (keep[j] >= j,
+// so no source is overwritten before it is read). One block per (layer, r, h).
+__global__ void kv_rollback_kernel(void* const* kcs, void* const* vcs, const int32_t* prefix, const int32_t* acc,
+                                   const int32_t* keep, int b, int n, int n_kv, int d, int s_max) {
+  const int layer = blockIdx.z, r = blockIdx.y, h = blockIdx.x;
+  const int a = acc[r], p = prefix[r];
+  uint16_t* kc = reinterpret_cast<uint16_t*>(kcs[layer]) + (size_t(r) * n_kv + h) * s_max * d;
+  uint16_t* vc = reinterpret_cast<uint16_t*>(vcs[layer]) + (size_t(r) * n_kv + h) * s_max * d;
+  for (int j = 1; j <= a; ++j) {
+    const int src = keep[size_t(r) * n + j];
+    if (src != j)
+      for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        kc[size_t(p + j) * d + c] = kc[size_t(p + src) * d + c];
+        vc[size_t(p + j) * d + c] = vc[size_t(p + src) * d + c];
+      }
+    __syncthreads();
+  }
+}
+
+__global__ void kv_len_kernel(const int32_t* prefix, const int32_t* acc, int b, int32_t* kv_len) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < b) kv_len[r] = prefix[r] + acc[r] + 1;
+}
+
+// Compact draft mask: bit j of row (r,i) = draft j is an ancestor-or-self of
+// draft i (chain: j <= i) — CompactMask::chain generalised to trees
+// (attention.hpp:52-57).
+__global__ void build_mask_kernel(const int32_t* __restrict__ parent, int b, int n, uint64_t* mask) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= b * n) return;
+  const int r = row / n, i = row % n;
+  uint64_t m = 0;
+  if (!parent) {
+    m = (i >= 63) ? ~0ull : ((1ull << (i + 1)) - 1ull);
+  } else {
+    int cur = i, guard = 0;
+    while (cur >= 0 && guard <= n) {
+      m |= 1ull << cur;
+      cur = (cur == 0) ? -1 : parent[size_t(r) * n + cur];
+      ++guard;
+    }
+  }
+  mask[row] = m;
+}
+
+inline int grid_for(uint64_t n, int block) {
+  const uint64_t g = (n + block - 1) / block;
+  return int(g > 148ull * 32 ? 148ull * 32 : (g ? g : 1));
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- launchers
+void fill_uniform(void* dst, uint64_t count, uint64_t seed, uint64_t tensor_id, uint64_t base, float scale,
+                  cudaStream_t st) {
+  if (!count) return;
+  SMO_REQUIRE(dst, "fill: null pointer");
+  const float s = std::ldexp(scale, -24);
+  fill_uniform_kernel<<<grid_for(count, 256), 256, 0, st>>>(reinterpret_cast<uint16_t*>(dst), count,
+                                                            seed ^ (tensor_id * 0x9e3779b97f4a7c15ULL), base, s);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+void fill_kv_prefix(void* cache, const int32_t* prefix, int b, int n_kv, int d, int s_max, uint64_t seed,
+                    uint64_t tensor_id, cudaStream_t st) {
+  SMO_REQUIRE(cache && prefix && b > 0 && n_kv > 0 && d > 0, "fill_kv_prefix: bad arguments");
+  dim3 grid(64, b * n_kv);
+  fill_kv_prefix_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<uint16_t*>(cache), prefix, n_kv, d, s_max,
+                                              seed ^ (tensor_id * 0x9e3779b97f4a7c15ULL), std::ldexp(1.0f, -24));
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+void router_topk(const void* x, const void* w, int T, int h, int E, int k, float* logits, int32_t* ids,
+                 float* weights, cudaStream_t st) {
+  SMO_REQUIRE(x && w && ids && weights, "router: null pointer");
+  SMO_REQUIRE(h % 256 == 0, "router: h must be a multiple of 256");
+  SMO_REQUIRE(E >= 1 && E <= kMaxExperts && k >= 1 && k <= kMaxTopK && k <= E, "router: bad E/k");
+  if (T <= 0) return;
+  const int warps_per_block = 4;
+  router_topk_kernel<<<(T + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0, st>>>(
+      reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(w), T, h, E, k, logits, ids, weights);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+void permute(const int32_t* ids, int T, int k, int E, const void* x, int h, int32_t* offsets, int32_t* perm,
+             int32_t* pos, void* xp, cudaStream_t st) {
+  SMO_REQUIRE(ids && offsets && perm && pos, "permute: null pointer");
+  SMO_REQUIRE(E >= 1 && E <= kMaxExperts, "permute: bad E");
+  const int P = T * k;
+  permute_kernel<<<1, 1024, 0, st>>>(ids, P, E, offsets, perm, pos);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+  if (x && xp && P > 0) {
+    SMO_REQUIRE(h % 8 == 0, "permute: h must be a multiple of 8");
+    gather_rows_kernel<<<P, 128, 0, st>>>(reinterpret_cast<const uint16_t*>(x), perm, k, h, P,
+                                          reinterpret_cast<uint16_t*>(xp));
+    count_launch();
+    SMO_CUDA_CHECK(cudaGetLastError());
+  }
+}
+
+void unpermute_combine(const float* y, const int32_t* pos, const float* w, int T, int k, int h, float* res,
+                       cudaStream_t st) {
+  SMO_REQUIRE(y && pos && w && res, "combine: null pointer");
+  SMO_REQUIRE(h % 4 == 0, "combine: h must be a multiple of 4");
+  if (T <= 0) return;
+  combine_kernel<<<T, 256, 0, st>>>(y, pos, w, T, k, h, res);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+void rmsnorm(const float* x, const void* gain, int T, int h, float eps, void* y, cudaStream_t st) {
+  SMO_REQUIRE(x && gain && y && h % 4 == 0, "rmsnorm: bad arguments");
+  if (T <= 0) return;
+  rmsnorm_kernel<<<T, 256, 0, st>>>(x, reinterpret_cast<const uint16_t*>(gain), h, eps,
+                                    reinterpret_cast<uint16_t*>(y));
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+void embed(const int32_t* tok, const void* emb, int T, int h, float* x, cudaStream_t st) {
+  SMO_REQUIRE(tok && emb && x, "embed: null pointer");
+  if (T <= 0) return;
+  embed_kernel<<<T, 256, 0, st>>>(tok, reinterpret_cast<const uint16_t*>(emb), h, x);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+void rope_append(const void* qkv, const int32_t* prefix, const int32_t* parent, int b, int n, int n_q, int n_kv,
+                 int d, int s_max, float theta, void* q_out, void* kc, void* vc, cudaStream_t st) {
+  SMO_REQUIRE(qkv && prefix && q_out && kc && vc, "rope_append: null pointer");
+  SMO_REQUIRE(d % 2 == 0, "rope_append: odd head_dim");
+  rope_append_kernel<<<b * n, 256, 0, st>>>(reinterpret_cast<const uint16_t*>(qkv), prefix, parent, n, n_q, n_kv,
+                                            d, s_max, double(theta), reinterpret_cast<uint16_t*>(q_out),
+                                            reinterpret_cast<uint16_t*>(kc), reinterpret_cast<uint16_t*>(vc));
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+void argmax_reduce(const float* val, const int32_t* idx, int rows, int parts, int32_t* target, cudaStream_t st) {
+  SMO_REQUIRE(val && idx && target, "argmax: null pointer");
+  if (rows <= 0) return;
+  argmax_reduce_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(val, idx, rows, parts, target);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+void argmax_rows(const float* logits, int rows, int V, int32_t* target, cudaStream_t st) {
+  SMO_REQUIRE(logits && target, "argmax: null pointer");
+  if (rows <= 0) return;
+  argmax_rows_kernel<<<rows, 256, 0, st>>>(logits, V, target);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+void greedy_accept(const int32_t* tokens, const int32_t* target, const int32_t* parent, int b, int n,
+                   int32_t* acc_len, int32_t* bonus, int32_t* keep, cudaStream_t st) {
+  SMO_REQUIRE(tokens && target && acc_len && bonus, "accept: null pointer");
+  SMO_REQUIRE(n >= 1 && n <= 64, "accept: n must be in [1, 64]");
+  if (b <= 0) return;
+  greedy_accept_kernel<<<(b + 63) / 64, 64, 0, st>>>(tokens, target, parent, b, n, acc_len, bonus, keep);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+void build_mask(const int32_t* parent, int b, int n, uint64_t* mask, cudaStream_t st) {
+  SMO_REQUIRE(mask && n >= 1 && n <= 64, "build_mask: bad arguments");
+  build_mask_kernel<<<(b * n + 127) / 128, 128, 0, st>>>(parent, b, n, mask);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+void kv_rollback(void* const* kcs, void* const* vcs, int n_layers, const int32_t* prefix, const int32_t* acc,
+                 const int32_t* keep, int b, int n, int n_kv, int d, int s_max, int32_t* kv_len, cudaStream_t st) {
+  SMO_REQUIRE(prefix && acc, "kv_rollback: null pointer");
+  if (keep && kcs && vcs && n_layers > 0) {
+    dim3 grid(n_kv, b, n_layers);
+    kv_rollback_kernel<<<grid, 128, 0, st>>>(kcs, vcs, prefix, acc, keep, b, n, n_kv, d, s_max);
+    count_launch();
+    SMO_CUDA_CHECK(cudaGetLastError());
+  }
+  if (kv_len) {
+    kv_len_kernel<<<(b + 127) / 128, 128, 0, st>>>(prefix, acc, b, kv_len);
+    count_launch();
+    SMO_CUDA_CHECK(cudaGetLastError());
+  }
+}
+
+}  // namespace smo

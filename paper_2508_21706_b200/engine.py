@@ -1,0 +1,158 @@
+"""VerifyEngine: Python handle over smo_engine_* (the measured verify step).
+
+Mirrors the additive engine API of SURVEY.md §8(b): construct from a model
+shape + options, `verify(batch)` runs one speculative verification step
+(the reference's target DAG, pipeline.hpp:147-206, realised on CUDA streams)
+and returns the greedy accept result; `last_times()` returns the measured
+stage durations in the reference's IterationBreakdown vocabulary
+(report.hpp:27-37).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib as L
+
+
+@dataclass
+class ModelShape:
+    hidden: int
+    inter: int
+    n_expert: int
+    top_k: int
+    n_layers: int
+    n_q_heads: int
+    n_kv_heads: int
+    head_dim: int
+    vocab: int
+    rope_theta: float = 1e6
+    rms_eps: float = 1e-5
+    seed: int = 0x5EED
+    lm_scale: float = 1.0
+    router_scale: float = 1.0
+
+    @property
+    def expert_bytes(self) -> int:
+        return 3 * self.hidden * self.inter * 2
+
+    def to_c(self) -> L.ModelConfig:
+        return L.ModelConfig(self.hidden, self.inter, self.n_expert, self.top_k, self.n_layers, self.n_q_heads,
+                             self.n_kv_heads, self.head_dim, self.vocab, self.rope_theta, self.rms_eps, self.seed,
+                             self.lm_scale, self.router_scale)
+
+
+# BASELINE.json configs
+TINY = ModelShape(hidden=512, inter=1792, n_expert=8, top_k=2, n_layers=2, n_q_heads=8, n_kv_heads=2,
+                  head_dim=64, vocab=32000)
+MIXTRAL_8X7B = ModelShape(hidden=4096, inter=14336, n_expert=8, top_k=2, n_layers=32, n_q_heads=32,
+                          n_kv_heads=8, head_dim=128, vocab=32000)
+MIXTRAL_8X22B = ModelShape(hidden=6144, inter=16384, n_expert=8, top_k=2, n_layers=56, n_q_heads=48,
+                           n_kv_heads=8, head_dim=128, vocab=32000)
+
+
+@dataclass
+class VerifyResult:
+    acc_len: np.ndarray
+    bonus: np.ndarray
+    keep: np.ndarray
+    target: np.ndarray
+
+
+class VerifyEngine:
+    def __init__(self, shape: ModelShape, *, max_batch: int, max_verify: int, max_seq: int, hbm_slots: int = 2,
+                 expert_cache_bytes: int = 0, host_alias_layers: int = 0, device: int = 0, debug: bool = False):
+        self.shape = shape
+        self.max_batch, self.max_verify, self.max_seq = max_batch, max_verify, max_seq
+        opt = L.EngineOptions(max_batch, max_verify, max_seq, hbm_slots, int(expert_cache_bytes),
+                              host_alias_layers, device, L.ENGINE_DEBUG if debug else 0, 0, 1, None)
+        cfg = shape.to_c()
+        h = C.c_void_p()
+        L.check(L.load().smo_engine_create(C.byref(cfg), C.byref(opt), C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            L.load().smo_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def fill_prefix(self, prefix_len) -> None:
+        p = np.ascontiguousarray(prefix_len, np.int32)
+        L.check(L.load().smo_engine_fill_prefix(self._h, p.ctypes.data_as(C.c_void_p), p.size))
+
+    def verify(self, tokens, prefix_len, parent=None, stream: Optional[int] = None) -> VerifyResult:
+        """One verify step from HOST arrays (the e2e path): tokens [b, n] int32
+        (column 0 = root), prefix_len [b]; parent [b, n] (tree) or None (chain)."""
+        tok = np.ascontiguousarray(tokens, np.int32)
+        b, n = tok.shape
+        pre = np.ascontiguousarray(prefix_len, np.int32)
+        par = None if parent is None else np.ascontiguousarray(parent, np.int32)
+        vp = lambda a: None if a is None else a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        acc = np.zeros(b, np.int32)
+        bonus = np.zeros(b, np.int32)
+        keep = np.zeros(b * n, np.int32)
+        target = np.zeros(b * n, np.int32)
+        inp = L.VerifyBatch(b, n, vp(tok), vp(par), vp(pre), 0)
+        out = L.VerifyOutput(vp(acc), vp(bonus), vp(keep), vp(target), 0)
+        L.check(L.load().smo_engine_verify(self._h, C.byref(inp), C.byref(out), C.c_void_p(stream or 0)))
+        return VerifyResult(acc, bonus, keep.reshape(b, n), target.reshape(b, n))
+
+    def verify_device(self, tokens, prefix_len, acc, bonus, parent=None, keep=None, target=None,
+                      stream: Optional[int] = None) -> None:
+        """Device-resident variant (torch CUDA tensors); asynchronous."""
+        b, n = tokens.shape
+        p = lambda t: None if t is None else C.c_void_p(t.data_ptr())  # noqa: E731
+        inp = L.VerifyBatch(b, n, p(tokens), p(parent), p(prefix_len), 1)
+        out = L.VerifyOutput(p(acc), p(bonus), p(keep), p(target), 1)
+        L.check(L.load().smo_engine_verify(self._h, C.byref(inp), C.byref(out), C.c_void_p(stream or 0)))
+
+    def last_times(self) -> dict:
+        t = L.StageTimes()
+        L.check(L.load().smo_engine_last_times(self._h, C.byref(t)))
+        return {k: getattr(t, k) for k, _ in L.StageTimes._fields_}
+
+    def debug_tensor(self, name: str, layer: int, shape, dtype) -> np.ndarray:
+        out = np.zeros(shape, dtype)
+        L.check(L.load().smo_engine_debug_tensor(self._h, name.encode(), layer, out.ctypes.data_as(C.c_void_p),
+                                                 out.nbytes))
+        return out
+
+    def tensor_ptr(self, name: str, layer: int = -1, expert: int = 0):
+        p, nb = C.c_void_p(), C.c_size_t()
+        L.check(L.load().smo_engine_tensor_ptr(self._h, name.encode(), layer, expert, C.byref(p), C.byref(nb)))
+        return p.value, nb.value
+
+
+def geometric_alpha(p: float, k: int) -> float:
+    """alpha(k) = sum_{i<=k} p^i (config.hpp:77-89)."""
+    return sum(p ** i for i in range(k + 1)) if p != 1.0 else float(k + 1)
+
+
+def step_roofline(shape: ModelShape, b: int, n: int, prefix: int, h2d_gbs: float, hbm_gbs: float,
+                  tflops: float, cached_blocks: int = 0) -> dict:
+    """Binding roofline of one verify step: the slower of
+    host-link bytes, HBM bytes and tensor peak (roofline.hpp:108-151)."""
+    s = shape
+    T = b * n
+    e_bytes = s.expert_bytes
+    activated = s.n_expert  # large batch: every expert activates
+    h2d = (s.n_layers * activated - cached_blocks) * e_bytes
+    kv = 2 * b * (prefix + n) * s.n_kv_heads * s.head_dim * 2
+    dense = (s.hidden * (s.n_q_heads + 2 * s.n_kv_heads) * s.head_dim + s.n_q_heads * s.head_dim * s.hidden) * 2
+    hbm = s.n_layers * (activated * e_bytes + kv + dense) + s.vocab * s.hidden * 2
+    flops = s.n_layers * (2 * 3 * s.hidden * s.inter * T * s.top_k + 2 * T * dense / 2
+                          + 4 * b * n * (prefix + n) * s.n_q_heads * s.head_dim) + 2 * T * s.hidden * s.vocab
+    t = {"h2d": h2d / (h2d_gbs * 1e9), "hbm": hbm / (hbm_gbs * 1e9), "tensor": flops / (tflops * 1e12)}
+    bound = max(t, key=t.get)
+    return {"bound": bound, "t_roof_s": t[bound], "h2d_bytes": h2d, "hbm_bytes": hbm, "flops": flops,
+            "times": t, "fits": math.isfinite(t[bound])}

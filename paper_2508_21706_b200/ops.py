@@ -1,0 +1,201 @@
+"""Torch-tensor front end over the C-ABI kernels (K1-K6 and support ops).
+
+Every function here launches sm_100a kernels from libspecmoe.so on the current
+torch CUDA stream; tensors must be CUDA tensors. There is no CPU path: on a
+machine without the library or a GPU these raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import torch
+
+from . import _lib as L
+
+_BF16 = torch.bfloat16
+
+
+def _p(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _req(t: torch.Tensor, dtype, name: str):
+    if not t.is_cuda:
+        raise ValueError(f"{name}: expected a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValueError(f"{name}: expected {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: expected a contiguous tensor")
+
+
+def fill_uniform_(t: torch.Tensor, seed: int, tensor_id: int, scale: float, base: int = 0) -> torch.Tensor:
+    """Procedural bf16 init, identical to the oracle's."""
+    _req(t, _BF16, "fill_uniform_")
+    L.check(L.load().smo_fill_uniform_bf16(_p(t), t.numel(), seed, tensor_id, base, scale, _stream()))
+    return t
+
+
+def verify_attention(q, k_cache, v_cache, mask, prefix_len, max_prefix: int, out=None):
+    """K1. q [b*n, n_q, d] bf16; caches [b, n_kv, s_max, d] bf16; mask int64 [b*n]
+    (bit j = draft j visible); prefix_len int32 [b]. Returns out [b*n, n_q, d]."""
+    b, n_kv, s_max, d = k_cache.shape
+    T, n_q, d2 = q.shape
+    if d2 != d or T % b:
+        raise ValueError("attention: shape mismatch")
+    n = T // b
+    for t, nm in ((q, "q"), (k_cache, "k_cache"), (v_cache, "v_cache")):
+        _req(t, _BF16, nm)
+    _req(mask, torch.int64, "mask")
+    _req(prefix_len, torch.int32, "prefix_len")
+    out = torch.empty_like(q) if out is None else out
+    a = L.AttnArgs(q=q.data_ptr(), k_cache=k_cache.data_ptr(), v_cache=v_cache.data_ptr(), mask=mask.data_ptr(),
+                   prefix_len=prefix_len.data_ptr(), out=out.data_ptr(), b=b, n=n, n_q=n_q, n_kv=n_kv, d=d,
+                   s_max=s_max, max_prefix=int(max_prefix), workspace=None, workspace_bytes=0)
+    lib = L.load()
+    ws_bytes = lib.smo_verify_attention_workspace(C.byref(a))
+    if ws_bytes == C.c_size_t(-1).value:
+        L.check(L.SMO_INVALID_ARG)
+    ws = torch.empty(max(16, ws_bytes), dtype=torch.uint8, device=q.device) if ws_bytes else None
+    if ws is not None:
+        a.workspace = ws.data_ptr()
+        a.workspace_bytes = ws_bytes
+    L.check(lib.smo_verify_attention(C.byref(a), _stream()))
+    return out
+
+
+def router_topk(x, w_router, k: int, want_logits: bool = False):
+    """K2. x [T, h] bf16, w_router [E, h] bf16 -> ids int32 [T,k], weights f32 [T,k] (, logits)."""
+    _req(x, _BF16, "x")
+    _req(w_router, _BF16, "w_router")
+    T, h = x.shape
+    E = w_router.shape[0]
+    ids = torch.empty((T, k), dtype=torch.int32, device=x.device)
+    wts = torch.empty((T, k), dtype=torch.float32, device=x.device)
+    logits = torch.empty((T, E), dtype=torch.float32, device=x.device) if want_logits else None
+    L.check(L.load().smo_router_topk(_p(x), _p(w_router), T, h, E, k, _p(logits), _p(ids), _p(wts), _stream()))
+    return (ids, wts, logits) if want_logits else (ids, wts)
+
+
+def permute(ids, n_expert: int, x=None):
+    """K3. ids [T,k] int32 -> offsets [E+1], perm [T*k], pos [T*k] (, x_perm [T*k, h])."""
+    _req(ids, torch.int32, "ids")
+    T, k = ids.shape
+    dev = ids.device
+    offsets = torch.empty(n_expert + 1, dtype=torch.int32, device=dev)
+    perm = torch.empty(T * k, dtype=torch.int32, device=dev)
+    pos = torch.empty(T * k, dtype=torch.int32, device=dev)
+    xp = None
+    h = 0
+    if x is not None:
+        _req(x, _BF16, "x")
+        h = x.shape[1]
+        xp = torch.empty((T * k, h), dtype=_BF16, device=dev)
+    L.check(L.load().smo_permute(_p(ids), T, k, n_expert, _p(x), h, _p(offsets), _p(perm), _p(pos), _p(xp),
+                                 _stream()))
+    return offsets, perm, pos, xp
+
+
+def unpermute_combine_(residual, y_perm, pos, weights):
+    """K3 combine: residual[t] += sum_j weights[t,j] * y_perm[pos[t*k+j]] (in place)."""
+    _req(residual, torch.float32, "residual")
+    _req(y_perm, torch.float32, "y_perm")
+    T, h = residual.shape
+    k = weights.shape[1]
+    L.check(L.load().smo_unpermute_combine(_p(y_perm), _p(pos), _p(weights), T, k, h, _p(residual), _stream()))
+    return residual
+
+
+def gemm(x, w, *, epilogue=L.EPI_BF16, out=None, w_up=None, row_offsets=None, w_index=None,
+         groups: int = 1, w_block_stride: int = 0, w_pool_blocks: int = 1, N: Optional[int] = None,
+         max_rows_per_group: Optional[int] = None):
+    """K4 (tcgen05). out[t, n] = x[t] . W_g[n] for the rows of group g.
+    Dense: w [N, K]. Grouped: w is a pool base pointer tensor and N must be given."""
+    _req(x, _BF16, "x")
+    rows, K = x.shape
+    if N is None:
+        N = w.shape[0]
+    dev = x.device
+    amax_v = amax_i = None
+    if epilogue == L.EPI_ARGMAX:
+        amax_v = torch.empty((rows, N // 128), dtype=torch.float32, device=dev)
+        amax_i = torch.empty((rows, N // 128), dtype=torch.int32, device=dev)
+    elif out is None:
+        dt = _BF16 if epilogue in (L.EPI_BF16, L.EPI_SWIGLU) else torch.float32
+        out = torch.zeros((rows, N), dtype=dt, device=dev)
+    a = L.GemmArgs(x=x.data_ptr(), rows=rows, K=K, N=N, groups=groups,
+                   row_offsets=None if row_offsets is None else row_offsets.data_ptr(),
+                   max_rows_per_group=max_rows_per_group or rows, w=w.data_ptr(),
+                   w_up=None if w_up is None else w_up.data_ptr(), w_block_stride=w_block_stride,
+                   w_pool_blocks=w_pool_blocks, w_index=None if w_index is None else w_index.data_ptr(),
+                   epilogue=epilogue, out=None if out is None else out.data_ptr(),
+                   ldo=0 if out is None else out.shape[-1],
+                   argmax_val=None if amax_v is None else amax_v.data_ptr(),
+                   argmax_idx=None if amax_i is None else amax_i.data_ptr(), split_k=1)
+    L.check(L.load().smo_gemm(C.byref(a), _stream()))
+    if epilogue == L.EPI_ARGMAX:
+        return amax_v, amax_i
+    return out
+
+
+def rmsnorm(x, gain, eps: float):
+    _req(x, torch.float32, "x")
+    y = torch.empty(x.shape, dtype=_BF16, device=x.device)
+    L.check(L.load().smo_rmsnorm(_p(x), _p(gain), x.shape[0], x.shape[1], eps, _p(y), _stream()))
+    return y
+
+
+def embed(tokens, table):
+    _req(tokens, torch.int32, "tokens")
+    x = torch.empty((tokens.numel(), table.shape[1]), dtype=torch.float32, device=tokens.device)
+    L.check(L.load().smo_embed(_p(tokens), _p(table), tokens.numel(), table.shape[1], _p(x), _stream()))
+    return x
+
+
+def rope_append(qkv, prefix_len, parent, b, n, n_q, n_kv, d, k_cache, v_cache, theta):
+    q = torch.empty((b * n, n_q, d), dtype=_BF16, device=qkv.device)
+    L.check(L.load().smo_rope_append(_p(qkv), _p(prefix_len), _p(parent), b, n, n_q, n_kv, d, k_cache.shape[2],
+                                     theta, _p(q), _p(k_cache), _p(v_cache), _stream()))
+    return q
+
+
+def argmax_reduce(val, idx):
+    rows, parts = val.shape
+    t = torch.empty(rows, dtype=torch.int32, device=val.device)
+    L.check(L.load().smo_argmax_reduce(_p(val), _p(idx), rows, parts, _p(t), _stream()))
+    return t
+
+
+def argmax_rows(logits):
+    _req(logits, torch.float32, "logits")
+    rows, V = logits.shape
+    t = torch.empty(rows, dtype=torch.int32, device=logits.device)
+    L.check(L.load().smo_argmax_rows(_p(logits), rows, V, _p(t), _stream()))
+    return t
+
+
+def greedy_accept(tokens, target, b: int, n: int, parent=None):
+    """K6. tokens/target int32 [b*n] -> acc_len [b], bonus [b], keep [b*n]."""
+    dev = tokens.device
+    acc = torch.empty(b, dtype=torch.int32, device=dev)
+    bonus = torch.empty(b, dtype=torch.int32, device=dev)
+    keep = torch.empty(b * n, dtype=torch.int32, device=dev)
+    L.check(L.load().smo_greedy_accept(_p(tokens), _p(target), _p(parent), b, n, _p(acc), _p(bonus), _p(keep),
+                                       _stream()))
+    return acc, bonus, keep
+
+
+def kv_rollback(k_caches, v_caches, prefix_len, acc_len, keep, b, n):
+    """Tree KV compaction over all layers; returns kv_len [b] = prefix + acc + 1."""
+    dev = prefix_len.device
+    n_kv, s_max, d = k_caches[0].shape[1:]
+    kp = torch.tensor([t.data_ptr() for t in k_caches], dtype=torch.int64, device=dev)
+    vp = torch.tensor([t.data_ptr() for t in v_caches], dtype=torch.int64, device=dev)
+    kv_len = torch.empty(b, dtype=torch.int32, device=dev)
+    L.check(L.load().smo_kv_rollback(_p(kp), _p(vp), len(k_caches), _p(prefix_len), _p(acc_len), _p(keep), b, n,
+                                     n_kv, d, s_max, _p(kv_len), _stream()))
+    return kv_len

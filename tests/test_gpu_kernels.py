@@ -1,0 +1,325 @@
+"""GPU parity of each kernel (K1-K6) against the CPU oracle / fp32 torch
+reference on identical inputs. Integer outputs are bit-exact; floating point
+within the tolerances written in each test."""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _bf16_rand(torch, shape, gen, scale=1.0, device="cuda"):
+    return (torch.rand(shape, generator=gen, device=device) * 2 - 1).mul_(scale).to(torch.bfloat16)
+
+
+def _u16(t):
+    import torch
+    return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+# ---------------------------------------------------------------- K4 GEMM
+@pytest.mark.parametrize("T,K,N", [(1, 512, 128), (20, 512, 768), (160, 4096, 1024), (288, 4096, 768),
+                                   (300, 1024, 256), (520, 512, 384), (37, 14336, 256)])
+def test_gemm_dense_f32_vs_torch(cuda, T, K, N):
+    import torch
+    from paper_2508_21706_b200 import ops, _lib as L
+    g = torch.Generator(device=cuda).manual_seed(T * 7 + K + N)
+    x = _bf16_rand(torch, (T, K), g)
+    w = _bf16_rand(torch, (N, K), g, scale=math.sqrt(3.0 / K))
+    out = ops.gemm(x, w, epilogue=L.EPI_F32)
+    ref = x.float() @ w.float().T
+    err = (out - ref).abs().max().item()
+    assert err <= 1e-4 * max(1.0, ref.abs().max().item()), err
+    out_bf = ops.gemm(x, w, epilogue=L.EPI_BF16)
+    assert torch.equal(out_bf, ref.to(torch.bfloat16)) or \
+        (out_bf.float() - ref).abs().max().item() <= 2 ** -7 * ref.abs().max().item()
+    acc = torch.ones((T, N), dtype=torch.float32, device=cuda)
+    ops.gemm(x, w, epilogue=L.EPI_F32_ADD, out=acc)
+    assert (acc - 1.0 - ref).abs().max().item() <= 1e-4 * max(1.0, ref.abs().max().item())
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("T,V", [(20, 32000), (288, 32000), (5, 1024)])
+def test_gemm_argmax_epilogue(cuda, T, V):
+    import torch
+    from paper_2508_21706_b200 import ops, _lib as L
+    g = torch.Generator(device=cuda).manual_seed(V + T)
+    K = 512
+    x = _bf16_rand(torch, (T, K), g)
+    w = _bf16_rand(torch, (V, K), g, scale=math.sqrt(3.0 / K))
+    val, idx = ops.gemm(x, w, epilogue=L.EPI_ARGMAX)
+    tgt = ops.argmax_reduce(val, idx)
+    logits = ops.gemm(x, w, epilogue=L.EPI_F32)
+    ref = torch.argmax(logits, dim=1).to(torch.int32)  # first max on ties
+    assert torch.equal(tgt, ref)
+    assert torch.equal(ops.argmax_rows(logits), ref)
+
+
+@pytest.mark.parametrize("T,E,k,h,hi", [(20, 8, 2, 512, 1792), (160, 8, 2, 1024, 512), (48, 64, 6, 512, 384)])
+def test_grouped_swiglu_and_down_vs_torch(cuda, T, E, k, h, hi):
+    import torch
+    from paper_2508_21706_b200 import ops, _lib as L
+    g = torch.Generator(device=cuda).manual_seed(E * 100 + T)
+    x = _bf16_rand(torch, (T, h), g)
+    # pool of E expert blocks [W1 | W3 | W2]
+    blk = 3 * h * hi
+    pool = _bf16_rand(torch, (E * blk,), g, scale=math.sqrt(3.0 / h))
+    logits = torch.randn((T, E), generator=g, device=cuda)
+    ids = torch.topk(logits, k, dim=1).indices.to(torch.int32).contiguous()
+    off, perm, pos, xp = ops.permute(ids, E, x)
+    hbuf = ops.gemm(xp, pool, epilogue=L.EPI_SWIGLU, w_up=pool[hi * h:], row_offsets=off, groups=E,
+                    w_block_stride=blk * 2, w_pool_blocks=E, N=hi, max_rows_per_group=T)
+    y = ops.gemm(hbuf, pool[2 * hi * h:], epilogue=L.EPI_F32, row_offsets=off, groups=E, w_block_stride=blk * 2,
+                 w_pool_blocks=E, N=h, max_rows_per_group=T)
+    offs = off.cpu().tolist()
+    for e in range(E):
+        a, b = offs[e], offs[e + 1]
+        if a == b:
+            continue
+        base = e * blk
+        w1 = pool[base:base + hi * h].view(hi, h).float()
+        w3 = pool[base + hi * h:base + 2 * hi * h].view(hi, h).float()
+        w2 = pool[base + 2 * hi * h:base + blk].view(h, hi).float()
+        X = xp[a:b].float()
+        gg, uu = X @ w1.T, X @ w3.T
+        H = (gg * torch.sigmoid(gg) * uu).to(torch.bfloat16)
+        dh = (hbuf[a:b].float() - H.float()).abs().max().item()
+        assert dh <= 2 ** -7 * max(1.0, H.float().abs().max().item()), (e, dh)
+        Y = hbuf[a:b].float() @ w2.T
+        dy = (y[a:b] - Y).abs().max().item()
+        assert dy <= 1e-4 * max(1.0, Y.abs().max().item()), (e, dy)
+
+
+# ---------------------------------------------------------------- K2 / K3
+@pytest.mark.parametrize("T,h,E,k", [(20, 512, 8, 2), (288, 4096, 8, 2), (64, 2048, 64, 6)])
+def test_router_bit_exact_vs_oracle(cuda, oracle, T, h, E, k):
+    import torch
+    from paper_2508_21706_b200 import ops
+    g = torch.Generator(device=cuda).manual_seed(T + h + E)
+    x = _bf16_rand(torch, (T, h), g)
+    w = _bf16_rand(torch, (E, h), g, scale=math.sqrt(3.0 / h))
+    ids, wts, lg = ops.router_topk(x, w, k, want_logits=True)
+    xn, wn = _u16(x), _u16(w)
+    ref_lg = np.zeros((T, E), np.float32)
+    oracle.lib().orc_router_logits(oracle._ptr(xn), oracle._ptr(wn), T, h, E, oracle._ptr(ref_lg))
+    assert np.array_equal(lg.cpu().numpy().view(np.uint32), ref_lg.view(np.uint32)), "router logits not bit-exact"
+    rid = np.zeros((T, k), np.int32)
+    rw = np.zeros((T, k), np.float32)
+    oracle.lib().orc_topk_softmax(oracle._ptr(ref_lg), T, E, k, oracle._ptr(rid), oracle._ptr(rw))
+    assert np.array_equal(ids.cpu().numpy(), rid)
+    assert np.allclose(wts.cpu().numpy(), rw, rtol=1e-5, atol=1e-6)
+    # permutation bit-exact
+    off, perm, pos, xp = ops.permute(ids, E, x)
+    o_off = np.zeros(E + 1, np.int32)
+    o_perm = np.zeros(T * k, np.int32)
+    o_pos = np.zeros(T * k, np.int32)
+    oracle.lib().orc_permute(oracle._ptr(rid), T, k, E, oracle._ptr(o_off), oracle._ptr(o_perm), oracle._ptr(o_pos))
+    assert np.array_equal(off.cpu().numpy(), o_off)
+    assert np.array_equal(perm.cpu().numpy(), o_perm)
+    assert np.array_equal(pos.cpu().numpy(), o_pos)
+    assert torch.equal(xp, x[perm.long() // k])
+
+
+def test_router_ties_go_to_lower_expert(cuda):
+    import torch
+    from paper_2508_21706_b200 import ops
+    x = torch.zeros((3, 256), dtype=torch.bfloat16, device=cuda)
+    w = torch.zeros((8, 256), dtype=torch.bfloat16, device=cuda)
+    ids, wts = ops.router_topk(x, w, 2)
+    assert ids.cpu().tolist() == [[0, 1]] * 3
+    assert torch.allclose(wts, torch.full_like(wts, 0.5))
+
+
+def test_combine_fixed_order(cuda):
+    import torch
+    from paper_2508_21706_b200 import ops
+    g = torch.Generator(device=cuda).manual_seed(3)
+    T, k, h = 33, 2, 512
+    y = torch.randn((T * k, h), generator=g, device=cuda)
+    pos = torch.randperm(T * k, generator=g, device=cuda).to(torch.int32)
+    w = torch.rand((T, k), generator=g, device=cuda)
+    res = torch.randn((T, h), generator=g, device=cuda)
+    ref = res + (w[:, :, None] * y[pos.long()].view(T, k, h)).sum(1)
+    ops.unpermute_combine_(res, y, pos, w)
+    assert torch.allclose(res, ref, rtol=1e-6, atol=1e-5)
+
+
+# ---------------------------------------------------------------- K1 attention
+def _attn_case(torch, cuda, b, n, nq, nkv, d, prefix, s_max, tree, seed):
+    g = torch.Generator(device=cuda).manual_seed(seed)
+    q = _bf16_rand(torch, (b * n, nq, d), g)
+    kc = _bf16_rand(torch, (b, nkv, s_max, d), g)
+    vc = _bf16_rand(torch, (b, nkv, s_max, d), g)
+    rng = np.random.default_rng(seed)
+    bits = np.zeros(b * n, np.uint64)
+    for r in range(b):
+        if tree:
+            par = [-1] + [int(rng.integers(0, i)) for i in range(1, n)]
+        for i in range(n):
+            if tree:
+                m, cur = 0, i
+                while cur >= 0:
+                    m |= 1 << cur
+                    cur = -1 if cur == 0 else par[cur]
+            else:
+                m = (1 << (i + 1)) - 1
+            bits[r * n + i] = m
+    mask = torch.from_numpy(bits.view(np.int64)).to(cuda)
+    pre = torch.tensor(prefix, dtype=torch.int32, device=cuda)
+    return q, kc, vc, mask, pre, bits
+
+
+@pytest.mark.parametrize("b,n,nq,nkv,d,prefix,tree", [
+    (4, 5, 8, 2, 64, [1024, 1000, 3, 0], False),       # tiny config (+ edge prefixes)
+    (2, 5, 32, 8, 128, [1024, 131], False),            # Mixtral heads
+    (2, 9, 32, 8, 128, [1024, 700], True),             # k=8 tree
+    (1, 16, 32, 8, 128, [5000], True),                 # 64 rows, split-KV
+    (3, 1, 32, 8, 128, [127, 128, 129], False),        # plain decode, chunk edges
+])
+def test_verify_attention_vs_oracle(cuda, oracle, b, n, nq, nkv, d, prefix, tree):
+    import torch
+    from paper_2508_21706_b200 import ops
+    s_max = max(prefix) + n + 64
+    q, kc, vc, mask, pre, bits = _attn_case(torch, cuda, b, n, nq, nkv, d, prefix, s_max, tree, seed=b * 31 + n)
+    out = ops.verify_attention(q, kc, vc, mask, pre, max(prefix))
+    ref = np.zeros((b * n, nq, d), np.uint16)
+    rc = oracle.lib().orc_verify_attention(oracle._ptr(_u16(q)), oracle._ptr(_u16(kc)), oracle._ptr(_u16(vc)),
+                                           oracle._ptr(bits), oracle._ptr(np.array(prefix, np.int32)), b, n, nq,
+                                           nkv, d, s_max, oracle._ptr(ref))
+    assert rc == 0
+    got = out.float().cpu().numpy()
+    exp = oracle.bf16_to_f32(ref).reshape(got.shape)
+    vmax = float(vc.float().abs().max())
+    # tolerance: max abs <= 2^-8 * max|V| (+ bf16 P rounding), rel-RMS <= 5e-3
+    assert np.max(np.abs(got - exp)) <= 2 ** -7 * vmax
+    rel_rms = np.sqrt(np.mean((got - exp) ** 2) / max(1e-30, np.mean(exp ** 2)))
+    assert rel_rms <= 5e-3, rel_rms
+
+
+def test_verify_attention_causality_exact(cuda):
+    """test_attention.cpp:111-132 on the GPU kernel: perturbing a blocked
+    draft's K/V leaves the rows that cannot see it bit-identical."""
+    import torch
+    from paper_2508_21706_b200 import ops
+    b, n, nq, nkv, d = 2, 5, 32, 8, 128
+    prefix = [300, 17]
+    s_max = 400
+    q, kc, vc, mask, pre, _ = _attn_case(torch, cuda, b, n, nq, nkv, d, prefix, s_max, False, 11)
+    base = ops.verify_attention(q, kc, vc, mask, pre, max(prefix))
+    kc2, vc2 = kc.clone(), vc.clone()
+    for r in range(b):
+        kc2[r, :, prefix[r] + 3] += 8.0
+        vc2[r, :, prefix[r] + 3] -= 4.0
+    out = ops.verify_attention(q, kc2, vc2, mask, pre, max(prefix))
+    rows = out.view(b, n, nq, d)
+    ref = base.view(b, n, nq, d)
+    assert torch.equal(rows[:, :3], ref[:, :3])
+    assert not torch.equal(rows[:, 3], ref[:, 3])
+
+
+def test_verify_attention_uniform_and_identity(cuda):
+    """Q = 0 gives the mean of visible V rows (test_attention.cpp:59-74);
+    n=1, p=0 returns the V row (:40-57)."""
+    import torch
+    from paper_2508_21706_b200 import ops
+    b, n, nq, nkv, d, p = 1, 1, 8, 2, 64, 7
+    q = torch.zeros((1, nq, d), dtype=torch.bfloat16, device=cuda)
+    kc = torch.randn((b, nkv, 64, d), device=cuda).to(torch.bfloat16)
+    vc = torch.randn((b, nkv, 64, d), device=cuda).to(torch.bfloat16)
+    mask = torch.ones(1, dtype=torch.int64, device=cuda)
+    out = ops.verify_attention(q, kc, vc, mask, torch.tensor([p], dtype=torch.int32, device=cuda), p)
+    mean = vc[0, :, :p + 1].float().mean(1)  # [nkv, d]
+    exp = mean.repeat_interleave(nq // nkv, 0)
+    assert torch.allclose(out[0].float(), exp, atol=2e-2)
+    out0 = ops.verify_attention(q + 1, kc, vc, mask, torch.tensor([0], dtype=torch.int32, device=cuda), 0)
+    assert torch.equal(out0[0], vc[0, :, 0].repeat_interleave(nq // nkv, 0))
+
+
+# ---------------------------------------------------------------- reference fp64 API
+def test_chunked_attention_f64_matches_reference_golden(cuda, oracle):
+    """moeplan::chunked_attention contract on the GPU fp64 kernel: the
+    reference's `verify-attention --random 42 50` outputs (golden), < 1e-6."""
+    import json
+    import os
+    from paper_2508_21706_b200 import attention as A
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_vectors.json")))
+    g = gold["random_cases"]["42"]
+    cases = oracle.random_cases(42, 50)
+    total = 0.0
+    for c, ref in zip(cases, g["out"]):
+        inst = A.AttentionInstance(c["n"], c["p"], c["d"], A.Matrix(c["n"], c["d"], c["Q"]),
+                                   A.Matrix(c["p"] + c["n"], c["d"], c["K"]), A.Matrix(c["p"] + c["n"], c["d"], c["V"]))
+        out = A.chunked_attention(inst, A.CompactMask(c["n"], c["mask"].astype(bool))).data
+        ref = np.array(ref)
+        assert np.max(np.abs(out - ref) / np.maximum(1e-12, np.abs(ref))) < 1e-6
+        total += out.sum()
+    assert total == pytest.approx(g["sum"], rel=1e-12)
+
+
+def test_chunked_attention_f64_errors(cuda):
+    from paper_2508_21706_b200 import attention as A
+    inst = A.AttentionInstance(2, 0, 3, A.Matrix(2, 3, np.ones((2, 3))), A.Matrix(2, 3, np.ones((2, 3))),
+                               A.Matrix(2, 3, np.ones((2, 3))))
+    with pytest.raises(ValueError, match="fully blocked"):
+        A.chunked_attention(inst, A.CompactMask(2))
+    with pytest.raises(ValueError, match="mask size mismatch"):
+        A.chunked_attention(inst, A.CompactMask.chain(3))
+    bad = A.AttentionInstance(2, 0, 3, A.Matrix(2, 3, np.ones((2, 3))), A.Matrix(3, 3), A.Matrix(2, 3))
+    with pytest.raises(ValueError, match="shape mismatch"):
+        A.chunked_attention(bad, A.CompactMask.chain(2))
+    nanq = np.ones((2, 3))
+    nanq[0, 0] = np.nan
+    inst.Q = A.Matrix(2, 3, nanq)
+    with pytest.raises(ValueError, match="non-finite Q"):
+        A.chunked_attention(inst, A.CompactMask.chain(2))
+
+
+# ---------------------------------------------------------------- K6
+def test_greedy_accept_vs_oracle(cuda, oracle):
+    import torch
+    from paper_2508_21706_b200 import ops
+    rng = np.random.default_rng(5)
+    for tree in (False, True):
+        b, n = 37, 9
+        tokens = rng.integers(0, 4, size=(b, n)).astype(np.int32)
+        target = rng.integers(0, 4, size=(b, n)).astype(np.int32)
+        parent = None
+        if tree:
+            parent = np.array([[-1] + [int(rng.integers(0, i)) for i in range(1, n)] for _ in range(b)], np.int32)
+        acc, bonus, keep = ops.greedy_accept(torch.from_numpy(tokens).to(cuda), torch.from_numpy(target).to(cuda),
+                                             b, n, None if parent is None else torch.from_numpy(parent).to(cuda))
+        oa, ob, ok = np.zeros(b, np.int32), np.zeros(b, np.int32), np.zeros(b * n, np.int32)
+        oracle.lib().orc_greedy_accept(oracle._ptr(tokens), oracle._ptr(target),
+                                       None if parent is None else oracle._ptr(parent), b, n, oracle._ptr(oa),
+                                       oracle._ptr(ob), oracle._ptr(ok))
+        assert np.array_equal(acc.cpu().numpy(), oa)
+        assert np.array_equal(bonus.cpu().numpy(), ob)
+        assert np.array_equal(keep.cpu().numpy(), ok)
+
+
+def test_kv_rollback_tree(cuda):
+    import torch
+    from paper_2508_21706_b200 import ops
+    b, n, nkv, d, s_max = 2, 5, 2, 64, 32
+    kc = [torch.randn((b, nkv, s_max, d), device=cuda).to(torch.bfloat16) for _ in range(2)]
+    vc = [torch.randn((b, nkv, s_max, d), device=cuda).to(torch.bfloat16) for _ in range(2)]
+    ref_k = [t.clone() for t in kc]
+    prefix = torch.tensor([3, 10], dtype=torch.int32, device=cuda)
+    acc = torch.tensor([2, 0], dtype=torch.int32, device=cuda)
+    keep = torch.tensor([0, 2, 4, -1, -1, 0, -1, -1, -1, -1], dtype=torch.int32, device=cuda)
+    kv_len = ops.kv_rollback(kc, vc, prefix, acc, keep, b, n)
+    assert kv_len.cpu().tolist() == [6, 11]
+    for L in range(2):
+        assert torch.equal(kc[L][0, :, 4], ref_k[L][0, :, 5])
+        assert torch.equal(kc[L][0, :, 5], ref_k[L][0, :, 7])
+        assert torch.equal(kc[L][1], ref_k[L][1])
+
+
+def test_fill_uniform_matches_oracle(cuda, oracle):
+    import torch
+    from paper_2508_21706_b200 import ops
+    t = torch.empty(100003, dtype=torch.bfloat16, device=cuda)
+    ops.fill_uniform_(t, 0x5EED, 4321, 0.03125, base=17)
+    ref = oracle.fill_uniform_bf16(t.numel(), 0x5EED, 4321, 0.03125, base=17)
+    assert np.array_equal(_u16(t), ref)
