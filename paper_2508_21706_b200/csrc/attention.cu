@@ -48,11 +48,14 @@ struct AttnSmem {
   static constexpr int kKBlocks = D / 64;
   static constexpr int kQBytes = kKBlocks * 16384;      // 128 rows x D
   static constexpr int kKvBytes = kKBlocks * 16384;     // 128 keys x D (K or V)
-  static constexpr int kPBytes = 2 * 16384;             // 128 rows x 128 keys
+  static constexpr int kPBytes = 2 * 16384;             // 128 rows x 128 keys (bf16)
+  // d=128 keeps one Q buffer so that P can be held as hi+lo bf16 planes
+  static constexpr int kQBufs = D == 128 ? 1 : 2;
   static constexpr int kQOff = 0;
-  static constexpr int kKvOff = 2 * kQBytes;
+  static constexpr int kKvOff = kQBufs * kQBytes;
   static constexpr int kPOff = kKvOff + kKvStages * 2 * kKvBytes;
-  static constexpr int kTotal = kPOff + kPBytes;
+  static constexpr int kPLoOff = kPOff + kPBytes;
+  static constexpr int kTotal = kPLoOff + kPBytes;
 };
 
 struct ItemInfo {
@@ -117,8 +120,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
         const ItemInfo it = item_info(p, item);
         if (it.c_end <= it.c_begin) continue;
-        const int qb = used & 1;
-        mbar_wait(&q_empty[qb], ((used >> 1) & 1) ^ 1);
+        const int qb = used % L::kQBufs;
+        mbar_wait(&q_empty[qb], ((used / L::kQBufs) & 1) ^ 1);
         ++used;
         const uint32_t qbytes = uint32_t(L::kKBlocks * 64 * p.g * p.n * 2);
         mbar_arrive_expect_tx(&q_full[qb], qbytes);
@@ -149,8 +152,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
         const ItemInfo it = item_info(p, item);
         if (it.c_end <= it.c_begin) continue;
-        const int qb = used & 1;
-        mbar_wait(&q_full[qb], (used >> 1) & 1);
+        const int qb = used % L::kQBufs;
+        mbar_wait(&q_full[qb], (used / L::kQBufs) & 1);
         ++used;
         const uint32_t q_addr = smem_u32(smem + L::kQOff + qb * L::kQBytes);
         const int nch = it.c_end - it.c_begin;
@@ -180,12 +183,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&o_empty[ob], ((g2 >> 1) & 1) ^ 1);
           tc_fence_after();
           const uint32_t p_addr = smem_u32(smem + L::kPOff);
+          const uint32_t plo_addr = smem_u32(smem + L::kPLoOff);
           const uint32_t v_addr = smem_u32(smem + L::kKvOff + s * 2 * L::kKvBytes + L::kKvBytes);
+          // O = P_hi V + P_lo V: P carried to ~16 mantissa bits
 #pragma unroll
           for (int kk = 0; kk < kChunk / 16; ++kk) {
             const uint32_t aoff = (kk / 4) * 16384 + (kk % 4) * 32;
-            umma_bf16(tmem + 256 + ob * 128, make_sdesc_sw128(p_addr + aoff, 16, 1024),
-                      make_sdesc_sw128(v_addr + kk * 2048, 16384, 1024), id_o, kk > 0 ? 1u : 0u);
+            const uint64_t vd = make_sdesc_sw128(v_addr + kk * 2048, 16384, 1024);
+            umma_bf16(tmem + 256 + ob * 128, make_sdesc_sw128(p_addr + aoff, 16, 1024), vd, id_o, kk > 0 ? 1u : 0u);
+            umma_bf16(tmem + 256 + ob * 128, make_sdesc_sw128(plo_addr + aoff, 16, 1024), vd, id_o, 1u);
           }
           umma_commit(&o_full[ob]);
           umma_commit(&kv_empty[s]);
@@ -261,25 +267,31 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t r[32];
           tmem_ld32(tmem + tlane + sb * 128 + c0, r);
           tmem_ld_wait();
-          uint32_t pk[16];
+          uint32_t pk[16], pl[16];
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
             float pv[2];
+            uint16_t hi[2], lo[2];
 #pragma unroll
             for (int t = 0; t < 2; ++t) {
               const int key = key0 + c0 + j + t;
               const bool vis = live && (key < prefix || (key < it.keys && ((mbits >> (key - prefix)) & 1ull)));
               pv[t] = vis ? exp2f(__uint_as_float(r[j + t]) * p.scale_log2 - m_use) : 0.f;
               psum += pv[t];
+              hi[t] = f2bf(pv[t]);
+              lo[t] = f2bf(pv[t] - bf2f(hi[t]));
             }
-            pk[j / 2] = uint32_t(f2bf(pv[0])) | (uint32_t(f2bf(pv[1])) << 16);
+            pk[j / 2] = uint32_t(hi[0]) | (uint32_t(hi[1]) << 16);
+            pl[j / 2] = uint32_t(lo[0]) | (uint32_t(lo[1]) << 16);
           }
           const int kb = c0 / 64;
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
             const int lc = ((c0 % 64) / 8) + t;
-            uint4 v = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
-            *reinterpret_cast<uint4*>(pbuf + kb * 16384 + row * 128 + ((lc ^ (row & 7)) * 16)) = v;
+            const int off = kb * 16384 + row * 128 + ((lc ^ (row & 7)) * 16);
+            *reinterpret_cast<uint4*>(pbuf + off) = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+            *reinterpret_cast<uint4*>(pbuf + (L::kPLoOff - L::kPOff) + off) =
+                make_uint4(pl[4 * t], pl[4 * t + 1], pl[4 * t + 2], pl[4 * t + 3]);
           }
         }
         tc_fence_before();

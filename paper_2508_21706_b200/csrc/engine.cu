@@ -663,6 +663,17 @@ smo_status smo_engine_debug_tensor(smo_engine* e, const char* name, int32_t laye
   return smo::run_guarded([&] {
     SMO_REQUIRE(e && name && dst, "engine: null argument");
     SMO_REQUIRE(e->impl.debug, "engine: created without SMO_ENGINE_DEBUG");
+    const std::string nm(name);
+    if (nm == "k_cache" || nm == "v_cache") {  // live cache contents of a layer
+      smo::Engine& g = e->impl;
+      SMO_REQUIRE(layer >= 0 && layer < g.L, "engine: layer out of range");
+      const size_t cb = size_t(g.maxB) * g.nkv * g.s_max * g.d * 2;
+      SMO_REQUIRE(bytes <= cb, "engine: debug tensor smaller than requested");
+      SMO_CUDA_CHECK(cudaDeviceSynchronize());
+      SMO_CUDA_CHECK(cudaMemcpy(dst, nm == "k_cache" ? g.layers[layer].kc : g.layers[layer].vc, bytes,
+                                cudaMemcpyDeviceToHost));
+      return;
+    }
     auto it = e->impl.dbg.find(name);
     SMO_REQUIRE(it != e->impl.dbg.end(), std::string("engine: unknown debug tensor ") + name);
     const size_t idx = size_t(layer + 1);
