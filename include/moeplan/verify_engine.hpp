@@ -1,0 +1,223 @@
+#pragma once
+// moeplan/verify_engine.hpp — the measured verify step behind the planner API.
+//
+// Additive engine API of SURVEY.md §8(b): a C++ VerifyEngine constructed from
+// the reference's own value types (HardwareSpec, ModelSpec, Hyperparameters,
+// MemoryPlan). verify() runs one speculative verification step on the B200
+// (libspecmoe.so: K1-K6 kernels + the K5 expert streamer) and returns the
+// reference's IterationResult with MEASURED durations: the target DAG of
+// pipeline.hpp:147-206 with one event per layer and stage, its measured
+// Schedule, and the Table-3 breakdown (report.hpp:27-37). profile() returns
+// ProfileSamples with the reference's driving variables (pipeline.hpp:256-264)
+// so fit_latency_models() -> optimize() -> DraftLengthController run on real
+// timings.
+//
+// Stage mapping: K1 attention -> CPU_ATTN (name kept),
+// norms/QKV/RoPE -> GPU_OTHER1, O-proj/router/permute -> GPU_OTHER2,
+// K4 experts + combine -> GPU_MOE, K5 copy-engine transfer -> H2D_EXPERTS.
+
+#include <cmath>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "moeplan/config.hpp"
+#include "moeplan/memory.hpp"
+#include "moeplan/optimizer.hpp"
+#include "moeplan/pipeline.hpp"
+#include "specmoe/c_api.h"
+
+namespace moeplan {
+
+struct EngineOptions {
+  std::int64_t max_seq = 0;            // KV capacity per request (0: workload total_len + k + 1)
+  int hbm_slots = 2;                   // expert staging slots
+  int host_alias_layers = 0;           // pinned host buffers shared by layers (0: one per layer)
+  int device = 0;
+  bool debug = false;
+  std::uint64_t seed = 0x5EED;         // procedural weights
+  float lm_scale = 1.0f;
+  float router_scale = 1.0f;
+};
+
+struct VerifyBatch {
+  std::int64_t b = 0;
+  std::int64_t n = 0;                  // verify rows per request = k + 1 (root + drafts)
+  std::vector<std::int32_t> tokens;    // b*n, row 0 of each request is the root
+  std::vector<std::int32_t> parent;    // empty: chain; else b*n tree parents (-1 root)
+  std::vector<std::int32_t> prefix_len;  // b
+};
+
+struct VerifyOutput {
+  std::vector<std::int32_t> acc_len;   // accepted drafts per request (committed = acc + 1)
+  std::vector<std::int32_t> bonus;     // greedy token at the accepted tip
+  std::vector<std::int32_t> keep;      // accepted rows, root first, -1 padded
+  std::vector<std::int32_t> target;    // argmax per verify row
+};
+
+namespace detail {
+inline void smo_check(smo_status st) {
+  if (st == SMO_OK) return;
+  if (st == SMO_INVALID_ARG) throw std::invalid_argument(smo_last_error());
+  if (st == SMO_CAPACITY) throw CapacityError(smo_last_error());
+  throw std::runtime_error(std::string("specmoe: ") + smo_last_error());
+}
+}  // namespace detail
+
+class VerifyEngine {
+ public:
+  VerifyEngine(const HardwareSpec& hw, const ModelSpec& model, const Hyperparameters& hyper, const MemoryPlan& plan,
+               const EngineOptions& opt = {})
+      : hw_(hw), model_(model), hyper_(hyper) {
+    if (!model.arch || model.arch->n_q_heads <= 0 || model.arch->head_dim <= 0 || model.arch->vocab <= 0)
+      throw std::invalid_argument("VerifyEngine: ModelSpec.arch (n_q_heads, head_dim, vocab) is required");
+    const ModelArch& a = *model.arch;
+    const std::int64_t kv_width = model.h / model.g;  // K (or V) width per token, config.hpp:54
+    if (kv_width % a.head_dim != 0) throw std::invalid_argument("VerifyEngine: h/g must be a multiple of head_dim");
+    smo_model_config c{};
+    c.hidden = std::int32_t(model.h);
+    c.inter = std::int32_t(model.h_i);
+    c.n_expert = std::int32_t(model.n_expert);
+    c.top_k = std::int32_t(model.n_activate);
+    c.n_layers = std::int32_t(model.n_layers);
+    c.n_q_heads = std::int32_t(a.n_q_heads);
+    c.n_kv_heads = std::int32_t(kv_width / a.head_dim);
+    c.head_dim = std::int32_t(a.head_dim);
+    c.vocab = std::int32_t(a.vocab);
+    c.rope_theta = float(a.rope_theta);
+    c.rms_eps = float(a.rms_eps);
+    c.seed = opt.seed;
+    c.lm_scale = opt.lm_scale;
+    c.router_scale = opt.router_scale;
+    smo_engine_options o{};
+    o.max_batch = std::int32_t(hyper.b);
+    o.max_verify = std::int32_t(std::max(1, hyper.k) + 1);
+    o.max_seq = std::int32_t(opt.max_seq > 0 ? opt.max_seq : 2048);
+    o.hbm_slots = opt.hbm_slots;
+    o.expert_cache_bytes = std::int64_t(plan.expert_cache_bytes);
+    o.host_alias_layers = opt.host_alias_layers;
+    o.device = opt.device;
+    o.flags = opt.debug ? SMO_ENGINE_DEBUG : 0;
+    o.ep_rank = 0;
+    o.ep_size = 1;
+    detail::smo_check(smo_engine_create(&c, &o, &h_));
+    layers_ = model.n_layers;
+  }
+  VerifyEngine(const VerifyEngine&) = delete;
+  VerifyEngine& operator=(const VerifyEngine&) = delete;
+  ~VerifyEngine() {
+    if (h_) smo_engine_destroy(h_);
+  }
+
+  void fill_prefix(const std::vector<std::int32_t>& prefix_len) {
+    detail::smo_check(smo_engine_fill_prefix(h_, prefix_len.data(), std::int32_t(prefix_len.size())));
+  }
+
+  // One verify step from host buffers; returns the measured IterationResult.
+  IterationResult verify(const VerifyBatch& in, VerifyOutput* out = nullptr) {
+    const std::size_t T = std::size_t(in.b * in.n);
+    if (in.tokens.size() != T || in.prefix_len.size() != std::size_t(in.b) ||
+        (!in.parent.empty() && in.parent.size() != T))
+      throw std::invalid_argument("VerifyEngine::verify: batch shape mismatch");
+    VerifyOutput local;
+    VerifyOutput& o = out ? *out : local;
+    o.acc_len.assign(std::size_t(in.b), 0);
+    o.bonus.assign(std::size_t(in.b), 0);
+    o.keep.assign(T, -1);
+    o.target.assign(T, 0);
+    smo_verify_batch vb{std::int32_t(in.b), std::int32_t(in.n), in.tokens.data(),
+                        in.parent.empty() ? nullptr : in.parent.data(), in.prefix_len.data(), 0};
+    smo_verify_output vo{o.acc_len.data(), o.bonus.data(), o.keep.data(), o.target.data(), 0};
+    detail::smo_check(smo_engine_verify(h_, &vb, &vo, nullptr));
+    return measured(in);
+  }
+
+  // Accumulated measured samples (one per stage kind and verify call).
+  const std::vector<ProfileSample>& profile() const { return samples_; }
+  void clear_profile() { samples_.clear(); }
+
+ private:
+  IterationResult measured(const VerifyBatch& in) {
+    smo_stage_times st{};
+    detail::smo_check(smo_engine_last_times(h_, &st));
+    std::vector<double> lt(std::size_t(layers_) * 9);
+    detail::smo_check(smo_engine_layer_times(h_, lt.data(), lt.size()));
+    IterationResult r;
+    EventDag& dag = r.target_dag;
+    Schedule& sc = r.target_schedule;
+    int prev_h2d = -1, prev_moe = -1;
+    auto add = [&](EventKind k, ExecResource res, double t0, double t1, std::vector<int> deps, std::string lbl) {
+      EventNode ev;
+      ev.id = int(dag.size());
+      ev.kind = k;
+      ev.resource = res;
+      ev.duration = std::max(0.0, t1 - t0);
+      ev.deps = std::move(deps);
+      ev.label = std::move(lbl);
+      dag.push_back(ev);
+      sc.start.push_back(t0);
+      sc.end.push_back(t0 + dag.back().duration);
+      sc.busy[std::size_t(res)] += dag.back().duration;
+      sc.makespan = std::max(sc.makespan, sc.end.back());
+      return ev.id;
+    };
+    double attn = 0, moe = 0, h2d = 0, o1 = 0, o2 = 0;
+    for (std::int64_t l = 0; l < layers_; ++l) {
+      const double* t = lt.data() + l * 9;  // h2d0 h2d1 attn0 attn1 moe0 moe1 layer0 premoe bytes
+      const std::string L = "L" + std::to_string(l);
+      std::vector<int> hd;
+      if (prev_h2d >= 0) hd.push_back(prev_h2d);
+      const int eh = add(EventKind::H2D_EXPERTS, ExecResource::H2D, t[0], t[1], hd, L + "/H2D_EXPERTS");
+      std::vector<int> od;
+      if (prev_moe >= 0) od.push_back(prev_moe);
+      const int e1 = add(EventKind::GPU_OTHER1, ExecResource::GPU, t[6], t[2], od, L + "/mb0/GPU_OTHER1");
+      const int ea = add(EventKind::CPU_ATTN, ExecResource::GPU, t[2], t[3], {e1}, L + "/mb0/CPU_ATTN");
+      const int e2 = add(EventKind::GPU_OTHER2, ExecResource::GPU, t[3], t[7], {ea}, L + "/mb0/GPU_OTHER2");
+      prev_moe = add(EventKind::GPU_MOE, ExecResource::GPU, t[4], t[5], {e2, eh}, L + "/mb0/GPU_MOE");
+      prev_h2d = eh;
+      h2d += t[1] - t[0];
+      attn += t[3] - t[2];
+      moe += t[5] - t[4];
+      o1 += t[2] - t[6];
+      o2 += t[7] - t[3];
+    }
+    IterationBreakdown& bd = r.breakdown;
+    bd.target_total = st.target_total;
+    bd.cpu_attention = attn;
+    bd.gpu_moe = moe;
+    bd.h2d_transfer = h2d;
+    bd.others = std::max(0.0, st.target_total - attn - moe - o1 - o2);
+    bd.iteration = st.target_total;
+    // driving variables as the reference defines them (pipeline.hpp:256-264);
+    // the engine verifies n = k+1 rows, the reference charges k (App. C.2)
+    const double b = double(in.b);
+    const double k = double(std::max<std::int64_t>(1, in.n - 1));
+    double s = 0;
+    for (auto p : in.prefix_len) s += double(p);
+    s /= std::max(1.0, double(in.prefix_len.size()));
+    const double nl = double(layers_);
+    samples_.push_back({EventKind::CPU_ATTN, b * (s + k) * k, attn / nl});
+    samples_.push_back({EventKind::GPU_MOE, b * k, moe / nl});
+    // one transfer sample per layer: bytes actually streamed (hot-cached
+    // experts excluded) -> the copy-engine's affine cost, as the paper's
+    // profiler fits it
+    for (std::int64_t l = 0; l < layers_; ++l) {
+      const double* t = lt.data() + l * 9;
+      if (t[8] > 0) samples_.push_back({EventKind::H2D_EXPERTS, t[8], t[1] - t[0]});
+    }
+    samples_.push_back({EventKind::GPU_OTHER1, b * k, o1 / nl});
+    samples_.push_back({EventKind::GPU_OTHER2, b * k, o2 / nl});
+    samples_.push_back({EventKind::OVERHEAD, b * (k + 1), bd.others});
+    return r;
+  }
+
+  HardwareSpec hw_;
+  ModelSpec model_;
+  Hyperparameters hyper_;
+  smo_engine* h_ = nullptr;
+  std::int64_t layers_ = 0;
+  std::vector<ProfileSample> samples_;
+};
+
+}  // namespace moeplan

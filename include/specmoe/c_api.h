@@ -259,6 +259,11 @@ typedef struct {
   double launches;     /* kernels launched */
 } smo_stage_times;
 smo_status smo_engine_last_times(smo_engine* e, smo_stage_times* t);
+/* Measured per-layer timeline of the last verify, 9 doubles per layer (s from
+ * the step start): H2D_EXPERTS start/end, K1 start/end, GPU_MOE start/end
+ * (after the slot wait), layer start, pre-MoE (after permute), and the bytes
+ * streamed for that layer (hot-cached experts excluded). n >= 9*L.         */
+smo_status smo_engine_layer_times(smo_engine* e, double* out, size_t n);
 
 /* Debug intermediates of the last verify (engine created with SMO_ENGINE_DEBUG).
  * name: "x_in" f32 [T,h] layer input, "xn1" bf16, "q" bf16 [T,n_q,d],

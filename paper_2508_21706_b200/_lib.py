@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libspecmoe.so")
+LIB_PATH = os.environ.get("SPECMOE_LIB", os.path.join(HERE, "libspecmoe.so"))
 
 SMO_OK, SMO_INVALID_ARG, SMO_CAPACITY, SMO_CUDA, SMO_NCCL, SMO_UNSUPPORTED = range(6)
 EPI_BF16, EPI_F32, EPI_F32_ADD, EPI_SWIGLU, EPI_ARGMAX = range(5)
@@ -100,6 +100,7 @@ _SIGS = {
     "smo_engine_fill_prefix": (C.c_int, [_vp, _vp, _i32]),
     "smo_engine_verify": (C.c_int, [_vp, C.POINTER(VerifyBatch), C.POINTER(VerifyOutput), _vp]),
     "smo_engine_last_times": (C.c_int, [_vp, C.POINTER(StageTimes)]),
+    "smo_engine_layer_times": (C.c_int, [_vp, _vp, _sz]),
     "smo_engine_debug_tensor": (C.c_int, [_vp, C.c_char_p, _i32, _vp, _sz]),
     "smo_engine_tensor_ptr": (C.c_int, [_vp, C.c_char_p, _i32, _i32, C.POINTER(_vp), C.POINTER(_sz)]),
 }

@@ -58,6 +58,22 @@ struct AttnSmem {
   static constexpr int kTotal = kPLoOff + kPBytes;
 };
 
+#ifdef SMO_ATTN_TRACE
+// Debug timeline of CTA 0 (globaltimer ns << 8 | event code) per role.
+__device__ unsigned long long g_trace[3][4096];
+__device__ int g_trace_n[3];
+__device__ __forceinline__ void trace_ev(int role, int code) {
+  if (blockIdx.x != 0) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  const int i = g_trace_n[role]++;
+  if (i < 4096) g_trace[role][i] = (t << 8) | unsigned(code);
+}
+#define TR(role, code) trace_ev(role, code)
+#else
+#define TR(role, code)
+#endif
+
 struct ItemInfo {
   int r, h, c_begin, c_end, keys;
 };
@@ -74,6 +90,20 @@ __device__ __forceinline__ ItemInfo item_info(const AttnParams& p, int item) {
   return it;
 }
 
+// Visibility of the 32 keys [p0, p0+32) for one query row: prefix keys are
+// implicitly visible, draft key d = key - prefix follows bit d of the row's
+// compact mask (bits >= n are clear). One 32-bit word per piece replaces
+// per-element 64-bit shifts.
+__device__ __forceinline__ uint32_t visible_bits(int p0, int prefix, uint64_t mbits) {
+  const int pre = prefix - p0;
+  const uint32_t pm = pre <= 0 ? 0u : (pre >= 32 ? 0xffffffffu : ((1u << pre) - 1u));
+  const int sh = p0 - prefix;
+  uint32_t dm = 0;
+  if (sh >= 0 && sh < 64) dm = uint32_t(mbits >> sh);
+  else if (sh < 0 && sh > -32) dm = uint32_t(mbits << (-sh));
+  return pm | dm;
+}
+
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     verify_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv_k,
@@ -83,7 +113,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t q_full[2], q_empty[2];
   __shared__ __align__(8) uint64_t kv_full[kKvStages], kv_empty[kKvStages];
-  __shared__ __align__(8) uint64_t s_full[2], s_empty[2], o_full[2], o_empty[2], p_full;
+  __shared__ __align__(8) uint64_t s_full[2], s_empty[2], o_full, p_full;
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -93,13 +123,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&q_empty[i], 1);
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 4);
-      mbar_init(&o_full[i], 1);
-      mbar_init(&o_empty[i], 4);
     }
     for (int i = 0; i < kKvStages; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
+    mbar_init(&o_full, 1);
     mbar_init(&p_full, 4);
     fence_barrier_init();
     tma_prefetch_desc(&tm_q);
@@ -111,7 +140,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
-  const int kv_row_base_stride = p.s_max;
+  constexpr uint32_t kOAcc = 256;  // O accumulator columns [256, 256+D)
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -123,15 +152,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int qb = used % L::kQBufs;
         mbar_wait(&q_empty[qb], ((used / L::kQBufs) & 1) ^ 1);
         ++used;
-        const uint32_t qbytes = uint32_t(L::kKBlocks * 64 * p.g * p.n * 2);
-        mbar_arrive_expect_tx(&q_full[qb], qbytes);
+        mbar_arrive_expect_tx(&q_full[qb], uint32_t(L::kKBlocks * 64 * p.g * p.n * 2));
         for (int kb = 0; kb < L::kKBlocks; ++kb)
           tma_load_3d(smem + L::kQOff + qb * L::kQBytes + kb * 16384, &tm_q, &q_full[qb], kb * 64, it.h * p.g,
                       it.r * p.n);
-        const int row_base = (it.r * p.n_kv + it.h) * kv_row_base_stride;
+        const int row_base = (it.r * p.n_kv + it.h) * p.s_max;
         for (int c = it.c_begin; c < it.c_end; ++c, ++gc) {
           const int s = gc % kKvStages;
+          TR(0, 1);
           mbar_wait(&kv_empty[s], ((gc / kKvStages) & 1) ^ 1);
+          TR(0, 2);
           mbar_arrive_expect_tx(&kv_full[s], uint32_t(2 * L::kKvBytes));
           uint8_t* kdst = smem + L::kKvOff + s * 2 * L::kKvBytes;
           uint8_t* vdst = kdst + L::kKvBytes;
@@ -160,6 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto issue_s = [&](int ci) {
           const int g2 = gc + ci;
           const int s = g2 % kKvStages, sb = g2 & 1;
+          TR(1, 1);
           mbar_wait(&kv_full[s], (g2 / kKvStages) & 1);
           mbar_wait(&s_empty[sb], ((g2 >> 1) & 1) ^ 1);
           tc_fence_after();
@@ -172,29 +203,33 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           umma_commit(&s_full[sb]);
           if (ci == nch - 1) umma_commit(&q_empty[qb]);
+          TR(1, 2);
         };
         issue_s(0);
         for (int ci = 0; ci < nch; ++ci) {
           if (ci + 1 < nch) issue_s(ci + 1);
           const int g2 = gc + ci;
-          const int s = g2 % kKvStages, ob = g2 & 1;
+          const int s = g2 % kKvStages;
+          TR(1, 4);
           mbar_wait(&p_full, p_phase);
+          TR(1, 5);
           p_phase ^= 1;
-          mbar_wait(&o_empty[ob], ((g2 >> 1) & 1) ^ 1);
           tc_fence_after();
           const uint32_t p_addr = smem_u32(smem + L::kPOff);
           const uint32_t plo_addr = smem_u32(smem + L::kPLoOff);
           const uint32_t v_addr = smem_u32(smem + L::kKvOff + s * 2 * L::kKvBytes + L::kKvBytes);
-          // O = P_hi V + P_lo V: P carried to ~16 mantissa bits
+          // O += P_hi V + P_lo V: P carried to ~16 mantissa bits
 #pragma unroll
           for (int kk = 0; kk < kChunk / 16; ++kk) {
             const uint32_t aoff = (kk / 4) * 16384 + (kk % 4) * 32;
             const uint64_t vd = make_sdesc_sw128(v_addr + kk * 2048, 16384, 1024);
-            umma_bf16(tmem + 256 + ob * 128, make_sdesc_sw128(p_addr + aoff, 16, 1024), vd, id_o, kk > 0 ? 1u : 0u);
-            umma_bf16(tmem + 256 + ob * 128, make_sdesc_sw128(plo_addr + aoff, 16, 1024), vd, id_o, 1u);
+            umma_bf16(tmem + kOAcc, make_sdesc_sw128(p_addr + aoff, 16, 1024), vd, id_o,
+                      (ci > 0 || kk > 0) ? 1u : 0u);
+            umma_bf16(tmem + kOAcc, make_sdesc_sw128(plo_addr + aoff, 16, 1024), vd, id_o, 1u);
           }
-          umma_commit(&o_full[ob]);
+          umma_commit(&o_full);
           umma_commit(&kv_empty[s]);
+          TR(1, 6);
         }
         gc += nch;
       }
@@ -204,6 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q4 = warp & 3;
     const int row = q4 * 32 + lane;
     const uint32_t tlane = uint32_t(q4 * 32) << 16;
+    const bool warp_live = q4 * 32 < p.rows;  // warp-uniform
     uint8_t* pbuf = smem + L::kPOff;
     int gc = 0;
     for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
@@ -212,86 +248,86 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool live = row < p.rows;
       const int qi = live ? row / p.g : 0;
       const int hh = live ? row % p.g : 0;
-      const uint64_t mbits = live ? p.mask[it.r * p.n + qi] : 0ull;
-      const int prefix = it.keys - p.n;
-      float O[D];
-#pragma unroll
-      for (int c = 0; c < D; ++c) O[c] = 0.f;
-      float m_run = -INFINITY, l_run = 0.f, m_fold = -INFINITY, m_pend = -INFINITY;
+      uint64_t mbits = live ? p.mask[it.r * p.n + qi] : 0ull;
+      if (p.n < 64) mbits &= (1ull << p.n) - 1ull;
+      const int prefix = live ? it.keys - p.n : 0;
+      float m_run = -INFINITY, l_run = 0.f;
       for (int ci = 0; ci < nch; ++ci) {
         const int g2 = gc + ci;
         const int sb = g2 & 1;
         const int key0 = (it.c_begin + ci) * kChunk;
+        if (warp == 4 && lane == 0) TR(2, 1);
         mbar_wait(&s_full[sb], (g2 >> 1) & 1);
+        if (warp == 4 && lane == 0) TR(2, 2);
         tc_fence_after();
-        // pass 1: masked row max of this chunk
-        float cmax = -INFINITY;
-#pragma unroll
-        for (int c0 = 0; c0 < kChunk; c0 += 32) {
-          uint32_t r[32];
-          tmem_ld32(tmem + tlane + sb * 128 + c0, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int key = key0 + c0 + j;
-            const bool vis = key < prefix || (key < it.keys && ((mbits >> (key - prefix)) & 1ull));
-            if (vis) cmax = fmaxf(cmax, __uint_as_float(r[j]));
-          }
-        }
-        const float m_new = fmaxf(m_run, cmax * p.scale_log2);
-        const float alpha = (m_run == -INFINITY) ? 0.f : exp2f(m_run - m_new);
-        const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
-        // fold the previous chunk's PV (relative to m_pend) before P is overwritten
-        if (ci > 0) {
-          const int pg = g2 - 1, ob = pg & 1;
-          mbar_wait(&o_full[ob], (pg >> 1) & 1);
-          tc_fence_after();
-          const float f = (m_fold == -INFINITY) ? 0.f : exp2f(m_fold - m_pend);
-#pragma unroll
-          for (int c0 = 0; c0 < D; c0 += 32) {
+        float m_new = m_run, alpha = 1.f;
+        if (warp_live) {
+          // pass 1: masked row max of this chunk (log2 domain)
+          float cmax = -INFINITY;
+#pragma unroll 1
+          for (int c0 = 0; c0 < kChunk; c0 += 32) {
             uint32_t r[32];
-            tmem_ld32(tmem + tlane + 256 + ob * 128 + c0, r);
+            tmem_ld32(tmem + tlane + sb * 128 + c0, r);
+            const uint32_t vb = visible_bits(key0 + c0, prefix, mbits);
             tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) O[c0 + j] = O[c0 + j] * f + __uint_as_float(r[j]);
+            for (int j = 0; j < 32; ++j)
+              if ((vb >> j) & 1u) cmax = fmaxf(cmax, __uint_as_float(r[j]));
           }
-          m_fold = m_pend;
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&o_empty[ob]);
+          m_new = fmaxf(m_run, cmax * p.scale_log2);
+          alpha = (m_run == -INFINITY) ? 0.f : ex2_approx(m_run - m_new);
         }
-        // pass 2: p = exp2(s*scale - m), row sum, bf16 P tile (swizzled K-major)
-        float psum = 0.f;
+        if (warp == 4 && lane == 0) TR(2, 3);
+        // the previous chunk's PV must be done before P is overwritten and
+        // before O is rescaled in TMEM (FA4-style correction, skipped when no
+        // row of this warp moved its maximum)
+        if (ci > 0) {
+          mbar_wait(&o_full, (g2 - 1) & 1);
+          tc_fence_after();
+          if (warp_live && __any_sync(0xffffffffu, live && alpha != 1.f)) {
+#pragma unroll 1
+            for (int c0 = 0; c0 < D; c0 += 32) {
+              uint32_t r[32];
+              tmem_ld32(tmem + tlane + kOAcc + c0, r);
+              tmem_ld_wait();
 #pragma unroll
-        for (int c0 = 0; c0 < kChunk; c0 += 32) {
-          uint32_t r[32];
-          tmem_ld32(tmem + tlane + sb * 128 + c0, r);
-          tmem_ld_wait();
-          uint32_t pk[16], pl[16];
-#pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            float pv[2];
-            uint16_t hi[2], lo[2];
-#pragma unroll
-            for (int t = 0; t < 2; ++t) {
-              const int key = key0 + c0 + j + t;
-              const bool vis = live && (key < prefix || (key < it.keys && ((mbits >> (key - prefix)) & 1ull)));
-              pv[t] = vis ? exp2f(__uint_as_float(r[j + t]) * p.scale_log2 - m_use) : 0.f;
-              psum += pv[t];
-              hi[t] = f2bf(pv[t]);
-              lo[t] = f2bf(pv[t] - bf2f(hi[t]));
+              for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * alpha);
+              tmem_st32(tmem + tlane + kOAcc + c0, r);
             }
-            pk[j / 2] = uint32_t(hi[0]) | (uint32_t(hi[1]) << 16);
-            pl[j / 2] = uint32_t(lo[0]) | (uint32_t(lo[1]) << 16);
+            tmem_st_wait();
           }
-          const int kb = c0 / 64;
+        }
+        if (warp == 4 && lane == 0) TR(2, 4);
+        // pass 2: p = 2^(s*scale - m), row sum, P = hi + lo bf16 planes
+        const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
+        float psum = 0.f;
+        if (warp_live) {
+#pragma unroll 1
+          for (int c0 = 0; c0 < kChunk; c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(tmem + tlane + sb * 128 + c0, r);
+            const uint32_t vb = live ? visible_bits(key0 + c0, prefix, mbits) : 0u;
+            tmem_ld_wait();
+            uint32_t pk[16], pl[16];
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int lc = ((c0 % 64) / 8) + t;
-            const int off = kb * 16384 + row * 128 + ((lc ^ (row & 7)) * 16);
-            *reinterpret_cast<uint4*>(pbuf + off) = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
-            *reinterpret_cast<uint4*>(pbuf + (L::kPLoOff - L::kPOff) + off) =
-                make_uint4(pl[4 * t], pl[4 * t + 1], pl[4 * t + 2], pl[4 * t + 3]);
+            for (int j = 0; j < 32; j += 2) {
+              const float a = ((vb >> j) & 1u) ? ex2_approx(__uint_as_float(r[j]) * p.scale_log2 - m_use) : 0.f;
+              const float b =
+                  ((vb >> (j + 1)) & 1u) ? ex2_approx(__uint_as_float(r[j + 1]) * p.scale_log2 - m_use) : 0.f;
+              psum += a + b;
+              const uint32_t hi = pack_bf16x2(a, b);
+              pk[j / 2] = hi;
+              pl[j / 2] = pack_bf16x2(a - __uint_as_float(hi << 16), b - __uint_as_float(hi & 0xffff0000u));
+            }
+            const int kb = c0 / 64;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int lc = ((c0 % 64) / 8) + t;
+              const int off = kb * 16384 + row * 128 + ((lc ^ (row & 7)) * 16);
+              *reinterpret_cast<uint4*>(pbuf + off) = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
+              *reinterpret_cast<uint4*>(pbuf + (L::kPLoOff - L::kPOff) + off) =
+                  make_uint4(pl[4 * t], pl[4 * t + 1], pl[4 * t + 2], pl[4 * t + 3]);
+            }
           }
         }
         tc_fence_before();
@@ -299,63 +335,62 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(&s_empty[sb]);
         l_run = l_run * alpha + psum;
         m_run = m_new;
-        m_pend = m_use;
         // keys past the request's end in the last chunk: zero their V rows so
         // stale (possibly non-finite) cache contents cannot reach the MMA
-        if (key0 + kChunk > it.keys) {
-          const int s = g2 % kKvStages;
-          uint8_t* vbuf = smem + L::kKvOff + s * 2 * L::kKvBytes + L::kKvBytes;
-          if (key0 + row >= it.keys) {
+        if (key0 + kChunk > it.keys && key0 + row >= it.keys) {
+          uint8_t* vbuf = smem + L::kKvOff + (g2 % kKvStages) * 2 * L::kKvBytes + L::kKvBytes;
 #pragma unroll
-            for (int kb = 0; kb < L::kKBlocks; ++kb)
+          for (int kb = 0; kb < L::kKBlocks; ++kb)
 #pragma unroll
-              for (int t = 0; t < 8; ++t)
-                *reinterpret_cast<uint4*>(vbuf + kb * 16384 + row * 128 + t * 16) = make_uint4(0, 0, 0, 0);
-          }
+            for (int t = 0; t < 8; ++t)
+              *reinterpret_cast<uint4*>(vbuf + kb * 16384 + row * 128 + t * 16) = make_uint4(0, 0, 0, 0);
         }
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full);
+        if (warp == 4 && lane == 0) TR(2, 5);
       }
       if (nch > 0) {
-        const int pg = gc + nch - 1, ob = pg & 1;
-        mbar_wait(&o_full[ob], (pg >> 1) & 1);
+        mbar_wait(&o_full, (gc + nch - 1) & 1);
         tc_fence_after();
-        const float f = (m_fold == -INFINITY) ? 0.f : exp2f(m_fold - m_pend);
-#pragma unroll
-        for (int c0 = 0; c0 < D; c0 += 32) {
-          uint32_t r[32];
-          tmem_ld32(tmem + tlane + 256 + ob * 128 + c0, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) O[c0 + j] = O[c0 + j] * f + __uint_as_float(r[j]);
-        }
-        m_fold = m_pend;
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&o_empty[ob]);
       }
       gc += nch;
-      if (!live) continue;
-      if (p.splits == 1) {
-        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-        uint16_t* dst = p.out + ((size_t(it.r) * p.n + qi) * p.n_q + size_t(it.h) * p.g + hh) * D;
+      if (!warp_live) continue;
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+#pragma unroll 1
+      for (int c0 = 0; c0 < D; c0 += 32) {
+        uint32_t r[32];
+        if (nch > 0) {
+          tmem_ld32(tmem + tlane + kOAcc + c0, r);
+          tmem_ld_wait();
+        } else {
 #pragma unroll
-        for (int c0 = 0; c0 < D; c0 += 8) {
-          uint4 v;
-          v.x = uint32_t(f2bf(O[c0] * inv)) | (uint32_t(f2bf(O[c0 + 1] * inv)) << 16);
-          v.y = uint32_t(f2bf(O[c0 + 2] * inv)) | (uint32_t(f2bf(O[c0 + 3] * inv)) << 16);
-          v.z = uint32_t(f2bf(O[c0 + 4] * inv)) | (uint32_t(f2bf(O[c0 + 5] * inv)) << 16);
-          v.w = uint32_t(f2bf(O[c0 + 6] * inv)) | (uint32_t(f2bf(O[c0 + 7] * inv)) << 16);
-          *reinterpret_cast<uint4*>(dst + c0) = v;
+          for (int j = 0; j < 32; ++j) r[j] = 0u;
         }
-      } else {
-        float* dst = p.ws_o + (size_t(item) * p.rows + row) * D;
+        if (!live) continue;
+        if (p.splits == 1) {
+          uint16_t* dst = p.out + ((size_t(it.r) * p.n + qi) * p.n_q + size_t(it.h) * p.g + hh) * D + c0;
 #pragma unroll
-        for (int c0 = 0; c0 < D; c0 += 4)
-          *reinterpret_cast<float4*>(dst + c0) = make_float4(O[c0], O[c0 + 1], O[c0 + 2], O[c0 + 3]);
-        p.ws_ml[size_t(item) * p.rows + row] = make_float2(nch > 0 ? m_fold : -INFINITY, l_run);
+          for (int j = 0; j < 32; j += 8) {
+            uint4 v;
+            v.x = pack_bf16x2(__uint_as_float(r[j]) * inv, __uint_as_float(r[j + 1]) * inv);
+            v.y = pack_bf16x2(__uint_as_float(r[j + 2]) * inv, __uint_as_float(r[j + 3]) * inv);
+            v.z = pack_bf16x2(__uint_as_float(r[j + 4]) * inv, __uint_as_float(r[j + 5]) * inv);
+            v.w = pack_bf16x2(__uint_as_float(r[j + 6]) * inv, __uint_as_float(r[j + 7]) * inv);
+            *reinterpret_cast<uint4*>(dst + j) = v;
+          }
+        } else {
+          float* dst = p.ws_o + (size_t(item) * p.rows + row) * D + c0;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(dst + j) =
+                make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                            __uint_as_float(r[j + 3]));
+        }
       }
+      if (live && p.splits > 1)
+        p.ws_ml[size_t(item) * p.rows + row] = make_float2(nch > 0 ? m_run : -INFINITY, l_run);
+      tc_fence_before();
     }
   }
   tc_fence_before();
@@ -576,6 +611,16 @@ __global__ void chunked_attention_f64_kernel(int n, int p, int d, const double* 
     out[size_t(i) * d + c] = acc;
   }
 }
+
+#ifdef SMO_ATTN_TRACE
+extern "C" int smo_debug_attn_trace(unsigned long long* out, int* counts) {
+  cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace));
+  cudaMemcpyFromSymbol(counts, g_trace_n, sizeof(g_trace_n));
+  int z[3] = {0, 0, 0};
+  cudaMemcpyToSymbol(g_trace_n, z, sizeof(z));
+  return 0;
+}
+#endif
 
 void chunked_attention_f64(size_t n, size_t p, size_t d, const double* Q, const double* K, const double* V,
                            size_t mask_n, const uint8_t* mask, double* out) {

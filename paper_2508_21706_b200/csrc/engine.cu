@@ -302,7 +302,7 @@ struct Engine {
     attn_ws = attn_ws_bytes ? dalloc<uint8_t>(attn_ws_bytes) : nullptr;
     h_stage_elems = size_t(maxT) * 4 + maxB * 4;
     SMO_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_stage), h_stage_elems * 4, cudaHostAllocPortable));
-    ev.resize(8 + size_t(L) * 6);
+    ev.resize(8 + size_t(L) * 8);
     for (auto& e : ev) SMO_CUDA_CHECK(cudaEventCreate(&e));
     SMO_CUDA_CHECK(cudaDeviceSynchronize());
   }
@@ -400,8 +400,8 @@ struct Engine {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> h2d_ev, attn_ev, moe_ev;
     auto tev = [&](int i) { return ev[8 + size_t(i)]; };
     for (int l = 0; l < std::min(slots, L); ++l) {
-      h2d_bytes += enqueue_h2d(l, tev(l * 6 + 0), tev(l * 6 + 1));
-      h2d_ev.push_back({tev(l * 6 + 0), tev(l * 6 + 1)});
+      h2d_bytes += enqueue_h2d(l, tev(l * 8 + 0), tev(l * 8 + 1));
+      h2d_ev.push_back({tev(l * 8 + 0), tev(l * 8 + 1)});
     }
     build_mask(parent, b, n, d_mask, st);
     embed(d_tokens, embed_w, T, h, x, st);
@@ -409,6 +409,7 @@ struct Engine {
     const int P = T * K;
     for (int l = 0; l < L; ++l) {
       Layer& ly = layers[l];
+      SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 6), st));
       snap("x_in", l, x, size_t(T) * h * 4, st);
       rmsnorm(x, ones, T, h, cfg.rms_eps, xn, st);
       snap("xn1", l, xn, size_t(T) * h * 2, st);
@@ -443,10 +444,10 @@ struct Engine {
       a.max_prefix = max_prefix;
       a.workspace = attn_ws;
       a.workspace_bytes = attn_ws_bytes;
-      SMO_CUDA_CHECK(cudaEventRecord(tev(l * 6 + 2), st));
+      SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 2), st));
       attention_launch(a, st);
-      SMO_CUDA_CHECK(cudaEventRecord(tev(l * 6 + 3), st));
-      attn_ev.push_back({tev(l * 6 + 2), tev(l * 6 + 3)});
+      SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 3), st));
+      attn_ev.push_back({tev(l * 8 + 2), tev(l * 8 + 3)});
       snap("attn", l, attn, size_t(T) * nq * d * 2, st);
       g = smo_gemm_args{};
       g.x = attn;
@@ -480,8 +481,9 @@ struct Engine {
       snap("offsets", l, offsets, size_t(E + 1) * 4, st);
       snap("pos", l, pos, size_t(P) * 4, st);
       // ---- MoE: wait for this layer's experts
+      SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 7), st));
       SMO_CUDA_CHECK(cudaStreamWaitEvent(st, slot_ready[l % slots], 0));
-      SMO_CUDA_CHECK(cudaEventRecord(tev(l * 6 + 4), st));
+      SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 4), st));
       g = smo_gemm_args{};
       g.x = xp;
       g.rows = P;
@@ -517,13 +519,13 @@ struct Engine {
       gemm_launch(g, st);
       SMO_CUDA_CHECK(cudaEventRecord(slot_free[l % slots], st));
       unpermute_combine(ybuf, pos, rw, T, K, h, x, st);
-      SMO_CUDA_CHECK(cudaEventRecord(tev(l * 6 + 5), st));
-      moe_ev.push_back({tev(l * 6 + 4), tev(l * 6 + 5)});
+      SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 5), st));
+      moe_ev.push_back({tev(l * 8 + 4), tev(l * 8 + 5)});
       snap("x_out", l, x, size_t(T) * h * 4, st);
       if (l + slots < L) {
         const int ln = l + slots;
-        h2d_bytes += enqueue_h2d(ln, tev(ln * 6 + 0), tev(ln * 6 + 1));
-        h2d_ev.push_back({tev(ln * 6 + 0), tev(ln * 6 + 1)});
+        h2d_bytes += enqueue_h2d(ln, tev(ln * 8 + 0), tev(ln * 8 + 1));
+        h2d_ev.push_back({tev(ln * 8 + 0), tev(ln * 8 + 1)});
       }
     }
     // ---- LM head with fused argmax partials, then K6
@@ -585,6 +587,23 @@ struct Engine {
   }
 
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending_attn, pending_moe, pending_h2d;
+
+  // Per layer: [h2d_start, h2d_end, attn_start, attn_end, moe_start, moe_end,
+  // layer_start, pre_moe] in seconds from the step's start event.
+  void layer_times(double* out, size_t n) {
+    SMO_REQUIRE(n >= size_t(L) * 9, "layer_times: output too small");
+    SMO_CUDA_CHECK(cudaDeviceSynchronize());
+    for (int l = 0; l < L; ++l) {
+      for (int k = 0; k < 8; ++k) {
+        float ms = 0;
+        SMO_CUDA_CHECK(cudaEventElapsedTime(&ms, ev[0], ev[8 + size_t(l) * 8 + k]));
+        out[size_t(l) * 9 + k] = ms * 1e-3;
+      }
+      int streamed = 0;
+      for (int e : owned) streamed += cache_blk[size_t(l) * E + e] < 0 ? 1 : 0;
+      out[size_t(l) * 9 + 8] = double(streamed) * double(blk_bytes);
+    }
+  }
 
   void times(smo_stage_times* t) {
     SMO_CUDA_CHECK(cudaDeviceSynchronize());
@@ -656,6 +675,13 @@ smo_status smo_engine_last_times(smo_engine* e, smo_stage_times* t) {
   return smo::run_guarded([&] {
     SMO_REQUIRE(e && t, "engine: null argument");
     e->impl.times(t);
+  });
+}
+
+smo_status smo_engine_layer_times(smo_engine* e, double* out, size_t n) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(e && out, "engine: null argument");
+    e->impl.layer_times(out, n);
   });
 }
 

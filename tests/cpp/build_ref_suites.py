@@ -62,3 +62,23 @@ def build(control: bool = True) -> list[str]:
 
 if __name__ == "__main__":
     print("\n".join(build()) or "reference tests not available", file=sys.stderr)
+
+
+OWN_GPU_SUITES = ["test_verify_engine"]
+
+
+def build_own() -> list[str]:
+    """This repository's own C++ GPU suites (need only the image's toolchain)."""
+    os.makedirs(OUT, exist_ok=True)
+    built = []
+    for name in OWN_GPU_SUITES:
+        src = os.path.join(ROOT, "tests", "cpp", name + ".cpp")
+        out = os.path.join(OUT, name)
+        inc = os.path.join(ROOT, "include")
+        deps = [src] + [os.path.join(inc, "moeplan", f) for f in os.listdir(os.path.join(inc, "moeplan"))]
+        if not os.path.exists(out) or os.path.getmtime(out) < max(os.path.getmtime(d) for d in deps):
+            if not os.path.isdir(JSON):
+                continue
+            _compile(src, out, inc, link_lib=True)
+        built.append(out)
+    return built

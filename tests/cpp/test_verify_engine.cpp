@@ -1,0 +1,140 @@
+// GPU test: the C++ VerifyEngine behind the reference's planner API.
+// Measured IterationResult / Schedule / ProfileSamples -> fit_latency_models
+// -> optimize -> DraftLengthController, on the tiny config (BASELINE config 1).
+#define DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
+#include <doctest.h>
+
+#include <sstream>
+
+#include "moeplan/optimizer.hpp"
+#include "moeplan/report.hpp"
+#include "moeplan/verify_engine.hpp"
+
+using namespace moeplan;
+
+namespace {
+
+HardwareSpec b200() {
+  HardwareSpec hw;
+  hw.p_gpu = 1384.5e12;  // MEASURED_PEAKS.json bf16 sustained
+  hw.b_gpu = 6555.5e9;   // MEASURED_PEAKS.json HBM
+  hw.b_h2d = 55.5e9;     // pinned PCIe Gen5 x16, tools/probe_box.py
+  hw.p_cpu = 2.0e12;
+  hw.b_cpu = 200e9;
+  hw.gpu_mem = 180e9;
+  hw.cpu_mem = 196e9;
+  return hw;
+}
+
+ModelSpec tiny() {
+  ModelSpec m;
+  m.h = 512;
+  m.h_i = 1792;
+  m.n_expert = 8;
+  m.n_activate = 2;
+  m.n_layers = 2;
+  m.g = 4;  // 2 KV heads of 64
+  m.draft.param_bytes = 1e8;
+  m.draft.kv_bytes_per_token = 16;  // keeps the planner clear of the draft-KV DRAM spill quirk
+  m.draft.ffn_ops_per_token = 1e7;
+  ModelArch a;
+  a.n_q_heads = 8;
+  a.head_dim = 64;
+  a.vocab = 32000;
+  m.arch = a;
+  return m;
+}
+
+WorkloadSpec apps() {
+  WorkloadSpec w;
+  w.mean_input_len = 512;
+  w.std_input_len = 0;
+  w.output_len = 128;
+  w.acceptance = AcceptanceCurve::geometric(0.8, 8);
+  return w;
+}
+
+VerifyBatch chain_batch(std::int64_t b, std::int64_t n, std::int32_t prefix) {
+  VerifyBatch vb;
+  vb.b = b;
+  vb.n = n;
+  for (std::int64_t i = 0; i < b * n; ++i) vb.tokens.push_back(std::int32_t((i * 7919) % 32000));
+  vb.prefix_len.assign(std::size_t(b), prefix);
+  return vb;
+}
+
+}  // namespace
+
+TEST_CASE("VerifyEngine measures the reference's target DAG") {
+  HardwareSpec hw = b200();
+  ModelSpec m = tiny();
+  WorkloadSpec w = apps();
+  Hyperparameters hp;
+  hp.b = 4;
+  hp.k = 8;
+  hp.exec_strategy.attention_placement = AttentionPlacement::GPU_RESIDENT;
+  MemoryPlan plan = plan_memory(hw, m, w, hp.b, hp.mem_policy);
+  EngineOptions opt;
+  opt.max_seq = 1024;
+  VerifyEngine eng(hw, m, hp, plan, opt);
+  eng.fill_prefix(std::vector<std::int32_t>(4, 600));
+
+  VerifyOutput out;
+  IterationResult r = eng.verify(chain_batch(4, 5, 600), &out);
+  CHECK(out.acc_len.size() == 4);
+  CHECK(r.target_dag.size() == std::size_t(5 * m.n_layers));
+  CHECK(r.breakdown.target_total > 0);
+  CHECK(r.breakdown.h2d_transfer > 0);
+  CHECK(r.breakdown.gpu_moe > 0);
+  CHECK(r.breakdown.cpu_attention > 0);
+  // measured schedule is consistent: every event starts after its deps end
+  for (const auto& ev : r.target_dag)
+    for (int d : ev.deps) CHECK(r.target_schedule.start[std::size_t(ev.id)] >= r.target_schedule.end[std::size_t(d)] - 1e-6);
+  // Table-3 report labels and a Chrome trace of the measured timeline
+  json rep = to_json(r.breakdown);
+  CHECK(rep.contains("HtoD Transfer"));
+  std::ostringstream tr;
+  emit_trace(r.target_dag, r.target_schedule, tr);
+  json trace = json::parse(tr.str());
+  CHECK(trace["traceEvents"].size() == r.target_dag.size() + 3);
+}
+
+TEST_CASE("measured profiles drive fit_latency_models, optimize and the controller") {
+  HardwareSpec hw = b200();
+  ModelSpec m = tiny();
+  WorkloadSpec w = apps();
+  Hyperparameters hp;
+  hp.b = 4;
+  hp.k = 8;
+  // three hot-cached experts: layer 0 streams 5 blocks, layer 1 streams 8
+  hp.mem_policy.expert_cache_bytes = 3.0 * 3.0 * m.expert_size() * 2.0;
+  MemoryPlan plan = plan_memory(hw, m, w, hp.b, hp.mem_policy);
+  EngineOptions opt;
+  opt.max_seq = 2048;
+  VerifyEngine eng(hw, m, hp, plan, opt);
+  eng.fill_prefix(std::vector<std::int32_t>(4, 1024));
+  for (int rep = 0; rep < 2; ++rep)
+    for (std::int64_t n : {2, 3, 5, 9}) {
+      eng.verify(chain_batch(4, n, 1024));
+      eng.verify(chain_batch(2, n, 512));
+    }
+  REQUIRE(eng.profile().size() == 2 * 8 * (5 + 2));
+  std::vector<std::string> warnings;
+  LatencyModel lm = fit_latency_models(eng.profile(), &warnings);
+  CHECK(lm.count(EventKind::CPU_ATTN) == 1);
+  CHECK(lm.count(EventKind::H2D_EXPERTS) == 1);
+  CHECK(lm.at(EventKind::H2D_EXPERTS).slope > 1.0 / 100e9);  // slower than 100 GB/s: it is the PCIe link
+  CHECK(lm.at(EventKind::GPU_MOE).intercept >= 0);
+  // the reference tuner on measured latencies
+  Plan p = optimize(hw, m, w, &lm, 8);
+  CHECK(p.k >= 0);
+  CHECK(p.expected_throughput > 0);
+  DraftLengthController ctl([&](std::int64_t prefix, std::int64_t active) {
+    Hyperparameters base;
+    (void)active;
+    return optimize(hw, m, w, &lm, 8, base, prefix).k;
+  });
+  const int k1 = ctl.update(600, 4);
+  const int k2 = ctl.update(700, 4);
+  CHECK(k2 <= k1);
+}

@@ -64,3 +64,17 @@ def test_reference_gpu_suite_passes(cuda, name):
     else:
         m = SUMMARY.search(r.stdout)
         assert m and m.group(3) == "0" and m.group(5) == "0", out
+
+
+@pytest.mark.gpu
+def test_cpp_verify_engine_planner_loop(cuda):
+    """C++ VerifyEngine (include/moeplan/verify_engine.hpp): measured
+    IterationResult + Chrome trace, ProfileSamples -> fit_latency_models ->
+    optimize -> DraftLengthController (SURVEY.md §8 b, f3)."""
+    path = os.path.join(B.OUT, "test_verify_engine")
+    if not os.path.exists(path):
+        B.build_own()
+    assert os.path.exists(path), "build/refsuites/test_verify_engine missing: run __graft_entry__.build()"
+    r = subprocess.run([path], capture_output=True, text=True, timeout=900, cwd=os.path.dirname(path))
+    m = SUMMARY.search(r.stdout)
+    assert r.returncode == 0 and m and m.group(3) == "0", r.stdout + r.stderr

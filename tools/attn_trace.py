@@ -1,0 +1,29 @@
+"""Debug: K1 timeline of CTA 0 (needs build/libspecmoe_trace.so, -DSMO_ATTN_TRACE)."""
+import ctypes as C, os, sys
+import numpy as np
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+os.environ["SPECMOE_LIB"] = os.path.join(ROOT, "build", "libspecmoe_trace.so")
+sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tools"))
+import torch
+import kbench
+from paper_2508_21706_b200 import _lib as L, ops
+lib = L.load()
+print(kbench.attn(32, 9, 1024))
+buf = np.zeros((3, 4096), np.uint64); cnt = np.zeros(3, np.int32)
+lib.smo_debug_attn_trace(buf.ctypes.data_as(C.c_void_p), cnt.ctypes.data_as(C.c_void_p))  # clear
+dev = torch.device("cuda:0")
+b, n, s, nq, nkv, d = 32, 9, 1024, 32, 8, 128
+q = torch.randn((b * n, nq, d), device=dev).to(torch.bfloat16)
+kc = torch.randn((b, nkv, s + 80, d), device=dev).to(torch.bfloat16)
+vc = torch.randn((b, nkv, s + 80, d), device=dev).to(torch.bfloat16)
+mask = torch.tensor([(1 << (i + 1)) - 1 for i in range(n)] * b, dtype=torch.int64, device=dev)
+pre = torch.full((b,), s, dtype=torch.int32, device=dev)
+ops.verify_attention(q, kc, vc, mask, pre, s)
+torch.cuda.synchronize()
+lib.smo_debug_attn_trace(buf.ctypes.data_as(C.c_void_p), cnt.ctypes.data_as(C.c_void_p))
+t0 = min(int(buf[r][0] >> 8) for r in range(3) if cnt[r])
+names = {0: "prod", 1: "mma", 2: "soft"}
+for r in range(3):
+    nn = min(int(cnt[r]), 4096)
+    evs = [(int(x >> 8) - t0, int(x & 255)) for x in buf[r][:nn]]
+    print(names[r], nn, " ".join(f"{c}@{t/1000:.2f}" for t, c in evs[:80]))

@@ -1,0 +1,112 @@
+"""Per-kernel microbench at BASELINE config-2/3 shapes (CUDA events, L2 flushed
+between reps). Prints one JSON line per kernel with achieved GB/s vs the
+measured HBM peak. Usage: python tools/kbench.py [attn|gemm|all] [--sweep]"""
+import json
+import math
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2508_21706_b200 import ops, _lib as L  # noqa: E402
+
+PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+dev = torch.device("cuda:0")
+flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+
+def timeit(fn, reps=10):
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e-3)
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
+def attn(b, n, s, nq=32, nkv=8, d=128, tree=False):
+    s_max = s + n + 64
+    g = torch.Generator(device=dev).manual_seed(1)
+    q = (torch.rand((b * n, nq, d), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
+    kc = (torch.rand((b, nkv, s_max, d), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
+    vc = (torch.rand((b, nkv, s_max, d), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
+    bits = [(1 << (i + 1)) - 1 for i in range(n)] * b
+    mask = torch.tensor(bits, dtype=torch.int64, device=dev)
+    pre = torch.full((b,), s, dtype=torch.int32, device=dev)
+    out = torch.empty_like(q)
+    t = timeit(lambda: ops.verify_attention(q, kc, vc, mask, pre, s, out=out))
+    byts = 2 * b * (s + n) * nkv * d * 2 + 2 * q.numel() * 2
+    return {"kernel": "K1 verify_attention", "b": b, "n": n, "s": s, "us": t * 1e6, "GBs": byts / t / 1e9,
+            "frac": byts / t / 1e9 / PEAK, "TFLOPs": 4 * b * n * (s + n) * nq * d / t / 1e12}
+
+
+def gemm(T, K, N, epi=L.EPI_BF16, name="dense"):
+    g = torch.Generator(device=dev).manual_seed(2)
+    x = (torch.rand((T, K), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
+    w = (torch.rand((N, K), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
+    out = torch.zeros((T, N), dtype=torch.float32 if epi in (L.EPI_F32, L.EPI_F32_ADD) else torch.bfloat16, device=dev)
+    t = timeit(lambda: ops.gemm(x, w, epilogue=epi, out=out))
+    byts = N * K * 2 + T * K * 2 + T * N * out.element_size()
+    return {"kernel": f"K4 gemm {name}", "T": T, "K": K, "N": N, "us": t * 1e6, "GBs": byts / t / 1e9,
+            "frac": byts / t / 1e9 / PEAK, "TFLOPs": 2 * T * K * N / t / 1e12}
+
+
+def moe(T=288, h=4096, hi=14336, E=8, k=2):
+    g = torch.Generator(device=dev).manual_seed(3)
+    x = (torch.rand((T, h), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
+    blk = 3 * h * hi
+    pool = (torch.rand((E * blk,), generator=g, device=dev) * 0.02).to(torch.bfloat16)
+    ids = torch.stack([torch.randperm(E, generator=g, device=dev)[:k] for _ in range(T)]).to(torch.int32)
+    off, perm, pos, xp = ops.permute(ids, E, x)
+    hbuf = torch.empty((T * k, hi), dtype=torch.bfloat16, device=dev)
+    y = torch.empty((T * k, h), dtype=torch.float32, device=dev)
+
+    def up():
+        ops.gemm(xp, pool, epilogue=L.EPI_SWIGLU, out=hbuf, w_up=pool[hi * h:], row_offsets=off, groups=E,
+                 w_block_stride=blk * 2, w_pool_blocks=E, N=hi, max_rows_per_group=T)
+
+    def down():
+        ops.gemm(hbuf, pool[2 * hi * h:], epilogue=L.EPI_F32, out=y, row_offsets=off, groups=E,
+                 w_block_stride=blk * 2, w_pool_blocks=E, N=h, max_rows_per_group=T)
+    r = []
+    for nm, fn, wb in (("swiglu gate/up", up, 2 * E * hi * h * 2), ("down", down, E * h * hi * 2)):
+        t = timeit(fn)
+        r.append({"kernel": f"K4 grouped {nm}", "T": T, "E": E, "us": t * 1e6, "GBs": wb / t / 1e9,
+                  "frac": wb / t / 1e9 / PEAK, "TFLOPs": (2 if "gate" in nm else 1) * 2 * T * k * h * hi / t / 1e12})
+    return r
+
+
+def main():
+    what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    res = []
+    if what in ("attn", "all"):
+        res.append(attn(32, 9, 1024))
+        res.append(attn(32, 5, 1024))
+        if "--sweep" in sys.argv:
+            for s in (1024, 4096, 16384, 32768):
+                for n in (1, 4, 8, 16):
+                    for b in (1, 16, 64):
+                        if b * n * 4 > 64 * 64 or (b * (s + n) * 8 * 128 * 4 > 20e9):
+                            continue
+                        res.append(attn(b, n, s))
+    if what in ("gemm", "all"):
+        res.append(gemm(288, 4096, 6144, name="qkv"))
+        res.append(gemm(288, 4096, 4096, L.EPI_F32_ADD, name="o-proj (+residual)"))
+        res.append(gemm(288, 4096, 32000, L.EPI_ARGMAX, name="lm-head argmax"))
+        res += moe()
+    for r in res:
+        print(json.dumps({k: (round(v, 3) if isinstance(v, float) else v) for k, v in r.items()}))
+
+
+if __name__ == "__main__":
+    main()
