@@ -135,8 +135,13 @@ typedef struct {
   int64_t ldo;
   float* argmax_val;          /* [rows, N/128] */
   int32_t* argmax_idx;
-  int32_t split_k;            /* 1 (reserved) */
+  int32_t split_k;            /* 0 = auto (dense GEMMs split K to cover the SMs), 1 = off, S */
+  void* workspace;            /* >= smo_gemm_workspace() bytes (fp32 split-K partials) */
+  size_t workspace_bytes;
 } smo_gemm_args;
+/* Split-K partials are reduced in fixed order (deterministic) and fused with
+ * the epilogue. Returns the workspace the call needs (0: none).            */
+size_t smo_gemm_workspace(const smo_gemm_args* a);
 smo_status smo_gemm(const smo_gemm_args* a, smo_stream stream);
 
 /* ---- support ops of the verify layer (standard Mixtral block, not in the

@@ -43,7 +43,8 @@ class GemmArgs(C.Structure):
     _fields_ = [("x", _vp), ("rows", _i32), ("K", _i32), ("N", _i32), ("groups", _i32),
                 ("row_offsets", _vp), ("max_rows_per_group", _i32), ("w", _vp), ("w_up", _vp),
                 ("w_block_stride", _u64), ("w_pool_blocks", _i32), ("w_index", _vp), ("epilogue", _i32),
-                ("out", _vp), ("ldo", _i64), ("argmax_val", _vp), ("argmax_idx", _vp), ("split_k", _i32)]
+                ("out", _vp), ("ldo", _i64), ("argmax_val", _vp), ("argmax_idx", _vp), ("split_k", _i32),
+                ("workspace", _vp), ("workspace_bytes", _sz)]
 
 
 class ModelConfig(C.Structure):
@@ -86,6 +87,7 @@ _SIGS = {
     "smo_router_topk": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "smo_permute": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp]),
     "smo_unpermute_combine": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp]),
+    "smo_gemm_workspace": (_sz, [C.POINTER(GemmArgs)]),
     "smo_gemm": (C.c_int, [C.POINTER(GemmArgs), _vp]),
     "smo_rmsnorm": (C.c_int, [_vp, _vp, _i32, _i32, _f32, _vp, _vp]),
     "smo_embed": (C.c_int, [_vp, _vp, _i32, _i32, _vp, _vp]),

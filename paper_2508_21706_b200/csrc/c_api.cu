@@ -17,6 +17,7 @@ void attention_launch(const smo_attn_args& a, cudaStream_t s);
 void chunked_attention_f64(size_t n, size_t p, size_t d, const double* Q, const double* K, const double* V,
                            size_t mask_n, const uint8_t* mask, double* out);
 void gemm_launch(const smo_gemm_args& a, cudaStream_t s);
+size_t gemm_workspace(const smo_gemm_args& a);
 void fill_uniform(void* dst, uint64_t count, uint64_t seed, uint64_t tensor_id, uint64_t base, float scale,
                   cudaStream_t st);
 void fill_kv_prefix(void* cache, const int32_t* prefix, int b, int n_kv, int d, int s_max, uint64_t seed,
@@ -153,6 +154,16 @@ smo_status smo_permute(const int32_t* ids, int32_t T, int32_t k, int32_t E, cons
 smo_status smo_unpermute_combine(const float* y, const int32_t* pos, const float* w, int32_t T, int32_t k,
                                  int32_t h, float* residual, smo_stream stream) {
   return guard([&] { smo::unpermute_combine(y, pos, w, T, k, h, residual, S(stream)); });
+}
+
+size_t smo_gemm_workspace(const smo_gemm_args* a) {
+  size_t r = 0;
+  if (guard([&] {
+        SMO_REQUIRE(a, "gemm: null args");
+        r = smo::gemm_workspace(*a);
+      }) != SMO_OK)
+    return size_t(-1);
+  return r;
 }
 
 smo_status smo_gemm(const smo_gemm_args* a, smo_stream stream) {

@@ -32,6 +32,7 @@ smo_status run_guarded(const std::function<void()>& f);
 size_t attention_workspace(const smo_attn_args& a);
 void attention_launch(const smo_attn_args& a, cudaStream_t s);
 void gemm_launch(const smo_gemm_args& a, cudaStream_t s);
+size_t gemm_workspace(const smo_gemm_args& a);
 void fill_uniform(void* dst, uint64_t count, uint64_t seed, uint64_t tensor_id, uint64_t base, float scale,
                   cudaStream_t st);
 void fill_kv_prefix(void* cache, const int32_t* prefix, int b, int n_kv, int d, int s_max, uint64_t seed,
@@ -101,6 +102,8 @@ struct Engine {
   uint64_t* d_mask = nullptr;
   void* attn_ws = nullptr;
   size_t attn_ws_bytes = 0;
+  void* gemm_ws = nullptr;  // split-K partials of the dense projections
+  size_t gemm_ws_bytes = 0;
   int32_t* h_stage = nullptr;  // pinned staging for host inputs/outputs
   size_t h_stage_elems = 0;
 
@@ -300,6 +303,23 @@ struct Engine {
       attn_ws_bytes = std::max(attn_ws_bytes, bound);
     }
     attn_ws = attn_ws_bytes ? dalloc<uint8_t>(attn_ws_bytes) : nullptr;
+    {
+      smo_gemm_args g{};
+      g.rows = maxT;
+      g.groups = 1;
+      g.max_rows_per_group = maxT;
+      g.epilogue = SMO_EPI_BF16;
+      g.K = h;
+      g.N = qkv_w;
+      gemm_ws_bytes = gemm_workspace(g);
+      g.K = nq * d;
+      g.N = h;
+      g.epilogue = SMO_EPI_F32_ADD;
+      gemm_ws_bytes = std::max(gemm_ws_bytes, gemm_workspace(g));
+      // smaller batches plan more splits: bound by 8 splits of the widest output
+      gemm_ws_bytes = std::max(gemm_ws_bytes, size_t(8) * maxT * std::max(qkv_w, h) * sizeof(float));
+      gemm_ws = dalloc<uint8_t>(gemm_ws_bytes);
+    }
     h_stage_elems = size_t(maxT) * 4 + maxB * 4;
     SMO_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_stage), h_stage_elems * 4, cudaHostAllocPortable));
     ev.resize(8 + size_t(L) * 8);
@@ -425,6 +445,8 @@ struct Engine {
       g.epilogue = SMO_EPI_BF16;
       g.out = qkv;
       g.ldo = qkv_w;
+      g.workspace = gemm_ws;
+      g.workspace_bytes = gemm_ws_bytes;
       gemm_launch(g, st);
       rope_append(qkv, d_prefix, parent, b, n, nq, nkv, d, s_max, cfg.rope_theta, q, ly.kc, ly.vc, st);
       snap("q", l, q, size_t(T) * nq * d * 2, st);
@@ -461,6 +483,8 @@ struct Engine {
       g.epilogue = SMO_EPI_F32_ADD;
       g.out = x;
       g.ldo = h;
+      g.workspace = gemm_ws;
+      g.workspace_bytes = gemm_ws_bytes;
       gemm_launch(g, st);
       rmsnorm(x, ones, T, h, cfg.rms_eps, xn, st);
       snap("xn2", l, xn, size_t(T) * h * 2, st);

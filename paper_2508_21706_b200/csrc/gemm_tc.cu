@@ -12,6 +12,8 @@
 // Algorithmic cost (roofline.hpp:56-64, moe_cost_large_batch):
 //   FLOPs = 2 * rows * N * K (x2 for SwiGLU), HBM bytes ~= weight bytes
 //   (N*K*2 per group, x2 for SwiGLU) + activations.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace smo {
@@ -36,6 +38,10 @@ struct GemmParams {
   float* amax_val;
   int32_t* amax_idx;
   int n_tiles;
+  int split_k;       // K split across blockIdx.z (deterministic partials + reduce)
+  int kb_per_split;
+  int token_tiles;
+  float* partial;    // [split_k][rows][N] fp32 when split_k > 1
 };
 
 __device__ __forceinline__ void tmem_alloc_dyn(uint32_t cols, uint32_t* dst) {
@@ -60,7 +66,7 @@ __device__ __forceinline__ void tmem_dealloc_dyn(uint32_t cols, uint32_t taddr) 
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_u,
                    const __grid_constant__ CUtensorMap tm_x, GemmParams p, uint32_t tmem_cols) {
-  const int nb = blockIdx.x, g = blockIdx.y, tt = blockIdx.z;
+  const int nb = blockIdx.x, g = blockIdx.y, tt = blockIdx.z % p.token_tiles, ks = blockIdx.z / p.token_tiles;
   const int g_begin = p.row_offsets ? p.row_offsets[g] : 0;
   const int g_end = p.row_offsets ? p.row_offsets[g + 1] : p.rows;
   const int row0 = g_begin + tt * p.tile_tokens;
@@ -74,7 +80,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int a_bytes = kTileBytesA * (swiglu ? 2 : 1);
   const int stage_bytes = a_bytes + p.tile_tokens * 128;
   const uint32_t tx_bytes = uint32_t(a_bytes + (n_load / 32) * 4096);
-  const int KB = p.K / kBK;
+  const int kb0 = ks * p.kb_per_split;
+  const int KB = min(p.K / kBK - kb0, p.kb_per_split);  // k-blocks of this CTA's K slice
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -109,11 +116,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&empty_bar[s], ph ^ 1);
         mbar_arrive_expect_tx(&full_bar[s], tx_bytes);
         uint8_t* sa = smem + s * stage_bytes;
-        tma_load_3d(sa, &tm_w, &full_bar[s], kb * kBK, nb * 128, wblk);
-        if (swiglu) tma_load_3d(sa + kTileBytesA, &tm_u, &full_bar[s], kb * kBK, nb * 128, wblk);
+        const int kc = (kb0 + kb) * kBK;
+        tma_load_3d(sa, &tm_w, &full_bar[s], kc, nb * 128, wblk);
+        if (swiglu) tma_load_3d(sa + kTileBytesA, &tm_u, &full_bar[s], kc, nb * 128, wblk);
         uint8_t* sb = sa + a_bytes;
         for (int i = 0; i < n_load / 32; ++i)
-          tma_load_2d(sb + i * 4096, &tm_x, &full_bar[s], kb * kBK, row0 + i * 32);
+          tma_load_2d(sb + i * 4096, &tm_x, &full_bar[s], kc, row0 + i * 32);
       }
     }
   } else if (warp == 1) {
@@ -200,7 +208,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else {
           tmem_ld_wait();
-          if (p.epilogue == SMO_EPI_BF16) {
+          if (p.split_k > 1) {  // fp32 partial of this K slice; reduced in fixed order later
+            float* part = p.partial + size_t(ks) * p.rows * p.N;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (c0 + j < cnt) part[size_t(row0 + c0 + j) * p.N + n] = __uint_as_float(r[j]);
+          } else if (p.epilogue == SMO_EPI_BF16) {
             uint16_t* out = reinterpret_cast<uint16_t*>(p.out);
 #pragma unroll
             for (int j = 0; j < 32; ++j)
@@ -210,11 +223,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               if (c0 + j < cnt) out[size_t(row0 + c0 + j) * p.ldo + n] = __uint_as_float(r[j]);
-          } else {  // SMO_EPI_F32_ADD
+          } else {  // SMO_EPI_F32_ADD: all loads first, then the stores (no
+                    // load-after-store serialisation through possible aliasing)
             float* out = reinterpret_cast<float*>(p.out);
+            float cur[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (c0 + j < cnt) out[size_t(row0 + c0 + j) * p.ldo + n] += __uint_as_float(r[j]);
+              cur[j] = (c0 + j < cnt) ? __ldcg(out + size_t(row0 + c0 + j) * p.ldo + n) : 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (c0 + j < cnt) out[size_t(row0 + c0 + j) * p.ldo + n] = cur[j] + __uint_as_float(r[j]);
           }
         }
       }
@@ -225,7 +243,84 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc_dyn(tmem_cols, tmem);
 }
 
+// Fixed-order split-K reduction fused with the epilogue: out = epi(sum_s P_s).
+__global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits, int rows, int N, int epilogue,
+                                     void* out, int64_t ldo) {
+  const size_t total4 = size_t(rows) * N / 4;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total4; i += size_t(gridDim.x) * blockDim.x) {
+    const size_t e = i * 4;
+    const int r = int(e / N), c = int(e % N);
+    float4 acc = reinterpret_cast<const float4*>(part)[i];
+    for (int s = 1; s < splits; ++s) {
+      const float4 v = reinterpret_cast<const float4*>(part + size_t(s) * rows * N)[i];
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    if (epilogue == SMO_EPI_BF16) {
+      uint16_t* o = reinterpret_cast<uint16_t*>(out) + size_t(r) * ldo + c;
+      *reinterpret_cast<uint2*>(o) = make_uint2(pack_bf16x2(acc.x, acc.y), pack_bf16x2(acc.z, acc.w));
+    } else {
+      float* o = reinterpret_cast<float*>(out) + size_t(r) * ldo + c;
+      if (epilogue == SMO_EPI_F32_ADD) {
+        const float4 cur = *reinterpret_cast<float4*>(o);
+        acc.x += cur.x;
+        acc.y += cur.y;
+        acc.z += cur.z;
+        acc.w += cur.w;
+      }
+      *reinterpret_cast<float4*>(o) = acc;
+    }
+  }
+}
+
+int device_sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+struct GemmPlan {
+  int tile, token_tiles, stages, split;
+  uint32_t cols;
+};
+
+GemmPlan plan_gemm(const smo_gemm_args& a) {
+  const bool swiglu = a.epilogue == SMO_EPI_SWIGLU;
+  const int per_group = a.max_rows_per_group > 0 ? std::min(a.max_rows_per_group, a.rows) : a.rows;
+  GemmPlan pl{};
+  const int cap = swiglu ? 256 : 512;
+  pl.tile = std::min(cap, (per_group + 31) & ~31);
+  pl.token_tiles = (per_group + pl.tile - 1) / pl.tile;
+  const int stage_bytes = kTileBytesA * (swiglu ? 2 : 1) + pl.tile * 128;
+  pl.stages = std::min(kMaxStages, kSmemBudget / stage_bytes);
+  pl.cols = 32;
+  const int need = swiglu ? 512 : pl.tile;
+  while (int(pl.cols) < need) pl.cols <<= 1;
+  // split K so that a dense GEMM with few weight tiles still covers the SMs;
+  // only for plain fp32/bf16/residual epilogues (argmax/SwiGLU need full sums)
+  pl.split = 1;
+  const bool splittable = a.epilogue == SMO_EPI_BF16 || a.epilogue == SMO_EPI_F32 || a.epilogue == SMO_EPI_F32_ADD;
+  const int tiles = (a.N / 128) * a.groups * pl.token_tiles;
+  if (splittable && a.groups == 1 && a.split_k != 1 && (a.N % 512) == 0) {
+    const int want = a.split_k > 1 ? a.split_k : device_sm_count() / std::max(1, tiles);
+    pl.split = std::max(1, std::min({want, a.K / kBK / 8, 8}));
+  }
+  return pl;
+}
+
 }  // namespace
+
+size_t gemm_workspace(const smo_gemm_args& a) {
+  const GemmPlan pl = plan_gemm(a);
+  return pl.split > 1 ? size_t(pl.split) * a.rows * a.N * sizeof(float) : 0;
+}
 
 void gemm_launch(const smo_gemm_args& a, cudaStream_t stream) {
   SMO_REQUIRE(a.x && a.w, "gemm: null operand");
@@ -237,17 +332,13 @@ void gemm_launch(const smo_gemm_args& a, cudaStream_t stream) {
   SMO_REQUIRE(!swiglu || a.w_up, "gemm: SWIGLU needs w_up");
   SMO_REQUIRE(a.epilogue != SMO_EPI_ARGMAX || (a.argmax_val && a.argmax_idx), "gemm: ARGMAX needs partial buffers");
   SMO_REQUIRE(a.epilogue == SMO_EPI_ARGMAX || a.out, "gemm: null output");
-  const int per_group = a.max_rows_per_group > 0 ? std::min(a.max_rows_per_group, a.rows) : a.rows;
-  const int cap = swiglu ? 256 : 512;
-  int tile = std::min(cap, (per_group + 31) & ~31);
-  const int token_tiles = (per_group + tile - 1) / tile;
-  const int a_bytes = kTileBytesA * (swiglu ? 2 : 1);
-  const int stage_bytes = a_bytes + tile * 128;
-  int stages = std::min(kMaxStages, kSmemBudget / stage_bytes);
+  const GemmPlan pl = plan_gemm(a);
+  const int tile = pl.tile, token_tiles = pl.token_tiles, stages = pl.stages;
+  const uint32_t cols = pl.cols;
   SMO_REQUIRE(stages >= 2, "gemm: token tile too large for the smem ring");
-  uint32_t cols = 32;
-  const int need = swiglu ? 512 : tile;
-  while (int(cols) < need) cols <<= 1;
+  const size_t ws_need = pl.split > 1 ? size_t(pl.split) * a.rows * a.N * sizeof(float) : 0;
+  SMO_REQUIRE(ws_need == 0 || (a.workspace && a.workspace_bytes >= ws_need),
+              "gemm: split-K workspace too small (smo_gemm_workspace)");
 
   CUtensorMap tw, tu, tx;
   const int pool = std::max(1, a.w_pool_blocks);
@@ -279,6 +370,11 @@ void gemm_launch(const smo_gemm_args& a, cudaStream_t stream) {
   p.amax_val = a.argmax_val;
   p.amax_idx = a.argmax_idx;
   p.n_tiles = a.N / 128;
+  p.split_k = pl.split;
+  p.kb_per_split = (a.K / kBK + pl.split - 1) / pl.split;
+  p.token_tiles = token_tiles;
+  p.partial = reinterpret_cast<float*>(a.workspace);
+  const int stage_bytes = kTileBytesA * (swiglu ? 2 : 1) + tile * 128;
   const size_t smem = size_t(stages) * stage_bytes + 1024;
   static bool attr_set = false;
   if (!attr_set) {
@@ -286,10 +382,17 @@ void gemm_launch(const smo_gemm_args& a, cudaStream_t stream) {
                                         kSmemBudget + 4096));
     attr_set = true;
   }
-  dim3 grid(a.N / 128, a.groups, token_tiles);
+  dim3 grid(a.N / 128, a.groups, token_tiles * pl.split);
   gemm_tc_kernel<<<grid, kThreads, smem, stream>>>(tw, tu, tx, p, cols);
   count_launch();
   SMO_CUDA_CHECK(cudaGetLastError());
+  if (pl.split > 1) {
+    const size_t total4 = size_t(a.rows) * a.N / 4;
+    const int blocks = int(std::min<size_t>((total4 + 255) / 256, size_t(device_sm_count()) * 8));
+    splitk_reduce_kernel<<<blocks, 256, 0, stream>>>(p.partial, pl.split, a.rows, a.N, a.epilogue, a.out, p.ldo);
+    count_launch();
+    SMO_CUDA_CHECK(cudaGetLastError());
+  }
 }
 
 }  // namespace smo

@@ -112,7 +112,7 @@ def unpermute_combine_(residual, y_perm, pos, weights):
 
 def gemm(x, w, *, epilogue=L.EPI_BF16, out=None, w_up=None, row_offsets=None, w_index=None,
          groups: int = 1, w_block_stride: int = 0, w_pool_blocks: int = 1, N: Optional[int] = None,
-         max_rows_per_group: Optional[int] = None):
+         max_rows_per_group: Optional[int] = None, split_k: int = 0):
     """K4 (tcgen05). out[t, n] = x[t] . W_g[n] for the rows of group g.
     Dense: w [N, K]. Grouped: w is a pool base pointer tensor and N must be given."""
     _req(x, _BF16, "x")
@@ -135,7 +135,13 @@ def gemm(x, w, *, epilogue=L.EPI_BF16, out=None, w_up=None, row_offsets=None, w_
                    epilogue=epilogue, out=None if out is None else out.data_ptr(),
                    ldo=0 if out is None else out.shape[-1],
                    argmax_val=None if amax_v is None else amax_v.data_ptr(),
-                   argmax_idx=None if amax_i is None else amax_i.data_ptr(), split_k=1)
+                   argmax_idx=None if amax_i is None else amax_i.data_ptr(), split_k=split_k)
+    ws_bytes = L.load().smo_gemm_workspace(C.byref(a))
+    if ws_bytes == C.c_size_t(-1).value:
+        L.check(L.SMO_INVALID_ARG)
+    ws = torch.empty(max(16, ws_bytes), dtype=torch.uint8, device=dev) if ws_bytes else None
+    if ws is not None:
+        a.workspace, a.workspace_bytes = ws.data_ptr(), ws_bytes
     L.check(L.load().smo_gemm(C.byref(a), _stream()))
     if epilogue == L.EPI_ARGMAX:
         return amax_v, amax_i
