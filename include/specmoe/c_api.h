@@ -222,8 +222,22 @@ typedef struct {
   int32_t device;
   int32_t flags;
   int32_t ep_rank, ep_size;   /* expert parallelism: this rank owns experts e % ep_size == ep_rank */
-  void* nccl_comm;            /* ncclComm_t when ep_size > 1 */
+  void* nccl_comm;            /* smo_ep_group* (NCCL or loopback) when ep_size > 1 */
 } smo_engine_options;
+
+/* ---- expert parallelism ----------------------------------
+ * Rank r of P owns experts e % P == r and streams only those; per layer the
+ * engine dispatches token rows to the owners and combines the results
+ * (fixed-capacity block all-to-all, owner-major order; results bit-identical
+ * to one GPU). Every rank must use identical engine options. The transport is
+ * an smo_ep_group: NCCL (one process per GPU; rank 0 makes the unique id and
+ * the caller broadcasts it) or an in-process loopback group (P engines on one
+ * device, one host thread per engine calling smo_engine_verify).          */
+typedef struct smo_ep_group smo_ep_group;
+smo_status smo_nccl_unique_id(uint8_t* id128);
+smo_status smo_ep_nccl_create(const uint8_t* id128, int32_t nranks, int32_t rank, smo_ep_group** out);
+smo_status smo_ep_loopback_create(int32_t ep_size, smo_ep_group** out);
+smo_status smo_ep_group_destroy(smo_ep_group* g);
 
 typedef struct smo_engine smo_engine;
 

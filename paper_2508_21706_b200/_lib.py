@@ -97,6 +97,10 @@ _SIGS = {
     "smo_argmax_rows": (C.c_int, [_vp, _i32, _i32, _vp, _vp]),
     "smo_greedy_accept": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
     "smo_kv_rollback": (C.c_int, [_vp, _vp, _i32, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "smo_nccl_unique_id": (C.c_int, [_vp]),
+    "smo_ep_nccl_create": (C.c_int, [_vp, _i32, _i32, C.POINTER(_vp)]),
+    "smo_ep_loopback_create": (C.c_int, [_i32, C.POINTER(_vp)]),
+    "smo_ep_group_destroy": (C.c_int, [_vp]),
     "smo_engine_create": (C.c_int, [C.POINTER(ModelConfig), C.POINTER(EngineOptions), C.POINTER(_vp)]),
     "smo_engine_destroy": (C.c_int, [_vp]),
     "smo_engine_fill_prefix": (C.c_int, [_vp, _vp, _i32]),

@@ -32,6 +32,15 @@ inline void cuda_check(cudaError_t e, const char* what) {
 // Counts kernel launches issued by this library (bench gpu_launches claim).
 void count_launch(int n = 1);
 
+// Expert-parallel transport (ep.cu): fixed-size block all-to-all on a stream.
+// send holds P blocks of `bytes` (block d -> rank d); recv receives P blocks
+// (block s <- rank s).
+struct EpTransport {
+  int P = 1;
+  virtual ~EpTransport() {}
+  virtual void alltoall(int rank, const void* send, void* recv, size_t bytes, cudaStream_t st) = 0;
+};
+
 // ---------------------------------------------------------------------------
 // bf16
 __host__ __device__ inline float bf2f(uint16_t h) {

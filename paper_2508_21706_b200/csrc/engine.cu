@@ -51,6 +51,17 @@ void argmax_reduce(const float* val, const int32_t* idx, int rows, int parts, in
 void greedy_accept(const int32_t* tokens, const int32_t* target, const int32_t* parent, int b, int n,
                    int32_t* acc_len, int32_t* bonus, int32_t* keep, cudaStream_t st);
 void build_mask(const int32_t* parent, int b, int n, uint64_t* mask, cudaStream_t st);
+// expert parallelism (ep.cu)
+EpTransport* ep_transport(void* group);
+void ep_remap(const int32_t* ids, int n, int P, int E_loc, int32_t* oid, cudaStream_t st);
+void ep_pack(const void* xp, const int32_t* offsets, int P, int E_loc, int C, int h, size_t block_bytes, void* send,
+             cudaStream_t st);
+void ep_pos(const int32_t* oid, const int32_t* pos, const int32_t* offsets, int n, int E_loc, int C, int32_t* pos_ep,
+            cudaStream_t st);
+void ep_unpack(const void* recv, int P, int E_loc, int C, int h, size_t block_bytes, void* xl, int32_t* offsets_l,
+               int32_t* back, cudaStream_t st);
+void ep_pack_back(const float* yl, const int32_t* back, const int32_t* offsets_l, int E_loc, int h, float* sendback,
+                  cudaStream_t st);
 
 // Procedural tensor ids; the oracle tests use the same ids.
 namespace tid {
@@ -91,6 +102,15 @@ struct Engine {
   std::vector<cudaEvent_t> slot_ready, slot_free;
   // EP: experts owned by this rank
   std::vector<int> owned;
+  // expert parallelism: transport, geometry and exchange buffers
+  EpTransport* ept = nullptr;
+  bool ep_on = false;
+  int P = 1, E_loc = 0, C = 0;
+  size_t blk_d = 0;  // dispatch block bytes (C bf16 rows + E_loc counts)
+  int32_t *oid = nullptr, *pos_ep = nullptr, *offsets_l = nullptr, *back = nullptr, *d_w_index_loc = nullptr;
+  uint8_t *ep_send = nullptr, *ep_recv = nullptr;
+  uint16_t* xl = nullptr;
+  float *yl = nullptr, *ep_sendback = nullptr, *ep_recvback = nullptr;
 
   // activations (max sizes)
   int maxT = 0, maxB = 0, maxN = 0, s_max = 0;
@@ -158,7 +178,18 @@ struct Engine {
     SMO_REQUIRE(nq > 0 && nkv > 0 && nq % nkv == 0 && (d == 64 || d == 128), "engine: bad attention shape");
     SMO_REQUIRE(h % 256 == 0 && hi % 128 == 0 && V % 128 == 0 && (nq * d) % 128 == 0, "engine: unsupported dims");
     SMO_REQUIRE(opt.max_batch > 0 && opt.max_verify > 0 && opt.max_verify <= 64, "engine: bad batch options");
-    SMO_REQUIRE(opt.ep_size <= 1, "engine: expert parallelism is driven by the Python EP front end (not here)");
+    // expert parallelism whenever a transport is given (ep_size 1 with a
+    // 1-rank group runs the full dispatch/combine path: a 1-GPU check of it)
+    if (opt.ep_size > 1 || opt.nccl_comm) {
+      const int ps = std::max(1, opt.ep_size);
+      SMO_REQUIRE(E % ps == 0, "engine: n_expert must be divisible by ep_size");
+      SMO_REQUIRE(opt.ep_rank >= 0 && opt.ep_rank < ps, "engine: bad ep_rank");
+      ept = ep_transport(opt.nccl_comm);
+      SMO_REQUIRE(ept && ept->P == ps, "engine: ep_size needs an smo_ep_group of that size");
+      P = ps;
+      ep_on = true;
+    }
+    E_loc = E / P;
     qkv_w = (nq + 2 * nkv) * d;
     blk_elems = size_t(3) * h * hi;
     blk_bytes = blk_elems * 2;
@@ -209,7 +240,7 @@ struct Engine {
     uint16_t* stage = dalloc<uint16_t>(blk_elems);
     for (int a = 0; a < host_alias; ++a) {
       void* hp = nullptr;
-      cudaError_t err = cudaHostAlloc(&hp, blk_bytes * E, cudaHostAllocPortable);
+      cudaError_t err = cudaHostAlloc(&hp, blk_bytes * E_loc, cudaHostAllocPortable);
       if (err != cudaSuccess)
         throw Error(SMO_CAPACITY, "engine: pinned host allocation of " + std::to_string(blk_bytes * E) +
                                       " bytes failed (" + cudaGetErrorString(err) + "); set host_alias_layers");
@@ -219,7 +250,7 @@ struct Engine {
         fill_uniform(stage, size_t(hi) * h, cfg.seed, base + 0, 0, std::sqrt(3.0f / h), st);
         fill_uniform(stage + size_t(hi) * h, size_t(hi) * h, cfg.seed, base + 1, 0, std::sqrt(3.0f / h), st);
         fill_uniform(stage + 2 * size_t(hi) * h, size_t(h) * hi, cfg.seed, base + 2, 0, std::sqrt(3.0f / hi), st);
-        SMO_CUDA_CHECK(cudaMemcpy(host_bufs[a] + size_t(e) * blk_elems, stage, blk_bytes, cudaMemcpyDeviceToHost));
+        SMO_CUDA_CHECK(cudaMemcpy(host_bufs[a] + size_t(local(e)) * blk_elems, stage, blk_bytes, cudaMemcpyDeviceToHost));
       }
     }
 
@@ -230,26 +261,33 @@ struct Engine {
     for (int l = 0; l < L && placed < cache_blocks; ++l)
       for (int e : owned) {
         if (placed >= cache_blocks) break;
-        cache_blk[size_t(l) * E + e] = slots * E + placed;
+        cache_blk[size_t(l) * E + e] = slots * E_loc + placed;
         ++placed;
       }
-    pool_blocks = slots * E + placed;
+    pool_blocks = slots * E_loc + placed;
     pool = dalloc<uint16_t>(size_t(pool_blocks) * blk_elems);
     for (int l = 0; l < L; ++l)
       for (int e : owned) {
         const int cb = cache_blk[size_t(l) * E + e];
         if (cb >= 0)
-          SMO_CUDA_CHECK(cudaMemcpy(pool + size_t(cb) * blk_elems, host_bufs[host_layer(l)] + size_t(e) * blk_elems,
+          SMO_CUDA_CHECK(cudaMemcpy(pool + size_t(cb) * blk_elems, host_bufs[host_layer(l)] + size_t(local(e)) * blk_elems,
                                     blk_bytes, cudaMemcpyHostToDevice));
       }
     std::vector<int32_t> widx(size_t(L) * E);
     for (int l = 0; l < L; ++l)
       for (int e = 0; e < E; ++e) {
         const int cb = cache_blk[size_t(l) * E + e];
-        widx[size_t(l) * E + e] = cb >= 0 ? cb : (l % slots) * E + e;
+        widx[size_t(l) * E + e] = cb >= 0 ? cb : (l % slots) * E_loc + local(e);
       }
     d_w_index = dalloc<int32_t>(widx.size());
     SMO_CUDA_CHECK(cudaMemcpy(d_w_index, widx.data(), widx.size() * 4, cudaMemcpyHostToDevice));
+    if (ep_on) {  // local expert le of this rank = global expert le*P + rank
+      std::vector<int32_t> wl(size_t(L) * E_loc);
+      for (int l = 0; l < L; ++l)
+        for (int le = 0; le < E_loc; ++le) wl[size_t(l) * E_loc + le] = widx[size_t(l) * E + le * P + opt.ep_rank];
+      d_w_index_loc = dalloc<int32_t>(wl.size());
+      SMO_CUDA_CHECK(cudaMemcpy(d_w_index_loc, wl.data(), wl.size() * 4, cudaMemcpyHostToDevice));
+    }
     slot_ready.resize(slots);
     slot_free.resize(slots);
     for (int s = 0; s < slots; ++s) {
@@ -270,7 +308,26 @@ struct Engine {
     perm = dalloc<int32_t>(P);
     pos = dalloc<int32_t>(P);
     xp = dalloc<uint16_t>(size_t(P) * h);
-    hbuf = dalloc<uint16_t>(size_t(P) * hi);
+    if (ep_on) {
+      // fixed capacity per destination: every local (token, slot) pair could
+      // target one owner; identical on all ranks (same options)
+      C = P;
+      const int PR = this->P;
+      blk_d = (size_t(C) * h * 2 + size_t(E_loc) * 4 + 15) & ~size_t(15);
+      oid = dalloc<int32_t>(P);
+      pos_ep = dalloc<int32_t>(P);
+      offsets_l = dalloc<int32_t>(E_loc + 1);
+      back = dalloc<int32_t>(size_t(PR) * C);
+      ep_send = dalloc<uint8_t>(size_t(PR) * blk_d);
+      ep_recv = dalloc<uint8_t>(size_t(PR) * blk_d);
+      xl = dalloc<uint16_t>(size_t(PR) * C * h);
+      yl = dalloc<float>(size_t(PR) * C * h);
+      ep_sendback = dalloc<float>(size_t(PR) * C * h);
+      ep_recvback = dalloc<float>(size_t(PR) * C * h);
+      hbuf = dalloc<uint16_t>(size_t(PR) * C * hi);
+    } else {
+      hbuf = dalloc<uint16_t>(size_t(P) * hi);
+    }
     ybuf = dalloc<float>(size_t(P) * h);
     amax_v = dalloc<float>(size_t(maxT) * (V / 128));
     amax_i = dalloc<int32_t>(size_t(maxT) * (V / 128));
@@ -340,25 +397,32 @@ struct Engine {
   }
 
   // Stream layer l's non-cached owned experts into slot l % slots.
+  // owned expert e -> its local index (host block / staging slot position)
+  int local(int e) const { return P > 1 ? e / P : e; }
+
+  // Stream layer l's non-cached owned experts into slot l % slots. Host and
+  // slot blocks are in local order, so runs of consecutive local experts go
+  // out as one copy (a whole layer when nothing is cached: 2.8 GB for 8x7B).
   double enqueue_h2d(int l, cudaEvent_t t0, cudaEvent_t t1) {
     const int s = l % slots;
     SMO_CUDA_CHECK(cudaStreamWaitEvent(copy, slot_free[s], 0));
     if (t0) SMO_CUDA_CHECK(cudaEventRecord(t0, copy));
     double bytes = 0;
     const uint16_t* hb = host_bufs[host_layer(l)];
-    int e = 0;
-    while (e < E) {
-      if (!owns(e) || cache_blk[size_t(l) * E + e] >= 0) {
-        ++e;
+    auto streamed = [&](int le) { return cache_blk[size_t(l) * E + owned[size_t(le)]] < 0; };
+    int le = 0;
+    while (le < E_loc) {
+      if (!streamed(le)) {
+        ++le;
         continue;
       }
-      int e2 = e;
-      while (e2 + 1 < E && owns(e2 + 1) && cache_blk[size_t(l) * E + e2 + 1] < 0 && opt.ep_size <= 1) ++e2;
-      const size_t nbytes = size_t(e2 - e + 1) * blk_bytes;
-      SMO_CUDA_CHECK(cudaMemcpyAsync(pool + (size_t(s) * E + e) * blk_elems, hb + size_t(e) * blk_elems, nbytes,
+      int le2 = le;
+      while (le2 + 1 < E_loc && streamed(le2 + 1)) ++le2;
+      const size_t nbytes = size_t(le2 - le + 1) * blk_bytes;
+      SMO_CUDA_CHECK(cudaMemcpyAsync(pool + (size_t(s) * E_loc + le) * blk_elems, hb + size_t(le) * blk_elems, nbytes,
                                      cudaMemcpyHostToDevice, copy));
       bytes += double(nbytes);
-      e = e2 + 1;
+      le = le2 + 1;
     }
     if (t1) SMO_CUDA_CHECK(cudaEventRecord(t1, copy));
     SMO_CUDA_CHECK(cudaEventRecord(slot_ready[s], copy));
@@ -377,6 +441,58 @@ struct Engine {
     }
     SMO_CUDA_CHECK(cudaMemcpyAsync(v[idx].p, src, bytes, cudaMemcpyDeviceToDevice, st));
   }
+
+  // Expert-parallel MoE of layer l (ep.cu): dispatch, local shard, combine.
+  void moe_ep(int l, int T, cudaStream_t st) {
+    const int PT = T * K;
+    const int rank = opt.ep_rank;
+    ep_pack(xp, offsets, P, E_loc, C, h, blk_d, ep_send, st);
+    ep_pos(oid, pos, offsets, PT, E_loc, C, pos_ep, st);
+    ept->alltoall(rank, ep_send, ep_recv, blk_d, st);
+    ep_unpack(ep_recv, P, E_loc, C, h, blk_d, xl, offsets_l, back, st);
+    SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 7), st));
+    SMO_CUDA_CHECK(cudaStreamWaitEvent(st, slot_ready[l % slots], 0));
+    SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 4), st));
+    smo_gemm_args g{};
+    g.x = xl;
+    g.rows = P * C;
+    g.K = h;
+    g.N = hi;
+    g.groups = E_loc;
+    g.row_offsets = offsets_l;
+    g.max_rows_per_group = P * maxT;
+    g.w = pool;
+    g.w_up = pool + size_t(hi) * h;
+    g.w_block_stride = blk_bytes;
+    g.w_pool_blocks = pool_blocks;
+    g.w_index = d_w_index_loc + size_t(l) * E_loc;
+    g.epilogue = SMO_EPI_SWIGLU;
+    g.out = hbuf;
+    g.ldo = hi;
+    gemm_launch(g, st);
+    g = smo_gemm_args{};
+    g.x = hbuf;
+    g.rows = P * C;
+    g.K = hi;
+    g.N = h;
+    g.groups = E_loc;
+    g.row_offsets = offsets_l;
+    g.max_rows_per_group = P * maxT;
+    g.w = pool + 2 * size_t(hi) * h;
+    g.w_block_stride = blk_bytes;
+    g.w_pool_blocks = pool_blocks;
+    g.w_index = d_w_index_loc + size_t(l) * E_loc;
+    g.epilogue = SMO_EPI_F32;
+    g.out = yl;
+    g.ldo = h;
+    gemm_launch(g, st);
+    SMO_CUDA_CHECK(cudaEventRecord(slot_free[l % slots], st));
+    ep_pack_back(yl, back, offsets_l, E_loc, h, ep_sendback, st);
+    ept->alltoall(rank, ep_sendback, ep_recvback, size_t(C) * h * sizeof(float), st);
+    unpermute_combine(ep_recvback, pos_ep, rw, T, K, h, x, st);
+  }
+
+  cudaEvent_t tev(int i) const { return ev[8 + size_t(i)]; }
 
   void verify(const smo_verify_batch& in, smo_verify_output& out, cudaStream_t st) {
     const int b = in.b, n = in.n, T = b * n;
@@ -418,7 +534,6 @@ struct Engine {
     SMO_CUDA_CHECK(cudaStreamWaitEvent(copy, e_start, 0));
     double h2d_bytes = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> h2d_ev, attn_ev, moe_ev;
-    auto tev = [&](int i) { return ev[8 + size_t(i)]; };
     for (int l = 0; l < std::min(slots, L); ++l) {
       h2d_bytes += enqueue_h2d(l, tev(l * 8 + 0), tev(l * 8 + 1));
       h2d_ev.push_back({tev(l * 8 + 0), tev(l * 8 + 1)});
@@ -426,7 +541,7 @@ struct Engine {
     build_mask(parent, b, n, d_mask, st);
     embed(d_tokens, embed_w, T, h, x, st);
 
-    const int P = T * K;
+    const int PT = T * K;  // (token, slot) pairs
     for (int l = 0; l < L; ++l) {
       Layer& ly = layers[l];
       SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 6), st));
@@ -499,50 +614,59 @@ struct Engine {
         rlog = reinterpret_cast<float*>(v[l + 1].p);
       }
       router_topk(xn, ly.router, T, h, E, K, rlog, ids, rw, st);
-      permute(ids, T, K, E, xn, h, offsets, perm, pos, xp, st);
-      snap("ids", l, ids, size_t(P) * 4, st);
-      snap("weights", l, rw, size_t(P) * 4, st);
+      if (ep_on) {  // owner-major order: rows bound for one rank are contiguous
+        ep_remap(ids, T * K, P, E_loc, oid, st);
+        permute(oid, T, K, E, xn, h, offsets, perm, pos, xp, st);
+      } else {
+        permute(ids, T, K, E, xn, h, offsets, perm, pos, xp, st);
+      }
+      snap("ids", l, ids, size_t(PT) * 4, st);
+      snap("weights", l, rw, size_t(PT) * 4, st);
       snap("offsets", l, offsets, size_t(E + 1) * 4, st);
-      snap("pos", l, pos, size_t(P) * 4, st);
+      snap("pos", l, pos, size_t(PT) * 4, st);
       // ---- MoE: wait for this layer's experts
-      SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 7), st));
-      SMO_CUDA_CHECK(cudaStreamWaitEvent(st, slot_ready[l % slots], 0));
-      SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 4), st));
-      g = smo_gemm_args{};
-      g.x = xp;
-      g.rows = P;
-      g.K = h;
-      g.N = hi;
-      g.groups = E;
-      g.row_offsets = offsets;
-      g.max_rows_per_group = T;  // a token selects an expert at most once
-      g.w = pool;
-      g.w_up = pool + size_t(hi) * h;
-      g.w_block_stride = blk_bytes;
-      g.w_pool_blocks = pool_blocks;
-      g.w_index = d_w_index + size_t(l) * E;
-      g.epilogue = SMO_EPI_SWIGLU;
-      g.out = hbuf;
-      g.ldo = hi;
-      gemm_launch(g, st);
-      g = smo_gemm_args{};
-      g.x = hbuf;
-      g.rows = P;
-      g.K = hi;
-      g.N = h;
-      g.groups = E;
-      g.row_offsets = offsets;
-      g.max_rows_per_group = T;
-      g.w = pool + 2 * size_t(hi) * h;
-      g.w_block_stride = blk_bytes;
-      g.w_pool_blocks = pool_blocks;
-      g.w_index = d_w_index + size_t(l) * E;
-      g.epilogue = SMO_EPI_F32;
-      g.out = ybuf;
-      g.ldo = h;
-      gemm_launch(g, st);
-      SMO_CUDA_CHECK(cudaEventRecord(slot_free[l % slots], st));
-      unpermute_combine(ybuf, pos, rw, T, K, h, x, st);
+      if (ep_on) {
+        moe_ep(l, T, st);
+      } else {
+        SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 7), st));
+        SMO_CUDA_CHECK(cudaStreamWaitEvent(st, slot_ready[l % slots], 0));
+        SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 4), st));
+        g = smo_gemm_args{};
+        g.x = xp;
+        g.rows = PT;
+        g.K = h;
+        g.N = hi;
+        g.groups = E;
+        g.row_offsets = offsets;
+        g.max_rows_per_group = T;  // a token selects an expert at most once
+        g.w = pool;
+        g.w_up = pool + size_t(hi) * h;
+        g.w_block_stride = blk_bytes;
+        g.w_pool_blocks = pool_blocks;
+        g.w_index = d_w_index + size_t(l) * E;
+        g.epilogue = SMO_EPI_SWIGLU;
+        g.out = hbuf;
+        g.ldo = hi;
+        gemm_launch(g, st);
+        g = smo_gemm_args{};
+        g.x = hbuf;
+        g.rows = PT;
+        g.K = hi;
+        g.N = h;
+        g.groups = E;
+        g.row_offsets = offsets;
+        g.max_rows_per_group = T;
+        g.w = pool + 2 * size_t(hi) * h;
+        g.w_block_stride = blk_bytes;
+        g.w_pool_blocks = pool_blocks;
+        g.w_index = d_w_index + size_t(l) * E;
+        g.epilogue = SMO_EPI_F32;
+        g.out = ybuf;
+        g.ldo = h;
+        gemm_launch(g, st);
+        SMO_CUDA_CHECK(cudaEventRecord(slot_free[l % slots], st));
+        unpermute_combine(ybuf, pos, rw, T, K, h, x, st);
+      }
       SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 5), st));
       moe_ev.push_back({tev(l * 8 + 4), tev(l * 8 + 5)});
       snap("x_out", l, x, size_t(T) * h * 4, st);
@@ -766,7 +890,8 @@ smo_status smo_engine_tensor_ptr(smo_engine* e, const char* name, int32_t layer,
     } else if (n == "expert_host") {
       need_layer();
       SMO_REQUIRE(expert >= 0 && expert < g.E, "engine: expert out of range");
-      *ptr = g.host_bufs[g.host_layer(layer)] + size_t(expert) * g.blk_elems;
+      SMO_REQUIRE(g.owns(expert), "engine: expert not owned by this rank");
+      *ptr = g.host_bufs[g.host_layer(layer)] + size_t(g.local(expert)) * g.blk_elems;
       *bytes = g.blk_bytes;
     } else {
       throw smo::Error(SMO_INVALID_ARG, "engine: unknown tensor " + n);

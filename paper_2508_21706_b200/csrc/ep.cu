@@ -1,0 +1,342 @@
+// ep.cu — expert parallelism: token dispatch / combine
+// around the grouped SwiGLU experts, and the transports that move the blocks.
+//
+// Rank r of P owns the experts e with e % P == r and streams only those
+// (K5 per-rank shard). Per layer, on each rank:
+//   router -> owner-major permutation -> ep_pack (fixed-capacity block per
+//   destination: C rows + per-local-expert counts) -> all-to-all ->
+//   ep_unpack (rows grouped by local expert, src-major inside an expert) ->
+//   grouped SwiGLU/down on the local shard -> ep_pack_back -> all-to-all ->
+//   combine at owner-major positions (fixed slot order, no atomics).
+// Every expert row is computed by the same kernel with the same K order as on
+// one GPU, so EP results are bit-identical to the single-GPU engine.
+//
+// Transports: NCCL grouped send/recv (libnccl.so.2 resolved with dlopen, so the
+// library has no link-time NCCL dependency) and an in-process loopback group
+// (P engines on one GPU, one host thread each) that makes dispatch/combine
+// testable on a single B200.
+#include <dlfcn.h>
+
+#include <atomic>
+#include <functional>
+#include <condition_variable>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace smo {
+
+// ---------------------------------------------------------------- kernels
+namespace {
+
+// owner-major expert id: experts of rank 0 first (in local order), then rank 1...
+__global__ void ep_remap_kernel(const int32_t* ids, int n, int P, int E_loc, int32_t* oid) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const int e = ids[i];
+    oid[i] = (e % P) * E_loc + e / P;
+  }
+}
+
+// send block d: rows [0, C) bf16 x h, then E_loc int32 counts.
+__global__ void ep_pack_kernel(const uint16_t* __restrict__ xp, const int32_t* __restrict__ offsets, int P,
+                               int E_loc, int C, int h, size_t block_bytes, uint8_t* __restrict__ send) {
+  const int d = blockIdx.y;
+  const int seg0 = offsets[d * E_loc], seg1 = offsets[(d + 1) * E_loc];
+  uint8_t* blk = send + size_t(d) * block_bytes;
+  if (blockIdx.x == 0 && threadIdx.x < E_loc) {
+    int32_t* cnt = reinterpret_cast<int32_t*>(blk + size_t(C) * h * 2);
+    cnt[threadIdx.x] = offsets[d * E_loc + threadIdx.x + 1] - offsets[d * E_loc + threadIdx.x];
+  }
+  const int rows = seg1 - seg0;
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+    const uint4* src = reinterpret_cast<const uint4*>(xp + size_t(seg0 + r) * h);
+    uint4* dst = reinterpret_cast<uint4*>(blk + size_t(r) * h * 2);
+    for (int c = threadIdx.x; c < h / 8; c += blockDim.x) dst[c] = src[c];
+  }
+}
+
+// position of each local (token, slot) pair's returned row: d*C + rank in d.
+__global__ void ep_pos_kernel(const int32_t* __restrict__ oid, const int32_t* __restrict__ pos,
+                              const int32_t* __restrict__ offsets, int n, int E_loc, int C, int32_t* pos_ep) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int d = oid[i] / E_loc;
+  pos_ep[i] = d * C + (pos[i] - offsets[d * E_loc]);
+}
+
+// recv block s -> rows grouped by local expert (src-major within an expert);
+// offsets_l [E_loc+1]; back[q] = s*C + i (where row q came from).
+__global__ void ep_unpack_kernel(const uint8_t* __restrict__ recv, int P, int E_loc, int C, int h,
+                                 size_t block_bytes, uint16_t* __restrict__ xl, int32_t* __restrict__ offsets_l,
+                                 int32_t* __restrict__ back) {
+  extern __shared__ int sh[];
+  int* cnt = sh;                // [P][E_loc]
+  int* dst0 = sh + P * E_loc;   // start row of (s, le) block in xl
+  int* src0 = dst0 + P * E_loc; // start row of (s, le) block in the recv block s
+  for (int i = threadIdx.x; i < P * E_loc; i += blockDim.x) {
+    const int s = i / E_loc, le = i % E_loc;
+    cnt[i] = reinterpret_cast<const int32_t*>(recv + size_t(s) * block_bytes + size_t(C) * h * 2)[le];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int le = 0; le < E_loc; ++le) {
+      offsets_l[le] = run;
+      for (int s = 0; s < P; ++s) {
+        dst0[s * E_loc + le] = run;
+        run += cnt[s * E_loc + le];
+      }
+    }
+    offsets_l[E_loc] = run;
+    for (int s = 0; s < P; ++s) {
+      int r = 0;
+      for (int le = 0; le < E_loc; ++le) {
+        src0[s * E_loc + le] = r;
+        r += cnt[s * E_loc + le];
+      }
+    }
+  }
+  __syncthreads();
+  for (int blk = blockIdx.x; blk < P * E_loc; blk += gridDim.x) {
+    const int s = blk / E_loc;
+    const int n = cnt[blk];
+    for (int i = 0; i < n; ++i) {
+      const int src_row = src0[blk] + i, dst_row = dst0[blk] + i;
+      const uint4* src = reinterpret_cast<const uint4*>(recv + size_t(s) * block_bytes + size_t(src_row) * h * 2);
+      uint4* dst = reinterpret_cast<uint4*>(xl + size_t(dst_row) * h);
+      for (int c = threadIdx.x; c < h / 8; c += blockDim.x) dst[c] = src[c];
+      if (threadIdx.x == 0) back[dst_row] = s * C + src_row;
+    }
+  }
+}
+
+// expert outputs back to their source ranks' slots (fp32 rows).
+__global__ void ep_pack_back_kernel(const float* __restrict__ yl, const int32_t* __restrict__ back,
+                                    const int32_t* __restrict__ offsets_l, int E_loc, int h,
+                                    float* __restrict__ sendback) {
+  const int rows = offsets_l[E_loc];
+  for (int q = blockIdx.x; q < rows; q += gridDim.x) {
+    const float4* src = reinterpret_cast<const float4*>(yl + size_t(q) * h);
+    float4* dst = reinterpret_cast<float4*>(sendback + size_t(back[q]) * h);
+    for (int c = threadIdx.x; c < h / 4; c += blockDim.x) dst[c] = src[c];
+  }
+}
+
+}  // namespace
+
+void ep_remap(const int32_t* ids, int n, int P, int E_loc, int32_t* oid, cudaStream_t st) {
+  ep_remap_kernel<<<(n + 255) / 256, 256, 0, st>>>(ids, n, P, E_loc, oid);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+void ep_pack(const void* xp, const int32_t* offsets, int P, int E_loc, int C, int h, size_t block_bytes, void* send,
+             cudaStream_t st) {
+  dim3 grid(64, P);
+  ep_pack_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const uint16_t*>(xp), offsets, P, E_loc, C, h, block_bytes,
+                                       reinterpret_cast<uint8_t*>(send));
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+void ep_pos(const int32_t* oid, const int32_t* pos, const int32_t* offsets, int n, int E_loc, int C, int32_t* pos_ep,
+            cudaStream_t st) {
+  ep_pos_kernel<<<(n + 255) / 256, 256, 0, st>>>(oid, pos, offsets, n, E_loc, C, pos_ep);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+void ep_unpack(const void* recv, int P, int E_loc, int C, int h, size_t block_bytes, void* xl, int32_t* offsets_l,
+               int32_t* back, cudaStream_t st) {
+  const size_t smem = size_t(3) * P * E_loc * sizeof(int);
+  ep_unpack_kernel<<<128, 256, smem, st>>>(reinterpret_cast<const uint8_t*>(recv), P, E_loc, C, h, block_bytes,
+                                           reinterpret_cast<uint16_t*>(xl), offsets_l, back);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+void ep_pack_back(const float* yl, const int32_t* back, const int32_t* offsets_l, int E_loc, int h, float* sendback,
+                  cudaStream_t st) {
+  ep_pack_back_kernel<<<256, 256, 0, st>>>(yl, back, offsets_l, E_loc, h, sendback);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------- transports
+// In-process loopback: P engines (one host thread each) on one device.
+struct LoopbackTransport : EpTransport {
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t generation = 0;
+  std::vector<const void*> sends;
+  std::vector<cudaEvent_t> sent, copied;
+
+  explicit LoopbackTransport(int p) {
+    P = p;
+    sends.assign(size_t(p), nullptr);
+    sent.resize(size_t(p));
+    copied.resize(size_t(p));
+    for (int i = 0; i < p; ++i) {
+      SMO_CUDA_CHECK(cudaEventCreateWithFlags(&sent[size_t(i)], cudaEventDisableTiming));
+      SMO_CUDA_CHECK(cudaEventCreateWithFlags(&copied[size_t(i)], cudaEventDisableTiming));
+    }
+  }
+  ~LoopbackTransport() override {
+    for (auto e : sent) cudaEventDestroy(e);
+    for (auto e : copied) cudaEventDestroy(e);
+  }
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t gen = generation;
+    if (++arrived == P) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != gen; });
+    }
+  }
+  void alltoall(int rank, const void* send, void* recv, size_t bytes, cudaStream_t st) override {
+    SMO_CUDA_CHECK(cudaEventRecord(sent[size_t(rank)], st));
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      sends[size_t(rank)] = send;
+    }
+    barrier();  // every rank's send buffer and event are published
+    for (int s = 0; s < P; ++s) {
+      SMO_CUDA_CHECK(cudaStreamWaitEvent(st, sent[size_t(s)], 0));
+      SMO_CUDA_CHECK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(recv) + size_t(s) * bytes,
+                                     reinterpret_cast<const uint8_t*>(sends[size_t(s)]) + size_t(rank) * bytes, bytes,
+                                     cudaMemcpyDeviceToDevice, st));
+    }
+    SMO_CUDA_CHECK(cudaEventRecord(copied[size_t(rank)], st));
+    barrier();  // every rank has enqueued its reads
+    for (int s = 0; s < P; ++s) SMO_CUDA_CHECK(cudaStreamWaitEvent(st, copied[size_t(s)], 0));
+    barrier();  // events consumed before they can be re-recorded
+  }
+};
+
+// NCCL grouped send/recv through a dlopen'd libnccl.so.2.
+struct NcclApi {
+  void* so = nullptr;
+  int (*getUniqueId)(void*) = nullptr;
+  void* commInitRank = nullptr;  // int(ncclComm_t*, int, ncclUniqueId /*by value*/, int)
+  int (*commDestroy)(void*) = nullptr;
+  int (*send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*groupStart)() = nullptr;
+  int (*groupEnd)() = nullptr;
+  const char* (*errStr)(int) = nullptr;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* cands[] = {"libnccl.so.2", "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2"};
+    for (const char* c : cands) {
+      api.so = dlopen(c, RTLD_NOW | RTLD_GLOBAL);
+      if (api.so) break;
+    }
+    if (!api.so) return;
+    api.getUniqueId = reinterpret_cast<int (*)(void*)>(dlsym(api.so, "ncclGetUniqueId"));
+    api.commInitRank = dlsym(api.so, "ncclCommInitRank");
+    api.commDestroy = reinterpret_cast<int (*)(void*)>(dlsym(api.so, "ncclCommDestroy"));
+    api.send = reinterpret_cast<int (*)(const void*, size_t, int, int, void*, cudaStream_t)>(dlsym(api.so, "ncclSend"));
+    api.recv = reinterpret_cast<int (*)(void*, size_t, int, int, void*, cudaStream_t)>(dlsym(api.so, "ncclRecv"));
+    api.groupStart = reinterpret_cast<int (*)()>(dlsym(api.so, "ncclGroupStart"));
+    api.groupEnd = reinterpret_cast<int (*)()>(dlsym(api.so, "ncclGroupEnd"));
+    api.errStr = reinterpret_cast<const char* (*)(int)>(dlsym(api.so, "ncclGetErrorString"));
+  });
+  if (!api.so || !api.send || !api.recv || !api.commInitRank)
+    throw Error(SMO_NCCL, "libnccl.so.2 not found (expert parallelism needs NCCL)");
+  return api;
+}
+
+static void nccl_check(int r, const char* what) {
+  if (r != 0) throw Error(SMO_NCCL, std::string(what) + ": " + (nccl().errStr ? nccl().errStr(r) : "nccl error"));
+}
+
+// ncclCommInitRank takes the 128-byte ncclUniqueId by value; passing a struct
+// of that size by value matches the x86-64 ABI of the real signature.
+struct UniqueId {
+  char b[128];
+};
+
+struct NcclTransport : EpTransport {
+  void* comm = nullptr;
+  NcclTransport(const uint8_t* id, int nranks, int rank) {
+    P = nranks;
+    UniqueId uid;
+    std::memcpy(uid.b, id, 128);
+    auto init = reinterpret_cast<int (*)(void**, int, UniqueId, int)>(nccl().commInitRank);
+    nccl_check(init(&comm, nranks, uid, rank), "ncclCommInitRank");
+  }
+  ~NcclTransport() override {
+    if (comm) nccl().commDestroy(comm);
+  }
+  void alltoall(int rank, const void* send, void* recv, size_t bytes, cudaStream_t st) override {
+    (void)rank;
+    NcclApi& a = nccl();
+    constexpr int kUint8 = 1;  // ncclUint8
+    nccl_check(a.groupStart(), "ncclGroupStart");
+    for (int peer = 0; peer < P; ++peer) {
+      nccl_check(a.send(reinterpret_cast<const uint8_t*>(send) + size_t(peer) * bytes, bytes, kUint8, peer, comm, st),
+                 "ncclSend");
+      nccl_check(a.recv(reinterpret_cast<uint8_t*>(recv) + size_t(peer) * bytes, bytes, kUint8, peer, comm, st),
+                 "ncclRecv");
+    }
+    nccl_check(a.groupEnd(), "ncclGroupEnd");
+  }
+};
+
+}  // namespace smo
+
+struct smo_ep_group {
+  smo::EpTransport* t = nullptr;
+  ~smo_ep_group() { delete t; }
+};
+
+namespace smo {
+smo_status run_guarded(const std::function<void()>& f);
+EpTransport* ep_transport(void* group) { return group ? reinterpret_cast<smo_ep_group*>(group)->t : nullptr; }
+}  // namespace smo
+
+extern "C" {
+
+smo_status smo_ep_loopback_create(int32_t ep_size, smo_ep_group** out) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(out && ep_size >= 1, "ep: bad arguments");
+    auto* g = new smo_ep_group();
+    g->t = new smo::LoopbackTransport(ep_size);
+    *out = g;
+  });
+}
+
+smo_status smo_nccl_unique_id(uint8_t* id128) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(id128, "ep: null id buffer");
+    smo::nccl_check(smo::nccl().getUniqueId(id128), "ncclGetUniqueId");
+  });
+}
+
+smo_status smo_ep_nccl_create(const uint8_t* id128, int32_t nranks, int32_t rank, smo_ep_group** out) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(id128 && out && nranks >= 1 && rank >= 0 && rank < nranks, "ep: bad arguments");
+    auto* g = new smo_ep_group();
+    try {
+      g->t = new smo::NcclTransport(id128, nranks, rank);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+smo_status smo_ep_group_destroy(smo_ep_group* g) {
+  return smo::run_guarded([&] { delete g; });
+}
+
+}  // extern "C"

@@ -55,6 +55,38 @@ MIXTRAL_8X22B = ModelShape(hidden=6144, inter=16384, n_expert=8, top_k=2, n_laye
                            n_kv_heads=8, head_dim=128, vocab=32000)
 
 
+class EpGroup:
+    """Expert-parallel transport (smo_ep_group): NCCL across processes, or an
+    in-process loopback group for P engines on one device."""
+
+    def __init__(self, handle):
+        self.handle = handle
+
+    @staticmethod
+    def loopback(ep_size: int) -> "EpGroup":
+        h = C.c_void_p()
+        L.check(L.load().smo_ep_loopback_create(ep_size, C.byref(h)))
+        return EpGroup(h)
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        L.check(L.load().smo_nccl_unique_id(buf))
+        return bytes(buf)
+
+    @staticmethod
+    def nccl(unique_id: bytes, nranks: int, rank: int) -> "EpGroup":
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        L.check(L.load().smo_ep_nccl_create(buf, nranks, rank, C.byref(h)))
+        return EpGroup(h)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            L.load().smo_ep_group_destroy(self.handle)
+            self.handle = None
+
+
 @dataclass
 class VerifyResult:
     acc_len: np.ndarray
@@ -65,11 +97,18 @@ class VerifyResult:
 
 class VerifyEngine:
     def __init__(self, shape: ModelShape, *, max_batch: int, max_verify: int, max_seq: int, hbm_slots: int = 2,
-                 expert_cache_bytes: int = 0, host_alias_layers: int = 0, device: int = 0, debug: bool = False):
+                 expert_cache_bytes: int = 0, host_alias_layers: int = 0, device: int = 0, debug: bool = False,
+                 ep_rank: int = 0, ep_size: int = 1, ep_group: Optional["EpGroup"] = None):
         self.shape = shape
         self.max_batch, self.max_verify, self.max_seq = max_batch, max_verify, max_seq
+        if ep_size > 1 and ep_group is None:
+            raise ValueError("ep_size > 1 needs an EpGroup (nccl or loopback)")
+        if ep_group is not None:
+            ep_size = max(1, ep_size)
+        self._group = ep_group  # keep the transport alive as long as the engine
         opt = L.EngineOptions(max_batch, max_verify, max_seq, hbm_slots, int(expert_cache_bytes),
-                              host_alias_layers, device, L.ENGINE_DEBUG if debug else 0, 0, 1, None)
+                              host_alias_layers, device, L.ENGINE_DEBUG if debug else 0, ep_rank, ep_size,
+                              None if ep_group is None else ep_group.handle)
         cfg = shape.to_c()
         h = C.c_void_p()
         L.check(L.load().smo_engine_create(C.byref(cfg), C.byref(opt), C.byref(h)))
@@ -139,19 +178,22 @@ def geometric_alpha(p: float, k: int) -> float:
 
 
 def step_roofline(shape: ModelShape, b: int, n: int, prefix: int, h2d_gbs: float, hbm_gbs: float,
-                  tflops: float, cached_blocks: int = 0) -> dict:
+                  tflops: float, cached_blocks: int = 0, ep: int = 1) -> dict:
     """Binding roofline of one verify step: the slower of
-    host-link bytes, HBM bytes and tensor peak (roofline.hpp:108-151)."""
+    host-link bytes, HBM bytes and tensor peak (roofline.hpp:108-151), per
+    GPU. `b` is the global batch; with expert parallelism over `ep` GPUs each
+    streams and reads E/ep experts per layer and attends b/ep requests."""
     s = shape
     T = b * n
     e_bytes = s.expert_bytes
     activated = s.n_expert  # large batch: every expert activates (SURVEY.md a11)
-    h2d = (s.n_layers * activated - cached_blocks) * e_bytes
-    kv = 2 * b * (prefix + n) * s.n_kv_heads * s.head_dim * 2
+    h2d = (s.n_layers * activated - cached_blocks) * e_bytes / ep
+    kv = 2 * (b / ep) * (prefix + n) * s.n_kv_heads * s.head_dim * 2
     dense = (s.hidden * (s.n_q_heads + 2 * s.n_kv_heads) * s.head_dim + s.n_q_heads * s.head_dim * s.hidden) * 2
-    hbm = s.n_layers * (activated * e_bytes + kv + dense) + s.vocab * s.hidden * 2
-    flops = s.n_layers * (2 * 3 * s.hidden * s.inter * T * s.top_k + 2 * T * dense / 2
-                          + 4 * b * n * (prefix + n) * s.n_q_heads * s.head_dim) + 2 * T * s.hidden * s.vocab
+    hbm = s.n_layers * (activated / ep * e_bytes + kv + dense) + s.vocab * s.hidden * 2
+    flops = (s.n_layers * (2 * 3 * s.hidden * s.inter * T * s.top_k / ep + 2 * (T / ep) * dense / 2
+                           + 4 * (b / ep) * n * (prefix + n) * s.n_q_heads * s.head_dim)
+             + 2 * (T / ep) * s.hidden * s.vocab)
     t = {"h2d": h2d / (h2d_gbs * 1e9), "hbm": hbm / (hbm_gbs * 1e9), "tensor": flops / (tflops * 1e12)}
     bound = max(t, key=t.get)
     return {"bound": bound, "t_roof_s": t[bound], "h2d_bytes": h2d, "hbm_bytes": hbm, "flops": flops,
