@@ -45,7 +45,8 @@ def parse():
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--k", type=int, default=8, help="draft length (verify rows = k+1)")
     ap.add_argument("--prefix", type=int, default=1024)
-    ap.add_argument("--model", default="mixtral-8x7b", choices=["mixtral-8x7b", "tiny", "mixtral-8x22b"])
+    ap.add_argument("--model", default="mixtral-8x7b",
+                    choices=["mixtral-8x7b", "tiny", "mixtral-8x22b", "dsv2-lite", "qwen2-57b"])
     ap.add_argument("--cache-gb", type=float, default=0.0, help="hot-expert HBM cache (GB)")
     ap.add_argument("--alias", type=int, default=0, help="host_alias_layers (0 = one pinned buffer per layer)")
     ap.add_argument("--slots", type=int, default=2)
@@ -56,7 +57,8 @@ def parse():
 
 def shape_of(name):
     from paper_2508_21706_b200 import engine as E
-    return {"mixtral-8x7b": E.MIXTRAL_8X7B, "tiny": E.TINY, "mixtral-8x22b": E.MIXTRAL_8X22B}[name]
+    return {"mixtral-8x7b": E.MIXTRAL_8X7B, "tiny": E.TINY, "mixtral-8x22b": E.MIXTRAL_8X22B,
+            "dsv2-lite": E.DSV2_LITE, "qwen2-57b": E.QWEN2_57B}[name]
 
 
 def peaks():
@@ -236,6 +238,12 @@ def cpu_layer_sample(shape, b, n, prefix, threads, use_reference=True):
         w1, w3, w2 = experts[e]
         L.orc_expert_swiglu(P(X), rows.size, h, hi, P(w1), P(w3), P(w2), P(Y))
         y[rows] += wts[rows, slots][:, None] * Y
+    if getattr(s, "shared_inter", 0):
+        si = s.shared_inter
+        ws = [O.fill_uniform_bf16(si * h, s.seed, 1050 + j, float(np.sqrt(3 / (h if j < 2 else si)))) for j in range(3)]
+        Ysh = np.zeros((T, h), np.float32)
+        L.orc_expert_swiglu(P(np.ascontiguousarray(xn)), T, h, si, P(ws[0]), P(ws[1]), P(ws[2]), P(Ysh))
+        y += Ysh
     t["moe"] = time.perf_counter() - t0
     t0 = time.perf_counter()
     lo = np.zeros((lm_rows, s.vocab), np.float32)

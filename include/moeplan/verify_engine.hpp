@@ -90,6 +90,7 @@ class VerifyEngine {
     c.seed = opt.seed;
     c.lm_scale = opt.lm_scale;
     c.router_scale = opt.router_scale;
+    c.shared_inter = std::int32_t(a.shared_expert_inter);
     smo_engine_options o{};
     o.max_batch = std::int32_t(hyper.b);
     o.max_verify = std::int32_t(std::max(1, hyper.k) + 1);

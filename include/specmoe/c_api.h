@@ -208,6 +208,8 @@ typedef struct {
   uint64_t seed;
   float lm_scale;      /* multiplier on the LM-head init scale (margin screening) */
   float router_scale;  /* multiplier on the router init scale */
+  int32_t shared_inter; /* always-on shared expert width (0: none; DeepSeek/Qwen-style,
+                           resident in HBM, SwiGLU over every token) */
 } smo_model_config;
 
 enum { SMO_ENGINE_DEBUG = 1 /* keep per-layer intermediates for parity tests */ };

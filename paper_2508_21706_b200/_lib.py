@@ -51,7 +51,7 @@ class ModelConfig(C.Structure):
     _fields_ = [("hidden", _i32), ("inter", _i32), ("n_expert", _i32), ("top_k", _i32), ("n_layers", _i32),
                 ("n_q_heads", _i32), ("n_kv_heads", _i32), ("head_dim", _i32), ("vocab", _i32),
                 ("rope_theta", _f32), ("rms_eps", _f32), ("seed", _u64), ("lm_scale", _f32),
-                ("router_scale", _f32)]
+                ("router_scale", _f32), ("shared_inter", _i32)]
 
 
 class EngineOptions(C.Structure):

@@ -20,6 +20,7 @@
 //  * HBM-bound: algorithmic bytes = 2*b*(s+n)*n_kv*d*2 (roofline.hpp:88) +
 //    Q/O; FLOPs = 4*n*(s+n)*n_q*d per request.
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -398,6 +399,357 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
+// ---------------------------------------------------------------------------
+// K1 v3 ("swap-AB"), used when the g*n query rows of a KV head fit in 64:
+// S^T = K Q^T puts the 128 keys of a chunk on the TMEM lanes and the query
+// rows on the columns, so each of the 128 softmax threads owns ONE key and
+// does NP=64 exps per chunk (v2: one row, 128 exps, mostly one busy warp).
+//   * P^T [keys][rows] is written by its key-thread as one 128-byte swizzled
+//     row (MN-major B operand); O^T [d][rows] = V^T P^T with V^T the MN-major
+//     A operand (V's natural layout); l[rows] = ones . P^T on the tensor core
+//     (a 256-byte all-ones A tile, SBO = 0) so no cross-thread row sums.
+//   * row maxima are kept per row and only refreshed (cross-thread reduce +
+//     O/l rescale in TMEM) when some score exceeds max + 8 in log2 units —
+//     always at an item's first chunk, rarely afterwards; p stays <= 2^8.
+namespace v3 {
+constexpr int kNP = 64;  // query rows per item (padded)
+
+template <int D>
+struct Smem {
+  static constexpr int kKBlocks = D / 64;
+  static constexpr int kQBytes = kKBlocks * 16384;
+  static constexpr int kKvBytes = kKBlocks * 16384;
+  static constexpr int kQOff = 0;
+  static constexpr int kKvOff = kQBytes;
+  static constexpr int kPOff = kKvOff + kKvStages * 2 * kKvBytes;  // P^T hi, then lo: [128 keys][64 rows]
+  static constexpr int kPPlane = 16384;
+  static constexpr int kOnesOff = kPOff + 2 * kPPlane;
+  static constexpr int kTotal = kOnesOff + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv_k,
+           const __grid_constant__ CUtensorMap tm_kv_v, AttnParams p) {
+  using L = Smem<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t q_full, q_empty;
+  __shared__ __align__(8) uint64_t kv_full[kKvStages], kv_empty[kKvStages];
+  __shared__ __align__(8) uint64_t s_full[2], s_empty[2], o_full, p_full;
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ float red_sh[4][kNP];
+  __shared__ float alpha_sh[kNP];
+  __shared__ float m_sh[kNP];  // per-row running max (log2 units)
+  __shared__ uint64_t vis_sh[64];  // draft key j -> rows that see it
+  __shared__ uint64_t mrow_sh[64]; // compact mask word of draft query i
+  __shared__ int flag_sh[4];
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == 0 && lane == 0) {
+    mbar_init(&q_full, 1);
+    mbar_init(&q_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 4);
+    }
+    for (int i = 0; i < kKvStages; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    mbar_init(&o_full, 1);
+    mbar_init(&p_full, 4);
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_kv_k);
+    tma_prefetch_desc(&tm_kv_v);
+  }
+  if (warp == 1) tmem_alloc<256>(&tmem_base_sh);
+  if (warp >= 2) {  // all-ones A tile for the row-sum MMA (bf16 1.0)
+    for (int i = threadIdx.x - 64; i < 64; i += 128) reinterpret_cast<uint32_t*>(smem + L::kOnesOff)[i] = 0x3F803F80u;
+    fence_proxy_async();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  constexpr uint32_t kS = 0, kO = 2 * kNP, kL = 3 * kNP;  // TMEM columns
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int used = 0, gc = 0;
+      for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+        const ItemInfo it = item_info(p, item);
+        if (it.c_end <= it.c_begin) continue;
+        mbar_wait(&q_empty, (used & 1) ^ 1);
+        ++used;
+        mbar_arrive_expect_tx(&q_full, uint32_t(L::kKBlocks * 64 * p.g * p.n * 2));
+        for (int kb = 0; kb < L::kKBlocks; ++kb)
+          tma_load_3d(smem + L::kQOff + kb * 16384, &tm_q, &q_full, kb * 64, it.h * p.g, it.r * p.n);
+        const int row_base = (it.r * p.n_kv + it.h) * p.s_max;
+        for (int c = it.c_begin; c < it.c_end; ++c, ++gc) {
+          const int s = gc % kKvStages;
+          TR(0, 1);
+          mbar_wait(&kv_empty[s], ((gc / kKvStages) & 1) ^ 1);
+          TR(0, 2);
+          mbar_arrive_expect_tx(&kv_full[s], uint32_t(2 * L::kKvBytes));
+          uint8_t* kdst = smem + L::kKvOff + s * 2 * L::kKvBytes;
+          uint8_t* vdst = kdst + L::kKvBytes;
+          for (int kb = 0; kb < L::kKBlocks; ++kb) {
+            tma_load_2d(kdst + kb * 16384, &tm_kv_k, &kv_full[s], kb * 64, row_base + c * kChunk);
+            tma_load_2d(vdst + kb * 16384, &tm_kv_v, &kv_full[s], kb * 64, row_base + c * kChunk);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      const uint32_t id_s = make_idesc_bf16(128, kNP);                      // K (keys) x Q^T
+      const uint32_t id_o = make_idesc_bf16(128, kNP, /*b_mn=*/1, /*a_mn=*/1);  // V^T x P^T
+      const uint32_t id_l = make_idesc_bf16(128, kNP, /*b_mn=*/1, /*a_mn=*/0);  // ones x P^T
+      const uint32_t q_addr = smem_u32(smem + L::kQOff);
+      const uint32_t p_addr = smem_u32(smem + L::kPOff);
+      // all-ones A: no swizzle, K core matrices 128 B apart, every 8-row group
+      // aliases the same 256 bytes (SBO = 0)
+      uint64_t ones_d = uint64_t((smem_u32(smem + L::kOnesOff) >> 4) & 0x3FFFu) | (uint64_t(128 >> 4) << 16) |
+                        (uint64_t(1) << 46);
+      int used = 0, gc = 0;
+      uint32_t p_phase = 0;
+      for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+        const ItemInfo it = item_info(p, item);
+        if (it.c_end <= it.c_begin) continue;
+        mbar_wait(&q_full, used & 1);
+        ++used;
+        const int nch = it.c_end - it.c_begin;
+        auto issue_s = [&](int ci) {
+          const int g2 = gc + ci;
+          const int s = g2 % kKvStages, sb = g2 & 1;
+          TR(1, 1);
+          mbar_wait(&kv_full[s], (g2 / kKvStages) & 1);
+          mbar_wait(&s_empty[sb], ((g2 >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t k_addr = smem_u32(smem + L::kKvOff + s * 2 * L::kKvBytes);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk / 4) * 16384 + (kk % 4) * 32;
+            umma_bf16(tmem + kS + sb * kNP, make_sdesc_sw128(k_addr + off, 16, 1024),
+                      make_sdesc_sw128(q_addr + off, 16, 1024), id_s, kk > 0 ? 1u : 0u);
+          }
+          umma_commit(&s_full[sb]);
+          if (ci == nch - 1) umma_commit(&q_empty);
+          TR(1, 2);
+        };
+        issue_s(0);
+        for (int ci = 0; ci < nch; ++ci) {
+          if (ci + 1 < nch) issue_s(ci + 1);
+          const int g2 = gc + ci;
+          const int s = g2 % kKvStages;
+          TR(1, 4);
+          mbar_wait(&p_full, p_phase);
+          TR(1, 5);
+          p_phase ^= 1;
+          tc_fence_after();
+          const uint32_t v_addr = smem_u32(smem + L::kKvOff + s * 2 * L::kKvBytes + L::kKvBytes);
+#pragma unroll
+          for (int kk = 0; kk < kChunk / 16; ++kk) {
+            const uint64_t vd = make_sdesc_sw128(v_addr + kk * 2048, 16384, 1024);
+            const uint64_t ph = make_sdesc_sw128(p_addr + kk * 2048, 16384, 1024);
+            const uint64_t pl = make_sdesc_sw128(p_addr + L::kPPlane + kk * 2048, 16384, 1024);
+            const uint32_t acc = (ci > 0 || kk > 0) ? 1u : 0u;
+            umma_bf16(tmem + kO, vd, ph, id_o, acc);
+            umma_bf16(tmem + kO, vd, pl, id_o, 1u);
+            umma_bf16(tmem + kL, ones_d, ph, id_l, acc);
+            umma_bf16(tmem + kL, ones_d, pl, id_l, 1u);
+          }
+          umma_commit(&o_full);
+          umma_commit(&kv_empty[s]);
+          TR(1, 6);
+        }
+        gc += nch;
+      }
+    }
+  } else {
+    // ---------------------------------------------- softmax: thread = key lane
+    const int q4 = warp & 3;
+    const int kt = q4 * 32 + lane;                 // key within the chunk (TMEM lane)
+    const uint32_t tl = uint32_t(q4 * 32) << 16;
+    const int st = threadIdx.x - 64;               // 0..127
+    uint8_t* pbuf = smem + L::kPOff;
+    int gc = 0;
+    for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+      const ItemInfo it = item_info(p, item);
+      const int nch = it.c_end - it.c_begin;
+      const int prefix = it.keys - p.n;
+      // draft visibility per draft key j: rows (i*g+hh) whose query i sees j
+      if (st < p.n) mrow_sh[st] = p.mask[it.r * p.n + st];
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      if (st < 64) {
+        uint64_t rows = 0;
+        if (st < p.n)
+          for (int r = 0; r < p.rows; ++r)
+            if ((mrow_sh[r / p.g] >> st) & 1ull) rows |= 1ull << r;
+        vis_sh[st] = rows;
+      }
+      const uint64_t live_rows = p.rows >= 64 ? ~0ull : ((1ull << p.rows) - 1ull);
+      if (st < kNP) m_sh[st] = -INFINITY;
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      if (st == 0) TR(2, 8);
+      for (int ci = 0; ci < nch; ++ci) {
+        const int g2 = gc + ci;
+        const int sb = g2 & 1;
+        const int key = (it.c_begin + ci) * kChunk + kt;
+        const uint64_t vis = key < prefix ? live_rows : (key < it.keys ? vis_sh[key - prefix] & live_rows : 0ull);
+        if (st == 0) TR(2, 1);
+        mbar_wait(&s_full[sb], (g2 >> 1) & 1);
+        if (st == 0) TR(2, 2);
+        tc_fence_after();
+        uint32_t sr[kNP];
+        {
+          uint32_t a[32], b[32];
+          tmem_ld32(tmem + tl + kS + sb * kNP, a);
+          tmem_ld32(tmem + tl + kS + sb * kNP + 32, b);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            sr[j] = __float_as_uint(__uint_as_float(a[j]) * p.scale_log2);
+            sr[j + 32] = __float_as_uint(__uint_as_float(b[j]) * p.scale_log2);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[sb]);
+        // does any visible score exceed its row max by more than 2^8?
+        bool grow = false;
+#pragma unroll
+        for (int j = 0; j < kNP; ++j) grow |= ((vis >> j) & 1ull) && (__uint_as_float(sr[j]) > m_sh[j] + 8.f);
+        grow = __any_sync(0xffffffffu, grow);
+        if (lane == 0) flag_sh[q4] = grow ? 1 : 0;
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        const bool any_grow = (flag_sh[0] | flag_sh[1] | flag_sh[2] | flag_sh[3]) != 0;
+        if (st == 0) TR(2, any_grow ? 9 : 3);
+        if (any_grow) {
+          // exact per-row max of this chunk over the 128 keys: warp max, then 4 warps
+#pragma unroll
+          for (int j = 0; j < kNP; ++j) {
+            const float v = warp_max(((vis >> j) & 1ull) ? __uint_as_float(sr[j]) : -INFINITY);
+            if (lane == 0) red_sh[q4][j] = v;
+          }
+          asm volatile("bar.sync 2, 128;" ::: "memory");
+          if (st < kNP) {
+            // per-row decision (a row's reference max depends only on its own
+            // scores, which keeps causality bit-exact): refresh only rows that
+            // are unset or grew past max + 8
+            const int j = st;
+            const float cm = fmaxf(fmaxf(red_sh[0][j], red_sh[1][j]), fmaxf(red_sh[2][j], red_sh[3][j]));
+            const float mo = m_sh[j];
+            const bool refresh = cm != -INFINITY && (mo == -INFINITY || cm > mo + 8.f);
+            const float mn = refresh ? cm : mo;
+            alpha_sh[j] = refresh ? (mo == -INFINITY ? 0.f : ex2_approx(mo - mn)) : 1.f;
+            m_sh[j] = mn;
+          }
+          asm volatile("bar.sync 2, 128;" ::: "memory");  // m_sh/alpha_sh visible, red_sh reusable
+        }
+        // previous PV must be done before P is overwritten / O rescaled
+        if (ci > 0) {
+          mbar_wait(&o_full, (g2 - 1) & 1);
+          tc_fence_after();
+          if (any_grow) {  // O^T[d][row] and l[row] *= alpha[row]
+#pragma unroll 1
+            for (int part = 0; part < 2; ++part) {
+              const uint32_t col = part == 0 ? kO : kL;
+#pragma unroll
+              for (int h2 = 0; h2 < 2; ++h2) {
+                uint32_t r[32];
+                tmem_ld32(tmem + tl + col + h2 * 32, r);
+                tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * alpha_sh[h2 * 32 + j]);
+                tmem_st32(tmem + tl + col + h2 * 32, r);
+              }
+            }
+            tmem_st_wait();
+          }
+        }
+        if (st == 0) TR(2, 4);
+        // p = 2^(s - m) for visible (key,row) pairs; P^T row `kt` as hi + lo bf16
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          uint32_t hi4[4], lo4[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int j = c * 8 + t * 2;
+            const float a = ((vis >> j) & 1ull) ? ex2_approx(__uint_as_float(sr[j]) - m_sh[j]) : 0.f;
+            const float b = ((vis >> (j + 1)) & 1ull) ? ex2_approx(__uint_as_float(sr[j + 1]) - m_sh[j + 1]) : 0.f;
+            const uint32_t hh = pack_bf16x2(a, b);
+            hi4[t] = hh;
+            lo4[t] = pack_bf16x2(a - __uint_as_float(hh << 16), b - __uint_as_float(hh & 0xffff0000u));
+          }
+          const int off = kt * 128 + ((c ^ (kt & 7)) * 16);
+          *reinterpret_cast<uint4*>(pbuf + off) = make_uint4(hi4[0], hi4[1], hi4[2], hi4[3]);
+          *reinterpret_cast<uint4*>(pbuf + L::kPPlane + off) = make_uint4(lo4[0], lo4[1], lo4[2], lo4[3]);
+        }
+        // keys past the request's end: zero their V rows (stale cache contents)
+        if (key >= it.keys) {
+          uint8_t* vbuf = smem + L::kKvOff + (g2 % kKvStages) * 2 * L::kKvBytes + L::kKvBytes;
+#pragma unroll
+          for (int kb = 0; kb < L::kKBlocks; ++kb)
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+              *reinterpret_cast<uint4*>(vbuf + kb * 16384 + kt * 128 + t * 16) = make_uint4(0, 0, 0, 0);
+        }
+        fence_proxy_async();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full);
+        if (st == 0) TR(2, 5);
+      }
+      if (nch > 0) {
+        mbar_wait(&o_full, (gc + nch - 1) & 1);
+        tc_fence_after();
+      }
+      if (st == 0) TR(2, 6);
+      gc += nch;
+      // epilogue: thread = d lane; l from the ones-MMA (identical on every lane)
+      if (kt < D) {
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          uint32_t lr[32], o[32];
+          if (nch > 0) {
+            tmem_ld32(tmem + tl + kL + h2 * 32, lr);
+            tmem_ld32(tmem + tl + kO + h2 * 32, o);
+            tmem_ld_wait();
+            if (st == 0) TR(2, 10 + h2);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) lr[j] = o[j] = 0u;
+          }
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) {
+            const int j = h2 * 32 + jj;
+            if (j >= p.rows) continue;
+            const float l = __uint_as_float(lr[jj]);
+            const int qi = j / p.g, hh = j % p.g;
+            if (p.splits == 1) {
+              p.out[((size_t(it.r) * p.n + qi) * p.n_q + size_t(it.h) * p.g + hh) * D + kt] =
+                  f2bf(l > 0.f ? __uint_as_float(o[jj]) / l : 0.f);
+            } else {
+              p.ws_o[(size_t(item) * p.rows + j) * D + kt] = __uint_as_float(o[jj]);
+              if (kt == 0) p.ws_ml[size_t(item) * p.rows + j] = make_float2(nch > 0 ? m_sh[j] : -INFINITY, l);
+            }
+          }
+        }
+      }
+      if (st == 0) TR(2, 7);
+      tc_fence_before();
+      asm volatile("bar.sync 2, 128;" ::: "memory");  // TMEM O/l read before the next item's PV(0)
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<256>(tmem);
+}
+}  // namespace v3
+
 // Merge the split-KV partials: O = sum_s O_s 2^(m_s - M) / sum_s l_s 2^(m_s - M).
 template <int D>
 __global__ void attn_combine_kernel(AttnParams p) {
@@ -465,6 +817,16 @@ int device_sms() {
   return sms;
 }
 
+// K1 variant for rows <= 64: 2 = row-per-thread (default), 3 = swap-AB
+// key-per-thread; SMO_ATTN_VARIANT overrides (read once)
+int attn_variant() {
+  static int v = [] {
+    const char* e = std::getenv("SMO_ATTN_VARIANT");
+    return e && std::atoi(e) == 3 ? 3 : 2;
+  }();
+  return v;
+}
+
 void check_attn_args(const smo_attn_args& a) {
   SMO_REQUIRE(a.q && a.k_cache && a.v_cache && a.mask && a.prefix_len && a.out, "attention: null pointer");
   SMO_REQUIRE(a.b > 0 && a.n > 0 && a.n_q > 0 && a.n_kv > 0, "attention: shape mismatch");
@@ -521,7 +883,25 @@ void attention_launch(const smo_attn_args& a, cudaStream_t stream) {
     make_tmap_bf16(&tk, a.k_cache, 2, dims, strides, box, true);
     make_tmap_bf16(&tv, a.v_cache, 2, dims, strides, box, true);
   }
-  if (a.d == 128) {
+  if (p.rows <= v3::kNP && attn_variant() == 3) {
+    if (a.d == 128) {
+      constexpr size_t smem = v3::Smem<128>::kTotal + 1024;
+      static bool set = false;
+      if (!set) {
+        SMO_CUDA_CHECK(cudaFuncSetAttribute(v3::kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        set = true;
+      }
+      v3::kernel<128><<<pl.grid, kThreads, smem, stream>>>(tq, tk, tv, p);
+    } else {
+      constexpr size_t smem = v3::Smem<64>::kTotal + 1024;
+      static bool set = false;
+      if (!set) {
+        SMO_CUDA_CHECK(cudaFuncSetAttribute(v3::kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        set = true;
+      }
+      v3::kernel<64><<<pl.grid, kThreads, smem, stream>>>(tq, tk, tv, p);
+    }
+  } else if (a.d == 128) {
     constexpr size_t smem = AttnSmem<128>::kTotal + 1024;
     static bool set = false;
     if (!set) {

@@ -67,7 +67,7 @@ void ep_pack_back(const float* yl, const int32_t* back, const int32_t* offsets_l
 namespace tid {
 constexpr uint64_t kEmbed = 1, kLmHead = 2;
 inline uint64_t layer(int l) { return 1000ull * uint64_t(l + 1); }
-constexpr uint64_t kWqkv = 1, kWo = 2, kRouter = 4, kExpert = 100;
+constexpr uint64_t kWqkv = 1, kWo = 2, kRouter = 4, kShared = 50, kExpert = 100;
 inline uint64_t kv(int l, int which) { return 900000ull + 2ull * uint64_t(l) + uint64_t(which); }
 }  // namespace tid
 
@@ -89,6 +89,7 @@ struct Engine {
   uint16_t *embed_w = nullptr, *lm_w = nullptr, *final_norm = nullptr, *ones = nullptr;
   struct Layer {
     uint16_t *wqkv, *wo, *router;
+    uint16_t *ws1 = nullptr, *ws3 = nullptr, *ws2 = nullptr;  // shared expert (resident)
     uint16_t *kc, *vc;
   };
   std::vector<Layer> layers;
@@ -116,6 +117,7 @@ struct Engine {
   int maxT = 0, maxB = 0, maxN = 0, s_max = 0;
   float *x = nullptr, *ybuf = nullptr, *rw = nullptr, *amax_v = nullptr;
   uint16_t *xn = nullptr, *qkv = nullptr, *q = nullptr, *attn = nullptr, *xp = nullptr, *hbuf = nullptr;
+  uint16_t* hs = nullptr;  // shared-expert SwiGLU activations [T, shared_inter]
   int32_t *ids = nullptr, *offsets = nullptr, *perm = nullptr, *pos = nullptr, *amax_i = nullptr, *target = nullptr;
   int32_t *d_tokens = nullptr, *d_parent = nullptr, *d_prefix = nullptr, *d_acc = nullptr, *d_bonus = nullptr,
           *d_keep = nullptr;
@@ -177,6 +179,7 @@ struct Engine {
     SMO_REQUIRE(h > 0 && hi > 0 && E > 0 && K > 0 && K <= E && L > 0, "engine: bad model shape");
     SMO_REQUIRE(nq > 0 && nkv > 0 && nq % nkv == 0 && (d == 64 || d == 128), "engine: bad attention shape");
     SMO_REQUIRE(h % 256 == 0 && hi % 128 == 0 && V % 128 == 0 && (nq * d) % 128 == 0, "engine: unsupported dims");
+    SMO_REQUIRE(cfg.shared_inter >= 0 && cfg.shared_inter % 128 == 0, "engine: shared_inter must be a multiple of 128");
     SMO_REQUIRE(opt.max_batch > 0 && opt.max_verify > 0 && opt.max_verify <= 64, "engine: bad batch options");
     // expert parallelism whenever a transport is given (ep_size 1 with a
     // 1-rank group runs the full dispatch/combine path: a 1-GPU check of it)
@@ -231,6 +234,15 @@ struct Engine {
                    st);
       fill_uniform(ly.router, size_t(E) * h, cfg.seed, tid::layer(l) + tid::kRouter, 0,
                    std::sqrt(3.0f / h) * cfg.router_scale, st);
+      if (cfg.shared_inter > 0) {
+        const size_t n = size_t(cfg.shared_inter) * h;
+        ly.ws1 = dalloc<uint16_t>(n);
+        ly.ws3 = dalloc<uint16_t>(n);
+        ly.ws2 = dalloc<uint16_t>(n);
+        fill_uniform(ly.ws1, n, cfg.seed, tid::layer(l) + tid::kShared + 0, 0, std::sqrt(3.0f / h), st);
+        fill_uniform(ly.ws3, n, cfg.seed, tid::layer(l) + tid::kShared + 1, 0, std::sqrt(3.0f / h), st);
+        fill_uniform(ly.ws2, n, cfg.seed, tid::layer(l) + tid::kShared + 2, 0, std::sqrt(3.0f / cfg.shared_inter), st);
+      }
     }
 
     // experts: generate each block on the device, stage to pinned host DRAM
@@ -308,6 +320,7 @@ struct Engine {
     perm = dalloc<int32_t>(P);
     pos = dalloc<int32_t>(P);
     xp = dalloc<uint16_t>(size_t(P) * h);
+    if (cfg.shared_inter > 0) hs = dalloc<uint16_t>(size_t(maxT) * cfg.shared_inter);
     if (ep_on) {
       // fixed capacity per destination: every local (token, slot) pair could
       // target one owner; identical on all ranks (same options)
@@ -624,6 +637,39 @@ struct Engine {
       snap("weights", l, rw, size_t(PT) * 4, st);
       snap("offsets", l, offsets, size_t(E + 1) * 4, st);
       snap("pos", l, pos, size_t(PT) * 4, st);
+      if (cfg.shared_inter > 0) {
+        // always-on shared expert (config 4): x += SwiGLU_shared(xn2); its
+        // weights are resident, so it runs before the wait for streamed experts
+        smo_gemm_args gs{};
+        gs.x = xn;
+        gs.rows = T;
+        gs.K = h;
+        gs.N = cfg.shared_inter;
+        gs.groups = 1;
+        gs.max_rows_per_group = T;
+        gs.w = ly.ws1;
+        gs.w_up = ly.ws3;
+        gs.w_pool_blocks = 1;
+        gs.epilogue = SMO_EPI_SWIGLU;
+        gs.out = hs;
+        gs.ldo = cfg.shared_inter;
+        gemm_launch(gs, st);
+        gs = smo_gemm_args{};
+        gs.x = hs;
+        gs.rows = T;
+        gs.K = cfg.shared_inter;
+        gs.N = h;
+        gs.groups = 1;
+        gs.max_rows_per_group = T;
+        gs.w = ly.ws2;
+        gs.w_pool_blocks = 1;
+        gs.epilogue = SMO_EPI_F32_ADD;
+        gs.out = x;
+        gs.ldo = h;
+        gs.workspace = gemm_ws;
+        gs.workspace_bytes = gemm_ws_bytes;
+        gemm_launch(gs, st);
+      }
       // ---- MoE: wait for this layer's experts
       if (ep_on) {
         moe_ep(l, T, st);

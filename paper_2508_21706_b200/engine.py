@@ -35,6 +35,7 @@ class ModelShape:
     seed: int = 0x5EED
     lm_scale: float = 1.0
     router_scale: float = 1.0
+    shared_inter: int = 0  # always-on shared expert (config 4), resident in HBM
 
     @property
     def expert_bytes(self) -> int:
@@ -43,7 +44,7 @@ class ModelShape:
     def to_c(self) -> L.ModelConfig:
         return L.ModelConfig(self.hidden, self.inter, self.n_expert, self.top_k, self.n_layers, self.n_q_heads,
                              self.n_kv_heads, self.head_dim, self.vocab, self.rope_theta, self.rms_eps, self.seed,
-                             self.lm_scale, self.router_scale)
+                             self.lm_scale, self.router_scale, self.shared_inter)
 
 
 # BASELINE.json configs
@@ -53,6 +54,14 @@ MIXTRAL_8X7B = ModelShape(hidden=4096, inter=14336, n_expert=8, top_k=2, n_layer
                           n_kv_heads=8, head_dim=128, vocab=32000)
 MIXTRAL_8X22B = ModelShape(hidden=6144, inter=16384, n_expert=8, top_k=2, n_layers=56, n_q_heads=48,
                            n_kv_heads=8, head_dim=128, vocab=32000)
+# BASELINE config 4: DeepSeek-V2-Lite-shaped fine-grained MoE (64 routed experts
+# top-6 + 2 shared experts of 1408 = one shared SwiGLU of 2816); GQA stands in
+# for MLA (not in the reference model).
+DSV2_LITE = ModelShape(hidden=2048, inter=1408, n_expert=64, top_k=6, n_layers=26, n_q_heads=16, n_kv_heads=4,
+                       head_dim=128, vocab=102400, shared_inter=2816)
+# Qwen2-57B-A14B-shaped: 64 experts top-8 + shared expert 20480
+QWEN2_57B = ModelShape(hidden=3584, inter=2560, n_expert=64, top_k=8, n_layers=28, n_q_heads=28, n_kv_heads=4,
+                       head_dim=128, vocab=151552, shared_inter=20480)
 
 
 class EpGroup:

@@ -59,6 +59,17 @@ class OracleModel:
         return self._fill(s.n_expert * s.hidden, tid_layer(l) + 4,
                           math.sqrt(3.0 / s.hidden) * s.router_scale).reshape(s.n_expert, s.hidden)
 
+    def shared(self, l):
+        s = self.s
+        if not getattr(s, "shared_inter", 0):
+            return None
+        h, si = s.hidden, s.shared_inter
+        base = tid_layer(l) + 50
+        w1 = self._fill(si * h, base, math.sqrt(3.0 / h)).reshape(si, h)
+        w3 = self._fill(si * h, base + 1, math.sqrt(3.0 / h)).reshape(si, h)
+        w2 = self._fill(h * si, base + 2, math.sqrt(3.0 / si)).reshape(h, si)
+        return w1, w3, w2
+
     def expert(self, l, e):
         s = self.s
         a = l % self.alias
@@ -212,6 +223,12 @@ class OracleModel:
         lg = self.router_logits(xn2, l)
         ids, w = self.topk(lg)
         off, perm, pos_p = self.permute(ids)
+        sh = self.shared(l)
+        if sh is not None:  # x += shared SwiGLU (fp32), before the routed sum
+            Ysh = np.zeros((T, s.hidden), np.float32)
+            O.lib().orc_expert_swiglu(O._ptr(np.ascontiguousarray(xn2)), T, s.hidden, s.shared_inter, O._ptr(sh[0]),
+                                      O._ptr(sh[1]), O._ptr(sh[2]), O._ptr(Ysh))
+            x = (x + Ysh).astype(np.float32)
         y = self.moe(xn2, l, ids, w)
         x_out = (x.astype(np.float64) + y).astype(np.float32)
         return x_out, dict(xn1=xn1, q=q, attn=attn, xn2=xn2, logits_r=lg, ids=ids, weights=w, offsets=off,

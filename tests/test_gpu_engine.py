@@ -21,17 +21,20 @@ B, K_DRAFT, PREFIX = 4, 4, 1024
 N = K_DRAFT + 1
 
 
-def _shape(seed=0x5EED + 1):
+def _shape(kind="tiny", seed=0x5EED + 1):
     from paper_2508_21706_b200.engine import TINY
     # LM-head scale raised so top-1 margins clear the bf16 noise
-    return dataclasses.replace(TINY, seed=seed, lm_scale=8.0, router_scale=4.0)
+    s = dataclasses.replace(TINY, seed=seed, lm_scale=8.0, router_scale=4.0)
+    if kind == "tiny_fg":  # config-4 features at tiny size: 16 experts top-4 + shared expert
+        s = dataclasses.replace(s, n_expert=16, top_k=4, shared_inter=512)
+    return s
 
 
-@pytest.fixture(scope="module")
-def setup(cuda):
+@pytest.fixture(scope="module", params=["tiny", "tiny_fg"])
+def setup(cuda, request):
     from paper_2508_21706_b200.engine import VerifyEngine
     import oracle_model
-    shape = _shape()
+    shape = _shape(request.param)
     s_max = PREFIX + N + 64
     eng = VerifyEngine(shape, max_batch=B, max_verify=N, max_seq=s_max, debug=True)
     prefix = np.array([PREFIX, PREFIX - 7, 300, 1], np.int32)
@@ -100,6 +103,9 @@ def test_engine_teacher_forced_stage_parity(setup, oracle):
         # experts + combine
         x_out = eng.debug_tensor("x_out", l, (T, s.hidden), np.float32)
         x_mid_gpu_equiv = x_mid  # O-proj parity already covered through xn2
+        sh = om.shared(l)
+        if sh is not None:  # always-on shared expert (config 4)
+            x_mid_gpu_equiv = x_mid + om.gemm(oracle.f32_to_bf16(_swiglu(om, xn2, sh)), sh[2])
         ref_out = x_mid_gpu_equiv + om.moe(xn2, l, ids, wts)
         _close(x_out, ref_out, 1e-2, f"L{l} moe+combine")
     # head
@@ -115,6 +121,12 @@ def test_engine_teacher_forced_stage_parity(setup, oracle):
                                    oracle._ptr(acc), oracle._ptr(bonus), oracle._ptr(keep))
     assert np.array_equal(res.acc_len, acc) and np.array_equal(res.bonus, bonus)
     assert np.array_equal(res.keep.ravel(), keep)
+
+
+def _swiglu(om, xn, w):
+    g = om.gemm(xn, w[0]).astype(np.float64)
+    u = om.gemm(xn, w[1]).astype(np.float64)
+    return (g / (1.0 + np.exp(-g)) * u).astype(np.float32)
 
 
 def _oracle_step(om, tokens, prefix, s_max):
