@@ -8,15 +8,18 @@
 //
 // Layout / mapping:
 //  * work item = (request r, KV head h, KV split); persistent CTAs stride over
-//    items. The g*n query rows sharing KV head h (row = i*g + hh) form the
-//    M=128 A tile (Q, K-major, TMA 3D box {64, g, n}); a 128-key chunk of K is
-//    the B operand of S = Q K^T (N=128); P (bf16, written by the softmax warps
-//    into a swizzled K-major smem tile) times V (MN-major B, N=d) gives the
-//    chunk's O contribution in TMEM, folded into fp32 registers with the
-//    online-softmax rescale.
-//  * warps: w0 TMA producer, w1 TMEM alloc + MMA issuer, w2..w5 softmax
-//    (thread = query row = TMEM lane).
-//  * TMEM: S double buffer cols [0,256), O-chunk double buffer cols [256,512).
+//    items. The g*n query rows sharing KV head h (row = i*g + hh) are loaded
+//    R = 128/(rows rounded up to 32/64/128) times into the M=128 Q tile (TMA
+//    3D box {64, g, n}); a 128-key chunk of K is the B operand of
+//    S = Q K^T (N=128) and replica k owns keys [k*128/R, (k+1)*128/R) of
+//    each chunk. P (hi + lo bf16 planes) is written over its S buffer in TMEM
+//    and O += P V reads A from TMEM, B = V (MN-major) from shared memory.
+//  * warps: w0 TMA producer, w1 TMEM alloc + MMA issuer, w2..w9 softmax (two
+//    warps per TMEM lane quadrant, each owning half of its replica's keys).
+//  * TMEM: S/P double buffer cols [0,256), O accumulator [256, 256+D).
+//  * shared memory: Q tile(s) + kStages K/V chunk stages (224 KB); the K tile
+//    of a consumed chunk doubles as the pair max-exchange buffer and the last
+//    chunk's stage as the epilogue's replica-merge scratch.
 //  * HBM-bound: algorithmic bytes = 2*b*(s+n)*n_kv*d*2 (roofline.hpp:88) +
 //    Q/O; FLOPs = 4*n*(s+n)*n_q*d per request.
 #include <cmath>
@@ -29,9 +32,9 @@ namespace smo {
 
 namespace {
 
-constexpr int kThreads = 192;
+constexpr int kSoftWarps = 8;                 // two per TMEM lane quadrant
+constexpr int kThreads = 64 + 32 * kSoftWarps;  // + TMA producer + MMA issuer
 constexpr int kChunk = 128;
-constexpr int kKvStages = 2;
 
 struct AttnParams {
   const uint64_t* mask;
@@ -49,14 +52,11 @@ struct AttnSmem {
   static constexpr int kKBlocks = D / 64;
   static constexpr int kQBytes = kKBlocks * 16384;      // 128 rows x D
   static constexpr int kKvBytes = kKBlocks * 16384;     // 128 keys x D (K or V)
-  static constexpr int kPBytes = 2 * 16384;             // 128 rows x 128 keys (bf16)
-  // d=128 keeps one Q buffer so that P can be held as hi+lo bf16 planes
   static constexpr int kQBufs = D == 128 ? 1 : 2;
+  static constexpr int kStages = D == 128 ? 3 : 6;      // K/V chunk stages in flight
   static constexpr int kQOff = 0;
   static constexpr int kKvOff = kQBufs * kQBytes;
-  static constexpr int kPOff = kKvOff + kKvStages * 2 * kKvBytes;
-  static constexpr int kPLoOff = kPOff + kPBytes;
-  static constexpr int kTotal = kPLoOff + kPBytes;
+  static constexpr int kTotal = kKvOff + kStages * 2 * kKvBytes;  // 224 KB
 };
 
 #ifdef SMO_ATTN_TRACE
@@ -105,16 +105,62 @@ __device__ __forceinline__ uint32_t visible_bits(int p0, int prefix, uint64_t mb
   return pm | dm;
 }
 
-template <int D>
+// Load this thread's C consecutive S columns (C = 16, 32 or 64) from TMEM.
+template <int C>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[C]) {
+  if constexpr (C == 16) {
+    tmem_ld16(taddr, r);
+  } else {
+#pragma unroll
+    for (int c = 0; c < C; c += 32) tmem_ld32(taddr + c, *reinterpret_cast<uint32_t(*)[32]>(&r[c]));
+  }
+}
+// Store C/2 packed bf16x2 P columns (C = 16, 32 or 64 keys) to TMEM.
+template <int C>
+__device__ __forceinline__ void tmem_st_pcols(uint32_t taddr, const uint32_t (&r)[C / 2]) {
+  if constexpr (C == 16) tmem_st8(taddr, r);
+  else if constexpr (C == 32) tmem_st16(taddr, r);
+  else tmem_st32(taddr, r);
+}
+
+// K1 main kernel. Template R = query-row replication: the g*n rows of a KV
+// head are loaded R times into the 128-row Q tile (replica k at TMEM lanes
+// [k*128/R, (k+1)*128/R)), and replica k owns key columns [k*128/R,
+// (k+1)*128/R) of every chunk. Two softmax warps share each TMEM lane
+// quadrant and split the replica's columns, so a softmax thread handles
+// kCols = 64/R keys per chunk instead of 128 — all 8 softmax warps busy even
+// for the 36 rows of a Mixtral verify. Each (lane, warp
+// pair) runs its own online softmax over its key subset; the R replicas are
+// merged exactly in the epilogue like split-KV partials.
+//  * P never touches shared memory: it is written (hi + lo bf16 planes) over
+//    its own S buffer in TMEM and PV reads its A operand from there, so P is
+//    double-buffered with S and the shared memory holds kStages K/V chunks.
+//  * lazy rescale: a lane's reference max only moves when a score exceeds it
+//    by more than 2^8; otherwise P(c+1) is produced without waiting for
+//    PV(c), and only lanes whose reference moved rescale O in TMEM.
+template <int D, int R>
 __global__ void __launch_bounds__(kThreads, 1)
     verify_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv_k,
                             const __grid_constant__ CUtensorMap tm_kv_v, AttnParams p) {
   using L = AttnSmem<D>;
+  constexpr int kStages = L::kStages;
+  constexpr int kLanes = 128 / R;         // TMEM lanes per replica
+  constexpr int kW = kChunk / R;          // key columns per replica
+  constexpr int kCols = kW / 2;           // key columns per softmax thread per chunk
+  constexpr int kOCols = D / 2;           // O columns per softmax thread (rescale / epilogue)
+  // TMEM columns: S/P buffer b at [128b, 128b+128) (P hi = first 64 columns,
+  // P lo = next 64, two bf16 per column), O at [256, 256+D)
+  constexpr uint32_t kOAcc = 256;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align within the shared array (keeps the shared address space visible to
+  // the compiler: LDS/STS instead of generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ __align__(8) uint64_t q_full[2], q_empty[2];
-  __shared__ __align__(8) uint64_t kv_full[kKvStages], kv_empty[kKvStages];
-  __shared__ __align__(8) uint64_t s_full[2], s_empty[2], o_full, p_full;
+  __shared__ __align__(8) uint64_t kv_full[kStages], kv_empty[kStages];
+  // o_full: one phase per PV (chunk); o_last: one phase per item (its last
+  // PV). Softmax warps skip o_full phases (lazy rescale), so the epilogue
+  // waits on o_last, which every warp observes once per item.
+  __shared__ __align__(8) uint64_t s_full[2], s_empty[2], o_full, o_last, p_full;
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -123,14 +169,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4);
+      mbar_init(&s_empty[i], 1);
     }
-    for (int i = 0; i < kKvStages; ++i) {
+    for (int i = 0; i < kStages; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
     mbar_init(&o_full, 1);
-    mbar_init(&p_full, 4);
+    mbar_init(&o_last, 1);
+    mbar_init(&p_full, kSoftWarps);
     fence_barrier_init();
     tma_prefetch_desc(&tm_q);
     tma_prefetch_desc(&tm_kv_k);
@@ -141,7 +188,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
-  constexpr uint32_t kOAcc = 256;  // O accumulator columns [256, 256+D)
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -153,15 +199,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int qb = used % L::kQBufs;
         mbar_wait(&q_empty[qb], ((used / L::kQBufs) & 1) ^ 1);
         ++used;
-        mbar_arrive_expect_tx(&q_full[qb], uint32_t(L::kKBlocks * 64 * p.g * p.n * 2));
+        mbar_arrive_expect_tx(&q_full[qb], uint32_t(R * L::kKBlocks * 64 * p.g * p.n * 2));
         for (int kb = 0; kb < L::kKBlocks; ++kb)
-          tma_load_3d(smem + L::kQOff + qb * L::kQBytes + kb * 16384, &tm_q, &q_full[qb], kb * 64, it.h * p.g,
-                      it.r * p.n);
+          for (int k = 0; k < R; ++k)
+            tma_load_3d(smem + L::kQOff + qb * L::kQBytes + kb * 16384 + k * kLanes * 128, &tm_q, &q_full[qb],
+                        kb * 64, it.h * p.g, it.r * p.n);
         const int row_base = (it.r * p.n_kv + it.h) * p.s_max;
         for (int c = it.c_begin; c < it.c_end; ++c, ++gc) {
-          const int s = gc % kKvStages;
+          const int s = gc % kStages;
           TR(0, 1);
-          mbar_wait(&kv_empty[s], ((gc / kKvStages) & 1) ^ 1);
+          mbar_wait(&kv_empty[s], ((gc / kStages) & 1) ^ 1);
           TR(0, 2);
           mbar_arrive_expect_tx(&kv_full[s], uint32_t(2 * L::kKvBytes));
           uint8_t* kdst = smem + L::kKvOff + s * 2 * L::kKvBytes;
@@ -188,11 +235,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++used;
         const uint32_t q_addr = smem_u32(smem + L::kQOff + qb * L::kQBytes);
         const int nch = it.c_end - it.c_begin;
+        // S(ci) may be issued once its K/V stage landed and its S/P buffer
+        // was consumed by PV two chunks earlier
+        auto s_ready = [&](int ci) {
+          const int g2 = gc + ci;
+          return mbar_test_wait(&kv_full[g2 % kStages], (g2 / kStages) & 1) &&
+                 mbar_test_wait(&s_empty[g2 & 1], ((g2 >> 1) & 1) ^ 1);
+        };
         auto issue_s = [&](int ci) {
           const int g2 = gc + ci;
-          const int s = g2 % kKvStages, sb = g2 & 1;
+          const int s = g2 % kStages, sb = g2 & 1;
           TR(1, 1);
-          mbar_wait(&kv_full[s], (g2 / kKvStages) & 1);
+          mbar_wait(&kv_full[s], (g2 / kStages) & 1);
           mbar_wait(&s_empty[sb], ((g2 >> 1) & 1) ^ 1);
           tc_fence_after();
           const uint32_t k_addr = smem_u32(smem + L::kKvOff + s * 2 * L::kKvBytes);
@@ -208,547 +262,289 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         issue_s(0);
         for (int ci = 0; ci < nch; ++ci) {
-          if (ci + 1 < nch) issue_s(ci + 1);
           const int g2 = gc + ci;
-          const int s = g2 % kKvStages;
+          const int s = g2 % kStages, sb = g2 & 1;
           TR(1, 4);
-          mbar_wait(&p_full, p_phase);
+          // PV(ci) must not queue behind the next chunk's K/V load (it frees
+          // that load's stage): issue S(ci+1) early only if it is ready
+          bool next_issued = ci + 1 >= nch;
+          while (!mbar_test_wait(&p_full, p_phase)) {
+            if (!next_issued && s_ready(ci + 1)) {
+              issue_s(ci + 1);
+              next_issued = true;
+            }
+          }
           TR(1, 5);
           p_phase ^= 1;
           tc_fence_after();
-          const uint32_t p_addr = smem_u32(smem + L::kPOff);
-          const uint32_t plo_addr = smem_u32(smem + L::kPLoOff);
           const uint32_t v_addr = smem_u32(smem + L::kKvOff + s * 2 * L::kKvBytes + L::kKvBytes);
-          // O += P_hi V + P_lo V: P carried to ~16 mantissa bits
+          // O += P_hi V + P_lo V with P read from TMEM: P carried to ~16
+          // mantissa bits
 #pragma unroll
           for (int kk = 0; kk < kChunk / 16; ++kk) {
-            const uint32_t aoff = (kk / 4) * 16384 + (kk % 4) * 32;
             const uint64_t vd = make_sdesc_sw128(v_addr + kk * 2048, 16384, 1024);
-            umma_bf16(tmem + kOAcc, make_sdesc_sw128(p_addr + aoff, 16, 1024), vd, id_o,
-                      (ci > 0 || kk > 0) ? 1u : 0u);
-            umma_bf16(tmem + kOAcc, make_sdesc_sw128(plo_addr + aoff, 16, 1024), vd, id_o, 1u);
+            umma_bf16_ts(tmem + kOAcc, tmem + sb * 128 + kk * 8, vd, id_o, (ci > 0 || kk > 0) ? 1u : 0u);
+            umma_bf16_ts(tmem + kOAcc, tmem + sb * 128 + 64 + kk * 8, vd, id_o, 1u);
           }
           umma_commit(&o_full);
-          umma_commit(&kv_empty[s]);
+          if (ci + 1 == nch) umma_commit(&o_last);
+          umma_commit(&s_empty[sb]);
+          // the last chunk's stage is released by the softmax warps after the
+          // epilogue (they use it as scratch)
+          if (ci + 1 < nch) umma_commit(&kv_empty[s]);
           TR(1, 6);
+          if (!next_issued) issue_s(ci + 1);
         }
         gc += nch;
       }
     }
   } else {
     // ------------------------------------------------------------ softmax
-    const int q4 = warp & 3;
-    const int row = q4 * 32 + lane;
+    const int q4 = warp & 3;                    // TMEM lane quadrant of this warp
+    const int half = (warp - 2) >> 2;           // which half of the replica's columns
+    const int lrow = q4 * 32 + lane;            // TMEM lane = Q tile row
+    const int rep = lrow / kLanes;              // warp-uniform (kLanes >= 32)
+    const int row = lrow % kLanes;              // query row (i*g + hh)
     const uint32_t tlane = uint32_t(q4 * 32) << 16;
-    const bool warp_live = q4 * 32 < p.rows;  // warp-uniform
-    uint8_t* pbuf = smem + L::kPOff;
-    int gc = 0;
+    const bool warp_live = (q4 * 32) % kLanes < p.rows;
+    const int col0 = rep * kW + half * kCols;   // this thread's key columns in a chunk
+    const int oc0 = half * kOCols;              // this thread's O columns
+    const uint32_t pair_bar = 1 + q4;           // named barrier of the two warps of a quadrant
+    int gc = 0, items_done = 0;
     for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
       const ItemInfo it = item_info(p, item);
       const int nch = it.c_end - it.c_begin;
+      if (nch <= 0) {  // empty split (only with split-KV): no keys, m = -inf
+        if (p.splits > 1 && rep == 0 && half == 0 && row < p.rows)
+          p.ws_ml[size_t(item) * p.rows + row] = make_float2(-INFINITY, 0.f);
+        continue;
+      }
       const bool live = row < p.rows;
       const int qi = live ? row / p.g : 0;
       const int hh = live ? row % p.g : 0;
       uint64_t mbits = live ? p.mask[it.r * p.n + qi] : 0ull;
       if (p.n < 64) mbits &= (1ull << p.n) - 1ull;
       const int prefix = live ? it.keys - p.n : 0;
-      float m_run = -INFINITY, l_run = 0.f;
+      float m_ref = -INFINITY, l_run = 0.f;  // reference max (log2 units), partial row sum
+      if (warp == 4 && lane == 0) TR(2, 11);
       for (int ci = 0; ci < nch; ++ci) {
         const int g2 = gc + ci;
         const int sb = g2 & 1;
         const int key0 = (it.c_begin + ci) * kChunk;
+        uint8_t* kbuf = smem + L::kKvOff + (g2 % kStages) * 2 * L::kKvBytes;
+        const uint32_t tsp = tmem + tlane + sb * 128;  // this quadrant's S/P buffer
         if (warp == 4 && lane == 0) TR(2, 1);
         mbar_wait(&s_full[sb], (g2 >> 1) & 1);
         if (warp == 4 && lane == 0) TR(2, 2);
         tc_fence_after();
-        float m_new = m_run, alpha = 1.f;
+        // this chunk's K tile is dead once S is in TMEM (it is refilled only
+        // after PV of this chunk, i.e. after every warp's p_full arrival):
+        // use it for the pair's max exchange
+        float* xchg = reinterpret_cast<float*>(kbuf);
+        uint32_t sv[kCols];
+        uint32_t vb[(kCols + 31) / 32];
+        float cmax = -INFINITY;
         if (warp_live) {
-          // pass 1: masked row max of this chunk (log2 domain)
-          float cmax = -INFINITY;
-#pragma unroll 1
-          for (int c0 = 0; c0 < kChunk; c0 += 32) {
-            uint32_t r[32];
-            tmem_ld32(tmem + tlane + sb * 128 + c0, r);
-            const uint32_t vb = visible_bits(key0 + c0, prefix, mbits);
-            tmem_ld_wait();
+          tmem_ld_cols<kCols>(tsp + col0, sv);
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if ((vb >> j) & 1u) cmax = fmaxf(cmax, __uint_as_float(r[j]));
-          }
-          m_new = fmaxf(m_run, cmax * p.scale_log2);
-          alpha = (m_run == -INFINITY) ? 0.f : ex2_approx(m_run - m_new);
+          for (int w = 0; w < (kCols + 31) / 32; ++w) vb[w] = visible_bits(key0 + col0 + 32 * w, prefix, mbits);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < kCols; ++j)
+            if ((vb[j / 32] >> (j % 32)) & 1u) cmax = fmaxf(cmax, __uint_as_float(sv[j]));
         }
+        xchg[half * 128 + lrow] = cmax;
+        // both warps' S columns are in registers after this barrier, so P may
+        // overwrite the S buffer
+        asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+        cmax = fmaxf(cmax, xchg[(half ^ 1) * 128 + lrow]) * p.scale_log2;
+        const bool grow = cmax > m_ref + 8.f;  // also true for the first visible score
+        const float m_new = grow ? cmax : m_ref;
+        const float alpha = grow ? (m_ref == -INFINITY ? 0.f : ex2_approx(m_ref - m_new)) : 1.f;
         if (warp == 4 && lane == 0) TR(2, 3);
-        // the previous chunk's PV must be done before P is overwritten and
-        // before O is rescaled in TMEM (FA4-style correction, skipped when no
-        // row of this warp moved its maximum)
-        if (ci > 0) {
-          mbar_wait(&o_full, (g2 - 1) & 1);
-          tc_fence_after();
-          if (warp_live && __any_sync(0xffffffffu, live && alpha != 1.f)) {
-#pragma unroll 1
-            for (int c0 = 0; c0 < D; c0 += 32) {
-              uint32_t r[32];
-              tmem_ld32(tmem + tlane + kOAcc + c0, r);
-              tmem_ld_wait();
-#pragma unroll
-              for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * alpha);
-              tmem_st32(tmem + tlane + kOAcc + c0, r);
-            }
-            tmem_st_wait();
-          }
-        }
-        if (warp == 4 && lane == 0) TR(2, 4);
-        // pass 2: p = 2^(s*scale - m), row sum, P = hi + lo bf16 planes
+        // p = 2^(s*scale - m) on visible keys (<= 2^8); P row = hi + lo bf16
         const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
         float psum = 0.f;
         if (warp_live) {
-#pragma unroll 1
-          for (int c0 = 0; c0 < kChunk; c0 += 32) {
-            uint32_t r[32];
-            tmem_ld32(tmem + tlane + sb * 128 + c0, r);
-            const uint32_t vb = live ? visible_bits(key0 + c0, prefix, mbits) : 0u;
-            tmem_ld_wait();
-            uint32_t pk[16], pl[16];
+          uint32_t phi[kCols / 2], plo[kCols / 2];
 #pragma unroll
-            for (int j = 0; j < 32; j += 2) {
-              const float a = ((vb >> j) & 1u) ? ex2_approx(__uint_as_float(r[j]) * p.scale_log2 - m_use) : 0.f;
-              const float b =
-                  ((vb >> (j + 1)) & 1u) ? ex2_approx(__uint_as_float(r[j + 1]) * p.scale_log2 - m_use) : 0.f;
-              psum += a + b;
-              const uint32_t hi = pack_bf16x2(a, b);
-              pk[j / 2] = hi;
-              pl[j / 2] = pack_bf16x2(a - __uint_as_float(hi << 16), b - __uint_as_float(hi & 0xffff0000u));
-            }
-            const int kb = c0 / 64;
+          for (int j = 0; j < kCols; j += 2) {
+            const float a = ((vb[j / 32] >> (j % 32)) & 1u) ? ex2_approx(__uint_as_float(sv[j]) * p.scale_log2 - m_use) : 0.f;
+            const float b =
+                ((vb[j / 32] >> ((j + 1) % 32)) & 1u) ? ex2_approx(__uint_as_float(sv[j + 1]) * p.scale_log2 - m_use) : 0.f;
+            psum += a + b;
+            const uint32_t hh2 = pack_bf16x2(a, b);
+            phi[j / 2] = hh2;
+            plo[j / 2] = pack_bf16x2(a - __uint_as_float(hh2 << 16), b - __uint_as_float(hh2 & 0xffff0000u));
+          }
+          tmem_st_pcols<kCols>(tsp + col0 / 2, phi);
+          tmem_st_pcols<kCols>(tsp + 64 + col0 / 2, plo);
+          if constexpr (R > 1) {
+            // keys of other replicas: zero P for this lane (half 0 the hi
+            // plane, half 1 the lo plane)
+            uint32_t z[8];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              const int lc = ((c0 % 64) / 8) + t;
-              const int off = kb * 16384 + row * 128 + ((lc ^ (row & 7)) * 16);
-              *reinterpret_cast<uint4*>(pbuf + off) = make_uint4(pk[4 * t], pk[4 * t + 1], pk[4 * t + 2], pk[4 * t + 3]);
-              *reinterpret_cast<uint4*>(pbuf + (L::kPLoOff - L::kPOff) + off) =
-                  make_uint4(pl[4 * t], pl[4 * t + 1], pl[4 * t + 2], pl[4 * t + 3]);
-            }
+            for (int j = 0; j < 8; ++j) z[j] = 0u;
+#pragma unroll
+            for (int c = 0; c < 64; c += 8)
+              if (c < rep * (kW / 2) || c >= (rep + 1) * (kW / 2)) tmem_st8(tsp + half * 64 + c, z);
           }
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_empty[sb]);
         l_run = l_run * alpha + psum;
-        m_run = m_new;
+        m_ref = m_new;
         // keys past the request's end in the last chunk: zero their V rows so
         // stale (possibly non-finite) cache contents cannot reach the MMA
-        if (key0 + kChunk > it.keys && key0 + row >= it.keys) {
-          uint8_t* vbuf = smem + L::kKvOff + (g2 % kKvStages) * 2 * L::kKvBytes + L::kKvBytes;
+        if (half == 0 && key0 + kChunk > it.keys && key0 + lrow >= it.keys) {
+          uint8_t* vbuf = kbuf + L::kKvBytes;
 #pragma unroll
           for (int kb = 0; kb < L::kKBlocks; ++kb)
 #pragma unroll
             for (int t = 0; t < 8; ++t)
-              *reinterpret_cast<uint4*>(vbuf + kb * 16384 + row * 128 + t * 16) = make_uint4(0, 0, 0, 0);
+              *reinterpret_cast<uint4*>(vbuf + kb * 16384 + lrow * 128 + t * 16) = make_uint4(0, 0, 0, 0);
+          fence_proxy_async();
         }
-        fence_proxy_async();
+        // lanes whose reference max moved rescale O (and only after PV(ci-1))
+        if (ci > 0 && warp_live && __any_sync(0xffffffffu, live && alpha != 1.f)) {
+          mbar_wait(&o_full, (g2 - 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c0 = 0; c0 < kOCols; c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(tmem + tlane + kOAcc + oc0 + c0, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * alpha);
+            tmem_st32(tmem + tlane + kOAcc + oc0 + c0, r);
+          }
+        }
+        if (warp == 4 && lane == 0) TR(2, 4);
+        tmem_st_wait();
+        tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full);
         if (warp == 4 && lane == 0) TR(2, 5);
       }
-      if (nch > 0) {
-        mbar_wait(&o_full, (gc + nch - 1) & 1);
-        tc_fence_after();
-      }
+      mbar_wait(&o_last, items_done & 1);
+      ++items_done;
+      tc_fence_after();
+      if (warp == 4 && lane == 0) TR(2, 6);
+      // ---- epilogue. The last chunk's K/V stage is held for us (released
+      // below): first the (m, l) exchange at its V tile, then the weighted
+      // replica partials [R][rows][D] fp32 over the whole stage (16-byte
+      // pieces XOR-swizzled by row).
+      uint8_t* kbuf = smem + L::kKvOff + ((gc + nch - 1) % kStages) * 2 * L::kKvBytes;
+      float* slots = reinterpret_cast<float*>(kbuf);
+      float* lsum = reinterpret_cast<float*>(kbuf + L::kKvBytes);            // [2][128]
+      float2* ml = reinterpret_cast<float2*>(kbuf + L::kKvBytes + 1024);     // [128]
+      const int s_last = (gc + nch - 1) % kStages;
       gc += nch;
-      if (!warp_live) continue;
-      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-#pragma unroll 1
-      for (int c0 = 0; c0 < D; c0 += 32) {
-        uint32_t r[32];
-        if (nch > 0) {
-          tmem_ld32(tmem + tlane + kOAcc + c0, r);
-          tmem_ld_wait();
-        } else {
+      lsum[half * 128 + lrow] = l_run;
+      asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+      const float l_tot = l_run + lsum[(half ^ 1) * 128 + lrow];
+      float M = m_ref, Ls = l_tot;
+      if (warp == 4 && lane == 0) TR(2, 7);
+      if constexpr (R > 1) {
+        if (half == 0) ml[lrow] = make_float2(m_ref, l_tot);
+        asm volatile("bar.sync 5, 256;" ::: "memory");
+        if (live) {
+          M = -INFINITY;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) r[j] = 0u;
-        }
-        if (!live) continue;
-        if (p.splits == 1) {
-          uint16_t* dst = p.out + ((size_t(it.r) * p.n + qi) * p.n_q + size_t(it.h) * p.g + hh) * D + c0;
+          for (int k = 0; k < R; ++k) M = fmaxf(M, ml[row + k * kLanes].x);
+          Ls = 0.f;
 #pragma unroll
-          for (int j = 0; j < 32; j += 8) {
-            uint4 v;
-            v.x = pack_bf16x2(__uint_as_float(r[j]) * inv, __uint_as_float(r[j + 1]) * inv);
-            v.y = pack_bf16x2(__uint_as_float(r[j + 2]) * inv, __uint_as_float(r[j + 3]) * inv);
-            v.z = pack_bf16x2(__uint_as_float(r[j + 4]) * inv, __uint_as_float(r[j + 5]) * inv);
-            v.w = pack_bf16x2(__uint_as_float(r[j + 6]) * inv, __uint_as_float(r[j + 7]) * inv);
-            *reinterpret_cast<uint4*>(dst + j) = v;
+          for (int k = 0; k < R; ++k) {
+            const float2 v = ml[row + k * kLanes];
+            if (v.x != -INFINITY) Ls += v.y * ex2_approx(v.x - M);
           }
-        } else {
-          float* dst = p.ws_o + (size_t(item) * p.rows + row) * D + c0;
+        }
+        asm volatile("bar.sync 5, 256;" ::: "memory");  // ml / lsum read: the stage becomes slots
+        if (warp == 4 && lane == 0) TR(2, 12);
+      }
+      // this replica's weight in the merged row (normalised unless split-KV
+      // partials are written for attn_combine_kernel)
+      float wgt = (live && m_ref != -INFINITY) ? ex2_approx(m_ref - M) : 0.f;
+      if (p.splits == 1) wgt *= Ls > 0.f ? 1.f / Ls : 0.f;
+      if (warp_live) {
+#pragma unroll 1
+        for (int c0 = 0; c0 < kOCols; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(tmem + tlane + kOAcc + oc0 + c0, r);
+          tmem_ld_wait();
+          if (!live) continue;
+          const int col = oc0 + c0;
+          if constexpr (R == 1) {
+            if (p.splits == 1) {
+              uint16_t* dst = p.out + ((size_t(it.r) * p.n + qi) * p.n_q + size_t(it.h) * p.g + hh) * D + col;
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(dst + j) =
-                make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                            __uint_as_float(r[j + 3]));
+              for (int j = 0; j < 32; j += 8) {
+                uint4 v;
+                v.x = pack_bf16x2(__uint_as_float(r[j]) * wgt, __uint_as_float(r[j + 1]) * wgt);
+                v.y = pack_bf16x2(__uint_as_float(r[j + 2]) * wgt, __uint_as_float(r[j + 3]) * wgt);
+                v.z = pack_bf16x2(__uint_as_float(r[j + 4]) * wgt, __uint_as_float(r[j + 5]) * wgt);
+                v.w = pack_bf16x2(__uint_as_float(r[j + 6]) * wgt, __uint_as_float(r[j + 7]) * wgt);
+                *reinterpret_cast<uint4*>(dst + j) = v;
+              }
+            } else {
+              float* dst = p.ws_o + (size_t(item) * p.rows + row) * D + col;
+#pragma unroll
+              for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4*>(dst + j) =
+                    make_float4(__uint_as_float(r[j]) * wgt, __uint_as_float(r[j + 1]) * wgt,
+                                __uint_as_float(r[j + 2]) * wgt, __uint_as_float(r[j + 3]) * wgt);
+            }
+          } else {
+            float4* slot = reinterpret_cast<float4*>(slots) + (rep * kLanes + row) * (D / 4);
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              slot[((col + j) / 4) ^ (row & 7)] =
+                  make_float4(__uint_as_float(r[j]) * wgt, __uint_as_float(r[j + 1]) * wgt,
+                              __uint_as_float(r[j + 2]) * wgt, __uint_as_float(r[j + 3]) * wgt);
+          }
         }
       }
-      if (live && p.splits > 1)
-        p.ws_ml[size_t(item) * p.rows + row] = make_float2(nch > 0 ? m_run : -INFINITY, l_run);
+      if constexpr (R > 1) {
+        asm volatile("bar.sync 5, 256;" ::: "memory");
+        if (warp == 4 && lane == 0) TR(2, 13);
+        // replica 0's threads sum the R partials in a fixed order
+        if (rep == 0 && live) {
+          const float4* s4 = reinterpret_cast<const float4*>(slots);
+#pragma unroll
+          for (int j = 0; j < kOCols; j += 8) {
+            float4 a = s4[row * (D / 4) + (((oc0 + j) / 4) ^ (row & 7))];
+            float4 b = s4[row * (D / 4) + (((oc0 + j) / 4 + 1) ^ (row & 7))];
+#pragma unroll
+            for (int k = 1; k < R; ++k) {
+              const float4 a2 = s4[(k * kLanes + row) * (D / 4) + (((oc0 + j) / 4) ^ (row & 7))];
+              const float4 b2 = s4[(k * kLanes + row) * (D / 4) + (((oc0 + j) / 4 + 1) ^ (row & 7))];
+              a.x += a2.x; a.y += a2.y; a.z += a2.z; a.w += a2.w;
+              b.x += b2.x; b.y += b2.y; b.z += b2.z; b.w += b2.w;
+            }
+            if (p.splits == 1) {
+              uint16_t* dst = p.out + ((size_t(it.r) * p.n + qi) * p.n_q + size_t(it.h) * p.g + hh) * D + oc0 + j;
+              *reinterpret_cast<uint4*>(dst) =
+                  make_uint4(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y), pack_bf16x2(b.z, b.w));
+            } else {
+              float* dst = p.ws_o + (size_t(item) * p.rows + row) * D + oc0 + j;
+              *reinterpret_cast<float4*>(dst) = a;
+              *reinterpret_cast<float4*>(dst + 4) = b;
+            }
+          }
+        }
+      }
+      if (warp == 4 && lane == 0) TR(2, 9);
+      if (live && rep == 0 && half == 0 && p.splits > 1) p.ws_ml[size_t(item) * p.rows + row] = make_float2(M, Ls);
+      // all scratch reads and TMEM O reads done -> hand the stage back to the producer
       tc_fence_before();
+      fence_proxy_async();
+      asm volatile("bar.sync 5, 256;" ::: "memory");
+      if (warp == 2 && lane == 0) mbar_arrive(&kv_empty[s_last]);
+      if (warp == 4 && lane == 0) TR(2, 10);
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
-
-// ---------------------------------------------------------------------------
-// K1 v3 ("swap-AB"), used when the g*n query rows of a KV head fit in 64:
-// S^T = K Q^T puts the 128 keys of a chunk on the TMEM lanes and the query
-// rows on the columns, so each of the 128 softmax threads owns ONE key and
-// does NP=64 exps per chunk (v2: one row, 128 exps, mostly one busy warp).
-//   * P^T [keys][rows] is written by its key-thread as one 128-byte swizzled
-//     row (MN-major B operand); O^T [d][rows] = V^T P^T with V^T the MN-major
-//     A operand (V's natural layout); l[rows] = ones . P^T on the tensor core
-//     (a 256-byte all-ones A tile, SBO = 0) so no cross-thread row sums.
-//   * row maxima are kept per row and only refreshed (cross-thread reduce +
-//     O/l rescale in TMEM) when some score exceeds max + 8 in log2 units —
-//     always at an item's first chunk, rarely afterwards; p stays <= 2^8.
-namespace v3 {
-constexpr int kNP = 64;  // query rows per item (padded)
-
-template <int D>
-struct Smem {
-  static constexpr int kKBlocks = D / 64;
-  static constexpr int kQBytes = kKBlocks * 16384;
-  static constexpr int kKvBytes = kKBlocks * 16384;
-  static constexpr int kQOff = 0;
-  static constexpr int kKvOff = kQBytes;
-  static constexpr int kPOff = kKvOff + kKvStages * 2 * kKvBytes;  // P^T hi, then lo: [128 keys][64 rows]
-  static constexpr int kPPlane = 16384;
-  static constexpr int kOnesOff = kPOff + 2 * kPPlane;
-  static constexpr int kTotal = kOnesOff + 1024;
-};
-
-template <int D>
-__global__ void __launch_bounds__(kThreads, 1)
-    kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv_k,
-           const __grid_constant__ CUtensorMap tm_kv_v, AttnParams p) {
-  using L = Smem<D>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t q_full, q_empty;
-  __shared__ __align__(8) uint64_t kv_full[kKvStages], kv_empty[kKvStages];
-  __shared__ __align__(8) uint64_t s_full[2], s_empty[2], o_full, p_full;
-  __shared__ uint32_t tmem_base_sh;
-  __shared__ float red_sh[4][kNP];
-  __shared__ float alpha_sh[kNP];
-  __shared__ float m_sh[kNP];  // per-row running max (log2 units)
-  __shared__ uint64_t vis_sh[64];  // draft key j -> rows that see it
-  __shared__ uint64_t mrow_sh[64]; // compact mask word of draft query i
-  __shared__ int flag_sh[4];
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (warp == 0 && lane == 0) {
-    mbar_init(&q_full, 1);
-    mbar_init(&q_empty, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4);
-    }
-    for (int i = 0; i < kKvStages; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-    }
-    mbar_init(&o_full, 1);
-    mbar_init(&p_full, 4);
-    fence_barrier_init();
-    tma_prefetch_desc(&tm_q);
-    tma_prefetch_desc(&tm_kv_k);
-    tma_prefetch_desc(&tm_kv_v);
-  }
-  if (warp == 1) tmem_alloc<256>(&tmem_base_sh);
-  if (warp >= 2) {  // all-ones A tile for the row-sum MMA (bf16 1.0)
-    for (int i = threadIdx.x - 64; i < 64; i += 128) reinterpret_cast<uint32_t*>(smem + L::kOnesOff)[i] = 0x3F803F80u;
-    fence_proxy_async();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = tmem_base_sh;
-  constexpr uint32_t kS = 0, kO = 2 * kNP, kL = 3 * kNP;  // TMEM columns
-
-  if (warp == 0) {
-    if (elect_one()) {
-      int used = 0, gc = 0;
-      for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
-        const ItemInfo it = item_info(p, item);
-        if (it.c_end <= it.c_begin) continue;
-        mbar_wait(&q_empty, (used & 1) ^ 1);
-        ++used;
-        mbar_arrive_expect_tx(&q_full, uint32_t(L::kKBlocks * 64 * p.g * p.n * 2));
-        for (int kb = 0; kb < L::kKBlocks; ++kb)
-          tma_load_3d(smem + L::kQOff + kb * 16384, &tm_q, &q_full, kb * 64, it.h * p.g, it.r * p.n);
-        const int row_base = (it.r * p.n_kv + it.h) * p.s_max;
-        for (int c = it.c_begin; c < it.c_end; ++c, ++gc) {
-          const int s = gc % kKvStages;
-          TR(0, 1);
-          mbar_wait(&kv_empty[s], ((gc / kKvStages) & 1) ^ 1);
-          TR(0, 2);
-          mbar_arrive_expect_tx(&kv_full[s], uint32_t(2 * L::kKvBytes));
-          uint8_t* kdst = smem + L::kKvOff + s * 2 * L::kKvBytes;
-          uint8_t* vdst = kdst + L::kKvBytes;
-          for (int kb = 0; kb < L::kKBlocks; ++kb) {
-            tma_load_2d(kdst + kb * 16384, &tm_kv_k, &kv_full[s], kb * 64, row_base + c * kChunk);
-            tma_load_2d(vdst + kb * 16384, &tm_kv_v, &kv_full[s], kb * 64, row_base + c * kChunk);
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (elect_one()) {
-      const uint32_t id_s = make_idesc_bf16(128, kNP);                      // K (keys) x Q^T
-      const uint32_t id_o = make_idesc_bf16(128, kNP, /*b_mn=*/1, /*a_mn=*/1);  // V^T x P^T
-      const uint32_t id_l = make_idesc_bf16(128, kNP, /*b_mn=*/1, /*a_mn=*/0);  // ones x P^T
-      const uint32_t q_addr = smem_u32(smem + L::kQOff);
-      const uint32_t p_addr = smem_u32(smem + L::kPOff);
-      // all-ones A: no swizzle, K core matrices 128 B apart, every 8-row group
-      // aliases the same 256 bytes (SBO = 0)
-      uint64_t ones_d = uint64_t((smem_u32(smem + L::kOnesOff) >> 4) & 0x3FFFu) | (uint64_t(128 >> 4) << 16) |
-                        (uint64_t(1) << 46);
-      int used = 0, gc = 0;
-      uint32_t p_phase = 0;
-      for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
-        const ItemInfo it = item_info(p, item);
-        if (it.c_end <= it.c_begin) continue;
-        mbar_wait(&q_full, used & 1);
-        ++used;
-        const int nch = it.c_end - it.c_begin;
-        auto issue_s = [&](int ci) {
-          const int g2 = gc + ci;
-          const int s = g2 % kKvStages, sb = g2 & 1;
-          TR(1, 1);
-          mbar_wait(&kv_full[s], (g2 / kKvStages) & 1);
-          mbar_wait(&s_empty[sb], ((g2 >> 1) & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t k_addr = smem_u32(smem + L::kKvOff + s * 2 * L::kKvBytes);
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk / 4) * 16384 + (kk % 4) * 32;
-            umma_bf16(tmem + kS + sb * kNP, make_sdesc_sw128(k_addr + off, 16, 1024),
-                      make_sdesc_sw128(q_addr + off, 16, 1024), id_s, kk > 0 ? 1u : 0u);
-          }
-          umma_commit(&s_full[sb]);
-          if (ci == nch - 1) umma_commit(&q_empty);
-          TR(1, 2);
-        };
-        issue_s(0);
-        for (int ci = 0; ci < nch; ++ci) {
-          if (ci + 1 < nch) issue_s(ci + 1);
-          const int g2 = gc + ci;
-          const int s = g2 % kKvStages;
-          TR(1, 4);
-          mbar_wait(&p_full, p_phase);
-          TR(1, 5);
-          p_phase ^= 1;
-          tc_fence_after();
-          const uint32_t v_addr = smem_u32(smem + L::kKvOff + s * 2 * L::kKvBytes + L::kKvBytes);
-#pragma unroll
-          for (int kk = 0; kk < kChunk / 16; ++kk) {
-            const uint64_t vd = make_sdesc_sw128(v_addr + kk * 2048, 16384, 1024);
-            const uint64_t ph = make_sdesc_sw128(p_addr + kk * 2048, 16384, 1024);
-            const uint64_t pl = make_sdesc_sw128(p_addr + L::kPPlane + kk * 2048, 16384, 1024);
-            const uint32_t acc = (ci > 0 || kk > 0) ? 1u : 0u;
-            umma_bf16(tmem + kO, vd, ph, id_o, acc);
-            umma_bf16(tmem + kO, vd, pl, id_o, 1u);
-            umma_bf16(tmem + kL, ones_d, ph, id_l, acc);
-            umma_bf16(tmem + kL, ones_d, pl, id_l, 1u);
-          }
-          umma_commit(&o_full);
-          umma_commit(&kv_empty[s]);
-          TR(1, 6);
-        }
-        gc += nch;
-      }
-    }
-  } else {
-    // ---------------------------------------------- softmax: thread = key lane
-    const int q4 = warp & 3;
-    const int kt = q4 * 32 + lane;                 // key within the chunk (TMEM lane)
-    const uint32_t tl = uint32_t(q4 * 32) << 16;
-    const int st = threadIdx.x - 64;               // 0..127
-    uint8_t* pbuf = smem + L::kPOff;
-    int gc = 0;
-    for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
-      const ItemInfo it = item_info(p, item);
-      const int nch = it.c_end - it.c_begin;
-      const int prefix = it.keys - p.n;
-      // draft visibility per draft key j: rows (i*g+hh) whose query i sees j
-      if (st < p.n) mrow_sh[st] = p.mask[it.r * p.n + st];
-      asm volatile("bar.sync 2, 128;" ::: "memory");
-      if (st < 64) {
-        uint64_t rows = 0;
-        if (st < p.n)
-          for (int r = 0; r < p.rows; ++r)
-            if ((mrow_sh[r / p.g] >> st) & 1ull) rows |= 1ull << r;
-        vis_sh[st] = rows;
-      }
-      const uint64_t live_rows = p.rows >= 64 ? ~0ull : ((1ull << p.rows) - 1ull);
-      if (st < kNP) m_sh[st] = -INFINITY;
-      asm volatile("bar.sync 2, 128;" ::: "memory");
-      if (st == 0) TR(2, 8);
-      for (int ci = 0; ci < nch; ++ci) {
-        const int g2 = gc + ci;
-        const int sb = g2 & 1;
-        const int key = (it.c_begin + ci) * kChunk + kt;
-        const uint64_t vis = key < prefix ? live_rows : (key < it.keys ? vis_sh[key - prefix] & live_rows : 0ull);
-        if (st == 0) TR(2, 1);
-        mbar_wait(&s_full[sb], (g2 >> 1) & 1);
-        if (st == 0) TR(2, 2);
-        tc_fence_after();
-        uint32_t sr[kNP];
-        {
-          uint32_t a[32], b[32];
-          tmem_ld32(tmem + tl + kS + sb * kNP, a);
-          tmem_ld32(tmem + tl + kS + sb * kNP + 32, b);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            sr[j] = __float_as_uint(__uint_as_float(a[j]) * p.scale_log2);
-            sr[j + 32] = __float_as_uint(__uint_as_float(b[j]) * p.scale_log2);
-          }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_empty[sb]);
-        // does any visible score exceed its row max by more than 2^8?
-        bool grow = false;
-#pragma unroll
-        for (int j = 0; j < kNP; ++j) grow |= ((vis >> j) & 1ull) && (__uint_as_float(sr[j]) > m_sh[j] + 8.f);
-        grow = __any_sync(0xffffffffu, grow);
-        if (lane == 0) flag_sh[q4] = grow ? 1 : 0;
-        asm volatile("bar.sync 2, 128;" ::: "memory");
-        const bool any_grow = (flag_sh[0] | flag_sh[1] | flag_sh[2] | flag_sh[3]) != 0;
-        if (st == 0) TR(2, any_grow ? 9 : 3);
-        if (any_grow) {
-          // exact per-row max of this chunk over the 128 keys: warp max, then 4 warps
-#pragma unroll
-          for (int j = 0; j < kNP; ++j) {
-            const float v = warp_max(((vis >> j) & 1ull) ? __uint_as_float(sr[j]) : -INFINITY);
-            if (lane == 0) red_sh[q4][j] = v;
-          }
-          asm volatile("bar.sync 2, 128;" ::: "memory");
-          if (st < kNP) {
-            // per-row decision (a row's reference max depends only on its own
-            // scores, which keeps causality bit-exact): refresh only rows that
-            // are unset or grew past max + 8
-            const int j = st;
-            const float cm = fmaxf(fmaxf(red_sh[0][j], red_sh[1][j]), fmaxf(red_sh[2][j], red_sh[3][j]));
-            const float mo = m_sh[j];
-            const bool refresh = cm != -INFINITY && (mo == -INFINITY || cm > mo + 8.f);
-            const float mn = refresh ? cm : mo;
-            alpha_sh[j] = refresh ? (mo == -INFINITY ? 0.f : ex2_approx(mo - mn)) : 1.f;
-            m_sh[j] = mn;
-          }
-          asm volatile("bar.sync 2, 128;" ::: "memory");  // m_sh/alpha_sh visible, red_sh reusable
-        }
-        // previous PV must be done before P is overwritten / O rescaled
-        if (ci > 0) {
-          mbar_wait(&o_full, (g2 - 1) & 1);
-          tc_fence_after();
-          if (any_grow) {  // O^T[d][row] and l[row] *= alpha[row]
-#pragma unroll 1
-            for (int part = 0; part < 2; ++part) {
-              const uint32_t col = part == 0 ? kO : kL;
-#pragma unroll
-              for (int h2 = 0; h2 < 2; ++h2) {
-                uint32_t r[32];
-                tmem_ld32(tmem + tl + col + h2 * 32, r);
-                tmem_ld_wait();
-#pragma unroll
-                for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * alpha_sh[h2 * 32 + j]);
-                tmem_st32(tmem + tl + col + h2 * 32, r);
-              }
-            }
-            tmem_st_wait();
-          }
-        }
-        if (st == 0) TR(2, 4);
-        // p = 2^(s - m) for visible (key,row) pairs; P^T row `kt` as hi + lo bf16
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          uint32_t hi4[4], lo4[4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int j = c * 8 + t * 2;
-            const float a = ((vis >> j) & 1ull) ? ex2_approx(__uint_as_float(sr[j]) - m_sh[j]) : 0.f;
-            const float b = ((vis >> (j + 1)) & 1ull) ? ex2_approx(__uint_as_float(sr[j + 1]) - m_sh[j + 1]) : 0.f;
-            const uint32_t hh = pack_bf16x2(a, b);
-            hi4[t] = hh;
-            lo4[t] = pack_bf16x2(a - __uint_as_float(hh << 16), b - __uint_as_float(hh & 0xffff0000u));
-          }
-          const int off = kt * 128 + ((c ^ (kt & 7)) * 16);
-          *reinterpret_cast<uint4*>(pbuf + off) = make_uint4(hi4[0], hi4[1], hi4[2], hi4[3]);
-          *reinterpret_cast<uint4*>(pbuf + L::kPPlane + off) = make_uint4(lo4[0], lo4[1], lo4[2], lo4[3]);
-        }
-        // keys past the request's end: zero their V rows (stale cache contents)
-        if (key >= it.keys) {
-          uint8_t* vbuf = smem + L::kKvOff + (g2 % kKvStages) * 2 * L::kKvBytes + L::kKvBytes;
-#pragma unroll
-          for (int kb = 0; kb < L::kKBlocks; ++kb)
-#pragma unroll
-            for (int t = 0; t < 8; ++t)
-              *reinterpret_cast<uint4*>(vbuf + kb * 16384 + kt * 128 + t * 16) = make_uint4(0, 0, 0, 0);
-        }
-        fence_proxy_async();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full);
-        if (st == 0) TR(2, 5);
-      }
-      if (nch > 0) {
-        mbar_wait(&o_full, (gc + nch - 1) & 1);
-        tc_fence_after();
-      }
-      if (st == 0) TR(2, 6);
-      gc += nch;
-      // epilogue: thread = d lane; l from the ones-MMA (identical on every lane)
-      if (kt < D) {
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          uint32_t lr[32], o[32];
-          if (nch > 0) {
-            tmem_ld32(tmem + tl + kL + h2 * 32, lr);
-            tmem_ld32(tmem + tl + kO + h2 * 32, o);
-            tmem_ld_wait();
-            if (st == 0) TR(2, 10 + h2);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) lr[j] = o[j] = 0u;
-          }
-#pragma unroll
-          for (int jj = 0; jj < 32; ++jj) {
-            const int j = h2 * 32 + jj;
-            if (j >= p.rows) continue;
-            const float l = __uint_as_float(lr[jj]);
-            const int qi = j / p.g, hh = j % p.g;
-            if (p.splits == 1) {
-              p.out[((size_t(it.r) * p.n + qi) * p.n_q + size_t(it.h) * p.g + hh) * D + kt] =
-                  f2bf(l > 0.f ? __uint_as_float(o[jj]) / l : 0.f);
-            } else {
-              p.ws_o[(size_t(item) * p.rows + j) * D + kt] = __uint_as_float(o[jj]);
-              if (kt == 0) p.ws_ml[size_t(item) * p.rows + j] = make_float2(nch > 0 ? m_sh[j] : -INFINITY, l);
-            }
-          }
-        }
-      }
-      if (st == 0) TR(2, 7);
-      tc_fence_before();
-      asm volatile("bar.sync 2, 128;" ::: "memory");  // TMEM O/l read before the next item's PV(0)
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc<256>(tmem);
-}
-}  // namespace v3
 
 // Merge the split-KV partials: O = sum_s O_s 2^(m_s - M) / sum_s l_s 2^(m_s - M).
 template <int D>
@@ -817,14 +613,17 @@ int device_sms() {
   return sms;
 }
 
-// K1 variant for rows <= 64: 2 = row-per-thread (default), 3 = swap-AB
-// key-per-thread; SMO_ATTN_VARIANT overrides (read once)
-int attn_variant() {
-  static int v = [] {
-    const char* e = std::getenv("SMO_ATTN_VARIANT");
-    return e && std::atoi(e) == 3 ? 3 : 2;
-  }();
-  return v;
+template <int D, int R>
+void launch_k1(int grid, cudaStream_t stream, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+               const AttnParams& p) {
+  constexpr size_t smem = AttnSmem<D>::kTotal + 1024;
+  static bool set = false;
+  if (!set) {
+    SMO_CUDA_CHECK(cudaFuncSetAttribute(verify_attention_kernel<D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(smem)));
+    set = true;
+  }
+  verify_attention_kernel<D, R><<<grid, kThreads, smem, stream>>>(tq, tk, tv, p);
 }
 
 void check_attn_args(const smo_attn_args& a) {
@@ -883,42 +682,16 @@ void attention_launch(const smo_attn_args& a, cudaStream_t stream) {
     make_tmap_bf16(&tk, a.k_cache, 2, dims, strides, box, true);
     make_tmap_bf16(&tv, a.v_cache, 2, dims, strides, box, true);
   }
-  if (p.rows <= v3::kNP && attn_variant() == 3) {
-    if (a.d == 128) {
-      constexpr size_t smem = v3::Smem<128>::kTotal + 1024;
-      static bool set = false;
-      if (!set) {
-        SMO_CUDA_CHECK(cudaFuncSetAttribute(v3::kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        set = true;
-      }
-      v3::kernel<128><<<pl.grid, kThreads, smem, stream>>>(tq, tk, tv, p);
-    } else {
-      constexpr size_t smem = v3::Smem<64>::kTotal + 1024;
-      static bool set = false;
-      if (!set) {
-        SMO_CUDA_CHECK(cudaFuncSetAttribute(v3::kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        set = true;
-      }
-      v3::kernel<64><<<pl.grid, kThreads, smem, stream>>>(tq, tk, tv, p);
-    }
-  } else if (a.d == 128) {
-    constexpr size_t smem = AttnSmem<128>::kTotal + 1024;
-    static bool set = false;
-    if (!set) {
-      SMO_CUDA_CHECK(cudaFuncSetAttribute(verify_attention_kernel<128>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      set = true;
-    }
-    verify_attention_kernel<128><<<pl.grid, kThreads, smem, stream>>>(tq, tk, tv, p);
+  // query-row replication: as many copies of the g*n rows as fit the 128 lanes
+  const int R = p.rows <= 32 ? 4 : (p.rows <= 64 ? 2 : 1);
+  if (a.d == 128) {
+    if (R == 4) launch_k1<128, 4>(pl.grid, stream, tq, tk, tv, p);
+    else if (R == 2) launch_k1<128, 2>(pl.grid, stream, tq, tk, tv, p);
+    else launch_k1<128, 1>(pl.grid, stream, tq, tk, tv, p);
   } else {
-    constexpr size_t smem = AttnSmem<64>::kTotal + 1024;
-    static bool set = false;
-    if (!set) {
-      SMO_CUDA_CHECK(cudaFuncSetAttribute(verify_attention_kernel<64>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      set = true;
-    }
-    verify_attention_kernel<64><<<pl.grid, kThreads, smem, stream>>>(tq, tk, tv, p);
+    if (R == 4) launch_k1<64, 4>(pl.grid, stream, tq, tk, tv, p);
+    else if (R == 2) launch_k1<64, 2>(pl.grid, stream, tq, tk, tv, p);
+    else launch_k1<64, 1>(pl.grid, stream, tq, tk, tv, p);
   }
   count_launch();
   SMO_CUDA_CHECK(cudaGetLastError());

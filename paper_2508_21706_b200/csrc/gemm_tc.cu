@@ -84,7 +84,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int KB = min(p.K / kBK - kb0, p.kb_per_split);  // k-blocks of this CTA's K slice
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align within the shared array (keeps the shared address space visible to
+  // the compiler: LDS/STS instead of generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ __align__(8) uint64_t full_bar[kMaxStages];
   __shared__ __align__(8) uint64_t empty_bar[kMaxStages];
   __shared__ __align__(8) uint64_t tmem_full_bar;

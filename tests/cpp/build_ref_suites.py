@@ -75,7 +75,8 @@ def build_own() -> list[str]:
         src = os.path.join(ROOT, "tests", "cpp", name + ".cpp")
         out = os.path.join(OUT, name)
         inc = os.path.join(ROOT, "include")
-        deps = [src] + [os.path.join(inc, "moeplan", f) for f in os.listdir(os.path.join(inc, "moeplan"))]
+        deps = [src, os.path.join(inc, "specmoe", "c_api.h")] + [
+            os.path.join(inc, "moeplan", f) for f in os.listdir(os.path.join(inc, "moeplan"))]
         if not os.path.exists(out) or os.path.getmtime(out) < max(os.path.getmtime(d) for d in deps):
             if not os.path.isdir(JSON):
                 continue

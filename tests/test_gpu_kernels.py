@@ -176,6 +176,9 @@ def _attn_case(torch, cuda, b, n, nq, nkv, d, prefix, s_max, tree, seed):
     (2, 9, 32, 8, 128, [1024, 700], True),             # k=8 tree
     (1, 16, 32, 8, 128, [5000], True),                 # 64 rows, split-KV
     (3, 1, 32, 8, 128, [127, 128, 129], False),        # plain decode, chunk edges
+    (1, 24, 32, 8, 128, [3000], True),                 # 96 rows: no row replication
+    (2, 9, 16, 16, 128, [255, 2049], False),           # MHA (g=1), 9 rows: 4 replicas
+    (2, 7, 24, 8, 64, [640, 77], True),                # g=3, d=64, 21 rows
 ])
 def test_verify_attention_vs_oracle(cuda, oracle, b, n, nq, nkv, d, prefix, tree):
     import torch
