@@ -68,7 +68,8 @@ typedef struct {
   void* out;
   int32_t b, n, n_q, n_kv, d, s_max;
   int32_t max_prefix; /* host upper bound of prefix_len (split planning) */
-  void* workspace;    /* >= smo_verify_attention_workspace() bytes */
+  void* workspace;    /* >= smo_verify_attention_workspace() bytes, zero-filled
+                         before its first use (the kernel leaves it so) */
   size_t workspace_bytes;
 } smo_attn_args;
 size_t smo_verify_attention_workspace(const smo_attn_args* a);

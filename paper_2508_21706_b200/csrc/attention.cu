@@ -16,7 +16,7 @@
 //    and O += P V reads A from TMEM, B = V (MN-major) from shared memory.
 //  * warps: w0 TMA producer, w1 TMEM alloc + MMA issuer, w2..w9 softmax (two
 //    warps per TMEM lane quadrant, each owning half of its replica's keys).
-//  * TMEM: S/P double buffer cols [0,256), O accumulator [256, 256+D).
+//  * TMEM: S/P triple buffer cols [0,384), O accumulator [384, 384+D).
 //  * shared memory: Q tile(s) + kStages K/V chunk stages (224 KB); the K tile
 //    of a consumed chunk doubles as the pair max-exchange buffer and the last
 //    chunk's stage as the epilogue's replica-merge scratch.
@@ -40,10 +40,13 @@ struct AttnParams {
   const uint64_t* mask;
   const int32_t* prefix;
   uint16_t* out;
-  float* ws_o;
-  float2* ws_ml;
+  float* ws_o;    // partial pieces [grid][2][rows][D] (unnormalised, replica-merged)
+  float2* ws_ml;  // their (reference max, row sum) [grid][2][rows]
+  int* ws_cnt;    // per (request, KV head) pieces-finished counter, zero between launches
   int b, n, n_q, n_kv, g, rows, s_max;
-  int splits, split_chunks, items;
+  int C;          // chunk slots per (request, KV head) = ceil((max_prefix + n) / 128)
+  int Q;          // chunks per CTA of the flat schedule
+  int total;      // pairs * C
   float scale_log2;
 };
 
@@ -60,35 +63,65 @@ struct AttnSmem {
 };
 
 #ifdef SMO_ATTN_TRACE
-// Debug timeline of CTA 0 (globaltimer ns << 8 | event code) per role.
+// Debug timeline of CTA 0 (globaltimer ns << 8 | event code) per role; the
+// event counters live in shared memory so a trace point costs no global
+// round trip.
 __device__ unsigned long long g_trace[3][4096];
 __device__ int g_trace_n[3];
+__shared__ int s_trace_n[3];
 __device__ __forceinline__ void trace_ev(int role, int code) {
   if (blockIdx.x != 0) return;
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  const int i = g_trace_n[role]++;
+  const int i = s_trace_n[role]++;
   if (i < 4096) g_trace[role][i] = (t << 8) | unsigned(code);
+  g_trace_n[role] = i + 1;
 }
 #define TR(role, code) trace_ev(role, code)
+#define TR_INIT() \
+  if (threadIdx.x < 3) s_trace_n[threadIdx.x] = 0
 #else
 #define TR(role, code)
+#define TR_INIT()
 #endif
 
-struct ItemInfo {
-  int r, h, c_begin, c_end, keys;
+// Flat ("stream-K") schedule: the (pair, chunk) slots of all requests and KV
+// heads are laid end to end and CTA i processes slots [i*Q, (i+1)*Q). The
+// run of slots a CTA holds for one pair is a piece; a piece covering a whole
+// pair writes the output, otherwise it leaves a partial (O, m, l) and the
+// pair's last finishing piece merges them (in-kernel split-KV combine).
+struct Piece {
+  int pair, r, h, c0, c1, keys;  // chunks [c0, c1) of pair (r, h); keys = prefix + n
+  int first_cta, npieces;        // CTAs holding the pair's non-empty pieces
+  int next_f;
 };
 
-__device__ __forceinline__ ItemInfo item_info(const AttnParams& p, int item) {
-  ItemInfo it;
-  const int pair = item / p.splits, split = item % p.splits;
-  it.r = pair / p.n_kv;
-  it.h = pair % p.n_kv;
-  it.keys = p.prefix[it.r] + p.n;
-  const int chunks = (it.keys + kChunk - 1) / kChunk;
-  it.c_begin = min(split * p.split_chunks, chunks);
-  it.c_end = min(it.c_begin + p.split_chunks, chunks);
-  return it;
+__device__ __forceinline__ Piece piece_make(const AttnParams& p, int f, int f_end, int prefix) {
+  Piece pc;
+  pc.pair = f / p.C;
+  const int c0 = f - pc.pair * p.C;
+  const int span = min(p.C - c0, f_end - f);
+  pc.next_f = f + span;
+  pc.r = pc.pair / p.n_kv;
+  pc.h = pc.pair % p.n_kv;
+  pc.keys = prefix + p.n;
+  const int A = min(p.C, (pc.keys + kChunk - 1) / kChunk);  // chunks this pair really has
+  pc.c0 = c0;
+  pc.c1 = min(c0 + span, A);
+  const int base = pc.pair * p.C;
+  pc.first_cta = base / p.Q;
+  pc.npieces = (base + A - 1) / p.Q - pc.first_cta + 1;
+  return pc;
+}
+__device__ __forceinline__ int piece_request(const AttnParams& p, int f) { return (f / p.C) / p.n_kv; }
+__device__ __forceinline__ Piece piece_at(const AttnParams& p, int f, int f_end) {
+  return piece_make(p, f, f_end, p.prefix[piece_request(p, f)]);
+}
+
+// Partial slot of the piece CTA `cta` holds for `pair`: 0 if it is the CTA's
+// first pair, else 1 (middle pieces of a CTA are always whole pairs).
+__device__ __forceinline__ int partial_slot(const AttnParams& p, int cta, int pair) {
+  return (cta * p.Q) / p.C == pair ? 2 * cta : 2 * cta + 1;
 }
 
 // Visibility of the 32 keys [p0, p0+32) for one query row: prefix keys are
@@ -134,23 +167,26 @@ __device__ __forceinline__ void tmem_st_pcols(uint32_t taddr, const uint32_t (&r
 // merged exactly in the epilogue like split-KV partials.
 //  * P never touches shared memory: it is written (hi + lo bf16 planes) over
 //    its own S buffer in TMEM and PV reads its A operand from there, so P is
-//    double-buffered with S and the shared memory holds kStages K/V chunks.
+//    triple-buffered with S and the shared memory holds kStages K/V chunks.
 //  * lazy rescale: a lane's reference max only moves when a score exceeds it
 //    by more than 2^8; otherwise P(c+1) is produced without waiting for
 //    PV(c), and only lanes whose reference moved rescale O in TMEM.
 template <int D, int R>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SMSP register file
     verify_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv_k,
-                            const __grid_constant__ CUtensorMap tm_kv_v, AttnParams p) {
+                            const __grid_constant__ CUtensorMap tm_kv_v, const __grid_constant__ CUtensorMap tm_v8,
+                            AttnParams p) {
   using L = AttnSmem<D>;
   constexpr int kStages = L::kStages;
   constexpr int kLanes = 128 / R;         // TMEM lanes per replica
   constexpr int kW = kChunk / R;          // key columns per replica
   constexpr int kCols = kW / 2;           // key columns per softmax thread per chunk
   constexpr int kOCols = D / 2;           // O columns per softmax thread (rescale / epilogue)
-  // TMEM columns: S/P buffer b at [128b, 128b+128) (P hi = first 64 columns,
-  // P lo = next 64, two bf16 per column), O at [256, 256+D)
-  constexpr uint32_t kOAcc = 256;
+  // TMEM columns: S/P buffer b < kSP at [128b, 128b+128) (P hi = first 64
+  // columns, P lo = next 64, two bf16 per column), O at [128*kSP, +D). Three
+  // S/P buffers let S(c+1) start before PV(c-1) has drained.
+  constexpr int kSP = 3;
+  constexpr uint32_t kOAcc = 128 * kSP;
   extern __shared__ uint8_t smem_raw[];
   // align within the shared array (keeps the shared address space visible to
   // the compiler: LDS/STS instead of generic LD/ST)
@@ -160,14 +196,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   // o_full: one phase per PV (chunk); o_last: one phase per item (its last
   // PV). Softmax warps skip o_full phases (lazy rescale), so the epilogue
   // waits on o_last, which every warp observes once per item.
-  __shared__ __align__(8) uint64_t s_full[2], s_empty[2], o_full, o_last, p_full;
+  __shared__ __align__(8) uint64_t s_full[kSP], s_empty[kSP], o_full, o_last, p_full;
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  TR_INIT();
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
+    }
+    for (int i = 0; i < kSP; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 1);
     }
@@ -182,20 +221,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tm_q);
     tma_prefetch_desc(&tm_kv_k);
     tma_prefetch_desc(&tm_kv_v);
+    tma_prefetch_desc(&tm_v8);
   }
   if (warp == 1) tmem_alloc<512>(&tmem_base_sh);
+  if (warp >= 2) {  // V tiles start finite (a last chunk keeps older rows past its end)
+    for (int st = 0; st < kStages; ++st)
+      for (int i = threadIdx.x - 64; i < L::kKvBytes / 16; i += 32 * kSoftWarps)
+        reinterpret_cast<uint4*>(smem + L::kKvOff + st * 2 * L::kKvBytes + L::kKvBytes)[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
+  const int f_begin = blockIdx.x * p.Q, f_end = min(p.total, f_begin + p.Q);
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (elect_one()) {
       int used = 0, gc = 0;
-      for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
-        const ItemInfo it = item_info(p, item);
-        if (it.c_end <= it.c_begin) continue;
+      for (int f = f_begin; f < f_end;) {
+        const Piece pc = piece_at(p, f, f_end);
+        f = pc.next_f;
+        if (pc.c1 <= pc.c0) continue;
         const int qb = used % L::kQBufs;
         mbar_wait(&q_empty[qb], ((used / L::kQBufs) & 1) ^ 1);
         ++used;
@@ -203,19 +251,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < L::kKBlocks; ++kb)
           for (int k = 0; k < R; ++k)
             tma_load_3d(smem + L::kQOff + qb * L::kQBytes + kb * 16384 + k * kLanes * 128, &tm_q, &q_full[qb],
-                        kb * 64, it.h * p.g, it.r * p.n);
-        const int row_base = (it.r * p.n_kv + it.h) * p.s_max;
-        for (int c = it.c_begin; c < it.c_end; ++c, ++gc) {
+                        kb * 64, pc.h * p.g, pc.r * p.n);
+        const int row_base = (pc.r * p.n_kv + pc.h) * p.s_max;
+        for (int c = pc.c0; c < pc.c1; ++c, ++gc) {
           const int s = gc % kStages;
           TR(0, 1);
           mbar_wait(&kv_empty[s], ((gc / kStages) & 1) ^ 1);
           TR(0, 2);
-          mbar_arrive_expect_tx(&kv_full[s], uint32_t(2 * L::kKvBytes));
           uint8_t* kdst = smem + L::kKvOff + s * 2 * L::kKvBytes;
           uint8_t* vdst = kdst + L::kKvBytes;
+          // a request's last chunk: V rows past its end (rounded up to 8) are
+          // not loaded, the tile keeps finite older rows there (P is zero)
+          const int vrows = min(kChunk, (pc.keys - c * kChunk + 7) & ~7);
+          mbar_arrive_expect_tx(&kv_full[s], uint32_t(L::kKvBytes + vrows * L::kKBlocks * 128));
           for (int kb = 0; kb < L::kKBlocks; ++kb) {
             tma_load_2d(kdst + kb * 16384, &tm_kv_k, &kv_full[s], kb * 64, row_base + c * kChunk);
-            tma_load_2d(vdst + kb * 16384, &tm_kv_v, &kv_full[s], kb * 64, row_base + c * kChunk);
+            if (vrows == kChunk) {
+              tma_load_2d(vdst + kb * 16384, &tm_kv_v, &kv_full[s], kb * 64, row_base + c * kChunk);
+            } else {
+              for (int r8 = 0; r8 < vrows; r8 += 8)
+                tma_load_2d(vdst + kb * 16384 + r8 * 128, &tm_v8, &kv_full[s], kb * 64, row_base + c * kChunk + r8);
+            }
           }
         }
       }
@@ -227,34 +283,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t id_o = make_idesc_bf16(128, D, /*b_mn_major=*/1);
       int used = 0, gc = 0;
       uint32_t p_phase = 0;
-      for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
-        const ItemInfo it = item_info(p, item);
-        if (it.c_end <= it.c_begin) continue;
+      for (int f = f_begin; f < f_end;) {
+        const Piece pc = piece_at(p, f, f_end);
+        f = pc.next_f;
+        if (pc.c1 <= pc.c0) continue;
         const int qb = used % L::kQBufs;
         mbar_wait(&q_full[qb], (used / L::kQBufs) & 1);
         ++used;
-        const uint32_t q_addr = smem_u32(smem + L::kQOff + qb * L::kQBytes);
-        const int nch = it.c_end - it.c_begin;
+        const uint64_t qd = make_sdesc_sw128(smem_u32(smem + L::kQOff + qb * L::kQBytes), 16, 1024);
+        const int nch = pc.c1 - pc.c0;
         // S(ci) may be issued once its K/V stage landed and its S/P buffer
         // was consumed by PV two chunks earlier
         auto s_ready = [&](int ci) {
           const int g2 = gc + ci;
           return mbar_test_wait(&kv_full[g2 % kStages], (g2 / kStages) & 1) &&
-                 mbar_test_wait(&s_empty[g2 & 1], ((g2 >> 1) & 1) ^ 1);
+                 mbar_test_wait(&s_empty[g2 % kSP], ((g2 / kSP) & 1) ^ 1);
         };
         auto issue_s = [&](int ci) {
           const int g2 = gc + ci;
-          const int s = g2 % kStages, sb = g2 & 1;
+          const int s = g2 % kStages, sb = g2 % kSP;
           TR(1, 1);
           mbar_wait(&kv_full[s], (g2 / kStages) & 1);
-          mbar_wait(&s_empty[sb], ((g2 >> 1) & 1) ^ 1);
+          mbar_wait(&s_empty[sb], ((g2 / kSP) & 1) ^ 1);
           tc_fence_after();
-          const uint32_t k_addr = smem_u32(smem + L::kKvOff + s * 2 * L::kKvBytes);
+          // descriptors are built once and advanced by constants: the single
+          // issuing thread must stay under the 64-cycle MMA time per step
+          const uint64_t kd = make_sdesc_sw128(smem_u32(smem + L::kKvOff + s * 2 * L::kKvBytes), 16, 1024);
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk / 4) * 16384 + (kk % 4) * 32;
-            umma_bf16(tmem + sb * 128, make_sdesc_sw128(q_addr + off, 16, 1024),
-                      make_sdesc_sw128(k_addr + off, 16, 1024), id_s, kk > 0 ? 1u : 0u);
+            const uint64_t off = uint64_t(((kk / 4) * 16384 + (kk % 4) * 32) >> 4);
+            umma_bf16(tmem + sb * 128, qd + off, kd + off, id_s, kk > 0 ? 1u : 0u);
           }
           umma_commit(&s_full[sb]);
           if (ci == nch - 1) umma_commit(&q_empty[qb]);
@@ -263,28 +321,44 @@ __global__ void __launch_bounds__(kThreads, 1)
         issue_s(0);
         for (int ci = 0; ci < nch; ++ci) {
           const int g2 = gc + ci;
-          const int s = g2 % kStages, sb = g2 & 1;
+          const int s = g2 % kStages, sb = g2 % kSP;
+          uint8_t* vbuf = smem + L::kKvOff + s * 2 * L::kKvBytes + L::kKvBytes;
+          // last chunk: the producer loaded V only up to the request's end
+          // rounded up to 8 rows; zero the loaded rows past the end (their P
+          // is zero, stale cache contents may be non-finite). The stage
+          // landed: S(ci) was issued after kv_full.
+          const int valid = pc.keys - (pc.c0 + ci) * kChunk;
+          if (valid < kChunk && (valid & 7)) {
+            for (int rr = valid; rr < ((valid + 7) & ~7); ++rr)
+#pragma unroll
+              for (int kb = 0; kb < L::kKBlocks; ++kb)
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                  *reinterpret_cast<uint4*>(vbuf + kb * 16384 + rr * 128 + t * 16) = make_uint4(0, 0, 0, 0);
+            fence_proxy_async();
+          }
           TR(1, 4);
           // PV(ci) must not queue behind the next chunk's K/V load (it frees
           // that load's stage): issue S(ci+1) early only if it is ready
           bool next_issued = ci + 1 >= nch;
-          while (!mbar_test_wait(&p_full, p_phase)) {
-            if (!next_issued && s_ready(ci + 1)) {
+          while (!next_issued && !mbar_test_wait(&p_full, p_phase)) {
+            if (s_ready(ci + 1)) {
               issue_s(ci + 1);
               next_issued = true;
             }
           }
+          mbar_wait(&p_full, p_phase);
           TR(1, 5);
           p_phase ^= 1;
           tc_fence_after();
-          const uint32_t v_addr = smem_u32(smem + L::kKvOff + s * 2 * L::kKvBytes + L::kKvBytes);
+          const uint64_t vd = make_sdesc_sw128(smem_u32(vbuf), 16384, 1024);
+          const uint32_t pt = tmem + sb * 128;
           // O += P_hi V + P_lo V with P read from TMEM: P carried to ~16
           // mantissa bits
 #pragma unroll
           for (int kk = 0; kk < kChunk / 16; ++kk) {
-            const uint64_t vd = make_sdesc_sw128(v_addr + kk * 2048, 16384, 1024);
-            umma_bf16_ts(tmem + kOAcc, tmem + sb * 128 + kk * 8, vd, id_o, (ci > 0 || kk > 0) ? 1u : 0u);
-            umma_bf16_ts(tmem + kOAcc, tmem + sb * 128 + 64 + kk * 8, vd, id_o, 1u);
+            umma_bf16_ts(tmem + kOAcc, pt + kk * 8, vd + uint64_t(kk * 128), id_o, (ci > 0 || kk > 0) ? 1u : 0u);
+            umma_bf16_ts(tmem + kOAcc, pt + 64 + kk * 8, vd + uint64_t(kk * 128), id_o, 1u);
           }
           umma_commit(&o_full);
           if (ci + 1 == nch) umma_commit(&o_last);
@@ -305,36 +379,65 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int lrow = q4 * 32 + lane;            // TMEM lane = Q tile row
     const int rep = lrow / kLanes;              // warp-uniform (kLanes >= 32)
     const int row = lrow % kLanes;              // query row (i*g + hh)
+    const int stid = threadIdx.x - 64;          // 0..255 over the softmax warps
     const uint32_t tlane = uint32_t(q4 * 32) << 16;
     const bool warp_live = (q4 * 32) % kLanes < p.rows;
+    const bool live = row < p.rows;
+    const int qi = live ? row / p.g : 0;
     const int col0 = rep * kW + half * kCols;   // this thread's key columns in a chunk
     const int oc0 = half * kOCols;              // this thread's O columns
     const uint32_t pair_bar = 1 + q4;           // named barrier of the two warps of a quadrant
+    __shared__ int last_sh;
     int gc = 0, items_done = 0;
-    for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
-      const ItemInfo it = item_info(p, item);
-      const int nch = it.c_end - it.c_begin;
-      if (nch <= 0) {  // empty split (only with split-KV): no keys, m = -inf
-        if (p.splits > 1 && rep == 0 && half == 0 && row < p.rows)
-          p.ws_ml[size_t(item) * p.rows + row] = make_float2(-INFINITY, 0.f);
-        continue;
+    // per-row output offsets (query i, head hh of the KV group) in rows of D
+    __shared__ int row_off_sh[128];
+    for (int rr = stid; rr < p.rows; rr += 32 * kSoftWarps) row_off_sh[rr] = (rr / p.g) * p.n_q + rr % p.g;
+    asm volatile("bar.sync 5, 256;" ::: "memory");
+    // the next piece's prefix length and mask word are loaded one piece ahead
+    // (pf_*), so the epilogue does not wait on them
+    int f = f_begin;
+    Piece pc{};
+    uint64_t mword = 0;
+    int pf_prefix = -1;
+    uint64_t pf_mask = 0;
+    auto advance = [&]() {
+      bool first = true;
+      while (f < f_end) {
+        const int rq = piece_request(p, f);
+        const int pre = first && pf_prefix >= 0 ? pf_prefix : p.prefix[rq];
+        const uint64_t mw = first && pf_prefix >= 0 ? pf_mask : (live ? p.mask[rq * p.n + qi] : 0ull);
+        first = false;
+        pc = piece_make(p, f, f_end, pre);
+        f = pc.next_f;
+        if (pc.c1 > pc.c0) {
+          mword = mw;
+          return true;
+        }
       }
-      const bool live = row < p.rows;
-      const int qi = live ? row / p.g : 0;
-      const int hh = live ? row % p.g : 0;
-      uint64_t mbits = live ? p.mask[it.r * p.n + qi] : 0ull;
+      return false;
+    };
+    bool have = advance();
+    while (have) {
+      const int nch = pc.c1 - pc.c0;
+      pf_prefix = -1;
+      if (f < f_end) {
+        const int rq = piece_request(p, f);
+        pf_prefix = __ldg(p.prefix + rq);
+        pf_mask = live ? __ldg(p.mask + rq * p.n + qi) : 0ull;
+      }
+      uint64_t mbits = mword;
       if (p.n < 64) mbits &= (1ull << p.n) - 1ull;
-      const int prefix = live ? it.keys - p.n : 0;
+      const int prefix = live ? pc.keys - p.n : 0;
       float m_ref = -INFINITY, l_run = 0.f;  // reference max (log2 units), partial row sum
       if (warp == 4 && lane == 0) TR(2, 11);
       for (int ci = 0; ci < nch; ++ci) {
         const int g2 = gc + ci;
-        const int sb = g2 & 1;
-        const int key0 = (it.c_begin + ci) * kChunk;
+        const int sb = g2 % kSP;
+        const int key0 = (pc.c0 + ci) * kChunk;
         uint8_t* kbuf = smem + L::kKvOff + (g2 % kStages) * 2 * L::kKvBytes;
         const uint32_t tsp = tmem + tlane + sb * 128;  // this quadrant's S/P buffer
         if (warp == 4 && lane == 0) TR(2, 1);
-        mbar_wait(&s_full[sb], (g2 >> 1) & 1);
+        mbar_wait(&s_full[sb], (g2 / kSP) & 1);
         if (warp == 4 && lane == 0) TR(2, 2);
         tc_fence_after();
         // this chunk's K tile is dead once S is in TMEM (it is refilled only
@@ -366,19 +469,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
         float psum = 0.f;
         if (warp_live) {
-          uint32_t phi[kCols / 2], plo[kCols / 2];
+          // 32-key blocks keep the register footprint flat. P = hi + lo: hi is
+          // the truncated bf16 pair (one PRMT), lo = p - hi is exact in fp32 and
+          // rounded once (one cvt per pair): |error| <= 2^-16 p
+          constexpr int kB = kCols < 32 ? kCols : 32;
 #pragma unroll
-          for (int j = 0; j < kCols; j += 2) {
-            const float a = ((vb[j / 32] >> (j % 32)) & 1u) ? ex2_approx(__uint_as_float(sv[j]) * p.scale_log2 - m_use) : 0.f;
-            const float b =
-                ((vb[j / 32] >> ((j + 1) % 32)) & 1u) ? ex2_approx(__uint_as_float(sv[j + 1]) * p.scale_log2 - m_use) : 0.f;
-            psum += a + b;
-            const uint32_t hh2 = pack_bf16x2(a, b);
-            phi[j / 2] = hh2;
-            plo[j / 2] = pack_bf16x2(a - __uint_as_float(hh2 << 16), b - __uint_as_float(hh2 & 0xffff0000u));
+          for (int c = 0; c < kCols; c += kB) {
+            uint32_t phi[kB / 2], plo[kB / 2];
+#pragma unroll
+            for (int j = c; j < c + kB; j += 2) {
+              const float a = ((vb[j / 32] >> (j % 32)) & 1u) ? ex2_approx(__uint_as_float(sv[j]) * p.scale_log2 - m_use) : 0.f;
+              const float b =
+                  ((vb[j / 32] >> ((j + 1) % 32)) & 1u) ? ex2_approx(__uint_as_float(sv[j + 1]) * p.scale_log2 - m_use) : 0.f;
+              psum += a + b;
+              const uint32_t ua = __float_as_uint(a), ub = __float_as_uint(b);
+              phi[(j - c) / 2] = __byte_perm(ua, ub, 0x7632);
+              plo[(j - c) / 2] = pack_bf16x2(a - __uint_as_float(ua & 0xffff0000u), b - __uint_as_float(ub & 0xffff0000u));
+            }
+            tmem_st_pcols<kB>(tsp + (col0 + c) / 2, phi);
+            tmem_st_pcols<kB>(tsp + 64 + (col0 + c) / 2, plo);
           }
-          tmem_st_pcols<kCols>(tsp + col0 / 2, phi);
-          tmem_st_pcols<kCols>(tsp + 64 + col0 / 2, plo);
           if constexpr (R > 1) {
             // keys of other replicas: zero P for this lane (half 0 the hi
             // plane, half 1 the lo plane)
@@ -392,17 +502,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         l_run = l_run * alpha + psum;
         m_ref = m_new;
-        // keys past the request's end in the last chunk: zero their V rows so
-        // stale (possibly non-finite) cache contents cannot reach the MMA
-        if (half == 0 && key0 + kChunk > it.keys && key0 + lrow >= it.keys) {
-          uint8_t* vbuf = kbuf + L::kKvBytes;
-#pragma unroll
-          for (int kb = 0; kb < L::kKBlocks; ++kb)
-#pragma unroll
-            for (int t = 0; t < 8; ++t)
-              *reinterpret_cast<uint4*>(vbuf + kb * 16384 + lrow * 128 + t * 16) = make_uint4(0, 0, 0, 0);
-          fence_proxy_async();
-        }
+        if (warp == 4 && lane == 0) TR(2, 20);
+        if (warp == 4 && lane == 0) TR(2, 21);
         // lanes whose reference max moved rescale O (and only after PV(ci-1))
         if (ci > 0 && warp_live && __any_sync(0xffffffffu, live && alpha != 1.f)) {
           mbar_wait(&o_full, (g2 - 1) & 1);
@@ -428,42 +529,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       ++items_done;
       tc_fence_after();
       if (warp == 4 && lane == 0) TR(2, 6);
+      const Piece cur = pc;
+      const bool whole = cur.npieces == 1;
+      have = advance();
       // ---- epilogue. The last chunk's K/V stage is held for us (released
-      // below): first the (m, l) exchange at its V tile, then the weighted
-      // replica partials [R][rows][D] fp32 over the whole stage (16-byte
-      // pieces XOR-swizzled by row).
-      uint8_t* kbuf = smem + L::kKvOff + ((gc + nch - 1) % kStages) * 2 * L::kKvBytes;
-      float* slots = reinterpret_cast<float*>(kbuf);
-      float* lsum = reinterpret_cast<float*>(kbuf + L::kKvBytes);            // [2][128]
-      float2* ml = reinterpret_cast<float2*>(kbuf + L::kKvBytes + 1024);     // [128]
+      // below): first the (m, l) exchange in its V tile, then the weighted
+      // replica partials [R][kLanes][D] fp32 over the stage (16-byte pieces
+      // XOR-swizzled by row), summed by all softmax threads with coalesced
+      // stores.
       const int s_last = (gc + nch - 1) % kStages;
       gc += nch;
+      uint8_t* stage = smem + L::kKvOff + s_last * 2 * L::kKvBytes;
+      float* slots = reinterpret_cast<float*>(stage);
+      float* lsum = reinterpret_cast<float*>(stage + L::kKvBytes);         // [2][128]
+      float2* ml = reinterpret_cast<float2*>(stage + L::kKvBytes + 1024);  // [128]
       lsum[half * 128 + lrow] = l_run;
       asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
       const float l_tot = l_run + lsum[(half ^ 1) * 128 + lrow];
-      float M = m_ref, Ls = l_tot;
+      if (half == 0) ml[lrow] = make_float2(m_ref, l_tot);
+      asm volatile("bar.sync 5, 256;" ::: "memory");
       if (warp == 4 && lane == 0) TR(2, 7);
-      if constexpr (R > 1) {
-        if (half == 0) ml[lrow] = make_float2(m_ref, l_tot);
-        asm volatile("bar.sync 5, 256;" ::: "memory");
-        if (live) {
-          M = -INFINITY;
+      float M = -INFINITY, Ls = 0.f;
+      if (live) {
 #pragma unroll
-          for (int k = 0; k < R; ++k) M = fmaxf(M, ml[row + k * kLanes].x);
-          Ls = 0.f;
+        for (int k = 0; k < R; ++k) M = fmaxf(M, ml[row + k * kLanes].x);
 #pragma unroll
-          for (int k = 0; k < R; ++k) {
-            const float2 v = ml[row + k * kLanes];
-            if (v.x != -INFINITY) Ls += v.y * ex2_approx(v.x - M);
-          }
+        for (int k = 0; k < R; ++k) {
+          const float2 v = ml[row + k * kLanes];
+          if (v.x != -INFINITY) Ls += v.y * ex2_approx(v.x - M);
         }
-        asm volatile("bar.sync 5, 256;" ::: "memory");  // ml / lsum read: the stage becomes slots
-        if (warp == 4 && lane == 0) TR(2, 12);
       }
-      // this replica's weight in the merged row (normalised unless split-KV
-      // partials are written for attn_combine_kernel)
+      // this replica's weight in the merged row (normalised for whole pieces)
       float wgt = (live && m_ref != -INFINITY) ? ex2_approx(m_ref - M) : 0.f;
-      if (p.splits == 1) wgt *= Ls > 0.f ? 1.f / Ls : 0.f;
+      if (whole) wgt *= Ls > 0.f ? 1.f / Ls : 0.f;
+      asm volatile("bar.sync 5, 256;" ::: "memory");  // ml / lsum read: the stage becomes slots
       if (warp_live) {
 #pragma unroll 1
         for (int c0 = 0; c0 < kOCols; c0 += 32) {
@@ -471,73 +570,122 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld32(tmem + tlane + kOAcc + oc0 + c0, r);
           tmem_ld_wait();
           if (!live) continue;
-          const int col = oc0 + c0;
-          if constexpr (R == 1) {
-            if (p.splits == 1) {
-              uint16_t* dst = p.out + ((size_t(it.r) * p.n + qi) * p.n_q + size_t(it.h) * p.g + hh) * D + col;
+          float4* slot = reinterpret_cast<float4*>(slots) + (rep * kLanes + row) * (D / 4);
 #pragma unroll
-              for (int j = 0; j < 32; j += 8) {
-                uint4 v;
-                v.x = pack_bf16x2(__uint_as_float(r[j]) * wgt, __uint_as_float(r[j + 1]) * wgt);
-                v.y = pack_bf16x2(__uint_as_float(r[j + 2]) * wgt, __uint_as_float(r[j + 3]) * wgt);
-                v.z = pack_bf16x2(__uint_as_float(r[j + 4]) * wgt, __uint_as_float(r[j + 5]) * wgt);
-                v.w = pack_bf16x2(__uint_as_float(r[j + 6]) * wgt, __uint_as_float(r[j + 7]) * wgt);
-                *reinterpret_cast<uint4*>(dst + j) = v;
-              }
-            } else {
-              float* dst = p.ws_o + (size_t(item) * p.rows + row) * D + col;
-#pragma unroll
-              for (int j = 0; j < 32; j += 4)
-                *reinterpret_cast<float4*>(dst + j) =
-                    make_float4(__uint_as_float(r[j]) * wgt, __uint_as_float(r[j + 1]) * wgt,
-                                __uint_as_float(r[j + 2]) * wgt, __uint_as_float(r[j + 3]) * wgt);
-            }
-          } else {
-            float4* slot = reinterpret_cast<float4*>(slots) + (rep * kLanes + row) * (D / 4);
-#pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              slot[((col + j) / 4) ^ (row & 7)] =
-                  make_float4(__uint_as_float(r[j]) * wgt, __uint_as_float(r[j + 1]) * wgt,
-                              __uint_as_float(r[j + 2]) * wgt, __uint_as_float(r[j + 3]) * wgt);
-          }
+          for (int j = 0; j < 32; j += 4)
+            slot[((oc0 + c0 + j) / 4) ^ (row & 7)] =
+                make_float4(__uint_as_float(r[j]) * wgt, __uint_as_float(r[j + 1]) * wgt,
+                            __uint_as_float(r[j + 2]) * wgt, __uint_as_float(r[j + 3]) * wgt);
         }
       }
-      if constexpr (R > 1) {
-        asm volatile("bar.sync 5, 256;" ::: "memory");
-        if (warp == 4 && lane == 0) TR(2, 13);
-        // replica 0's threads sum the R partials in a fixed order
-        if (rep == 0 && live) {
-          const float4* s4 = reinterpret_cast<const float4*>(slots);
+      tc_fence_before();  // TMEM O reads done before the next piece's PV overwrites it
+      asm volatile("bar.sync 5, 256;" ::: "memory");
+      if (warp == 4 && lane == 0) TR(2, 13);
+      const int my_slot = whole ? 0 : partial_slot(p, blockIdx.x, cur.pair);
+      {
+        // replicas summed in a fixed order; thread -> (row, 4 columns)
+        const float4* s4 = reinterpret_cast<const float4*>(slots);
+        for (int e = stid; e < p.rows * (D / 4); e += 32 * kSoftWarps) {
+          const int rr = e / (D / 4), c4 = e % (D / 4);
+          float4 a = s4[rr * (D / 4) + (c4 ^ (rr & 7))];
 #pragma unroll
-          for (int j = 0; j < kOCols; j += 8) {
-            float4 a = s4[row * (D / 4) + (((oc0 + j) / 4) ^ (row & 7))];
-            float4 b = s4[row * (D / 4) + (((oc0 + j) / 4 + 1) ^ (row & 7))];
-#pragma unroll
-            for (int k = 1; k < R; ++k) {
-              const float4 a2 = s4[(k * kLanes + row) * (D / 4) + (((oc0 + j) / 4) ^ (row & 7))];
-              const float4 b2 = s4[(k * kLanes + row) * (D / 4) + (((oc0 + j) / 4 + 1) ^ (row & 7))];
-              a.x += a2.x; a.y += a2.y; a.z += a2.z; a.w += a2.w;
-              b.x += b2.x; b.y += b2.y; b.z += b2.z; b.w += b2.w;
-            }
-            if (p.splits == 1) {
-              uint16_t* dst = p.out + ((size_t(it.r) * p.n + qi) * p.n_q + size_t(it.h) * p.g + hh) * D + oc0 + j;
-              *reinterpret_cast<uint4*>(dst) =
-                  make_uint4(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y), pack_bf16x2(b.z, b.w));
-            } else {
-              float* dst = p.ws_o + (size_t(item) * p.rows + row) * D + oc0 + j;
-              *reinterpret_cast<float4*>(dst) = a;
-              *reinterpret_cast<float4*>(dst + 4) = b;
-            }
+          for (int k = 1; k < R; ++k) {
+            const float4 b = s4[(k * kLanes + rr) * (D / 4) + (c4 ^ (rr & 7))];
+            a.x += b.x;
+            a.y += b.y;
+            a.z += b.z;
+            a.w += b.w;
+          }
+          if (whole) {
+            uint16_t* dst = p.out + (size_t(cur.r) * p.n * p.n_q + size_t(cur.h) * p.g + row_off_sh[rr]) * D;
+            *reinterpret_cast<uint2*>(dst + 4 * c4) = make_uint2(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w));
+          } else {
+            reinterpret_cast<float4*>(p.ws_o + (size_t(my_slot) * p.rows + rr) * D)[c4] = a;
           }
         }
+        if (!whole && live && rep == 0 && half == 0) p.ws_ml[size_t(my_slot) * p.rows + row] = make_float2(M, Ls);
       }
       if (warp == 4 && lane == 0) TR(2, 9);
-      if (live && rep == 0 && half == 0 && p.splits > 1) p.ws_ml[size_t(item) * p.rows + row] = make_float2(M, Ls);
-      // all scratch reads and TMEM O reads done -> hand the stage back to the producer
-      tc_fence_before();
+      if (!whole) {
+        // publish the partial; the pair's last piece merges all of them
+        __threadfence();
+        asm volatile("bar.sync 5, 256;" ::: "memory");
+        if (warp == 4 && lane == 0) TR(2, 30);
+        if (stid == 0) last_sh = atomicAdd(p.ws_cnt + cur.pair, 1) == cur.npieces - 1;
+        asm volatile("bar.sync 5, 256;" ::: "memory");
+        if (warp == 4 && lane == 0) TR(2, 31);
+        if (last_sh) {
+          __threadfence();
+          // merge weights w[j][row] = 2^(m_j - M) / L into the stage, slot
+          // indices of the pair's pieces first (npieces <= 16)
+          float* w = slots;
+          int* slot_of = reinterpret_cast<int*>(slots + 16 * 128);
+          if (stid < cur.npieces) slot_of[stid] = partial_slot(p, cur.first_cta + stid, cur.pair);
+          asm volatile("bar.sync 5, 256;" ::: "memory");
+          const int np = cur.npieces;
+          for (int rr = stid; rr < p.rows; rr += 32 * kSoftWarps) {
+            float Mx = -INFINITY, Lx = 0.f;
+#pragma unroll 4
+            for (int j = 0; j < np; ++j) Mx = fmaxf(Mx, __ldcg(&p.ws_ml[size_t(slot_of[j]) * p.rows + rr]).x);
+#pragma unroll 4
+            for (int j = 0; j < np; ++j) {
+              const float2 v = __ldcg(&p.ws_ml[size_t(slot_of[j]) * p.rows + rr]);
+              const float e2 = v.x == -INFINITY ? 0.f : ex2_approx(v.x - Mx);
+              w[j * 128 + rr] = e2;
+              Lx += v.y * e2;
+            }
+            const float inv = Lx > 0.f ? 1.f / Lx : 0.f;
+            for (int j = 0; j < np; ++j) w[j * 128 + rr] *= inv;
+          }
+          if (warp == 4 && lane == 0) TR(2, 32);
+          asm volatile("bar.sync 5, 256;" ::: "memory");
+          // every thread keeps kE independent partial loads in flight (the
+          // L2 round trip, not bandwidth, bounds this loop)
+          constexpr int kE = 4;
+          const int n_e = p.rows * (D / 4);
+          for (int e0 = stid; e0 < n_e; e0 += 32 * kSoftWarps * kE) {
+            float4 acc[kE];
+#pragma unroll
+            for (int u = 0; u < kE; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int j = 0; j < np; ++j) {
+              const float4* src = reinterpret_cast<const float4*>(p.ws_o + size_t(slot_of[j]) * p.rows * D);
+              float4 v[kE];
+#pragma unroll
+              for (int u = 0; u < kE; ++u) {
+                const int e = e0 + u * 32 * kSoftWarps;
+                if (e < n_e) v[u] = __ldcg(src + e);
+              }
+#pragma unroll
+              for (int u = 0; u < kE; ++u) {
+                const int e = e0 + u * 32 * kSoftWarps;
+                if (e < n_e) {
+                  const float wj = w[j * 128 + e / (D / 4)];
+                  acc[u].x += v[u].x * wj;
+                  acc[u].y += v[u].y * wj;
+                  acc[u].z += v[u].z * wj;
+                  acc[u].w += v[u].w * wj;
+                }
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < kE; ++u) {
+              const int e = e0 + u * 32 * kSoftWarps;
+              if (e < n_e) {
+                const int rr = e / (D / 4), c4 = e % (D / 4);
+                uint16_t* dst = p.out + (size_t(cur.r) * p.n * p.n_q + size_t(cur.h) * p.g + row_off_sh[rr]) * D;
+                *reinterpret_cast<uint2*>(dst + 4 * c4) =
+                    make_uint2(pack_bf16x2(acc[u].x, acc[u].y), pack_bf16x2(acc[u].z, acc[u].w));
+              }
+            }
+          }
+          if (warp == 4 && lane == 0) TR(2, 33);
+          if (stid == 0) p.ws_cnt[cur.pair] = 0;  // ready for the next launch
+        }
+      }
+      // all stage reads done -> hand the stage back to the producer
       fence_proxy_async();
       asm volatile("bar.sync 5, 256;" ::: "memory");
-      if (warp == 2 && lane == 0) mbar_arrive(&kv_empty[s_last]);
+      if (stid == 0) mbar_arrive(&kv_empty[s_last]);
       if (warp == 4 && lane == 0) TR(2, 10);
     }
   }
@@ -546,59 +694,49 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
-// Merge the split-KV partials: O = sum_s O_s 2^(m_s - M) / sum_s l_s 2^(m_s - M).
-template <int D>
-__global__ void attn_combine_kernel(AttnParams p) {
-  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
-  const int lane = threadIdx.x % 32;
-  const int pairs = p.b * p.n_kv;
-  if (warp_global >= pairs * p.rows) return;
-  const int pair = warp_global / p.rows, row = warp_global % p.rows;
-  const int r = pair / p.n_kv, h = pair % p.n_kv;
-  float M = -INFINITY;
-  for (int s = 0; s < p.splits; ++s) M = fmaxf(M, p.ws_ml[size_t(pair * p.splits + s) * p.rows + row].x);
-  constexpr int V = D / 32;
-  float acc[V];
-#pragma unroll
-  for (int v = 0; v < V; ++v) acc[v] = 0.f;
-  float L = 0.f;
-  for (int s = 0; s < p.splits; ++s) {
-    const size_t item = size_t(pair) * p.splits + s;
-    const float2 ml = p.ws_ml[item * p.rows + row];
-    if (ml.x == -INFINITY) continue;
-    const float w = exp2f(ml.x - M);
-    L += ml.y * w;
-    const float* src = p.ws_o + (item * p.rows + row) * D;
-#pragma unroll
-    for (int v = 0; v < V; ++v) acc[v] += src[lane + 32 * v] * w;
-  }
-  const float inv = L > 0.f ? 1.f / L : 0.f;
-  const int qi = row / p.g, hh = row % p.g;
-  uint16_t* dst = p.out + ((size_t(r) * p.n + qi) * p.n_q + size_t(h) * p.g + hh) * D;
-#pragma unroll
-  for (int v = 0; v < V; ++v) dst[lane + 32 * v] = f2bf(acc[v] * inv);
-}
 
 struct AttnPlan {
-  int splits, split_chunks, items, grid;
-  size_t ws_bytes;
+  int C, Q, total, grid;
+  size_t ws_o_off, ws_ml_off, ws_cnt_off, ws_bytes;
 };
 
+constexpr size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Flat schedule: C chunk slots per (request, KV head), Q consecutive slots per
+// CTA so that the grid fills the SMs once; Q >= C/15 keeps a pair's pieces
+// (the in-kernel merge reads all of them from one CTA) within 16. Workspace: two partial slots per CTA
+// (sized for a full grid, so it does not depend on the prefix lengths) and
+// one counter per pair.
 AttnPlan plan_attention(const smo_attn_args& a, int sms) {
   AttnPlan pl{};
-  const int g = a.n_q / a.n_kv;
-  const int rows = g * a.n;
-  const int max_keys = std::max(1, a.max_prefix + a.n);
-  const int chunks = (max_keys + kChunk - 1) / kChunk;
+  const int rows = (a.n_q / a.n_kv) * a.n;
   const int pairs = a.b * a.n_kv;
-  // enough items for ~2 rounds of the persistent grid, at least 2 chunks each
-  int splits = std::max(1, std::min(chunks, (2 * sms + pairs - 1) / pairs));
-  if (splits > 1) splits = std::min(splits, std::max(1, chunks / 2));
-  pl.split_chunks = (chunks + splits - 1) / splits;
-  pl.splits = (chunks + pl.split_chunks - 1) / pl.split_chunks;
-  pl.items = pairs * pl.splits;
-  pl.grid = std::min(pl.items, sms);
-  pl.ws_bytes = pl.splits > 1 ? size_t(pl.items) * rows * (a.d * sizeof(float) + sizeof(float2)) : 0;
+  pl.C = std::max(1, (a.max_prefix + a.n + kChunk - 1) / kChunk);
+  pl.total = pairs * pl.C;
+  // Q: at least total/sms (one wave). Candidates aligned with pairs (a
+  // multiple or a divisor of C) avoid partial pieces; pick the lowest
+  // modelled CTA time  Q*t_chunk + pieces*t_epilogue + partials*t_merge
+  // (t ~ 1.6 / 4 / 3 us, measured on B200, profiles/).
+  const int qmin = (pl.total + sms - 1) / sms;
+  auto cost = [&](int q) {
+    const bool aligned = q % pl.C == 0 || pl.C % q == 0;
+    const double pieces = q >= pl.C ? double(q) / pl.C + (aligned ? 0.0 : 1.0) : (aligned ? 1.0 : 2.0);
+    const double partials = aligned ? (q >= pl.C ? 0.0 : 1.0) : 2.0;
+    return q * 1.6 + pieces * 4.0 + partials * 3.0;
+  };
+  int q = qmin;
+  const int qa = qmin >= pl.C ? pl.C * ((qmin + pl.C - 1) / pl.C) : [&] {
+    for (int d = qmin; d <= pl.C; ++d)
+      if (pl.C % d == 0) return d;
+    return pl.C;
+  }();
+  if (cost(qa) < cost(qmin)) q = qa;
+  pl.Q = std::max(q, (pl.C + 14) / 15);
+  pl.grid = (pl.total + pl.Q - 1) / pl.Q;
+  pl.ws_o_off = 0;
+  pl.ws_ml_off = align256(size_t(sms) * 2 * rows * a.d * sizeof(float));
+  pl.ws_cnt_off = pl.ws_ml_off + align256(size_t(sms) * 2 * rows * sizeof(float2));
+  pl.ws_bytes = pl.ws_cnt_off + align256(size_t(pairs) * sizeof(int));
   return pl;
 }
 
@@ -615,7 +753,7 @@ int device_sms() {
 
 template <int D, int R>
 void launch_k1(int grid, cudaStream_t stream, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-               const AttnParams& p) {
+               const CUtensorMap& tv8, const AttnParams& p) {
   constexpr size_t smem = AttnSmem<D>::kTotal + 1024;
   static bool set = false;
   if (!set) {
@@ -623,7 +761,7 @@ void launch_k1(int grid, cudaStream_t stream, const CUtensorMap& tq, const CUten
                                         int(smem)));
     set = true;
   }
-  verify_attention_kernel<D, R><<<grid, kThreads, smem, stream>>>(tq, tk, tv, p);
+  verify_attention_kernel<D, R><<<grid, kThreads, smem, stream>>>(tq, tk, tv, tv8, p);
 }
 
 void check_attn_args(const smo_attn_args& a) {
@@ -646,16 +784,16 @@ size_t attention_workspace(const smo_attn_args& a) {
 void attention_launch(const smo_attn_args& a, cudaStream_t stream) {
   check_attn_args(a);
   const AttnPlan pl = plan_attention(a, device_sms());
-  SMO_REQUIRE(pl.ws_bytes == 0 || (a.workspace && a.workspace_bytes >= pl.ws_bytes),
-              "attention: workspace too small");
+  SMO_REQUIRE(a.workspace && a.workspace_bytes >= pl.ws_bytes, "attention: workspace too small");
   const int g = a.n_q / a.n_kv;
+  uint8_t* ws = reinterpret_cast<uint8_t*>(a.workspace);
   AttnParams p{};
   p.mask = a.mask;
   p.prefix = a.prefix_len;
   p.out = reinterpret_cast<uint16_t*>(a.out);
-  p.ws_o = reinterpret_cast<float*>(a.workspace);
-  p.ws_ml = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(a.workspace) +
-                                      (pl.ws_bytes ? size_t(pl.items) * g * a.n * a.d * sizeof(float) : 0));
+  p.ws_o = reinterpret_cast<float*>(ws + pl.ws_o_off);
+  p.ws_ml = reinterpret_cast<float2*>(ws + pl.ws_ml_off);
+  p.ws_cnt = reinterpret_cast<int*>(ws + pl.ws_cnt_off);
   p.b = a.b;
   p.n = a.n;
   p.n_q = a.n_q;
@@ -663,12 +801,12 @@ void attention_launch(const smo_attn_args& a, cudaStream_t stream) {
   p.g = g;
   p.rows = g * a.n;
   p.s_max = a.s_max;
-  p.splits = pl.splits;
-  p.split_chunks = pl.split_chunks;
-  p.items = pl.items;
+  p.C = pl.C;
+  p.Q = pl.Q;
+  p.total = pl.total;
   p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(a.d)));
 
-  CUtensorMap tq, tk, tv;
+  CUtensorMap tq, tk, tv, tv8;
   {
     uint64_t dims[3] = {uint64_t(a.d), uint64_t(a.n_q), uint64_t(a.b) * a.n};
     uint64_t strides[2] = {uint64_t(a.d) * 2, uint64_t(a.n_q) * a.d * 2};
@@ -681,30 +819,22 @@ void attention_launch(const smo_attn_args& a, cudaStream_t stream) {
     uint32_t box[2] = {64, uint32_t(kChunk)};
     make_tmap_bf16(&tk, a.k_cache, 2, dims, strides, box, true);
     make_tmap_bf16(&tv, a.v_cache, 2, dims, strides, box, true);
+    uint32_t box8[2] = {64, 8};
+    make_tmap_bf16(&tv8, a.v_cache, 2, dims, strides, box8, true);
   }
   // query-row replication: as many copies of the g*n rows as fit the 128 lanes
   const int R = p.rows <= 32 ? 4 : (p.rows <= 64 ? 2 : 1);
   if (a.d == 128) {
-    if (R == 4) launch_k1<128, 4>(pl.grid, stream, tq, tk, tv, p);
-    else if (R == 2) launch_k1<128, 2>(pl.grid, stream, tq, tk, tv, p);
-    else launch_k1<128, 1>(pl.grid, stream, tq, tk, tv, p);
+    if (R == 4) launch_k1<128, 4>(pl.grid, stream, tq, tk, tv, tv8, p);
+    else if (R == 2) launch_k1<128, 2>(pl.grid, stream, tq, tk, tv, tv8, p);
+    else launch_k1<128, 1>(pl.grid, stream, tq, tk, tv, tv8, p);
   } else {
-    if (R == 4) launch_k1<64, 4>(pl.grid, stream, tq, tk, tv, p);
-    else if (R == 2) launch_k1<64, 2>(pl.grid, stream, tq, tk, tv, p);
-    else launch_k1<64, 1>(pl.grid, stream, tq, tk, tv, p);
+    if (R == 4) launch_k1<64, 4>(pl.grid, stream, tq, tk, tv, tv8, p);
+    else if (R == 2) launch_k1<64, 2>(pl.grid, stream, tq, tk, tv, tv8, p);
+    else launch_k1<64, 1>(pl.grid, stream, tq, tk, tv, tv8, p);
   }
   count_launch();
   SMO_CUDA_CHECK(cudaGetLastError());
-  if (pl.splits > 1) {
-    const int warps = a.b * a.n_kv * p.rows;
-    const int blocks = (warps * 32 + 255) / 256;
-    if (a.d == 128)
-      attn_combine_kernel<128><<<blocks, 256, 0, stream>>>(p);
-    else
-      attn_combine_kernel<64><<<blocks, 256, 0, stream>>>(p);
-    count_launch();
-    SMO_CUDA_CHECK(cudaGetLastError());
-  }
 }
 
 // ---------------------------------------------------------------------------

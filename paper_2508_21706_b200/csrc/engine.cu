@@ -364,15 +364,9 @@ struct Engine {
     wa.mask = reinterpret_cast<const uint64_t*>(1);
     wa.prefix_len = reinterpret_cast<const int32_t*>(1);
     attn_ws_bytes = attention_workspace(wa);
-    // split planning gives items <= pairs * ceil(2*SMs / pairs) <= 2*SMs + pairs
-    // for any batch <= maxB and prefix <= s_max - n: size for that bound
-    {
-      int sms = 0;
-      SMO_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, opt.device));
-      const size_t bound = size_t(2 * sms + maxB * nkv) * size_t(nq / nkv) * maxN * (size_t(d) * 4 + 8);
-      attn_ws_bytes = std::max(attn_ws_bytes, bound);
-    }
-    attn_ws = attn_ws_bytes ? dalloc<uint8_t>(attn_ws_bytes) : nullptr;
+    // (the flat-schedule workspace is sized for a full grid at maxB, any prefix)
+    attn_ws = dalloc<uint8_t>(attn_ws_bytes);
+    SMO_CUDA_CHECK(cudaMemset(attn_ws, 0, attn_ws_bytes));  // K1's pair counters start at zero
     {
       smo_gemm_args g{};
       g.rows = maxT;

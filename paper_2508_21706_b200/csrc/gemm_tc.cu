@@ -139,20 +139,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t a_addr = smem_u32(smem + s * stage_bytes);
         const uint32_t b_addr = a_addr + a_bytes;
+        // descriptors built once per stage and advanced by constants (keeps
+        // the single issuing thread ahead of the tensor pipe)
+        const uint64_t ad = make_sdesc_sw128(a_addr, 16, 1024);
+        const uint64_t bd0 = make_sdesc_sw128(b_addr, 16, 1024);
+        const uint64_t bd1 = bd0 + uint64_t((256 * 128) >> 4);
+        const uint64_t au = ad + uint64_t(kTileBytesA >> 4);
 #pragma unroll
         for (int k = 0; k < kBK / 16; ++k) {
           const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
-          const uint64_t ad = make_sdesc_sw128(a_addr + k * 32, 16, 1024);
-          const uint64_t bd0 = make_sdesc_sw128(b_addr + k * 32, 16, 1024);
-          umma_bf16(tmem, ad, bd0, id0, acc);
-          if (nc1 > 0) {
-            const uint64_t bd1 = make_sdesc_sw128(b_addr + 256 * 128 + k * 32, 16, 1024);
-            umma_bf16(tmem + 256, ad, bd1, id1, acc);
-          }
-          if (swiglu) {
-            const uint64_t au = make_sdesc_sw128(a_addr + kTileBytesA + k * 32, 16, 1024);
-            umma_bf16(tmem + 256, au, bd0, id0, acc);
-          }
+          const uint64_t ko = uint64_t((k * 32) >> 4);
+          umma_bf16(tmem, ad + ko, bd0 + ko, id0, acc);
+          if (nc1 > 0) umma_bf16(tmem + 256, ad + ko, bd1 + ko, id1, acc);
+          if (swiglu) umma_bf16(tmem + 256, au + ko, bd0 + ko, id0, acc);
         }
         umma_commit(&empty_bar[s]);
       }

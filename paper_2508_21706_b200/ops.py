@@ -60,7 +60,8 @@ def verify_attention(q, k_cache, v_cache, mask, prefix_len, max_prefix: int, out
     ws_bytes = lib.smo_verify_attention_workspace(C.byref(a))
     if ws_bytes == C.c_size_t(-1).value:
         L.check(L.SMO_INVALID_ARG)
-    ws = torch.empty(max(16, ws_bytes), dtype=torch.uint8, device=q.device) if ws_bytes else None
+    # zero-filled: K1 keeps per-pair counters there (and leaves them at zero)
+    ws = torch.zeros(max(16, ws_bytes), dtype=torch.uint8, device=q.device) if ws_bytes else None
     if ws is not None:
         a.workspace = ws.data_ptr()
         a.workspace_bytes = ws_bytes
