@@ -293,6 +293,17 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def moe_traffic_per_layer():
+    """dram__bytes_read+write of the K4 gate/up + down launches of one layer,
+    from the committed ncu --set full capture (profiles/r01b_traffic.json)."""
+    p = os.path.join(ROOT, "profiles", "r01b_traffic.json")
+    try:
+        k = json.load(open(p))["kernels"]
+        return sum(k[n]["dram_read_bytes"] + k[n]["dram_write_bytes"] for n in ("K4_swiglu_gate_up", "K4_down"))
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------- GPU path
 def run_ours(args):
     import torch
@@ -373,13 +384,18 @@ def run_ours(args):
     torch.cuda.synchronize()
     l0 = _lib.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    prof = os.environ.get("SMO_PROFILE_TIMED") == "1"  # ncu --profile-from-start off: the timed steps only
     with ClockSampler(local) as clk:
+        if prof:
+            torch.cuda.cudart().cudaProfilerStart()
         with torch.cuda.stream(stream):
             ev0.record(stream)
             for _ in range(args.steps):
                 eng.verify_device(tokens, pre_d, acc, bonus, stream=sh)
             ev1.record(stream)
         stream.synchronize()
+        if prof:
+            torch.cuda.cudart().cudaProfilerStop()
     launches = _lib.launch_count() - l0
     t_local = ev0.elapsed_time(ev1) * 1e-3
     barrier(world)
@@ -431,7 +447,9 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "kernel": "K4 grouped SwiGLU gate/up + down (+combine), per step",
                      "achieved": moe_bytes_step / moe_t / 1e9 if moe_t > 0 else None, "peak": pk["hbm_gbs"],
                      "unit": "GB/s", "frac": (moe_bytes_step / moe_t / 1e9) / pk["hbm_gbs"] if moe_t > 0 else None,
-                     "traffic": None, "peak_kind": pk_kind},
+                     "traffic": moe_traffic_per_layer() if (args.model == "mixtral-8x7b" and ep_size == 1) else None, "traffic_unit": "dram bytes per layer (gate/up + down "
+                     "launches, ncu profiles/r01b_traffic.json); algorithmic per layer = " + str(
+                         (shape.n_expert // ep_size) * shape.expert_bytes), "peak_kind": pk_kind},
         "step_roofline": {"bound": roof["bound"], "t_roof_s": roof["t_roof_s"], "t_meas_s": t_step,
                           "frac": roof["t_roof_s"] / t_step, "h2d_peak_gbs": h2d_peak,
                           "hbm_peak_gbs": pk["hbm_gbs"], "times_s": roof["times"]},
