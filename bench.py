@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--slots", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-decode", action="store_true", help="skip the prefill + decode-loop measurement")
     return ap.parse_args()
 
 
@@ -304,6 +305,45 @@ def moe_traffic_per_layer():
         return None
 
 
+def decode_loop(eng, shape, b, prefix, k, stream, sh, iters=3):
+    """SURVEY.md §8 f1/f2 on the bench engine: layer-major prefill of b
+    random prompts of `prefix` tokens (each layer's experts streamed once),
+    then `iters` draft -> verify -> accept -> commit iterations with the
+    on-device drafter. Random-init drafter and target: acceptance ~0, so a
+    step commits ~1 token per request (the bonus); the numbers show the
+    prefill throughput and the drafter's share of an iteration."""
+    import torch
+    rng = np.random.default_rng(77)
+    prompts = rng.integers(0, shape.vocab, size=(b, prefix)).astype(np.int32)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    eng.prefill(prompts, stream=sh)
+    t_pf = time.perf_counter() - t0
+    pf_h2d = eng.last_times()["h2d_bytes"]
+    eng.decode_step(k, stream=sh)  # warm the drafter path
+    stream.synchronize()
+    _, n0, _, _ = eng.decode_read(b, 1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    draft = 0.0
+    e0.record(stream)
+    for _ in range(iters):
+        eng.decode_step(k, stream=sh)
+    e1.record(stream)
+    stream.synchronize()
+    draft = eng.last_times()["draft"]
+    t = e0.elapsed_time(e1) * 1e-3
+    _, n1, kv, _ = eng.decode_read(b, 1)
+    committed = int((n1 - n0).sum())
+    return {"prefill": {"requests": b, "prompt_tokens": prefix, "seconds": t_pf,
+                        "tokens_per_s": b * prefix / t_pf, "h2d_gbs": pf_h2d / t_pf / 1e9,
+                        "note": "wall clock incl. scratch allocation; experts streamed once per layer"},
+            "decode": {"k": k, "iterations": iters, "ms_per_iteration": t / iters * 1e3,
+                       "verified_tokens_per_s": b * (k + 1) * iters / t, "committed_tokens_per_s": committed / t,
+                       "mean_accepted_drafts": committed / (b * iters) - 1.0,
+                       "draft_ms_last_iteration": draft * 1e3,
+                       "drafter": f"{shape.draft_layers} dense layer(s), SwiGLU {shape.draft_inter}, random-init"}}
+
+
 # ---------------------------------------------------------------- GPU path
 def run_ours(args):
     import torch
@@ -313,6 +353,12 @@ def run_ours(args):
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
     shape = shape_of(args.model)
+    if world == 1 and not args.no_decode:
+        # the drafter of the reference's config (DraftModelSpec, mixtral8x7b.json:
+        # 1 layer, ffn_ops_per_token 3.52e8 = 6*h*draft_inter) for the decode loop
+        import dataclasses
+        shape = dataclasses.replace(shape, draft_layers=1,
+                                    draft_inter=max(128, int(round(3.52e8 / (6 * shape.hidden) / 128)) * 128))
     b, n, prefix = args.batch, args.k + 1, args.prefix
     pk, pk_kind = peaks()
     s_max = prefix + n + 64
@@ -421,6 +467,13 @@ def run_ours(args):
                                          res.target.nbytes),
                "api": "smo_engine_verify (host buffers)"}
 
+    decode = None
+    if world == 1 and not args.no_decode:
+        try:
+            decode = decode_loop(eng, shape, b, prefix, args.k, stream, sh)
+        except Exception as ex:  # reported, never hides the headline
+            decode = {"error": str(ex)}
+
     roof = step_roofline(shape, b * ep_size, n, prefix, h2d_peak, pk["hbm_gbs"],
                          pk.get("bf16_tflops_sustained", 1400.0),
                          cached_blocks=int(args.cache_gb * 1e9) // shape.expert_bytes, ep=ep_size)
@@ -460,6 +513,8 @@ def run_ours(args):
         "gpu_launches": launches, "engine_create_s": t_create,
     }
     line["clocks"] = clk.summary()
+    if decode:
+        line["decode_loop"] = decode
     if e2e:
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -16,6 +16,7 @@
 // norms/QKV/RoPE -> GPU_OTHER1, O-proj/router/permute -> GPU_OTHER2,
 // K4 experts + combine -> GPU_MOE, K5 copy-engine transfer -> H2D_EXPERTS.
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <stdexcept>
@@ -26,6 +27,7 @@
 #include "moeplan/memory.hpp"
 #include "moeplan/optimizer.hpp"
 #include "moeplan/pipeline.hpp"
+#include "moeplan/specdec.hpp"
 #include "specmoe/c_api.h"
 
 namespace moeplan {
@@ -39,6 +41,7 @@ struct EngineOptions {
   std::uint64_t seed = 0x5EED;         // procedural weights
   float lm_scale = 1.0f;
   float router_scale = 1.0f;
+  bool drafter = true;                 // build the drafter from ModelSpec.draft (f1) when it has FFN ops
 };
 
 struct VerifyBatch {
@@ -91,6 +94,13 @@ class VerifyEngine {
     c.lm_scale = opt.lm_scale;
     c.router_scale = opt.router_scale;
     c.shared_inter = std::int32_t(a.shared_expert_inter);
+    // drafter: DraftModelSpec (config.hpp:40-45) -> dense
+    // decoder layers; ffn_ops_per_token = 2*3*h*draft_inter
+    if (opt.drafter && model.draft.n_layers > 0 && model.draft.ffn_ops_per_token > 0) {
+      const double di = model.draft.ffn_ops_per_token / (6.0 * double(model.h));
+      c.draft_layers = std::int32_t(model.draft.n_layers);
+      c.draft_inter = std::int32_t(std::max(1.0, std::round(di / 128.0)) * 128.0);
+    }
     smo_engine_options o{};
     o.max_batch = std::int32_t(hyper.b);
     o.max_verify = std::int32_t(std::max(1, hyper.k) + 1);
@@ -104,6 +114,7 @@ class VerifyEngine {
     o.ep_size = 1;
     detail::smo_check(smo_engine_create(&c, &o, &h_));
     layers_ = model.n_layers;
+    max_verify_ = o.max_verify;
   }
   VerifyEngine(const VerifyEngine&) = delete;
   VerifyEngine& operator=(const VerifyEngine&) = delete;
@@ -133,6 +144,109 @@ class VerifyEngine {
     detail::smo_check(smo_engine_verify(h_, &vb, &vo, nullptr));
     return measured(in);
   }
+
+  // ---- KV lifecycle + decode loop ----------------------
+  // Prefill (f2): the prompts' real K/V for the target and the drafter,
+  // layer-major (each layer's experts streamed once). Returns the greedy next
+  // token per request and starts the decode state (kv_len = prompt length).
+  std::vector<std::int32_t> prefill(const std::vector<std::vector<std::int32_t>>& prompts) {
+    if (prompts.empty()) throw std::invalid_argument("VerifyEngine::prefill: no prompts");
+    std::size_t lmax = 0;
+    for (const auto& p : prompts) lmax = std::max(lmax, p.size());
+    std::vector<std::int32_t> tok(prompts.size() * lmax, 0), len, next(prompts.size(), 0);
+    for (std::size_t r = 0; r < prompts.size(); ++r) {
+      std::copy(prompts[r].begin(), prompts[r].end(), tok.begin() + std::ptrdiff_t(r * lmax));
+      len.push_back(std::int32_t(prompts[r].size()));
+    }
+    detail::smo_check(smo_engine_prefill(h_, tok.data(), len.data(), std::int32_t(prompts.size()),
+                                         std::int32_t(lmax), next.data(), nullptr));
+    kv_len_ = len;
+    return next;
+  }
+
+  void decode_begin(const std::vector<std::int32_t>& root, const std::vector<std::int32_t>& kv_len) {
+    if (root.size() != kv_len.size()) throw std::invalid_argument("VerifyEngine::decode_begin: size mismatch");
+    detail::smo_check(smo_engine_decode_begin(h_, root.data(), kv_len.data(), std::int32_t(root.size())));
+    kv_len_ = kv_len;
+  }
+
+  // One decode iteration (f1): k drafts from the on-device drafter (or the
+  // planted b*k tokens) -> verify -> greedy accept -> commit. Returns the
+  // measured IterationResult with the draft DAG (pipeline.hpp:208-253) of
+  // k+1 DRAFT_GPU_STEP events and breakdown.iteration = draft + target.
+  IterationResult decode_step(int k, const std::vector<std::int32_t>* planted = nullptr) {
+    if (kv_len_.empty()) throw std::invalid_argument("VerifyEngine::decode_step: call prefill or decode_begin first");
+    if (planted && planted->size() != kv_len_.size() * std::size_t(std::max(k, 0)))
+      throw std::invalid_argument("VerifyEngine::decode_step: planted drafts must be b*k tokens");
+    VerifyBatch vb;  // driving variables of this step (pipeline.hpp:256-264)
+    vb.b = std::int64_t(kv_len_.size());
+    vb.n = k + 1;
+    vb.prefix_len = kv_len_;
+    detail::smo_check(smo_engine_decode_step(h_, k, planted ? planted->data() : nullptr, nullptr));
+    IterationResult r = measured(vb);
+    std::vector<double> dt(std::size_t(k) + 2, 0.0);
+    std::int32_t steps = 0;
+    detail::smo_check(smo_engine_draft_times(h_, dt.data(), dt.size(), &steps));
+    double s = 0;
+    for (auto p : kv_len_) s += double(p);
+    s /= double(kv_len_.size());
+    double t0 = 0;
+    for (int t = 0; t < steps; ++t) {
+      EventNode ev;
+      ev.id = t;
+      ev.kind = EventKind::DRAFT_GPU_STEP;
+      ev.resource = ExecResource::GPU;
+      ev.duration = dt[std::size_t(t)];
+      if (t > 0) ev.deps.push_back(t - 1);
+      ev.label = "draft/step" + std::to_string(t) + "/GPU_STEP";
+      r.draft_dag.push_back(ev);
+      r.draft_schedule.start.push_back(t0);
+      r.draft_schedule.end.push_back(t0 + ev.duration);
+      r.draft_schedule.busy[std::size_t(ExecResource::GPU)] += ev.duration;
+      t0 += ev.duration;
+      samples_.push_back({EventKind::DRAFT_GPU_STEP, double(vb.b) * s, ev.duration});
+    }
+    r.draft_schedule.makespan = t0;
+    r.breakdown.draft_total = t0;
+    r.breakdown.draft_gpu_part = t0;
+    r.breakdown.iteration = r.breakdown.target_total + t0;
+    std::vector<std::int32_t> kv(kv_len_.size());
+    detail::smo_check(smo_engine_decode_read(h_, nullptr, 0, nullptr, kv.data(), nullptr));
+    kv_len_ = kv;
+    return r;
+  }
+
+  // Closed loop (f3): each iteration asks the controller for k at the current
+  // mean prefix (DraftLengthController::update, specdec.hpp:97-124) — its
+  // SweepFn typically runs optimize() on fit_latency_models(profile()) — and
+  // runs one measured decode step with it (clamped to the engine's capacity).
+  std::vector<IterationResult> decode(int iterations, DraftLengthController& ctl) {
+    std::vector<IterationResult> out;
+    for (int it = 0; it < iterations; ++it) {
+      double s = 0;
+      for (auto p : kv_len_) s += double(p);
+      s /= double(std::max<std::size_t>(1, kv_len_.size()));
+      const int k = std::clamp(ctl.update(std::int64_t(s), std::int64_t(kv_len_.size())), 0, max_verify_ - 1);
+      ks_.push_back(k);
+      out.push_back(decode_step(k));
+    }
+    return out;
+  }
+
+  // Committed tokens per request since prefill/decode_begin (accepted drafts
+  // + bonus of every step; the prefill's next token is the first root).
+  std::vector<std::vector<std::int32_t>> committed() {
+    const std::int32_t b = std::int32_t(kv_len_.size()), cap = 4096;
+    std::vector<std::int32_t> buf(static_cast<std::size_t>(b) * std::size_t(cap)), n(static_cast<std::size_t>(b));
+    detail::smo_check(smo_engine_decode_read(h_, buf.data(), cap, n.data(), nullptr, nullptr));
+    std::vector<std::vector<std::int32_t>> out(static_cast<std::size_t>(b));
+    for (std::int32_t r = 0; r < b; ++r)
+      out[std::size_t(r)].assign(buf.begin() + std::ptrdiff_t(r) * cap,
+                                 buf.begin() + std::ptrdiff_t(r) * cap + std::min<std::int32_t>(cap, n[std::size_t(r)]));
+    return out;
+  }
+  const std::vector<std::int32_t>& kv_len() const { return kv_len_; }
+  const std::vector<int>& chosen_k() const { return ks_; }
 
   // Accumulated measured samples (one per stage kind and verify call).
   const std::vector<ProfileSample>& profile() const { return samples_; }
@@ -218,6 +332,9 @@ class VerifyEngine {
   Hyperparameters hyper_;
   smo_engine* h_ = nullptr;
   std::int64_t layers_ = 0;
+  int max_verify_ = 1;
+  std::vector<std::int32_t> kv_len_;  // decode state mirror (host)
+  std::vector<int> ks_;
   std::vector<ProfileSample> samples_;
 };
 

@@ -211,6 +211,10 @@ typedef struct {
   float router_scale;  /* multiplier on the router init scale */
   int32_t shared_inter; /* always-on shared expert width (0: none; DeepSeek/Qwen-style,
                            resident in HBM, SwiGLU over every token) */
+  int32_t draft_layers; /* drafter depth, DraftModelSpec.n_layers (config.hpp:40-45); 0: no drafter.
+                           Dense decoder layers with the target's attention shape, sharing
+                           its embedding and LM head (EAGLE convention), resident in HBM */
+  int32_t draft_inter;  /* drafter SwiGLU width: DraftModelSpec.ffn_ops_per_token = 6*h*draft_inter */
 } smo_model_config;
 
 enum { SMO_ENGINE_DEBUG = 1 /* keep per-layer intermediates for parity tests */ };
@@ -279,6 +283,7 @@ typedef struct {
   double others;       /* norms, QKV/O GEMMs, router, permute, LM head, accept */
   double h2d_bytes;    /* bytes streamed */
   double launches;     /* kernels launched */
+  double draft;        /* drafter time of the last decode step (DRAFT_GPU_STEP total) */
 } smo_stage_times;
 smo_status smo_engine_last_times(smo_engine* e, smo_stage_times* t);
 /* Measured per-layer timeline of the last verify, 9 doubles per layer (s from
@@ -286,6 +291,36 @@ smo_status smo_engine_last_times(smo_engine* e, smo_stage_times* t);
  * (after the slot wait), layer start, pre-MoE (after permute), and the bytes
  * streamed for that layer (hot-cached experts excluded). n >= 9*L.         */
 smo_status smo_engine_layer_times(smo_engine* e, double* out, size_t n);
+
+/* ---- prefill + decode loop ------------------------------
+ * The KV lifecycle around the verify step, all on the engine's device state:
+ *  smo_engine_prefill: runs the prompts through the target (and drafter) and
+ *    writes their real K/V at positions 0..len_r-1. Layer-major: each layer's
+ *    experts are streamed ONCE for the whole prompt batch; attention runs the
+ *    prompt as causal verify-shaped chunks of C = min(64, 128*n_kv/n_q) rows
+ *    (K1 with a chain mask and prefix = c*C). tokens: host [b, max_len]
+ *    (row r valid up to len[r], 1 <= len[r] <= max_len); next_token: host [b]
+ *    greedy token after each prompt. Sets the decode state: kv_len = len,
+ *    root = next_token, empty history. Not available with expert parallelism.
+ *  smo_engine_decode_begin: sets the decode state from host arrays instead
+ *    (e.g. after smo_engine_fill_prefix).
+ *  smo_engine_decode_step: one iteration = draft (k+1 drafter steps: chain,
+ *    greedy; the last one only appends d_k's draft K/V) -> verify (n = k+1,
+ *    prefix = kv_len) -> greedy accept -> commit (kv_len += acc+1, root =
+ *    bonus, accepted drafts + bonus appended to the history). drafts: NULL
+ *    (drafter proposes) or host [b*k] planted drafts (the drafter still runs
+ *    teacher-forced to keep its K/V in step). k = 0 is plain decoding.
+ *  smo_engine_decode_read: history [b, cap] (-1 padded), its lengths, kv_len
+ *    and the next root, to host (synchronous).                             */
+smo_status smo_engine_prefill(smo_engine* e, const int32_t* tokens, const int32_t* len, int32_t b,
+                              int32_t max_len, int32_t* next_token, smo_stream stream);
+smo_status smo_engine_decode_begin(smo_engine* e, const int32_t* root, const int32_t* kv_len, int32_t b);
+smo_status smo_engine_decode_step(smo_engine* e, int32_t k, const int32_t* drafts, smo_stream stream);
+/* Measured duration (s) of each drafter step of the last decode step
+ * (DRAFT_GPU_STEP events, pipeline.hpp:208-253); *steps = k+1 (0: no drafter). */
+smo_status smo_engine_draft_times(smo_engine* e, double* out, size_t n, int32_t* steps);
+smo_status smo_engine_decode_read(smo_engine* e, int32_t* committed, int32_t cap, int32_t* n_committed,
+                                  int32_t* kv_len, int32_t* root);
 
 /* Debug intermediates of the last verify (engine created with SMO_ENGINE_DEBUG).
  * name: "x_in" f32 [T,h] layer input, "xn1" bf16, "q" bf16 [T,n_q,d],

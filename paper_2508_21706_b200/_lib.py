@@ -51,7 +51,7 @@ class ModelConfig(C.Structure):
     _fields_ = [("hidden", _i32), ("inter", _i32), ("n_expert", _i32), ("top_k", _i32), ("n_layers", _i32),
                 ("n_q_heads", _i32), ("n_kv_heads", _i32), ("head_dim", _i32), ("vocab", _i32),
                 ("rope_theta", _f32), ("rms_eps", _f32), ("seed", _u64), ("lm_scale", _f32),
-                ("router_scale", _f32), ("shared_inter", _i32)]
+                ("router_scale", _f32), ("shared_inter", _i32), ("draft_layers", _i32), ("draft_inter", _i32)]
 
 
 class EngineOptions(C.Structure):
@@ -72,7 +72,7 @@ class VerifyOutput(C.Structure):
 class StageTimes(C.Structure):
     _fields_ = [("target_total", C.c_double), ("attention", C.c_double), ("gpu_moe", C.c_double),
                 ("h2d_transfer", C.c_double), ("others", C.c_double), ("h2d_bytes", C.c_double),
-                ("launches", C.c_double)]
+                ("launches", C.c_double), ("draft", C.c_double)]
 
 
 _SIGS = {
@@ -106,6 +106,11 @@ _SIGS = {
     "smo_engine_fill_prefix": (C.c_int, [_vp, _vp, _i32]),
     "smo_engine_verify": (C.c_int, [_vp, C.POINTER(VerifyBatch), C.POINTER(VerifyOutput), _vp]),
     "smo_engine_last_times": (C.c_int, [_vp, C.POINTER(StageTimes)]),
+    "smo_engine_prefill": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _vp, _vp]),
+    "smo_engine_decode_begin": (C.c_int, [_vp, _vp, _vp, _i32]),
+    "smo_engine_decode_step": (C.c_int, [_vp, _i32, _vp, _vp]),
+    "smo_engine_decode_read": (C.c_int, [_vp, _vp, _i32, _vp, _vp, _vp]),
+    "smo_engine_draft_times": (C.c_int, [_vp, _vp, _sz, _vp]),
     "smo_engine_layer_times": (C.c_int, [_vp, _vp, _sz]),
     "smo_engine_debug_tensor": (C.c_int, [_vp, C.c_char_p, _i32, _vp, _sz]),
     "smo_engine_tensor_ptr": (C.c_int, [_vp, C.c_char_p, _i32, _i32, C.POINTER(_vp), C.POINTER(_sz)]),

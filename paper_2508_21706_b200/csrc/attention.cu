@@ -733,9 +733,14 @@ AttnPlan plan_attention(const smo_attn_args& a, int sms) {
   if (cost(qa) < cost(qmin)) q = qa;
   pl.Q = std::max(q, (pl.C + 14) / 15);
   pl.grid = (pl.total + pl.Q - 1) / pl.Q;
+  // the layout is sized for the largest tile (128 rows) so that the counter
+  // region sits at the same offset for every n: a workspace shared by calls
+  // of different shapes (verify, drafter, prefill chunks) keeps its
+  // zero-between-launches counters where the next call looks for them
+  (void)rows;
   pl.ws_o_off = 0;
-  pl.ws_ml_off = align256(size_t(sms) * 2 * rows * a.d * sizeof(float));
-  pl.ws_cnt_off = pl.ws_ml_off + align256(size_t(sms) * 2 * rows * sizeof(float2));
+  pl.ws_ml_off = align256(size_t(sms) * 2 * 128 * a.d * sizeof(float));
+  pl.ws_cnt_off = pl.ws_ml_off + align256(size_t(sms) * 2 * 128 * sizeof(float2));
   pl.ws_bytes = pl.ws_cnt_off + align256(size_t(pairs) * sizeof(int));
   return pl;
 }

@@ -51,6 +51,13 @@ void argmax_reduce(const float* val, const int32_t* idx, int rows, int parts, in
 void greedy_accept(const int32_t* tokens, const int32_t* target, const int32_t* parent, int b, int n,
                    int32_t* acc_len, int32_t* bonus, int32_t* keep, cudaStream_t st);
 void build_mask(const int32_t* parent, int b, int n, uint64_t* mask, cudaStream_t st);
+void decode_prep(const int32_t* root, const int32_t* drafts, int b, int n, int32_t* tokens, cudaStream_t st);
+void draft_io(const int32_t* tokens, const int32_t* kv_len, int t, int b, int n, int32_t* tok_in, int32_t* pos,
+              cudaStream_t st);
+void draft_scatter(const int32_t* out, int b, int n, int t, int32_t* tokens, cudaStream_t st);
+void decode_commit(const int32_t* tokens, const int32_t* acc, const int32_t* bonus, int b, int n, int cap,
+                   int32_t* hist, int32_t* hist_n, int32_t* kv_len, int32_t* root, cudaStream_t st);
+void prefill_last(const float* x, const int32_t* len, int b, int C, int h, float* out, cudaStream_t st);
 // expert parallelism (ep.cu)
 EpTransport* ep_transport(void* group);
 void ep_remap(const int32_t* ids, int n, int P, int E_loc, int32_t* oid, cudaStream_t st);
@@ -69,6 +76,9 @@ constexpr uint64_t kEmbed = 1, kLmHead = 2;
 inline uint64_t layer(int l) { return 1000ull * uint64_t(l + 1); }
 constexpr uint64_t kWqkv = 1, kWo = 2, kRouter = 4, kShared = 50, kExpert = 100;
 inline uint64_t kv(int l, int which) { return 900000ull + 2ull * uint64_t(l) + uint64_t(which); }
+// drafter layer l: +1 Wqkv, +2 Wo, +3 W1, +4 W3, +5 W2; its prefix K/V
+inline uint64_t draft(int l) { return 700000ull + 100ull * uint64_t(l); }
+inline uint64_t draft_kv(int l, int which) { return 910000ull + 2ull * uint64_t(l) + uint64_t(which); }
 }  // namespace tid
 
 struct DevBuf {
@@ -93,6 +103,23 @@ struct Engine {
     uint16_t *kc, *vc;
   };
   std::vector<Layer> layers;
+  // drafter: dense decoder layers, resident in HBM
+  struct DLayer {
+    uint16_t *wqkv, *wo, *w1, *w3, *w2, *kc, *vc;
+  };
+  std::vector<DLayer> dlayers;
+  int dL = 0, dI = 0;
+  uint16_t* dh = nullptr;  // drafter SwiGLU activations [maxT, dI]
+  int32_t *d_dtok = nullptr, *d_dpos = nullptr, *d_dout = nullptr;
+  uint64_t* d_mask1 = nullptr;  // single-row chain mask (bit 0) per request
+  // decode state: committed K/V length, next root, history
+  int dec_b = 0, hist_cap = 0;
+  int64_t kv_bound = 0;  // host upper bound of kv_len (K1 split planning)
+  int32_t *d_kvlen = nullptr, *d_root = nullptr, *d_hist = nullptr, *d_hist_n = nullptr, *d_dec_tok = nullptr,
+          *d_drafts = nullptr;
+  bool last_was_decode = false;
+  std::vector<cudaEvent_t> draft_ev;  // [maxN + 1]: boundaries of the drafter steps
+  int last_draft_steps = 0;
   std::vector<uint16_t*> host_bufs;  // pinned, E blocks each
   int host_alias = 0;
   // expert pool in HBM
@@ -142,6 +169,7 @@ struct Engine {
     for (auto e : slot_ready) cudaEventDestroy(e);
     for (auto e : slot_free) cudaEventDestroy(e);
     for (auto e : ev) cudaEventDestroy(e);
+    for (auto e : draft_ev) cudaEventDestroy(e);
     for (auto hb : host_bufs) cudaFreeHost(hb);
     if (h_stage) cudaFreeHost(h_stage);
     for (auto& a : allocs) cudaFree(a.p);
@@ -243,6 +271,32 @@ struct Engine {
         fill_uniform(ly.ws3, n, cfg.seed, tid::layer(l) + tid::kShared + 1, 0, std::sqrt(3.0f / h), st);
         fill_uniform(ly.ws2, n, cfg.seed, tid::layer(l) + tid::kShared + 2, 0, std::sqrt(3.0f / cfg.shared_inter), st);
       }
+    }
+
+    // drafter: dense decoder layers with the target's attention shape,
+    // sharing the target's embedding and LM head (EAGLE convention)
+    dL = cfg.draft_layers;
+    dI = cfg.draft_inter;
+    SMO_REQUIRE(dL >= 0 && (dL == 0 || (dI > 0 && dI % 128 == 0)),
+                "engine: draft_inter must be a positive multiple of 128 when draft_layers > 0");
+    dlayers.resize(dL);
+    for (int l = 0; l < dL; ++l) {
+      DLayer& dl = dlayers[l];
+      const uint64_t base = tid::draft(l);
+      dl.wqkv = dalloc<uint16_t>(size_t(qkv_w) * h);
+      dl.wo = dalloc<uint16_t>(size_t(h) * nq * d);
+      dl.w1 = dalloc<uint16_t>(size_t(dI) * h);
+      dl.w3 = dalloc<uint16_t>(size_t(dI) * h);
+      dl.w2 = dalloc<uint16_t>(size_t(h) * dI);
+      dl.kc = dalloc<uint16_t>(size_t(maxB) * nkv * s_max * d);
+      dl.vc = dalloc<uint16_t>(size_t(maxB) * nkv * s_max * d);
+      SMO_CUDA_CHECK(cudaMemset(dl.kc, 0, size_t(maxB) * nkv * s_max * d * 2));
+      SMO_CUDA_CHECK(cudaMemset(dl.vc, 0, size_t(maxB) * nkv * s_max * d * 2));
+      fill_uniform(dl.wqkv, size_t(qkv_w) * h, cfg.seed, base + 1, 0, std::sqrt(3.0f / h), st);
+      fill_uniform(dl.wo, size_t(h) * nq * d, cfg.seed, base + 2, 0, std::sqrt(3.0f / (nq * d)), st);
+      fill_uniform(dl.w1, size_t(dI) * h, cfg.seed, base + 3, 0, std::sqrt(3.0f / h), st);
+      fill_uniform(dl.w3, size_t(dI) * h, cfg.seed, base + 4, 0, std::sqrt(3.0f / h), st);
+      fill_uniform(dl.w2, size_t(h) * dI, cfg.seed, base + 5, 0, std::sqrt(3.0f / dI), st);
     }
 
     // experts: generate each block on the device, stage to pinned host DRAM
@@ -384,10 +438,29 @@ struct Engine {
       gemm_ws_bytes = std::max(gemm_ws_bytes, size_t(8) * maxT * std::max(qkv_w, h) * sizeof(float));
       gemm_ws = dalloc<uint8_t>(gemm_ws_bytes);
     }
+    // drafter + decode-loop state
+    if (dL > 0) dh = dalloc<uint16_t>(size_t(maxT) * dI);
+    d_dtok = dalloc<int32_t>(maxB);
+    d_dpos = dalloc<int32_t>(maxB);
+    d_dout = dalloc<int32_t>(maxB);
+    d_mask1 = dalloc<uint64_t>(maxB);
+    {
+      std::vector<uint64_t> one(maxB, 1ull);
+      SMO_CUDA_CHECK(cudaMemcpy(d_mask1, one.data(), size_t(maxB) * 8, cudaMemcpyHostToDevice));
+    }
+    hist_cap = s_max;
+    d_kvlen = dalloc<int32_t>(maxB);
+    d_root = dalloc<int32_t>(maxB);
+    d_hist = dalloc<int32_t>(size_t(maxB) * hist_cap);
+    d_hist_n = dalloc<int32_t>(maxB);
+    d_dec_tok = dalloc<int32_t>(maxT);
+    d_drafts = dalloc<int32_t>(maxT);
     h_stage_elems = size_t(maxT) * 4 + maxB * 4;
     SMO_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_stage), h_stage_elems * 4, cudaHostAllocPortable));
     ev.resize(8 + size_t(L) * 8);
     for (auto& e : ev) SMO_CUDA_CHECK(cudaEventCreate(&e));
+    draft_ev.resize(size_t(maxN) + 1);
+    for (auto& e : draft_ev) SMO_CUDA_CHECK(cudaEventCreate(&e));
     SMO_CUDA_CHECK(cudaDeviceSynchronize());
   }
 
@@ -399,6 +472,10 @@ struct Engine {
     for (int l = 0; l < L; ++l) {
       fill_kv_prefix(layers[l].kc, d_prefix, b, nkv, d, s_max, cfg.seed, tid::kv(l, 0), nullptr);
       fill_kv_prefix(layers[l].vc, d_prefix, b, nkv, d, s_max, cfg.seed, tid::kv(l, 1), nullptr);
+    }
+    for (int l = 0; l < dL; ++l) {
+      fill_kv_prefix(dlayers[l].kc, d_prefix, b, nkv, d, s_max, cfg.seed, tid::draft_kv(l, 0), nullptr);
+      fill_kv_prefix(dlayers[l].vc, d_prefix, b, nkv, d, s_max, cfg.seed, tid::draft_kv(l, 1), nullptr);
     }
     SMO_CUDA_CHECK(cudaDeviceSynchronize());
   }
@@ -532,21 +609,57 @@ struct Engine {
         SMO_CUDA_CHECK(cudaMemcpyAsync(d_parent, hs + T + b, size_t(T) * 4, cudaMemcpyHostToDevice, st));
     }
     const int32_t* parent = in.parent ? d_parent : nullptr;
-    const uint64_t launches0 = 0;
-    (void)launches0;
-
-    cudaEvent_t e_start = ev[0], e_end = ev[1];
-    SMO_CUDA_CHECK(cudaEventRecord(e_start, st));
-    // order the copy stream after the step start (so H2D timing is step-relative)
-    SMO_CUDA_CHECK(cudaStreamWaitEvent(copy, e_start, 0));
-    double h2d_bytes = 0;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> h2d_ev, attn_ev, moe_ev;
-    for (int l = 0; l < std::min(slots, L); ++l) {
-      h2d_bytes += enqueue_h2d(l, tev(l * 8 + 0), tev(l * 8 + 1));
-      h2d_ev.push_back({tev(l * 8 + 0), tev(l * 8 + 1)});
+    last_was_decode = false;
+    begin_step(st);
+    verify_core(b, n, d_tokens, parent, d_prefix, max_prefix, st);
+    // ---- outputs
+    if (out.on_device) {
+      SMO_CUDA_CHECK(cudaMemcpyAsync(out.acc_len, d_acc, size_t(b) * 4, cudaMemcpyDeviceToDevice, st));
+      SMO_CUDA_CHECK(cudaMemcpyAsync(out.bonus, d_bonus, size_t(b) * 4, cudaMemcpyDeviceToDevice, st));
+      if (out.keep) SMO_CUDA_CHECK(cudaMemcpyAsync(out.keep, d_keep, size_t(T) * 4, cudaMemcpyDeviceToDevice, st));
+      if (out.target)
+        SMO_CUDA_CHECK(cudaMemcpyAsync(out.target, target, size_t(T) * 4, cudaMemcpyDeviceToDevice, st));
+    } else {
+      int32_t* hs = h_stage + 2 * size_t(T) + b;
+      SMO_CUDA_CHECK(cudaMemcpyAsync(hs, d_acc, size_t(b) * 4, cudaMemcpyDeviceToHost, st));
+      SMO_CUDA_CHECK(cudaMemcpyAsync(hs + b, d_bonus, size_t(b) * 4, cudaMemcpyDeviceToHost, st));
+      SMO_CUDA_CHECK(cudaMemcpyAsync(hs + 2 * b, d_keep, size_t(T) * 4, cudaMemcpyDeviceToHost, st));
+      SMO_CUDA_CHECK(cudaMemcpyAsync(hs + 2 * b + T, target, size_t(T) * 4, cudaMemcpyDeviceToHost, st));
+      SMO_CUDA_CHECK(cudaStreamSynchronize(st));
+      std::memcpy(out.acc_len, hs, size_t(b) * 4);
+      std::memcpy(out.bonus, hs + b, size_t(b) * 4);
+      if (out.keep) std::memcpy(out.keep, hs + 2 * b, size_t(T) * 4);
+      if (out.target) std::memcpy(out.target, hs + 2 * b + T, size_t(T) * 4);
     }
+  }
+
+  // Step start: event 0, then the copy engine starts streaming the first
+  // `slots` layers (it only waits for the slot-release edges). Called before
+  // the drafter in a decode step so that the first transfers overlap drafting.
+  double step_h2d_bytes = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> step_h2d_ev;
+  void begin_step(cudaStream_t st) {
+    SMO_CUDA_CHECK(cudaEventRecord(ev[0], st));
+    // order the copy stream after the step start (so H2D timing is step-relative)
+    SMO_CUDA_CHECK(cudaStreamWaitEvent(copy, ev[0], 0));
+    step_h2d_bytes = 0;
+    step_h2d_ev.clear();
+    for (int l = 0; l < std::min(slots, L); ++l) {
+      step_h2d_bytes += enqueue_h2d(l, tev(l * 8 + 0), tev(l * 8 + 1));
+      step_h2d_ev.push_back({tev(l * 8 + 0), tev(l * 8 + 1)});
+    }
+  }
+
+  // The target verification DAG on device inputs: tokens [b*n], parent
+  // [b*n] or null, prefix [b]; results in d_acc / d_bonus / d_keep / target.
+  void verify_core(int b, int n, const int32_t* tokens, const int32_t* parent, const int32_t* prefix, int max_prefix,
+                   cudaStream_t st) {
+    const int T = b * n;
+    cudaEvent_t e_end = ev[1];
+    double h2d_bytes = step_h2d_bytes;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> h2d_ev = step_h2d_ev, attn_ev, moe_ev;
     build_mask(parent, b, n, d_mask, st);
-    embed(d_tokens, embed_w, T, h, x, st);
+    embed(tokens, embed_w, T, h, x, st);
 
     const int PT = T * K;  // (token, slot) pairs
     for (int l = 0; l < L; ++l) {
@@ -570,14 +683,14 @@ struct Engine {
       g.workspace = gemm_ws;
       g.workspace_bytes = gemm_ws_bytes;
       gemm_launch(g, st);
-      rope_append(qkv, d_prefix, parent, b, n, nq, nkv, d, s_max, cfg.rope_theta, q, ly.kc, ly.vc, st);
+      rope_append(qkv, prefix, parent, b, n, nq, nkv, d, s_max, cfg.rope_theta, q, ly.kc, ly.vc, st);
       snap("q", l, q, size_t(T) * nq * d * 2, st);
       smo_attn_args a{};
       a.q = q;
       a.k_cache = ly.kc;
       a.v_cache = ly.vc;
       a.mask = d_mask;
-      a.prefix_len = d_prefix;
+      a.prefix_len = prefix;
       a.out = attn;
       a.b = b;
       a.n = n;
@@ -745,33 +858,364 @@ struct Engine {
       gemm_launch(g, st);
     }
     argmax_reduce(amax_v, amax_i, T, V / 128, target, st);
-    greedy_accept(d_tokens, target, parent, b, n, d_acc, d_bonus, d_keep, st);
+    greedy_accept(tokens, target, parent, b, n, d_acc, d_bonus, d_keep, st);
     SMO_CUDA_CHECK(cudaEventRecord(e_end, st));
     // the step is complete only when the copy engine is idle too
     SMO_CUDA_CHECK(cudaStreamWaitEvent(st, slot_ready[(L - 1) % slots], 0));
-    // ---- outputs
-    if (out.on_device) {
-      SMO_CUDA_CHECK(cudaMemcpyAsync(out.acc_len, d_acc, size_t(b) * 4, cudaMemcpyDeviceToDevice, st));
-      SMO_CUDA_CHECK(cudaMemcpyAsync(out.bonus, d_bonus, size_t(b) * 4, cudaMemcpyDeviceToDevice, st));
-      if (out.keep) SMO_CUDA_CHECK(cudaMemcpyAsync(out.keep, d_keep, size_t(T) * 4, cudaMemcpyDeviceToDevice, st));
-      if (out.target)
-        SMO_CUDA_CHECK(cudaMemcpyAsync(out.target, target, size_t(T) * 4, cudaMemcpyDeviceToDevice, st));
-    } else {
-      int32_t* hs = h_stage + 2 * size_t(T) + b;
-      SMO_CUDA_CHECK(cudaMemcpyAsync(hs, d_acc, size_t(b) * 4, cudaMemcpyDeviceToHost, st));
-      SMO_CUDA_CHECK(cudaMemcpyAsync(hs + b, d_bonus, size_t(b) * 4, cudaMemcpyDeviceToHost, st));
-      SMO_CUDA_CHECK(cudaMemcpyAsync(hs + 2 * b, d_keep, size_t(T) * 4, cudaMemcpyDeviceToHost, st));
-      SMO_CUDA_CHECK(cudaMemcpyAsync(hs + 2 * b + T, target, size_t(T) * 4, cudaMemcpyDeviceToHost, st));
-      SMO_CUDA_CHECK(cudaStreamSynchronize(st));
-      std::memcpy(out.acc_len, hs, size_t(b) * 4);
-      std::memcpy(out.bonus, hs + b, size_t(b) * 4);
-      if (out.keep) std::memcpy(out.keep, hs + 2 * b, size_t(T) * 4);
-      if (out.target) std::memcpy(out.target, hs + 2 * b + T, size_t(T) * 4);
-    }
     pending_attn = attn_ev;
     pending_moe = moe_ev;
     pending_h2d = h2d_ev;
     last_h2d_bytes = h2d_bytes;
+  }
+
+  // ------------------------------------------------------------------ dense
+  // building blocks shared by the drafter and the prefill
+  struct Scratch {
+    float* x;
+    uint16_t *xn, *qkv, *q, *attn;
+    void* attn_ws;
+    size_t attn_ws_bytes;
+    int split;  // 0: auto split-K (engine workspace), 1: off
+  };
+
+  void dense_gemm(const void* xin, int rows, int Kd, int N, const void* w, const void* w_up, int epi, void* out,
+                  int split, cudaStream_t st) {
+    smo_gemm_args g{};
+    g.x = xin;
+    g.rows = rows;
+    g.K = Kd;
+    g.N = N;
+    g.groups = 1;
+    g.max_rows_per_group = rows;
+    g.w = w;
+    g.w_up = w_up;
+    g.w_pool_blocks = 1;
+    g.epilogue = epi;
+    g.out = out;
+    g.ldo = N;
+    g.split_k = split;
+    if (split != 1) {
+      g.workspace = gemm_ws;
+      g.workspace_bytes = gemm_ws_bytes;
+    }
+    gemm_launch(g, st);
+  }
+
+  // x += Wo . attn(RoPE(Wqkv . rmsnorm(x))) for rows organised as `nch`
+  // chunks of b*n verify rows; chunk c's row (r, i) sits at position
+  // prefix[c*b + r] + i and sees the prefix plus the chain `mask`. K/V rows
+  // are appended to kc/vc (the K1 contract of smo_verify_attention).
+  void attn_sublayer(const Scratch& sc, const uint16_t* wqkv, const uint16_t* wo, uint16_t* kc, uint16_t* vc, int b,
+                     int n, int nch, const int32_t* prefix, const std::vector<int>& max_prefix, const uint64_t* mask,
+                     cudaStream_t st) {
+    const int rows = b * n * nch;
+    rmsnorm(sc.x, ones, rows, h, cfg.rms_eps, sc.xn, st);
+    dense_gemm(sc.xn, rows, h, qkv_w, wqkv, nullptr, SMO_EPI_BF16, sc.qkv, sc.split, st);
+    for (int c = 0; c < nch; ++c) {
+      const size_t r0 = size_t(c) * b * n;
+      rope_append(sc.qkv + r0 * qkv_w, prefix + size_t(c) * b, nullptr, b, n, nq, nkv, d, s_max, cfg.rope_theta,
+                  sc.q + r0 * nq * d, kc, vc, st);
+      smo_attn_args a{};
+      a.q = sc.q + r0 * nq * d;
+      a.k_cache = kc;
+      a.v_cache = vc;
+      a.mask = mask;
+      a.prefix_len = prefix + size_t(c) * b;
+      a.out = sc.attn + r0 * nq * d;
+      a.b = b;
+      a.n = n;
+      a.n_q = nq;
+      a.n_kv = nkv;
+      a.d = d;
+      a.s_max = s_max;
+      a.max_prefix = max_prefix[size_t(c)];
+      a.workspace = sc.attn_ws;
+      a.workspace_bytes = sc.attn_ws_bytes;
+      attention_launch(a, st);
+    }
+    dense_gemm(sc.attn, rows, nq * d, h, wo, nullptr, SMO_EPI_F32_ADD, sc.x, sc.split, st);
+  }
+
+  // x += W2 . (silu(W1 . rmsnorm(x)) * W3 . rmsnorm(x))  (dense SwiGLU)
+  void ffn_dense(const Scratch& sc, uint16_t* hb, int rows, const uint16_t* w1, const uint16_t* w3,
+                 const uint16_t* w2, int inter, cudaStream_t st) {
+    rmsnorm(sc.x, ones, rows, h, cfg.rms_eps, sc.xn, st);
+    dense_gemm(sc.xn, rows, h, inter, w1, w3, SMO_EPI_SWIGLU, hb, 1, st);
+    dense_gemm(hb, rows, inter, h, w2, nullptr, SMO_EPI_F32_ADD, sc.x, sc.split, st);
+  }
+
+  // final RMSNorm -> LM head with fused argmax partials -> per-row argmax
+  void lm_argmax(const float* xr, int rows, int32_t* out, cudaStream_t st) {
+    rmsnorm(xr, final_norm, rows, h, cfg.rms_eps, xn, st);
+    smo_gemm_args g{};
+    g.x = xn;
+    g.rows = rows;
+    g.K = h;
+    g.N = V;
+    g.groups = 1;
+    g.max_rows_per_group = rows;
+    g.w = lm_w;
+    g.w_pool_blocks = 1;
+    g.epilogue = SMO_EPI_ARGMAX;
+    g.argmax_val = amax_v;
+    g.argmax_idx = amax_i;
+    gemm_launch(g, st);
+    argmax_reduce(amax_v, amax_i, rows, V / 128, out, st);
+  }
+
+  // One drafter step for b requests: token tok_in[r] at position pos[r]
+  // (its K/V appended there), greedy next token into out_tok[r].
+  void draft_forward(int b, const int32_t* tok_in, const int32_t* pos, int max_pos, int32_t* out_tok,
+                     cudaStream_t st) {
+    const Scratch sc{x, xn, qkv, q, attn, attn_ws, attn_ws_bytes, 0};
+    embed(tok_in, embed_w, b, h, x, st);
+    const std::vector<int> mp{max_pos};
+    for (auto& dl : dlayers) {
+      attn_sublayer(sc, dl.wqkv, dl.wo, dl.kc, dl.vc, b, 1, 1, pos, mp, d_mask1, st);
+      ffn_dense(sc, dh, b, dl.w1, dl.w3, dl.w2, dI, st);
+    }
+    lm_argmax(x, b, out_tok, st);
+  }
+
+  // ------------------------------------------------------------------ decode
+  void decode_begin(const int32_t* root_h, const int32_t* kv_h, int b) {
+    SMO_REQUIRE(b > 0 && b <= maxB, "decode_begin: batch exceeds engine capacity");
+    int64_t mx = 0;
+    for (int r = 0; r < b; ++r) {
+      SMO_REQUIRE(kv_h[r] >= 0 && kv_h[r] < s_max, "decode_begin: kv_len out of range");
+      SMO_REQUIRE(root_h[r] >= 0 && root_h[r] < V, "decode_begin: root token out of range");
+      mx = std::max<int64_t>(mx, kv_h[r]);
+    }
+    SMO_CUDA_CHECK(cudaDeviceSynchronize());
+    SMO_CUDA_CHECK(cudaMemcpy(d_root, root_h, size_t(b) * 4, cudaMemcpyHostToDevice));
+    SMO_CUDA_CHECK(cudaMemcpy(d_kvlen, kv_h, size_t(b) * 4, cudaMemcpyHostToDevice));
+    SMO_CUDA_CHECK(cudaMemset(d_hist_n, 0, size_t(maxB) * 4));
+    SMO_CUDA_CHECK(cudaMemset(d_hist, 0xFF, size_t(maxB) * hist_cap * 4));
+    dec_b = b;
+    kv_bound = mx;
+  }
+
+  // draft (k+1 drafter steps) -> verify -> greedy accept -> commit, on device
+  void decode_step(int k, const int32_t* drafts_h, cudaStream_t st) {
+    const int b = dec_b, n = k + 1;
+    SMO_REQUIRE(b > 0, "decode: call smo_engine_prefill or smo_engine_decode_begin first");
+    SMO_REQUIRE(k >= 0 && n <= maxN, "decode: k + 1 exceeds max_verify");
+    SMO_REQUIRE(kv_bound + n <= s_max, "decode: KV capacity (max_seq) exhausted");
+    SMO_REQUIRE(drafts_h || k == 0 || dL > 0, "decode: k > 0 needs a drafter (draft_layers) or planted drafts");
+    const bool planted = drafts_h && k > 0;
+    if (planted) {
+      SMO_CUDA_CHECK(cudaStreamSynchronize(st));  // staging buffer reuse
+      std::memcpy(h_stage, drafts_h, size_t(b) * k * 4);
+      SMO_CUDA_CHECK(cudaMemcpyAsync(d_drafts, h_stage, size_t(b) * k * 4, cudaMemcpyHostToDevice, st));
+    }
+    last_was_decode = true;
+    begin_step(st);  // the first layers' experts stream while the drafter runs
+    decode_prep(d_root, planted ? d_drafts : nullptr, b, n, d_dec_tok, st);
+    // drafter: step t consumes row t (root, d_1, ..., d_k) at kv_len + t and
+    // proposes d_{t+1}; the extra step t = k only appends d_k's draft K/V so
+    // that a fully accepted chain leaves no hole in the drafter's cache
+    last_draft_steps = dL > 0 ? k + 1 : 0;
+    for (int t = 0; dL > 0 && t <= k; ++t) {
+      SMO_CUDA_CHECK(cudaEventRecord(draft_ev[size_t(t)], st));
+      draft_io(d_dec_tok, d_kvlen, t, b, n, d_dtok, d_dpos, st);
+      draft_forward(b, d_dtok, d_dpos, int(kv_bound) + t, d_dout, st);
+      if (!planted && t < k) draft_scatter(d_dout, b, n, t, d_dec_tok, st);
+    }
+    SMO_CUDA_CHECK(cudaEventRecord(ev[3], st));
+    if (last_draft_steps > 0) SMO_CUDA_CHECK(cudaEventRecord(draft_ev[size_t(last_draft_steps)], st));
+    verify_core(b, n, d_dec_tok, nullptr, d_kvlen, int(kv_bound), st);
+    decode_commit(d_dec_tok, d_acc, d_bonus, b, n, hist_cap, d_hist, d_hist_n, d_kvlen, d_root, st);
+    kv_bound += n;
+  }
+
+  // durations (s) of the drafter steps of the last decode step; returns count
+  int draft_times(double* out, size_t n) {
+    SMO_CUDA_CHECK(cudaDeviceSynchronize());
+    if (!last_was_decode) return 0;
+    const int m = last_draft_steps;
+    SMO_REQUIRE(n >= size_t(m), "draft_times: output too small");
+    for (int t = 0; t < m; ++t) {
+      float ms = 0;
+      SMO_CUDA_CHECK(cudaEventElapsedTime(&ms, draft_ev[size_t(t)], draft_ev[size_t(t) + 1]));
+      out[t] = ms * 1e-3;
+    }
+    return m;
+  }
+
+  void decode_read(int32_t* committed, int cap, int32_t* n_committed, int32_t* kv_len, int32_t* root) {
+    SMO_REQUIRE(dec_b > 0, "decode_read: no decode state");
+    const int b = dec_b;
+    SMO_CUDA_CHECK(cudaDeviceSynchronize());
+    if (committed) {
+      SMO_REQUIRE(cap > 0, "decode_read: bad capacity");
+      std::vector<int32_t> hh(size_t(b) * hist_cap);
+      SMO_CUDA_CHECK(cudaMemcpy(hh.data(), d_hist, hh.size() * 4, cudaMemcpyDeviceToHost));
+      for (int r = 0; r < b; ++r)
+        for (int j = 0; j < cap; ++j) committed[size_t(r) * cap + j] = j < hist_cap ? hh[size_t(r) * hist_cap + j] : -1;
+    }
+    if (n_committed) SMO_CUDA_CHECK(cudaMemcpy(n_committed, d_hist_n, size_t(b) * 4, cudaMemcpyDeviceToHost));
+    if (kv_len) SMO_CUDA_CHECK(cudaMemcpy(kv_len, d_kvlen, size_t(b) * 4, cudaMemcpyDeviceToHost));
+    if (root) SMO_CUDA_CHECK(cudaMemcpy(root, d_root, size_t(b) * 4, cudaMemcpyDeviceToHost));
+  }
+
+  // ------------------------------------------------------------------ prefill
+  // Layer-major prefill: every layer's experts are streamed once for the
+  // whole prompt batch; attention runs the prompt as causal chunks of C rows.
+  void prefill(const int32_t* tok_h, const int32_t* len_h, int b, int Lmax, int32_t* next_h, cudaStream_t st) {
+    SMO_REQUIRE(!ep_on, "prefill: not available with expert parallelism");
+    SMO_REQUIRE(b > 0 && b <= maxB && Lmax > 0, "prefill: bad batch");
+    SMO_REQUIRE(tok_h && len_h && next_h, "prefill: null argument");
+    const int g = nq / nkv;
+    const int C = std::max(1, std::min(64, 128 / g));
+    const int nch = (Lmax + C - 1) / C;
+    SMO_REQUIRE(int64_t(nch) * C + maxN <= s_max, "prefill: prompt exceeds max_seq");
+    for (int r = 0; r < b; ++r) SMO_REQUIRE(len_h[r] >= 1 && len_h[r] <= Lmax, "prefill: len out of range");
+    const int Tp = b * nch * C;
+    std::vector<int32_t> tok(size_t(Tp), 0), pre(size_t(nch) * b);
+    for (int c = 0; c < nch; ++c)
+      for (int r = 0; r < b; ++r) {
+        pre[size_t(c) * b + r] = c * C;
+        for (int i = 0; i < C; ++i) {
+          const int p = c * C + i;
+          const int32_t t = p < len_h[r] ? tok_h[size_t(r) * Lmax + p] : 0;
+          SMO_REQUIRE(t >= 0 && t < V, "prefill: token out of range");
+          tok[(size_t(c) * b + r) * C + i] = t;
+        }
+      }
+    std::vector<int> maxpre(static_cast<size_t>(nch));
+    for (int c = 0; c < nch; ++c) maxpre[size_t(c)] = c * C;
+    // prompt-sized scratch (freed at the end: prefill is not a per-step call)
+    std::vector<void*> tmp;
+    auto talloc = [&](size_t bytes) {
+      void* p = nullptr;
+      cudaError_t e = cudaMalloc(&p, std::max<size_t>(bytes, 16));
+      if (e != cudaSuccess) {
+        for (void* q2 : tmp) cudaFree(q2);
+        throw Error(SMO_CAPACITY, "prefill: cudaMalloc(" + std::to_string(bytes) + ") failed");
+      }
+      tmp.push_back(p);
+      return p;
+    };
+    const int PT = Tp * K;
+    auto* p_tok = static_cast<int32_t*>(talloc(size_t(Tp) * 4));
+    auto* p_pre = static_cast<int32_t*>(talloc(pre.size() * 4));
+    auto* p_len = static_cast<int32_t*>(talloc(size_t(b) * 4));
+    auto* p_mask = static_cast<uint64_t*>(talloc(size_t(b) * C * 8));
+    Scratch sc{};
+    sc.x = static_cast<float*>(talloc(size_t(Tp) * h * 4));
+    sc.xn = static_cast<uint16_t*>(talloc(size_t(Tp) * h * 2));
+    sc.qkv = static_cast<uint16_t*>(talloc(size_t(Tp) * qkv_w * 2));
+    sc.q = static_cast<uint16_t*>(talloc(size_t(Tp) * nq * d * 2));
+    sc.attn = static_cast<uint16_t*>(talloc(size_t(Tp) * nq * d * 2));
+    sc.split = 1;
+    {
+      smo_attn_args wa{};
+      wa.b = b;
+      wa.n = C;
+      wa.n_q = nq;
+      wa.n_kv = nkv;
+      wa.d = d;
+      wa.s_max = s_max;
+      wa.max_prefix = (nch - 1) * C;
+      wa.q = wa.k_cache = wa.v_cache = wa.out = reinterpret_cast<void*>(1);
+      wa.mask = reinterpret_cast<const uint64_t*>(1);
+      wa.prefix_len = reinterpret_cast<const int32_t*>(1);
+      sc.attn_ws_bytes = attention_workspace(wa);
+      sc.attn_ws = talloc(sc.attn_ws_bytes);
+      SMO_CUDA_CHECK(cudaMemsetAsync(sc.attn_ws, 0, sc.attn_ws_bytes, st));
+    }
+    auto* p_ids = static_cast<int32_t*>(talloc(size_t(PT) * 4));
+    auto* p_rw = static_cast<float*>(talloc(size_t(PT) * 4));
+    auto* p_off = static_cast<int32_t*>(talloc(size_t(E + 1) * 4));
+    auto* p_perm = static_cast<int32_t*>(talloc(size_t(PT) * 4));
+    auto* p_pos = static_cast<int32_t*>(talloc(size_t(PT) * 4));
+    auto* p_xp = static_cast<uint16_t*>(talloc(size_t(PT) * h * 2));
+    auto* p_hb = static_cast<uint16_t*>(talloc(size_t(PT) * hi * 2));
+    auto* p_y = static_cast<float*>(talloc(size_t(PT) * h * 4));
+    uint16_t* p_hs = cfg.shared_inter > 0 ? static_cast<uint16_t*>(talloc(size_t(Tp) * cfg.shared_inter * 2)) : nullptr;
+    uint16_t* p_dh = dL > 0 ? static_cast<uint16_t*>(talloc(size_t(Tp) * dI * 2)) : nullptr;
+    SMO_CUDA_CHECK(cudaMemcpyAsync(p_tok, tok.data(), tok.size() * 4, cudaMemcpyHostToDevice, st));
+    SMO_CUDA_CHECK(cudaMemcpyAsync(p_pre, pre.data(), pre.size() * 4, cudaMemcpyHostToDevice, st));
+    SMO_CUDA_CHECK(cudaMemcpyAsync(p_len, len_h, size_t(b) * 4, cudaMemcpyHostToDevice, st));
+    build_mask(nullptr, b, C, p_mask, st);
+
+    // target: layer-major, experts streamed once per layer
+    last_was_decode = false;
+    begin_step(st);
+    double h2d_bytes = step_h2d_bytes;
+    embed(p_tok, embed_w, Tp, h, sc.x, st);
+    for (int l = 0; l < L; ++l) {
+      Layer& ly = layers[l];
+      attn_sublayer(sc, ly.wqkv, ly.wo, ly.kc, ly.vc, b, C, nch, p_pre, maxpre, p_mask, st);
+      rmsnorm(sc.x, ones, Tp, h, cfg.rms_eps, sc.xn, st);
+      router_topk(sc.xn, ly.router, Tp, h, E, K, nullptr, p_ids, p_rw, st);
+      permute(p_ids, Tp, K, E, sc.xn, h, p_off, p_perm, p_pos, p_xp, st);
+      if (cfg.shared_inter > 0) {
+        dense_gemm(sc.xn, Tp, h, cfg.shared_inter, ly.ws1, ly.ws3, SMO_EPI_SWIGLU, p_hs, 1, st);
+        dense_gemm(p_hs, Tp, cfg.shared_inter, h, ly.ws2, nullptr, SMO_EPI_F32_ADD, sc.x, 1, st);
+      }
+      SMO_CUDA_CHECK(cudaStreamWaitEvent(st, slot_ready[l % slots], 0));
+      smo_gemm_args g2{};
+      g2.x = p_xp;
+      g2.rows = PT;
+      g2.K = h;
+      g2.N = hi;
+      g2.groups = E;
+      g2.row_offsets = p_off;
+      g2.max_rows_per_group = Tp;
+      g2.w = pool;
+      g2.w_up = pool + size_t(hi) * h;
+      g2.w_block_stride = blk_bytes;
+      g2.w_pool_blocks = pool_blocks;
+      g2.w_index = d_w_index + size_t(l) * E;
+      g2.epilogue = SMO_EPI_SWIGLU;
+      g2.out = p_hb;
+      g2.ldo = hi;
+      gemm_launch(g2, st);
+      g2 = smo_gemm_args{};
+      g2.x = p_hb;
+      g2.rows = PT;
+      g2.K = hi;
+      g2.N = h;
+      g2.groups = E;
+      g2.row_offsets = p_off;
+      g2.max_rows_per_group = Tp;
+      g2.w = pool + 2 * size_t(hi) * h;
+      g2.w_block_stride = blk_bytes;
+      g2.w_pool_blocks = pool_blocks;
+      g2.w_index = d_w_index + size_t(l) * E;
+      g2.epilogue = SMO_EPI_F32;
+      g2.out = p_y;
+      g2.ldo = h;
+      gemm_launch(g2, st);
+      SMO_CUDA_CHECK(cudaEventRecord(slot_free[l % slots], st));
+      unpermute_combine(p_y, p_pos, p_rw, Tp, K, h, sc.x, st);
+      if (l + slots < L) h2d_bytes += enqueue_h2d(l + slots, nullptr, nullptr);
+    }
+    SMO_CUDA_CHECK(cudaStreamWaitEvent(st, slot_ready[(L - 1) % slots], 0));
+    prefill_last(sc.x, p_len, b, C, h, x, st);
+    lm_argmax(x, b, d_root, st);
+    // drafter: its own residual stream over the same prompt
+    if (dL > 0) {
+      embed(p_tok, embed_w, Tp, h, sc.x, st);
+      for (auto& dl : dlayers) {
+        attn_sublayer(sc, dl.wqkv, dl.wo, dl.kc, dl.vc, b, C, nch, p_pre, maxpre, p_mask, st);
+        ffn_dense(sc, p_dh, Tp, dl.w1, dl.w3, dl.w2, dI, st);
+      }
+    }
+    SMO_CUDA_CHECK(cudaEventRecord(ev[1], st));
+    SMO_CUDA_CHECK(cudaMemcpyAsync(d_kvlen, p_len, size_t(b) * 4, cudaMemcpyDeviceToDevice, st));
+    SMO_CUDA_CHECK(cudaMemsetAsync(d_hist_n, 0, size_t(maxB) * 4, st));
+    SMO_CUDA_CHECK(cudaMemsetAsync(d_hist, 0xFF, size_t(maxB) * hist_cap * 4, st));
+    SMO_CUDA_CHECK(cudaMemcpyAsync(next_h, d_root, size_t(b) * 4, cudaMemcpyDeviceToHost, st));
+    SMO_CUDA_CHECK(cudaStreamSynchronize(st));
+    for (void* p : tmp) cudaFree(p);
+    pending_attn.clear();
+    pending_moe.clear();
+    pending_h2d.clear();
+    last_h2d_bytes = h2d_bytes;
+    dec_b = b;
+    kv_bound = Lmax;
   }
 
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending_attn, pending_moe, pending_h2d;
@@ -805,7 +1249,14 @@ struct Engine {
     };
     smo_stage_times r{};
     float ms = 0;
-    cudaEventElapsedTime(&ms, ev[0], ev[1]);
+    if (last_was_decode) {  // iteration = draft (ev0 -> ev3) + target (ev3 -> ev1)
+      float md = 0;
+      cudaEventElapsedTime(&md, ev[0], ev[3]);
+      cudaEventElapsedTime(&ms, ev[3], ev[1]);
+      r.draft = md * 1e-3;
+    } else {
+      cudaEventElapsedTime(&ms, ev[0], ev[1]);
+    }
     r.target_total = ms * 1e-3;
     r.attention = span(pending_attn);
     r.gpu_moe = span(pending_moe);
@@ -859,6 +1310,43 @@ smo_status smo_engine_verify(smo_engine* e, const smo_verify_batch* in, smo_veri
   });
 }
 
+smo_status smo_engine_prefill(smo_engine* e, const int32_t* tokens, const int32_t* len, int32_t b, int32_t max_len,
+                              int32_t* next_token, smo_stream stream) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(e, "engine: null argument");
+    e->impl.prefill(tokens, len, b, max_len, next_token, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+smo_status smo_engine_decode_begin(smo_engine* e, const int32_t* root, const int32_t* kv_len, int32_t b) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(e && root && kv_len, "engine: null argument");
+    e->impl.decode_begin(root, kv_len, b);
+  });
+}
+
+smo_status smo_engine_decode_step(smo_engine* e, int32_t k, const int32_t* drafts, smo_stream stream) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(e, "engine: null argument");
+    e->impl.decode_step(k, drafts, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+smo_status smo_engine_decode_read(smo_engine* e, int32_t* committed, int32_t cap, int32_t* n_committed,
+                                  int32_t* kv_len, int32_t* root) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(e, "engine: null argument");
+    e->impl.decode_read(committed, cap, n_committed, kv_len, root);
+  });
+}
+
+smo_status smo_engine_draft_times(smo_engine* e, double* out, size_t n, int32_t* steps) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(e && out && steps, "engine: null argument");
+    *steps = e->impl.draft_times(out, n);
+  });
+}
+
 smo_status smo_engine_last_times(smo_engine* e, smo_stage_times* t) {
   return smo::run_guarded([&] {
     SMO_REQUIRE(e && t, "engine: null argument");
@@ -878,14 +1366,18 @@ smo_status smo_engine_debug_tensor(smo_engine* e, const char* name, int32_t laye
     SMO_REQUIRE(e && name && dst, "engine: null argument");
     SMO_REQUIRE(e->impl.debug, "engine: created without SMO_ENGINE_DEBUG");
     const std::string nm(name);
-    if (nm == "k_cache" || nm == "v_cache") {  // live cache contents of a layer
+    if (nm == "k_cache" || nm == "v_cache" || nm == "draft_k_cache" || nm == "draft_v_cache") {
+      // live cache contents of a (target or drafter) layer
       smo::Engine& g = e->impl;
-      SMO_REQUIRE(layer >= 0 && layer < g.L, "engine: layer out of range");
+      const bool dr = nm.rfind("draft_", 0) == 0;
+      SMO_REQUIRE(layer >= 0 && layer < (dr ? g.dL : g.L), "engine: layer out of range");
       const size_t cb = size_t(g.maxB) * g.nkv * g.s_max * g.d * 2;
       SMO_REQUIRE(bytes <= cb, "engine: debug tensor smaller than requested");
       SMO_CUDA_CHECK(cudaDeviceSynchronize());
-      SMO_CUDA_CHECK(cudaMemcpy(dst, nm == "k_cache" ? g.layers[layer].kc : g.layers[layer].vc, bytes,
-                                cudaMemcpyDeviceToHost));
+      const bool kk = nm == "k_cache" || nm == "draft_k_cache";
+      const void* src = dr ? (kk ? g.dlayers[layer].kc : g.dlayers[layer].vc)
+                           : (kk ? g.layers[layer].kc : g.layers[layer].vc);
+      SMO_CUDA_CHECK(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
       return;
     }
     auto it = e->impl.dbg.find(name);

@@ -384,6 +384,65 @@ __global__ void build_mask_kernel(const int32_t* __restrict__ parent, int b, int
   mask[row] = m;
 }
 
+
+// ---------------------------------------------------------------- decode loop
+// (draft -> verify -> accept -> commit, all on device so a
+// decode iteration needs no host round trip)
+
+// tokens[r*n] = root[r]; planted drafts (test/bench input) fill rows 1..k.
+__global__ void decode_prep_kernel(const int32_t* __restrict__ root, const int32_t* __restrict__ drafts, int b,
+                                   int n, int32_t* __restrict__ tokens) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= b * n) return;
+  const int r = i / n, j = i % n;
+  if (j == 0) tokens[i] = root[r];
+  else if (drafts) tokens[i] = drafts[size_t(r) * (n - 1) + (j - 1)];
+}
+
+// Draft step t: input token tokens[r*n + t] at position kv_len[r] + t.
+__global__ void draft_io_kernel(const int32_t* __restrict__ tokens, const int32_t* __restrict__ kv_len, int t, int b,
+                                int n, int32_t* __restrict__ tok_in, int32_t* __restrict__ pos) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= b) return;
+  tok_in[r] = tokens[size_t(r) * n + t];
+  pos[r] = kv_len[r] + t;
+}
+
+__global__ void draft_scatter_kernel(const int32_t* __restrict__ out, int b, int n, int t, int32_t* __restrict__ tokens) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < b) tokens[size_t(r) * n + t + 1] = out[r];
+}
+
+// Commit the greedy verdict of a chain step: accepted drafts d_1..d_a and the
+// bonus token are appended to the history (committed = a + 1, config.hpp:69-70);
+// the chain's K/V rows root..d_a are already in place, so kv_len += a + 1 and
+// the bonus becomes the next root.
+__global__ void decode_commit_kernel(const int32_t* __restrict__ tokens, const int32_t* __restrict__ acc,
+                                     const int32_t* __restrict__ bonus, int b, int n, int cap, int32_t* hist,
+                                     int32_t* hist_n, int32_t* kv_len, int32_t* root) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= b) return;
+  const int a = acc[r];
+  int h = hist_n[r];
+  int32_t* dst = hist + size_t(r) * cap;
+  for (int j = 1; j <= a; ++j)
+    if (h < cap) dst[h++] = tokens[size_t(r) * n + j];
+  if (h < cap) dst[h++] = bonus[r];
+  hist_n[r] = h;
+  kv_len[r] += a + 1;
+  root[r] = bonus[r];
+}
+
+// Prefill: copy the residual row of each request's last prompt token
+// (position len-1; rows are chunk-major: ((c*b + r)*C + i)) to row r.
+__global__ void prefill_last_kernel(const float* __restrict__ x, const int32_t* __restrict__ len, int b, int C, int h,
+                                    float* __restrict__ out) {
+  const int r = blockIdx.x;
+  const int p = len[r] - 1, c = p / C, i = p % C;
+  const float* src = x + (size_t(c * b + r) * C + i) * h;
+  for (int j = threadIdx.x; j < h; j += blockDim.x) out[size_t(r) * h + j] = src[j];
+}
+
 inline int grid_for(uint64_t n, int block) {
   const uint64_t g = (n + block - 1) / block;
   return int(g > 148ull * 32 ? 148ull * 32 : (g ? g : 1));
@@ -528,6 +587,38 @@ void kv_rollback(void* const* kcs, void* const* vcs, int n_layers, const int32_t
     count_launch();
     SMO_CUDA_CHECK(cudaGetLastError());
   }
+}
+
+void decode_prep(const int32_t* root, const int32_t* drafts, int b, int n, int32_t* tokens, cudaStream_t st) {
+  decode_prep_kernel<<<(b * n + 127) / 128, 128, 0, st>>>(root, drafts, b, n, tokens);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+void draft_io(const int32_t* tokens, const int32_t* kv_len, int t, int b, int n, int32_t* tok_in, int32_t* pos,
+              cudaStream_t st) {
+  draft_io_kernel<<<(b + 127) / 128, 128, 0, st>>>(tokens, kv_len, t, b, n, tok_in, pos);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+void draft_scatter(const int32_t* out, int b, int n, int t, int32_t* tokens, cudaStream_t st) {
+  draft_scatter_kernel<<<(b + 127) / 128, 128, 0, st>>>(out, b, n, t, tokens);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+void decode_commit(const int32_t* tokens, const int32_t* acc, const int32_t* bonus, int b, int n, int cap,
+                   int32_t* hist, int32_t* hist_n, int32_t* kv_len, int32_t* root, cudaStream_t st) {
+  decode_commit_kernel<<<(b + 127) / 128, 128, 0, st>>>(tokens, acc, bonus, b, n, cap, hist, hist_n, kv_len, root);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+void prefill_last(const float* x, const int32_t* len, int b, int C, int h, float* out, cudaStream_t st) {
+  prefill_last_kernel<<<b, 256, 0, st>>>(x, len, b, C, h, out);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
 }
 
 }  // namespace smo

@@ -36,6 +36,8 @@ class ModelShape:
     lm_scale: float = 1.0
     router_scale: float = 1.0
     shared_inter: int = 0  # always-on shared expert (config 4), resident in HBM
+    draft_layers: int = 0  # drafter depth (DraftModelSpec.n_layers); 0: no drafter
+    draft_inter: int = 0   # drafter dense SwiGLU width
 
     @property
     def expert_bytes(self) -> int:
@@ -44,7 +46,8 @@ class ModelShape:
     def to_c(self) -> L.ModelConfig:
         return L.ModelConfig(self.hidden, self.inter, self.n_expert, self.top_k, self.n_layers, self.n_q_heads,
                              self.n_kv_heads, self.head_dim, self.vocab, self.rope_theta, self.rms_eps, self.seed,
-                             self.lm_scale, self.router_scale, self.shared_inter)
+                             self.lm_scale, self.router_scale, self.shared_inter, self.draft_layers,
+                             self.draft_inter)
 
 
 # BASELINE.json configs
@@ -163,6 +166,48 @@ class VerifyEngine:
         inp = L.VerifyBatch(b, n, p(tokens), p(parent), p(prefix_len), 1)
         out = L.VerifyOutput(p(acc), p(bonus), p(keep), p(target), 1)
         L.check(L.load().smo_engine_verify(self._h, C.byref(inp), C.byref(out), C.c_void_p(stream or 0)))
+
+    # ------------------------------------------------------------ decode loop
+    def prefill(self, prompts, stream: Optional[int] = None) -> np.ndarray:
+        """Run prompts (list of int sequences, or [b, L] array with all rows
+        full) through the target and drafter; returns the greedy next token per
+        request and sets the decode state (kv_len = prompt length)."""
+        if isinstance(prompts, np.ndarray) and prompts.ndim == 2:
+            seqs = [list(r) for r in prompts]
+        else:
+            seqs = [list(p) for p in prompts]
+        b, lmax = len(seqs), max(len(p) for p in seqs)
+        tok = np.zeros((b, lmax), np.int32)
+        for r, p in enumerate(seqs):
+            tok[r, :len(p)] = p
+        ln = np.array([len(p) for p in seqs], np.int32)
+        nxt = np.zeros(b, np.int32)
+        L.check(L.load().smo_engine_prefill(self._h, tok.ctypes.data_as(C.c_void_p), ln.ctypes.data_as(C.c_void_p), b,
+                                            lmax, nxt.ctypes.data_as(C.c_void_p), C.c_void_p(stream or 0)))
+        return nxt
+
+    def decode_begin(self, root, kv_len) -> None:
+        r = np.ascontiguousarray(root, np.int32)
+        k = np.ascontiguousarray(kv_len, np.int32)
+        L.check(L.load().smo_engine_decode_begin(self._h, r.ctypes.data_as(C.c_void_p), k.ctypes.data_as(C.c_void_p),
+                                                 r.size))
+
+    def decode_step(self, k: int, drafts=None, stream: Optional[int] = None) -> None:
+        """One draft -> verify -> accept -> commit iteration (asynchronous).
+        drafts: None (drafter proposes) or [b, k] planted drafts."""
+        d = None if drafts is None else np.ascontiguousarray(drafts, np.int32)
+        L.check(L.load().smo_engine_decode_step(self._h, k, None if d is None else d.ctypes.data_as(C.c_void_p),
+                                                C.c_void_p(stream or 0)))
+
+    def decode_read(self, b: int, cap: int):
+        """(committed [b, cap] -1 padded, n_committed [b], kv_len [b], root [b])"""
+        com = np.zeros((b, cap), np.int32)
+        n = np.zeros(b, np.int32)
+        kv = np.zeros(b, np.int32)
+        root = np.zeros(b, np.int32)
+        vp = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        L.check(L.load().smo_engine_decode_read(self._h, vp(com), cap, vp(n), vp(kv), vp(root)))
+        return com, n, kv, root
 
     def last_times(self) -> dict:
         t = L.StageTimes()

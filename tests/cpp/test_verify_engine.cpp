@@ -138,3 +138,64 @@ TEST_CASE("measured profiles drive fit_latency_models, optimize and the controll
   const int k2 = ctl.update(700, 4);
   CHECK(k2 <= k1);
 }
+
+TEST_CASE("closed loop: prefill -> measured fit -> controller picks k -> decode commits the greedy sequence") {
+  HardwareSpec hw = b200();
+  ModelSpec m = tiny();
+  WorkloadSpec w = apps();
+  Hyperparameters hp;
+  hp.b = 3;
+  hp.k = 4;
+  // two hot-cached experts: the layers stream different byte counts, so the
+  // H2D_EXPERTS fit has two driving values
+  hp.mem_policy.expert_cache_bytes = 2.0 * 3.0 * m.expert_size() * 2.0;
+  MemoryPlan plan = plan_memory(hw, m, w, hp.b, hp.mem_policy);
+  EngineOptions opt;
+  opt.max_seq = 512;
+  opt.seed = 0x5EED + 7;
+  opt.lm_scale = 8.0f;  // decisive greedy margins (SURVEY.md §7.5 screening)
+  opt.router_scale = 4.0f;
+  std::vector<std::vector<std::int32_t>> prompts(3);
+  std::uint64_t lcg = 12345;
+  const int lens[3] = {40, 17, 9};
+  for (int r = 0; r < 3; ++r)
+    for (int i = 0; i < lens[r]; ++i) {
+      lcg = lcg * 6364136223846793005ull + 1442695040888963407ull;
+      prompts[std::size_t(r)].push_back(std::int32_t((lcg >> 33) % 32000));
+    }
+
+  VerifyEngine eng(hw, m, hp, plan, opt);
+  const std::vector<std::int32_t> next = eng.prefill(prompts);
+  CHECK(eng.kv_len() == std::vector<std::int32_t>({40, 17, 9}));
+  for (int k : {1, 2, 4}) {  // measured warm-up across draft lengths
+    IterationResult r = eng.decode_step(k);
+    CHECK(r.draft_dag.size() == std::size_t(k + 1));
+    CHECK(r.breakdown.draft_total > 0);
+    CHECK(r.breakdown.iteration >= r.breakdown.target_total);
+  }
+  LatencyModel lm = fit_latency_models(eng.profile());
+  CHECK(lm.count(EventKind::DRAFT_GPU_STEP) == 1);
+  DraftLengthController ctl([&](std::int64_t prefix, std::int64_t active) {
+    Hyperparameters base;
+    base.b = active;
+    return optimize(hw, m, w, &lm, 4, base, prefix).k;
+  });
+  const std::vector<IterationResult> rs = eng.decode(6, ctl);
+  CHECK(rs.size() == 6);
+  CHECK(eng.chosen_k().size() == 6);
+  for (std::size_t i = 1; i < eng.chosen_k().size(); ++i) CHECK(eng.chosen_k()[i] <= eng.chosen_k()[i - 1]);
+  const auto spec = eng.committed();
+
+  // greedy invariance: plain decoding (k = 0) on a second engine commits the
+  // same tokens (acceptance only changes how many per step)
+  VerifyEngine plain(hw, m, hp, plan, opt);
+  CHECK(plain.prefill(prompts) == next);
+  std::size_t need = 0;
+  for (const auto& c : spec) need = std::max(need, c.size());
+  for (std::size_t i = 0; i < need; ++i) plain.decode_step(0);
+  const auto ref = plain.committed();
+  for (std::size_t r = 0; r < spec.size(); ++r) {
+    REQUIRE(ref[r].size() >= spec[r].size());
+    CHECK(std::vector<std::int32_t>(ref[r].begin(), ref[r].begin() + std::ptrdiff_t(spec[r].size())) == spec[r]);
+  }
+}

@@ -238,3 +238,100 @@ class OracleModel:
         xf = self.rmsnorm(x)
         logits = self.gemm(xf, self.lm_head())
         return xf, logits
+
+
+# ------------------------------------------------------------------ drafter
+# (engine.cu tid::draft: layer l base 700000 + 100 l; +1 Wqkv, +2 Wo, +3 W1,
+# +4 W3, +5 W2 — dense decoder layers sharing the target's embed / LM head)
+def _draft_tid(l):
+    return 700000 + 100 * l
+
+
+def draft_weights(om, l):
+    s = om.s
+    key = ("draft", l)
+    if key not in om._cache:
+        h, di, k = s.hidden, s.draft_inter, s.n_q_heads * s.head_dim
+        b = _draft_tid(l)
+        om._cache[key] = (om._fill(om.qkv_w * h, b + 1, math.sqrt(3.0 / h)).reshape(om.qkv_w, h),
+                          om._fill(h * k, b + 2, math.sqrt(3.0 / k)).reshape(h, k),
+                          om._fill(di * h, b + 3, math.sqrt(3.0 / h)).reshape(di, h),
+                          om._fill(di * h, b + 4, math.sqrt(3.0 / h)).reshape(di, h),
+                          om._fill(h * di, b + 5, math.sqrt(3.0 / di)).reshape(h, di))
+    return om._cache[key]
+
+
+def attn_block(om, x, wqkv, wo, kc, vc, prefix, n):
+    """x + Wo·attn(RoPE(Wqkv·rmsnorm(x))) for a batch of chains (rows r*n+i
+    at prefix[r]+i); K/V appended to kc/vc [b, n_kv, s_max, d] in place."""
+    s = om.s
+    b = len(prefix)
+    T = b * n
+    d, nq, nkv = s.head_dim, s.n_q_heads, s.n_kv_heads
+    qkv = O.f32_to_bf16(om.gemm(om.rmsnorm(x), wqkv)).reshape(T, -1)
+    pos = np.concatenate([prefix[r] + np.arange(n) for r in range(b)]).astype(np.int32)
+    q = om.rope(qkv[:, :nq * d], pos, nq).reshape(T, nq, d)
+    k = om.rope(qkv[:, nq * d:(nq + nkv) * d], pos, nkv).reshape(T, nkv, d)
+    v = qkv[:, (nq + nkv) * d:].reshape(T, nkv, d)
+    for r in range(b):
+        for i in range(n):
+            kc[r, :, prefix[r] + i] = k[r * n + i]
+            vc[r, :, prefix[r] + i] = v[r * n + i]
+    mbits = np.tile(om.mask_bits(None, n), b)
+    attn = om.attention(q, kc, vc, mbits, np.asarray(prefix, np.int32), n)
+    return (x + om.gemm(attn.reshape(T, nq * d), wo)).astype(np.float32)
+
+
+def swiglu_dense(om, x, w1, w3, w2):
+    """x + W2·bf16(silu(W1·xn)·(W3·xn)) with xn = rmsnorm(x) (fp32 out)."""
+    xn = om.rmsnorm(x)
+    y = np.zeros((x.shape[0], om.s.hidden), np.float32)
+    O.lib().orc_expert_swiglu(O._ptr(np.ascontiguousarray(xn)), x.shape[0], om.s.hidden, w1.shape[0], O._ptr(w1),
+                              O._ptr(w3), O._ptr(w2), O._ptr(y))
+    return (x + y).astype(np.float32)
+
+
+class OracleDecoder:
+    """Greedy autoregressive decoding of ONE request by the CPU oracle: the
+    sequence every speculative decode must commit under greedy verification
+    (acceptance only decides how many of these tokens one step commits)."""
+
+    def __init__(self, om, s_max):
+        s = om.s
+        self.om, self.s_max = om, s_max
+        shape = (1, s.n_kv_heads, s_max, s.head_dim)
+        self.kc = [np.zeros(shape, np.uint16) for _ in range(s.n_layers)]
+        self.vc = [np.zeros(shape, np.uint16) for _ in range(s.n_layers)]
+        self.len = 0
+
+    def run(self, tokens):
+        """Feed tokens (a chain) at the current position; returns fp32 logits [n, V]."""
+        om = self.om
+        n = len(tokens)
+        x = O.bf16_to_f32(om.embed()[np.asarray(tokens)]).astype(np.float32)
+        for l in range(om.s.n_layers):
+            x, _ = om.layer(l, x, self.kc[l], self.vc[l], np.array([self.len], np.int32), n)
+        self.len += n
+        return om.head(x)[1]
+
+    def prefill(self, prompt, chunk):
+        logits = None
+        for c in range(0, len(prompt), chunk):
+            logits = self.run(prompt[c:c + chunk])
+        return logits[-1]
+
+    @staticmethod
+    def margin(logits_row):
+        top = np.sort(logits_row)[-2:]
+        return float(top[1] - top[0]) / float(np.std(logits_row) + 1e-30)
+
+    def greedy(self, prompt, steps, chunk):
+        """(tokens: the greedy next token after the prompt then `steps` more,
+        margins: top-1 minus top-2 logit over the logit std for each)."""
+        lg = self.prefill(list(prompt), chunk)
+        toks, margins = [int(np.argmax(lg))], [self.margin(lg)]
+        for _ in range(steps):
+            lg = self.run([toks[-1]])[-1]
+            toks.append(int(np.argmax(lg)))
+            margins.append(self.margin(lg))
+        return toks, margins

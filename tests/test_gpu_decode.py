@@ -1,0 +1,214 @@
+"""GPU: the KV lifecycle and decode loop around the verify step (SURVEY.md §8
+f1/f2): layer-major chunked prefill, drafter, draft -> verify -> accept ->
+commit on device.
+
+The oracle is greedy autoregressive decoding by the CPU restatement
+(tests/oracle_model.OracleDecoder). Under greedy verification every committed
+token of ANY speculative decode is the target's greedy token given the
+history — acceptance only decides how many tokens a step commits
+(specdec.hpp:57-85 with the draw replaced by argmax). The
+oracle walks along the GPU's own committed sequence (teacher forcing), so one
+near-tie cannot derail the comparison: positions whose oracle top-1/top-2
+logit margin is below MARGIN (bf16 noise) only need to be within that margin
+(margin screening as in SURVEY.md §7.5).
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+MARGIN = 0.05  # top-1 minus top-2 logit, in units of the row's logit std
+PROMPTS = [70, 33, 5]  # ragged prompt lengths (chunks of C = 32 rows for g = 4)
+
+
+def _shape():
+    from paper_2508_21706_b200.engine import TINY
+    return dataclasses.replace(TINY, seed=0x5EED + 7, lm_scale=8.0, router_scale=4.0, draft_layers=1,
+                               draft_inter=512)
+
+
+def _chunk(s):
+    return max(1, min(64, 128 // (s.n_q_heads // s.n_kv_heads)))
+
+
+def _prompts(s):
+    rng = np.random.default_rng(11)
+    return [rng.integers(0, s.vocab, size=L).astype(np.int32) for L in PROMPTS]
+
+
+@pytest.fixture(scope="module")
+def ref(cuda):
+    """Oracle greedy continuations (+ margins) of the test prompts."""
+    import oracle_model
+    s = _shape()
+    om = oracle_model.OracleModel(s)
+    s_max = 256
+    out = []
+    for p in _prompts(s):
+        dec = oracle_model.OracleDecoder(om, s_max)
+        toks, margins = dec.greedy(p, 0, _chunk(s))
+        out.append((toks, margins))
+    return s, om, out
+
+
+def _engine(s, n_max=6, debug=False):
+    from paper_2508_21706_b200.engine import VerifyEngine
+    return VerifyEngine(s, max_batch=len(PROMPTS), max_verify=n_max, max_seq=256, debug=debug)
+
+
+def test_prefill_matches_oracle(ref, oracle):
+    import oracle_model
+    s, om, out = ref
+    eng = _engine(s, debug=True)
+    prompts = _prompts(s)
+    nxt = eng.prefill(prompts)
+    for r, (toks, margins) in enumerate(out):
+        if margins[0] >= MARGIN:
+            assert nxt[r] == toks[0], f"request {r}: prefill next token {nxt[r]} != oracle {toks[0]}"
+    # K/V written by the chunked prefill vs the oracle's (teacher-forced per chunk)
+    f32 = oracle.bf16_to_f32
+    d, nkv = s.head_dim, s.n_kv_heads
+    for r, p in enumerate(prompts):
+        dec = oracle_model.OracleDecoder(om, 256)
+        dec.prefill(list(p), _chunk(s))
+        for l in range(s.n_layers):
+            kc = eng.debug_tensor("k_cache", l, (len(PROMPTS), nkv, 256, d), np.uint16)
+            vc = eng.debug_tensor("v_cache", l, (len(PROMPTS), nkv, 256, d), np.uint16)
+            for got, exp, nm in ((kc, dec.kc[l], "K"), (vc, dec.vc[l], "V")):
+                g = f32(got[r, :, :len(p)]).astype(np.float64)
+                e = f32(exp[0, :, :len(p)]).astype(np.float64)
+                err = np.sqrt(np.mean((g - e) ** 2) / np.mean(e ** 2))
+                assert err < 2e-2, f"request {r} layer {l} {nm}: rel-RMS {err:.3e}"
+    # the drafter's K/V over the same prompt (dense layers, oracle restated)
+    dw = oracle_model.draft_weights(om, 0)
+    for r, p in enumerate(prompts):
+        kc = np.zeros((1, nkv, 256, d), np.uint16)
+        vc = np.zeros_like(kc)
+        C = _chunk(s)
+        for c in range(0, len(p), C):
+            x = f32(om.embed()[p[c:c + C]]).astype(np.float32)
+            oracle_model.attn_block(om, x, dw[0], dw[1], kc, vc, np.array([c], np.int32), len(p[c:c + C]))
+        got = eng.debug_tensor("draft_k_cache", 0, (len(PROMPTS), nkv, 256, d), np.uint16)
+        g = f32(got[r, :, :len(p)]).astype(np.float64)
+        e = f32(kc[0, :, :len(p)]).astype(np.float64)
+        err = np.sqrt(np.mean((g - e) ** 2) / np.mean(e ** 2))
+        assert err < 1e-2, f"request {r} drafter K: rel-RMS {err:.3e}"
+    eng.close()
+
+
+def _assert_greedy(lg, tok, where):
+    """tok must be the argmax of the oracle logits row lg; where the top-1 /
+    top-2 margin is below MARGIN (a bf16-noise tie) it must be within it."""
+    top = int(np.argmax(lg))
+    std = float(np.std(lg))
+    if (lg[top] - np.sort(lg)[-2]) / std >= MARGIN:
+        assert tok == top, f"{where}: committed {tok} != oracle greedy {top}"
+        return 1
+    assert lg[tok] >= lg[top] - MARGIN * std, f"{where}: committed {tok} is not a near-tie of {top}"
+    return 0
+
+
+def _teacher_forced(om, prompt, root, committed, where):
+    """Walk the oracle along the GPU's own sequence: the prefill's next token
+    (root) and every committed token must be the oracle's greedy choice given
+    everything before it. Returns the number of decisive checks."""
+    import oracle_model
+    dec = oracle_model.OracleDecoder(om, 256)
+    lg = dec.prefill(list(prompt), _chunk(om.s))
+    ok = 0
+    for i, tok in enumerate([int(root)] + [int(t) for t in committed]):
+        ok += _assert_greedy(lg, tok, f"{where} token {i}")
+        lg = dec.run([tok])[-1]
+    return ok
+
+
+def test_decode_planted_drafts_commit_greedy_sequence(ref):
+    """Planted drafts = the oracle's next k greedy tokens (from the GPU's own
+    committed state) corrupted from a random index on: each step must accept
+    exactly the uncorrupted prefix, and every committed token is greedy."""
+    import copy
+    import oracle_model
+    s, om, _ = ref
+    b, k = len(PROMPTS), 4
+    prompts = _prompts(s)
+    eng = _engine(s)
+    nxt = eng.prefill(prompts)
+    decs, lgs = [], []
+    for r, p in enumerate(prompts):  # oracle state after prompt + root
+        dec = oracle_model.OracleDecoder(om, 256)
+        lg = dec.prefill(list(p), _chunk(s))
+        _assert_greedy(lg, int(nxt[r]), f"request {r} prefill")
+        decs.append(dec)
+        lgs.append(dec.run([int(nxt[r])])[-1])
+    rng = np.random.default_rng(5)
+    pos = np.zeros(b, np.int64)
+    seen = set()
+    for step in range(8):
+        drafts = np.zeros((b, k), np.int32)
+        cut = rng.integers(0, k + 1, size=b)  # first corrupted draft index (k: none)
+        decisive = np.zeros(b, bool)
+        for r in range(b):
+            sim, lg, margins = copy.deepcopy(decs[r]), lgs[r], []
+            for j in range(k):
+                t = int(np.argmax(lg))
+                margins.append(oracle_model.OracleDecoder.margin(lg))
+                drafts[r, j] = t if j < cut[r] else (t + 1 + j) % s.vocab
+                lg = sim.run([t])[-1]
+            decisive[r] = all(m >= MARGIN for m in margins[:cut[r]])
+        eng.decode_step(k, drafts)
+        com, n, kv, root = eng.decode_read(b, 64)
+        for r in range(b):
+            new = [int(t) for t in com[r, pos[r]:n[r]]]
+            if decisive[r]:
+                assert len(new) - 1 == cut[r], f"step {step} request {r}: accepted {len(new) - 1} != planted {cut[r]}"
+                seen.add(int(cut[r]))
+            for i, t in enumerate(new):  # teacher-forced: every committed token is greedy
+                _assert_greedy(lgs[r], t, f"step {step} request {r} token {i}")
+                lgs[r] = decs[r].run([t])[-1]
+            pos[r] = n[r]
+        assert np.array_equal(kv, np.array(PROMPTS) + n), "kv_len must advance by the committed count"
+        assert np.array_equal(root, com[np.arange(b), n - 1]), "the bonus token becomes the next root"
+    assert len(seen) >= 3, f"planted cuts should exercise several acceptance lengths: {seen}"
+    eng.close()
+
+
+@pytest.mark.parametrize("k", [0, 3])
+def test_decode_with_drafter_commits_greedy_sequence(ref, k):
+    """The on-device drafter proposes (random-init: mostly rejected); k = 0 is
+    plain autoregressive decoding. Either way every committed token is the
+    target's greedy token given the GPU's own history."""
+    s, om, _ = ref
+    b, steps = len(PROMPTS), 12
+    prompts = _prompts(s)
+    eng = _engine(s)
+    nxt = eng.prefill(prompts)
+    for _ in range(steps):
+        eng.decode_step(k)
+    com, n, kv, root = eng.decode_read(b, 128)
+    assert np.all(n >= steps)
+    decisive = sum(_teacher_forced(om, prompts[r], nxt[r], com[r, :n[r]], f"request {r}") for r in range(b))
+    assert decisive >= b * steps // 2, f"too few decisive positions ({decisive})"
+    t = eng.last_times()
+    if k > 0:
+        assert t["draft"] > 0.0
+    eng.close()
+
+
+def test_decode_errors(ref):
+    s, _, _ = ref
+    eng = _engine(s)
+    with pytest.raises(ValueError, match="prefill or smo_engine_decode_begin"):
+        eng.decode_step(1)
+    eng.decode_begin(np.zeros(3, np.int32), np.array([10, 10, 10], np.int32))
+    with pytest.raises(ValueError, match="max_verify"):
+        eng.decode_step(6)
+    eng.close()
+    from paper_2508_21706_b200.engine import VerifyEngine
+    e2 = VerifyEngine(dataclasses.replace(s, draft_layers=0, draft_inter=0), max_batch=2, max_verify=4, max_seq=64)
+    e2.decode_begin(np.zeros(2, np.int32), np.array([3, 4], np.int32))
+    with pytest.raises(ValueError, match="drafter"):
+        e2.decode_step(2)
+    e2.decode_step(2, np.ones((2, 2), np.int32))  # planted drafts need no drafter
+    e2.close()
