@@ -682,7 +682,14 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
           if (stid == 0) p.ws_cnt[cur.pair] = 0;  // ready for the next launch
         }
       }
-      // all stage reads done -> hand the stage back to the producer
+      // all stage reads done -> restore the V tile to zeros and hand the
+      // stage back to the producer. The epilogue scratch above left fp32 bit
+      // patterns in it; a later partial last chunk only loads V rows up to its
+      // end and keeps the rest, whose P is zero — but 0 * (a bf16 NaN/Inf
+      // pattern) is not zero in the PV MMA.
+      asm volatile("bar.sync 5, 256;" ::: "memory");
+      for (int i = stid; i < L::kKvBytes / 16; i += 32 * kSoftWarps)
+        reinterpret_cast<uint4*>(stage + L::kKvBytes)[i] = make_uint4(0, 0, 0, 0);
       fence_proxy_async();
       asm volatile("bar.sync 5, 256;" ::: "memory");
       if (stid == 0) mbar_arrive(&kv_empty[s_last]);

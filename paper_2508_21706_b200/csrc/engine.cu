@@ -17,6 +17,8 @@
 // E blocks each plus the hot-expert cache (MemoryPolicy.expert_cache_bytes,
 // config.hpp:103-108), filled once at creation.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -940,7 +942,7 @@ struct Engine {
   void ffn_dense(const Scratch& sc, uint16_t* hb, int rows, const uint16_t* w1, const uint16_t* w3,
                  const uint16_t* w2, int inter, cudaStream_t st) {
     rmsnorm(sc.x, ones, rows, h, cfg.rms_eps, sc.xn, st);
-    dense_gemm(sc.xn, rows, h, inter, w1, w3, SMO_EPI_SWIGLU, hb, 1, st);
+    dense_gemm(sc.xn, rows, h, inter, w1, w3, SMO_EPI_SWIGLU, hb, 0, st);
     dense_gemm(hb, rows, inter, h, w2, nullptr, SMO_EPI_F32_ADD, sc.x, sc.split, st);
   }
 
@@ -1058,6 +1060,32 @@ struct Engine {
     if (root) SMO_CUDA_CHECK(cudaMemcpy(root, d_root, size_t(b) * 4, cudaMemcpyDeviceToHost));
   }
 
+  // SMO_PREFILL_CHECK=1: host scan for non-finite values after each prefill
+  // stage (diagnostics only; synchronises)
+  static bool prefill_check_on() {
+    const char* e = std::getenv("SMO_PREFILL_CHECK");
+    return e && e[0] == '1';
+  }
+  void check_finite(const char* what, int layer, const void* p, size_t count, bool bf16, cudaStream_t st) {
+    SMO_CUDA_CHECK(cudaStreamSynchronize(st));
+    std::vector<uint16_t> hb;
+    std::vector<float> hf;
+    size_t bad = 0, first = 0;
+    if (bf16) {
+      hb.resize(count);
+      SMO_CUDA_CHECK(cudaMemcpy(hb.data(), p, count * 2, cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < count; ++i)
+        if (!std::isfinite(bf2f(hb[i])) && !bad++) first = i;
+    } else {
+      hf.resize(count);
+      SMO_CUDA_CHECK(cudaMemcpy(hf.data(), p, count * 4, cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < count; ++i)
+        if (!std::isfinite(hf[i]) && !bad++) first = i;
+    }
+    std::fprintf(stderr, "[prefill-check] L%d %-8s %zu non-finite of %zu (first at %zu)\n", layer, what, bad, count,
+                 first);
+  }
+
   // ------------------------------------------------------------------ prefill
   // Layer-major prefill: every layer's experts are streamed once for the
   // whole prompt batch; attention runs the prompt as causal chunks of C rows.
@@ -1107,7 +1135,7 @@ struct Engine {
     sc.qkv = static_cast<uint16_t*>(talloc(size_t(Tp) * qkv_w * 2));
     sc.q = static_cast<uint16_t*>(talloc(size_t(Tp) * nq * d * 2));
     sc.attn = static_cast<uint16_t*>(talloc(size_t(Tp) * nq * d * 2));
-    sc.split = 1;
+    sc.split = 1;  // prompt-sized row counts fill the SMs without split-K
     {
       smo_attn_args wa{};
       wa.b = b;
@@ -1146,10 +1174,19 @@ struct Engine {
     embed(p_tok, embed_w, Tp, h, sc.x, st);
     for (int l = 0; l < L; ++l) {
       Layer& ly = layers[l];
+      const bool chk = prefill_check_on();
+      if (chk) check_finite("x_in", l, sc.x, size_t(Tp) * h, false, st);
       attn_sublayer(sc, ly.wqkv, ly.wo, ly.kc, ly.vc, b, C, nch, p_pre, maxpre, p_mask, st);
+      if (chk) {
+        check_finite("qkv", l, sc.qkv, size_t(Tp) * qkv_w, true, st);
+        check_finite("q", l, sc.q, size_t(Tp) * nq * d, true, st);
+        check_finite("attn", l, sc.attn, size_t(Tp) * nq * d, true, st);
+        check_finite("x_mid", l, sc.x, size_t(Tp) * h, false, st);
+      }
       rmsnorm(sc.x, ones, Tp, h, cfg.rms_eps, sc.xn, st);
       router_topk(sc.xn, ly.router, Tp, h, E, K, nullptr, p_ids, p_rw, st);
       permute(p_ids, Tp, K, E, sc.xn, h, p_off, p_perm, p_pos, p_xp, st);
+      if (chk) check_finite("xp", l, p_xp, size_t(PT) * h, true, st);
       if (cfg.shared_inter > 0) {
         dense_gemm(sc.xn, Tp, h, cfg.shared_inter, ly.ws1, ly.ws3, SMO_EPI_SWIGLU, p_hs, 1, st);
         dense_gemm(p_hs, Tp, cfg.shared_inter, h, ly.ws2, nullptr, SMO_EPI_F32_ADD, sc.x, 1, st);
@@ -1189,6 +1226,10 @@ struct Engine {
       g2.ldo = h;
       gemm_launch(g2, st);
       SMO_CUDA_CHECK(cudaEventRecord(slot_free[l % slots], st));
+      if (chk) {
+        check_finite("h_swiglu", l, p_hb, size_t(PT) * hi, true, st);
+        check_finite("y_down", l, p_y, size_t(PT) * h, false, st);
+      }
       unpermute_combine(p_y, p_pos, p_rw, Tp, K, h, sc.x, st);
       if (l + slots < L) h2d_bytes += enqueue_h2d(l + slots, nullptr, nullptr);
     }

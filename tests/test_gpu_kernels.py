@@ -20,7 +20,7 @@ def _u16(t):
 
 # ---------------------------------------------------------------- K4 GEMM
 @pytest.mark.parametrize("T,K,N", [(1, 512, 128), (20, 512, 768), (160, 4096, 1024), (288, 4096, 768),
-                                   (300, 1024, 256), (520, 512, 384), (37, 14336, 256)])
+                                   (300, 1024, 256), (520, 512, 384), (37, 14336, 256), (4100, 512, 384)])
 def test_gemm_dense_f32_vs_torch(cuda, T, K, N):
     import torch
     from paper_2508_21706_b200 import ops, _lib as L
@@ -179,6 +179,12 @@ def _attn_case(torch, cuda, b, n, nq, nkv, d, prefix, s_max, tree, seed):
     (1, 24, 32, 8, 128, [3000], True),                 # 96 rows: no row replication
     (2, 9, 16, 16, 128, [255, 2049], False),           # MHA (g=1), 9 rows: 4 replicas
     (2, 7, 24, 8, 64, [640, 77], True),                # g=3, d=64, 21 rows
+    (2, 32, 32, 8, 128, [0, 32], False),               # prefill chunk: 128 rows, empty prefix
+    (4, 32, 8, 2, 64, [0, 32, 64, 96], False),         # prefill chunks, d=64
+    # full batches: several (request, head) pairs per persistent CTA
+    (32, 9, 32, 8, 128, [1024] * 32, False),           # BASELINE config 2 verify shape
+    (32, 32, 32, 8, 128, [256] * 32, False),           # Mixtral prefill chunk 8, b=32
+    (64, 1, 32, 8, 128, [4096] * 64, False),           # plain decode, long prefix
 ])
 def test_verify_attention_vs_oracle(cuda, oracle, b, n, nq, nkv, d, prefix, tree):
     import torch

@@ -61,7 +61,7 @@ def gemm(T, K, N, epi=L.EPI_BF16, name="dense"):
             "frac": byts / t / 1e9 / PEAK, "TFLOPs": 2 * T * K * N / t / 1e12}
 
 
-def moe(T=288, h=4096, hi=14336, E=8, k=2):
+def moe(T=288, h=4096, hi=14336, E=8, k=2, split=0):
     g = torch.Generator(device=dev).manual_seed(3)
     x = (torch.rand((T, h), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
     blk = 3 * h * hi
@@ -73,15 +73,15 @@ def moe(T=288, h=4096, hi=14336, E=8, k=2):
 
     def up():
         ops.gemm(xp, pool, epilogue=L.EPI_SWIGLU, out=hbuf, w_up=pool[hi * h:], row_offsets=off, groups=E,
-                 w_block_stride=blk * 2, w_pool_blocks=E, N=hi, max_rows_per_group=T)
+                 w_block_stride=blk * 2, w_pool_blocks=E, N=hi, max_rows_per_group=T, split_k=split)
 
     def down():
         ops.gemm(hbuf, pool[2 * hi * h:], epilogue=L.EPI_F32, out=y, row_offsets=off, groups=E,
-                 w_block_stride=blk * 2, w_pool_blocks=E, N=h, max_rows_per_group=T)
+                 w_block_stride=blk * 2, w_pool_blocks=E, N=h, max_rows_per_group=T, split_k=split)
     r = []
     for nm, fn, wb in (("swiglu gate/up", up, 2 * E * hi * h * 2), ("down", down, E * h * hi * 2)):
         t = timeit(fn)
-        r.append({"kernel": f"K4 grouped {nm}", "T": T, "E": E, "us": t * 1e6, "GBs": wb / t / 1e9,
+        r.append({"kernel": f"K4 grouped {nm}" + (f" split {split}" if split else ""), "T": T, "E": E, "us": t * 1e6, "GBs": wb / t / 1e9,
                   "frac": wb / t / 1e9 / PEAK, "TFLOPs": (2 if "gate" in nm else 1) * 2 * T * k * h * hi / t / 1e12})
     return r
 
@@ -104,6 +104,9 @@ def main():
         res.append(gemm(288, 4096, 4096, L.EPI_F32_ADD, name="o-proj (+residual)"))
         res.append(gemm(288, 4096, 32000, L.EPI_ARGMAX, name="lm-head argmax"))
         res += moe()
+        if "--splits" in sys.argv:
+            for sp in (1, 2, 4, 8):
+                res += moe(split=sp)
     for r in res:
         print(json.dumps({k: (round(v, 3) if isinstance(v, float) else v) for k, v in r.items()}))
 
