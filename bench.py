@@ -489,7 +489,8 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong" if ep_size > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (procedural random-init)",
-        "config": {"workload": f"{args.model} offloaded verify step (BASELINE config 2)", "batch": b * ep_size,
+        "config": {"workload": f"{args.model} offloaded verify step (BASELINE config "
+                   f"{ {'mixtral-8x7b': 2, 'dsv2-lite': 4, 'qwen2-57b': 4, 'mixtral-8x22b': 5}.get(args.model, 1)})", "batch": b * ep_size,
                    "draft_len": args.k, "verify_rows": b * n, "prefix": prefix, "experts_in": "pinned host DRAM",
                    "expert_cache_gb": args.cache_gb, "hbm_slots": args.slots, "host_alias_layers": alias,
                    "l2": "inputs larger than L2 (90.2 GB of experts + 4.6 GB KV streamed per step)",

@@ -42,6 +42,7 @@ struct EngineOptions {
   float lm_scale = 1.0f;
   float router_scale = 1.0f;
   bool drafter = true;                 // build the drafter from ModelSpec.draft (f1) when it has FFN ops
+  int kv_pages = 0;                    // K/V layout (f2): 0 contiguous, > 0 paged pool size, -1 paged auto
 };
 
 struct VerifyBatch {
@@ -112,6 +113,7 @@ class VerifyEngine {
     o.flags = opt.debug ? SMO_ENGINE_DEBUG : 0;
     o.ep_rank = 0;
     o.ep_size = 1;
+    o.kv_pages = opt.kv_pages;
     detail::smo_check(smo_engine_create(&c, &o, &h_));
     layers_ = model.n_layers;
     max_verify_ = o.max_verify;

@@ -71,6 +71,12 @@ typedef struct {
   void* workspace;    /* >= smo_verify_attention_workspace() bytes, zero-filled
                          before its first use (the kernel leaves it so) */
   size_t workspace_bytes;
+  /* Paged K/V: when block_table is non-NULL the caches are
+   * page pools [num_pages, n_kv, 128, d] and position pos of request r lives
+   * in page block_table[r * max_pages + pos / 128] (one page = one 128-key
+   * chunk); s_max is then ignored and max_prefix + n <= 128 * max_pages.  */
+  const int32_t* block_table;
+  int32_t max_pages, num_pages;
 } smo_attn_args;
 size_t smo_verify_attention_workspace(const smo_attn_args* a);
 smo_status smo_verify_attention(const smo_attn_args* a, smo_stream stream);
@@ -230,6 +236,10 @@ typedef struct {
   int32_t flags;
   int32_t ep_rank, ep_size;   /* expert parallelism: this rank owns experts e % ep_size == ep_rank */
   void* nccl_comm;            /* smo_ep_group* (NCCL or loopback) when ep_size > 1 */
+  int32_t kv_pages;           /* K/V layout: 0 = contiguous [b][n_kv][max_seq][d];
+                                 > 0 = paged pool of that many 128-token pages per layer, one block
+                                 table shared by all layers, pages assigned as requests grow;
+                                 -1 = paged, pool = max_batch * ceil(max_seq / 128) */
 } smo_engine_options;
 
 /* ---- expert parallelism ----------------------------------

@@ -36,7 +36,8 @@ class CapacityError(SmoError):
 class AttnArgs(C.Structure):
     _fields_ = [("q", _vp), ("k_cache", _vp), ("v_cache", _vp), ("mask", _vp), ("prefix_len", _vp),
                 ("out", _vp), ("b", _i32), ("n", _i32), ("n_q", _i32), ("n_kv", _i32), ("d", _i32),
-                ("s_max", _i32), ("max_prefix", _i32), ("workspace", _vp), ("workspace_bytes", _sz)]
+                ("s_max", _i32), ("max_prefix", _i32), ("workspace", _vp), ("workspace_bytes", _sz),
+                ("block_table", _vp), ("max_pages", _i32), ("num_pages", _i32)]
 
 
 class GemmArgs(C.Structure):
@@ -57,7 +58,7 @@ class ModelConfig(C.Structure):
 class EngineOptions(C.Structure):
     _fields_ = [("max_batch", _i32), ("max_verify", _i32), ("max_seq", _i32), ("hbm_slots", _i32),
                 ("expert_cache_bytes", _i64), ("host_alias_layers", _i32), ("device", _i32), ("flags", _i32),
-                ("ep_rank", _i32), ("ep_size", _i32), ("nccl_comm", _vp)]
+                ("ep_rank", _i32), ("ep_size", _i32), ("nccl_comm", _vp), ("kv_pages", _i32)]
 
 
 class VerifyBatch(C.Structure):

@@ -35,6 +35,7 @@ namespace {
 constexpr int kSoftWarps = 8;                 // two per TMEM lane quadrant
 constexpr int kThreads = 64 + 32 * kSoftWarps;  // + TMA producer + MMA issuer
 constexpr int kChunk = 128;
+static_assert(kChunk == kKvPage, "a K/V page is one K1 key chunk");
 
 struct AttnParams {
   const uint64_t* mask;
@@ -44,6 +45,8 @@ struct AttnParams {
   float2* ws_ml;  // their (reference max, row sum) [grid][2][rows]
   int* ws_cnt;    // per (request, KV head) pieces-finished counter, zero between launches
   int b, n, n_q, n_kv, g, rows, s_max;
+  const int32_t* bt;  // paged K/V block table [b][max_pages] (null: contiguous)
+  int max_pages;
   int C;          // chunk slots per (request, KV head) = ceil((max_prefix + n) / 128)
   int Q;          // chunks per CTA of the flat schedule
   int total;      // pairs * C
@@ -254,6 +257,8 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
                         kb * 64, pc.h * p.g, pc.r * p.n);
         const int row_base = (pc.r * p.n_kv + pc.h) * p.s_max;
         for (int c = pc.c0; c < pc.c1; ++c, ++gc) {
+          // first cache row of chunk c: contiguous, or its page (one page = one chunk)
+          const int crow = p.bt ? (p.bt[pc.r * p.max_pages + c] * p.n_kv + pc.h) * kChunk : row_base + c * kChunk;
           const int s = gc % kStages;
           TR(0, 1);
           mbar_wait(&kv_empty[s], ((gc / kStages) & 1) ^ 1);
@@ -265,12 +270,12 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
           const int vrows = min(kChunk, (pc.keys - c * kChunk + 7) & ~7);
           mbar_arrive_expect_tx(&kv_full[s], uint32_t(L::kKvBytes + vrows * L::kKBlocks * 128));
           for (int kb = 0; kb < L::kKBlocks; ++kb) {
-            tma_load_2d(kdst + kb * 16384, &tm_kv_k, &kv_full[s], kb * 64, row_base + c * kChunk);
+            tma_load_2d(kdst + kb * 16384, &tm_kv_k, &kv_full[s], kb * 64, crow);
             if (vrows == kChunk) {
-              tma_load_2d(vdst + kb * 16384, &tm_kv_v, &kv_full[s], kb * 64, row_base + c * kChunk);
+              tma_load_2d(vdst + kb * 16384, &tm_kv_v, &kv_full[s], kb * 64, crow);
             } else {
               for (int r8 = 0; r8 < vrows; r8 += 8)
-                tma_load_2d(vdst + kb * 16384 + r8 * 128, &tm_v8, &kv_full[s], kb * 64, row_base + c * kChunk + r8);
+                tma_load_2d(vdst + kb * 16384 + r8 * 128, &tm_v8, &kv_full[s], kb * 64, crow + r8);
             }
           }
         }
@@ -783,7 +788,12 @@ void check_attn_args(const smo_attn_args& a) {
   SMO_REQUIRE(a.d == 64 || a.d == 128, "attention: head_dim must be 64 or 128");
   SMO_REQUIRE(a.n <= 64, "attention: mask size mismatch");
   SMO_REQUIRE((a.n_q / a.n_kv) * a.n <= 128, "attention: n * (n_q/n_kv) must be <= 128");
-  SMO_REQUIRE(a.max_prefix >= 0 && a.max_prefix + a.n <= a.s_max, "attention: shape mismatch");
+  if (a.block_table) {
+    SMO_REQUIRE(a.max_pages > 0 && a.num_pages > 0, "attention: paged K/V needs max_pages and num_pages");
+    SMO_REQUIRE(a.max_prefix >= 0 && a.max_prefix + a.n <= a.max_pages * kChunk, "attention: shape mismatch");
+  } else {
+    SMO_REQUIRE(a.max_prefix >= 0 && a.max_prefix + a.n <= a.s_max, "attention: shape mismatch");
+  }
 }
 
 }  // namespace
@@ -813,6 +823,8 @@ void attention_launch(const smo_attn_args& a, cudaStream_t stream) {
   p.g = g;
   p.rows = g * a.n;
   p.s_max = a.s_max;
+  p.bt = a.block_table;
+  p.max_pages = a.max_pages;
   p.C = pl.C;
   p.Q = pl.Q;
   p.total = pl.total;
@@ -826,7 +838,9 @@ void attention_launch(const smo_attn_args& a, cudaStream_t stream) {
     make_tmap_bf16(&tq, a.q, 3, dims, strides, box, true);
   }
   {
-    uint64_t dims[2] = {uint64_t(a.d), uint64_t(a.b) * a.n_kv * a.s_max};
+    const uint64_t cache_rows =
+        a.block_table ? uint64_t(a.num_pages) * a.n_kv * kChunk : uint64_t(a.b) * a.n_kv * a.s_max;
+    uint64_t dims[2] = {uint64_t(a.d), cache_rows};
     uint64_t strides[1] = {uint64_t(a.d) * 2};
     uint32_t box[2] = {64, uint32_t(kChunk)};
     make_tmap_bf16(&tk, a.k_cache, 2, dims, strides, box, true);

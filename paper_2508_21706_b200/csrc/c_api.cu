@@ -21,7 +21,7 @@ size_t gemm_workspace(const smo_gemm_args& a);
 void fill_uniform(void* dst, uint64_t count, uint64_t seed, uint64_t tensor_id, uint64_t base, float scale,
                   cudaStream_t st);
 void fill_kv_prefix(void* cache, const int32_t* prefix, int b, int n_kv, int d, int s_max, uint64_t seed,
-                    uint64_t tensor_id, cudaStream_t st);
+                    uint64_t tensor_id, cudaStream_t st, const int32_t* bt = nullptr, int max_pages = 0);
 void router_topk(const void* x, const void* w, int T, int h, int E, int k, float* logits, int32_t* ids,
                  float* weights, cudaStream_t st);
 void permute(const int32_t* ids, int T, int k, int E, const void* x, int h, int32_t* offsets, int32_t* perm,
@@ -31,13 +31,15 @@ void unpermute_combine(const float* y, const int32_t* pos, const float* w, int T
 void rmsnorm(const float* x, const void* gain, int T, int h, float eps, void* y, cudaStream_t st);
 void embed(const int32_t* tok, const void* emb, int T, int h, float* x, cudaStream_t st);
 void rope_append(const void* qkv, const int32_t* prefix, const int32_t* parent, int b, int n, int n_q, int n_kv,
-                 int d, int s_max, float theta, void* q_out, void* kc, void* vc, cudaStream_t st);
+                 int d, int s_max, float theta, void* q_out, void* kc, void* vc, cudaStream_t st,
+                 const int32_t* bt = nullptr, int max_pages = 0);
 void argmax_reduce(const float* val, const int32_t* idx, int rows, int parts, int32_t* target, cudaStream_t st);
 void argmax_rows(const float* logits, int rows, int V, int32_t* target, cudaStream_t st);
 void greedy_accept(const int32_t* tokens, const int32_t* target, const int32_t* parent, int b, int n,
                    int32_t* acc_len, int32_t* bonus, int32_t* keep, cudaStream_t st);
 void kv_rollback(void* const* kcs, void* const* vcs, int n_layers, const int32_t* prefix, const int32_t* acc,
-                 const int32_t* keep, int b, int n, int n_kv, int d, int s_max, int32_t* kv_len, cudaStream_t st);
+                 const int32_t* keep, int b, int n, int n_kv, int d, int s_max, int32_t* kv_len, cudaStream_t st,
+                 const int32_t* bt = nullptr, int max_pages = 0);
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(uint64_t(n), std::memory_order_relaxed); }

@@ -29,6 +29,21 @@ inline void cuda_check(cudaError_t e, const char* what) {
 #define SMO_REQUIRE(cond, msg) \
   do { if (!(cond)) throw ::smo::Error(SMO_INVALID_ARG, (msg)); } while (0)
 
+// K/V cache addressing. Contiguous: [b][n_kv][s_max][d].
+// Paged: a pool [pages][n_kv][kKvPage][d] per layer and a block table
+// bt[r * max_pages + pos / kKvPage] shared by every layer; a page is one K1
+// key chunk, so a chunk load is one page. Returns the row (of d elements)
+// holding (request r, KV head h, position pos), or -1 for an unmapped page.
+constexpr int kKvPage = 128;
+__host__ __device__ inline long long kv_row(const int32_t* bt, int max_pages, int r, int h, int pos, int n_kv,
+                                            int s_max) {
+  if (bt) {
+    const int pg = bt[(long long)r * max_pages + pos / kKvPage];
+    return pg < 0 ? -1 : ((long long)pg * n_kv + h) * kKvPage + pos % kKvPage;
+  }
+  return ((long long)r * n_kv + h) * s_max + pos;
+}
+
 // Counts kernel launches issued by this library (bench gpu_launches claim).
 void count_launch(int n = 1);
 

@@ -38,7 +38,7 @@ size_t gemm_workspace(const smo_gemm_args& a);
 void fill_uniform(void* dst, uint64_t count, uint64_t seed, uint64_t tensor_id, uint64_t base, float scale,
                   cudaStream_t st);
 void fill_kv_prefix(void* cache, const int32_t* prefix, int b, int n_kv, int d, int s_max, uint64_t seed,
-                    uint64_t tensor_id, cudaStream_t st);
+                    uint64_t tensor_id, cudaStream_t st, const int32_t* bt = nullptr, int max_pages = 0);
 void router_topk(const void* x, const void* w, int T, int h, int E, int k, float* logits, int32_t* ids,
                  float* weights, cudaStream_t st);
 void permute(const int32_t* ids, int T, int k, int E, const void* x, int h, int32_t* offsets, int32_t* perm,
@@ -48,7 +48,8 @@ void unpermute_combine(const float* y, const int32_t* pos, const float* w, int T
 void rmsnorm(const float* x, const void* gain, int T, int h, float eps, void* y, cudaStream_t st);
 void embed(const int32_t* tok, const void* emb, int T, int h, float* x, cudaStream_t st);
 void rope_append(const void* qkv, const int32_t* prefix, const int32_t* parent, int b, int n, int n_q, int n_kv,
-                 int d, int s_max, float theta, void* q_out, void* kc, void* vc, cudaStream_t st);
+                 int d, int s_max, float theta, void* q_out, void* kc, void* vc, cudaStream_t st,
+                 const int32_t* bt = nullptr, int max_pages = 0);
 void argmax_reduce(const float* val, const int32_t* idx, int rows, int parts, int32_t* target, cudaStream_t st);
 void greedy_accept(const int32_t* tokens, const int32_t* target, const int32_t* parent, int b, int n,
                    int32_t* acc_len, int32_t* bonus, int32_t* keep, cudaStream_t st);
@@ -120,6 +121,15 @@ struct Engine {
   int32_t *d_kvlen = nullptr, *d_root = nullptr, *d_hist = nullptr, *d_hist_n = nullptr, *d_dec_tok = nullptr,
           *d_drafts = nullptr;
   bool last_was_decode = false;
+  // paged K/V: pool of num_pages 128-token pages per layer,
+  // host-managed block table (pinned mirror + device copy), free list
+  bool paged = false;
+  int max_pages = 0, num_pages = 0;
+  int32_t* h_bt = nullptr;  // pinned [maxB * max_pages], -1 = unmapped
+  int32_t* d_bt = nullptr;
+  std::vector<int> free_pages, req_pages;
+  std::vector<int64_t> kv_known;  // host bound of each request's K/V length
+  bool bt_dirty = false;
   std::vector<cudaEvent_t> draft_ev;  // [maxN + 1]: boundaries of the drafter steps
   int last_draft_steps = 0;
   std::vector<uint16_t*> host_bufs;  // pinned, E blocks each
@@ -174,6 +184,7 @@ struct Engine {
     for (auto e : draft_ev) cudaEventDestroy(e);
     for (auto hb : host_bufs) cudaFreeHost(hb);
     if (h_stage) cudaFreeHost(h_stage);
+    if (h_bt) cudaFreeHost(h_bt);
     for (auto& a : allocs) cudaFree(a.p);
     for (auto& kv : dbg)
       for (auto& b : kv.second) cudaFree(b.p);
@@ -190,6 +201,38 @@ struct Engine {
                                     cudaGetErrorString(e));
     allocs.push_back({p, bytes});
     return reinterpret_cast<T*>(p);
+  }
+
+  size_t kv_elems() const {
+    return paged ? size_t(num_pages) * nkv * kKvPage * d : size_t(maxB) * nkv * s_max * d;
+  }
+  const int32_t* bt() const { return paged ? d_bt : nullptr; }
+  // every page back to the free list (lowest ids handed out first)
+  void bt_reset() {
+    if (!paged) return;
+    for (size_t i = 0; i < size_t(maxB) * max_pages; ++i) h_bt[i] = -1;
+    free_pages.clear();
+    for (int pg = num_pages - 1; pg >= 0; --pg) free_pages.push_back(pg);
+    req_pages.assign(size_t(maxB), 0);
+    bt_dirty = true;
+  }
+  // map pages for positions [0, len) of request r
+  void bt_ensure(int r, int64_t len) {
+    if (!paged) return;
+    const int need = int(std::min<int64_t>(max_pages, (len + kKvPage - 1) / kKvPage));
+    while (req_pages[size_t(r)] < need) {
+      if (free_pages.empty())
+        throw Error(SMO_CAPACITY, "engine: K/V page pool exhausted (" + std::to_string(num_pages) + " pages)");
+      h_bt[size_t(r) * max_pages + req_pages[size_t(r)]] = free_pages.back();
+      free_pages.pop_back();
+      ++req_pages[size_t(r)];
+      bt_dirty = true;
+    }
+  }
+  void bt_sync(cudaStream_t st) {
+    if (!paged || !bt_dirty) return;
+    SMO_CUDA_CHECK(cudaMemcpyAsync(d_bt, h_bt, size_t(maxB) * max_pages * 4, cudaMemcpyHostToDevice, st));
+    bt_dirty = false;
   }
 
   int host_layer(int l) const { return host_alias > 0 ? l % host_alias : l; }
@@ -236,6 +279,17 @@ struct Engine {
     debug = (opt.flags & SMO_ENGINE_DEBUG) != 0;
     SMO_CUDA_CHECK(cudaSetDevice(opt.device));
     SMO_CUDA_CHECK(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+    if (opt.kv_pages != 0) {
+      paged = true;
+      max_pages = (s_max + kKvPage - 1) / kKvPage;
+      num_pages = opt.kv_pages > 0 ? opt.kv_pages : maxB * max_pages;
+      SMO_REQUIRE(num_pages > 0, "engine: bad kv_pages");
+      SMO_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_bt), size_t(maxB) * max_pages * 4,
+                                   cudaHostAllocPortable));
+      d_bt = dalloc<int32_t>(size_t(maxB) * max_pages);
+      bt_reset();
+    }
+    kv_known.assign(size_t(maxB), 0);
     cudaStream_t st = nullptr;
 
     // dense weights
@@ -255,10 +309,10 @@ struct Engine {
       ly.wqkv = dalloc<uint16_t>(size_t(qkv_w) * h);
       ly.wo = dalloc<uint16_t>(size_t(h) * nq * d);
       ly.router = dalloc<uint16_t>(size_t(E) * h);
-      ly.kc = dalloc<uint16_t>(size_t(maxB) * nkv * s_max * d);
-      ly.vc = dalloc<uint16_t>(size_t(maxB) * nkv * s_max * d);
-      SMO_CUDA_CHECK(cudaMemset(ly.kc, 0, size_t(maxB) * nkv * s_max * d * 2));
-      SMO_CUDA_CHECK(cudaMemset(ly.vc, 0, size_t(maxB) * nkv * s_max * d * 2));
+      ly.kc = dalloc<uint16_t>(kv_elems());
+      ly.vc = dalloc<uint16_t>(kv_elems());
+      SMO_CUDA_CHECK(cudaMemset(ly.kc, 0, kv_elems() * 2));
+      SMO_CUDA_CHECK(cudaMemset(ly.vc, 0, kv_elems() * 2));
       fill_uniform(ly.wqkv, size_t(qkv_w) * h, cfg.seed, tid::layer(l) + tid::kWqkv, 0, std::sqrt(3.0f / h), st);
       fill_uniform(ly.wo, size_t(h) * nq * d, cfg.seed, tid::layer(l) + tid::kWo, 0, std::sqrt(3.0f / (nq * d)),
                    st);
@@ -290,10 +344,10 @@ struct Engine {
       dl.w1 = dalloc<uint16_t>(size_t(dI) * h);
       dl.w3 = dalloc<uint16_t>(size_t(dI) * h);
       dl.w2 = dalloc<uint16_t>(size_t(h) * dI);
-      dl.kc = dalloc<uint16_t>(size_t(maxB) * nkv * s_max * d);
-      dl.vc = dalloc<uint16_t>(size_t(maxB) * nkv * s_max * d);
-      SMO_CUDA_CHECK(cudaMemset(dl.kc, 0, size_t(maxB) * nkv * s_max * d * 2));
-      SMO_CUDA_CHECK(cudaMemset(dl.vc, 0, size_t(maxB) * nkv * s_max * d * 2));
+      dl.kc = dalloc<uint16_t>(kv_elems());
+      dl.vc = dalloc<uint16_t>(kv_elems());
+      SMO_CUDA_CHECK(cudaMemset(dl.kc, 0, kv_elems() * 2));
+      SMO_CUDA_CHECK(cudaMemset(dl.vc, 0, kv_elems() * 2));
       fill_uniform(dl.wqkv, size_t(qkv_w) * h, cfg.seed, base + 1, 0, std::sqrt(3.0f / h), st);
       fill_uniform(dl.wo, size_t(h) * nq * d, cfg.seed, base + 2, 0, std::sqrt(3.0f / (nq * d)), st);
       fill_uniform(dl.w1, size_t(dI) * h, cfg.seed, base + 3, 0, std::sqrt(3.0f / h), st);
@@ -470,14 +524,23 @@ struct Engine {
     SMO_REQUIRE(b > 0 && b <= maxB, "fill_prefix: bad batch");
     for (int r = 0; r < b; ++r)
       SMO_REQUIRE(prefix_host[r] >= 0 && prefix_host[r] + maxN <= s_max, "fill_prefix: prefix exceeds max_seq");
+    SMO_CUDA_CHECK(cudaDeviceSynchronize());
     SMO_CUDA_CHECK(cudaMemcpy(d_prefix, prefix_host, size_t(b) * 4, cudaMemcpyHostToDevice));
+    bt_reset();
+    for (int r = 0; r < b; ++r) {
+      bt_ensure(r, int64_t(prefix_host[r]) + maxN);
+      kv_known[size_t(r)] = prefix_host[r];
+    }
+    bt_sync(nullptr);
     for (int l = 0; l < L; ++l) {
-      fill_kv_prefix(layers[l].kc, d_prefix, b, nkv, d, s_max, cfg.seed, tid::kv(l, 0), nullptr);
-      fill_kv_prefix(layers[l].vc, d_prefix, b, nkv, d, s_max, cfg.seed, tid::kv(l, 1), nullptr);
+      fill_kv_prefix(layers[l].kc, d_prefix, b, nkv, d, s_max, cfg.seed, tid::kv(l, 0), nullptr, bt(), max_pages);
+      fill_kv_prefix(layers[l].vc, d_prefix, b, nkv, d, s_max, cfg.seed, tid::kv(l, 1), nullptr, bt(), max_pages);
     }
     for (int l = 0; l < dL; ++l) {
-      fill_kv_prefix(dlayers[l].kc, d_prefix, b, nkv, d, s_max, cfg.seed, tid::draft_kv(l, 0), nullptr);
-      fill_kv_prefix(dlayers[l].vc, d_prefix, b, nkv, d, s_max, cfg.seed, tid::draft_kv(l, 1), nullptr);
+      fill_kv_prefix(dlayers[l].kc, d_prefix, b, nkv, d, s_max, cfg.seed, tid::draft_kv(l, 0), nullptr, bt(),
+                     max_pages);
+      fill_kv_prefix(dlayers[l].vc, d_prefix, b, nkv, d, s_max, cfg.seed, tid::draft_kv(l, 1), nullptr, bt(),
+                     max_pages);
     }
     SMO_CUDA_CHECK(cudaDeviceSynchronize());
   }
@@ -611,6 +674,13 @@ struct Engine {
         SMO_CUDA_CHECK(cudaMemcpyAsync(d_parent, hs + T + b, size_t(T) * 4, cudaMemcpyHostToDevice, st));
     }
     const int32_t* parent = in.parent ? d_parent : nullptr;
+    // pages for the appended rows (device inputs: up to the known lengths)
+    for (int r = 0; r < b; ++r) {
+      const int64_t pre = in.on_device ? kv_known[size_t(r)] : int64_t(in.prefix_len[r]);
+      if (!in.on_device) kv_known[size_t(r)] = pre;
+      bt_ensure(r, pre + n);
+    }
+    bt_sync(st);
     last_was_decode = false;
     begin_step(st);
     verify_core(b, n, d_tokens, parent, d_prefix, max_prefix, st);
@@ -685,12 +755,16 @@ struct Engine {
       g.workspace = gemm_ws;
       g.workspace_bytes = gemm_ws_bytes;
       gemm_launch(g, st);
-      rope_append(qkv, prefix, parent, b, n, nq, nkv, d, s_max, cfg.rope_theta, q, ly.kc, ly.vc, st);
+      rope_append(qkv, prefix, parent, b, n, nq, nkv, d, s_max, cfg.rope_theta, q, ly.kc, ly.vc, st, bt(),
+                  max_pages);
       snap("q", l, q, size_t(T) * nq * d * 2, st);
       smo_attn_args a{};
       a.q = q;
       a.k_cache = ly.kc;
       a.v_cache = ly.vc;
+      a.block_table = bt();
+      a.max_pages = max_pages;
+      a.num_pages = num_pages;
       a.mask = d_mask;
       a.prefix_len = prefix;
       a.out = attn;
@@ -916,11 +990,14 @@ struct Engine {
     for (int c = 0; c < nch; ++c) {
       const size_t r0 = size_t(c) * b * n;
       rope_append(sc.qkv + r0 * qkv_w, prefix + size_t(c) * b, nullptr, b, n, nq, nkv, d, s_max, cfg.rope_theta,
-                  sc.q + r0 * nq * d, kc, vc, st);
+                  sc.q + r0 * nq * d, kc, vc, st, bt(), max_pages);
       smo_attn_args a{};
       a.q = sc.q + r0 * nq * d;
       a.k_cache = kc;
       a.v_cache = vc;
+      a.block_table = bt();
+      a.max_pages = max_pages;
+      a.num_pages = num_pages;
       a.mask = mask;
       a.prefix_len = prefix + size_t(c) * b;
       a.out = sc.attn + r0 * nq * d;
@@ -993,6 +1070,12 @@ struct Engine {
     SMO_CUDA_CHECK(cudaMemcpy(d_kvlen, kv_h, size_t(b) * 4, cudaMemcpyHostToDevice));
     SMO_CUDA_CHECK(cudaMemset(d_hist_n, 0, size_t(maxB) * 4));
     SMO_CUDA_CHECK(cudaMemset(d_hist, 0xFF, size_t(maxB) * hist_cap * 4));
+    for (int r = 0; r < b; ++r) {
+      bt_ensure(r, int64_t(kv_h[r]) + 1);
+      kv_known[size_t(r)] = kv_h[r];
+    }
+    bt_sync(nullptr);
+    SMO_CUDA_CHECK(cudaDeviceSynchronize());
     dec_b = b;
     kv_bound = mx;
   }
@@ -1005,6 +1088,11 @@ struct Engine {
     SMO_REQUIRE(kv_bound + n <= s_max, "decode: KV capacity (max_seq) exhausted");
     SMO_REQUIRE(drafts_h || k == 0 || dL > 0, "decode: k > 0 needs a drafter (draft_layers) or planted drafts");
     const bool planted = drafts_h && k > 0;
+    for (int r = 0; r < b; ++r) {
+      bt_ensure(r, kv_bound + n);
+      kv_known[size_t(r)] = kv_bound + n;  // upper bound (the device holds the exact length)
+    }
+    bt_sync(st);
     if (planted) {
       SMO_CUDA_CHECK(cudaStreamSynchronize(st));  // staging buffer reuse
       std::memcpy(h_stage, drafts_h, size_t(b) * k * 4);
@@ -1162,6 +1250,13 @@ struct Engine {
     auto* p_y = static_cast<float*>(talloc(size_t(PT) * h * 4));
     uint16_t* p_hs = cfg.shared_inter > 0 ? static_cast<uint16_t*>(talloc(size_t(Tp) * cfg.shared_inter * 2)) : nullptr;
     uint16_t* p_dh = dL > 0 ? static_cast<uint16_t*>(talloc(size_t(Tp) * dI * 2)) : nullptr;
+    SMO_CUDA_CHECK(cudaStreamSynchronize(st));
+    bt_reset();
+    for (int r = 0; r < b; ++r) {
+      bt_ensure(r, int64_t(nch) * C);  // the padded chunk rows are appended too
+      kv_known[size_t(r)] = len_h[r];
+    }
+    bt_sync(st);
     SMO_CUDA_CHECK(cudaMemcpyAsync(p_tok, tok.data(), tok.size() * 4, cudaMemcpyHostToDevice, st));
     SMO_CUDA_CHECK(cudaMemcpyAsync(p_pre, pre.data(), pre.size() * 4, cudaMemcpyHostToDevice, st));
     SMO_CUDA_CHECK(cudaMemcpyAsync(p_len, len_h, size_t(b) * 4, cudaMemcpyHostToDevice, st));
@@ -1412,7 +1507,7 @@ smo_status smo_engine_debug_tensor(smo_engine* e, const char* name, int32_t laye
       smo::Engine& g = e->impl;
       const bool dr = nm.rfind("draft_", 0) == 0;
       SMO_REQUIRE(layer >= 0 && layer < (dr ? g.dL : g.L), "engine: layer out of range");
-      const size_t cb = size_t(g.maxB) * g.nkv * g.s_max * g.d * 2;
+      const size_t cb = g.kv_elems() * 2;
       SMO_REQUIRE(bytes <= cb, "engine: debug tensor smaller than requested");
       SMO_CUDA_CHECK(cudaDeviceSynchronize());
       const bool kk = nm == "k_cache" || nm == "draft_k_cache";
@@ -1459,7 +1554,7 @@ smo_status smo_engine_tensor_ptr(smo_engine* e, const char* name, int32_t layer,
     } else if (n == "k_cache" || n == "v_cache") {
       need_layer();
       *ptr = n == "k_cache" ? g.layers[layer].kc : g.layers[layer].vc;
-      *bytes = size_t(g.maxB) * g.nkv * g.s_max * g.d * 2;
+      *bytes = g.kv_elems() * 2;
     } else if (n == "expert_host") {
       need_layer();
       SMO_REQUIRE(expert >= 0 && expert < g.E, "engine: expert out of range");

@@ -24,9 +24,9 @@ __global__ void fill_uniform_kernel(uint16_t* dst, uint64_t count, uint64_t key,
 }
 
 __global__ void fill_kv_prefix_kernel(uint16_t* cache, const int32_t* prefix, int n_kv, int d, int s_max,
-                                      uint64_t key, float s) {
+                                      uint64_t key, float s, const int32_t* bt, int max_pages) {
   const int rh = blockIdx.y;  // r * n_kv + h
-  const int r = rh / n_kv;
+  const int r = rh / n_kv, h = rh % n_kv;
   const int len = prefix[r];
   const uint64_t total = uint64_t(len) * d;
   for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < total;
@@ -34,7 +34,8 @@ __global__ void fill_kv_prefix_kernel(uint16_t* cache, const int32_t* prefix, in
     const uint64_t idx = (uint64_t(rh) << 32) | e;
     const uint64_t x = splitmix64(splitmix64(key ^ idx));
     const int32_t c = int32_t((x >> 40) << 1) - (1 << 24);
-    cache[uint64_t(rh) * s_max * d + e] = f2bf(__fmul_rn(float(c), s));
+    const long long row = kv_row(bt, max_pages, r, h, int(e / d), n_kv, s_max);
+    if (row >= 0) cache[uint64_t(row) * d + e % d] = f2bf(__fmul_rn(float(c), s));
   }
 }
 
@@ -213,7 +214,7 @@ __global__ void embed_kernel(const int32_t* __restrict__ tok, const uint16_t* __
 __global__ void rope_append_kernel(const uint16_t* __restrict__ qkv, const int32_t* __restrict__ prefix,
                                    const int32_t* __restrict__ parent, int n, int n_q, int n_kv, int d, int s_max,
                                    double theta, uint16_t* __restrict__ q_out, uint16_t* __restrict__ kc,
-                                   uint16_t* __restrict__ vc) {
+                                   uint16_t* __restrict__ vc, const int32_t* __restrict__ bt, int max_pages) {
   const int row = blockIdx.x;
   const int r = row / n, i = row % n;
   int depth = i;
@@ -243,15 +244,17 @@ __global__ void rope_append_kernel(const uint16_t* __restrict__ qkv, const int32
       dst[j] = o0;
       dst[j + half] = o1;
     } else {
-      const int hk = head - n_q;
-      uint16_t* dst = kc + ((size_t(r) * n_kv + hk) * s_max + slot) * d;
+      const long long kr = kv_row(bt, max_pages, r, head - n_q, slot, n_kv, s_max);
+      if (kr < 0) continue;
+      uint16_t* dst = kc + size_t(kr) * d;
       dst[j] = o0;
       dst[j + half] = o1;
     }
   }
   for (int e = threadIdx.x; e < n_kv * d; e += blockDim.x) {
     const int hk = e / d, c = e % d;
-    vc[((size_t(r) * n_kv + hk) * s_max + slot) * d + c] = src[(n_q + n_kv) * d + e];
+    const long long vr = kv_row(bt, max_pages, r, hk, slot, n_kv, s_max);
+    if (vr >= 0) vc[size_t(vr) * d + c] = src[(n_q + n_kv) * d + e];
   }
 }
 
@@ -342,17 +345,20 @@ __global__ void greedy_accept_kernel(const int32_t* __restrict__ tokens, const i
 // Tree KV compaction: row keep[r, j] -> prefix + j, j ascending (keep[j] >= j,
 // so no source is overwritten before it is read). One block per (layer, r, h).
 __global__ void kv_rollback_kernel(void* const* kcs, void* const* vcs, const int32_t* prefix, const int32_t* acc,
-                                   const int32_t* keep, int b, int n, int n_kv, int d, int s_max) {
+                                   const int32_t* keep, int b, int n, int n_kv, int d, int s_max, const int32_t* bt,
+                                   int max_pages) {
   const int layer = blockIdx.z, r = blockIdx.y, h = blockIdx.x;
   const int a = acc[r], p = prefix[r];
-  uint16_t* kc = reinterpret_cast<uint16_t*>(kcs[layer]) + (size_t(r) * n_kv + h) * s_max * d;
-  uint16_t* vc = reinterpret_cast<uint16_t*>(vcs[layer]) + (size_t(r) * n_kv + h) * s_max * d;
+  uint16_t* kc = reinterpret_cast<uint16_t*>(kcs[layer]);
+  uint16_t* vc = reinterpret_cast<uint16_t*>(vcs[layer]);
   for (int j = 1; j <= a; ++j) {
     const int src = keep[size_t(r) * n + j];
-    if (src != j)
+    const long long rd = kv_row(bt, max_pages, r, h, p + j, n_kv, s_max);
+    const long long rs = kv_row(bt, max_pages, r, h, p + src, n_kv, s_max);
+    if (src != j && rd >= 0 && rs >= 0)
       for (int c = threadIdx.x; c < d; c += blockDim.x) {
-        kc[size_t(p + j) * d + c] = kc[size_t(p + src) * d + c];
-        vc[size_t(p + j) * d + c] = vc[size_t(p + src) * d + c];
+        kc[size_t(rd) * d + c] = kc[size_t(rs) * d + c];
+        vc[size_t(rd) * d + c] = vc[size_t(rs) * d + c];
       }
     __syncthreads();
   }
@@ -463,11 +469,12 @@ void fill_uniform(void* dst, uint64_t count, uint64_t seed, uint64_t tensor_id, 
 }
 
 void fill_kv_prefix(void* cache, const int32_t* prefix, int b, int n_kv, int d, int s_max, uint64_t seed,
-                    uint64_t tensor_id, cudaStream_t st) {
+                    uint64_t tensor_id, cudaStream_t st, const int32_t* bt, int max_pages) {
   SMO_REQUIRE(cache && prefix && b > 0 && n_kv > 0 && d > 0, "fill_kv_prefix: bad arguments");
   dim3 grid(64, b * n_kv);
   fill_kv_prefix_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<uint16_t*>(cache), prefix, n_kv, d, s_max,
-                                              seed ^ (tensor_id * 0x9e3779b97f4a7c15ULL), std::ldexp(1.0f, -24));
+                                              seed ^ (tensor_id * 0x9e3779b97f4a7c15ULL), std::ldexp(1.0f, -24),
+                                              bt, max_pages);
   count_launch();
   SMO_CUDA_CHECK(cudaGetLastError());
 }
@@ -530,12 +537,14 @@ void embed(const int32_t* tok, const void* emb, int T, int h, float* x, cudaStre
 }
 
 void rope_append(const void* qkv, const int32_t* prefix, const int32_t* parent, int b, int n, int n_q, int n_kv,
-                 int d, int s_max, float theta, void* q_out, void* kc, void* vc, cudaStream_t st) {
+                 int d, int s_max, float theta, void* q_out, void* kc, void* vc, cudaStream_t st, const int32_t* bt,
+                 int max_pages) {
   SMO_REQUIRE(qkv && prefix && q_out && kc && vc, "rope_append: null pointer");
   SMO_REQUIRE(d % 2 == 0, "rope_append: odd head_dim");
   rope_append_kernel<<<b * n, 256, 0, st>>>(reinterpret_cast<const uint16_t*>(qkv), prefix, parent, n, n_q, n_kv,
                                             d, s_max, double(theta), reinterpret_cast<uint16_t*>(q_out),
-                                            reinterpret_cast<uint16_t*>(kc), reinterpret_cast<uint16_t*>(vc));
+                                            reinterpret_cast<uint16_t*>(kc), reinterpret_cast<uint16_t*>(vc), bt,
+                                            max_pages);
   count_launch();
   SMO_CUDA_CHECK(cudaGetLastError());
 }
@@ -574,11 +583,12 @@ void build_mask(const int32_t* parent, int b, int n, uint64_t* mask, cudaStream_
 }
 
 void kv_rollback(void* const* kcs, void* const* vcs, int n_layers, const int32_t* prefix, const int32_t* acc,
-                 const int32_t* keep, int b, int n, int n_kv, int d, int s_max, int32_t* kv_len, cudaStream_t st) {
+                 const int32_t* keep, int b, int n, int n_kv, int d, int s_max, int32_t* kv_len, cudaStream_t st,
+                 const int32_t* bt, int max_pages) {
   SMO_REQUIRE(prefix && acc, "kv_rollback: null pointer");
   if (keep && kcs && vcs && n_layers > 0) {
     dim3 grid(n_kv, b, n_layers);
-    kv_rollback_kernel<<<grid, 128, 0, st>>>(kcs, vcs, prefix, acc, keep, b, n, n_kv, d, s_max);
+    kv_rollback_kernel<<<grid, 128, 0, st>>>(kcs, vcs, prefix, acc, keep, b, n, n_kv, d, s_max, bt, max_pages);
     count_launch();
     SMO_CUDA_CHECK(cudaGetLastError());
   }

@@ -110,7 +110,7 @@ class VerifyResult:
 class VerifyEngine:
     def __init__(self, shape: ModelShape, *, max_batch: int, max_verify: int, max_seq: int, hbm_slots: int = 2,
                  expert_cache_bytes: int = 0, host_alias_layers: int = 0, device: int = 0, debug: bool = False,
-                 ep_rank: int = 0, ep_size: int = 1, ep_group: Optional["EpGroup"] = None):
+                 ep_rank: int = 0, ep_size: int = 1, ep_group: Optional["EpGroup"] = None, kv_pages: int = 0):
         self.shape = shape
         self.max_batch, self.max_verify, self.max_seq = max_batch, max_verify, max_seq
         if ep_size > 1 and ep_group is None:
@@ -120,7 +120,7 @@ class VerifyEngine:
         self._group = ep_group  # keep the transport alive as long as the engine
         opt = L.EngineOptions(max_batch, max_verify, max_seq, hbm_slots, int(expert_cache_bytes),
                               host_alias_layers, device, L.ENGINE_DEBUG if debug else 0, ep_rank, ep_size,
-                              None if ep_group is None else ep_group.handle)
+                              None if ep_group is None else ep_group.handle, kv_pages)
         cfg = shape.to_c()
         h = C.c_void_p()
         L.check(L.load().smo_engine_create(C.byref(cfg), C.byref(opt), C.byref(h)))

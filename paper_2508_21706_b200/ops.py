@@ -40,11 +40,22 @@ def fill_uniform_(t: torch.Tensor, seed: int, tensor_id: int, scale: float, base
     return t
 
 
-def verify_attention(q, k_cache, v_cache, mask, prefix_len, max_prefix: int, out=None):
-    """K1. q [b*n, n_q, d] bf16; caches [b, n_kv, s_max, d] bf16; mask int64 [b*n]
-    (bit j = draft j visible); prefix_len int32 [b]. Returns out [b*n, n_q, d]."""
-    b, n_kv, s_max, d = k_cache.shape
+def verify_attention(q, k_cache, v_cache, mask, prefix_len, max_prefix: int, out=None, block_table=None):
+    """K1. q [b*n, n_q, d] bf16; caches [b, n_kv, s_max, d] bf16 — or, with
+    block_table int32 [b, max_pages], page pools [num_pages, n_kv, 128, d];
+    mask int64 [b*n] (bit j = draft j visible); prefix_len int32 [b].
+    Returns out [b*n, n_q, d]."""
     T, n_q, d2 = q.shape
+    if block_table is not None:
+        _req(block_table, torch.int32, "block_table")
+        b, max_pages = block_table.shape
+        num_pages, n_kv, page, d = k_cache.shape
+        if page != 128:
+            raise ValueError("attention: pages hold 128 tokens")
+        s_max = 128 * max_pages
+    else:
+        b, n_kv, s_max, d = k_cache.shape
+        max_pages = num_pages = 0
     if d2 != d or T % b:
         raise ValueError("attention: shape mismatch")
     n = T // b
@@ -55,7 +66,9 @@ def verify_attention(q, k_cache, v_cache, mask, prefix_len, max_prefix: int, out
     out = torch.empty_like(q) if out is None else out
     a = L.AttnArgs(q=q.data_ptr(), k_cache=k_cache.data_ptr(), v_cache=v_cache.data_ptr(), mask=mask.data_ptr(),
                    prefix_len=prefix_len.data_ptr(), out=out.data_ptr(), b=b, n=n, n_q=n_q, n_kv=n_kv, d=d,
-                   s_max=s_max, max_prefix=int(max_prefix), workspace=None, workspace_bytes=0)
+                   s_max=s_max, max_prefix=int(max_prefix), workspace=None, workspace_bytes=0,
+                   block_table=None if block_table is None else block_table.data_ptr(), max_pages=max_pages,
+                   num_pages=num_pages)
     lib = L.load()
     ws_bytes = lib.smo_verify_attention_workspace(C.byref(a))
     if ws_bytes == C.c_size_t(-1).value:

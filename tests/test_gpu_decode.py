@@ -212,3 +212,40 @@ def test_decode_errors(ref):
         e2.decode_step(2)
     e2.decode_step(2, np.ones((2, 2), np.int32))  # planted drafts need no drafter
     e2.close()
+
+
+def test_paged_kv_engine_matches_contiguous(ref):
+    """Paged K/V: the engine on a page pool (block table
+    shared by all layers, pages assigned as requests grow) commits exactly
+    what the contiguous layout commits — prefill, drafter and planted-draft
+    decoding."""
+    from paper_2508_21706_b200.engine import VerifyEngine
+    s, _, _ = ref
+    b, k = len(PROMPTS), 4
+    prompts = _prompts(s)
+    rng = np.random.default_rng(9)
+    plants = [rng.integers(0, s.vocab, size=(b, k)).astype(np.int32) for _ in range(3)]
+    outs = []
+    for pages in (0, 6):  # 6 pages of 128 tokens: less than b * ceil(256 / 128)
+        eng = VerifyEngine(s, max_batch=b, max_verify=6, max_seq=256, kv_pages=pages)
+        nxt = eng.prefill(prompts)
+        for d in plants:
+            eng.decode_step(k, d)
+        for _ in range(3):
+            eng.decode_step(3)
+        outs.append((nxt, eng.decode_read(b, 64)))
+        eng.close()
+    (n0, r0), (n1, r1) = outs
+    assert np.array_equal(n0, n1)
+    for a, c in zip(r0, r1):
+        assert np.array_equal(a, c)
+
+
+def test_paged_kv_pool_exhaustion(ref):
+    from paper_2508_21706_b200 import _lib
+    from paper_2508_21706_b200.engine import VerifyEngine
+    s, _, _ = ref
+    eng = VerifyEngine(s, max_batch=3, max_verify=6, max_seq=256, kv_pages=2)
+    with pytest.raises(_lib.CapacityError, match="page pool exhausted"):
+        eng.prefill(_prompts(s))
+    eng.close()

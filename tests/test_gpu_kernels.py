@@ -332,3 +332,31 @@ def test_fill_uniform_matches_oracle(cuda, oracle):
     ops.fill_uniform_(t, 0x5EED, 4321, 0.03125, base=17)
     ref = oracle.fill_uniform_bf16(t.numel(), 0x5EED, 4321, 0.03125, base=17)
     assert np.array_equal(_u16(t), ref)
+
+
+@pytest.mark.parametrize("b,n,nq,nkv,d,prefix", [
+    (3, 5, 32, 8, 128, [1024, 131, 7]),     # verify shape, ragged
+    (4, 32, 8, 2, 64, [0, 32, 300, 96]),    # prefill chunks
+    (32, 9, 32, 8, 128, [1024] * 32),       # BASELINE config 2
+])
+def test_verify_attention_paged_bit_identical(cuda, b, n, nq, nkv, d, prefix):
+    """Paged K/V: the same caches scattered over a shuffled
+    page pool through a block table give bit-identical K1 outputs."""
+    import torch
+    from paper_2508_21706_b200 import ops
+    s_max = max(prefix) + n + 64
+    q, kc, vc, mask, pre, _ = _attn_case(torch, cuda, b, n, nq, nkv, d, prefix, s_max, False, seed=b * 7 + n)
+    ref = ops.verify_attention(q, kc, vc, mask, pre, max(prefix))
+    max_pages = (s_max + 127) // 128
+    num_pages = b * max_pages + 5
+    perm = torch.randperm(num_pages, generator=torch.Generator().manual_seed(b))[:b * max_pages]
+    bt = perm.view(b, max_pages).to(torch.int32).to(cuda)
+    pad = max_pages * 128 - s_max
+    kp = torch.full((num_pages, nkv, 128, d), float("nan"), dtype=torch.bfloat16, device=cuda)  # unused pages: NaN
+    vp = kp.clone()
+    kf = torch.nn.functional.pad(kc, (0, 0, 0, pad)).view(b, nkv, max_pages, 128, d).transpose(1, 2)
+    vf = torch.nn.functional.pad(vc, (0, 0, 0, pad)).view(b, nkv, max_pages, 128, d).transpose(1, 2)
+    kp[bt.long().view(-1)] = kf.reshape(b * max_pages, nkv, 128, d)
+    vp[bt.long().view(-1)] = vf.reshape(b * max_pages, nkv, 128, d)
+    got = ops.verify_attention(q, kp, vp, mask, pre, max(prefix), block_table=bt)
+    assert torch.equal(got, ref)
