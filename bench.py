@@ -53,6 +53,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-decode", action="store_true", help="skip the prefill + decode-loop measurement")
+    ap.add_argument("--moe-batching", default="large", choices=["large", "one"],
+                    help="LARGE_BATCH (stream whole layers ahead) or BATCH_ONE (stream router-selected experts)")
+    ap.add_argument("--attn-cpu", action="store_true",
+                    help="AttentionPlacement::CPU: target K/V in pinned host DRAM, attention on the host pool")
     return ap.parse_args()
 
 
@@ -390,7 +394,8 @@ def run_ours(args):
         try:
             eng = VerifyEngine(shape, max_batch=b, max_verify=n, max_seq=s_max, hbm_slots=args.slots,
                                expert_cache_bytes=int(args.cache_gb * 1e9), host_alias_layers=a, device=local,
-                               ep_rank=ep_rank, ep_size=ep_size, ep_group=grp)
+                               ep_rank=ep_rank, ep_size=ep_size, ep_group=grp, attn_cpu=args.attn_cpu,
+                               batch_one=args.moe_batching == "one")
             alias = a
             break
         except _lib.CapacityError as e:
@@ -476,7 +481,8 @@ def run_ours(args):
 
     roof = step_roofline(shape, b * ep_size, n, prefix, h2d_peak, pk["hbm_gbs"],
                          pk.get("bf16_tflops_sustained", 1400.0),
-                         cached_blocks=int(args.cache_gb * 1e9) // shape.expert_bytes, ep=ep_size)
+                         cached_blocks=int(args.cache_gb * 1e9) // shape.expert_bytes, ep=ep_size,
+                         h2d_bytes=stages["h2d_bytes"] if args.moe_batching == "one" else None)
     h2d_bytes = stages["h2d_bytes"]
     t_step = t_all / args.steps
     # dominant GPU kernel by device time: K4 grouped SwiGLU (+down +combine),
@@ -493,6 +499,9 @@ def run_ours(args):
                    f"{ {'mixtral-8x7b': 2, 'dsv2-lite': 4, 'qwen2-57b': 4, 'mixtral-8x22b': 5}.get(args.model, 1)})", "batch": b * ep_size,
                    "draft_len": args.k, "verify_rows": b * n, "prefix": prefix, "experts_in": "pinned host DRAM",
                    "expert_cache_gb": args.cache_gb, "hbm_slots": args.slots, "host_alias_layers": alias,
+                   "attention_placement": "CPU (host K/V, host thread pool)" if args.attn_cpu else "GPU_RESIDENT (K1)",
+                   "moe_batching": "BATCH_ONE (router-selected experts)" if args.moe_batching == "one"
+                   else "LARGE_BATCH (whole layers)",
                    "l2": "inputs larger than L2 (90.2 GB of experts + 4.6 GB KV streamed per step)",
                    "parallelism": mode},
         "committed_tokens_per_s_model": world * b * geometric_alpha(0.8, args.k) / t_step,

@@ -114,6 +114,12 @@ class VerifyEngine {
     o.ep_rank = 0;
     o.ep_size = 1;
     o.kv_pages = opt.kv_pages;
+    // AttentionPlacement::CPU (the reference's default, config.hpp:110): target
+    // K/V in pinned host DRAM, attention on the host pool (f4); GPU_TRANSFER
+    // and GPU_RESIDENT run K1 on HBM-resident K/V
+    o.attn_cpu = hyper.exec_strategy.attention_placement == AttentionPlacement::CPU ? 1 : 0;
+    // MoeBatching::BATCH_ONE (config.hpp:111): stream only router-selected experts
+    o.moe_batching = hyper.exec_strategy.moe_batching == MoeBatching::BATCH_ONE ? 1 : 0;
     detail::smo_check(smo_engine_create(&c, &o, &h_));
     layers_ = model.n_layers;
     max_verify_ = o.max_verify;

@@ -81,6 +81,12 @@ typedef struct {
 size_t smo_verify_attention_workspace(const smo_attn_args* a);
 smo_status smo_verify_attention(const smo_attn_args* a, smo_stream stream);
 
+/* Host verification attention (the CPU placement's kernel, fp32 on bf16
+ * inputs): same arguments as smo_verify_attention but every pointer is HOST
+ * memory (contiguous K/V only; workspace unused); synchronous, `threads`
+ * host threads (0 = all cores).                                           */
+smo_status smo_cpu_verify_attention(const smo_attn_args* a, int32_t threads);
+
 /* The reference's desk-scale fp64 operator, one head of one request, host
  * buffers in and out, computed by an fp64 CUDA kernel (synchronous).
  * Same contract as moeplan::chunked_attention (attention.hpp:117); the
@@ -240,6 +246,15 @@ typedef struct {
                                  > 0 = paged pool of that many 128-token pages per layer, one block
                                  table shared by all layers, pages assigned as requests grow;
                                  -1 = paged, pool = max_batch * ceil(max_seq / 128) */
+  int32_t attn_cpu;           /* AttentionPlacement::CPU (config.hpp:110): the
+                                 target K/V live in pinned host DRAM (the GPU appends rows through
+                                 mapped memory) and verification attention runs on a host thread
+                                 pool; 0 = GPU_RESIDENT (K1 on HBM). Contiguous K/V only. */
+  int32_t moe_batching;       /* ExecStrategy::moe_batching (config.hpp:110-116, optimizer.hpp:81-96):
+                                 0 = LARGE_BATCH: stream whole layers ahead (layer l+S during l);
+                                 1 = BATCH_ONE: after layer l's router, stream only the experts its
+                                 tokens selected (host waits for the routing, then issues the copies).
+                                 Prefill always streams whole layers. Not with expert parallelism. */
 } smo_engine_options;
 
 /* ---- expert parallelism ----------------------------------

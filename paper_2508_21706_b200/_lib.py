@@ -58,7 +58,8 @@ class ModelConfig(C.Structure):
 class EngineOptions(C.Structure):
     _fields_ = [("max_batch", _i32), ("max_verify", _i32), ("max_seq", _i32), ("hbm_slots", _i32),
                 ("expert_cache_bytes", _i64), ("host_alias_layers", _i32), ("device", _i32), ("flags", _i32),
-                ("ep_rank", _i32), ("ep_size", _i32), ("nccl_comm", _vp), ("kv_pages", _i32)]
+                ("ep_rank", _i32), ("ep_size", _i32), ("nccl_comm", _vp), ("kv_pages", _i32),
+                ("attn_cpu", _i32), ("moe_batching", _i32)]
 
 
 class VerifyBatch(C.Structure):
@@ -84,6 +85,7 @@ _SIGS = {
     "smo_fill_uniform_bf16": (C.c_int, [_vp, _u64, _u64, _u64, _u64, _f32, _vp]),
     "smo_verify_attention_workspace": (_sz, [C.POINTER(AttnArgs)]),
     "smo_verify_attention": (C.c_int, [C.POINTER(AttnArgs), _vp]),
+    "smo_cpu_verify_attention": (C.c_int, [C.POINTER(AttnArgs), _i32]),
     "smo_chunked_attention_f64": (C.c_int, [_sz, _sz, _sz, _vp, _vp, _vp, _sz, _vp, _vp]),
     "smo_router_topk": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "smo_permute": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp]),

@@ -11,6 +11,9 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libspecmoe.so")
 SOURCES = ["c_api.cu", "ops.cu", "gemm_tc.cu", "attention.cu", "engine.cu", "ep.cu"]
+CXX_SOURCES = ["cpu_attn.cpp"]  # host code (CPU attention placement), g++ with AVX2/FMA
+CXX = os.environ.get("CXX", "g++")
+CXX_FLAGS = ["-O3", "-mavx2", "-mfma", "-std=c++17", "-fPIC", "-pthread", "-I", CSRC]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"),
@@ -27,7 +30,8 @@ def _stale(out: str, deps: list[str]) -> bool:
 def build(verbose: bool = False, jobs: int = 8) -> str:
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    headers = [os.path.join(CSRC, "common.cuh"), os.path.join(ROOT, "include", "specmoe", "c_api.h")]
+    headers = [os.path.join(CSRC, "common.cuh"), os.path.join(CSRC, "cpu_attn.h"),
+               os.path.join(ROOT, "include", "specmoe", "c_api.h")]
     procs, objs = [], []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
@@ -40,6 +44,15 @@ def build(verbose: bool = False, jobs: int = 8) -> str:
             procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         while len([p for _, p in procs if p.poll() is None]) >= jobs:
             procs[0][1].wait()
+    for src in CXX_SOURCES:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(objdir, src.replace(".cpp", ".o"))
+        objs.append(o)
+        if _stale(o, [s] + headers):
+            cmd = [CXX, *CXX_FLAGS, "-c", s, "-o", o]
+            if verbose:
+                print(" ".join(cmd))
+            procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
     errs = []
     for src, p in procs:
         out, _ = p.communicate()
@@ -50,7 +63,8 @@ def build(verbose: bool = False, jobs: int = 8) -> str:
     if errs:
         raise RuntimeError("nvcc failed:\n" + "\n".join(errs))
     if _stale(OUT, objs):
-        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", OUT, *objs]
+        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", OUT, *objs,
+               "-Xcompiler", "-pthread"]
         subprocess.run(cmd, check=True)
     return OUT
 

@@ -7,7 +7,10 @@
 #include <mutex>
 #include <string>
 
+#include <thread>
+
 #include "common.cuh"
+#include "cpu_attn.h"
 
 namespace smo {
 
@@ -135,6 +138,23 @@ smo_status smo_verify_attention(const smo_attn_args* a, smo_stream stream) {
   return guard([&] {
     SMO_REQUIRE(a, "attention: null args");
     smo::attention_launch(*a, S(stream));
+  });
+}
+
+smo_status smo_cpu_verify_attention(const smo_attn_args* a, int32_t threads) {
+  return guard([&] {
+    SMO_REQUIRE(a && a->q && a->k_cache && a->v_cache && a->mask && a->prefix_len && a->out,
+                "attention: null pointer");
+    SMO_REQUIRE(!a->block_table, "attention: the host kernel takes contiguous K/V");
+    SMO_REQUIRE(a->b > 0 && a->n > 0 && a->n <= 64 && a->n_kv > 0 && a->n_q % a->n_kv == 0 && a->d % 8 == 0,
+                "attention: shape mismatch");
+    for (int r = 0; r < a->b; ++r)
+      SMO_REQUIRE(a->prefix_len[r] >= 0 && a->prefix_len[r] + a->n <= a->s_max, "attention: shape mismatch");
+    smo::CpuPool pool(threads > 0 ? threads : int(std::max(1u, std::thread::hardware_concurrency())));
+    smo::CpuAttnJob j{reinterpret_cast<const uint16_t*>(a->q), reinterpret_cast<const uint16_t*>(a->k_cache),
+                      reinterpret_cast<const uint16_t*>(a->v_cache), a->mask, a->prefix_len,
+                      reinterpret_cast<uint16_t*>(a->out), a->b, a->n, a->n_q, a->n_kv, a->d, a->s_max, 1};
+    smo::cpu_verify_attention(j, pool);
   });
 }
 

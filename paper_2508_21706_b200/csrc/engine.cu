@@ -23,10 +23,13 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <memory>
+#include <thread>
 #include <string>
 #include <vector>
 
 #include "common.cuh"
+#include "cpu_attn.h"
 
 namespace smo {
 
@@ -130,6 +133,23 @@ struct Engine {
   std::vector<int> free_pages, req_pages;
   std::vector<int64_t> kv_known;  // host bound of each request's K/V length
   bool bt_dirty = false;
+  // CPU attention placement: host K/V + host thread pool
+  bool attn_cpu = false;
+  std::unique_ptr<CpuPool> cpu_pool;
+  std::vector<void*> host_allocs;         // cudaFreeHost at destruction
+  uint16_t *q_host = nullptr, *attn_host = nullptr;  // pinned mapped [maxT, n_q, d]
+  int32_t* prefix_host = nullptr;         // pinned [maxB]
+  uint64_t* mask_host = nullptr;          // pinned [maxT]
+  struct HostAttn {
+    CpuPool* pool;
+    CpuAttnJob job;
+  };
+  std::vector<HostAttn> host_jobs;        // one per target layer (enqueued ahead of execution)
+  // BATCH_ONE expert streaming: stream only router-selected experts
+  bool batch_one = false;
+  int32_t* h_offsets = nullptr;           // pinned [E+1] routed offsets of the current layer
+  cudaEvent_t route_ev = nullptr;
+  std::vector<double> layer_bytes;        // bytes streamed per layer in the last step
   std::vector<cudaEvent_t> draft_ev;  // [maxN + 1]: boundaries of the drafter steps
   int last_draft_steps = 0;
   std::vector<uint16_t*> host_bufs;  // pinned, E blocks each
@@ -182,9 +202,12 @@ struct Engine {
     for (auto e : slot_free) cudaEventDestroy(e);
     for (auto e : ev) cudaEventDestroy(e);
     for (auto e : draft_ev) cudaEventDestroy(e);
+    if (route_ev) cudaEventDestroy(route_ev);
     for (auto hb : host_bufs) cudaFreeHost(hb);
     if (h_stage) cudaFreeHost(h_stage);
     if (h_bt) cudaFreeHost(h_bt);
+    cpu_pool.reset();
+    for (void* hp : host_allocs) cudaFreeHost(hp);
     for (auto& a : allocs) cudaFree(a.p);
     for (auto& kv : dbg)
       for (auto& b : kv.second) cudaFree(b.p);
@@ -201,6 +224,26 @@ struct Engine {
                                     cudaGetErrorString(e));
     allocs.push_back({p, bytes});
     return reinterpret_cast<T*>(p);
+  }
+
+  // pinned host memory the GPU reads/writes directly (UVA: same address)
+  template <class T>
+  T* halloc_mapped(size_t count) {
+    void* hp = nullptr;
+    const size_t bytes = std::max<size_t>(16, count * sizeof(T));
+    cudaError_t e = cudaHostAlloc(&hp, bytes, cudaHostAllocPortable | cudaHostAllocMapped);
+    if (e != cudaSuccess)
+      throw Error(SMO_CAPACITY, "engine: pinned host allocation of " + std::to_string(bytes) + " bytes failed");
+    host_allocs.push_back(hp);
+    void* dp = nullptr;
+    SMO_CUDA_CHECK(cudaHostGetDevicePointer(&dp, hp, 0));
+    SMO_REQUIRE(dp == hp, "engine: mapped host memory needs unified addressing");
+    std::memset(hp, 0, bytes);
+    return reinterpret_cast<T*>(hp);
+  }
+  static void CUDART_CB host_attn_cb(void* arg) {
+    auto* j = static_cast<HostAttn*>(arg);
+    cpu_verify_attention(j->job, *j->pool);
   }
 
   size_t kv_elems() const {
@@ -290,6 +333,16 @@ struct Engine {
       bt_reset();
     }
     kv_known.assign(size_t(maxB), 0);
+    if (opt.moe_batching) {
+      SMO_REQUIRE(!(opt.ep_size > 1 || opt.nccl_comm), "engine: BATCH_ONE streaming is not available with expert parallelism");
+      batch_one = true;
+      SMO_CUDA_CHECK(cudaEventCreateWithFlags(&route_ev, cudaEventDisableTiming));
+    }
+    if (opt.attn_cpu) {
+      SMO_REQUIRE(!paged, "engine: the CPU attention placement keeps contiguous host K/V (kv_pages = 0)");
+      attn_cpu = true;
+      cpu_pool.reset(new CpuPool(int(std::max(1u, std::thread::hardware_concurrency()))));
+    }
     cudaStream_t st = nullptr;
 
     // dense weights
@@ -309,10 +362,15 @@ struct Engine {
       ly.wqkv = dalloc<uint16_t>(size_t(qkv_w) * h);
       ly.wo = dalloc<uint16_t>(size_t(h) * nq * d);
       ly.router = dalloc<uint16_t>(size_t(E) * h);
-      ly.kc = dalloc<uint16_t>(kv_elems());
-      ly.vc = dalloc<uint16_t>(kv_elems());
-      SMO_CUDA_CHECK(cudaMemset(ly.kc, 0, kv_elems() * 2));
-      SMO_CUDA_CHECK(cudaMemset(ly.vc, 0, kv_elems() * 2));
+      if (attn_cpu) {  // K/V in pinned host DRAM (the GPU appends through mapped memory)
+        ly.kc = halloc_mapped<uint16_t>(kv_elems());
+        ly.vc = halloc_mapped<uint16_t>(kv_elems());
+      } else {
+        ly.kc = dalloc<uint16_t>(kv_elems());
+        ly.vc = dalloc<uint16_t>(kv_elems());
+        SMO_CUDA_CHECK(cudaMemset(ly.kc, 0, kv_elems() * 2));
+        SMO_CUDA_CHECK(cudaMemset(ly.vc, 0, kv_elems() * 2));
+      }
       fill_uniform(ly.wqkv, size_t(qkv_w) * h, cfg.seed, tid::layer(l) + tid::kWqkv, 0, std::sqrt(3.0f / h), st);
       fill_uniform(ly.wo, size_t(h) * nq * d, cfg.seed, tid::layer(l) + tid::kWo, 0, std::sqrt(3.0f / (nq * d)),
                    st);
@@ -494,6 +552,15 @@ struct Engine {
       gemm_ws_bytes = std::max(gemm_ws_bytes, size_t(8) * maxT * std::max(qkv_w, h) * sizeof(float));
       gemm_ws = dalloc<uint8_t>(gemm_ws_bytes);
     }
+    layer_bytes.assign(size_t(L), 0.0);
+    if (batch_one) h_offsets = halloc_mapped<int32_t>(size_t(E) + 1);
+    if (attn_cpu) {
+      q_host = halloc_mapped<uint16_t>(size_t(maxT) * nq * d);
+      attn_host = halloc_mapped<uint16_t>(size_t(maxT) * nq * d);
+      prefix_host = halloc_mapped<int32_t>(maxB);
+      mask_host = halloc_mapped<uint64_t>(maxT);
+      host_jobs.resize(size_t(L));
+    }
     // drafter + decode-loop state
     if (dL > 0) dh = dalloc<uint16_t>(size_t(maxT) * dI);
     d_dtok = dalloc<int32_t>(maxB);
@@ -552,13 +619,16 @@ struct Engine {
   // Stream layer l's non-cached owned experts into slot l % slots. Host and
   // slot blocks are in local order, so runs of consecutive local experts go
   // out as one copy (a whole layer when nothing is cached: 2.8 GB for 8x7B).
-  double enqueue_h2d(int l, cudaEvent_t t0, cudaEvent_t t1) {
+  // active (optional, BATCH_ONE): per local expert, 0 = not routed to -> not streamed
+  double enqueue_h2d(int l, cudaEvent_t t0, cudaEvent_t t1, const uint8_t* active = nullptr) {
     const int s = l % slots;
     SMO_CUDA_CHECK(cudaStreamWaitEvent(copy, slot_free[s], 0));
     if (t0) SMO_CUDA_CHECK(cudaEventRecord(t0, copy));
     double bytes = 0;
     const uint16_t* hb = host_bufs[host_layer(l)];
-    auto streamed = [&](int le) { return cache_blk[size_t(l) * E + owned[size_t(le)]] < 0; };
+    auto streamed = [&](int le) {
+      return cache_blk[size_t(l) * E + owned[size_t(le)]] < 0 && (!active || active[le]);
+    };
     int le = 0;
     while (le < E_loc) {
       if (!streamed(le)) {
@@ -575,6 +645,7 @@ struct Engine {
     }
     if (t1) SMO_CUDA_CHECK(cudaEventRecord(t1, copy));
     SMO_CUDA_CHECK(cudaEventRecord(slot_ready[s], copy));
+    layer_bytes[size_t(l)] = bytes;
     return bytes;
   }
 
@@ -682,7 +753,7 @@ struct Engine {
     }
     bt_sync(st);
     last_was_decode = false;
-    begin_step(st);
+    begin_step(st, !batch_one);
     verify_core(b, n, d_tokens, parent, d_prefix, max_prefix, st);
     // ---- outputs
     if (out.on_device) {
@@ -710,13 +781,14 @@ struct Engine {
   // the drafter in a decode step so that the first transfers overlap drafting.
   double step_h2d_bytes = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> step_h2d_ev;
-  void begin_step(cudaStream_t st) {
+  void begin_step(cudaStream_t st, bool prefetch = true) {
     SMO_CUDA_CHECK(cudaEventRecord(ev[0], st));
     // order the copy stream after the step start (so H2D timing is step-relative)
     SMO_CUDA_CHECK(cudaStreamWaitEvent(copy, ev[0], 0));
     step_h2d_bytes = 0;
     step_h2d_ev.clear();
-    for (int l = 0; l < std::min(slots, L); ++l) {
+    std::fill(layer_bytes.begin(), layer_bytes.end(), 0.0);
+    for (int l = 0; prefetch && l < std::min(slots, L); ++l) {
       step_h2d_bytes += enqueue_h2d(l, tev(l * 8 + 0), tev(l * 8 + 1));
       step_h2d_ev.push_back({tev(l * 8 + 0), tev(l * 8 + 1)});
     }
@@ -755,9 +827,10 @@ struct Engine {
       g.workspace = gemm_ws;
       g.workspace_bytes = gemm_ws_bytes;
       gemm_launch(g, st);
-      rope_append(qkv, prefix, parent, b, n, nq, nkv, d, s_max, cfg.rope_theta, q, ly.kc, ly.vc, st, bt(),
+      uint16_t* q_dst = attn_cpu ? q_host : q;  // CPU placement: q straight into pinned host memory
+      rope_append(qkv, prefix, parent, b, n, nq, nkv, d, s_max, cfg.rope_theta, q_dst, ly.kc, ly.vc, st, bt(),
                   max_pages);
-      snap("q", l, q, size_t(T) * nq * d * 2, st);
+      snap("q", l, q_dst, size_t(T) * nq * d * 2, st);
       smo_attn_args a{};
       a.q = q;
       a.k_cache = ly.kc;
@@ -778,7 +851,19 @@ struct Engine {
       a.workspace = attn_ws;
       a.workspace_bytes = attn_ws_bytes;
       SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 2), st));
-      attention_launch(a, st);
+      if (attn_cpu) {
+        // the paper's CPU attention: prefix lengths and mask to the host, the
+        // host pool attends over the host K/V, the output goes back for O-proj
+        SMO_CUDA_CHECK(cudaMemcpyAsync(prefix_host, prefix, size_t(b) * 4, cudaMemcpyDeviceToHost, st));
+        SMO_CUDA_CHECK(cudaMemcpyAsync(mask_host, d_mask, size_t(T) * 8, cudaMemcpyDeviceToHost, st));
+        HostAttn& hj = host_jobs[size_t(l)];
+        hj.pool = cpu_pool.get();
+        hj.job = CpuAttnJob{q_host, ly.kc, ly.vc, mask_host, prefix_host, attn_host, b, n, nq, nkv, d, s_max, 1};
+        SMO_CUDA_CHECK(cudaLaunchHostFunc(st, host_attn_cb, &hj));
+        SMO_CUDA_CHECK(cudaMemcpyAsync(attn, attn_host, size_t(T) * nq * d * 2, cudaMemcpyHostToDevice, st));
+      } else {
+        attention_launch(a, st);
+      }
       SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 3), st));
       attn_ev.push_back({tev(l * 8 + 2), tev(l * 8 + 3)});
       snap("attn", l, attn, size_t(T) * nq * d * 2, st);
@@ -820,6 +905,17 @@ struct Engine {
       snap("weights", l, rw, size_t(PT) * 4, st);
       snap("offsets", l, offsets, size_t(E + 1) * 4, st);
       snap("pos", l, pos, size_t(PT) * 4, st);
+      if (batch_one) {
+        // BATCH_ONE (optimizer.hpp:81-96): wait for this layer's routing, then
+        // stream only the experts its tokens selected
+        SMO_CUDA_CHECK(cudaMemcpyAsync(h_offsets, offsets, size_t(E + 1) * 4, cudaMemcpyDeviceToHost, st));
+        SMO_CUDA_CHECK(cudaEventRecord(route_ev, st));
+        SMO_CUDA_CHECK(cudaEventSynchronize(route_ev));
+        std::vector<uint8_t> act(size_t(E_loc), 0);
+        for (int e = 0; e < E; ++e) act[size_t(local(e))] = h_offsets[e + 1] > h_offsets[e] ? 1 : 0;
+        h2d_bytes += enqueue_h2d(l, tev(l * 8 + 0), tev(l * 8 + 1), act.data());
+        h2d_ev.push_back({tev(l * 8 + 0), tev(l * 8 + 1)});
+      }
       if (cfg.shared_inter > 0) {
         // always-on shared expert (config 4): x += SwiGLU_shared(xn2); its
         // weights are resident, so it runs before the wait for streamed experts
@@ -899,7 +995,7 @@ struct Engine {
       SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 5), st));
       moe_ev.push_back({tev(l * 8 + 4), tev(l * 8 + 5)});
       snap("x_out", l, x, size_t(T) * h * 4, st);
-      if (l + slots < L) {
+      if (!batch_one && l + slots < L) {
         const int ln = l + slots;
         h2d_bytes += enqueue_h2d(ln, tev(ln * 8 + 0), tev(ln * 8 + 1));
         h2d_ev.push_back({tev(ln * 8 + 0), tev(ln * 8 + 1)});
@@ -1015,6 +1111,28 @@ struct Engine {
     dense_gemm(sc.attn, rows, nq * d, h, wo, nullptr, SMO_EPI_F32_ADD, sc.x, sc.split, st);
   }
 
+  // attn_sublayer with the CPU placement: q and the appended K/V rows go to
+  // pinned host memory, one host job attends over all `nch` chunks (chunk c
+  // only sees its prefix + own rows), the output comes back for O-proj.
+  // qh/ah: pinned mapped [b*n*nch, n_q, d]; pre_h [nch*b], mask_h [b*n] host.
+  void attn_sublayer_cpu(const Scratch& sc, const uint16_t* wqkv, const uint16_t* wo, uint16_t* kc, uint16_t* vc,
+                         int b, int n, int nch, const int32_t* prefix, uint16_t* qh, uint16_t* ah,
+                         const int32_t* pre_h, const uint64_t* mask_h, HostAttn& job, cudaStream_t st) {
+    const int rows = b * n * nch;
+    rmsnorm(sc.x, ones, rows, h, cfg.rms_eps, sc.xn, st);
+    dense_gemm(sc.xn, rows, h, qkv_w, wqkv, nullptr, SMO_EPI_BF16, sc.qkv, sc.split, st);
+    for (int c = 0; c < nch; ++c) {
+      const size_t r0 = size_t(c) * b * n;
+      rope_append(sc.qkv + r0 * qkv_w, prefix + size_t(c) * b, nullptr, b, n, nq, nkv, d, s_max, cfg.rope_theta,
+                  qh + r0 * nq * d, kc, vc, st);
+    }
+    job.pool = cpu_pool.get();
+    job.job = CpuAttnJob{qh, kc, vc, mask_h, pre_h, ah, b, n, nq, nkv, d, s_max, nch};
+    SMO_CUDA_CHECK(cudaLaunchHostFunc(st, host_attn_cb, &job));
+    SMO_CUDA_CHECK(cudaMemcpyAsync(sc.attn, ah, size_t(rows) * nq * d * 2, cudaMemcpyHostToDevice, st));
+    dense_gemm(sc.attn, rows, nq * d, h, wo, nullptr, SMO_EPI_F32_ADD, sc.x, sc.split, st);
+  }
+
   // x += W2 . (silu(W1 . rmsnorm(x)) * W3 . rmsnorm(x))  (dense SwiGLU)
   void ffn_dense(const Scratch& sc, uint16_t* hb, int rows, const uint16_t* w1, const uint16_t* w3,
                  const uint16_t* w2, int inter, cudaStream_t st) {
@@ -1099,7 +1217,7 @@ struct Engine {
       SMO_CUDA_CHECK(cudaMemcpyAsync(d_drafts, h_stage, size_t(b) * k * 4, cudaMemcpyHostToDevice, st));
     }
     last_was_decode = true;
-    begin_step(st);  // the first layers' experts stream while the drafter runs
+    begin_step(st, !batch_one);  // the first layers' experts stream while the drafter runs
     decode_prep(d_root, planted ? d_drafts : nullptr, b, n, d_dec_tok, st);
     // drafter: step t consumes row t (root, d_1, ..., d_k) at kv_len + t and
     // proposes d_{t+1}; the extra step t = k only appends d_k's draft K/V so
@@ -1250,6 +1368,32 @@ struct Engine {
     auto* p_y = static_cast<float*>(talloc(size_t(PT) * h * 4));
     uint16_t* p_hs = cfg.shared_inter > 0 ? static_cast<uint16_t*>(talloc(size_t(Tp) * cfg.shared_inter * 2)) : nullptr;
     uint16_t* p_dh = dL > 0 ? static_cast<uint16_t*>(talloc(size_t(Tp) * dI * 2)) : nullptr;
+    // CPU placement: pinned host q / attention rows, prefix and chain mask
+    std::vector<void*> htmp;
+    std::vector<HostAttn> pf_jobs(attn_cpu ? size_t(L) : 0);
+    uint16_t *pq_h = nullptr, *pa_h = nullptr;
+    int32_t* ppre_h = nullptr;
+    uint64_t* pmask_h = nullptr;
+    if (attn_cpu) {
+      auto hal = [&](size_t bytes) {
+        void* hp = nullptr;
+        if (cudaHostAlloc(&hp, std::max<size_t>(bytes, 16), cudaHostAllocPortable | cudaHostAllocMapped) !=
+            cudaSuccess) {
+          for (void* q2 : htmp) cudaFreeHost(q2);
+          for (void* q2 : tmp) cudaFree(q2);
+          throw Error(SMO_CAPACITY, "prefill: pinned host allocation failed");
+        }
+        htmp.push_back(hp);
+        return hp;
+      };
+      pq_h = static_cast<uint16_t*>(hal(size_t(Tp) * nq * d * 2));
+      pa_h = static_cast<uint16_t*>(hal(size_t(Tp) * nq * d * 2));
+      ppre_h = static_cast<int32_t*>(hal(pre.size() * 4));
+      pmask_h = static_cast<uint64_t*>(hal(size_t(b) * C * 8));
+      std::memcpy(ppre_h, pre.data(), pre.size() * 4);
+      for (int r = 0; r < b; ++r)
+        for (int i = 0; i < C; ++i) pmask_h[size_t(r) * C + i] = i >= 63 ? ~0ull : ((1ull << (i + 1)) - 1ull);
+    }
     SMO_CUDA_CHECK(cudaStreamSynchronize(st));
     bt_reset();
     for (int r = 0; r < b; ++r) {
@@ -1271,7 +1415,11 @@ struct Engine {
       Layer& ly = layers[l];
       const bool chk = prefill_check_on();
       if (chk) check_finite("x_in", l, sc.x, size_t(Tp) * h, false, st);
-      attn_sublayer(sc, ly.wqkv, ly.wo, ly.kc, ly.vc, b, C, nch, p_pre, maxpre, p_mask, st);
+      if (attn_cpu)
+        attn_sublayer_cpu(sc, ly.wqkv, ly.wo, ly.kc, ly.vc, b, C, nch, p_pre, pq_h, pa_h, ppre_h, pmask_h,
+                          pf_jobs[size_t(l)], st);
+      else
+        attn_sublayer(sc, ly.wqkv, ly.wo, ly.kc, ly.vc, b, C, nch, p_pre, maxpre, p_mask, st);
       if (chk) {
         check_finite("qkv", l, sc.qkv, size_t(Tp) * qkv_w, true, st);
         check_finite("q", l, sc.q, size_t(Tp) * nq * d, true, st);
@@ -1346,6 +1494,7 @@ struct Engine {
     SMO_CUDA_CHECK(cudaMemcpyAsync(next_h, d_root, size_t(b) * 4, cudaMemcpyDeviceToHost, st));
     SMO_CUDA_CHECK(cudaStreamSynchronize(st));
     for (void* p : tmp) cudaFree(p);
+    for (void* p : htmp) cudaFreeHost(p);
     pending_attn.clear();
     pending_moe.clear();
     pending_h2d.clear();
@@ -1367,9 +1516,7 @@ struct Engine {
         SMO_CUDA_CHECK(cudaEventElapsedTime(&ms, ev[0], ev[8 + size_t(l) * 8 + k]));
         out[size_t(l) * 9 + k] = ms * 1e-3;
       }
-      int streamed = 0;
-      for (int e : owned) streamed += cache_blk[size_t(l) * E + e] < 0 ? 1 : 0;
-      out[size_t(l) * 9 + 8] = double(streamed) * double(blk_bytes);
+      out[size_t(l) * 9 + 8] = layer_bytes[size_t(l)];
     }
   }
 

@@ -82,6 +82,24 @@ def verify_attention(q, k_cache, v_cache, mask, prefix_len, max_prefix: int, out
     return out
 
 
+def cpu_verify_attention(q, k_cache, v_cache, mask, prefix_len, threads: int = 0):
+    """Host verification attention (AttentionPlacement::CPU, SURVEY.md §8 f4)
+    on numpy arrays: q uint16(bf16) [b*n, n_q, d], caches [b, n_kv, s_max, d],
+    mask uint64 [b*n], prefix_len int32 [b]. Returns bf16 bits [b*n, n_q, d]."""
+    import numpy as np
+    b, n_kv, s_max, d = k_cache.shape
+    T, n_q, _ = q.shape
+    arrs = [np.ascontiguousarray(x) for x in (q, k_cache, v_cache)]
+    m = np.ascontiguousarray(mask, np.uint64)
+    pre = np.ascontiguousarray(prefix_len, np.int32)
+    out = np.zeros((T, n_q, d), np.uint16)
+    vp = lambda a: a.ctypes.data  # noqa: E731
+    a = L.AttnArgs(q=vp(arrs[0]), k_cache=vp(arrs[1]), v_cache=vp(arrs[2]), mask=vp(m), prefix_len=vp(pre),
+                   out=vp(out), b=b, n=T // b, n_q=n_q, n_kv=n_kv, d=d, s_max=s_max, max_prefix=int(pre.max()))
+    L.check(L.load().smo_cpu_verify_attention(C.byref(a), threads))
+    return out
+
+
 def router_topk(x, w_router, k: int, want_logits: bool = False):
     """K2. x [T, h] bf16, w_router [E, h] bf16 -> ids int32 [T,k], weights f32 [T,k] (, logits)."""
     _req(x, _BF16, "x")

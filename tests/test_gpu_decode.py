@@ -53,9 +53,9 @@ def ref(cuda):
     return s, om, out
 
 
-def _engine(s, n_max=6, debug=False):
+def _engine(s, n_max=6, debug=False, attn_cpu=False):
     from paper_2508_21706_b200.engine import VerifyEngine
-    return VerifyEngine(s, max_batch=len(PROMPTS), max_verify=n_max, max_seq=256, debug=debug)
+    return VerifyEngine(s, max_batch=len(PROMPTS), max_verify=n_max, max_seq=256, debug=debug, attn_cpu=attn_cpu)
 
 
 def test_prefill_matches_oracle(ref, oracle):
@@ -124,16 +124,19 @@ def _teacher_forced(om, prompt, root, committed, where):
     return ok
 
 
-def test_decode_planted_drafts_commit_greedy_sequence(ref):
+@pytest.mark.parametrize("placement", ["gpu", "cpu"])
+def test_decode_planted_drafts_commit_greedy_sequence(ref, placement):
     """Planted drafts = the oracle's next k greedy tokens (from the GPU's own
     committed state) corrupted from a random index on: each step must accept
-    exactly the uncorrupted prefix, and every committed token is greedy."""
+    exactly the uncorrupted prefix, and every committed token is greedy.
+    placement "cpu": AttentionPlacement::CPU — target K/V in pinned host DRAM,
+    prefill and verify attention on the host pool."""
     import copy
     import oracle_model
     s, om, _ = ref
     b, k = len(PROMPTS), 4
     prompts = _prompts(s)
-    eng = _engine(s)
+    eng = _engine(s, attn_cpu=placement == "cpu")
     nxt = eng.prefill(prompts)
     decs, lgs = [], []
     for r, p in enumerate(prompts):  # oracle state after prompt + root

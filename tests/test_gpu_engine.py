@@ -222,3 +222,24 @@ def test_engine_stage_times_and_h2d_bytes(setup):
     s = om.s
     assert t["h2d_bytes"] == s.n_layers * s.n_expert * s.expert_bytes
     assert t["target_total"] > 0 and t["h2d_transfer"] > 0 and t["attention"] > 0 and t["gpu_moe"] > 0
+
+
+def test_batch_one_streams_only_routed_experts(cuda):
+    """MoeBatching::BATCH_ONE (config.hpp:111, optimizer.hpp:81-96): after
+    each layer's routing only the selected experts cross the link; results are
+    bit-identical to LARGE_BATCH (same math, fewer bytes)."""
+    from paper_2508_21706_b200.engine import VerifyEngine
+    s = _shape()
+    b, n, prefix = 1, 2, np.array([300], np.int32)  # 2 tokens x top-2: at most 4 of 8 experts per layer
+    tokens = np.array([[17, 4242]], np.int32)
+    out = {}
+    for one in (False, True):
+        eng = VerifyEngine(s, max_batch=b, max_verify=n, max_seq=512, batch_one=one)
+        eng.fill_prefix(prefix)
+        r = eng.verify(tokens, prefix)
+        out[one] = (r, eng.last_times()["h2d_bytes"])
+        eng.close()
+    (r0, b0), (r1, b1) = out[False], out[True]
+    assert np.array_equal(r0.target, r1.target) and np.array_equal(r0.acc_len, r1.acc_len)
+    assert b0 == s.n_layers * s.n_expert * s.expert_bytes
+    assert 0 < b1 <= s.n_layers * 4 * s.expert_bytes
