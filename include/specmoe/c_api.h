@@ -117,6 +117,12 @@ smo_status smo_permute(const int32_t* ids, int32_t T, int32_t k, int32_t E, cons
  * j order fixed, no atomics). y_perm fp32 [T*k, h].                         */
 smo_status smo_unpermute_combine(const float* y_perm, const int32_t* pos, const float* weights,
                                  int32_t T, int32_t k, int32_t h, float* residual, smo_stream stream);
+/* Same with the down projection in K slices y_perm[s] (split_stride
+ * elements apart, s < splits), summed in slice order per (token, slot), as
+ * produced by smo_moe_experts.                                             */
+smo_status smo_unpermute_combine_split(const float* y_perm, int32_t splits, uint64_t split_stride,
+                                       const int32_t* pos, const float* weights, int32_t T, int32_t k, int32_t h,
+                                       float* residual, smo_stream stream);
 
 /* ---- K4: tcgen05 GEMMs ------------------------------------------------------
  * out[t, n] = sum_c x[t,c] * W_g[n,c] for the rows t of group g
@@ -156,6 +162,22 @@ typedef struct {
  * the epilogue. Returns the workspace the call needs (0: none).            */
 size_t smo_gemm_workspace(const smo_gemm_args* a);
 smo_status smo_gemm(const smo_gemm_args* a, smo_stream stream);
+
+/* ---- K4-MoE: the whole expert block of one layer in ONE persistent kernel
+ * (grouped SwiGLU gate/up, then the down projection; moe_tc.cu):
+ *   h_out bf16 [rows, h_i] = silu(x W1_e^T) * (x W3_e^T)   for the rows of e
+ *   sum_s y[s] f32 [rows, h] = h_out W2_e^T, the K dimension cut into `splits`
+ *            slices (1, 2 or 4; 0 = chosen by a waves model, written to
+ *            *splits_used); y holds [splits][rows][h] (room for 4 when 0);
+ *            sum them with smo_unpermute_combine_split.
+ * x_perm bf16 [rows, h] grouped by offsets [E+1] (device); expert e uses pool
+ * block w_index[e] = [W1 | W3 | W2] (nn.Linear layouts), blocks
+ * w_block_stride bytes apart. scratch: >= E int32 (device). E <= 64,
+ * h and h_i multiples of 128. The roofline.hpp:56-64 expert cost.          */
+smo_status smo_moe_experts(const void* x_perm, int32_t rows, int32_t h, int32_t h_i, int32_t E,
+                           const int32_t* offsets, const void* w_pool, uint64_t w_block_stride,
+                           int32_t w_pool_blocks, const int32_t* w_index, void* h_out, float* y, int32_t splits,
+                           int32_t* splits_used, int32_t* scratch, smo_stream stream);
 
 /* ---- support ops of the verify layer (standard Mixtral block, not in the
  *      reference: SURVEY.md §2.3 "support")                                 */

@@ -90,6 +90,9 @@ _SIGS = {
     "smo_router_topk": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "smo_permute": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp]),
     "smo_unpermute_combine": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp]),
+    "smo_unpermute_combine_split": (C.c_int, [_vp, _i32, _u64, _vp, _vp, _i32, _i32, _i32, _vp, _vp]),
+    "smo_moe_experts": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _vp, _vp, _u64, _i32, _vp, _vp, _vp, _i32, _vp, _vp,
+                                  _vp]),
     "smo_gemm_workspace": (_sz, [C.POINTER(GemmArgs)]),
     "smo_gemm": (C.c_int, [C.POINTER(GemmArgs), _vp]),
     "smo_rmsnorm": (C.c_int, [_vp, _vp, _i32, _i32, _f32, _vp, _vp]),

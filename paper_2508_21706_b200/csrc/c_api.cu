@@ -30,7 +30,10 @@ void router_topk(const void* x, const void* w, int T, int h, int E, int k, float
 void permute(const int32_t* ids, int T, int k, int E, const void* x, int h, int32_t* offsets, int32_t* perm,
              int32_t* pos, void* xp, cudaStream_t st);
 void unpermute_combine(const float* y, const int32_t* pos, const float* w, int T, int k, int h, float* res,
-                       cudaStream_t st);
+                       cudaStream_t st, int splits = 1, size_t split_stride = 0);
+int moe_launch(const void* x_perm, int rows, int h, int hi, int E, const int32_t* offsets, const void* pool,
+               uint64_t w_block_stride, int pool_blocks, const int32_t* w_index, void* hbuf, float* y, int splits,
+               int max_splits, int* done, cudaStream_t st);
 void rmsnorm(const float* x, const void* gain, int T, int h, float eps, void* y, cudaStream_t st);
 void embed(const int32_t* tok, const void* emb, int T, int h, float* x, cudaStream_t st);
 void rope_append(const void* qkv, const int32_t* prefix, const int32_t* parent, int b, int n, int n_q, int n_kv,
@@ -176,6 +179,26 @@ smo_status smo_permute(const int32_t* ids, int32_t T, int32_t k, int32_t E, cons
 smo_status smo_unpermute_combine(const float* y, const int32_t* pos, const float* w, int32_t T, int32_t k,
                                  int32_t h, float* residual, smo_stream stream) {
   return guard([&] { smo::unpermute_combine(y, pos, w, T, k, h, residual, S(stream)); });
+}
+
+smo_status smo_unpermute_combine_split(const float* y, int32_t splits, uint64_t split_stride, const int32_t* pos,
+                                       const float* w, int32_t T, int32_t k, int32_t h, float* residual,
+                                       smo_stream stream) {
+  return guard([&] {
+    SMO_REQUIRE(splits >= 1, "combine: splits >= 1");
+    smo::unpermute_combine(y, pos, w, T, k, h, residual, S(stream), splits, size_t(split_stride));
+  });
+}
+
+smo_status smo_moe_experts(const void* x_perm, int32_t rows, int32_t h, int32_t h_i, int32_t E,
+                           const int32_t* offsets, const void* w_pool, uint64_t w_block_stride,
+                           int32_t w_pool_blocks, const int32_t* w_index, void* h_out, float* y, int32_t splits,
+                           int32_t* splits_used, int32_t* scratch, smo_stream stream) {
+  return guard([&] {
+    const int sp = smo::moe_launch(x_perm, rows, h, h_i, E, offsets, w_pool, w_block_stride, w_pool_blocks, w_index,
+                                   h_out, y, splits, 4, scratch, S(stream));
+    if (splits_used) *splits_used = sp;
+  });
 }
 
 size_t smo_gemm_workspace(const smo_gemm_args* a) {

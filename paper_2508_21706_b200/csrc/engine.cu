@@ -47,7 +47,7 @@ void router_topk(const void* x, const void* w, int T, int h, int E, int k, float
 void permute(const int32_t* ids, int T, int k, int E, const void* x, int h, int32_t* offsets, int32_t* perm,
              int32_t* pos, void* xp, cudaStream_t st);
 void unpermute_combine(const float* y, const int32_t* pos, const float* w, int T, int k, int h, float* res,
-                       cudaStream_t st);
+                       cudaStream_t st, int splits = 1, size_t split_stride = 0);
 void rmsnorm(const float* x, const void* gain, int T, int h, float eps, void* y, cudaStream_t st);
 void embed(const int32_t* tok, const void* emb, int T, int h, float* x, cudaStream_t st);
 void rope_append(const void* qkv, const int32_t* prefix, const int32_t* parent, int b, int n, int n_q, int n_kv,
@@ -74,7 +74,11 @@ void ep_pos(const int32_t* oid, const int32_t* pos, const int32_t* offsets, int 
 void ep_unpack(const void* recv, int P, int E_loc, int C, int h, size_t block_bytes, void* xl, int32_t* offsets_l,
                int32_t* back, cudaStream_t st);
 void ep_pack_back(const float* yl, const int32_t* back, const int32_t* offsets_l, int E_loc, int h, float* sendback,
-                  cudaStream_t st);
+                  cudaStream_t st, int splits = 1, size_t split_stride = 0);
+int moe_launch(const void* x_perm, int rows, int h, int hi, int E, const int32_t* offsets, const void* pool,
+               uint64_t w_block_stride, int pool_blocks, const int32_t* w_index, void* hbuf, float* y, int splits,
+               int max_splits, int* done, cudaStream_t st);
+int pick_moe_splits(int rows, int h, int hi, int E, int max_splits);
 
 // Procedural tensor ids; the oracle tests use the same ids.
 namespace tid {
@@ -175,6 +179,9 @@ struct Engine {
   // activations (max sizes)
   int maxT = 0, maxB = 0, maxN = 0, s_max = 0;
   float *x = nullptr, *ybuf = nullptr, *rw = nullptr, *amax_v = nullptr;
+  int moe_splits = 1;      // down-projection K slices of the fused MoE kernel (from the global shapes)
+  int* d_done = nullptr;   // fused MoE kernel: finished gate/up units per expert
+  bool moe_fused = true;   // SMO_MOE_FUSED=0: two grouped GEMM launches instead (A/B runs)
   uint16_t *xn = nullptr, *qkv = nullptr, *q = nullptr, *attn = nullptr, *xp = nullptr, *hbuf = nullptr;
   uint16_t* hs = nullptr;  // shared-expert SwiGLU activations [T, shared_inter]
   int32_t *ids = nullptr, *offsets = nullptr, *perm = nullptr, *pos = nullptr, *amax_i = nullptr, *target = nullptr;
@@ -502,14 +509,22 @@ struct Engine {
       ep_send = dalloc<uint8_t>(size_t(PR) * blk_d);
       ep_recv = dalloc<uint8_t>(size_t(PR) * blk_d);
       xl = dalloc<uint16_t>(size_t(PR) * C * h);
-      yl = dalloc<float>(size_t(PR) * C * h);
+      yl = dalloc<float>(size_t(4) * PR * C * h);  // room for the fused kernel's down slices
       ep_sendback = dalloc<float>(size_t(PR) * C * h);
       ep_recvback = dalloc<float>(size_t(PR) * C * h);
       hbuf = dalloc<uint16_t>(size_t(PR) * C * hi);
     } else {
       hbuf = dalloc<uint16_t>(size_t(P) * hi);
     }
-    ybuf = dalloc<float>(size_t(P) * h);
+    {
+      const char* f = std::getenv("SMO_MOE_FUSED");
+      moe_fused = !(f && f[0] == '0');
+    }
+    // fused MoE down splits from the GLOBAL shapes (every EP rank uses the
+    // same S, so expert parallelism reproduces one GPU bit for bit)
+    moe_splits = moe_fused ? pick_moe_splits(maxT * K, h, hi, E, 4) : 1;
+    ybuf = dalloc<float>(size_t(moe_splits) * P * h);
+    d_done = dalloc<int>(64);
     amax_v = dalloc<float>(size_t(maxT) * (V / 128));
     amax_i = dalloc<int32_t>(size_t(maxT) * (V / 128));
     target = dalloc<int32_t>(maxT);
@@ -673,6 +688,15 @@ struct Engine {
     SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 7), st));
     SMO_CUDA_CHECK(cudaStreamWaitEvent(st, slot_ready[l % slots], 0));
     SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 4), st));
+    if (moe_fused) {
+      moe_launch(xl, P * C, h, hi, E_loc, offsets_l, pool, blk_bytes, pool_blocks, d_w_index_loc + size_t(l) * E_loc,
+                 hbuf, yl, moe_splits, 4, d_done, st);
+      SMO_CUDA_CHECK(cudaEventRecord(slot_free[l % slots], st));
+      ep_pack_back(yl, back, offsets_l, E_loc, h, ep_sendback, st, moe_splits, size_t(P) * C * h);
+      ept->alltoall(rank, ep_sendback, ep_recvback, size_t(C) * h * sizeof(float), st);
+      unpermute_combine(ep_recvback, pos_ep, rw, T, K, h, x, st);
+      return;
+    }
     smo_gemm_args g{};
     g.x = xl;
     g.rows = P * C;
@@ -956,6 +980,12 @@ struct Engine {
         SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 7), st));
         SMO_CUDA_CHECK(cudaStreamWaitEvent(st, slot_ready[l % slots], 0));
         SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 4), st));
+        if (moe_fused) {
+          moe_launch(xp, PT, h, hi, E, offsets, pool, blk_bytes, pool_blocks, d_w_index + size_t(l) * E, hbuf, ybuf,
+                     moe_splits, moe_splits, d_done, st);
+          SMO_CUDA_CHECK(cudaEventRecord(slot_free[l % slots], st));
+          unpermute_combine(ybuf, pos, rw, T, K, h, x, st, moe_splits, size_t(PT) * h);
+        } else {
         g = smo_gemm_args{};
         g.x = xp;
         g.rows = PT;
@@ -991,6 +1021,7 @@ struct Engine {
         gemm_launch(g, st);
         SMO_CUDA_CHECK(cudaEventRecord(slot_free[l % slots], st));
         unpermute_combine(ybuf, pos, rw, T, K, h, x, st);
+        }
       }
       SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 5), st));
       moe_ev.push_back({tev(l * 8 + 4), tev(l * 8 + 5)});
@@ -1365,7 +1396,8 @@ struct Engine {
     auto* p_pos = static_cast<int32_t*>(talloc(size_t(PT) * 4));
     auto* p_xp = static_cast<uint16_t*>(talloc(size_t(PT) * h * 2));
     auto* p_hb = static_cast<uint16_t*>(talloc(size_t(PT) * hi * 2));
-    auto* p_y = static_cast<float*>(talloc(size_t(PT) * h * 4));
+    const int pf_splits = moe_fused ? pick_moe_splits(PT, h, hi, E, 2) : 1;
+    auto* p_y = static_cast<float*>(talloc(size_t(pf_splits) * PT * h * 4));
     uint16_t* p_hs = cfg.shared_inter > 0 ? static_cast<uint16_t*>(talloc(size_t(Tp) * cfg.shared_inter * 2)) : nullptr;
     uint16_t* p_dh = dL > 0 ? static_cast<uint16_t*>(talloc(size_t(Tp) * dI * 2)) : nullptr;
     // CPU placement: pinned host q / attention rows, prefix and chain mask
@@ -1435,6 +1467,10 @@ struct Engine {
         dense_gemm(p_hs, Tp, cfg.shared_inter, h, ly.ws2, nullptr, SMO_EPI_F32_ADD, sc.x, 1, st);
       }
       SMO_CUDA_CHECK(cudaStreamWaitEvent(st, slot_ready[l % slots], 0));
+      if (moe_fused) {
+        moe_launch(p_xp, PT, h, hi, E, p_off, pool, blk_bytes, pool_blocks, d_w_index + size_t(l) * E, p_hb, p_y,
+                   pf_splits, pf_splits, d_done, st);
+      } else {
       smo_gemm_args g2{};
       g2.x = p_xp;
       g2.rows = PT;
@@ -1468,12 +1504,13 @@ struct Engine {
       g2.out = p_y;
       g2.ldo = h;
       gemm_launch(g2, st);
+      }
       SMO_CUDA_CHECK(cudaEventRecord(slot_free[l % slots], st));
       if (chk) {
         check_finite("h_swiglu", l, p_hb, size_t(PT) * hi, true, st);
         check_finite("y_down", l, p_y, size_t(PT) * h, false, st);
       }
-      unpermute_combine(p_y, p_pos, p_rw, Tp, K, h, sc.x, st);
+      unpermute_combine(p_y, p_pos, p_rw, Tp, K, h, sc.x, st, pf_splits, size_t(PT) * h);
       if (l + slots < L) h2d_bytes += enqueue_h2d(l + slots, nullptr, nullptr);
     }
     SMO_CUDA_CHECK(cudaStreamWaitEvent(st, slot_ready[(L - 1) % slots], 0));

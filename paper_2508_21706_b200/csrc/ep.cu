@@ -1,3 +1,4 @@
+#include <algorithm>
 // ep.cu — expert parallelism: token dispatch / combine
 // around the grouped SwiGLU experts, and the transports that move the blocks.
 //
@@ -115,14 +116,26 @@ __global__ void ep_unpack_kernel(const uint8_t* __restrict__ recv, int P, int E_
 }
 
 // expert outputs back to their source ranks' slots (fp32 rows).
+// splits > 1: down-projection K slices (split_stride elements apart) summed
+// in slice order — the same fixed order as the single-GPU combine
 __global__ void ep_pack_back_kernel(const float* __restrict__ yl, const int32_t* __restrict__ back,
                                     const int32_t* __restrict__ offsets_l, int E_loc, int h,
-                                    float* __restrict__ sendback) {
+                                    float* __restrict__ sendback, int splits, size_t split_stride) {
   const int rows = offsets_l[E_loc];
   for (int q = blockIdx.x; q < rows; q += gridDim.x) {
     const float4* src = reinterpret_cast<const float4*>(yl + size_t(q) * h);
     float4* dst = reinterpret_cast<float4*>(sendback + size_t(back[q]) * h);
-    for (int c = threadIdx.x; c < h / 4; c += blockDim.x) dst[c] = src[c];
+    for (int c = threadIdx.x; c < h / 4; c += blockDim.x) {
+      float4 v = src[c];
+      for (int s = 1; s < splits; ++s) {
+        const float4 v2 = reinterpret_cast<const float4*>(yl + size_t(s) * split_stride + size_t(q) * h)[c];
+        v.x += v2.x;
+        v.y += v2.y;
+        v.z += v2.z;
+        v.w += v2.w;
+      }
+      dst[c] = v;
+    }
   }
 }
 
@@ -156,8 +169,9 @@ void ep_unpack(const void* recv, int P, int E_loc, int C, int h, size_t block_by
   SMO_CUDA_CHECK(cudaGetLastError());
 }
 void ep_pack_back(const float* yl, const int32_t* back, const int32_t* offsets_l, int E_loc, int h, float* sendback,
-                  cudaStream_t st) {
-  ep_pack_back_kernel<<<256, 256, 0, st>>>(yl, back, offsets_l, E_loc, h, sendback);
+                  cudaStream_t st, int splits, size_t split_stride) {
+  ep_pack_back_kernel<<<256, 256, 0, st>>>(yl, back, offsets_l, E_loc, h, sendback, std::max(1, splits),
+                                           split_stride);
   count_launch();
   SMO_CUDA_CHECK(cudaGetLastError());
 }

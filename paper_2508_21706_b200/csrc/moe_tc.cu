@@ -1,0 +1,395 @@
+// moe_tc.cu — K4-MoE: the whole expert block of one layer (grouped SwiGLU
+// gate/up, then the down projection) as ONE persistent tcgen05 kernel.
+//
+// Why: as two grouped GEMMs each CTA streams one 128-row weight tile of one
+// expert (2 MB gate/up, 3.7 MB down for Mixtral); 896 gate/up tiles are 6.05
+// waves of 148 SMs and 256 down tiles 1.7 waves, so the last wave of each
+// kernel runs on a few SMs (ncu: SMs active 85 % of the gate/up kernel, 0.76
+// of HBM). Here one cooperative grid of one CTA per SM walks a single unit
+// list — every gate/up tile (expert-major), then every down tile split into
+// S K slices (S = 1, 2 or 4 by a waves model) — round robin, so the down
+// units of early experts fill the gate/up tail and the grid drains on
+// small units.
+//
+// Dependencies: a down unit of expert e reads rows of H written by the
+// SwiGLU epilogues of e's gate/up units (other CTAs). Each gate/up epilogue
+// publishes with a release fence + atomicAdd on done[e]; the down unit's TMA
+// producer spins on done[e] (acquire), then orders the async-proxy reads
+// after it (fence.proxy.async). Gate/up units precede down units in every
+// CTA's sequence, so the waits always resolve (co-residency: cooperative
+// launch, one CTA per SM).
+//
+// The down K slices land in y[0..S) (fp32); the combine (K3) adds them in
+// slice order — deterministic, and expert parallelism packs the same sum, so
+// EP stays bit-identical to one GPU (S depends only on the shapes).
+//
+// Per unit the warp roles are those of gemm_tc.cu (swap-AB: weight tile =
+// 128-row A operand, tokens = MMA N <= 256): w0 TMA producer, w1 MMA issuer,
+// w2..w5 epilogue (TMEM -> registers -> global). The smem ring runs
+// continuously across units, so the producer prefetches the next unit's
+// k-blocks while the epilogue drains the previous one (tmem_empty barrier).
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+#include "common.cuh"
+
+namespace smo {
+
+namespace {
+
+constexpr int kThreads = 192;
+constexpr int kBK = 64;
+constexpr int kTileA = 128 * kBK * 2;                  // weight tile per k-block (16 KB)
+constexpr int kTok = 256;                              // token tile (gate + up = 512 TMEM columns)
+constexpr int kStageBytes = 2 * kTileA + kTok * 128;   // 64 KB
+constexpr int kStages = 3;
+constexpr int kMaxE = 64;
+
+struct MoeParams {
+  int h, hi, E;
+  const int32_t* offsets;  // [E+1] row offsets of the permuted (token, slot) pairs
+  const int32_t* w_index;  // [E] pool block of each expert's [W1 | W3 | W2]
+  uint16_t* hbuf;          // [rows, hi] bf16 SwiGLU activations
+  float* y;                // [splits][rows, h] fp32 down partials, slice s over K in [s, s+1) * hi/splits
+  size_t y_stride;         // rows * h
+  int splits;
+  int* done;               // [E] finished gate/up units (zero at launch)
+};
+
+struct Unit {
+  int down, e, row0, cnt, nb, ks;
+};
+
+struct Schedule {
+  int nA, nB;           // units per token tile: hi/128 gate/up, splits*h/128 down
+  int totalA, total;
+  int splits;
+  int a_base[kMaxE + 1], b_base[kMaxE + 1];
+  int off[kMaxE + 1];
+};
+
+__device__ __forceinline__ Unit unit_at(const Schedule& S, int u) {
+  Unit x{};
+  if (u < S.totalA) {
+    int e = 0;
+    while (S.a_base[e + 1] <= u) ++e;
+    const int v = u - S.a_base[e];
+    x.down = 0;
+    x.e = e;
+    x.row0 = S.off[e] + (v / S.nA) * kTok;
+    x.nb = v % S.nA;
+    x.ks = 0;
+  } else {
+    const int w = u - S.totalA;
+    int e = 0;
+    while (S.b_base[e + 1] <= w) ++e;
+    const int v = w - S.b_base[e];
+    x.down = 1;
+    x.e = e;
+    x.row0 = S.off[e] + (v / S.nB) * kTok;
+    const int r = v % S.nB;
+    x.nb = r / S.splits;
+    x.ks = r % S.splits;
+  }
+  x.cnt = min(kTok, S.off[x.e + 1] - x.row0);
+  return x;
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    moe_fused_kernel(const __grid_constant__ CUtensorMap tm_w1, const __grid_constant__ CUtensorMap tm_w3,
+                     const __grid_constant__ CUtensorMap tm_w2, const __grid_constant__ CUtensorMap tm_x,
+                     const __grid_constant__ CUtensorMap tm_h, MoeParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
+  __shared__ __align__(8) uint64_t tmem_full, tmem_empty;
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ Schedule S;
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    S.nA = p.hi / 128;
+    S.splits = p.splits;
+    S.nB = p.splits * (p.h / 128);
+    S.a_base[0] = S.b_base[0] = 0;
+    for (int e = 0; e < p.E; ++e) {
+      S.off[e] = p.offsets[e];
+      const int cnt = p.offsets[e + 1] - p.offsets[e];
+      const int tt = (cnt + kTok - 1) / kTok;
+      S.a_base[e + 1] = S.a_base[e] + tt * S.nA;
+      S.b_base[e + 1] = S.b_base[e] + tt * S.nB;
+    }
+    S.off[p.E] = p.offsets[p.E];
+    S.totalA = S.a_base[p.E];
+    S.total = S.totalA + S.b_base[p.E];
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&tmem_full, 1);
+    mbar_init(&tmem_empty, 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_w1);
+    tma_prefetch_desc(&tm_w3);
+    tma_prefetch_desc(&tm_w2);
+    tma_prefetch_desc(&tm_x);
+    tma_prefetch_desc(&tm_h);
+  }
+  if (warp == 1) tmem_alloc<512>(&tmem_base_sh);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  const int KBa = p.h / kBK;             // gate/up k-blocks
+  const int KBd = (p.hi / kBK) / p.splits;  // k-blocks per down slice
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      int kbg = 0;
+      for (int u = blockIdx.x; u < S.total; u += gridDim.x) {
+        const Unit x = unit_at(S, u);
+        const int wblk = p.w_index[x.e];
+        const int n_load = (x.cnt + 31) & ~31;
+        if (x.down) {
+          // every gate/up unit of expert e has published its H rows
+          const int need = ((S.off[x.e + 1] - S.off[x.e] + kTok - 1) / kTok) * S.nA;
+          while (ld_acquire(p.done + x.e) < need) {
+          }
+          fence_proxy_async_global();
+        }
+        const int KB = x.down ? KBd : KBa;
+        const int kb0 = x.down ? x.ks * KBd : 0;
+        const uint32_t tx = uint32_t((x.down ? kTileA : 2 * kTileA) + (n_load / 32) * 4096);
+        for (int kb = 0; kb < KB; ++kb, ++kbg) {
+          const int s = kbg % kStages;
+          mbar_wait(&empty_bar[s], ((kbg / kStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full_bar[s], tx);
+          uint8_t* sa = smem + s * kStageBytes;
+          uint8_t* sb = sa + 2 * kTileA;
+          const int kc = (kb0 + kb) * kBK;
+          if (x.down) {
+            tma_load_3d(sa, &tm_w2, &full_bar[s], kc, x.nb * 128, wblk);
+            for (int i = 0; i < n_load / 32; ++i) tma_load_2d(sb + i * 4096, &tm_h, &full_bar[s], kc, x.row0 + i * 32);
+          } else {
+            tma_load_3d(sa, &tm_w1, &full_bar[s], kc, x.nb * 128, wblk);
+            tma_load_3d(sa + kTileA, &tm_w3, &full_bar[s], kc, x.nb * 128, wblk);
+            for (int i = 0; i < n_load / 32; ++i) tma_load_2d(sb + i * 4096, &tm_x, &full_bar[s], kc, x.row0 + i * 32);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      int kbg = 0, it = 0;
+      for (int u = blockIdx.x; u < S.total; u += gridDim.x, ++it) {
+        const Unit x = unit_at(S, u);
+        const int n_pad = (x.cnt + 15) & ~15;
+        const uint32_t idesc = make_idesc_bf16(128, n_pad);
+        const int KB = x.down ? KBd : KBa;
+        // the epilogue has drained the accumulators of the previous unit
+        mbar_wait(&tmem_empty, (it & 1) ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < KB; ++kb, ++kbg) {
+          const int s = kbg % kStages;
+          mbar_wait(&full_bar[s], (kbg / kStages) & 1);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + s * kStageBytes);
+          const uint64_t ad = make_sdesc_sw128(a_addr, 16, 1024);
+          const uint64_t au = ad + uint64_t(kTileA >> 4);
+          const uint64_t bd = make_sdesc_sw128(a_addr + 2 * kTileA, 16, 1024);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+            const uint64_t ko = uint64_t((k * 32) >> 4);
+            umma_bf16(tmem, ad + ko, bd + ko, idesc, acc);
+            if (!x.down) umma_bf16(tmem + 256, au + ko, bd + ko, idesc, acc);
+          }
+          umma_commit(&empty_bar[s]);
+        }
+        umma_commit(&tmem_full);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;
+    const int row = q * 32 + lane;  // weight row within the 128-row tile
+    const uint32_t trow = tmem + (uint32_t(q * 32) << 16);
+    int it = 0;
+    for (int u = blockIdx.x; u < S.total; u += gridDim.x, ++it) {
+      const Unit x = unit_at(S, u);
+      const int n_pad = (x.cnt + 15) & ~15;
+      mbar_wait(&tmem_full, it & 1);
+      tc_fence_after();
+      if (!x.down) {
+        const int n = x.nb * 128 + row;  // intermediate feature
+        for (int c0 = 0; c0 < n_pad; c0 += 32) {
+          uint32_t g[32], v[32];
+          tmem_ld32(trow + c0, g);
+          tmem_ld32(trow + 256 + c0, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j < x.cnt) {
+              const float gv = __uint_as_float(g[j]);
+              p.hbuf[size_t(x.row0 + c0 + j) * p.hi + n] = f2bf(gv / (1.0f + __expf(-gv)) * __uint_as_float(v[j]));
+            }
+        }
+        __threadfence();  // release this unit's H rows before the count
+      } else {
+        const int n = x.nb * 128 + row;  // output feature
+        float* y = p.y + size_t(x.ks) * p.y_stride;
+        for (int c0 = 0; c0 < n_pad; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(trow + c0, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j < x.cnt) y[size_t(x.row0 + c0 + j) * p.h + n] = __uint_as_float(r[j]);
+        }
+      }
+      tc_fence_before();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (warp == 2 && lane == 0) {
+        if (!x.down) {
+          __threadfence();
+          atomicAdd(p.done + x.e, 1);
+        }
+        mbar_arrive(&tmem_empty);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+}  // namespace
+
+// Down-projection K splits for a launch: more, smaller down units make the
+// round-robin unit list end on a fuller last round; each extra split costs
+// one more fp32 partial write + read in the combine. Override with
+// SMO_MOE_SPLITS (1, 2 or 4) for A/B runs.
+int pick_moe_splits(int rows, int h, int hi, int E, int max_splits) {
+  const char* env = std::getenv("SMO_MOE_SPLITS");
+  int forced = env ? std::atoi(env) : 0;
+  auto ok = [&](int sp) { return sp <= max_splits && (hi / kBK) % sp == 0; };
+  if (forced > 0 && ok(forced)) return forced;
+  const double G = sm_count();
+  const double tiles = std::max(1.0, std::ceil(double(rows) / E / kTok));  // token tiles per expert (even routing)
+  const double W = 3.0 * h * hi * 2.0 * E * tiles;                          // weight bytes streamed
+  int best = 1;
+  double best_t = 1e300;
+  for (int sp : {1, 2, 4}) {
+    if (!ok(sp)) continue;
+    const double units = E * tiles * (hi / 128 + double(h / 128) * sp);
+    const double t = std::ceil(units / G) * (W / units) * (1.0 + (sp - 1) * double(rows) * h * 8.0 / W);
+    if (t < best_t * 0.999) {
+      best_t = t;
+      best = sp;
+    }
+  }
+  return best;
+}
+
+// Expert block of one layer: H = SwiGLU(x_perm W1^T, x_perm W3^T) per expert,
+// sum_s y[s] = H W2^T (K split in `splits` slices; 0 = pick_moe_splits;
+// returned). Callers that must reproduce another launch bit for bit (expert
+// parallelism vs one GPU) pass the same explicit splits. x_perm bf16
+// [rows, h] grouped by offsets [E+1]; pool blocks [W1 | W3 | W2]
+// (w_block_stride bytes apart), w_index [E]; y has room for max_splits
+// slices of [rows, h]; done: >= E ints of scratch (zeroed here).
+int moe_launch(const void* x_perm, int rows, int h, int hi, int E, const int32_t* offsets, const void* pool,
+               uint64_t w_block_stride, int pool_blocks, const int32_t* w_index, void* hbuf, float* y, int splits,
+               int max_splits, int* done, cudaStream_t st) {
+  SMO_REQUIRE(x_perm && offsets && pool && w_index && hbuf && y && done, "moe: null pointer");
+  SMO_REQUIRE(E >= 1 && E <= kMaxE, "moe: 1 <= n_expert <= 64");
+  SMO_REQUIRE(h % 128 == 0 && hi % 128 == 0, "moe: h and h_i must be multiples of 128");
+  SMO_REQUIRE(rows > 0 && max_splits >= 1, "moe: no rows");
+  if (splits <= 0) splits = pick_moe_splits(rows, h, hi, E, max_splits);
+  SMO_REQUIRE(splits <= max_splits && (hi / kBK) % splits == 0, "moe: bad down split");
+  const size_t wb = size_t(hi) * h * 2;  // one matrix of a block
+  CUtensorMap t1, t3, t2, tx, th;
+  {
+    uint64_t dims[3] = {uint64_t(h), uint64_t(hi), uint64_t(pool_blocks)};
+    uint64_t strides[2] = {uint64_t(h) * 2, w_block_stride};
+    uint32_t box[3] = {uint32_t(kBK), 128, 1};
+    make_tmap_bf16(&t1, pool, 3, dims, strides, box, true);
+    make_tmap_bf16(&t3, reinterpret_cast<const uint8_t*>(pool) + wb, 3, dims, strides, box, true);
+  }
+  {
+    uint64_t dims[3] = {uint64_t(hi), uint64_t(h), uint64_t(pool_blocks)};
+    uint64_t strides[2] = {uint64_t(hi) * 2, w_block_stride};
+    uint32_t box[3] = {uint32_t(kBK), 128, 1};
+    make_tmap_bf16(&t2, reinterpret_cast<const uint8_t*>(pool) + 2 * wb, 3, dims, strides, box, true);
+  }
+  {
+    uint64_t dims[2] = {uint64_t(h), uint64_t(rows)};
+    uint64_t strides[1] = {uint64_t(h) * 2};
+    uint32_t box[2] = {uint32_t(kBK), 32};
+    make_tmap_bf16(&tx, x_perm, 2, dims, strides, box, true);
+  }
+  {
+    uint64_t dims[2] = {uint64_t(hi), uint64_t(rows)};
+    uint64_t strides[1] = {uint64_t(hi) * 2};
+    uint32_t box[2] = {uint32_t(kBK), 32};
+    make_tmap_bf16(&th, hbuf, 2, dims, strides, box, true);
+  }
+  MoeParams p{};
+  p.h = h;
+  p.hi = hi;
+  p.E = E;
+  p.offsets = offsets;
+  p.w_index = w_index;
+  p.hbuf = reinterpret_cast<uint16_t*>(hbuf);
+  p.y = y;
+  p.y_stride = size_t(rows) * h;
+  p.splits = splits;
+  p.done = done;
+  const size_t smem = size_t(kStages) * kStageBytes + 1024;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SMO_CUDA_CHECK(cudaFuncSetAttribute(moe_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr_set = true;
+  }
+  SMO_CUDA_CHECK(cudaMemsetAsync(done, 0, size_t(E) * sizeof(int), st));
+  // one CTA per SM, co-resident (cooperative): down units wait on gate/up
+  // units of other CTAs
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(sm_count()));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SMO_CUDA_CHECK(cudaLaunchKernelEx(&cfg, moe_fused_kernel, t1, t3, t2, tx, th, p));
+  count_launch();
+  return splits;
+}
+
+}  // namespace smo

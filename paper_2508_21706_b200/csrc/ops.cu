@@ -146,15 +146,26 @@ __global__ void gather_rows_kernel(const uint16_t* __restrict__ x, const int32_t
   for (int c = threadIdx.x; c < h / 8; c += blockDim.x) d[c] = s[c];
 }
 
+// splits > 1: the down projection arrives as K slices y[s] (moe_tc.cu,
+// split_stride elements apart), summed in slice order before the weighting.
 __global__ void combine_kernel(const float* __restrict__ y, const int32_t* __restrict__ pos,
-                               const float* __restrict__ w, int T, int k, int h, float* __restrict__ res) {
+                               const float* __restrict__ w, int T, int k, int h, float* __restrict__ res,
+                               int splits, size_t split_stride) {
   const int t = blockIdx.x;
   for (int c = threadIdx.x * 4; c < h; c += blockDim.x * 4) {
     float4 acc = *reinterpret_cast<float4*>(res + size_t(t) * h + c);
     float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int j = 0; j < k; ++j) {
       const float wj = w[size_t(t) * k + j];
-      const float4 v = *reinterpret_cast<const float4*>(y + size_t(pos[size_t(t) * k + j]) * h + c);
+      const size_t at = size_t(pos[size_t(t) * k + j]) * h + c;
+      float4 v = *reinterpret_cast<const float4*>(y + at);
+      for (int s = 1; s < splits; ++s) {
+        const float4 v2 = *reinterpret_cast<const float4*>(y + size_t(s) * split_stride + at);
+        v.x += v2.x;
+        v.y += v2.y;
+        v.z += v2.z;
+        v.w += v2.w;
+      }
       sum.x = __fmaf_rn(wj, v.x, sum.x);
       sum.y = __fmaf_rn(wj, v.y, sum.y);
       sum.z = __fmaf_rn(wj, v.z, sum.z);
@@ -510,11 +521,11 @@ void permute(const int32_t* ids, int T, int k, int E, const void* x, int h, int3
 }
 
 void unpermute_combine(const float* y, const int32_t* pos, const float* w, int T, int k, int h, float* res,
-                       cudaStream_t st) {
+                       cudaStream_t st, int splits, size_t split_stride) {
   SMO_REQUIRE(y && pos && w && res, "combine: null pointer");
   SMO_REQUIRE(h % 4 == 0, "combine: h must be a multiple of 4");
   if (T <= 0) return;
-  combine_kernel<<<T, 256, 0, st>>>(y, pos, w, T, k, h, res);
+  combine_kernel<<<T, 256, 0, st>>>(y, pos, w, T, k, h, res, std::max(1, splits), split_stride);
   count_launch();
   SMO_CUDA_CHECK(cudaGetLastError());
 }

@@ -100,6 +100,27 @@ def cpu_verify_attention(q, k_cache, v_cache, mask, prefix_len, threads: int = 0
     return out
 
 
+def moe_experts(x_perm, offsets, pool, *, h: int, h_i: int, n_expert: int, w_block_stride: int,
+                w_pool_blocks: int, w_index=None, splits: int = 0):
+    """K4-MoE (one persistent kernel): x_perm bf16 [rows, h] grouped by
+    offsets int32 [E+1]; pool = base of [W1 | W3 | W2] blocks. Returns
+    (h_out bf16 [rows, h_i], y f32 [S, rows, h]); the down projection is
+    y.sum(0) taken in slice order (S = splits, 0 = the kernel's choice)."""
+    _req(x_perm, _BF16, "x_perm")
+    rows = x_perm.shape[0]
+    dev = x_perm.device
+    if w_index is None:
+        w_index = torch.arange(n_expert, dtype=torch.int32, device=dev)
+    hout = torch.empty((rows, h_i), dtype=_BF16, device=dev)
+    y = torch.empty((splits or 4, rows, h), dtype=torch.float32, device=dev)
+    scratch = torch.empty(64, dtype=torch.int32, device=dev)
+    used = C.c_int32(0)
+    L.check(L.load().smo_moe_experts(_p(x_perm), rows, h, h_i, n_expert, _p(offsets), _p(pool), w_block_stride,
+                                     w_pool_blocks, _p(w_index), _p(hout), _p(y), splits, C.byref(used), _p(scratch),
+                                     _stream()))
+    return hout, y[:used.value]
+
+
 def router_topk(x, w_router, k: int, want_logits: bool = False):
     """K2. x [T, h] bf16, w_router [E, h] bf16 -> ids int32 [T,k], weights f32 [T,k] (, logits)."""
     _req(x, _BF16, "x")

@@ -91,6 +91,49 @@ def test_grouped_swiglu_and_down_vs_torch(cuda, T, E, k, h, hi):
         assert dy <= 1e-4 * max(1.0, Y.abs().max().item()), (e, dy)
 
 
+@pytest.mark.parametrize("T,E,k,h,hi,splits", [(20, 8, 2, 512, 1792, 0), (288, 8, 2, 1024, 512, 4),
+                                                (48, 64, 6, 512, 384, 2), (700, 4, 2, 256, 256, 1),
+                                                (288, 8, 2, 512, 1792, 0)])
+def test_fused_moe_kernel_vs_torch(cuda, T, E, k, h, hi, splits):
+    """K4-MoE: gate/up + SwiGLU + down of every expert in one persistent
+    kernel (moe_tc.cu) == the per-expert torch reference; the down projection
+    arrives as two K halves y0 + y1. T=700 x top-2 over 4 experts gives
+    several 256-row token tiles per expert; splits 1/2/4 cut the down K."""
+    import torch
+    from paper_2508_21706_b200 import ops
+    g = torch.Generator(device=cuda).manual_seed(E * 100 + T + 1)
+    x = _bf16_rand(torch, (T, h), g)
+    blk = 3 * h * hi
+    pool = _bf16_rand(torch, (E * blk,), g, scale=math.sqrt(3.0 / h))
+    logits = torch.randn((T, E), generator=g, device=cuda)
+    ids = torch.topk(logits, k, dim=1).indices.to(torch.int32).contiguous()
+    off, perm, pos, xp = ops.permute(ids, E, x)
+    widx = torch.randperm(E, generator=torch.Generator().manual_seed(T)).to(torch.int32).to(cuda)
+    hbuf, ys = ops.moe_experts(xp, off, pool, h=h, h_i=hi, n_expert=E, w_block_stride=blk * 2,
+                               w_pool_blocks=E, w_index=widx, splits=splits)
+    assert ys.shape[0] == (splits or ys.shape[0])
+    ysum = ys[0].clone()
+    for s_ in range(1, ys.shape[0]):
+        ysum += ys[s_]
+    offs = off.cpu().tolist()
+    for e in range(E):
+        a, b = offs[e], offs[e + 1]
+        if a == b:
+            continue
+        base = int(widx[e]) * blk
+        w1 = pool[base:base + hi * h].view(hi, h).float()
+        w3 = pool[base + hi * h:base + 2 * hi * h].view(hi, h).float()
+        w2 = pool[base + 2 * hi * h:base + blk].view(h, hi).float()
+        X = xp[a:b].float()
+        gg, uu = X @ w1.T, X @ w3.T
+        H = (gg * torch.sigmoid(gg) * uu).to(torch.bfloat16)
+        dh = (hbuf[a:b].float() - H.float()).abs().max().item()
+        assert dh <= 2 ** -7 * max(1.0, H.float().abs().max().item()), (e, dh)
+        Y = hbuf[a:b].float() @ w2.T
+        dy = (ysum[a:b] - Y).abs().max().item()
+        assert dy <= 1e-4 * max(1.0, Y.abs().max().item()), (e, dy)
+
+
 # ---------------------------------------------------------------- K2 / K3
 @pytest.mark.parametrize("T,h,E,k", [(20, 512, 8, 2), (288, 4096, 8, 2), (64, 2048, 64, 6)])
 def test_router_bit_exact_vs_oracle(cuda, oracle, T, h, E, k):

@@ -78,11 +78,22 @@ def moe(T=288, h=4096, hi=14336, E=8, k=2, split=0):
     def down():
         ops.gemm(hbuf, pool[2 * hi * h:], epilogue=L.EPI_F32, out=y, row_offsets=off, groups=E,
                  w_block_stride=blk * 2, w_pool_blocks=E, N=h, max_rows_per_group=T, split_k=split)
+    y4 = torch.empty((4, T * k, h), dtype=torch.float32, device=dev)
+    scratch = torch.empty(64, dtype=torch.int32, device=dev)
+    widx = torch.arange(E, dtype=torch.int32, device=dev)
+
+    def fused():
+        L.check(L.load().smo_moe_experts(xp.data_ptr(), T * k, h, hi, E, off.data_ptr(), pool.data_ptr(), blk * 2, E,
+                                         widx.data_ptr(), hbuf.data_ptr(), y4.data_ptr(), split, None,
+                                         scratch.data_ptr(), torch.cuda.current_stream().cuda_stream))
     r = []
-    for nm, fn, wb in (("swiglu gate/up", up, 2 * E * hi * h * 2), ("down", down, E * h * hi * 2)):
+    for nm, fn, wb in (("swiglu gate/up", up, 2 * E * hi * h * 2), ("down", down, E * h * hi * 2),
+                       ("fused moe (gate/up + down, one kernel)", fused, 3 * E * hi * h * 2)):
+        if split and "fused" not in nm:
+            continue
         t = timeit(fn)
         r.append({"kernel": f"K4 grouped {nm}" + (f" split {split}" if split else ""), "T": T, "E": E, "us": t * 1e6, "GBs": wb / t / 1e9,
-                  "frac": wb / t / 1e9 / PEAK, "TFLOPs": (2 if "gate" in nm else 1) * 2 * T * k * h * hi / t / 1e12})
+                  "frac": wb / t / 1e9 / PEAK, "TFLOPs": (3 if "fused" in nm else 2 if "gate" in nm else 1) * 2 * T * k * h * hi / t / 1e12})
     return r
 
 
@@ -105,7 +116,7 @@ def main():
         res.append(gemm(288, 4096, 32000, L.EPI_ARGMAX, name="lm-head argmax"))
         res += moe()
         if "--splits" in sys.argv:
-            for sp in (1, 2, 4, 8):
+            for sp in (1, 2, 4):
                 res += moe(split=sp)
     for r in res:
         print(json.dumps({k: (round(v, 3) if isinstance(v, float) else v) for k, v in r.items()}))
