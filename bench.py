@@ -299,12 +299,13 @@ def run_reference(args):
 
 
 def moe_traffic_per_layer():
-    """dram__bytes_read+write of the K4 gate/up + down launches of one layer,
-    from the committed ncu --set full capture (profiles/r01b_traffic.json)."""
-    p = os.path.join(ROOT, "profiles", "r01b_traffic.json")
+    """dram__bytes_read+write of one layer's expert block (the fused K4-MoE
+    launch) from the committed ncu --set full capture of the bench step
+    (profiles/r01c_traffic.json)."""
+    p = os.path.join(ROOT, "profiles", "r01c_traffic.json")
     try:
-        k = json.load(open(p))["kernels"]
-        return sum(k[n]["dram_read_bytes"] + k[n]["dram_write_bytes"] for n in ("K4_swiglu_gate_up", "K4_down"))
+        k = json.load(open(p))["kernels"]["K4_moe_fused"]
+        return k["dram_read_bytes"] + k["dram_write_bytes"]
     except Exception:
         return None
 
@@ -507,11 +508,12 @@ def run_ours(args):
         "committed_tokens_per_s_model": world * b * geometric_alpha(0.8, args.k) / t_step,
         "h2d": {"achieved_gbs": h2d_bytes / t_step / 1e9, "link_peak_gbs": h2d_peak,
                 "bytes_per_step": h2d_bytes, "copy_engine_busy_s": stages["h2d_transfer"]},
-        "roofline": {"bound": "hbm", "kernel": "K4 grouped SwiGLU gate/up + down (+combine), per step",
+        "roofline": {"bound": "hbm", "kernel": "K4-MoE fused expert block (gate/up + SwiGLU + down, one "
+                     "persistent launch per layer) + combine, per step",
                      "achieved": moe_bytes_step / moe_t / 1e9 if moe_t > 0 else None, "peak": pk["hbm_gbs"],
                      "unit": "GB/s", "frac": (moe_bytes_step / moe_t / 1e9) / pk["hbm_gbs"] if moe_t > 0 else None,
-                     "traffic": moe_traffic_per_layer() if (args.model == "mixtral-8x7b" and ep_size == 1) else None, "traffic_unit": "dram bytes per layer (gate/up + down "
-                     "launches, ncu profiles/r01b_traffic.json); algorithmic per layer = " + str(
+                     "traffic": moe_traffic_per_layer() if (args.model == "mixtral-8x7b" and ep_size == 1) else None, "traffic_unit": "dram bytes per layer (the fused expert "
+                     "launch, ncu profiles/r01c_traffic.json); algorithmic per layer = " + str(
                          (shape.n_expert // ep_size) * shape.expert_bytes), "peak_kind": pk_kind},
         "step_roofline": {"bound": roof["bound"], "t_roof_s": roof["t_roof_s"], "t_meas_s": t_step,
                           "frac": roof["t_roof_s"] / t_step, "h2d_peak_gbs": h2d_peak,

@@ -41,9 +41,7 @@ namespace {
 constexpr int kThreads = 192;
 constexpr int kBK = 64;
 constexpr int kTileA = 128 * kBK * 2;                  // weight tile per k-block (16 KB)
-constexpr int kTok = 256;                              // token tile (gate + up = 512 TMEM columns)
-constexpr int kStageBytes = 2 * kTileA + kTok * 128;   // 64 KB
-constexpr int kStages = 3;
+constexpr int kTok = 256;                              // largest token tile (gate + up = 512 TMEM columns)
 constexpr int kMaxE = 64;
 
 struct MoeParams {
@@ -64,7 +62,7 @@ struct Unit {
 struct Schedule {
   int nA, nB;           // units per token tile: hi/128 gate/up, splits*h/128 down
   int totalA, total;
-  int splits;
+  int splits, tok;      // down K slices, token tile of this variant
   int a_base[kMaxE + 1], b_base[kMaxE + 1];
   int off[kMaxE + 1];
 };
@@ -77,7 +75,7 @@ __device__ __forceinline__ Unit unit_at(const Schedule& S, int u) {
     const int v = u - S.a_base[e];
     x.down = 0;
     x.e = e;
-    x.row0 = S.off[e] + (v / S.nA) * kTok;
+    x.row0 = S.off[e] + (v / S.nA) * S.tok;
     x.nb = v % S.nA;
     x.ks = 0;
   } else {
@@ -87,12 +85,12 @@ __device__ __forceinline__ Unit unit_at(const Schedule& S, int u) {
     const int v = w - S.b_base[e];
     x.down = 1;
     x.e = e;
-    x.row0 = S.off[e] + (v / S.nB) * kTok;
+    x.row0 = S.off[e] + (v / S.nB) * S.tok;
     const int r = v % S.nB;
     x.nb = r / S.splits;
     x.ks = r % S.splits;
   }
-  x.cnt = min(kTok, S.off[x.e + 1] - x.row0);
+  x.cnt = min(S.tok, S.off[x.e + 1] - x.row0);
   return x;
 }
 
@@ -105,12 +103,18 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// kSub k-blocks of 64 per pipeline stage (kSub = 2: each weight row is read
+// 256 contiguous bytes at a time), kTokT-row token tiles, kStagesT stages.
+template <int kSub, int kTokT, int kStagesT>
 __global__ void __launch_bounds__(kThreads, 1)
     moe_fused_kernel(const __grid_constant__ CUtensorMap tm_w1, const __grid_constant__ CUtensorMap tm_w3,
                      const __grid_constant__ CUtensorMap tm_w2, const __grid_constant__ CUtensorMap tm_x,
                      const __grid_constant__ CUtensorMap tm_h, MoeParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  constexpr int kStages = kStagesT;
+  constexpr int kXBytes = kTokT * 128;                              // one k-block of token rows
+  constexpr int kStageBytes = kSub * (2 * kTileA + kXBytes);
   __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
   __shared__ __align__(8) uint64_t tmem_full, tmem_empty;
   __shared__ uint32_t tmem_base_sh;
@@ -120,12 +124,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     S.nA = p.hi / 128;
     S.splits = p.splits;
+    S.tok = kTokT;
     S.nB = p.splits * (p.h / 128);
     S.a_base[0] = S.b_base[0] = 0;
     for (int e = 0; e < p.E; ++e) {
       S.off[e] = p.offsets[e];
       const int cnt = p.offsets[e + 1] - p.offsets[e];
-      const int tt = (cnt + kTok - 1) / kTok;
+      const int tt = (cnt + kTokT - 1) / kTokT;
       S.a_base[e + 1] = S.a_base[e] + tt * S.nA;
       S.b_base[e + 1] = S.b_base[e] + tt * S.nB;
     }
@@ -150,8 +155,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
-  const int KBa = p.h / kBK;             // gate/up k-blocks
-  const int KBd = (p.hi / kBK) / p.splits;  // k-blocks per down slice
+  const int KBa = p.h / (kBK * kSub);                 // gate/up stages per unit
+  const int KBd = (p.hi / (kBK * kSub)) / p.splits;   // stages per down slice
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -163,28 +168,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n_load = (x.cnt + 31) & ~31;
         if (x.down) {
           // every gate/up unit of expert e has published its H rows
-          const int need = ((S.off[x.e + 1] - S.off[x.e] + kTok - 1) / kTok) * S.nA;
+          const int need = ((S.off[x.e + 1] - S.off[x.e] + kTokT - 1) / kTokT) * S.nA;
           while (ld_acquire(p.done + x.e) < need) {
           }
           fence_proxy_async_global();
         }
         const int KB = x.down ? KBd : KBa;
         const int kb0 = x.down ? x.ks * KBd : 0;
-        const uint32_t tx = uint32_t((x.down ? kTileA : 2 * kTileA) + (n_load / 32) * 4096);
+        const uint32_t tx = uint32_t(kSub * ((x.down ? kTileA : 2 * kTileA) + (n_load / 32) * 4096));
         for (int kb = 0; kb < KB; ++kb, ++kbg) {
           const int s = kbg % kStages;
           mbar_wait(&empty_bar[s], ((kbg / kStages) & 1) ^ 1);
           mbar_arrive_expect_tx(&full_bar[s], tx);
           uint8_t* sa = smem + s * kStageBytes;
-          uint8_t* sb = sa + 2 * kTileA;
-          const int kc = (kb0 + kb) * kBK;
-          if (x.down) {
-            tma_load_3d(sa, &tm_w2, &full_bar[s], kc, x.nb * 128, wblk);
-            for (int i = 0; i < n_load / 32; ++i) tma_load_2d(sb + i * 4096, &tm_h, &full_bar[s], kc, x.row0 + i * 32);
-          } else {
-            tma_load_3d(sa, &tm_w1, &full_bar[s], kc, x.nb * 128, wblk);
-            tma_load_3d(sa + kTileA, &tm_w3, &full_bar[s], kc, x.nb * 128, wblk);
-            for (int i = 0; i < n_load / 32; ++i) tma_load_2d(sb + i * 4096, &tm_x, &full_bar[s], kc, x.row0 + i * 32);
+          // stage layout: W1 (or W2) sub-tiles, W3 sub-tiles, token sub-tiles
+#pragma unroll
+          for (int j = 0; j < kSub; ++j) {
+            const int kc = ((kb0 + kb) * kSub + j) * kBK;
+            uint8_t* sb = sa + 2 * kSub * kTileA + j * kXBytes;
+            if (x.down) {
+              tma_load_3d(sa + j * kTileA, &tm_w2, &full_bar[s], kc, x.nb * 128, wblk);
+              for (int i = 0; i < n_load / 32; ++i) tma_load_2d(sb + i * 4096, &tm_h, &full_bar[s], kc, x.row0 + i * 32);
+            } else {
+              tma_load_3d(sa + j * kTileA, &tm_w1, &full_bar[s], kc, x.nb * 128, wblk);
+              tma_load_3d(sa + (kSub + j) * kTileA, &tm_w3, &full_bar[s], kc, x.nb * 128, wblk);
+              for (int i = 0; i < n_load / 32; ++i) tma_load_2d(sb + i * 4096, &tm_x, &full_bar[s], kc, x.row0 + i * 32);
+            }
           }
         }
       }
@@ -206,15 +215,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&full_bar[s], (kbg / kStages) & 1);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + s * kStageBytes);
-          const uint64_t ad = make_sdesc_sw128(a_addr, 16, 1024);
-          const uint64_t au = ad + uint64_t(kTileA >> 4);
-          const uint64_t bd = make_sdesc_sw128(a_addr + 2 * kTileA, 16, 1024);
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
-            const uint64_t ko = uint64_t((k * 32) >> 4);
-            umma_bf16(tmem, ad + ko, bd + ko, idesc, acc);
-            if (!x.down) umma_bf16(tmem + 256, au + ko, bd + ko, idesc, acc);
+          for (int j = 0; j < kSub; ++j) {
+            const uint64_t ad = make_sdesc_sw128(a_addr + j * kTileA, 16, 1024);
+            const uint64_t au = make_sdesc_sw128(a_addr + (kSub + j) * kTileA, 16, 1024);
+            const uint64_t bd = make_sdesc_sw128(a_addr + 2 * kSub * kTileA + j * kXBytes, 16, 1024);
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint32_t acc = (kb > 0 || j > 0 || k > 0) ? 1u : 0u;
+              const uint64_t ko = uint64_t((k * 32) >> 4);
+              umma_bf16(tmem, ad + ko, bd + ko, idesc, acc);
+              if (!x.down) umma_bf16(tmem + 256, au + ko, bd + ko, idesc, acc);
+            }
           }
           umma_commit(&empty_bar[s]);
         }
@@ -288,30 +300,22 @@ int sm_count() {
 
 }  // namespace
 
-// Down-projection K splits for a launch: more, smaller down units make the
-// round-robin unit list end on a fuller last round; each extra split costs
-// one more fp32 partial write + read in the combine. Override with
-// SMO_MOE_SPLITS (1, 2 or 4) for A/B runs.
+// Down-projection K splits for a launch: 1 unless the unit list would not
+// cover the SMs once (small models), then the smallest S that does. Measured
+// at config 2 (round 1): S = 1 / 2 / 4 -> 516 / 520 / 524 us — the grid is
+// already 94 % busy (ncu sm__cycles_active), so finer down units buy less
+// than their extra fp32 partial traffic. SMO_MOE_SPLITS overrides (A/B runs).
 int pick_moe_splits(int rows, int h, int hi, int E, int max_splits) {
   const char* env = std::getenv("SMO_MOE_SPLITS");
-  int forced = env ? std::atoi(env) : 0;
+  const int forced = env ? std::atoi(env) : 0;
   auto ok = [&](int sp) { return sp <= max_splits && (hi / kBK) % sp == 0; };
   if (forced > 0 && ok(forced)) return forced;
-  const double G = sm_count();
   const double tiles = std::max(1.0, std::ceil(double(rows) / E / kTok));  // token tiles per expert (even routing)
-  const double W = 3.0 * h * hi * 2.0 * E * tiles;                          // weight bytes streamed
-  int best = 1;
-  double best_t = 1e300;
   for (int sp : {1, 2, 4}) {
-    if (!ok(sp)) continue;
     const double units = E * tiles * (hi / 128 + double(h / 128) * sp);
-    const double t = std::ceil(units / G) * (W / units) * (1.0 + (sp - 1) * double(rows) * h * 8.0 / W);
-    if (t < best_t * 0.999) {
-      best_t = t;
-      best = sp;
-    }
+    if (ok(sp) && units >= sm_count()) return sp;
   }
-  return best;
+  return ok(2) ? 2 : 1;
 }
 
 // Expert block of one layer: H = SwiGLU(x_perm W1^T, x_perm W3^T) per expert,
@@ -368,10 +372,14 @@ int moe_launch(const void* x_perm, int rows, int h, int hi, int E, const int32_t
   p.y_stride = size_t(rows) * h;
   p.splits = splits;
   p.done = done;
-  const size_t smem = size_t(kStages) * kStageBytes + 1024;
+  // one k-block (64) per stage, 256-row token tiles, 3 stages of 64 KB. (Two
+  // k-blocks per stage — 256 contiguous bytes per weight row per request,
+  // 128-row tiles, 2 stages — measured 510 vs 516 us at config 2: not kept.)
+  auto kern = moe_fused_kernel<1, kTok, 3>;
+  const size_t smem = size_t(3) * (2 * kTileA + kTok * 128) + 1024;
   static bool attr_set = false;
   if (!attr_set) {
-    SMO_CUDA_CHECK(cudaFuncSetAttribute(moe_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    SMO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr_set = true;
   }
   SMO_CUDA_CHECK(cudaMemsetAsync(done, 0, size_t(E) * sizeof(int), st));
@@ -387,7 +395,7 @@ int moe_launch(const void* x_perm, int rows, int h, int hi, int E, const int32_t
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  SMO_CUDA_CHECK(cudaLaunchKernelEx(&cfg, moe_fused_kernel, t1, t3, t2, tx, th, p));
+  SMO_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, t1, t3, t2, tx, th, p));
   count_launch();
   return splits;
 }

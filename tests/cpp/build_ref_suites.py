@@ -65,13 +65,14 @@ if __name__ == "__main__":
 
 
 OWN_GPU_SUITES = ["test_verify_engine"]
+OWN_CPU_SUITES = ["test_profile_csv"]
 
 
 def build_own() -> list[str]:
-    """This repository's own C++ GPU suites (need only the image's toolchain)."""
+    """This repository's own C++ suites (need only the image's toolchain)."""
     os.makedirs(OUT, exist_ok=True)
     built = []
-    for name in OWN_GPU_SUITES:
+    for name in OWN_GPU_SUITES + OWN_CPU_SUITES:
         src = os.path.join(ROOT, "tests", "cpp", name + ".cpp")
         out = os.path.join(OUT, name)
         inc = os.path.join(ROOT, "include")
@@ -80,6 +81,6 @@ def build_own() -> list[str]:
         if not os.path.exists(out) or os.path.getmtime(out) < max(os.path.getmtime(d) for d in deps):
             if not os.path.isdir(JSON):
                 continue
-            _compile(src, out, inc, link_lib=True)
+            _compile(src, out, inc, link_lib=name in OWN_GPU_SUITES)
         built.append(out)
     return built

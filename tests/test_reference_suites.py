@@ -78,3 +78,14 @@ def test_cpp_verify_engine_planner_loop(cuda):
     r = subprocess.run([path], capture_output=True, text=True, timeout=900, cwd=os.path.dirname(path))
     m = SUMMARY.search(r.stdout)
     assert r.returncode == 0 and m and m.group(3) == "0", r.stdout + r.stderr
+
+
+def test_cpp_profile_csv_ingest():
+    """CPU: ProfileSample CSV write/read (the ingest SPEC.md:592 promises) round
+    trips exactly and fits the same LatencyModel."""
+    B.build_own()
+    path = os.path.join(B.OUT, "test_profile_csv")
+    assert os.path.exists(path), "build/refsuites/test_profile_csv missing"
+    r = subprocess.run([path], capture_output=True, text=True, timeout=300, cwd=os.path.dirname(path))
+    m = SUMMARY.search(r.stdout)
+    assert r.returncode == 0 and m and m.group(3) == "0", r.stdout + r.stderr
