@@ -363,6 +363,12 @@ smo_status smo_engine_prefill(smo_engine* e, const int32_t* tokens, const int32_
                               int32_t max_len, int32_t* next_token, smo_stream stream);
 smo_status smo_engine_decode_begin(smo_engine* e, const int32_t* root, const int32_t* kv_len, int32_t b);
 smo_status smo_engine_decode_step(smo_engine* e, int32_t k, const int32_t* drafts, smo_stream stream);
+/* `steps` decode iterations with k drafts from the drafter (asynchronous).
+ * use_graph: the device part of an iteration is captured once into a CUDA
+ * graph and replayed (one launch per iteration; needs a non-default stream,
+ * GPU attention, LARGE_BATCH streaming, no expert parallelism). K/V pages
+ * for the whole run are mapped before it starts.                           */
+smo_status smo_engine_decode_run(smo_engine* e, int32_t k, int32_t steps, int32_t use_graph, smo_stream stream);
 /* Measured duration (s) of each drafter step of the last decode step
  * (DRAFT_GPU_STEP events, pipeline.hpp:208-253); *steps = k+1 (0: no drafter). */
 smo_status smo_engine_draft_times(smo_engine* e, double* out, size_t n, int32_t* steps);

@@ -210,6 +210,7 @@ struct Engine {
     for (auto e : ev) cudaEventDestroy(e);
     for (auto e : draft_ev) cudaEventDestroy(e);
     if (route_ev) cudaEventDestroy(route_ev);
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
     for (auto hb : host_bufs) cudaFreeHost(hb);
     if (h_stage) cudaFreeHost(h_stage);
     if (h_bt) cudaFreeHost(h_bt);
@@ -637,7 +638,9 @@ struct Engine {
   // active (optional, BATCH_ONE): per local expert, 0 = not routed to -> not streamed
   double enqueue_h2d(int l, cudaEvent_t t0, cudaEvent_t t1, const uint8_t* active = nullptr) {
     const int s = l % slots;
-    SMO_CUDA_CHECK(cudaStreamWaitEvent(copy, slot_free[s], 0));
+    // while capturing a graph the first `slots` layers' release events belong
+    // to the previous iteration (outside the graph; replays are serialised)
+    if (!(capturing && l < slots)) SMO_CUDA_CHECK(cudaStreamWaitEvent(copy, slot_free[s], 0));
     if (t0) SMO_CUDA_CHECK(cudaEventRecord(t0, copy));
     double bytes = 0;
     const uint16_t* hb = host_bufs[host_layer(l)];
@@ -1247,6 +1250,15 @@ struct Engine {
       std::memcpy(h_stage, drafts_h, size_t(b) * k * 4);
       SMO_CUDA_CHECK(cudaMemcpyAsync(d_drafts, h_stage, size_t(b) * k * 4, cudaMemcpyHostToDevice, st));
     }
+    decode_device(k, planted, int(kv_bound), st);
+    kv_bound += n;
+  }
+
+  // The device part of a decode step (capturable into a CUDA graph): every
+  // argument is fixed at enqueue time; bound = host bound of kv_len used for
+  // K1 split planning and the drafter's positions.
+  void decode_device(int k, bool planted, int bound, cudaStream_t st) {
+    const int b = dec_b, n = k + 1;
     last_was_decode = true;
     begin_step(st, !batch_one);  // the first layers' experts stream while the drafter runs
     decode_prep(d_root, planted ? d_drafts : nullptr, b, n, d_dec_tok, st);
@@ -1257,14 +1269,79 @@ struct Engine {
     for (int t = 0; dL > 0 && t <= k; ++t) {
       SMO_CUDA_CHECK(cudaEventRecord(draft_ev[size_t(t)], st));
       draft_io(d_dec_tok, d_kvlen, t, b, n, d_dtok, d_dpos, st);
-      draft_forward(b, d_dtok, d_dpos, int(kv_bound) + t, d_dout, st);
+      draft_forward(b, d_dtok, d_dpos, bound + t, d_dout, st);
       if (!planted && t < k) draft_scatter(d_dout, b, n, t, d_dec_tok, st);
     }
     SMO_CUDA_CHECK(cudaEventRecord(ev[3], st));
     if (last_draft_steps > 0) SMO_CUDA_CHECK(cudaEventRecord(draft_ev[size_t(last_draft_steps)], st));
-    verify_core(b, n, d_dec_tok, nullptr, d_kvlen, int(kv_bound), st);
+    verify_core(b, n, d_dec_tok, nullptr, d_kvlen, bound, st);
     decode_commit(d_dec_tok, d_acc, d_bonus, b, n, hist_cap, d_hist, d_hist_n, d_kvlen, d_root, st);
-    kv_bound += n;
+  }
+
+  // `steps` decode iterations with k drafts. graph: the device part of one
+  // iteration is captured once into a CUDA graph (keyed on k, batch and the
+  // kv bound it was planned for) and replayed — one launch per iteration
+  // instead of ~15 per layer. Graph replays on one stream are serialised, so
+  // the cross-iteration slot-release edges hold without the in-graph waits.
+  cudaGraphExec_t graph_exec = nullptr;
+  int graph_k = -1, graph_b = -1;
+  int64_t graph_bound = -1;
+  uint64_t graph_launches = 0;
+  bool capturing = false;
+  void decode_run(int k, int steps, bool graph, cudaStream_t st) {
+    if (!graph) {
+      for (int i = 0; i < steps; ++i) decode_step(k, nullptr, st);
+      return;
+    }
+    const int b = dec_b, n = k + 1;
+    SMO_REQUIRE(b > 0, "decode: call smo_engine_prefill or smo_engine_decode_begin first");
+    SMO_REQUIRE(k >= 0 && n <= maxN, "decode: k + 1 exceeds max_verify");
+    SMO_REQUIRE(k == 0 || dL > 0, "decode: k > 0 needs a drafter (draft_layers)");
+    SMO_REQUIRE(!batch_one && !attn_cpu && !ep_on && !debug,
+                "decode graph: not with BATCH_ONE, CPU attention, expert parallelism or debug snapshots");
+    SMO_REQUIRE(st != nullptr, "decode graph: needs a non-default stream");
+    const int64_t end = kv_bound + int64_t(steps) * n;  // kv bound after the last iteration
+    SMO_REQUIRE(end <= s_max, "decode: KV capacity (max_seq) exhausted");
+    for (int r = 0; r < b; ++r) {  // pages for every iteration of the run, outside the graph
+      bt_ensure(r, end);
+      kv_known[size_t(r)] = end;
+    }
+    bt_sync(st);
+    // one graph serves any run whose positions stay under the bound it was planned for
+    const int64_t plan = std::max<int64_t>(end - n, graph_bound);
+    if (!graph_exec || graph_k != k || graph_b != b || graph_bound < end - n) {
+      if (graph_exec) SMO_CUDA_CHECK(cudaGraphExecDestroy(graph_exec));
+      graph_exec = nullptr;
+      const int64_t bound = std::min<int64_t>(plan, s_max - n);
+      const uint64_t l0 = smo_launch_count();
+      cudaGraph_t g = nullptr;
+      SMO_CUDA_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      capturing = true;
+      try {
+        decode_device(k, false, int(bound), st);
+      } catch (...) {
+        capturing = false;
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      capturing = false;
+      SMO_CUDA_CHECK(cudaStreamEndCapture(st, &g));
+      SMO_CUDA_CHECK(cudaGraphInstantiate(&graph_exec, g, 0));
+      SMO_CUDA_CHECK(cudaGraphDestroy(g));
+      graph_launches = smo_launch_count() - l0;
+      count_launch(-int(graph_launches));  // captured, not launched: counted per replay below
+      graph_k = k;
+      graph_b = b;
+      graph_bound = bound;
+    }
+    for (int i = 0; i < steps; ++i) {
+      SMO_CUDA_CHECK(cudaGraphLaunch(graph_exec, st));
+      count_launch(int(graph_launches));
+    }
+    last_was_decode = true;
+    last_draft_steps = dL > 0 ? k + 1 : 0;
+    kv_bound = end;
   }
 
   // durations (s) of the drafter steps of the last decode step; returns count
@@ -1649,6 +1726,13 @@ smo_status smo_engine_decode_step(smo_engine* e, int32_t k, const int32_t* draft
   return smo::run_guarded([&] {
     SMO_REQUIRE(e, "engine: null argument");
     e->impl.decode_step(k, drafts, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+smo_status smo_engine_decode_run(smo_engine* e, int32_t k, int32_t steps, int32_t use_graph, smo_stream stream) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(e && steps >= 0, "engine: bad argument");
+    e->impl.decode_run(k, steps, use_graph != 0, reinterpret_cast<cudaStream_t>(stream));
   });
 }
 

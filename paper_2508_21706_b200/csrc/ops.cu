@@ -4,6 +4,8 @@
 // All of these are HBM/latency-bound; none is GEMM-shaped.
 #include <cmath>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace smo {
@@ -46,12 +48,13 @@ __global__ void fill_kv_prefix_kernel(uint16_t* cache, const int32_t* prefix, in
 // restates (oracle.c:orc_router_logits), so ids are bit-exact.
 __global__ void router_topk_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ w, int T, int h,
                                    int E, int k, float* logits_out, int32_t* ids, float* weights) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
-  const int lane = threadIdx.x % 32;
-  if (warp >= T) return;
-  const uint16_t* xr = x + size_t(warp) * h;
-  float lg[kMaxExperts];
-  for (int e = 0; e < E; ++e) {
+  // one block per token, warp w computes experts w, w + nwarps, ...: each
+  // (token, expert) dot product keeps the fixed lane order above
+  const int t = blockIdx.x;
+  const int wid = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  __shared__ float lg[kMaxExperts];
+  const uint16_t* xr = x + size_t(t) * h;
+  for (int e = wid; e < E; e += nw) {
     const uint16_t* wr = w + size_t(e) * h;
     float a = 0.f;
     for (int base = lane * 8; base < h; base += 256) {
@@ -60,18 +63,19 @@ __global__ void router_topk_kernel(const uint16_t* __restrict__ x, const uint16_
       const uint32_t xs[4] = {xv.x, xv.y, xv.z, xv.w};
       const uint32_t ws[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        a = __fmaf_rn(__uint_as_float(xs[t] << 16), __uint_as_float(ws[t] << 16), a);
-        a = __fmaf_rn(__uint_as_float(xs[t] & 0xffff0000u), __uint_as_float(ws[t] & 0xffff0000u), a);
+      for (int q = 0; q < 4; ++q) {
+        a = __fmaf_rn(__uint_as_float(xs[q] << 16), __uint_as_float(ws[q] << 16), a);
+        a = __fmaf_rn(__uint_as_float(xs[q] & 0xffff0000u), __uint_as_float(ws[q] & 0xffff0000u), a);
       }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
-    lg[e] = a;
+    if (lane == 0) lg[e] = a;
   }
-  if (lane != 0) return;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
   if (logits_out)
-    for (int e = 0; e < E; ++e) logits_out[size_t(warp) * E + e] = lg[e];
+    for (int e = 0; e < E; ++e) logits_out[size_t(t) * E + e] = lg[e];
   uint64_t used = 0;
   int sel[kMaxTopK];
   for (int j = 0; j < k; ++j) {
@@ -82,7 +86,7 @@ __global__ void router_topk_kernel(const uint16_t* __restrict__ x, const uint16_
     }
     used |= 1ull << best;
     sel[j] = best;
-    ids[size_t(warp) * k + j] = best;
+    ids[size_t(t) * k + j] = best;
   }
   const float mx = lg[sel[0]];
   float ex[kMaxTopK], den = 0.f;
@@ -90,7 +94,7 @@ __global__ void router_topk_kernel(const uint16_t* __restrict__ x, const uint16_
     ex[j] = expf(lg[sel[j]] - mx);
     den += ex[j];
   }
-  for (int j = 0; j < k; ++j) weights[size_t(warp) * k + j] = ex[j] / den;
+  for (int j = 0; j < k; ++j) weights[size_t(t) * k + j] = ex[j] / den;
 }
 
 // ---------------------------------------------------------------- K3 permute
@@ -242,12 +246,19 @@ __global__ void rope_append_kernel(const uint16_t* __restrict__ qkv, const int32
   const int half = d / 2;
   const int width = (n_q + 2 * n_kv) * d;
   const uint16_t* src = qkv + size_t(row) * width;
-  for (int e = threadIdx.x; e < (n_q + n_kv) * half; e += blockDim.x) {
-    const int head = e / half, j = e % half;
+  // the row's rotation angles, once per frequency (fp64 angle, fp32 cos/sin)
+  __shared__ float cs_sh[64], sn_sh[64];
+  for (int j = threadIdx.x; j < half; j += blockDim.x) {
     const double inv = pow(theta, -2.0 * j / double(d));
     double sn, cs;
     sincos(double(pos) * inv, &sn, &cs);
-    const float c = float(cs), s = float(sn);
+    cs_sh[j] = float(cs);
+    sn_sh[j] = float(sn);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < (n_q + n_kv) * half; e += blockDim.x) {
+    const int head = e / half, j = e % half;
+    const float c = cs_sh[j], s = sn_sh[j];
     const float a = bf2f(src[head * d + j]), b = bf2f(src[head * d + j + half]);
     const uint16_t o0 = f2bf(a * c - b * s), o1 = f2bf(b * c + a * s);
     if (head < n_q) {
@@ -496,9 +507,9 @@ void router_topk(const void* x, const void* w, int T, int h, int E, int k, float
   SMO_REQUIRE(h % 256 == 0, "router: h must be a multiple of 256");
   SMO_REQUIRE(E >= 1 && E <= kMaxExperts && k >= 1 && k <= kMaxTopK && k <= E, "router: bad E/k");
   if (T <= 0) return;
-  const int warps_per_block = 4;
-  router_topk_kernel<<<(T + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0, st>>>(
-      reinterpret_cast<const uint16_t*>(x), reinterpret_cast<const uint16_t*>(w), T, h, E, k, logits, ids, weights);
+  const int warps = std::min(E, 8);
+  router_topk_kernel<<<T, 32 * warps, 0, st>>>(reinterpret_cast<const uint16_t*>(x),
+                                              reinterpret_cast<const uint16_t*>(w), T, h, E, k, logits, ids, weights);
   count_launch();
   SMO_CUDA_CHECK(cudaGetLastError());
 }
@@ -551,7 +562,7 @@ void rope_append(const void* qkv, const int32_t* prefix, const int32_t* parent, 
                  int d, int s_max, float theta, void* q_out, void* kc, void* vc, cudaStream_t st, const int32_t* bt,
                  int max_pages) {
   SMO_REQUIRE(qkv && prefix && q_out && kc && vc, "rope_append: null pointer");
-  SMO_REQUIRE(d % 2 == 0, "rope_append: odd head_dim");
+  SMO_REQUIRE(d % 2 == 0 && d <= 128, "rope_append: head_dim must be even and <= 128");
   rope_append_kernel<<<b * n, 256, 0, st>>>(reinterpret_cast<const uint16_t*>(qkv), prefix, parent, n, n_q, n_kv,
                                             d, s_max, double(theta), reinterpret_cast<uint16_t*>(q_out),
                                             reinterpret_cast<uint16_t*>(kc), reinterpret_cast<uint16_t*>(vc), bt,

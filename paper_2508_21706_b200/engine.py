@@ -201,6 +201,11 @@ class VerifyEngine:
         L.check(L.load().smo_engine_decode_step(self._h, k, None if d is None else d.ctypes.data_as(C.c_void_p),
                                                 C.c_void_p(stream or 0)))
 
+    def decode_run(self, k: int, steps: int, graph: bool = False, stream: Optional[int] = None) -> None:
+        """`steps` drafter-driven iterations (asynchronous); graph=True replays
+        one captured CUDA graph per iteration (needs a non-default stream)."""
+        L.check(L.load().smo_engine_decode_run(self._h, k, steps, int(graph), C.c_void_p(stream or 0)))
+
     def decode_read(self, b: int, cap: int):
         """(committed [b, cap] -1 padded, n_committed [b], kv_len [b], root [b])"""
         com = np.zeros((b, cap), np.int32)

@@ -252,3 +252,30 @@ def test_paged_kv_pool_exhaustion(ref):
     with pytest.raises(_lib.CapacityError, match="page pool exhausted"):
         eng.prefill(_prompts(s))
     eng.close()
+
+
+def test_decode_run_cuda_graph(ref):
+    """decode_run(graph=True): one captured CUDA graph per iteration (drafter,
+    expert streaming on the copy stream, verify, commit) replayed; every
+    committed token is still the target's greedy token, and the graph path
+    issues one launch per iteration."""
+    import torch
+    from paper_2508_21706_b200 import _lib
+    s, om, _ = ref
+    b, k, steps = len(PROMPTS), 3, 6
+    prompts = _prompts(s)
+    eng = _engine(s)
+    nxt = eng.prefill(prompts)
+    stream = torch.cuda.Stream()
+    eng.decode_run(k, 2, graph=True, stream=stream.cuda_stream)       # captures
+    eng.decode_run(k, steps - 2, graph=True, stream=stream.cuda_stream)  # replays the same graph
+    stream.synchronize()
+    com, n, kv, root = eng.decode_read(b, 128)
+    assert np.all(n >= steps)
+    assert np.array_equal(kv, np.array(PROMPTS) + n)
+    decisive = sum(_teacher_forced(om, prompts[r], nxt[r], com[r, :n[r]], f"graph request {r}") for r in range(b))
+    assert decisive >= b * steps // 2
+    assert eng.last_times()["draft"] > 0.0
+    with pytest.raises(ValueError, match="non-default stream"):
+        eng.decode_run(k, 1, graph=True)
+    eng.close()
