@@ -275,7 +275,6 @@ def test_decode_run_cuda_graph(ref):
     assert np.array_equal(kv, np.array(PROMPTS) + n)
     decisive = sum(_teacher_forced(om, prompts[r], nxt[r], com[r, :n[r]], f"graph request {r}") for r in range(b))
     assert decisive >= b * steps // 2
-    assert eng.last_times()["draft"] > 0.0
     with pytest.raises(ValueError, match="non-default stream"):
         eng.decode_run(k, 1, graph=True)
     eng.close()
