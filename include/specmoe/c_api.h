@@ -363,6 +363,16 @@ smo_status smo_engine_prefill(smo_engine* e, const int32_t* tokens, const int32_
                               int32_t max_len, int32_t* next_token, smo_stream stream);
 smo_status smo_engine_decode_begin(smo_engine* e, const int32_t* root, const int32_t* kv_len, int32_t b);
 smo_status smo_engine_decode_step(smo_engine* e, int32_t k, const int32_t* drafts, smo_stream stream);
+/* One iteration with a planted draft TREE of n nodes per request: node 0 is
+ * the root (the current root token), tokens host [b*(n-1)] for nodes 1..n-1,
+ * parents host [b*n] (parents[r*n] = -1, 0 <= parents[r*n+i] < i). The
+ * drafter runs over all nodes at once (tree positions and mask), verify uses
+ * the ancestor-or-self mask, greedy accept takes the longest matching root
+ * path (children in id order), and that path's K/V rows of every target and
+ * drafter layer are compacted to kv_len + j (smo_kv_rollback) before the
+ * commit — the tree K/V lifecycle of SURVEY.md §8 f2.                      */
+smo_status smo_engine_decode_step_tree(smo_engine* e, int32_t n, const int32_t* tokens, const int32_t* parents,
+                                       smo_stream stream);
 /* `steps` decode iterations with k drafts from the drafter (asynchronous).
  * use_graph: the device part of an iteration is captured once into a CUDA
  * graph and replayed (one launch per iteration; needs a non-default stream,

@@ -116,6 +116,7 @@ _SIGS = {
     "smo_engine_decode_begin": (C.c_int, [_vp, _vp, _vp, _i32]),
     "smo_engine_decode_step": (C.c_int, [_vp, _i32, _vp, _vp]),
     "smo_engine_decode_run": (C.c_int, [_vp, _i32, _i32, _i32, _vp]),
+    "smo_engine_decode_step_tree": (C.c_int, [_vp, _i32, _vp, _vp, _vp]),
     "smo_engine_decode_read": (C.c_int, [_vp, _vp, _i32, _vp, _vp, _vp]),
     "smo_engine_draft_times": (C.c_int, [_vp, _vp, _sz, _vp]),
     "smo_engine_layer_times": (C.c_int, [_vp, _vp, _sz]),

@@ -62,7 +62,11 @@ void draft_io(const int32_t* tokens, const int32_t* kv_len, int t, int b, int n,
               cudaStream_t st);
 void draft_scatter(const int32_t* out, int b, int n, int t, int32_t* tokens, cudaStream_t st);
 void decode_commit(const int32_t* tokens, const int32_t* acc, const int32_t* bonus, int b, int n, int cap,
-                   int32_t* hist, int32_t* hist_n, int32_t* kv_len, int32_t* root, cudaStream_t st);
+                   int32_t* hist, int32_t* hist_n, int32_t* kv_len, int32_t* root, cudaStream_t st,
+                   const int32_t* keep = nullptr);
+void kv_rollback(void* const* kcs, void* const* vcs, int n_layers, const int32_t* prefix, const int32_t* acc,
+                 const int32_t* keep, int b, int n, int n_kv, int d, int s_max, int32_t* kv_len, cudaStream_t st,
+                 const int32_t* bt = nullptr, int max_pages = 0);
 void prefill_last(const float* x, const int32_t* len, int b, int C, int h, float* out, cudaStream_t st);
 // expert parallelism (ep.cu)
 EpTransport* ep_transport(void* group);
@@ -126,7 +130,8 @@ struct Engine {
   int dec_b = 0, hist_cap = 0;
   int64_t kv_bound = 0;  // host upper bound of kv_len (K1 split planning)
   int32_t *d_kvlen = nullptr, *d_root = nullptr, *d_hist = nullptr, *d_hist_n = nullptr, *d_dec_tok = nullptr,
-          *d_drafts = nullptr;
+          *d_drafts = nullptr, *d_dec_parent = nullptr;
+  void** d_cache_ptrs = nullptr;  // [2][L + dL]: K then V caches of target + drafter layers (tree compaction)
   bool last_was_decode = false;
   // paged K/V: pool of num_pages 128-token pages per layer,
   // host-managed block table (pinned mirror + device copy), free list
@@ -594,6 +599,16 @@ struct Engine {
     d_hist_n = dalloc<int32_t>(maxB);
     d_dec_tok = dalloc<int32_t>(maxT);
     d_drafts = dalloc<int32_t>(maxT);
+    d_dec_parent = dalloc<int32_t>(maxT);
+    {
+      std::vector<void*> ptrs;
+      for (int l = 0; l < L; ++l) ptrs.push_back(layers[l].kc);
+      for (int l = 0; l < dL; ++l) ptrs.push_back(dlayers[l].kc);
+      for (int l = 0; l < L; ++l) ptrs.push_back(layers[l].vc);
+      for (int l = 0; l < dL; ++l) ptrs.push_back(dlayers[l].vc);
+      d_cache_ptrs = dalloc<void*>(ptrs.size());
+      SMO_CUDA_CHECK(cudaMemcpy(d_cache_ptrs, ptrs.data(), ptrs.size() * sizeof(void*), cudaMemcpyHostToDevice));
+    }
     h_stage_elems = size_t(maxT) * 4 + maxB * 4;
     SMO_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_stage), h_stage_elems * 4, cudaHostAllocPortable));
     ev.resize(8 + size_t(L) * 8);
@@ -1113,13 +1128,13 @@ struct Engine {
   // are appended to kc/vc (the K1 contract of smo_verify_attention).
   void attn_sublayer(const Scratch& sc, const uint16_t* wqkv, const uint16_t* wo, uint16_t* kc, uint16_t* vc, int b,
                      int n, int nch, const int32_t* prefix, const std::vector<int>& max_prefix, const uint64_t* mask,
-                     cudaStream_t st) {
+                     cudaStream_t st, const int32_t* parent = nullptr) {
     const int rows = b * n * nch;
     rmsnorm(sc.x, ones, rows, h, cfg.rms_eps, sc.xn, st);
     dense_gemm(sc.xn, rows, h, qkv_w, wqkv, nullptr, SMO_EPI_BF16, sc.qkv, sc.split, st);
     for (int c = 0; c < nch; ++c) {
       const size_t r0 = size_t(c) * b * n;
-      rope_append(sc.qkv + r0 * qkv_w, prefix + size_t(c) * b, nullptr, b, n, nq, nkv, d, s_max, cfg.rope_theta,
+      rope_append(sc.qkv + r0 * qkv_w, prefix + size_t(c) * b, parent, b, n, nq, nkv, d, s_max, cfg.rope_theta,
                   sc.q + r0 * nq * d, kc, vc, st, bt(), max_pages);
       smo_attn_args a{};
       a.q = sc.q + r0 * nq * d;
@@ -1233,8 +1248,9 @@ struct Engine {
   }
 
   // draft (k+1 drafter steps) -> verify -> greedy accept -> commit, on device
-  void decode_step(int k, const int32_t* drafts_h, cudaStream_t st) {
+  void decode_step(int k, const int32_t* drafts_h, cudaStream_t st, const int32_t* parents_h = nullptr) {
     const int b = dec_b, n = k + 1;
+    SMO_REQUIRE(!parents_h || (drafts_h && k > 0), "decode: a draft tree needs planted drafts");
     SMO_REQUIRE(b > 0, "decode: call smo_engine_prefill or smo_engine_decode_begin first");
     SMO_REQUIRE(k >= 0 && n <= maxN, "decode: k + 1 exceeds max_verify");
     SMO_REQUIRE(kv_bound + n <= s_max, "decode: KV capacity (max_seq) exhausted");
@@ -1250,18 +1266,55 @@ struct Engine {
       std::memcpy(h_stage, drafts_h, size_t(b) * k * 4);
       SMO_CUDA_CHECK(cudaMemcpyAsync(d_drafts, h_stage, size_t(b) * k * 4, cudaMemcpyHostToDevice, st));
     }
-    decode_device(k, planted, int(kv_bound), st);
+    if (parents_h) {
+      for (int r = 0; r < b; ++r) {
+        SMO_REQUIRE(parents_h[size_t(r) * n] == -1, "decode: tree node 0 is the root (parent -1)");
+        for (int i = 1; i < n; ++i)
+          SMO_REQUIRE(parents_h[size_t(r) * n + i] >= 0 && parents_h[size_t(r) * n + i] < i,
+                      "decode: tree parents must precede their children");
+      }
+      int32_t* hp = h_stage + size_t(b) * k;
+      std::memcpy(hp, parents_h, size_t(b) * n * 4);
+      SMO_CUDA_CHECK(cudaMemcpyAsync(d_dec_parent, hp, size_t(b) * n * 4, cudaMemcpyHostToDevice, st));
+    }
+    decode_device(k, planted, int(kv_bound), st, parents_h != nullptr);
     kv_bound += n;
   }
 
   // The device part of a decode step (capturable into a CUDA graph): every
   // argument is fixed at enqueue time; bound = host bound of kv_len used for
   // K1 split planning and the drafter's positions.
-  void decode_device(int k, bool planted, int bound, cudaStream_t st) {
+  void decode_device(int k, bool planted, int bound, cudaStream_t st, bool tree = false) {
     const int b = dec_b, n = k + 1;
     last_was_decode = true;
     begin_step(st, !batch_one);  // the first layers' experts stream while the drafter runs
     decode_prep(d_root, planted ? d_drafts : nullptr, b, n, d_dec_tok, st);
+    if (tree) {
+      // planted draft tree: the drafter runs its layers over all n nodes at
+      // once (tree positions and mask) so its K/V covers every node; verify
+      // with the tree mask; the accepted root path's K/V rows of every target
+      // and drafter layer are compacted to kv_len + j; commit along it
+      last_draft_steps = dL > 0 ? 1 : 0;
+      if (dL > 0) SMO_CUDA_CHECK(cudaEventRecord(draft_ev[0], st));
+      if (dL > 0) {
+        build_mask(d_dec_parent, b, n, d_mask, st);
+        const Scratch sc{x, xn, qkv, q, attn, attn_ws, attn_ws_bytes, 0};
+        embed(d_dec_tok, embed_w, b * n, h, x, st);
+        const std::vector<int> mp{bound};
+        for (auto& dl : dlayers) {
+          attn_sublayer(sc, dl.wqkv, dl.wo, dl.kc, dl.vc, b, n, 1, d_kvlen, mp, d_mask, st, d_dec_parent);
+          ffn_dense(sc, dh, b * n, dl.w1, dl.w3, dl.w2, dI, st);
+        }
+      }
+      SMO_CUDA_CHECK(cudaEventRecord(ev[3], st));
+      if (dL > 0) SMO_CUDA_CHECK(cudaEventRecord(draft_ev[1], st));
+      verify_core(b, n, d_dec_tok, d_dec_parent, d_kvlen, bound, st);
+      void* const* kp = d_cache_ptrs;
+      void* const* vp = d_cache_ptrs + (L + dL);
+      kv_rollback(kp, vp, L + dL, d_kvlen, d_acc, d_keep, b, n, nkv, d, s_max, nullptr, st, bt(), max_pages);
+      decode_commit(d_dec_tok, d_acc, d_bonus, b, n, hist_cap, d_hist, d_hist_n, d_kvlen, d_root, st, d_keep);
+      return;
+    }
     // drafter: step t consumes row t (root, d_1, ..., d_k) at kv_len + t and
     // proposes d_{t+1}; the extra step t = k only appends d_k's draft K/V so
     // that a fully accepted chain leaves no hole in the drafter's cache
@@ -1726,6 +1779,14 @@ smo_status smo_engine_decode_step(smo_engine* e, int32_t k, const int32_t* draft
   return smo::run_guarded([&] {
     SMO_REQUIRE(e, "engine: null argument");
     e->impl.decode_step(k, drafts, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+smo_status smo_engine_decode_step_tree(smo_engine* e, int32_t n, const int32_t* tokens, const int32_t* parents,
+                                       smo_stream stream) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(e && tokens && parents && n >= 2, "engine: bad argument");
+    e->impl.decode_step(n - 1, tokens, reinterpret_cast<cudaStream_t>(stream), parents);
   });
 }
 

@@ -445,16 +445,18 @@ __global__ void draft_scatter_kernel(const int32_t* __restrict__ out, int b, int
 // bonus token are appended to the history (committed = a + 1, config.hpp:69-70);
 // the chain's K/V rows root..d_a are already in place, so kv_len += a + 1 and
 // the bonus becomes the next root.
+// keep (trees): the accepted root path's node ids (greedy_accept); its K/V
+// rows were compacted to kv_len + j by kv_rollback before this runs.
 __global__ void decode_commit_kernel(const int32_t* __restrict__ tokens, const int32_t* __restrict__ acc,
-                                     const int32_t* __restrict__ bonus, int b, int n, int cap, int32_t* hist,
-                                     int32_t* hist_n, int32_t* kv_len, int32_t* root) {
+                                     const int32_t* __restrict__ bonus, const int32_t* __restrict__ keep, int b, int n,
+                                     int cap, int32_t* hist, int32_t* hist_n, int32_t* kv_len, int32_t* root) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= b) return;
   const int a = acc[r];
   int h = hist_n[r];
   int32_t* dst = hist + size_t(r) * cap;
   for (int j = 1; j <= a; ++j)
-    if (h < cap) dst[h++] = tokens[size_t(r) * n + j];
+    if (h < cap) dst[h++] = tokens[size_t(r) * n + (keep ? keep[size_t(r) * n + j] : j)];
   if (h < cap) dst[h++] = bonus[r];
   hist_n[r] = h;
   kv_len[r] += a + 1;
@@ -641,8 +643,10 @@ void draft_scatter(const int32_t* out, int b, int n, int t, int32_t* tokens, cud
 }
 
 void decode_commit(const int32_t* tokens, const int32_t* acc, const int32_t* bonus, int b, int n, int cap,
-                   int32_t* hist, int32_t* hist_n, int32_t* kv_len, int32_t* root, cudaStream_t st) {
-  decode_commit_kernel<<<(b + 127) / 128, 128, 0, st>>>(tokens, acc, bonus, b, n, cap, hist, hist_n, kv_len, root);
+                   int32_t* hist, int32_t* hist_n, int32_t* kv_len, int32_t* root, cudaStream_t st,
+                   const int32_t* keep) {
+  decode_commit_kernel<<<(b + 127) / 128, 128, 0, st>>>(tokens, acc, bonus, keep, b, n, cap, hist, hist_n, kv_len,
+                                                        root);
   count_launch();
   SMO_CUDA_CHECK(cudaGetLastError());
 }

@@ -201,6 +201,14 @@ class VerifyEngine:
         L.check(L.load().smo_engine_decode_step(self._h, k, None if d is None else d.ctypes.data_as(C.c_void_p),
                                                 C.c_void_p(stream or 0)))
 
+    def decode_step_tree(self, tokens, parents, stream: Optional[int] = None) -> None:
+        """One iteration with a planted draft tree: tokens [b, n-1] for nodes
+        1..n-1, parents [b, n] (parents[:, 0] = -1, parents[:, i] < i)."""
+        t = np.ascontiguousarray(tokens, np.int32)
+        p = np.ascontiguousarray(parents, np.int32)
+        L.check(L.load().smo_engine_decode_step_tree(self._h, p.shape[1], t.ctypes.data_as(C.c_void_p),
+                                                     p.ctypes.data_as(C.c_void_p), C.c_void_p(stream or 0)))
+
     def decode_run(self, k: int, steps: int, graph: bool = False, stream: Optional[int] = None) -> None:
         """`steps` drafter-driven iterations (asynchronous); graph=True replays
         one captured CUDA graph per iteration (needs a non-default stream)."""

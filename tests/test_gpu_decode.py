@@ -278,3 +278,75 @@ def test_decode_run_cuda_graph(ref):
     with pytest.raises(ValueError, match="non-default stream"):
         eng.decode_run(k, 1, graph=True)
     eng.close()
+
+
+def test_decode_planted_tree_compacts_kv(ref):
+    """Tree K/V lifecycle: each step plants a 7-node tree —
+    a spine of the oracle's greedy tokens (correct up to a random cut) with a
+    decoy sibling at every level, sibling order random. Greedy accept must take
+    exactly the spine prefix, and because the next steps attend over the
+    COMPACTED K/V (spine rows moved to kv_len + j in every target and drafter
+    layer), every later committed token is still the greedy one."""
+    import copy
+    import oracle_model
+    s, om, _ = ref
+    b, n = len(PROMPTS), 7
+    prompts = _prompts(s)
+    eng = _engine(s, n_max=8)
+    nxt = eng.prefill(prompts)
+    decs, lgs = [], []
+    for r, p in enumerate(prompts):
+        dec = oracle_model.OracleDecoder(om, 256)
+        dec.prefill(list(p), _chunk(s))
+        decs.append(dec)
+        lgs.append(dec.run([int(nxt[r])])[-1])
+    rng = np.random.default_rng(21)
+    pos = np.zeros(b, np.int64)
+    seen = set()
+    for step in range(6):
+        tokens = np.zeros((b, n - 1), np.int32)
+        parents = np.full((b, n), -1, np.int32)
+        cut = rng.integers(0, 4, size=b)
+        decisive = np.zeros(b, bool)
+        for r in range(b):
+            sim, lg, margins = copy.deepcopy(decs[r]), lgs[r], []
+            spine_parent, node = 0, 1
+            for lvl in range(3):
+                g = int(np.argmax(lg))
+                margins.append(oracle_model.OracleDecoder.margin(lg))
+                spine_tok = g if lvl < cut[r] else (g + 7 + lvl) % s.vocab
+                decoy_tok = (g + 1 + lvl) % s.vocab
+                order = [("spine", spine_tok), ("decoy", decoy_tok)]
+                if rng.integers(0, 2):
+                    order.reverse()
+                spine_node = None
+                for kind, tok in order:
+                    tokens[r, node - 1] = tok
+                    parents[r, node] = spine_parent
+                    if kind == "spine":
+                        spine_node = node
+                    node += 1
+                spine_parent = spine_node
+                lg = sim.run([g])[-1]
+            decisive[r] = all(m >= MARGIN for m in margins[:cut[r]])
+        eng.decode_step_tree(tokens, parents)
+        com, cnt, kv, root = eng.decode_read(b, 64)
+        for r in range(b):
+            new = [int(t) for t in com[r, pos[r]:cnt[r]]]
+            if decisive[r]:
+                assert len(new) - 1 == cut[r], f"step {step} request {r}: accepted {len(new) - 1} != {cut[r]}"
+                seen.add(int(cut[r]))
+            for i, t in enumerate(new):
+                _assert_greedy(lgs[r], t, f"tree step {step} request {r} token {i}")
+                lgs[r] = decs[r].run([t])[-1]
+            pos[r] = cnt[r]
+        assert np.array_equal(kv, np.array(PROMPTS) + cnt)
+    assert len(seen) >= 2, seen
+    # a chain step after the trees still commits greedy tokens (drafter K/V compacted too)
+    eng.decode_step(3)
+    com, cnt, kv, root = eng.decode_read(b, 64)
+    for r in range(b):
+        for i, t in enumerate(com[r, pos[r]:cnt[r]]):
+            _assert_greedy(lgs[r], int(t), f"post-tree request {r} token {i}")
+            lgs[r] = decs[r].run([int(t)])[-1]
+    eng.close()
