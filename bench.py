@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-decode", action="store_true", help="skip the prefill + decode-loop measurement")
     ap.add_argument("--moe-batching", default="large", choices=["large", "one"],
                     help="LARGE_BATCH (stream whole layers ahead) or BATCH_ONE (stream router-selected experts)")
+    ap.add_argument("--no-compress", dest="compress", action="store_false",
+                    help="stream raw bf16 experts instead of the lossless code (default: coded, expanded in HBM)")
     ap.add_argument("--attn-cpu", action="store_true",
                     help="AttentionPlacement::CPU: target K/V in pinned host DRAM, attention on the host pool")
     return ap.parse_args()
@@ -396,7 +398,7 @@ def run_ours(args):
             eng = VerifyEngine(shape, max_batch=b, max_verify=n, max_seq=s_max, hbm_slots=args.slots,
                                expert_cache_bytes=int(args.cache_gb * 1e9), host_alias_layers=a, device=local,
                                ep_rank=ep_rank, ep_size=ep_size, ep_group=grp, attn_cpu=args.attn_cpu,
-                               batch_one=args.moe_batching == "one")
+                               batch_one=args.moe_batching == "one", compress_experts=args.compress)
             alias = a
             break
         except _lib.CapacityError as e:
@@ -483,9 +485,10 @@ def run_ours(args):
     roof = step_roofline(shape, b * ep_size, n, prefix, h2d_peak, pk["hbm_gbs"],
                          pk.get("bf16_tflops_sustained", 1400.0),
                          cached_blocks=int(args.cache_gb * 1e9) // shape.expert_bytes, ep=ep_size,
-                         h2d_bytes=stages["h2d_bytes"] if args.moe_batching == "one" else None)
+                         h2d_bytes=stages["h2d_bytes"] if (args.moe_batching == "one" or args.compress) else None)
     h2d_bytes = stages["h2d_bytes"]
     t_step = t_all / args.steps
+    raw_h2d = stages["h2d_raw_bytes"]  # the bf16 bytes those transfers carry (coded blocks expand)
     # dominant GPU kernel by device time: K4 grouped SwiGLU (+down +combine),
     # HBM-bound: algorithmic bytes = expert weights read once per layer
     moe_bytes_step = shape.n_layers * (shape.n_expert // ep_size) * shape.expert_bytes
@@ -503,11 +506,14 @@ def run_ours(args):
                    "attention_placement": "CPU (host K/V, host thread pool)" if args.attn_cpu else "GPU_RESIDENT (K1)",
                    "moe_batching": "BATCH_ONE (router-selected experts)" if args.moe_batching == "one"
                    else "LARGE_BATCH (whole layers)",
+                   "expert_transfer": "lossless exponent-coded blocks (xfer.cu, 11.4 bits/weight), expanded in HBM "
+                   "before the expert kernel" if args.compress else "raw bf16",
                    "l2": "inputs larger than L2 (90.2 GB of experts + 4.6 GB KV streamed per step)",
                    "parallelism": mode},
         "committed_tokens_per_s_model": world * b * geometric_alpha(0.8, args.k) / t_step,
         "h2d": {"achieved_gbs": h2d_bytes / t_step / 1e9, "link_peak_gbs": h2d_peak,
-                "bytes_per_step": h2d_bytes, "copy_engine_busy_s": stages["h2d_transfer"]},
+                "bytes_per_step": h2d_bytes, "copy_engine_busy_s": stages["h2d_transfer"],
+                "raw_bf16_bytes_per_step": raw_h2d, "raw_equivalent_gbs": raw_h2d / t_step / 1e9},
         "roofline": {"bound": "hbm", "kernel": "K4-MoE fused expert block (gate/up + SwiGLU + down, one "
                      "persistent launch per layer) + combine, per step",
                      "achieved": moe_bytes_step / moe_t / 1e9 if moe_t > 0 else None, "peak": pk["hbm_gbs"],

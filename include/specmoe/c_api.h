@@ -179,6 +179,19 @@ smo_status smo_moe_experts(const void* x_perm, int32_t rows, int32_t h, int32_t 
                            int32_t w_pool_blocks, const int32_t* w_index, void* h_out, float* y, int32_t splits,
                            int32_t* splits_used, int32_t* scratch, smo_stream stream);
 
+/* ---- K5 codec: lossless expert-weight packing for the host link (xfer.cu)
+ * bf16 values in segments of 1024: sign + mantissa verbatim (1 byte), the
+ * exponent as a `bits`-bit code (3 or 4) against a per-segment base with up
+ * to 32 escaped exponents per segment — 1456 (3 bits: 11.4 bits/value) or
+ * 1584 (4 bits: 12.4 bits/value) bytes per 1024 values. count % 1024 == 0.
+ * encode sets *overflow (device int) to 1 when a segment needs more than 32
+ * escapes (retry with 4 bits or keep the block raw). Decode is the exact
+ * inverse (bit-identical bf16).                                             */
+size_t smo_expert_code_bytes(uint64_t count, int32_t bits);
+smo_status smo_expert_encode(const void* src, uint64_t count, int32_t bits, void* dst, int32_t* overflow,
+                             smo_stream stream);
+smo_status smo_expert_decode(const void* src, uint64_t count, int32_t bits, void* dst, smo_stream stream);
+
 /* ---- support ops of the verify layer (standard Mixtral block, not in the
  *      reference: SURVEY.md §2.3 "support")                                 */
 /* y bf16 [T,h] = x f32 [T,h] * rsqrt(mean(x^2)+eps) * gain bf16 [h] */
@@ -277,6 +290,11 @@ typedef struct {
                                  1 = BATCH_ONE: after layer l's router, stream only the experts its
                                  tokens selected (host waits for the routing, then issues the copies).
                                  Prefill always streams whole layers. Not with expert parallelism. */
+  int32_t compress_experts;   /* 1: experts sit in pinned host DRAM in the lossless code of
+                                 smo_expert_encode (3-bit exponents: 1.41x fewer bytes; blocks that
+                                 need it get 4 bits: 1.29x; blocks neither can hold stay raw) and
+                                 cross the link coded; the compute stream expands each layer's
+                                 blocks into its HBM slot before the expert kernel. */
 } smo_engine_options;
 
 /* ---- expert parallelism ----------------------------------
@@ -331,6 +349,7 @@ typedef struct {
   double h2d_bytes;    /* bytes streamed */
   double launches;     /* kernels launched */
   double draft;        /* drafter time of the last decode step (DRAFT_GPU_STEP total) */
+  double h2d_raw_bytes; /* bf16 bytes the streamed blocks carry (= h2d_bytes unless coded) */
 } smo_stage_times;
 smo_status smo_engine_last_times(smo_engine* e, smo_stage_times* t);
 /* Measured per-layer timeline of the last verify, 9 doubles per layer (s from

@@ -59,7 +59,8 @@ class EngineOptions(C.Structure):
     _fields_ = [("max_batch", _i32), ("max_verify", _i32), ("max_seq", _i32), ("hbm_slots", _i32),
                 ("expert_cache_bytes", _i64), ("host_alias_layers", _i32), ("device", _i32), ("flags", _i32),
                 ("ep_rank", _i32), ("ep_size", _i32), ("nccl_comm", _vp), ("kv_pages", _i32),
-                ("attn_cpu", _i32), ("moe_batching", _i32)]
+                ("attn_cpu", _i32), ("moe_batching", _i32),
+                ("compress_experts", _i32)]
 
 
 class VerifyBatch(C.Structure):
@@ -74,7 +75,7 @@ class VerifyOutput(C.Structure):
 class StageTimes(C.Structure):
     _fields_ = [("target_total", C.c_double), ("attention", C.c_double), ("gpu_moe", C.c_double),
                 ("h2d_transfer", C.c_double), ("others", C.c_double), ("h2d_bytes", C.c_double),
-                ("launches", C.c_double), ("draft", C.c_double)]
+                ("launches", C.c_double), ("draft", C.c_double), ("h2d_raw_bytes", C.c_double)]
 
 
 _SIGS = {
@@ -86,6 +87,9 @@ _SIGS = {
     "smo_verify_attention_workspace": (_sz, [C.POINTER(AttnArgs)]),
     "smo_verify_attention": (C.c_int, [C.POINTER(AttnArgs), _vp]),
     "smo_cpu_verify_attention": (C.c_int, [C.POINTER(AttnArgs), _i32]),
+    "smo_expert_code_bytes": (_sz, [_u64, _i32]),
+    "smo_expert_encode": (C.c_int, [_vp, _u64, _i32, _vp, _vp, _vp]),
+    "smo_expert_decode": (C.c_int, [_vp, _u64, _i32, _vp, _vp]),
     "smo_chunked_attention_f64": (C.c_int, [_sz, _sz, _sz, _vp, _vp, _vp, _sz, _vp, _vp]),
     "smo_router_topk": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "smo_permute": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp]),

@@ -34,6 +34,9 @@ void unpermute_combine(const float* y, const int32_t* pos, const float* w, int T
 int moe_launch(const void* x_perm, int rows, int h, int hi, int E, const int32_t* offsets, const void* pool,
                uint64_t w_block_stride, int pool_blocks, const int32_t* w_index, void* hbuf, float* y, int splits,
                int max_splits, int* done, cudaStream_t st);
+size_t expert_code_bytes(size_t count, int bits);
+void expert_encode(const void* src, size_t count, int bits, void* dst, int* overflow, cudaStream_t st);
+void expert_decode(const void* src, size_t count, int bits, void* dst, cudaStream_t st);
 void rmsnorm(const float* x, const void* gain, int T, int h, float eps, void* y, cudaStream_t st);
 void embed(const int32_t* tok, const void* emb, int T, int h, float* x, cudaStream_t st);
 void rope_append(const void* qkv, const int32_t* prefix, const int32_t* parent, int b, int n, int n_q, int n_kv,
@@ -179,6 +182,17 @@ smo_status smo_permute(const int32_t* ids, int32_t T, int32_t k, int32_t E, cons
 smo_status smo_unpermute_combine(const float* y, const int32_t* pos, const float* w, int32_t T, int32_t k,
                                  int32_t h, float* residual, smo_stream stream) {
   return guard([&] { smo::unpermute_combine(y, pos, w, T, k, h, residual, S(stream)); });
+}
+
+smo_status smo_expert_encode(const void* src, uint64_t count, int32_t bits, void* dst, int32_t* overflow,
+                             smo_stream stream) {
+  return guard([&] { smo::expert_encode(src, size_t(count), bits, dst, overflow, S(stream)); });
+}
+smo_status smo_expert_decode(const void* src, uint64_t count, int32_t bits, void* dst, smo_stream stream) {
+  return guard([&] { smo::expert_decode(src, size_t(count), bits, dst, S(stream)); });
+}
+size_t smo_expert_code_bytes(uint64_t count, int32_t bits) {
+  return (bits == 3 || bits == 4) ? smo::expert_code_bytes(size_t(count), bits) : 0;
 }
 
 smo_status smo_unpermute_combine_split(const float* y, int32_t splits, uint64_t split_stride, const int32_t* pos,

@@ -83,6 +83,9 @@ int moe_launch(const void* x_perm, int rows, int h, int hi, int E, const int32_t
                uint64_t w_block_stride, int pool_blocks, const int32_t* w_index, void* hbuf, float* y, int splits,
                int max_splits, int* done, cudaStream_t st);
 int pick_moe_splits(int rows, int h, int hi, int E, int max_splits);
+size_t expert_code_bytes(size_t count, int bits);
+void expert_encode(const void* src, size_t count, int bits, void* dst, int* overflow, cudaStream_t st);
+void expert_decode(const void* src, size_t count, int bits, void* dst, cudaStream_t st);
 
 // Procedural tensor ids; the oracle tests use the same ids.
 namespace tid {
@@ -159,6 +162,14 @@ struct Engine {
   int32_t* h_offsets = nullptr;           // pinned [E+1] routed offsets of the current layer
   cudaEvent_t route_ev = nullptr;
   std::vector<double> layer_bytes;        // bytes streamed per layer in the last step
+  std::vector<double> layer_raw_bytes;    // their bf16 size (coded blocks expand)
+  // lossless expert codec on the link (xfer.cu): coded blocks cross into
+  // cstage and are expanded into the pool slot on the compute stream
+  bool xcomp = false;
+  size_t cblk_bytes = 0;                  // coded bytes of one [W1|W3|W2] block at 4 bits (staging stride)
+  std::vector<uint8_t> blk_coded;         // [host_alias * E_loc] exponent bits of the host block (0 = raw)
+  uint8_t* cstage = nullptr;              // [slots][E_loc][cblk_bytes]
+  std::vector<std::vector<int>> coded_streamed;  // per layer: local experts streamed coded
   std::vector<cudaEvent_t> draft_ev;  // [maxN + 1]: boundaries of the drafter steps
   int last_draft_steps = 0;
   std::vector<uint16_t*> host_bufs;  // pinned, E blocks each
@@ -289,6 +300,17 @@ struct Engine {
     if (!paged || !bt_dirty) return;
     SMO_CUDA_CHECK(cudaMemcpyAsync(d_bt, h_bt, size_t(maxB) * max_pages * 4, cudaMemcpyHostToDevice, st));
     bt_dirty = false;
+  }
+
+  // exponent bits of layer l's local expert le on the host (0: raw bf16)
+  int code_bits(int l, int le) const { return xcomp ? blk_coded[size_t(host_layer(l)) * E_loc + size_t(le)] : 0; }
+  // expand layer l's coded blocks (streamed into cstage) into its pool slot,
+  // on the compute stream after slot_ready(l)
+  void decode_slot(int l, cudaStream_t st) {
+    const int s = l % slots;
+    for (int le : coded_streamed[size_t(l)])
+      expert_decode(cstage + (size_t(s) * E_loc + le) * cblk_bytes, blk_elems, code_bits(l, le),
+                    pool + (size_t(s) * E_loc + le) * blk_elems, st);
   }
 
   int host_layer(int l) const { return host_alias > 0 ? l % host_alias : l; }
@@ -431,6 +453,15 @@ struct Engine {
       if (owns(e)) owned.push_back(e);
     host_bufs.assign(host_alias, nullptr);
     uint16_t* stage = dalloc<uint16_t>(blk_elems);
+    xcomp = opt.compress_experts != 0;
+    uint8_t* cenc = nullptr;
+    int* d_ovf = nullptr;
+    if (xcomp) {
+      cblk_bytes = expert_code_bytes(blk_elems, 4);
+      cenc = dalloc<uint8_t>(cblk_bytes);
+      d_ovf = dalloc<int>(1);
+      blk_coded.assign(size_t(host_alias) * E_loc, 0);
+    }
     for (int a = 0; a < host_alias; ++a) {
       void* hp = nullptr;
       cudaError_t err = cudaHostAlloc(&hp, blk_bytes * E_loc, cudaHostAllocPortable);
@@ -443,7 +474,20 @@ struct Engine {
         fill_uniform(stage, size_t(hi) * h, cfg.seed, base + 0, 0, std::sqrt(3.0f / h), st);
         fill_uniform(stage + size_t(hi) * h, size_t(hi) * h, cfg.seed, base + 1, 0, std::sqrt(3.0f / h), st);
         fill_uniform(stage + 2 * size_t(hi) * h, size_t(h) * hi, cfg.seed, base + 2, 0, std::sqrt(3.0f / hi), st);
-        SMO_CUDA_CHECK(cudaMemcpy(host_bufs[a] + size_t(local(e)) * blk_elems, stage, blk_bytes, cudaMemcpyDeviceToHost));
+        uint16_t* hdst = host_bufs[a] + size_t(local(e)) * blk_elems;
+        bool coded = false;
+        for (int bits = 3; xcomp && !coded && bits <= 4; ++bits) {  // the narrowest code that holds the block
+          SMO_CUDA_CHECK(cudaMemset(d_ovf, 0, sizeof(int)));
+          expert_encode(stage, blk_elems, bits, cenc, d_ovf, st);
+          int ovf = 0;
+          SMO_CUDA_CHECK(cudaMemcpy(&ovf, d_ovf, sizeof(int), cudaMemcpyDeviceToHost));
+          if (!ovf) {
+            SMO_CUDA_CHECK(cudaMemcpy(hdst, cenc, expert_code_bytes(blk_elems, bits), cudaMemcpyDeviceToHost));
+            blk_coded[size_t(a) * E_loc + local(e)] = uint8_t(bits);
+            coded = true;
+          }
+        }
+        if (!coded) SMO_CUDA_CHECK(cudaMemcpy(hdst, stage, blk_bytes, cudaMemcpyDeviceToHost));
       }
     }
 
@@ -459,12 +503,19 @@ struct Engine {
       }
     pool_blocks = slots * E_loc + placed;
     pool = dalloc<uint16_t>(size_t(pool_blocks) * blk_elems);
+    coded_streamed.assign(size_t(L), {});
+    if (xcomp) cstage = dalloc<uint8_t>(size_t(slots) * E_loc * cblk_bytes);
     for (int l = 0; l < L; ++l)
       for (int e : owned) {
         const int cb = cache_blk[size_t(l) * E + e];
-        if (cb >= 0)
-          SMO_CUDA_CHECK(cudaMemcpy(pool + size_t(cb) * blk_elems, host_bufs[host_layer(l)] + size_t(local(e)) * blk_elems,
-                                    blk_bytes, cudaMemcpyHostToDevice));
+        if (cb < 0) continue;
+        const uint16_t* hsrc = host_bufs[host_layer(l)] + size_t(local(e)) * blk_elems;
+        if (const int bits = code_bits(l, local(e))) {
+          SMO_CUDA_CHECK(cudaMemcpy(cenc, hsrc, expert_code_bytes(blk_elems, bits), cudaMemcpyHostToDevice));
+          expert_decode(cenc, blk_elems, bits, pool + size_t(cb) * blk_elems, st);
+        } else {
+          SMO_CUDA_CHECK(cudaMemcpy(pool + size_t(cb) * blk_elems, hsrc, blk_bytes, cudaMemcpyHostToDevice));
+        }
       }
     std::vector<int32_t> widx(size_t(L) * E);
     for (int l = 0; l < L; ++l)
@@ -574,6 +625,7 @@ struct Engine {
       gemm_ws = dalloc<uint8_t>(gemm_ws_bytes);
     }
     layer_bytes.assign(size_t(L), 0.0);
+    layer_raw_bytes.assign(size_t(L), 0.0);
     if (batch_one) h_offsets = halloc_mapped<int32_t>(size_t(E) + 1);
     if (attn_cpu) {
       q_host = halloc_mapped<uint16_t>(size_t(maxT) * nq * d);
@@ -662,7 +714,25 @@ struct Engine {
     auto streamed = [&](int le) {
       return cache_blk[size_t(l) * E + owned[size_t(le)]] < 0 && (!active || active[le]);
     };
-    int le = 0;
+    coded_streamed[size_t(l)].clear();
+    if (xcomp) {
+      // coded blocks into cstage (expanded by decode_slot), raw ones straight into the slot
+      for (int q = 0; q < E_loc; ++q) {
+        if (!streamed(q)) continue;
+        if (const int bits = code_bits(l, q)) {
+          const size_t cb = expert_code_bytes(blk_elems, bits);
+          SMO_CUDA_CHECK(cudaMemcpyAsync(cstage + (size_t(s) * E_loc + q) * cblk_bytes, hb + size_t(q) * blk_elems,
+                                         cb, cudaMemcpyHostToDevice, copy));
+          bytes += double(cb);
+          coded_streamed[size_t(l)].push_back(q);
+        } else {
+          SMO_CUDA_CHECK(cudaMemcpyAsync(pool + (size_t(s) * E_loc + q) * blk_elems, hb + size_t(q) * blk_elems,
+                                         blk_bytes, cudaMemcpyHostToDevice, copy));
+          bytes += double(blk_bytes);
+        }
+      }
+    }
+    int le = xcomp ? E_loc : 0;
     while (le < E_loc) {
       if (!streamed(le)) {
         ++le;
@@ -679,6 +749,9 @@ struct Engine {
     if (t1) SMO_CUDA_CHECK(cudaEventRecord(t1, copy));
     SMO_CUDA_CHECK(cudaEventRecord(slot_ready[s], copy));
     layer_bytes[size_t(l)] = bytes;
+    int nstreamed = 0;
+    for (int q = 0; q < E_loc; ++q) nstreamed += streamed(q) ? 1 : 0;
+    layer_raw_bytes[size_t(l)] = double(nstreamed) * double(blk_bytes);
     return bytes;
   }
 
@@ -705,6 +778,7 @@ struct Engine {
     ep_unpack(ep_recv, P, E_loc, C, h, blk_d, xl, offsets_l, back, st);
     SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 7), st));
     SMO_CUDA_CHECK(cudaStreamWaitEvent(st, slot_ready[l % slots], 0));
+    decode_slot(l, st);
     SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 4), st));
     if (moe_fused) {
       moe_launch(xl, P * C, h, hi, E_loc, offsets_l, pool, blk_bytes, pool_blocks, d_w_index_loc + size_t(l) * E_loc,
@@ -830,6 +904,7 @@ struct Engine {
     step_h2d_bytes = 0;
     step_h2d_ev.clear();
     std::fill(layer_bytes.begin(), layer_bytes.end(), 0.0);
+    std::fill(layer_raw_bytes.begin(), layer_raw_bytes.end(), 0.0);
     for (int l = 0; prefetch && l < std::min(slots, L); ++l) {
       step_h2d_bytes += enqueue_h2d(l, tev(l * 8 + 0), tev(l * 8 + 1));
       step_h2d_ev.push_back({tev(l * 8 + 0), tev(l * 8 + 1)});
@@ -997,6 +1072,7 @@ struct Engine {
       } else {
         SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 7), st));
         SMO_CUDA_CHECK(cudaStreamWaitEvent(st, slot_ready[l % slots], 0));
+        decode_slot(l, st);  // coded expert blocks -> bf16 slot (compress_experts)
         SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 4), st));
         if (moe_fused) {
           moe_launch(xp, PT, h, hi, E, offsets, pool, blk_bytes, pool_blocks, d_w_index + size_t(l) * E, hbuf, ybuf,
@@ -1597,6 +1673,7 @@ struct Engine {
         dense_gemm(p_hs, Tp, cfg.shared_inter, h, ly.ws2, nullptr, SMO_EPI_F32_ADD, sc.x, 1, st);
       }
       SMO_CUDA_CHECK(cudaStreamWaitEvent(st, slot_ready[l % slots], 0));
+      decode_slot(l, st);
       if (moe_fused) {
         moe_launch(p_xp, PT, h, hi, E, p_off, pool, blk_bytes, pool_blocks, d_w_index + size_t(l) * E, p_hb, p_y,
                    pf_splits, pf_splits, d_done, st);
@@ -1712,6 +1789,7 @@ struct Engine {
     r.gpu_moe = span(pending_moe);
     r.h2d_transfer = span(pending_h2d);
     r.h2d_bytes = last_h2d_bytes;
+    for (double v : layer_raw_bytes) r.h2d_raw_bytes += v;
     r.others = std::max(0.0, r.target_total - r.attention - r.gpu_moe);
     *t = r;
   }

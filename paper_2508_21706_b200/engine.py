@@ -111,7 +111,7 @@ class VerifyEngine:
     def __init__(self, shape: ModelShape, *, max_batch: int, max_verify: int, max_seq: int, hbm_slots: int = 2,
                  expert_cache_bytes: int = 0, host_alias_layers: int = 0, device: int = 0, debug: bool = False,
                  ep_rank: int = 0, ep_size: int = 1, ep_group: Optional["EpGroup"] = None, kv_pages: int = 0,
-                 attn_cpu: bool = False, batch_one: bool = False):
+                 attn_cpu: bool = False, batch_one: bool = False, compress_experts: bool = False):
         self.shape = shape
         self.max_batch, self.max_verify, self.max_seq = max_batch, max_verify, max_seq
         if ep_size > 1 and ep_group is None:
@@ -122,7 +122,7 @@ class VerifyEngine:
         opt = L.EngineOptions(max_batch, max_verify, max_seq, hbm_slots, int(expert_cache_bytes),
                               host_alias_layers, device, L.ENGINE_DEBUG if debug else 0, ep_rank, ep_size,
                               None if ep_group is None else ep_group.handle, kv_pages, int(attn_cpu),
-                              int(batch_one))
+                              int(batch_one), int(compress_experts))
         cfg = shape.to_c()
         h = C.c_void_p()
         L.check(L.load().smo_engine_create(C.byref(cfg), C.byref(opt), C.byref(h)))
@@ -257,9 +257,8 @@ def step_roofline(shape: ModelShape, b: int, n: int, prefix: int, h2d_gbs: float
     e_bytes = s.expert_bytes
     activated = s.n_expert  # large batch: every expert activates
     h2d = (s.n_layers * activated - cached_blocks) * e_bytes / ep
-    if h2d_bytes is not None:  # BATCH_ONE: the router-selected experts actually streamed
+    if h2d_bytes is not None:  # the bytes actually streamed (BATCH_ONE selection, coded experts)
         h2d = h2d_bytes
-        activated = h2d_bytes / (s.n_layers * e_bytes) + cached_blocks / s.n_layers
     kv = 2 * (b / ep) * (prefix + n) * s.n_kv_heads * s.head_dim * 2
     dense = (s.hidden * (s.n_q_heads + 2 * s.n_kv_heads) * s.head_dim + s.n_q_heads * s.head_dim * s.hidden) * 2
     hbm = s.n_layers * (activated / ep * e_bytes + kv + dense) + s.vocab * s.hidden * 2

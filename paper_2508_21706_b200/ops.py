@@ -121,6 +121,25 @@ def moe_experts(x_perm, offsets, pool, *, h: int, h_i: int, n_expert: int, w_blo
     return hout, y[:used.value]
 
 
+def expert_encode(x, bits: int = 3):
+    """Lossless code of a bf16 tensor (numel % 1024 == 0) with `bits`-bit
+    exponent codes: returns (uint8 code, overflow) — overflow means a segment
+    needed > 32 escapes (retry with 4 bits or keep the tensor raw)."""
+    _req(x, _BF16, "x")
+    n = x.numel()
+    code = torch.empty(int(L.load().smo_expert_code_bytes(n, bits)), dtype=torch.uint8, device=x.device)
+    ovf = torch.zeros(1, dtype=torch.int32, device=x.device)
+    L.check(L.load().smo_expert_encode(_p(x), n, bits, _p(code), _p(ovf), _stream()))
+    return code, bool(ovf.item())
+
+
+def expert_decode(code, n: int, bits: int = 3):
+    """Inverse of expert_encode: n bf16 values."""
+    out = torch.empty(n, dtype=_BF16, device=code.device)
+    L.check(L.load().smo_expert_decode(_p(code), n, bits, _p(out), _stream()))
+    return out
+
+
 def router_topk(x, w_router, k: int, want_logits: bool = False):
     """K2. x [T, h] bf16, w_router [E, h] bf16 -> ids int32 [T,k], weights f32 [T,k] (, logits)."""
     _req(x, _BF16, "x")

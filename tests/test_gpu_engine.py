@@ -243,3 +243,27 @@ def test_batch_one_streams_only_routed_experts(cuda):
     assert np.array_equal(r0.target, r1.target) and np.array_equal(r0.acc_len, r1.acc_len)
     assert b0 == s.n_layers * s.n_expert * s.expert_bytes
     assert 0 < b1 <= s.n_layers * 4 * s.expert_bytes
+
+
+@pytest.mark.parametrize("batch_one", [False, True])
+def test_compressed_expert_stream_bit_identical(cuda, batch_one):
+    """compress_experts: experts cross the link in the lossless 11.4-bit code
+    and are expanded in HBM — verify results bit-identical to raw streaming,
+    1456/2048 of the bytes on the link."""
+    from paper_2508_21706_b200.engine import VerifyEngine
+    s = _shape()
+    b, n = 4, 5
+    prefix = np.array([300, 17, 64, 1], np.int32)
+    tokens = np.random.default_rng(8).integers(0, s.vocab, size=(b, n)).astype(np.int32)
+    out = {}
+    for comp in (False, True):
+        eng = VerifyEngine(s, max_batch=b, max_verify=n, max_seq=512, compress_experts=comp, batch_one=batch_one,
+                           expert_cache_bytes=2 * s.expert_bytes)
+        eng.fill_prefix(prefix)
+        r = eng.verify(tokens, prefix)
+        out[comp] = (r, eng.last_times()["h2d_bytes"])
+        eng.close()
+    (r0, b0), (r1, b1) = out[False], out[True]
+    assert np.array_equal(r0.target, r1.target)
+    assert np.array_equal(r0.acc_len, r1.acc_len) and np.array_equal(r0.bonus, r1.bonus)
+    assert b1 > 0 and abs(b1 / b0 - 1456 / 2048) < 1e-9

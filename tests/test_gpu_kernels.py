@@ -403,3 +403,67 @@ def test_verify_attention_paged_bit_identical(cuda, b, n, nq, nkv, d, prefix):
     vp[bt.long().view(-1)] = vf.reshape(b * max_pages, nkv, 128, d)
     got = ops.verify_attention(q, kp, vp, mask, pre, max(prefix), block_table=bt)
     assert torch.equal(got, ref)
+
+
+# ---------------------------------------------------------------- K5 codec
+def _np_decode_segment(seg: np.ndarray, bits: int) -> np.ndarray:
+    """The documented format (xfer.cu header), restated in numpy."""
+    base = int(seg[0])
+    lo = seg[16:1040].astype(np.uint32)
+    esc_code = (1 << bits) - 1
+    codes = np.zeros(1024, np.uint32)
+    for lane in range(32):
+        words = seg[1040 + 4 * bits * lane:1040 + 4 * bits * (lane + 1)].view(np.uint32)
+        acc = 0
+        for q, w in enumerate(words):
+            acc |= int(w) << (32 * q)
+        for j in range(32):
+            codes[lane * 32 + j] = (acc >> (bits * j)) & esc_code
+    esc = seg[1040 + 128 * bits:1040 + 128 * bits + 32]
+    e = np.zeros(1024, np.uint32)
+    k = 0
+    for i in range(1024):
+        if codes[i] == esc_code:
+            e[i] = esc[k]
+            k += 1
+        else:
+            e[i] = base + codes[i]
+    return (((lo & 0x80) << 8) | (e << 7) | (lo & 0x7F)).astype(np.uint16)
+
+
+@pytest.mark.parametrize("kind,bits", [("procedural", 3), ("procedural", 4), ("normal", 3), ("normal", 4),
+                                       ("wide", 4)])
+def test_expert_codec_lossless(cuda, oracle, kind, bits):
+    """smo_expert_encode/decode (the link codec of compress_experts): bit-exact
+    round trip; the byte layout matches the documented format. Uniform-init
+    weights fit 3-bit exponent codes; gaussian weights with zeros and large
+    outliers need 4 bits (3 bits overflows); exponents spread over all 256
+    values cannot be coded (the block then stays raw)."""
+    import torch
+    from paper_2508_21706_b200 import ops
+    n = 1024 * 300
+    if kind == "procedural":  # the engine's expert weights (DESIGN.md §3.1)
+        x = torch.from_numpy(oracle.fill_uniform_bf16(n, 0x5EED, 1234, math.sqrt(3.0 / 4096)).view(np.int16)).to(cuda)
+        x = x.view(torch.bfloat16)
+    elif kind == "normal":  # trained-weight-like: gaussian, exact zeros, a few outliers
+        g = torch.Generator(device=cuda).manual_seed(5)
+        x = (torch.randn(n, generator=g, device=cuda) * 0.02).to(torch.bfloat16)
+        x[::997] = 0
+        x[::4099] *= 64
+    else:  # exponents uniform over 0..255
+        g = torch.Generator(device=cuda).manual_seed(6)
+        x = torch.randint(0, 1 << 16, (n,), generator=g, device=cuda, dtype=torch.int32).to(torch.int16)
+        x = x.view(torch.bfloat16)
+    code, ovf = ops.expert_encode(x, bits)
+    if kind == "wide" or (kind == "normal" and bits == 3):
+        assert ovf
+        return
+    assert not ovf
+    assert code.numel() == n // 1024 * (1040 + 128 * bits + 32)
+    y = ops.expert_decode(code, n, bits)
+    assert torch.equal(y.view(torch.int16), x.view(torch.int16))
+    c = code.cpu().numpy()
+    xs = x.view(torch.int16).cpu().numpy().view(np.uint16)
+    sb = 1040 + 128 * bits + 32
+    for sgm in (0, 7, 299):
+        assert np.array_equal(_np_decode_segment(c[sgm * sb:(sgm + 1) * sb], bits), xs[sgm * 1024:(sgm + 1) * 1024])
