@@ -418,15 +418,16 @@ def run_ours(args):
     # live H2D link peak on this box (pinned, 2 GiB copies)
     hbuf = torch.empty(1 << 31, dtype=torch.uint8, pin_memory=True)
     dbuf = torch.empty(1 << 31, dtype=torch.uint8, device=dev)
+    h2d_peak = 0.0
     with torch.cuda.stream(stream):
         dbuf.copy_(hbuf, non_blocking=True)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(3):
+        for _ in range(4):  # best of four 2 GiB copies
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
             dbuf.copy_(hbuf, non_blocking=True)
-        e1.record(stream)
-    stream.synchronize()
-    h2d_peak = 3 * (1 << 31) / (e0.elapsed_time(e1) * 1e-3) / 1e9
+            e1.record(stream)
+            stream.synchronize()
+            h2d_peak = max(h2d_peak, (1 << 31) / (e0.elapsed_time(e1) * 1e-3) / 1e9)
     del hbuf, dbuf
     torch.cuda.empty_cache()
 
