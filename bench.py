@@ -525,6 +525,8 @@ def run_ours(args):
         "step_roofline": {"bound": roof["bound"], "t_roof_s": roof["t_roof_s"], "t_meas_s": t_step,
                           "frac": roof["t_roof_s"] / t_step, "h2d_peak_gbs": h2d_peak,
                           "hbm_peak_gbs": pk["hbm_gbs"], "times_s": roof["times"]},
+        "expert_tflops": (shape.n_layers * 2 * 3 * shape.hidden * shape.inter * b * n * shape.top_k / moe_t / 1e12
+                          if moe_t > 0 else None),
         "attention_roofline": {"bound": "hbm", "achieved": attn_bytes_step / stages["attention"] / 1e9
                                if stages["attention"] > 0 else None, "peak": pk["hbm_gbs"], "unit": "GB/s"},
         "stage_seconds_last_step": {k: stages[k] for k in ("target_total", "attention", "gpu_moe",

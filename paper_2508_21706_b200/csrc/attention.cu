@@ -744,6 +744,7 @@ AttnPlan plan_attention(const smo_attn_args& a, int sms) {
   }();
   if (cost(qa) < cost(qmin)) q = qa;
   pl.Q = std::max(q, (pl.C + 14) / 15);
+  if (const char* fq = std::getenv("SMO_ATTN_Q")) pl.Q = std::max(std::atoi(fq), (pl.C + 14) / 15);  // A/B runs
   pl.grid = (pl.total + pl.Q - 1) / pl.Q;
   // the layout is sized for the largest tile (128 rows) so that the counter
   // region sits at the same offset for every n: a workspace shared by calls
