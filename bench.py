@@ -493,6 +493,8 @@ def run_ours(args):
     # dominant GPU kernel by device time: K4 grouped SwiGLU (+down +combine),
     # HBM-bound: algorithmic bytes = expert weights read once per layer
     moe_bytes_step = shape.n_layers * (shape.n_expert // ep_size) * shape.expert_bytes
+    if args.moe_batching == "one":  # only routed experts are read: the streamed ones + the hot cache
+        moe_bytes_step = stages["h2d_raw_bytes"] + int(args.cache_gb * 1e9) // shape.expert_bytes * shape.expert_bytes
     moe_t = stages["gpu_moe"]
     attn_bytes_step = shape.n_layers * 2 * b * (prefix + n) * shape.n_kv_heads * shape.head_dim * 2
     line = {

@@ -14,13 +14,13 @@ pytestmark = pytest.mark.gpu
 B, N, PREFIX = 4, 5, 300
 
 
-def _run_ep(shape, P, tokens, prefix, s_max, debug=True):
+def _run_ep(shape, P, tokens, prefix, s_max, debug=True, **kw):
     import torch
     from paper_2508_21706_b200.engine import EpGroup, VerifyEngine
     grp = EpGroup.loopback(P)
     bl = B // P
     engines = [VerifyEngine(shape, max_batch=bl, max_verify=N, max_seq=s_max, debug=debug, ep_rank=r, ep_size=P,
-                            ep_group=grp) for r in range(P)]
+                            ep_group=grp, **kw) for r in range(P)]
     streams = [torch.cuda.Stream() for _ in range(P)]
     results, errors = [None] * P, []
     for r, e in enumerate(engines):
@@ -42,8 +42,8 @@ def _run_ep(shape, P, tokens, prefix, s_max, debug=True):
     return engines, results, grp
 
 
-@pytest.mark.parametrize("P", [2, 4])
-def test_ep_loopback_bit_identical_to_single_gpu(cuda, P):
+@pytest.mark.parametrize("P,compress", [(2, False), (4, False), (2, True)])
+def test_ep_loopback_bit_identical_to_single_gpu(cuda, P, compress):
     """Rank r's tokens go to every owner and come back; each token's result
     depends only on its own request, so rank r's EP outputs must equal a
     single-GPU engine run on rank r's requests alone, bit for bit (the
@@ -54,7 +54,7 @@ def test_ep_loopback_bit_identical_to_single_gpu(cuda, P):
     rng = np.random.default_rng(11)
     tokens = rng.integers(0, shape.vocab, size=(B, N)).astype(np.int32)
     prefix = np.array([PREFIX, PREFIX - 3, 200, 1], np.int32)
-    engines, results, grp = _run_ep(shape, P, tokens, prefix, s_max)
+    engines, results, grp = _run_ep(shape, P, tokens, prefix, s_max, compress_experts=compress)
     bl = B // P
     for r in range(P):
         ref = VerifyEngine(shape, max_batch=bl, max_verify=N, max_seq=s_max, debug=True)
@@ -70,7 +70,9 @@ def test_ep_loopback_bit_identical_to_single_gpu(cuda, P):
         ref.close()
     # each rank streamed only its shard of the experts
     t0 = engines[0].last_times()
-    assert t0["h2d_bytes"] == shape.n_layers * (shape.n_expert // P) * shape.expert_bytes
+    raw = shape.n_layers * (shape.n_expert // P) * shape.expert_bytes
+    assert t0["h2d_raw_bytes"] == raw
+    assert t0["h2d_bytes"] == (raw * 1456 // 2048 if compress else raw)  # coded blocks: 1456 B per 1024 weights
     for e in engines:
         e.close()
     grp.close()
