@@ -518,7 +518,7 @@ def run_ours(args):
                 "bytes_per_step": h2d_bytes, "copy_engine_busy_s": stages["h2d_transfer"],
                 "raw_bf16_bytes_per_step": raw_h2d, "raw_equivalent_gbs": raw_h2d / t_step / 1e9},
         "roofline": {"bound": "hbm", "kernel": "K4-MoE fused expert block (gate/up + SwiGLU + down, one "
-                     "persistent launch per layer) + combine, per step",
+                     "persistent launch per layer; CUDA events around the launch on its stream), per step",
                      "achieved": moe_bytes_step / moe_t / 1e9 if moe_t > 0 else None, "peak": pk["hbm_gbs"],
                      "unit": "GB/s", "frac": (moe_bytes_step / moe_t / 1e9) / pk["hbm_gbs"] if moe_t > 0 else None,
                      "traffic": moe_traffic_per_layer() if (args.model == "mixtral-8x7b" and ep_size == 1) else None, "traffic_unit": "dram bytes per layer (the fused expert "

@@ -656,6 +656,7 @@ void Engine::verify_core(int b, int n, const int32_t* tokens, const int32_t* par
   const int PT = T * K;  // (token, slot) pairs
   for (int l = 0; l < L; ++l) {
     Layer& ly = layers[l];
+    bool moe_end_recorded = false;
     SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 6), st));
     snap("x_in", l, x, size_t(T) * h * 4, st);
     rmsnorm(x, ones, T, h, cfg.rms_eps, xn, st);
@@ -808,6 +809,9 @@ void Engine::verify_core(int b, int n, const int32_t* tokens, const int32_t* par
       if (moe_fused) {
         moe_launch(xp, PT, h, hi, E, offsets, pool, blk_bytes, pool_blocks, d_w_index + size_t(l) * E, hbuf, ybuf,
                    moe_splits, moe_splits, d_done, st);
+        // GPU_MOE = the expert kernel itself (the bench's kernel roofline)
+        SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 5), st));
+        moe_end_recorded = true;
         SMO_CUDA_CHECK(cudaEventRecord(slot_free[l % slots], st));
         unpermute_combine(ybuf, pos, rw, T, K, h, x, st, moe_splits, size_t(PT) * h);
       } else {
@@ -848,7 +852,7 @@ void Engine::verify_core(int b, int n, const int32_t* tokens, const int32_t* par
       unpermute_combine(ybuf, pos, rw, T, K, h, x, st);
       }
     }
-    SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 5), st));
+    if (!moe_end_recorded) SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 5), st));
     moe_ev.push_back({tev(l * 8 + 4), tev(l * 8 + 5)});
     snap("x_out", l, x, size_t(T) * h * 4, st);
     if (!batch_one && l + slots < L) {

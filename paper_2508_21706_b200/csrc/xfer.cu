@@ -10,9 +10,9 @@
 // Segment = 1024 consecutive bf16 values, 16 + 1024 + 128 B + 32 bytes:
 //   [0, 16)               header: byte 0 = base exponent, byte 1 = escapes
 //   [16, 1040)            lo[i] = sign << 7 | mantissa (7 bits)
-//   [1040, 1040 + 128 B)  B-bit exponent codes, lane l's 32 codes in bytes
-//                         [4Bl, 4B(l+1)) (code c < 2^B - 1: exponent =
-//                         base + c; 2^B - 1: escape)
+//   [1040, 1040 + 128 B)  B-bit exponent codes in value order: value i's
+//                         code at bits [B i, B i + B), little-endian (code
+//                         c < 2^B - 1: exponent = base + c; 2^B - 1: escape)
 //   [.., + 32)            up to 32 escaped exponents, in position order
 // base: of the W = 2^B - 1 windows ending at e_max, e_max - 1, ..., e_max - 6
 // the one holding the most values (a few large outliers then escape instead
@@ -20,8 +20,9 @@
 // coded: the encoder raises a flag; callers retry with B = 4, then keep the
 // block raw (bf16) — lossless either way. Uniform-init weights code at B = 3
 // (0.8 % escapes), gaussian-like trained weights need B = 4.
-// One warp per segment in both directions: each lane owns 32 consecutive
-// values, escapes are ranked with a warp exclusive scan.
+// One warp per segment in both directions; lane l owns the 8-value groups
+// 32q + l, so every memory instruction is one contiguous run; escapes are
+// ranked in position order with a warp exclusive scan per group column.
 #include "common.cuh"
 
 namespace smo {
@@ -50,6 +51,27 @@ __device__ __forceinline__ int warp_excl_scan(int v, int lane, int* total) {
   return x - v;
 }
 
+// Lane l of a segment's warp owns the four 8-value groups G = 32q + l
+// (q = 0..3): every load and store instruction of the warp then touches one
+// contiguous run (512 B of bf16, 256 B of lo bytes, 32·B bytes of codes).
+template <int B>
+__device__ __forceinline__ uint32_t load_group_codes(const uint8_t* codes, int G) {
+  if constexpr (B == 4) return reinterpret_cast<const uint32_t*>(codes)[G];
+  const uint8_t* c = codes + 3 * G;
+  return uint32_t(c[0]) | (uint32_t(c[1]) << 8) | (uint32_t(c[2]) << 16);
+}
+template <int B>
+__device__ __forceinline__ void store_group_codes(uint8_t* codes, int G, uint32_t w) {
+  if constexpr (B == 4) {
+    reinterpret_cast<uint32_t*>(codes)[G] = w;
+  } else {
+    uint8_t* c = codes + 3 * G;
+    c[0] = uint8_t(w);
+    c[1] = uint8_t(w >> 8);
+    c[2] = uint8_t(w >> 16);
+  }
+}
+
 template <int B>
 __global__ void expert_encode_kernel(const uint16_t* __restrict__ src, size_t segs, uint8_t* __restrict__ dst,
                                      int* __restrict__ overflow) {
@@ -57,12 +79,12 @@ __global__ void expert_encode_kernel(const uint16_t* __restrict__ src, size_t se
   const size_t warp = (size_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x % 32;
   if (warp >= segs) return;
-  const uint16_t* s = src + warp * kSeg + lane * 32;
+  const uint16_t* s = src + warp * kSeg;
   uint8_t* d = dst + warp * F::kSegBytes;
-  uint16_t v[32];
+  uint16_t v[32];  // v[8q + j] = value 8 (32q + lane) + j
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const uint4 u = reinterpret_cast<const uint4*>(s)[q];
+    const uint4 u = reinterpret_cast<const uint4*>(s)[32 * q + lane];
     const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
@@ -95,82 +117,101 @@ __global__ void expert_encode_kernel(const uint16_t* __restrict__ src, size_t se
       base = b0;
     }
   }
-  uint32_t cw[B + 1];
+  // escapes in position order: group-major (q), then lane
+  int at[4], total = 0;
 #pragma unroll
-  for (int q = 0; q <= B; ++q) cw[q] = 0u;
-  int nesc = 0;
-  uint32_t lo[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+  for (int q = 0; q < 4; ++q) {
+    int cnt = 0;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const int e = (v[j] >> 7) & 0xff;
-    const uint32_t c = (e >= base && e < base + F::kWin) ? uint32_t(e - base) : F::kEscape;
-    nesc += c == F::kEscape;
-    const int p = B * j;
-    cw[p >> 5] |= c << (p & 31);
-    if ((p & 31) > 32 - B) cw[(p >> 5) + 1] |= c >> (32 - (p & 31));
-    lo[j >> 2] |= uint32_t(((v[j] >> 8) & 0x80) | (v[j] & 0x7f)) << (8 * (j & 3));
+    for (int j = 0; j < 8; ++j) {
+      const int e = (v[8 * q + j] >> 7) & 0xff;
+      cnt += (e >= base && e < base + F::kWin) ? 0 : 1;
+    }
+    int tq = 0;
+    at[q] = total + warp_excl_scan(cnt, lane, &tq);
+    total += tq;
   }
-  int total = 0;
-  int at = warp_excl_scan(nesc, lane, &total);
   if (total > kMaxEsc) {
     if (lane == 0) atomicOr(overflow, 1);
     return;
   }
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const int e = (v[j] >> 7) & 0xff;
-    if (!(e >= base && e < base + F::kWin)) d[F::kEscOff + at++] = uint8_t(e);
-  }
-  uint4* lo4 = reinterpret_cast<uint4*>(d + kLoOff + lane * 32);
-  lo4[0] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-  lo4[1] = make_uint4(lo[4], lo[5], lo[6], lo[7]);
-  uint32_t* c4 = reinterpret_cast<uint32_t*>(d + kCodeOff + lane * 4 * B);
+  for (int q = 0; q < 4; ++q) {
+    const int G = 32 * q + lane;
+    uint32_t code = 0u, lo0 = 0u, lo1 = 0u;
 #pragma unroll
-  for (int q = 0; q < B; ++q) c4[q] = cw[q];
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t x = v[8 * q + j];
+      const int e = int((x >> 7) & 0xffu);
+      const bool in = e >= base && e < base + F::kWin;
+      code |= (in ? uint32_t(e - base) : F::kEscape) << (B * j);
+      if (!in) d[F::kEscOff + at[q]++] = uint8_t(e);
+      const uint32_t lo = ((x >> 8) & 0x80u) | (x & 0x7fu);
+      if (j < 4) lo0 |= lo << (8 * j);
+      else lo1 |= lo << (8 * (j - 4));
+    }
+    reinterpret_cast<uint2*>(d + kLoOff)[G] = make_uint2(lo0, lo1);
+    store_group_codes<B>(d + kCodeOff, G, code);
+  }
   if (lane == 0) *reinterpret_cast<uint4*>(d) = make_uint4(uint32_t(base) | (uint32_t(total) << 8), 0u, 0u, 0u);
   if (lane < kMaxEsc - total) d[F::kEscOff + total + lane] = 0;  // deterministic padding
 }
 
+// Decode stages the warp's whole segment in shared memory with coalesced
+// 16-byte loads first (3 per lane, all in flight together), then expands it
+// from there — the byte-granular code / escape reads never wait on DRAM.
+constexpr int kDecWarps = 8;
+constexpr int kDecSegs = 1;  // segments per warp (2: 135 us vs 117 us per Mixtral block, profiles/r01_codec.md)
 template <int B>
-__global__ void expert_decode_kernel(const uint8_t* __restrict__ src, size_t segs, uint16_t* __restrict__ dst) {
+__global__ void __launch_bounds__(32 * kDecWarps) expert_decode_kernel(const uint8_t* __restrict__ src, size_t segs,
+                                                                       uint16_t* __restrict__ dst) {
   using F = Fmt<B>;
-  const size_t warp = (size_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
-  const int lane = threadIdx.x % 32;
-  if (warp >= segs) return;
-  const uint8_t* s = src + warp * F::kSegBytes;
-  const uint32_t hdr = *reinterpret_cast<const uint32_t*>(s);
-  const int base = int(hdr & 0xffu);
-  const uint4 la = reinterpret_cast<const uint4*>(s + kLoOff + lane * 32)[0];
-  const uint4 lb = reinterpret_cast<const uint4*>(s + kLoOff + lane * 32)[1];
-  const uint32_t lo[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
-  const uint32_t* c4 = reinterpret_cast<const uint32_t*>(s + kCodeOff + lane * 4 * B);
-  uint32_t cw[B + 1];
+  constexpr int kVec = F::kSegBytes / 16;  // 91 (B = 3) or 99 (B = 4) uint4 per segment
+  constexpr int kLd = (kDecSegs * kVec + 31) / 32;
+  __shared__ uint4 stage[kDecWarps][kDecSegs * kVec];
+  const int wib = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const size_t seg0 = (size_t(blockIdx.x) * kDecWarps + wib) * kDecSegs;
+  if (seg0 >= segs) return;
+  const int nseg = segs - seg0 < size_t(kDecSegs) ? int(segs - seg0) : kDecSegs;
+  // all of the warp's segments in flight at once (contiguous in the code)
+  const uint4* g = reinterpret_cast<const uint4*>(src + seg0 * F::kSegBytes);
+  uint4 r[kLd];
 #pragma unroll
-  for (int q = 0; q < B; ++q) cw[q] = c4[q];
-  cw[B] = 0u;
-  uint32_t codes[32];
-  int nesc = 0;
+  for (int i = 0; i < kLd; ++i)
+    if (lane + 32 * i < nseg * kVec) r[i] = g[lane + 32 * i];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const int p = B * j;
-    const uint64_t pair = (uint64_t(cw[(p >> 5) + 1]) << 32) | cw[p >> 5];
-    codes[j] = uint32_t(pair >> (p & 31)) & F::kEscape;
-    nesc += codes[j] == F::kEscape;
-  }
+  for (int i = 0; i < kLd; ++i)
+    if (lane + 32 * i < nseg * kVec) stage[wib][lane + 32 * i] = r[i];
+  __syncwarp();
+  for (int sg = 0; sg < nseg; ++sg) {
+  const uint8_t* s = reinterpret_cast<const uint8_t*>(stage[wib] + sg * kVec);
+  const int base = int(s[0]);
+  uint4* d = reinterpret_cast<uint4*>(dst + (seg0 + sg) * kSeg);
   int total = 0;
-  int at = warp_excl_scan(nesc, lane, &total);
-  uint32_t out[16];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const uint32_t e = codes[j] == F::kEscape ? uint32_t(s[F::kEscOff + at++]) : uint32_t(base) + codes[j];
-    const uint32_t bb = (lo[j >> 2] >> (8 * (j & 3))) & 0xffu;
-    const uint32_t val = ((bb & 0x80u) << 8) | (e << 7) | (bb & 0x7fu);
-    if (j & 1) out[j >> 1] |= val << 16;
-    else out[j >> 1] = val;
+  for (int q = 0; q < 4; ++q) {
+    const int G = 32 * q + lane;
+    const uint2 lo = reinterpret_cast<const uint2*>(s + kLoOff)[G];
+    const uint32_t code = load_group_codes<B>(s + kCodeOff, G);
+    int cnt = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) cnt += ((code >> (B * j)) & F::kEscape) == F::kEscape;
+    int tq = 0;
+    int at = total + warp_excl_scan(cnt, lane, &tq);
+    total += tq;
+    uint32_t out[4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t c = (code >> (B * j)) & F::kEscape;
+      const uint32_t e = c == F::kEscape ? uint32_t(s[F::kEscOff + at++]) : uint32_t(base) + c;
+      const uint32_t bb = ((j < 4 ? lo.x : lo.y) >> (8 * (j & 3))) & 0xffu;
+      const uint32_t val = ((bb & 0x80u) << 8) | (e << 7) | (bb & 0x7fu);
+      if (j & 1) out[j >> 1] |= val << 16;
+      else out[j >> 1] = val;
+    }
+    d[G] = make_uint4(out[0], out[1], out[2], out[3]);
   }
-  uint4* d = reinterpret_cast<uint4*>(dst + warp * kSeg + lane * 32);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) d[q] = make_uint4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
+  }
 }
 
 }  // namespace
@@ -203,8 +244,8 @@ void expert_decode(const void* src, size_t count, int bits, void* dst, cudaStrea
   SMO_REQUIRE(bits == 3 || bits == 4, "expert codec: bits must be 3 or 4");
   const size_t segs = count / kSeg;
   if (!segs) return;
-  const int threads = 256;
-  const unsigned grid = unsigned((segs * 32 + threads - 1) / threads);
+  const int threads = 32 * kDecWarps;
+  const unsigned grid = unsigned((segs + kDecWarps * kDecSegs - 1) / (kDecWarps * kDecSegs));
   auto s8 = reinterpret_cast<const uint8_t*>(src);
   auto d16 = reinterpret_cast<uint16_t*>(dst);
   if (bits == 3) expert_decode_kernel<3><<<grid, threads, 0, st>>>(s8, segs, d16);

@@ -411,14 +411,9 @@ def _np_decode_segment(seg: np.ndarray, bits: int) -> np.ndarray:
     base = int(seg[0])
     lo = seg[16:1040].astype(np.uint32)
     esc_code = (1 << bits) - 1
-    codes = np.zeros(1024, np.uint32)
-    for lane in range(32):
-        words = seg[1040 + 4 * bits * lane:1040 + 4 * bits * (lane + 1)].view(np.uint32)
-        acc = 0
-        for q, w in enumerate(words):
-            acc |= int(w) << (32 * q)
-        for j in range(32):
-            codes[lane * 32 + j] = (acc >> (bits * j)) & esc_code
+    area = seg[1040:1040 + 128 * bits]
+    acc = int.from_bytes(area.tobytes(), "little")  # value i's code at bits [bits*i, bits*i + bits)
+    codes = np.array([(acc >> (bits * i)) & esc_code for i in range(1024)], np.uint32)
     esc = seg[1040 + 128 * bits:1040 + 128 * bits + 32]
     e = np.zeros(1024, np.uint32)
     k = 0
