@@ -300,6 +300,16 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def codec_traffic_per_block():
+    """dram__bytes_read+write of one expert_decode launch (one Mixtral expert
+    block) from the committed ncu capture (profiles/r01f_traffic.json)."""
+    try:
+        k = json.load(open(os.path.join(ROOT, "profiles", "r01f_traffic.json")))["kernels"]["K5_expert_decode"]
+        return k["dram_read_bytes"] + k["dram_write_bytes"]
+    except Exception:
+        return None
+
+
 def moe_traffic_per_layer():
     """dram__bytes_read+write of one layer's expert block (the fused K4-MoE
     launch) from the committed ncu --set full capture of the bench step
@@ -497,6 +507,26 @@ def run_ours(args):
         moe_bytes_step = stages["h2d_raw_bytes"] + int(args.cache_gb * 1e9) // shape.expert_bytes * shape.expert_bytes
     moe_t = stages["gpu_moe"]
     attn_bytes_step = shape.n_layers * 2 * b * (prefix + n) * shape.n_kv_heads * shape.head_dim * 2
+    # the fused expert kernel (per step: expert bytes / kernel time from CUDA events on its stream)
+    moe_roof = {"bound": "hbm", "kernel": "K4-MoE fused expert block (gate/up + SwiGLU + down, one persistent launch "
+                "per layer; CUDA events around the launch on its stream), per step",
+                "achieved": moe_bytes_step / moe_t / 1e9 if moe_t > 0 else None, "peak": pk["hbm_gbs"],
+                "unit": "GB/s", "frac": (moe_bytes_step / moe_t / 1e9) / pk["hbm_gbs"] if moe_t > 0 else None,
+                "traffic": moe_traffic_per_layer() if (args.model == "mixtral-8x7b" and ep_size == 1) else None,
+                "traffic_unit": "dram bytes per layer (the fused expert launch, ncu profiles/r01c_traffic.json); "
+                "algorithmic per layer = " + str((shape.n_expert // ep_size) * shape.expert_bytes),
+                "peak_kind": pk_kind}
+    # with the coded transfer the block expansion is the largest device-time kernel
+    # (profiles/r01f_launches.md): algorithmic bytes = code read + bf16 written
+    codec_roof = None
+    if args.compress and stages.get("codec", 0) > 0:
+        cb = stages["h2d_bytes"] + stages["h2d_raw_bytes"]
+        codec_roof = {"bound": "hbm", "kernel": "K5 expert_decode (coded blocks -> bf16 HBM slot), per step",
+                      "achieved": cb / stages["codec"] / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                      "frac": cb / stages["codec"] / 1e9 / pk["hbm_gbs"], "traffic": codec_traffic_per_block(),
+                      "traffic_unit": "dram bytes per expert block (one decode launch, ncu profiles/r01f_traffic.json);"
+                      " algorithmic per block = " + str(int(shape.expert_bytes * (1 + 1456 / 2048))),
+                      "peak_kind": pk_kind}
     line = {
         "metric": "verified decode tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -517,13 +547,8 @@ def run_ours(args):
         "h2d": {"achieved_gbs": h2d_bytes / t_step / 1e9, "link_peak_gbs": h2d_peak,
                 "bytes_per_step": h2d_bytes, "copy_engine_busy_s": stages["h2d_transfer"],
                 "raw_bf16_bytes_per_step": raw_h2d, "raw_equivalent_gbs": raw_h2d / t_step / 1e9},
-        "roofline": {"bound": "hbm", "kernel": "K4-MoE fused expert block (gate/up + SwiGLU + down, one "
-                     "persistent launch per layer; CUDA events around the launch on its stream), per step",
-                     "achieved": moe_bytes_step / moe_t / 1e9 if moe_t > 0 else None, "peak": pk["hbm_gbs"],
-                     "unit": "GB/s", "frac": (moe_bytes_step / moe_t / 1e9) / pk["hbm_gbs"] if moe_t > 0 else None,
-                     "traffic": moe_traffic_per_layer() if (args.model == "mixtral-8x7b" and ep_size == 1) else None, "traffic_unit": "dram bytes per layer (the fused expert "
-                     "launch, ncu profiles/r01c_traffic.json); algorithmic per layer = " + str(
-                         (shape.n_expert // ep_size) * shape.expert_bytes), "peak_kind": pk_kind},
+        "roofline": codec_roof if codec_roof else moe_roof,
+        "expert_roofline": moe_roof,
         "step_roofline": {"bound": roof["bound"], "t_roof_s": roof["t_roof_s"], "t_meas_s": t_step,
                           "frac": roof["t_roof_s"] / t_step, "h2d_peak_gbs": h2d_peak,
                           "hbm_peak_gbs": pk["hbm_gbs"], "times_s": roof["times"]},
@@ -531,7 +556,7 @@ def run_ours(args):
                           if moe_t > 0 else None),
         "attention_roofline": {"bound": "hbm", "achieved": attn_bytes_step / stages["attention"] / 1e9
                                if stages["attention"] > 0 else None, "peak": pk["hbm_gbs"], "unit": "GB/s"},
-        "stage_seconds_last_step": {k: stages[k] for k in ("target_total", "attention", "gpu_moe",
+        "stage_seconds_last_step": {k: stages[k] for k in ("target_total", "attention", "gpu_moe", "codec",
                                                            "h2d_transfer", "others")},
         "gpu_launches": launches, "engine_create_s": t_create,
     }

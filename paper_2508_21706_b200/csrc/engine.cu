@@ -54,9 +54,13 @@ void Engine::bt_sync(cudaStream_t st) {
 // on the compute stream after slot_ready(l)
 void Engine::decode_slot(int l, cudaStream_t st) {
   const int s = l % slots;
+  if (coded_streamed[size_t(l)].empty()) return;
+  SMO_CUDA_CHECK(cudaEventRecord(dec_ev[size_t(2 * l)], st));
   for (int le : coded_streamed[size_t(l)])
     expert_decode(cstage + (size_t(s) * E_loc + le) * cblk_bytes, blk_elems, code_bits(l, le),
                   pool + (size_t(s) * E_loc + le) * blk_elems, st);
+  SMO_CUDA_CHECK(cudaEventRecord(dec_ev[size_t(2 * l + 1)], st));
+  step_dec_ev.push_back({dec_ev[size_t(2 * l)], dec_ev[size_t(2 * l + 1)]});
 }
 
 void Engine::create() {
@@ -409,6 +413,8 @@ void Engine::create() {
   for (auto& e : ev) SMO_CUDA_CHECK(cudaEventCreate(&e));
   draft_ev.resize(size_t(maxN) + 1);
   for (auto& e : draft_ev) SMO_CUDA_CHECK(cudaEventCreate(&e));
+  dec_ev.resize(size_t(2) * L);
+  for (auto& e : dec_ev) SMO_CUDA_CHECK(cudaEventCreate(&e));
   SMO_CUDA_CHECK(cudaDeviceSynchronize());
 }
 
@@ -634,6 +640,7 @@ void Engine::begin_step(cudaStream_t st, bool prefetch) {
   SMO_CUDA_CHECK(cudaStreamWaitEvent(copy, ev[0], 0));
   step_h2d_bytes = 0;
   step_h2d_ev.clear();
+  step_dec_ev.clear();
   std::fill(layer_bytes.begin(), layer_bytes.end(), 0.0);
   std::fill(layer_raw_bytes.begin(), layer_raw_bytes.end(), 0.0);
   for (int l = 0; prefetch && l < std::min(slots, L); ++l) {
@@ -940,6 +947,7 @@ void Engine::times(smo_stage_times* t) {
   r.gpu_moe = span(pending_moe);
   r.h2d_transfer = span(pending_h2d);
   r.h2d_bytes = last_h2d_bytes;
+  r.codec = span(step_dec_ev);
   for (double v : layer_raw_bytes) r.h2d_raw_bytes += v;
   r.others = std::max(0.0, r.target_total - r.attention - r.gpu_moe);
   *t = r;

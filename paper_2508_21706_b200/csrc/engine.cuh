@@ -156,6 +156,8 @@ struct Engine {
   std::vector<uint8_t> blk_coded;         // [host_alias * E_loc] exponent bits of the host block (0 = raw)
   uint8_t* cstage = nullptr;              // [slots][E_loc][cblk_bytes]
   std::vector<std::vector<int>> coded_streamed;  // per layer: local experts streamed coded
+  std::vector<cudaEvent_t> dec_ev;        // [2L] around each layer's block expansion
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> step_dec_ev;
   std::vector<cudaEvent_t> draft_ev;  // [maxN + 1]: boundaries of the drafter steps
   int last_draft_steps = 0;
   std::vector<uint16_t*> host_bufs;  // pinned, E blocks each
@@ -211,6 +213,7 @@ struct Engine {
     for (auto e : slot_free) cudaEventDestroy(e);
     for (auto e : ev) cudaEventDestroy(e);
     for (auto e : draft_ev) cudaEventDestroy(e);
+    for (auto e : dec_ev) cudaEventDestroy(e);
     if (route_ev) cudaEventDestroy(route_ev);
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     for (auto hb : host_bufs) cudaFreeHost(hb);

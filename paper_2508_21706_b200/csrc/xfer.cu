@@ -38,6 +38,7 @@ struct Fmt {
   static constexpr int kSegBytes = kEscOff + kMaxEsc;  // 1456 (B=3), 1584 (B=4)
   static constexpr int kWin = (1 << B) - 1;         // exponents a code can name
   static constexpr uint32_t kEscape = (1u << B) - 1u;
+  static constexpr uint32_t kLsbMask = B == 3 ? 0x00249249u : 0x11111111u;  // bit 0 of each of 8 fields
 };
 
 __device__ __forceinline__ int warp_excl_scan(int v, int lane, int* total) {
@@ -187,27 +188,52 @@ __global__ void __launch_bounds__(32 * kDecWarps) expert_decode_kernel(const uin
   const uint8_t* s = reinterpret_cast<const uint8_t*>(stage[wib] + sg * kVec);
   const int base = int(s[0]);
   uint4* d = reinterpret_cast<uint4*>(dst + (seg0 + sg) * kSeg);
-  int total = 0;
+  // escape counts of the lane's four groups packed in 8-bit fields (each
+  // column sum <= 32 escapes per segment): one warp scan ranks them all
+  uint2 lo[4];
+  uint32_t code[4], em[4];
+  uint32_t packed = 0u;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int G = 32 * q + lane;
-    const uint2 lo = reinterpret_cast<const uint2*>(s + kLoOff)[G];
-    const uint32_t code = load_group_codes<B>(s + kCodeOff, G);
-    int cnt = 0;
+    lo[q] = reinterpret_cast<const uint2*>(s + kLoOff)[G];
+    code[q] = load_group_codes<B>(s + kCodeOff, G);
+    // escape fields are all-ones: AND the field's bits down onto its LSB
+    uint32_t m = code[q];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) cnt += ((code >> (B * j)) & F::kEscape) == F::kEscape;
-    int tq = 0;
-    int at = total + warp_excl_scan(cnt, lane, &tq);
-    total += tq;
+    for (int b = 1; b < B; ++b) m &= code[q] >> b;
+    em[q] = m & F::kLsbMask;
+    packed |= uint32_t(__popc(em[q])) << (8 * q);
+  }
+  int ptot = 0;
+  const uint32_t pexcl = uint32_t(warp_excl_scan(int(packed), lane, &ptot));
+  int col = 0;  // escapes in the columns q' < q (all lanes)
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int G = 32 * q + lane;
+    int at = col + int((pexcl >> (8 * q)) & 0xffu);
+    col += (ptot >> (8 * q)) & 0xff;
+    // two values per 32-bit word: lo bytes spread to 16-bit lanes (PRMT),
+    // exponents base + code added in both lanes at once; escaped values
+    // (rare) are patched afterwards, so warps never split into two paths
     uint32_t out[4];
+    const uint32_t base2 = uint32_t(base) * 0x10001u;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint32_t c = (code >> (B * j)) & F::kEscape;
-      const uint32_t e = c == F::kEscape ? uint32_t(s[F::kEscOff + at++]) : uint32_t(base) + c;
-      const uint32_t bb = ((j < 4 ? lo.x : lo.y) >> (8 * (j & 3))) & 0xffu;
-      const uint32_t val = ((bb & 0x80u) << 8) | (e << 7) | (bb & 0x7fu);
-      if (j & 1) out[j >> 1] |= val << 16;
-      else out[j >> 1] = val;
+    for (int p2 = 0; p2 < 4; ++p2) {
+      const uint32_t lw = p2 < 2 ? lo[q].x : lo[q].y;
+      const uint32_t l16 = __byte_perm(lw, 0u, (p2 & 1) ? 0x4342u : 0x4140u);
+      const uint32_t c2 =
+          ((code[q] >> (2 * B * p2)) & F::kEscape) | (((code[q] >> (2 * B * p2 + B)) & F::kEscape) << 16);
+      out[p2] = ((l16 & 0x00800080u) << 8) | (l16 & 0x007f007fu) | ((base2 + c2) << 7);
+    }
+    for (uint32_t m = em[q]; m; m &= m - 1u) {
+      const int j = (__ffs(m) - 1) / B;  // escapes in position order
+      const int sh = 7 + 16 * (j & 1);
+      const uint32_t e = uint32_t(s[F::kEscOff + at++]);
+      const uint32_t keep = ~(0xffu << sh);
+#pragma unroll
+      for (int p2 = 0; p2 < 4; ++p2)
+        if (p2 == (j >> 1)) out[p2] = (out[p2] & keep) | (e << sh);
     }
     d[G] = make_uint4(out[0], out[1], out[2], out[3]);
   }
