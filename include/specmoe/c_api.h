@@ -172,7 +172,8 @@ smo_status smo_gemm(const smo_gemm_args* a, smo_stream stream);
  *            sum them with smo_unpermute_combine_split.
  * x_perm bf16 [rows, h] grouped by offsets [E+1] (device); expert e uses pool
  * block w_index[e] = [W1 | W3 | W2] (nn.Linear layouts), blocks
- * w_block_stride bytes apart. scratch: >= E int32 (device). E <= 64,
+ * w_block_stride bytes apart. scratch: >= 65 int32 (device), zero before the
+ * first call (every call leaves it zero). E <= 64,
  * h and h_i multiples of 128. The roofline.hpp:56-64 expert cost.          */
 smo_status smo_moe_experts(const void* x_perm, int32_t rows, int32_t h, int32_t h_i, int32_t E,
                            const int32_t* offsets, const void* w_pool, uint64_t w_block_stride,

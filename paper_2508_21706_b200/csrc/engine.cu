@@ -56,9 +56,22 @@ void Engine::decode_slot(int l, cudaStream_t st) {
   const int s = l % slots;
   if (coded_streamed[size_t(l)].empty()) return;
   SMO_CUDA_CHECK(cudaEventRecord(dec_ev[size_t(2 * l)], st));
-  for (int le : coded_streamed[size_t(l)])
-    expert_decode(cstage + (size_t(s) * E_loc + le) * cblk_bytes, blk_elems, code_bits(l, le),
-                  pool + (size_t(s) * E_loc + le) * blk_elems, st);
+  for (int bits = 3; bits <= 4; ++bits) {  // one launch per code width (blocks of a layer share it in practice)
+    const void* src[64];
+    void* dst[64];
+    int n = 0;
+    for (int le : coded_streamed[size_t(l)]) {
+      if (code_bits(l, le) != bits) continue;
+      if (n == 64) {
+        expert_decode_blocks(src, dst, n, blk_elems, bits, st);
+        n = 0;
+      }
+      src[n] = cstage + (size_t(s) * E_loc + le) * cblk_bytes;
+      dst[n] = pool + (size_t(s) * E_loc + le) * blk_elems;
+      ++n;
+    }
+    expert_decode_blocks(src, dst, n, blk_elems, bits, st);
+  }
   SMO_CUDA_CHECK(cudaEventRecord(dec_ev[size_t(2 * l + 1)], st));
   step_dec_ev.push_back({dec_ev[size_t(2 * l)], dec_ev[size_t(2 * l + 1)]});
 }
@@ -327,7 +340,8 @@ void Engine::create() {
   // same S, so expert parallelism reproduces one GPU bit for bit)
   moe_splits = moe_fused ? pick_moe_splits(maxT * K, h, hi, E, 4) : 1;
   ybuf = dalloc<float>(size_t(moe_splits) * P * h);
-  d_done = dalloc<int>(64);
+  d_done = dalloc<int>(128);
+  SMO_CUDA_CHECK(cudaMemset(d_done, 0, 128 * sizeof(int)));  // the expert kernel leaves its counters zero
   amax_v = dalloc<float>(size_t(maxT) * (V / 128));
   amax_i = dalloc<int32_t>(size_t(maxT) * (V / 128));
   target = dalloc<int32_t>(maxT);

@@ -72,6 +72,7 @@ int pick_moe_splits(int rows, int h, int hi, int E, int max_splits);
 size_t expert_code_bytes(size_t count, int bits);
 void expert_encode(const void* src, size_t count, int bits, void* dst, int* overflow, cudaStream_t st);
 void expert_decode(const void* src, size_t count, int bits, void* dst, cudaStream_t st);
+void expert_decode_blocks(const void* const* srcs, void* const* dsts, int n, size_t count, int bits, cudaStream_t st);
 
 // Procedural tensor ids; the oracle tests use the same ids.
 namespace tid {

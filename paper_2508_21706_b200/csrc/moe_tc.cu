@@ -285,6 +285,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<512>(tmem);
+  // the last CTA to finish zeroes the counters for the next launch (every
+  // wait on them is over: all other CTAs have exited their unit loops)
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(p.done + kMaxE, 1) == int(gridDim.x) - 1) {
+      for (int e = 0; e < p.E; ++e) atomicExch(p.done + e, 0);
+      atomicExch(p.done + kMaxE, 0);
+    }
+  }
 }
 
 int sm_count() {
@@ -321,10 +330,11 @@ int pick_moe_splits(int rows, int h, int hi, int E, int max_splits) {
 // Expert block of one layer: H = SwiGLU(x_perm W1^T, x_perm W3^T) per expert,
 // sum_s y[s] = H W2^T (K split in `splits` slices; 0 = pick_moe_splits;
 // returned). Callers that must reproduce another launch bit for bit (expert
-// parallelism vs one GPU) pass the same explicit splits. x_perm bf16
+// parallelism vs one GPU) pass the same explicit splits. done: >= 65 ints,
+// zero before the first launch; the kernel leaves them zero. x_perm bf16
 // [rows, h] grouped by offsets [E+1]; pool blocks [W1 | W3 | W2]
 // (w_block_stride bytes apart), w_index [E]; y has room for max_splits
-// slices of [rows, h]; done: >= E ints of scratch (zeroed here).
+// slices of [rows, h].
 int moe_launch(const void* x_perm, int rows, int h, int hi, int E, const int32_t* offsets, const void* pool,
                uint64_t w_block_stride, int pool_blocks, const int32_t* w_index, void* hbuf, float* y, int splits,
                int max_splits, int* done, cudaStream_t st) {
@@ -382,7 +392,6 @@ int moe_launch(const void* x_perm, int rows, int h, int hi, int E, const int32_t
     SMO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr_set = true;
   }
-  SMO_CUDA_CHECK(cudaMemsetAsync(done, 0, size_t(E) * sizeof(int), st));
   // one CTA per SM, co-resident (cooperative): down units wait on gate/up
   // units of other CTAs
   cudaLaunchConfig_t cfg{};

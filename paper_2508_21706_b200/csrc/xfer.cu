@@ -163,10 +163,19 @@ __global__ void expert_encode_kernel(const uint16_t* __restrict__ src, size_t se
 // from there — the byte-granular code / escape reads never wait on DRAM.
 constexpr int kDecWarps = 8;
 constexpr int kDecSegs = 1;  // segments per warp (2: 135 us vs 117 us per Mixtral block, profiles/r01_codec.md)
+// Up to 64 equally sized blocks per launch (one layer's experts): blockIdx.y
+// picks the block, so a layer's expansion is one launch with no tail per block.
+struct DecodeJobs {
+  const uint8_t* src[64];
+  uint16_t* dst[64];
+};
+
 template <int B>
-__global__ void __launch_bounds__(32 * kDecWarps) expert_decode_kernel(const uint8_t* __restrict__ src, size_t segs,
-                                                                       uint16_t* __restrict__ dst) {
+__global__ void __launch_bounds__(32 * kDecWarps) expert_decode_kernel(const __grid_constant__ DecodeJobs jobs,
+                                                                       size_t segs) {
   using F = Fmt<B>;
+  const uint8_t* __restrict__ src = jobs.src[blockIdx.y];
+  uint16_t* __restrict__ dst = jobs.dst[blockIdx.y];
   constexpr int kVec = F::kSegBytes / 16;  // 91 (B = 3) or 99 (B = 4) uint4 per segment
   constexpr int kLd = (kDecSegs * kVec + 31) / 32;
   __shared__ uint4 stage[kDecWarps][kDecSegs * kVec];
@@ -265,19 +274,28 @@ void expert_encode(const void* src, size_t count, int bits, void* dst, int* over
   SMO_CUDA_CHECK(cudaGetLastError());
 }
 
-void expert_decode(const void* src, size_t count, int bits, void* dst, cudaStream_t st) {
-  SMO_REQUIRE(src && dst && count % kSeg == 0, "expert codec: count must be a multiple of 1024");
+// Expand n blocks of `count` values each (srcs[i] -> dsts[i], all `bits`) in one launch.
+void expert_decode_blocks(const void* const* srcs, void* const* dsts, int n, size_t count, int bits, cudaStream_t st) {
+  SMO_REQUIRE(n >= 0 && n <= 64 && count % kSeg == 0, "expert codec: up to 64 blocks of a multiple of 1024 values");
   SMO_REQUIRE(bits == 3 || bits == 4, "expert codec: bits must be 3 or 4");
   const size_t segs = count / kSeg;
-  if (!segs) return;
-  const int threads = 32 * kDecWarps;
-  const unsigned grid = unsigned((segs + kDecWarps * kDecSegs - 1) / (kDecWarps * kDecSegs));
-  auto s8 = reinterpret_cast<const uint8_t*>(src);
-  auto d16 = reinterpret_cast<uint16_t*>(dst);
-  if (bits == 3) expert_decode_kernel<3><<<grid, threads, 0, st>>>(s8, segs, d16);
-  else expert_decode_kernel<4><<<grid, threads, 0, st>>>(s8, segs, d16);
+  if (!segs || !n) return;
+  DecodeJobs jobs{};
+  for (int i = 0; i < n; ++i) {
+    SMO_REQUIRE(srcs[i] && dsts[i], "expert codec: null block");
+    jobs.src[i] = reinterpret_cast<const uint8_t*>(srcs[i]);
+    jobs.dst[i] = reinterpret_cast<uint16_t*>(dsts[i]);
+  }
+  const dim3 grid(unsigned((segs + kDecWarps * kDecSegs - 1) / (kDecWarps * kDecSegs)), unsigned(n));
+  if (bits == 3) expert_decode_kernel<3><<<grid, 32 * kDecWarps, 0, st>>>(jobs, segs);
+  else expert_decode_kernel<4><<<grid, 32 * kDecWarps, 0, st>>>(jobs, segs);
   count_launch();
   SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+void expert_decode(const void* src, size_t count, int bits, void* dst, cudaStream_t st) {
+  SMO_REQUIRE(src && dst && count % kSeg == 0, "expert codec: count must be a multiple of 1024");
+  expert_decode_blocks(&src, &dst, 1, count, bits, st);
 }
 
 }  // namespace smo

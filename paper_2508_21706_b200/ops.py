@@ -113,7 +113,7 @@ def moe_experts(x_perm, offsets, pool, *, h: int, h_i: int, n_expert: int, w_blo
         w_index = torch.arange(n_expert, dtype=torch.int32, device=dev)
     hout = torch.empty((rows, h_i), dtype=_BF16, device=dev)
     y = torch.empty((splits or 4, rows, h), dtype=torch.float32, device=dev)
-    scratch = torch.empty(64, dtype=torch.int32, device=dev)
+    scratch = torch.zeros(128, dtype=torch.int32, device=dev)
     used = C.c_int32(0)
     L.check(L.load().smo_moe_experts(_p(x_perm), rows, h, h_i, n_expert, _p(offsets), _p(pool), w_block_stride,
                                      w_pool_blocks, _p(w_index), _p(hout), _p(y), splits, C.byref(used), _p(scratch),

@@ -79,7 +79,7 @@ def moe(T=288, h=4096, hi=14336, E=8, k=2, split=0):
         ops.gemm(hbuf, pool[2 * hi * h:], epilogue=L.EPI_F32, out=y, row_offsets=off, groups=E,
                  w_block_stride=blk * 2, w_pool_blocks=E, N=h, max_rows_per_group=T, split_k=split)
     y4 = torch.empty((4, T * k, h), dtype=torch.float32, device=dev)
-    scratch = torch.empty(64, dtype=torch.int32, device=dev)
+    scratch = torch.zeros(128, dtype=torch.int32, device=dev)
     widx = torch.arange(E, dtype=torch.int32, device=dev)
 
     def fused():
