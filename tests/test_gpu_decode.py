@@ -350,3 +350,31 @@ def test_decode_planted_tree_compacts_kv(ref):
             _assert_greedy(lgs[r], int(t), f"post-tree request {r} token {i}")
             lgs[r] = decs[r].run([int(t)])[-1]
     eng.close()
+
+
+def test_engine_option_conflicts(ref):
+    """Unsupported option mixes fail loudly at creation, with the reason."""
+    from paper_2508_21706_b200.engine import VerifyEngine
+    s, _, _ = ref
+    with pytest.raises(ValueError, match="contiguous host K/V"):
+        VerifyEngine(s, max_batch=2, max_verify=4, max_seq=256, attn_cpu=True, kv_pages=-1)
+
+
+def test_paged_graph_decode_matches_paged_eager(ref):
+    """decode_run(graph=True) maps every page the run needs before replaying;
+    on a paged pool it commits what the eager paged loop commits."""
+    import torch
+    from paper_2508_21706_b200.engine import VerifyEngine
+    s, _, _ = ref
+    b, k, steps = len(PROMPTS), 3, 5
+    out = []
+    stream = torch.cuda.Stream()
+    for graph in (False, True):
+        eng = VerifyEngine(s, max_batch=b, max_verify=6, max_seq=256, kv_pages=-1)
+        eng.prefill(_prompts(s), stream=stream.cuda_stream)
+        eng.decode_run(k, steps, graph=graph, stream=stream.cuda_stream)
+        stream.synchronize()
+        out.append(eng.decode_read(b, 64))
+        eng.close()
+    for a, c in zip(out[0], out[1]):
+        assert np.array_equal(a, c)
