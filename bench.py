@@ -57,6 +57,8 @@ def parse():
                     help="LARGE_BATCH (stream whole layers ahead) or BATCH_ONE (stream router-selected experts)")
     ap.add_argument("--no-compress", dest="compress", action="store_false",
                     help="stream raw bf16 experts instead of the lossless code (default: coded, expanded in HBM)")
+    ap.add_argument("--ep-transport", default="nccl", choices=["nccl", "ipc"],
+                    help="N>1 expert-parallel exchange: NCCL send/recv or CUDA-IPC peer mailboxes")
     ap.add_argument("--attn-cpu", action="store_true",
                     help="AttentionPlacement::CPU: target K/V in pinned host DRAM, attention on the host pool")
     return ap.parse_args()
@@ -389,13 +391,28 @@ def run_ours(args):
     if world > 1:
         from paper_2508_21706_b200.engine import EpGroup
         import torch.distributed as dist
+        gloo = dist.new_group(backend="gloo")  # host barriers of the peer-memory transport (collective call)
         try:
             if b % world or shape.n_expert % world:
                 raise ValueError(f"batch {b} / experts {shape.n_expert} not divisible by {world}")
-            uid = [EpGroup.nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(uid, src=0)
-            grp = EpGroup.nccl(uid[0], world, rank)
-            ep_rank, ep_size, mode = rank, world, f"ep{world}"
+            grp = None
+            if args.ep_transport == "nccl":
+                try:
+                    uid = [EpGroup.nccl_unique_id() if rank == 0 else None]
+                    dist.broadcast_object_list(uid, src=0)
+                    grp = EpGroup.nccl(uid[0], world, rank)
+                except Exception as ex:
+                    print(f"[bench] NCCL transport unavailable ({ex}); using the peer-memory transport",
+                          file=sys.stderr)
+            if grp is None:  # CUDA IPC mailboxes over NVLink, no NCCL
+                def all_gather(blob):
+                    out = [None] * world
+                    dist.all_gather_object(out, blob, group=gloo)
+                    return out
+                grp = EpGroup.ipc(world, rank, EpGroup.ipc_slot_bytes(shape, b // world, n), all_gather,
+                                  lambda: dist.barrier(group=gloo))
+                args.ep_transport = "ipc"
+            ep_rank, ep_size, mode = rank, world, f"ep{world} ({args.ep_transport})"
             b = b // world
         except Exception as ex:  # reported in the line; replicas keep the run measurable
             print(f"[bench] expert parallelism unavailable ({ex}); running {world} replicas", file=sys.stderr)

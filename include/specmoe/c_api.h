@@ -311,6 +311,19 @@ smo_status smo_nccl_unique_id(uint8_t* id128);
 smo_status smo_ep_nccl_create(const uint8_t* id128, int32_t nranks, int32_t rank, smo_ep_group** out);
 smo_status smo_ep_loopback_create(int32_t ep_size, smo_ep_group** out);
 smo_status smo_ep_group_destroy(smo_ep_group* g);
+/* Peer-memory transport (CUDA IPC; NVLink between GPUs, or several processes
+ * on one GPU): each rank owns a mailbox [2][nranks][slot_bytes] peers write
+ * into directly, plus interprocess events. create returns this rank's handle
+ * blob (smo_ep_ipc_handle_bytes() bytes); the caller all-gathers the blobs
+ * (rank order) and connects with a host barrier callback over the same ranks
+ * (called once per exchange, from the thread running smo_engine_verify).
+ * slot_bytes >= the largest exchange block: max(T*k*h*2 + 16 + 4*E/P,
+ * T*k*h*4) for the engine's T = max_batch * max_verify.                    */
+typedef void (*smo_barrier_fn)(void* ctx);
+size_t smo_ep_ipc_handle_bytes(void);
+smo_status smo_ep_ipc_create(int32_t nranks, int32_t rank, uint64_t slot_bytes, smo_ep_group** out,
+                             uint8_t* handles);
+smo_status smo_ep_ipc_connect(smo_ep_group* g, const uint8_t* all_handles, smo_barrier_fn barrier, void* ctx);
 
 typedef struct smo_engine smo_engine;
 

@@ -112,6 +112,9 @@ _SIGS = {
     "smo_ep_nccl_create": (C.c_int, [_vp, _i32, _i32, C.POINTER(_vp)]),
     "smo_ep_loopback_create": (C.c_int, [_i32, C.POINTER(_vp)]),
     "smo_ep_group_destroy": (C.c_int, [_vp]),
+    "smo_ep_ipc_handle_bytes": (_sz, []),
+    "smo_ep_ipc_create": (C.c_int, [_i32, _i32, _u64, C.POINTER(_vp), _vp]),
+    "smo_ep_ipc_connect": (C.c_int, [_vp, _vp, _vp, _vp]),
     "smo_engine_create": (C.c_int, [C.POINTER(ModelConfig), C.POINTER(EngineOptions), C.POINTER(_vp)]),
     "smo_engine_destroy": (C.c_int, [_vp]),
     "smo_engine_fill_prefix": (C.c_int, [_vp, _vp, _i32]),

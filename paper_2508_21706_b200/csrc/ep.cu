@@ -305,6 +305,104 @@ struct NcclTransport : EpTransport {
   }
 };
 
+// Peer-memory transport (CUDA IPC): every rank owns a mailbox [2][P][slot]
+// that the other ranks write into directly — over NVLink between GPUs, or
+// within one GPU between processes. Round e uses half e % 2: rank r copies
+// its block for p into p's mailbox slot [e%2][r] (after p has consumed the
+// half it is about to reuse), records its interprocess `sent` event, and
+// after a host barrier (the events' record order is then fixed) waits on
+// every peer's `sent` and copies its own mailbox out. No NCCL, no spin.
+struct IpcTransport : EpTransport {
+  int rank = 0;
+  size_t slot = 0;
+  uint8_t* mailbox = nullptr;
+  cudaEvent_t sent = nullptr, consumed = nullptr;
+  std::vector<uint8_t*> peer_mb;
+  std::vector<cudaEvent_t> peer_sent, peer_consumed;
+  smo_barrier_fn barrier = nullptr;
+  void* barrier_ctx = nullptr;
+  int parity = 0;
+
+  IpcTransport(int nranks, int r, size_t slot_bytes) {
+    P = nranks;
+    rank = r;
+    slot = (slot_bytes + 255) & ~size_t(255);
+    SMO_CUDA_CHECK(cudaMalloc(&mailbox, 2 * size_t(P) * slot));
+    SMO_CUDA_CHECK(cudaEventCreateWithFlags(&sent, cudaEventDisableTiming | cudaEventInterprocess));
+    SMO_CUDA_CHECK(cudaEventCreateWithFlags(&consumed, cudaEventDisableTiming | cudaEventInterprocess));
+  }
+  ~IpcTransport() override {
+    for (int p = 0; p < int(peer_mb.size()); ++p)
+      if (p != rank && peer_mb[size_t(p)]) cudaIpcCloseMemHandle(peer_mb[size_t(p)]);
+    for (int p = 0; p < int(peer_sent.size()); ++p)
+      if (p != rank) {
+        cudaEventDestroy(peer_sent[size_t(p)]);
+        cudaEventDestroy(peer_consumed[size_t(p)]);
+      }
+    if (sent) cudaEventDestroy(sent);
+    if (consumed) cudaEventDestroy(consumed);
+    if (mailbox) cudaFree(mailbox);
+  }
+  // handle blob: mailbox memory handle, sent event, consumed event
+  static constexpr size_t kBlob = sizeof(cudaIpcMemHandle_t) + 2 * sizeof(cudaIpcEventHandle_t);
+  void export_handles(uint8_t* out) const {
+    cudaIpcMemHandle_t mh;
+    cudaIpcEventHandle_t eh;
+    SMO_CUDA_CHECK(cudaIpcGetMemHandle(&mh, mailbox));
+    std::memcpy(out, &mh, sizeof(mh));
+    SMO_CUDA_CHECK(cudaIpcGetEventHandle(&eh, sent));
+    std::memcpy(out + sizeof(mh), &eh, sizeof(eh));
+    SMO_CUDA_CHECK(cudaIpcGetEventHandle(&eh, consumed));
+    std::memcpy(out + sizeof(mh) + sizeof(eh), &eh, sizeof(eh));
+  }
+  void connect(const uint8_t* all, smo_barrier_fn fn, void* ctx) {
+    barrier = fn;
+    barrier_ctx = ctx;
+    peer_mb.assign(size_t(P), nullptr);
+    peer_sent.assign(size_t(P), nullptr);
+    peer_consumed.assign(size_t(P), nullptr);
+    for (int p = 0; p < P; ++p) {
+      if (p == rank) {
+        peer_mb[size_t(p)] = mailbox;
+        peer_sent[size_t(p)] = sent;
+        peer_consumed[size_t(p)] = consumed;
+        continue;
+      }
+      const uint8_t* b = all + size_t(p) * kBlob;
+      cudaIpcMemHandle_t mh;
+      cudaIpcEventHandle_t eh;
+      std::memcpy(&mh, b, sizeof(mh));
+      void* ptr = nullptr;
+      SMO_CUDA_CHECK(cudaIpcOpenMemHandle(&ptr, mh, cudaIpcMemLazyEnablePeerAccess));
+      peer_mb[size_t(p)] = reinterpret_cast<uint8_t*>(ptr);
+      std::memcpy(&eh, b + sizeof(mh), sizeof(eh));
+      SMO_CUDA_CHECK(cudaIpcOpenEventHandle(&peer_sent[size_t(p)], eh));
+      std::memcpy(&eh, b + sizeof(mh) + sizeof(eh), sizeof(eh));
+      SMO_CUDA_CHECK(cudaIpcOpenEventHandle(&peer_consumed[size_t(p)], eh));
+    }
+  }
+  void alltoall(int r, const void* send, void* recv, size_t bytes, cudaStream_t st) override {
+    SMO_REQUIRE(r == rank && bytes <= slot, "ep ipc: block larger than the mailbox slot");
+    SMO_REQUIRE(barrier && !peer_mb.empty(), "ep ipc: transport not connected");
+    const int half = parity;
+    parity ^= 1;
+    for (int p = 0; p < P; ++p) {  // p has finished reading the half we are about to overwrite
+      if (p != rank) SMO_CUDA_CHECK(cudaStreamWaitEvent(st, peer_consumed[size_t(p)], 0));
+      SMO_CUDA_CHECK(cudaMemcpyAsync(peer_mb[size_t(p)] + (size_t(half) * P + rank) * slot,
+                                     reinterpret_cast<const uint8_t*>(send) + size_t(p) * bytes, bytes,
+                                     cudaMemcpyDeviceToDevice, st));
+    }
+    SMO_CUDA_CHECK(cudaEventRecord(sent, st));
+    barrier(barrier_ctx);  // every rank has recorded this round's `sent`
+    for (int p = 0; p < P; ++p)
+      if (p != rank) SMO_CUDA_CHECK(cudaStreamWaitEvent(st, peer_sent[size_t(p)], 0));
+    for (int p = 0; p < P; ++p)
+      SMO_CUDA_CHECK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(recv) + size_t(p) * bytes,
+                                     mailbox + (size_t(half) * P + p) * slot, bytes, cudaMemcpyDeviceToDevice, st));
+    SMO_CUDA_CHECK(cudaEventRecord(consumed, st));
+  }
+};
+
 }  // namespace smo
 
 struct smo_ep_group {
@@ -346,6 +444,33 @@ smo_status smo_ep_nccl_create(const uint8_t* id128, int32_t nranks, int32_t rank
       throw;
     }
     *out = g;
+  });
+}
+
+size_t smo_ep_ipc_handle_bytes(void) { return smo::IpcTransport::kBlob; }
+
+smo_status smo_ep_ipc_create(int32_t nranks, int32_t rank, uint64_t slot_bytes, smo_ep_group** out, uint8_t* handles) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(out && handles && nranks >= 1 && rank >= 0 && rank < nranks && slot_bytes > 0, "ep: bad arguments");
+    auto* g = new smo_ep_group();
+    try {
+      auto* t = new smo::IpcTransport(nranks, rank, size_t(slot_bytes));
+      g->t = t;
+      t->export_handles(handles);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+smo_status smo_ep_ipc_connect(smo_ep_group* g, const uint8_t* all_handles, smo_barrier_fn barrier, void* ctx) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(g && all_handles && barrier, "ep: bad arguments");
+    auto* t = dynamic_cast<smo::IpcTransport*>(g->t);
+    SMO_REQUIRE(t, "ep: not an IPC group");
+    t->connect(all_handles, barrier, ctx);
   });
 }
 

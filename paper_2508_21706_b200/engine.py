@@ -93,6 +93,31 @@ class EpGroup:
         L.check(L.load().smo_ep_nccl_create(buf, nranks, rank, C.byref(h)))
         return EpGroup(h)
 
+    BARRIER_FN = C.CFUNCTYPE(None, C.c_void_p)
+
+    @staticmethod
+    def ipc(nranks: int, rank: int, slot_bytes: int, all_gather, barrier) -> "EpGroup":
+        """Peer-memory transport over CUDA IPC (no NCCL): `all_gather(bytes)`
+        returns every rank's bytes in rank order and `barrier()` synchronises
+        the ranks (e.g. torch.distributed over gloo)."""
+        lib = L.load()
+        blob = (C.c_uint8 * int(lib.smo_ep_ipc_handle_bytes()))()
+        h = C.c_void_p()
+        L.check(lib.smo_ep_ipc_create(nranks, rank, slot_bytes, C.byref(h), blob))
+        allb = b"".join(all_gather(bytes(blob)))
+        buf = (C.c_uint8 * len(allb)).from_buffer_copy(allb)
+        cb = EpGroup.BARRIER_FN(lambda _ctx: barrier())
+        L.check(lib.smo_ep_ipc_connect(h, buf, C.cast(cb, C.c_void_p), None))
+        g = EpGroup(h)
+        g._keep = cb  # the callback must outlive the group
+        return g
+
+    @staticmethod
+    def ipc_slot_bytes(shape: "ModelShape", max_batch: int, max_verify: int) -> int:
+        """Mailbox slot that fits the engine's dispatch and combine blocks."""
+        rows = max_batch * max_verify * shape.top_k
+        return max(rows * shape.hidden * 2 + 16 + 4 * shape.n_expert, rows * shape.hidden * 4) + 256
+
     def close(self):
         if getattr(self, "handle", None):
             L.load().smo_ep_group_destroy(self.handle)

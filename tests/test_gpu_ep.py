@@ -100,3 +100,74 @@ def test_ep_single_rank_transport_path(cuda, kind):
     assert np.array_equal(outs[0][0].target, outs[1][0].target)
     assert np.array_equal(outs[0][1].view(np.uint32), outs[1][1].view(np.uint32))
     grp.close()
+
+
+def _ipc_rank(rank, world, port, out_q):
+    """One process of the IPC expert-parallel test (both on cuda:0)."""
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    try:
+        import torch
+        import torch.distributed as dist
+        from paper_2508_21706_b200.engine import TINY, EpGroup, VerifyEngine
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        shape = dataclasses.replace(TINY, seed=0x5EED + 3, lm_scale=8.0, router_scale=4.0)
+        s_max = PREFIX + N + 64
+        rng = np.random.default_rng(11)
+        tokens = rng.integers(0, shape.vocab, size=(B, N)).astype(np.int32)
+        prefix = np.array([PREFIX, PREFIX - 3, 200, 1], np.int32)
+        bl = B // world
+
+        def all_gather(blob):
+            out = [None] * world
+            dist.all_gather_object(out, blob)
+            return out
+
+        grp = EpGroup.ipc(world, rank, EpGroup.ipc_slot_bytes(shape, bl, N), all_gather, dist.barrier)
+        eng = VerifyEngine(shape, max_batch=bl, max_verify=N, max_seq=s_max, ep_rank=rank, ep_size=world,
+                           ep_group=grp, compress_experts=True)
+        mine = slice(rank * bl, (rank + 1) * bl)
+        eng.fill_prefix(prefix[mine])
+        stream = torch.cuda.Stream()
+        got = [eng.verify(tokens[mine], prefix[mine], stream=stream.cuda_stream) for _ in range(2)]
+        stream.synchronize()
+        eng.close()
+        dist.barrier()
+        ref = VerifyEngine(shape, max_batch=bl, max_verify=N, max_seq=s_max, compress_experts=True)
+        ref.fill_prefix(prefix[mine])
+        want = ref.verify(tokens[mine], prefix[mine])
+        ok = all(np.array_equal(g.target, want.target) and np.array_equal(g.acc_len, want.acc_len)
+                 and np.array_equal(g.bonus, want.bonus) for g in got)
+        ref.close()
+        grp.close()
+        dist.destroy_process_group()
+        out_q.put((rank, ok, ""))
+    except Exception as ex:  # reported to the parent
+        import traceback
+        out_q.put((rank, False, traceback.format_exc()))
+
+
+def test_ep_ipc_two_processes_bit_identical(cuda):
+    """Expert parallelism across two PROCESSES over the peer-memory (CUDA IPC)
+    transport — the multi-process path with no NCCL, run here with both ranks
+    on one B200: each rank's verify results equal a single-GPU engine's on its
+    requests, bit for bit."""
+    import socket
+
+    import torch.multiprocessing as mp
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+    for rank, ok, err in sorted(res):
+        assert ok, f"rank {rank}: {err}"
