@@ -54,6 +54,19 @@ struct EpTransport {
   int P = 1;
   virtual ~EpTransport() {}
   virtual void alltoall(int rank, const void* send, void* recv, size_t bytes, cudaStream_t st) = 0;
+  // Direct exchange (peer stores): the producing kernel writes rank p's block
+  // straight into p's receive buffer through dests[p]; this rank's receive
+  // buffer holds P blocks `direct_slot()` bytes apart. Sequence per round:
+  // dests = direct_begin(&recv); producer kernel; direct_exchange(); consumer
+  // kernel reading recv; direct_done(). direct_slot() == 0: staged only.
+  virtual size_t direct_slot() const { return 0; }
+  virtual uint8_t* const* direct_begin(cudaStream_t st, const uint8_t** recv) {
+    (void)st;
+    *recv = nullptr;
+    return nullptr;
+  }
+  virtual void direct_exchange(cudaStream_t st) { (void)st; }
+  virtual void direct_done(cudaStream_t st) { (void)st; }
 };
 
 // ---------------------------------------------------------------------------

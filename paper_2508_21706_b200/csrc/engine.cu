@@ -322,12 +322,20 @@ void Engine::create() {
     pos_ep = dalloc<int32_t>(P);
     offsets_l = dalloc<int32_t>(E_loc + 1);
     back = dalloc<int32_t>(size_t(PR) * C);
-    ep_send = dalloc<uint8_t>(size_t(PR) * blk_d);
-    ep_recv = dalloc<uint8_t>(size_t(PR) * blk_d);
+    {
+      const size_t ds = ept->direct_slot();
+      const char* f = std::getenv("SMO_EP_STAGED");
+      ep_direct = !(f && f[0] == '1') && ds >= std::max(blk_d, size_t(C) * h * 4) && ds % (size_t(h) * 4) == 0;
+      ep_rows = ep_direct ? int(ds / (size_t(h) * 4)) : C;
+    }
+    if (!ep_direct) {
+      ep_send = dalloc<uint8_t>(size_t(PR) * blk_d);
+      ep_recv = dalloc<uint8_t>(size_t(PR) * blk_d);
+      ep_sendback = dalloc<float>(size_t(PR) * C * h);
+      ep_recvback = dalloc<float>(size_t(PR) * C * h);
+    }
     xl = dalloc<uint16_t>(size_t(PR) * C * h);
     yl = dalloc<float>(size_t(4) * PR * C * h);  // room for the fused kernel's down slices
-    ep_sendback = dalloc<float>(size_t(PR) * C * h);
-    ep_recvback = dalloc<float>(size_t(PR) * C * h);
     hbuf = dalloc<uint16_t>(size_t(PR) * C * hi);
   } else {
     hbuf = dalloc<uint16_t>(size_t(P) * hi);
@@ -530,60 +538,76 @@ void Engine::snap(const char* name, int layer, const void* src, size_t bytes, cu
 void Engine::moe_ep(int l, int T, cudaStream_t st) {
   const int PT = T * K;
   const int rank = opt.ep_rank;
-  ep_pack(xp, offsets, P, E_loc, C, h, blk_d, ep_send, st);
-  ep_pos(oid, pos, offsets, PT, E_loc, C, pos_ep, st);
-  ept->alltoall(rank, ep_send, ep_recv, blk_d, st);
-  ep_unpack(ep_recv, P, E_loc, C, h, blk_d, xl, offsets_l, back, st);
+  ep_pos(oid, pos, offsets, PT, E_loc, ep_rows, pos_ep, st);
+  if (ep_direct) {  // dispatch kernel stores each block into its owner's mailbox
+    const uint8_t* recv = nullptr;
+    uint8_t* const* dests = ept->direct_begin(st, &recv);
+    ep_pack(xp, offsets, P, E_loc, C, h, blk_d, nullptr, st, dests);
+    ept->direct_exchange(st);
+    ep_unpack(recv, P, E_loc, C, h, ept->direct_slot(), xl, offsets_l, back, st);
+    ept->direct_done(st);
+  } else {
+    ep_pack(xp, offsets, P, E_loc, C, h, blk_d, ep_send, st);
+    ept->alltoall(rank, ep_send, ep_recv, blk_d, st);
+    ep_unpack(ep_recv, P, E_loc, C, h, blk_d, xl, offsets_l, back, st);
+  }
   SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 7), st));
   SMO_CUDA_CHECK(cudaStreamWaitEvent(st, slot_ready[l % slots], 0));
   decode_slot(l, st);
   SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 4), st));
+  int splits = 1;
   if (moe_fused) {
     moe_launch(xl, P * C, h, hi, E_loc, offsets_l, pool, blk_bytes, pool_blocks, d_w_index_loc + size_t(l) * E_loc,
                hbuf, yl, moe_splits, 4, d_done, st);
-    SMO_CUDA_CHECK(cudaEventRecord(slot_free[l % slots], st));
-    ep_pack_back(yl, back, offsets_l, E_loc, h, ep_sendback, st, moe_splits, size_t(P) * C * h);
+    splits = moe_splits;
+  } else {
+    smo_gemm_args g{};
+    g.x = xl;
+    g.rows = P * C;
+    g.K = h;
+    g.N = hi;
+    g.groups = E_loc;
+    g.row_offsets = offsets_l;
+    g.max_rows_per_group = P * maxT;
+    g.w = pool;
+    g.w_up = pool + size_t(hi) * h;
+    g.w_block_stride = blk_bytes;
+    g.w_pool_blocks = pool_blocks;
+    g.w_index = d_w_index_loc + size_t(l) * E_loc;
+    g.epilogue = SMO_EPI_SWIGLU;
+    g.out = hbuf;
+    g.ldo = hi;
+    gemm_launch(g, st);
+    g = smo_gemm_args{};
+    g.x = hbuf;
+    g.rows = P * C;
+    g.K = hi;
+    g.N = h;
+    g.groups = E_loc;
+    g.row_offsets = offsets_l;
+    g.max_rows_per_group = P * maxT;
+    g.w = pool + 2 * size_t(hi) * h;
+    g.w_block_stride = blk_bytes;
+    g.w_pool_blocks = pool_blocks;
+    g.w_index = d_w_index_loc + size_t(l) * E_loc;
+    g.epilogue = SMO_EPI_F32;
+    g.out = yl;
+    g.ldo = h;
+    gemm_launch(g, st);
+  }
+  SMO_CUDA_CHECK(cudaEventRecord(slot_free[l % slots], st));
+  if (ep_direct) {  // combine rows stored straight into the source ranks' mailboxes
+    const uint8_t* recv = nullptr;
+    uint8_t* const* dests = ept->direct_begin(st, &recv);
+    ep_pack_back(yl, back, offsets_l, E_loc, h, nullptr, st, splits, size_t(P) * C * h, dests, C);
+    ept->direct_exchange(st);
+    unpermute_combine(reinterpret_cast<const float*>(recv), pos_ep, rw, T, K, h, x, st);
+    ept->direct_done(st);
+  } else {
+    ep_pack_back(yl, back, offsets_l, E_loc, h, ep_sendback, st, splits, size_t(P) * C * h);
     ept->alltoall(rank, ep_sendback, ep_recvback, size_t(C) * h * sizeof(float), st);
     unpermute_combine(ep_recvback, pos_ep, rw, T, K, h, x, st);
-    return;
   }
-  smo_gemm_args g{};
-  g.x = xl;
-  g.rows = P * C;
-  g.K = h;
-  g.N = hi;
-  g.groups = E_loc;
-  g.row_offsets = offsets_l;
-  g.max_rows_per_group = P * maxT;
-  g.w = pool;
-  g.w_up = pool + size_t(hi) * h;
-  g.w_block_stride = blk_bytes;
-  g.w_pool_blocks = pool_blocks;
-  g.w_index = d_w_index_loc + size_t(l) * E_loc;
-  g.epilogue = SMO_EPI_SWIGLU;
-  g.out = hbuf;
-  g.ldo = hi;
-  gemm_launch(g, st);
-  g = smo_gemm_args{};
-  g.x = hbuf;
-  g.rows = P * C;
-  g.K = hi;
-  g.N = h;
-  g.groups = E_loc;
-  g.row_offsets = offsets_l;
-  g.max_rows_per_group = P * maxT;
-  g.w = pool + 2 * size_t(hi) * h;
-  g.w_block_stride = blk_bytes;
-  g.w_pool_blocks = pool_blocks;
-  g.w_index = d_w_index_loc + size_t(l) * E_loc;
-  g.epilogue = SMO_EPI_F32;
-  g.out = yl;
-  g.ldo = h;
-  gemm_launch(g, st);
-  SMO_CUDA_CHECK(cudaEventRecord(slot_free[l % slots], st));
-  ep_pack_back(yl, back, offsets_l, E_loc, h, ep_sendback, st);
-  ept->alltoall(rank, ep_sendback, ep_recvback, size_t(C) * h * sizeof(float), st);
-  unpermute_combine(ep_recvback, pos_ep, rw, T, K, h, x, st);
 }
 
 void Engine::verify(const smo_verify_batch& in, smo_verify_output& out, cudaStream_t st) {

@@ -58,13 +58,14 @@ void prefill_last(const float* x, const int32_t* len, int b, int C, int h, float
 EpTransport* ep_transport(void* group);
 void ep_remap(const int32_t* ids, int n, int P, int E_loc, int32_t* oid, cudaStream_t st);
 void ep_pack(const void* xp, const int32_t* offsets, int P, int E_loc, int C, int h, size_t block_bytes, void* send,
-             cudaStream_t st);
+             cudaStream_t st, uint8_t* const* dests = nullptr);
 void ep_pos(const int32_t* oid, const int32_t* pos, const int32_t* offsets, int n, int E_loc, int C, int32_t* pos_ep,
             cudaStream_t st);
 void ep_unpack(const void* recv, int P, int E_loc, int C, int h, size_t block_bytes, void* xl, int32_t* offsets_l,
                int32_t* back, cudaStream_t st);
 void ep_pack_back(const float* yl, const int32_t* back, const int32_t* offsets_l, int E_loc, int h, float* sendback,
-                  cudaStream_t st, int splits = 1, size_t split_stride = 0);
+                  cudaStream_t st, int splits = 1, size_t split_stride = 0, uint8_t* const* dests = nullptr,
+                  int C = 1);
 int moe_launch(const void* x_perm, int rows, int h, int hi, int E, const int32_t* offsets, const void* pool,
                uint64_t w_block_stride, int pool_blocks, const int32_t* w_index, void* hbuf, float* y, int splits,
                int max_splits, int* done, cudaStream_t st);
@@ -174,6 +175,8 @@ struct Engine {
   // expert parallelism: transport, geometry and exchange buffers
   EpTransport* ept = nullptr;
   bool ep_on = false;
+  bool ep_direct = false;  // dispatch/combine kernels store into the peers' mailboxes
+  int ep_rows = 0;         // rows per returned block in the combine input (C, or the mailbox stride)
   int P = 1, E_loc = 0, C = 0;
   size_t blk_d = 0;  // dispatch block bytes (C bf16 rows + E_loc counts)
   int32_t *oid = nullptr, *pos_ep = nullptr, *offsets_l = nullptr, *back = nullptr, *d_w_index_loc = nullptr;

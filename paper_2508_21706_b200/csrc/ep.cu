@@ -42,12 +42,14 @@ __global__ void ep_remap_kernel(const int32_t* ids, int n, int P, int E_loc, int
   }
 }
 
-// send block d: rows [0, C) bf16 x h, then E_loc int32 counts.
+// send block d: rows [0, C) bf16 x h, then E_loc int32 counts. With `dests`
+// (direct exchange) block d is stored straight into rank d's receive buffer.
 __global__ void ep_pack_kernel(const uint16_t* __restrict__ xp, const int32_t* __restrict__ offsets, int P,
-                               int E_loc, int C, int h, size_t block_bytes, uint8_t* __restrict__ send) {
+                               int E_loc, int C, int h, size_t block_bytes, uint8_t* __restrict__ send,
+                               uint8_t* const* __restrict__ dests) {
   const int d = blockIdx.y;
   const int seg0 = offsets[d * E_loc], seg1 = offsets[(d + 1) * E_loc];
-  uint8_t* blk = send + size_t(d) * block_bytes;
+  uint8_t* blk = dests ? dests[d] : send + size_t(d) * block_bytes;
   if (blockIdx.x == 0 && threadIdx.x < E_loc) {
     int32_t* cnt = reinterpret_cast<int32_t*>(blk + size_t(C) * h * 2);
     cnt[threadIdx.x] = offsets[d * E_loc + threadIdx.x + 1] - offsets[d * E_loc + threadIdx.x];
@@ -60,7 +62,8 @@ __global__ void ep_pack_kernel(const uint16_t* __restrict__ xp, const int32_t* _
   }
 }
 
-// position of each local (token, slot) pair's returned row: d*C + rank in d.
+// position of each local (token, slot) pair's returned row: d*C + rank in d
+// (C = rows per returned block: the capacity, or the direct receive stride).
 __global__ void ep_pos_kernel(const int32_t* __restrict__ oid, const int32_t* __restrict__ pos,
                               const int32_t* __restrict__ offsets, int n, int E_loc, int C, int32_t* pos_ep) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -120,11 +123,14 @@ __global__ void ep_unpack_kernel(const uint8_t* __restrict__ recv, int P, int E_
 // in slice order — the same fixed order as the single-GPU combine
 __global__ void ep_pack_back_kernel(const float* __restrict__ yl, const int32_t* __restrict__ back,
                                     const int32_t* __restrict__ offsets_l, int E_loc, int h,
-                                    float* __restrict__ sendback, int splits, size_t split_stride) {
+                                    float* __restrict__ sendback, int splits, size_t split_stride,
+                                    uint8_t* const* __restrict__ dests, int C) {
   const int rows = offsets_l[E_loc];
   for (int q = blockIdx.x; q < rows; q += gridDim.x) {
     const float4* src = reinterpret_cast<const float4*>(yl + size_t(q) * h);
-    float4* dst = reinterpret_cast<float4*>(sendback + size_t(back[q]) * h);
+    const int bq = back[q];
+    float4* dst = dests ? reinterpret_cast<float4*>(dests[bq / C]) + size_t(bq % C) * (h / 4)
+                        : reinterpret_cast<float4*>(sendback + size_t(bq) * h);
     for (int c = threadIdx.x; c < h / 4; c += blockDim.x) {
       float4 v = src[c];
       for (int s = 1; s < splits; ++s) {
@@ -147,10 +153,10 @@ void ep_remap(const int32_t* ids, int n, int P, int E_loc, int32_t* oid, cudaStr
   SMO_CUDA_CHECK(cudaGetLastError());
 }
 void ep_pack(const void* xp, const int32_t* offsets, int P, int E_loc, int C, int h, size_t block_bytes, void* send,
-             cudaStream_t st) {
+             cudaStream_t st, uint8_t* const* dests) {
   dim3 grid(64, P);
   ep_pack_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const uint16_t*>(xp), offsets, P, E_loc, C, h, block_bytes,
-                                       reinterpret_cast<uint8_t*>(send));
+                                       reinterpret_cast<uint8_t*>(send), dests);
   count_launch();
   SMO_CUDA_CHECK(cudaGetLastError());
 }
@@ -169,9 +175,9 @@ void ep_unpack(const void* recv, int P, int E_loc, int C, int h, size_t block_by
   SMO_CUDA_CHECK(cudaGetLastError());
 }
 void ep_pack_back(const float* yl, const int32_t* back, const int32_t* offsets_l, int E_loc, int h, float* sendback,
-                  cudaStream_t st, int splits, size_t split_stride) {
+                  cudaStream_t st, int splits, size_t split_stride, uint8_t* const* dests, int C) {
   ep_pack_back_kernel<<<256, 256, 0, st>>>(yl, back, offsets_l, E_loc, h, sendback, std::max(1, splits),
-                                           split_stride);
+                                           split_stride, dests, std::max(1, C));
   count_launch();
   SMO_CUDA_CHECK(cudaGetLastError());
 }
@@ -307,15 +313,19 @@ struct NcclTransport : EpTransport {
 
 // Peer-memory transport (CUDA IPC): every rank owns a mailbox [2][P][slot]
 // that the other ranks write into directly — over NVLink between GPUs, or
-// within one GPU between processes. Round e uses half e % 2: rank r copies
+// within one GPU between processes. Round e uses half e % 2: rank r stores
 // its block for p into p's mailbox slot [e%2][r] (after p has consumed the
-// half it is about to reuse), records its interprocess `sent` event, and
+// round that last used that half), records its interprocess `sent` event, and
 // after a host barrier (the events' record order is then fixed) waits on
-// every peer's `sent` and copies its own mailbox out. No NCCL, no spin.
+// every peer's `sent` and reads its own mailbox. No NCCL, no spin.
+// Direct mode: the dispatch / combine kernels store into the peers'
+// mailboxes themselves (dests[half][p] = p's slot [half][r]); the staged
+// alltoall is the same protocol with copies on both sides.
 struct IpcTransport : EpTransport {
   int rank = 0;
   size_t slot = 0;
   uint8_t* mailbox = nullptr;
+  uint8_t** d_dests = nullptr;  // device [2][P]
   cudaEvent_t sent = nullptr, consumed = nullptr;
   std::vector<uint8_t*> peer_mb;
   std::vector<cudaEvent_t> peer_sent, peer_consumed;
@@ -328,6 +338,7 @@ struct IpcTransport : EpTransport {
     rank = r;
     slot = (slot_bytes + 255) & ~size_t(255);
     SMO_CUDA_CHECK(cudaMalloc(&mailbox, 2 * size_t(P) * slot));
+    SMO_CUDA_CHECK(cudaMalloc(&d_dests, 2 * size_t(P) * sizeof(uint8_t*)));
     SMO_CUDA_CHECK(cudaEventCreateWithFlags(&sent, cudaEventDisableTiming | cudaEventInterprocess));
     SMO_CUDA_CHECK(cudaEventCreateWithFlags(&consumed, cudaEventDisableTiming | cudaEventInterprocess));
   }
@@ -341,6 +352,7 @@ struct IpcTransport : EpTransport {
       }
     if (sent) cudaEventDestroy(sent);
     if (consumed) cudaEventDestroy(consumed);
+    if (d_dests) cudaFree(d_dests);
     if (mailbox) cudaFree(mailbox);
   }
   // handle blob: mailbox memory handle, sent event, consumed event
@@ -380,26 +392,46 @@ struct IpcTransport : EpTransport {
       std::memcpy(&eh, b + sizeof(mh) + sizeof(eh), sizeof(eh));
       SMO_CUDA_CHECK(cudaIpcOpenEventHandle(&peer_consumed[size_t(p)], eh));
     }
+    std::vector<uint8_t*> dests(2 * size_t(P));
+    for (int half = 0; half < 2; ++half)
+      for (int p = 0; p < P; ++p)
+        dests[size_t(half) * P + p] = peer_mb[size_t(p)] + (size_t(half) * P + rank) * slot;
+    SMO_CUDA_CHECK(cudaMemcpy(d_dests, dests.data(), dests.size() * sizeof(uint8_t*), cudaMemcpyHostToDevice));
   }
-  void alltoall(int r, const void* send, void* recv, size_t bytes, cudaStream_t st) override {
-    SMO_REQUIRE(r == rank && bytes <= slot, "ep ipc: block larger than the mailbox slot");
+  size_t direct_slot() const override { return slot; }
+  // Waiting on a peer's latest `consumed` record is enough: the barrier of the
+  // previous round orders it after the peer's read of the half reused now
+  // (a later record only makes the wait conservative).
+  uint8_t* const* direct_begin(cudaStream_t st, const uint8_t** recv) override {
     SMO_REQUIRE(barrier && !peer_mb.empty(), "ep ipc: transport not connected");
     const int half = parity;
     parity ^= 1;
-    for (int p = 0; p < P; ++p) {  // p has finished reading the half we are about to overwrite
+    for (int p = 0; p < P; ++p)
       if (p != rank) SMO_CUDA_CHECK(cudaStreamWaitEvent(st, peer_consumed[size_t(p)], 0));
-      SMO_CUDA_CHECK(cudaMemcpyAsync(peer_mb[size_t(p)] + (size_t(half) * P + rank) * slot,
-                                     reinterpret_cast<const uint8_t*>(send) + size_t(p) * bytes, bytes,
-                                     cudaMemcpyDeviceToDevice, st));
-    }
+    *recv = mailbox + size_t(half) * P * slot;
+    return d_dests + size_t(half) * P;
+  }
+  void direct_exchange(cudaStream_t st) override {
     SMO_CUDA_CHECK(cudaEventRecord(sent, st));
     barrier(barrier_ctx);  // every rank has recorded this round's `sent`
     for (int p = 0; p < P; ++p)
       if (p != rank) SMO_CUDA_CHECK(cudaStreamWaitEvent(st, peer_sent[size_t(p)], 0));
+  }
+  void direct_done(cudaStream_t st) override { SMO_CUDA_CHECK(cudaEventRecord(consumed, st)); }
+  void alltoall(int r, const void* send, void* recv, size_t bytes, cudaStream_t st) override {
+    SMO_REQUIRE(r == rank && bytes <= slot, "ep ipc: block larger than the mailbox slot");
+    const int half = parity;
+    const uint8_t* mine = nullptr;
+    direct_begin(st, &mine);
     for (int p = 0; p < P; ++p)
-      SMO_CUDA_CHECK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(recv) + size_t(p) * bytes,
-                                     mailbox + (size_t(half) * P + p) * slot, bytes, cudaMemcpyDeviceToDevice, st));
-    SMO_CUDA_CHECK(cudaEventRecord(consumed, st));
+      SMO_CUDA_CHECK(cudaMemcpyAsync(peer_mb[size_t(p)] + (size_t(half) * P + rank) * slot,
+                                     reinterpret_cast<const uint8_t*>(send) + size_t(p) * bytes, bytes,
+                                     cudaMemcpyDeviceToDevice, st));
+    direct_exchange(st);
+    for (int p = 0; p < P; ++p)
+      SMO_CUDA_CHECK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(recv) + size_t(p) * bytes, mine + size_t(p) * slot,
+                                     bytes, cudaMemcpyDeviceToDevice, st));
+    direct_done(st);
   }
 };
 

@@ -114,9 +114,13 @@ class EpGroup:
 
     @staticmethod
     def ipc_slot_bytes(shape: "ModelShape", max_batch: int, max_verify: int) -> int:
-        """Mailbox slot that fits the engine's dispatch and combine blocks."""
+        """Mailbox slot that fits the engine's dispatch and combine blocks, a
+        whole number of fp32 rows so the engine can use direct (peer-store)
+        dispatch / combine into it."""
         rows = max_batch * max_verify * shape.top_k
-        return max(rows * shape.hidden * 2 + 16 + 4 * shape.n_expert, rows * shape.hidden * 4) + 256
+        row = shape.hidden * 4
+        dispatch = rows * shape.hidden * 2 + 16 + 4 * shape.n_expert
+        return max(rows, -(-dispatch // row)) * row
 
     def close(self):
         if getattr(self, "handle", None):

@@ -102,10 +102,11 @@ def test_ep_single_rank_transport_path(cuda, kind):
     grp.close()
 
 
-def _ipc_rank(rank, world, port, out_q):
+def _ipc_rank(rank, world, port, out_q, staged=False):
     """One process of the IPC expert-parallel test (both on cuda:0)."""
     import os
     import sys
+    os.environ["SMO_EP_STAGED"] = "1" if staged else "0"
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
     try:
@@ -126,7 +127,9 @@ def _ipc_rank(rank, world, port, out_q):
             dist.all_gather_object(out, blob)
             return out
 
-        grp = EpGroup.ipc(world, rank, EpGroup.ipc_slot_bytes(shape, bl, N), all_gather, dist.barrier)
+        slot = EpGroup.ipc_slot_bytes(shape, bl, N)
+        assert slot % (4 * shape.hidden) == 0  # whole fp32 rows: the engine takes the direct path
+        grp = EpGroup.ipc(world, rank, slot, all_gather, dist.barrier)
         eng = VerifyEngine(shape, max_batch=bl, max_verify=N, max_seq=s_max, ep_rank=rank, ep_size=world,
                            ep_group=grp, compress_experts=True)
         mine = slice(rank * bl, (rank + 1) * bl)
@@ -150,11 +153,13 @@ def _ipc_rank(rank, world, port, out_q):
         out_q.put((rank, False, traceback.format_exc()))
 
 
-def test_ep_ipc_two_processes_bit_identical(cuda):
+@pytest.mark.parametrize("staged", [False, True], ids=["direct", "staged"])
+def test_ep_ipc_two_processes_bit_identical(cuda, staged):
     """Expert parallelism across two PROCESSES over the peer-memory (CUDA IPC)
     transport — the multi-process path with no NCCL, run here with both ranks
     on one B200: each rank's verify results equal a single-GPU engine's on its
-    requests, bit for bit."""
+    requests, bit for bit. `direct`: the dispatch / combine kernels store into
+    the peer's mailbox themselves; `staged`: pack buffer + copies."""
     import socket
 
     import torch.multiprocessing as mp
@@ -163,7 +168,7 @@ def test_ep_ipc_two_processes_bit_identical(cuda):
         port = sk.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_ipc_rank, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_ipc_rank, args=(r, 2, port, q, staged)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=600) for _ in procs]
