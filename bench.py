@@ -302,14 +302,17 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def codec_traffic_per_block():
+def codec_traffic_per_block(kernel="K5_expert_decode_unary"):
     """dram__bytes_read+write of one expert_decode launch (one Mixtral expert
-    block) from the committed ncu capture (profiles/r01f_traffic.json)."""
-    try:
-        k = json.load(open(os.path.join(ROOT, "profiles", "r01f_traffic.json")))["kernels"]["K5_expert_decode"]
-        return k["dram_read_bytes"] + k["dram_write_bytes"]
-    except Exception:
-        return None
+    block) from the committed ncu capture (profiles/r01h_traffic.json: the
+    unary decoder the engine uses; r01f_traffic.json: the 3-bit one)."""
+    for f in ("r01h_traffic.json", "r01f_traffic.json"):
+        try:
+            k = json.load(open(os.path.join(ROOT, "profiles", f)))["kernels"][kernel]
+            return k["dram_read_bytes"] + k["dram_write_bytes"]
+        except Exception:
+            continue
+    return None
 
 
 def moe_traffic_per_layer():
@@ -556,7 +559,8 @@ def run_ours(args):
                    "attention_placement": "CPU (host K/V, host thread pool)" if args.attn_cpu else "GPU_RESIDENT (K1)",
                    "moe_batching": "BATCH_ONE (router-selected experts)" if args.moe_batching == "one"
                    else "LARGE_BATCH (whole layers)",
-                   "expert_transfer": "lossless exponent-coded blocks (xfer.cu, 11.4 bits/weight), expanded in HBM "
+                   "expert_transfer": f"lossless exponent-coded blocks (xfer.cu, "
+                   f"{16.0 * stages['h2d_bytes'] / max(1.0, stages['h2d_raw_bytes']):.2f} bits/weight), expanded in HBM "
                    "before the expert kernel" if args.compress else "raw bf16",
                    "l2": "inputs larger than L2 (90.2 GB of experts + 4.6 GB KV streamed per step)",
                    "parallelism": mode},

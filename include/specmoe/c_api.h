@@ -187,8 +187,15 @@ smo_status smo_moe_experts(const void* x_perm, int32_t rows, int32_t h, int32_t 
  * 1584 (4 bits: 12.4 bits/value) bytes per 1024 values. count % 1024 == 0.
  * encode sets *overflow (device int) to 1 when a segment needs more than 32
  * escapes (retry with 4 bits or keep the block raw). Decode is the exact
- * inverse (bit-identical bf16).                                             */
+ * inverse (bit-identical bf16).
+ * bits = 1: the variable-length UNARY exponent code (xfer.cu header: j = E - e
+ * ones then a zero, per-segment table; ~10.2 bits/value on uniform-init
+ * weights). smo_expert_code_bytes(count, 1) is its capacity (worst case);
+ * encode is synchronous on `stream` for bits = 1 and never overflows;
+ * smo_expert_coded_size gives the bytes actually used (reads the device
+ * code's table; 3 / 4 bits: the fixed size).                               */
 size_t smo_expert_code_bytes(uint64_t count, int32_t bits);
+uint64_t smo_expert_coded_size(const void* code, uint64_t count, int32_t bits);
 smo_status smo_expert_encode(const void* src, uint64_t count, int32_t bits, void* dst, int32_t* overflow,
                              smo_stream stream);
 smo_status smo_expert_decode(const void* src, uint64_t count, int32_t bits, void* dst, smo_stream stream);

@@ -89,6 +89,7 @@ _SIGS = {
     "smo_verify_attention": (C.c_int, [C.POINTER(AttnArgs), _vp]),
     "smo_cpu_verify_attention": (C.c_int, [C.POINTER(AttnArgs), _i32]),
     "smo_expert_code_bytes": (_sz, [_u64, _i32]),
+    "smo_expert_coded_size": (_u64, [_vp, _u64, _i32]),
     "smo_expert_encode": (C.c_int, [_vp, _u64, _i32, _vp, _vp, _vp]),
     "smo_expert_decode": (C.c_int, [_vp, _u64, _i32, _vp, _vp]),
     "smo_chunked_attention_f64": (C.c_int, [_sz, _sz, _sz, _vp, _vp, _vp, _sz, _vp, _vp]),

@@ -35,6 +35,7 @@ int moe_launch(const void* x_perm, int rows, int h, int hi, int E, const int32_t
                uint64_t w_block_stride, int pool_blocks, const int32_t* w_index, void* hbuf, float* y, int splits,
                int max_splits, int* done, cudaStream_t st);
 size_t expert_code_bytes(size_t count, int bits);
+size_t expert_coded_size(const void* code, size_t count, int bits);
 void expert_encode(const void* src, size_t count, int bits, void* dst, int* overflow, cudaStream_t st);
 void expert_decode(const void* src, size_t count, int bits, void* dst, cudaStream_t st);
 void rmsnorm(const float* x, const void* gain, int T, int h, float eps, void* y, cudaStream_t st);
@@ -192,7 +193,13 @@ smo_status smo_expert_decode(const void* src, uint64_t count, int32_t bits, void
   return guard([&] { smo::expert_decode(src, size_t(count), bits, dst, S(stream)); });
 }
 size_t smo_expert_code_bytes(uint64_t count, int32_t bits) {
-  return (bits == 3 || bits == 4) ? smo::expert_code_bytes(size_t(count), bits) : 0;
+  return (bits == 1 || bits == 3 || bits == 4) ? smo::expert_code_bytes(size_t(count), bits) : 0;
+}
+uint64_t smo_expert_coded_size(const void* code, uint64_t count, int32_t bits) {
+  if (!(bits == 1 || bits == 3 || bits == 4) || (bits == 1 && !code)) return 0;
+  uint64_t r = 0;
+  if (guard([&] { r = smo::expert_coded_size(code, size_t(count), bits); }) != SMO_OK) return 0;
+  return r;
 }
 
 smo_status smo_unpermute_combine_split(const float* y, int32_t splits, uint64_t split_stride, const int32_t* pos,

@@ -1,3 +1,4 @@
+#include <cstring>
 // engine.cu — VerifyEngine: the measured realisation of the reference's
 // target-verification DAG (pipeline.hpp:147-206) on one B200.
 //
@@ -56,7 +57,7 @@ void Engine::decode_slot(int l, cudaStream_t st) {
   const int s = l % slots;
   if (coded_streamed[size_t(l)].empty()) return;
   SMO_CUDA_CHECK(cudaEventRecord(dec_ev[size_t(2 * l)], st));
-  for (int bits = 3; bits <= 4; ++bits) {  // one launch per code width (blocks of a layer share it in practice)
+  for (int bits : {1, 3, 4}) {  // one launch per code (blocks of a layer share it in practice)
     const void* src[64];
     void* dst[64];
     int n = 0;
@@ -215,11 +216,15 @@ void Engine::create() {
   xcomp = opt.compress_experts != 0;
   uint8_t* cenc = nullptr;
   int* d_ovf = nullptr;
+  bool unary = false;
   if (xcomp) {
-    cblk_bytes = expert_code_bytes(blk_elems, 4);
-    cenc = dalloc<uint8_t>(cblk_bytes);
+    cblk_bytes = expert_code_bytes(blk_elems, 4);  // staging stride: no block is kept coded above it
+    const char* f = std::getenv("SMO_CODEC");
+    unary = !(f && std::strcmp(f, "fixed") == 0);
+    cenc = dalloc<uint8_t>(unary ? expert_code_bytes(blk_elems, 1) : cblk_bytes);
     d_ovf = dalloc<int>(1);
     blk_coded.assign(size_t(host_alias) * E_loc, 0);
+    blk_csize.assign(size_t(host_alias) * E_loc, 0);
   }
   for (int a = 0; a < host_alias; ++a) {
     void* hp = nullptr;
@@ -235,16 +240,32 @@ void Engine::create() {
       fill_uniform(stage + 2 * size_t(hi) * h, size_t(h) * hi, cfg.seed, base + 2, 0, std::sqrt(3.0f / hi), st);
       uint16_t* hdst = host_bufs[a] + size_t(local(e)) * blk_elems;
       bool coded = false;
-      for (int bits = 3; xcomp && !coded && bits <= 4; ++bits) {  // the narrowest code that holds the block
+      // the smallest code that holds the block: unary (variable length) when
+      // it beats the 3-bit window, else 3 or 4 bits, else unary if still
+      // within the staging stride, else raw bf16 — lossless in every case
+      size_t ubytes = 0;
+      if (xcomp && unary) {
+        SMO_CUDA_CHECK(cudaStreamSynchronize(st));
+        expert_encode(stage, blk_elems, 1, cenc, d_ovf, st);
+        ubytes = expert_coded_size(cenc, blk_elems, 1);
+      }
+      auto keep = [&](int bits, size_t cb) {
+        SMO_CUDA_CHECK(cudaMemcpy(hdst, cenc, cb, cudaMemcpyDeviceToHost));
+        blk_coded[size_t(a) * E_loc + local(e)] = uint8_t(bits);
+        blk_csize[size_t(a) * E_loc + local(e)] = cb;
+        coded = true;
+      };
+      if (ubytes && ubytes <= expert_code_bytes(blk_elems, 3)) keep(1, ubytes);
+      for (int bits = 3; xcomp && !coded && bits <= 4; ++bits) {
         SMO_CUDA_CHECK(cudaMemset(d_ovf, 0, sizeof(int)));
         expert_encode(stage, blk_elems, bits, cenc, d_ovf, st);
         int ovf = 0;
         SMO_CUDA_CHECK(cudaMemcpy(&ovf, d_ovf, sizeof(int), cudaMemcpyDeviceToHost));
-        if (!ovf) {
-          SMO_CUDA_CHECK(cudaMemcpy(hdst, cenc, expert_code_bytes(blk_elems, bits), cudaMemcpyDeviceToHost));
-          blk_coded[size_t(a) * E_loc + local(e)] = uint8_t(bits);
-          coded = true;
-        }
+        if (!ovf) keep(bits, expert_code_bytes(blk_elems, bits));
+      }
+      if (xcomp && !coded && ubytes && ubytes <= cblk_bytes) {
+        expert_encode(stage, blk_elems, 1, cenc, d_ovf, st);
+        keep(1, ubytes);
       }
       if (!coded) SMO_CUDA_CHECK(cudaMemcpy(hdst, stage, blk_bytes, cudaMemcpyDeviceToHost));
     }
@@ -270,7 +291,8 @@ void Engine::create() {
       if (cb < 0) continue;
       const uint16_t* hsrc = host_bufs[host_layer(l)] + size_t(local(e)) * blk_elems;
       if (const int bits = code_bits(l, local(e))) {
-        SMO_CUDA_CHECK(cudaMemcpy(cenc, hsrc, expert_code_bytes(blk_elems, bits), cudaMemcpyHostToDevice));
+        SMO_CUDA_CHECK(cudaMemcpy(cenc, hsrc, blk_csize[size_t(host_layer(l)) * E_loc + size_t(local(e))],
+                                  cudaMemcpyHostToDevice));
         expert_decode(cenc, blk_elems, bits, pool + size_t(cb) * blk_elems, st);
       } else {
         SMO_CUDA_CHECK(cudaMemcpy(pool + size_t(cb) * blk_elems, hsrc, blk_bytes, cudaMemcpyHostToDevice));
@@ -486,7 +508,8 @@ double Engine::enqueue_h2d(int l, cudaEvent_t t0, cudaEvent_t t1, const uint8_t*
     for (int q = 0; q < E_loc; ++q) {
       if (!streamed(q)) continue;
       if (const int bits = code_bits(l, q)) {
-        const size_t cb = expert_code_bytes(blk_elems, bits);
+        (void)bits;
+        const size_t cb = blk_csize[size_t(host_layer(l)) * E_loc + size_t(q)];
         SMO_CUDA_CHECK(cudaMemcpyAsync(cstage + (size_t(s) * E_loc + q) * cblk_bytes, hb + size_t(q) * blk_elems,
                                        cb, cudaMemcpyHostToDevice, copy));
         bytes += double(cb);

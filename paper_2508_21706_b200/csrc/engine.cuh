@@ -71,6 +71,7 @@ int moe_launch(const void* x_perm, int rows, int h, int hi, int E, const int32_t
                int max_splits, int* done, cudaStream_t st);
 int pick_moe_splits(int rows, int h, int hi, int E, int max_splits);
 size_t expert_code_bytes(size_t count, int bits);
+size_t expert_coded_size(const void* code, size_t count, int bits);
 void expert_encode(const void* src, size_t count, int bits, void* dst, int* overflow, cudaStream_t st);
 void expert_decode(const void* src, size_t count, int bits, void* dst, cudaStream_t st);
 void expert_decode_blocks(const void* const* srcs, void* const* dsts, int n, size_t count, int bits, cudaStream_t st);
@@ -155,7 +156,8 @@ struct Engine {
   // cstage and are expanded into the pool slot on the compute stream
   bool xcomp = false;
   size_t cblk_bytes = 0;                  // coded bytes of one [W1|W3|W2] block at 4 bits (staging stride)
-  std::vector<uint8_t> blk_coded;         // [host_alias * E_loc] exponent bits of the host block (0 = raw)
+  std::vector<uint8_t> blk_coded;         // [host_alias * E_loc] code of the host block: 0 raw, 1 unary, 3 / 4 bits
+  std::vector<size_t> blk_csize;          // [host_alias * E_loc] coded bytes of the host block
   uint8_t* cstage = nullptr;              // [slots][E_loc][cblk_bytes]
   std::vector<std::vector<int>> coded_streamed;  // per layer: local experts streamed coded
   std::vector<cudaEvent_t> dec_ev;        // [2L] around each layer's block expansion

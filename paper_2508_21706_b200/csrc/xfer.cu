@@ -23,6 +23,29 @@
 // One warp per segment in both directions; lane l owns the 8-value groups
 // 32q + l, so every memory instruction is one contiguous run; escapes are
 // ranked in position order with a warp exclusive scan per group column.
+//
+// Unary format (bits = 1, variable length, the engine's first choice):
+// exponent e of a segment with base E codes as j = E - e ONES followed by
+// a ZERO (bit stream MSB-first in 32-bit words: stream bit k = bit
+// 31 - k % 32 of word k / 32, so a code's length is one count-leading-ones); j = 15 is an escape (15 ones + zero, the
+// exponent byte in the escape list) for e > E or e <= E - 15. E is the
+// segment maximum or up to 7 below it, whichever gives the fewest bits. For uniform-init weights j is geometric
+// with p = 1/2 — unary is its optimal prefix code, 2 bits per exponent on
+// average: ~10.2 bits/weight (1.57x) against 11.4 for the 3-bit window, and
+// 3.3 instead of 4 bits for gaussian weights. Block layout:
+//   table  USeg[segs + 1] (8 B each: byte offset of the segment in the block,
+//          base E, 1 if the segment has escapes, stream words nw), entry [segs].off = total coded bytes;
+//          padded to 16 B
+//   per segment (16-B aligned): lo[1024] (sign << 7 | mantissa), nw 32-bit
+//          code words (trailing bits of the last word are ones), escaped
+//          exponent bytes in position order, zero padding.
+// Decoding is parallel without per-value offsets: value i ends at the i-th
+// zero of the stream, so where each lane's run of 32 values starts follows
+// from a warp scan of zero counts per code word.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
 #include "common.cuh"
 
 namespace smo {
@@ -249,10 +272,264 @@ __global__ void __launch_bounds__(32 * kDecWarps) expert_decode_kernel(const __g
   }
 }
 
+// ---------------------------------------------------------------- unary
+struct USeg {
+  uint32_t off;   // segment byte offset in the block (entry [segs]: total bytes)
+  uint8_t emax;   // largest exponent of the segment
+  uint8_t flags;  // bit 0: the segment has escapes
+  uint16_t nw;    // code stream words
+};
+static_assert(sizeof(USeg) == 8, "USeg is 8 bytes");
+constexpr int kUEsc = 15;        // j >= 15 escapes
+constexpr int kUMaxWords = 512;  // 1024 codes of <= 16 bits
+constexpr int kUEncWarps = 8;
+__host__ __device__ inline size_t u_table_bytes(size_t segs) { return ((segs + 1) * sizeof(USeg) + 15) & ~size_t(15); }
+
+// Pass 1 (write = false): per-segment E, nw and padded size into the table
+// (off = size). Pass 2: the host has turned sizes into offsets; write.
+// Lane l owns values [32 l, 32 l + 32) so stream order is value order.
+__global__ void __launch_bounds__(32 * kUEncWarps) unary_encode_kernel(const uint16_t* __restrict__ src, size_t segs,
+                                                                       uint8_t* __restrict__ dst, bool write) {
+  __shared__ uint32_t words[kUEncWarps][kUMaxWords];
+  const int wib = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const size_t seg = size_t(blockIdx.x) * kUEncWarps + wib;
+  if (seg >= segs) return;
+  const uint4* s = reinterpret_cast<const uint4*>(src + seg * kSeg + 32 * lane);
+  uint16_t v[32];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint4 u = s[i];
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      v[8 * i + 2 * t] = uint16_t(w[t] & 0xffffu);
+      v[8 * i + 2 * t + 1] = uint16_t(w[t] >> 16);
+    }
+  }
+  int emax = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) emax = max(emax, int((v[i] >> 7) & 0xff));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+  int emax_base = emax;
+  // base E: of emax, emax - 1, ..., emax - 7 the one with the fewest bits
+  // (values above E escape: a few outliers then cost 24 bits each instead of
+  // lengthening every code of the segment)
+  int best = 1 << 30;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int b0 = emax - c;
+    int cost = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int e = int((v[i] >> 7) & 0xff);
+      cost += e <= b0 ? min(b0 - e, kUEsc) + 1 : kUEsc + 1 + 8;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cost += __shfl_xor_sync(0xffffffffu, cost, o);
+    if (b0 >= 0 && cost < best) {
+      best = cost;
+      emax_base = b0;
+    }
+  }
+  const int ebase = emax_base;
+  int nbits = 0, nesc = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int e = int((v[i] >> 7) & 0xff);
+    const int j = e <= ebase ? min(ebase - e, kUEsc) : kUEsc;
+    nbits += j + 1;
+    nesc += j == kUEsc;
+  }
+  int tbits = 0, tesc = 0;
+  const int bit0 = warp_excl_scan(nbits, lane, &tbits);
+  const int esc0 = warp_excl_scan(nesc, lane, &tesc);
+  const int nw = (tbits + 31) / 32;
+  const uint32_t bytes = uint32_t((kSeg + 4 * nw + tesc + 15) & ~15);
+  USeg* table = reinterpret_cast<USeg*>(dst);
+  if (!write) {
+    if (lane == 0) table[seg] = USeg{bytes, uint8_t(ebase), uint8_t(tesc ? 1 : 0), uint16_t(nw)};
+    return;
+  }
+  uint8_t* d = dst + table[seg].off;
+  uint32_t* wd = words[wib];
+  for (int k = lane; k < nw; k += 32) wd[k] = 0u;
+  __syncwarp();
+  int pos = bit0;
+  uint32_t lo[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+  int e_at = esc0;
+  uint8_t* esc = d + kSeg + 4 * nw;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const uint32_t x = v[i];
+    const int e = int((x >> 7) & 0xff);
+    const int j = e <= ebase ? min(ebase - e, kUEsc) : kUEsc;
+    if (j) {  // j ones at stream bits [pos, pos + j) (MSB-first): at most two words
+      const uint64_t ones = ((uint64_t(1) << j) - 1u) << (64 - (pos & 31) - j);
+      atomicOr(&wd[pos >> 5], uint32_t(ones >> 32));
+      if (uint32_t(ones)) atomicOr(&wd[(pos >> 5) + 1], uint32_t(ones));
+    }
+    if (j == kUEsc) esc[e_at++] = uint8_t(e);
+    pos += j + 1;
+    lo[i / 4] |= (((x >> 8) & 0x80u) | (x & 0x7fu)) << (8 * (i % 4));
+  }
+  if (lane == 0 && (tbits & 31)) atomicOr(&wd[tbits >> 5], (1u << (32 - (tbits & 31))) - 1u);  // trailing ones
+  reinterpret_cast<uint4*>(d)[2 * lane] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  reinterpret_cast<uint4*>(d)[2 * lane + 1] = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+  __syncwarp();
+  uint32_t* cw = reinterpret_cast<uint32_t*>(d + kSeg);
+  for (int k = lane; k < nw; k += 32) cw[k] = wd[k];
+  const int used = kSeg + 4 * nw + tesc;
+  if (lane < int(bytes) - used) d[used + lane] = 0;  // deterministic padding
+}
+
+// position (0-based, from the MSB) of the k-th set bit of x, k < popc(x):
+// binary search with population counts, branch-free
+__device__ __forceinline__ int select_msb(uint32_t x, int k) {
+  int pos = 0;
+#pragma unroll
+  for (int w = 16; w; w >>= 1) {
+    const int c = __popc(x >> (32 - w));  // set bits in the top w bits
+    const bool skip = k >= c;
+    k -= skip ? c : 0;
+    pos += skip ? w : 0;
+    x = skip ? x << w : x;
+  }
+  return pos;
+}
+
+// Decode: a warp stages the segment's code words in shared memory, finds
+// where each lane's 32 values start (value 32 L begins after zero 32 L - 1 of
+// the stream: a warp scan of zero counts over 3-word runs, then a popc
+// select inside the word), and every lane then walks its own 32 codes with a
+// 32-bit window — one count-leading-ones per value, no divergence — and
+// builds its 64 output bytes in registers from its 32 lo bytes.
+constexpr int kUDecWarps = 8;
+constexpr int kURun = 3;  // code words per lane per scan round
+__global__ void __launch_bounds__(32 * kUDecWarps) unary_decode_kernel(const __grid_constant__ DecodeJobs jobs,
+                                                                       size_t segs) {
+  __shared__ uint32_t wbuf[kUDecWarps][kUMaxWords + 8];
+  __shared__ int start[kUDecWarps][33];
+  const uint8_t* __restrict__ src = jobs.src[blockIdx.y];
+  uint16_t* __restrict__ dst = jobs.dst[blockIdx.y];
+  const int wib = threadIdx.x / 32, lane = threadIdx.x % 32;
+  uint32_t* wb = wbuf[wib];
+  int* st = start[wib];
+  // grid-stride over segments: a warp decodes several, launch cost amortised
+  for (size_t seg = size_t(blockIdx.x) * kUDecWarps + wib; seg < segs; seg += size_t(gridDim.x) * kUDecWarps) {
+    const uint2 tw = reinterpret_cast<const uint2*>(src)[seg];
+    const uint8_t* sb = src + tw.x;
+    const int base = int(tw.y & 0xffu), nw = int(tw.y >> 16);
+    const bool has_esc = (tw.y >> 8) & 1u;
+    const uint32_t* codes = reinterpret_cast<const uint32_t*>(sb + kSeg);
+    const uint4 lo0 = reinterpret_cast<const uint4*>(sb)[2 * lane];  // this lane's 32 lo bytes
+    const uint4 lo1 = reinterpret_cast<const uint4*>(sb)[2 * lane + 1];
+    // coalesced staging of the stream (words past the end read as ones)
+    for (int w = lane; w < nw + 6; w += 32) wb[w] = w < nw ? codes[w] : 0xffffffffu;
+    __syncwarp();
+    int cum = 0;
+    for (int c0 = 0; c0 < nw; c0 += 32 * kURun) {
+      const int w0 = c0 + kURun * lane;
+      uint32_t z[kURun];
+      int cnt[kURun], n = 0;
+#pragma unroll
+      for (int r = 0; r < kURun; ++r) {
+        z[r] = w0 + r < nw ? ~wb[w0 + r] : 0u;  // zeros = value ends
+        cnt[r] = __popc(z[r]);
+        n += cnt[r];
+      }
+      int tot = 0;
+      int before = cum + warp_excl_scan(n, lane, &tot);
+      cum += tot;
+      // lanes L whose first value follows zero 32 L - 1 when it lies in this run
+#pragma unroll
+      for (int r = 0; r < kURun; ++r) {
+        for (int L = (before + 32) / 32; L < 32 && 32 * L - 1 < before + cnt[r]; ++L)
+          st[L] = (w0 + r) * 32 + select_msb(z[r], 32 * L - 1 - before) + 1;
+        before += cnt[r];
+      }
+    }
+    if (lane == 0) {
+      st[0] = 0;
+      st[32] = 32 * nw;
+    }
+    __syncwarp();
+    const int p0 = st[lane];
+    // the lane's codes sit in words k0 .. k0 + 4 when its run is short (the
+    // common case): walk them from registers, shifting a 5-word queue
+    const int k0 = p0 >> 5;
+    const bool fits = st[lane + 1] - 32 * k0 <= 160;
+    uint32_t e4[8];
+    if (__all_sync(0xffffffffu, fits)) {
+      uint32_t q0 = wb[k0], q1 = wb[k0 + 1], q2 = wb[k0 + 2], q3 = wb[k0 + 3], q4 = wb[k0 + 4];
+      int pos = p0 & 31;  // bit offset inside q0
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int j = __clz(~__funnelshift_l(q1, q0, pos));  // <= 15: every code fits the window
+        pos += j + 1;
+        const bool cross = pos >= 32;
+        q0 = cross ? q1 : q0;
+        q1 = cross ? q2 : q1;
+        q2 = cross ? q3 : q2;
+        q3 = cross ? q4 : q3;
+        q4 = cross ? 0xffffffffu : q4;
+        pos &= 31;
+        const uint32_t e = uint32_t(base - j) & 0xffu;
+        e4[i / 4] = (i % 4 == 0) ? e : (e4[i / 4] | (e << (8 * (i % 4))));
+      }
+    } else {
+      int pos = p0;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int j = __clz(~__funnelshift_l(wb[(pos >> 5) + 1], wb[pos >> 5], pos & 31));
+        pos += j + 1;
+        const uint32_t e = uint32_t(base - j) & 0xffu;
+        e4[i / 4] = (i % 4 == 0) ? e : (e4[i / 4] | (e << (8 * (i % 4))));
+      }
+    }
+    if (has_esc) {  // rare: escaped exponents (j = 15), in position order
+      int p = p0, nesc = 0;
+      for (int i = 0; i < 32; ++i) {
+        const int j = __clz(~__funnelshift_l(wb[(p >> 5) + 1], wb[p >> 5], p & 31));
+        p += j + 1;
+        nesc += j == kUEsc;
+      }
+      int etot = 0;
+      int er = warp_excl_scan(nesc, lane, &etot);
+      const uint8_t* esc = sb + kSeg + 4 * nw;
+      p = p0;
+      for (int i = 0; i < 32 && nesc; ++i) {
+        const int j = __clz(~__funnelshift_l(wb[(p >> 5) + 1], wb[p >> 5], p & 31));
+        p += j + 1;
+        if (j == kUEsc) {
+          const int sh = 8 * (i % 4);
+          e4[i / 4] = (e4[i / 4] & ~(0xffu << sh)) | (uint32_t(esc[er++]) << sh);
+          --nesc;
+        }
+      }
+    }
+    // 32 values -> 64 bytes: two values per word, lo bytes and exponents
+    // spread to 16-bit lanes with PRMT
+    const uint32_t lw[8] = {lo0.x, lo0.y, lo0.z, lo0.w, lo1.x, lo1.y, lo1.z, lo1.w};
+    uint32_t out[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const uint32_t sel = (k & 1) ? 0x4342u : 0x4140u;
+      const uint32_t l16 = __byte_perm(lw[k / 2], 0u, sel), x16 = __byte_perm(e4[k / 2], 0u, sel);
+      out[k] = ((l16 & 0x00800080u) << 8) | (l16 & 0x007f007fu) | (x16 << 7);
+    }
+    uint4* d = reinterpret_cast<uint4*>(dst + seg * kSeg + 32 * lane);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) d[k] = make_uint4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
+    __syncwarp();  // wb / st are reused by the next segment
+  }
+}
+
 }  // namespace
 
 size_t expert_code_bytes(size_t count, int bits) {
-  SMO_REQUIRE(bits == 3 || bits == 4, "expert codec: bits must be 3 or 4");
+  SMO_REQUIRE(bits == 1 || bits == 3 || bits == 4, "expert codec: bits must be 1 (unary), 3 or 4");
+  if (bits == 1) return u_table_bytes(count / kSeg) + (count / kSeg) * size_t(kSeg + 4 * kUMaxWords + kSeg);
   return (count / kSeg) * size_t(bits == 3 ? Fmt<3>::kSegBytes : Fmt<4>::kSegBytes);
 }
 
@@ -261,8 +538,39 @@ size_t expert_code_bytes(size_t count, int bits) {
 // keep the block raw).
 void expert_encode(const void* src, size_t count, int bits, void* dst, int* overflow, cudaStream_t st) {
   SMO_REQUIRE(src && dst && overflow && count % kSeg == 0, "expert codec: count must be a multiple of 1024");
-  SMO_REQUIRE(bits == 3 || bits == 4, "expert codec: bits must be 3 or 4");
+  SMO_REQUIRE(bits == 1 || bits == 3 || bits == 4, "expert codec: bits must be 1 (unary), 3 or 4");
   const size_t segs = count / kSeg;
+  if (bits == 1) {  // two passes around a host scan of the segment sizes (synchronous on st)
+    auto s16 = reinterpret_cast<const uint16_t*>(src);
+    auto d8 = reinterpret_cast<uint8_t*>(dst);
+    const unsigned grid = unsigned((segs + kUEncWarps - 1) / kUEncWarps);
+    std::vector<USeg> t(segs + 1);
+    if (segs) {
+      unary_encode_kernel<<<grid, 32 * kUEncWarps, 0, st>>>(s16, segs, d8, false);
+      count_launch();
+      SMO_CUDA_CHECK(cudaGetLastError());
+      SMO_CUDA_CHECK(cudaMemcpyAsync(t.data(), d8, segs * sizeof(USeg), cudaMemcpyDeviceToHost, st));
+      SMO_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+    size_t off = u_table_bytes(segs);
+    for (size_t i = 0; i < segs; ++i) {
+      const size_t b = t[i].off;
+      t[i].off = uint32_t(off);
+      off += b;
+    }
+    SMO_REQUIRE(off < (size_t(1) << 32), "expert codec: block too large for 32-bit segment offsets");
+    t[segs] = USeg{uint32_t(off), 0, 0, 0};
+    std::vector<uint8_t> head(u_table_bytes(segs), 0);
+    std::memcpy(head.data(), t.data(), t.size() * sizeof(USeg));
+    SMO_CUDA_CHECK(cudaMemcpyAsync(d8, head.data(), head.size(), cudaMemcpyHostToDevice, st));
+    if (segs) {
+      unary_encode_kernel<<<grid, 32 * kUEncWarps, 0, st>>>(s16, segs, d8, true);
+      count_launch();
+      SMO_CUDA_CHECK(cudaGetLastError());
+    }
+    SMO_CUDA_CHECK(cudaStreamSynchronize(st));
+    return;
+  }
   if (!segs) return;
   const int threads = 256;
   const unsigned grid = unsigned((segs * 32 + threads - 1) / threads);
@@ -277,7 +585,7 @@ void expert_encode(const void* src, size_t count, int bits, void* dst, int* over
 // Expand n blocks of `count` values each (srcs[i] -> dsts[i], all `bits`) in one launch.
 void expert_decode_blocks(const void* const* srcs, void* const* dsts, int n, size_t count, int bits, cudaStream_t st) {
   SMO_REQUIRE(n >= 0 && n <= 64 && count % kSeg == 0, "expert codec: up to 64 blocks of a multiple of 1024 values");
-  SMO_REQUIRE(bits == 3 || bits == 4, "expert codec: bits must be 3 or 4");
+  SMO_REQUIRE(bits == 1 || bits == 3 || bits == 4, "expert codec: bits must be 1 (unary), 3 or 4");
   const size_t segs = count / kSeg;
   if (!segs || !n) return;
   DecodeJobs jobs{};
@@ -286,11 +594,31 @@ void expert_decode_blocks(const void* const* srcs, void* const* dsts, int n, siz
     jobs.src[i] = reinterpret_cast<const uint8_t*>(srcs[i]);
     jobs.dst[i] = reinterpret_cast<uint16_t*>(dsts[i]);
   }
+  if (bits == 1) {
+    // ~8 resident blocks per SM (148 SMs) in total, split over the n blocks
+    const size_t want = (segs + kUDecWarps - 1) / kUDecWarps;
+    const size_t cap = std::max<size_t>(1, (148 * 8 + n - 1) / n);
+    const dim3 ug(unsigned(std::min(want, cap)), unsigned(n));
+    unary_decode_kernel<<<ug, 32 * kUDecWarps, 0, st>>>(jobs, segs);
+    count_launch();
+    SMO_CUDA_CHECK(cudaGetLastError());
+    return;
+  }
   const dim3 grid(unsigned((segs + kDecWarps * kDecSegs - 1) / (kDecWarps * kDecSegs)), unsigned(n));
   if (bits == 3) expert_decode_kernel<3><<<grid, 32 * kDecWarps, 0, st>>>(jobs, segs);
   else expert_decode_kernel<4><<<grid, 32 * kDecWarps, 0, st>>>(jobs, segs);
   count_launch();
   SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+// Bytes of a coded block: fixed for 3 / 4 bits; unary reads the table's last
+// entry from the (device) code.
+size_t expert_coded_size(const void* code, size_t count, int bits) {
+  if (bits != 1) return expert_code_bytes(count, bits);
+  USeg t{};
+  SMO_CUDA_CHECK(cudaMemcpy(&t, reinterpret_cast<const uint8_t*>(code) + (count / kSeg) * sizeof(USeg), sizeof(t),
+                            cudaMemcpyDeviceToHost));
+  return t.off;
 }
 
 void expert_decode(const void* src, size_t count, int bits, void* dst, cudaStream_t st) {

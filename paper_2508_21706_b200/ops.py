@@ -123,13 +123,17 @@ def moe_experts(x_perm, offsets, pool, *, h: int, h_i: int, n_expert: int, w_blo
 
 def expert_encode(x, bits: int = 3):
     """Lossless code of a bf16 tensor (numel % 1024 == 0) with `bits`-bit
-    exponent codes: returns (uint8 code, overflow) — overflow means a segment
-    needed > 32 escapes (retry with 4 bits or keep the tensor raw)."""
+    exponent codes (bits = 1: the variable-length unary code): returns
+    (uint8 code, overflow) — overflow means a segment needed > 32 escapes
+    (retry with 4 bits or keep the tensor raw); unary never overflows and its
+    code is trimmed to the bytes used."""
     _req(x, _BF16, "x")
     n = x.numel()
     code = torch.empty(int(L.load().smo_expert_code_bytes(n, bits)), dtype=torch.uint8, device=x.device)
     ovf = torch.zeros(1, dtype=torch.int32, device=x.device)
     L.check(L.load().smo_expert_encode(_p(x), n, bits, _p(code), _p(ovf), _stream()))
+    if bits == 1:
+        code = code[:int(L.load().smo_expert_coded_size(_p(code), n, bits))]
     return code, bool(ovf.item())
 
 

@@ -426,6 +426,68 @@ def _np_decode_segment(seg: np.ndarray, bits: int) -> np.ndarray:
     return (((lo & 0x80) << 8) | (e << 7) | (lo & 0x7F)).astype(np.uint16)
 
 
+def _np_unary_decode(code: np.ndarray, n: int, segs_to_check) -> dict:
+    """The unary block format (xfer.cu header), restated in numpy: table of
+    (offset u32, E u8, flags u8, nw u16); per segment lo[1024], nw MSB-first code
+    words (value i ends at the i-th zero; j ones before it: e = E - j, j >= 15
+    escapes to the next escape byte), escape bytes."""
+    segs = n // 1024
+    table = code[:8 * (segs + 1)].view(np.uint8)
+    out = {}
+    for sgm in segs_to_check:
+        t = table[8 * sgm:8 * sgm + 8]
+        off = int(t[:4].view(np.uint32)[0])
+        emax, flags, nw = int(t[4]), int(t[5]), int(t[6:8].view(np.uint16)[0])
+        lo = code[off:off + 1024].astype(np.uint32)
+        words = code[off + 1024:off + 1024 + 4 * nw].view(np.uint32)  # MSB-first within each word
+        bits = np.unpackbits(words.astype(">u4").view(np.uint8))
+        zeros = np.flatnonzero(bits == 0)
+        assert len(zeros) == 1024 and np.all(bits[zeros[-1] + 1:] == 1)
+        j = np.diff(np.concatenate([[-1], zeros])) - 1
+        e = (emax - j).astype(np.uint32)  # emax = the segment's base E
+        esc_at = np.flatnonzero(j >= 15)
+        assert flags == (1 if len(esc_at) else 0)
+        e[esc_at] = code[off + 1024 + 4 * nw:off + 1024 + 4 * nw + len(esc_at)]
+        out[sgm] = (((lo & 0x80) << 8) | (e << 7) | (lo & 0x7F)).astype(np.uint16)
+    return out
+
+
+@pytest.mark.parametrize("kind", ["procedural", "normal", "wide"])
+def test_expert_codec_unary_lossless(cuda, oracle, kind):
+    """The unary exponent code (bits = 1, the engine's default link code):
+    bit-exact round trip for uniform-init, gaussian-with-outliers and
+    fully random bit patterns (escapes everywhere); byte layout matches the
+    numpy restatement; size ~10.2 bits/weight on the engine's weights."""
+    import torch
+    from paper_2508_21706_b200 import ops
+    n = 1024 * 300
+    if kind == "procedural":
+        x = torch.from_numpy(oracle.fill_uniform_bf16(n, 0x5EED, 1234, math.sqrt(3.0 / 4096)).view(np.int16)).to(cuda)
+        x = x.view(torch.bfloat16)
+    elif kind == "normal":
+        g = torch.Generator(device=cuda).manual_seed(5)
+        x = (torch.randn(n, generator=g, device=cuda) * 0.02).to(torch.bfloat16)
+        x[::997] = 0
+        x[::4099] *= 64
+    else:
+        g = torch.Generator(device=cuda).manual_seed(6)
+        x = torch.randint(0, 1 << 16, (n,), generator=g, device=cuda, dtype=torch.int32).to(torch.int16)
+        x = x.view(torch.bfloat16)
+    code, ovf = ops.expert_encode(x, 1)
+    assert not ovf
+    bpw = code.numel() * 8 / n
+    if kind == "procedural":
+        assert 9.9 < bpw < 10.6, bpw
+    elif kind == "normal":  # below the 4-bit window code's 12.375
+        assert bpw < 12.0, bpw
+    y = ops.expert_decode(code, n, 1)
+    assert torch.equal(y.view(torch.int16), x.view(torch.int16))
+    c = code.cpu().numpy()
+    xs = x.view(torch.int16).cpu().numpy().view(np.uint16)
+    for sgm, v in _np_unary_decode(c, n, (0, 7, 150, 299)).items():
+        assert np.array_equal(v, xs[sgm * 1024:(sgm + 1) * 1024]), sgm
+
+
 @pytest.mark.parametrize("kind,bits", [("procedural", 3), ("procedural", 4), ("normal", 3), ("normal", 4),
                                        ("wide", 4)])
 def test_expert_codec_lossless(cuda, oracle, kind, bits):

@@ -97,18 +97,20 @@ def moe(T=288, h=4096, hi=14336, E=8, k=2, split=0):
     return r
 
 
-def codec(n=3 * 4096 * 14336):
+def codec(n=3 * 4096 * 14336, bits=3):
     """K5 codec on one Mixtral expert block: decode reads the code, writes bf16."""
     g = torch.Generator(device=dev).manual_seed(4)
     x = ((torch.rand((n,), generator=g, device=dev) * 2 - 1) * 0.027).to(torch.bfloat16)
-    code, ovf = ops.expert_encode(x, 3)
+    code, ovf = ops.expert_encode(x, bits)
     assert not ovf
     out = torch.empty_like(x)
-    t = timeit(lambda: L.check(L.load().smo_expert_decode(code.data_ptr(), n, 3, out.data_ptr(),
+    t = timeit(lambda: L.check(L.load().smo_expert_decode(code.data_ptr(), n, bits, out.data_ptr(),
                                                           torch.cuda.current_stream().cuda_stream)))
+    assert torch.equal(out.view(torch.int16), x.view(torch.int16))
     byts = code.numel() + 2 * n
-    return {"kernel": "K5 expert_decode (3-bit)", "N": n, "us": t * 1e6, "GBs": byts / t / 1e9, "frac": byts / t / 1e9 / PEAK,
-            "TFLOPs": 0.0}
+    name = "unary" if bits == 1 else f"{bits}-bit"
+    return {"kernel": f"K5 expert_decode ({name})", "N": n, "bits_per_weight": code.numel() * 8 / n,
+            "us": t * 1e6, "GBs": byts / t / 1e9, "frac": byts / t / 1e9 / PEAK, "TFLOPs": 0.0}
 
 
 def main():
@@ -125,7 +127,8 @@ def main():
                             continue
                         res.append(attn(b, n, s))
     if what in ("codec", "all"):
-        res.append(codec())
+        res.append(codec(bits=3))
+        res.append(codec(bits=1))
     if what in ("gemm", "all"):
         res.append(gemm(288, 4096, 6144, name="qkv"))
         res.append(gemm(288, 4096, 4096, L.EPI_F32_ADD, name="o-proj (+residual)"))
