@@ -537,15 +537,18 @@ def run_ours(args):
                 "algorithmic per layer = " + str((shape.n_expert // ep_size) * shape.expert_bytes),
                 "peak_kind": pk_kind}
     # with the coded transfer the block expansion is the largest device-time kernel
-    # (profiles/r01f_launches.md): algorithmic bytes = code read + bf16 written
+    # (profiles/r01h_launches.md): algorithmic bytes = code read + bf16 written
     codec_roof = None
     if args.compress and stages.get("codec", 0) > 0:
         cb = stages["h2d_bytes"] + stages["h2d_raw_bytes"]
         codec_roof = {"bound": "hbm", "kernel": "K5 expert_decode (coded blocks -> bf16 HBM slot), per step",
                       "achieved": cb / stages["codec"] / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
                       "frac": cb / stages["codec"] / 1e9 / pk["hbm_gbs"], "traffic": codec_traffic_per_block(),
-                      "traffic_unit": "dram bytes per expert block (one decode launch, ncu profiles/r01f_traffic.json);"
-                      " algorithmic per block = " + str(int(shape.expert_bytes * (1 + 1456 / 2048))),
+                      "traffic_unit": "dram bytes per expert block (one layer's decode launch / its blocks, ncu "
+                      "profiles/r01h_traffic.json); algorithmic per block = "
+                      + str(int(cb / max(1.0, stages["h2d_raw_bytes"]) * shape.expert_bytes)),
+                      "bound_note": "the unary decoder is ALU-issue bound (ALU pipe 84 % of peak, ncu "
+                      "profiles/r01h_launches.md); HBM is not its limiter",
                       "peak_kind": pk_kind}
     line = {
         "metric": "verified decode tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world,

@@ -72,7 +72,10 @@ def test_ep_loopback_bit_identical_to_single_gpu(cuda, P, compress):
     t0 = engines[0].last_times()
     raw = shape.n_layers * (shape.n_expert // P) * shape.expert_bytes
     assert t0["h2d_raw_bytes"] == raw
-    assert t0["h2d_bytes"] == (raw * 1456 // 2048 if compress else raw)  # coded blocks: 1456 B per 1024 weights
+    if compress:  # coded blocks: the unary code, below the 3-bit window's 1456 B per 1024 weights
+        assert 0 < t0["h2d_bytes"] <= raw * 1456 // 2048
+    else:
+        assert t0["h2d_bytes"] == raw
     for e in engines:
         e.close()
     grp.close()
