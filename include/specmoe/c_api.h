@@ -298,11 +298,12 @@ typedef struct {
                                  1 = BATCH_ONE: after layer l's router, stream only the experts its
                                  tokens selected (host waits for the routing, then issues the copies).
                                  Prefill always streams whole layers. Not with expert parallelism. */
-  int32_t compress_experts;   /* 1: experts sit in pinned host DRAM in the lossless code of
-                                 smo_expert_encode (3-bit exponents: 1.41x fewer bytes; blocks that
-                                 need it get 4 bits: 1.29x; blocks neither can hold stay raw) and
-                                 cross the link coded; the compute stream expands each layer's
-                                 blocks into its HBM slot before the expert kernel. */
+  int32_t compress_experts;   /* 1: experts sit in pinned host DRAM in the smallest lossless code of
+                                 smo_expert_encode that holds the block (unary exponents: 1.56x fewer
+                                 bytes on uniform-init weights; 3-bit window 1.41x; 4-bit 1.29x;
+                                 else raw; env SMO_CODEC=fixed skips unary) and cross the link
+                                 coded; the compute stream expands each layer's blocks into its HBM
+                                 slot before the expert kernel. */
 } smo_engine_options;
 
 /* ---- expert parallelism ----------------------------------
