@@ -200,6 +200,41 @@ smo_status smo_expert_encode(const void* src, uint64_t count, int32_t bits, void
                              smo_stream stream);
 smo_status smo_expert_decode(const void* src, uint64_t count, int32_t bits, void* dst, smo_stream stream);
 
+/* ---- K5 expert streamer as a standalone handle (streamer.cu) --------------
+ * The reference's H2D_EXPERTS(l) stage and the GPU_MOE(l) dependency on it
+ * (pipeline.hpp:147-206; transfer bytes roofline.hpp:56-77; LARGE_BATCH vs
+ * BATCH_ONE roofline.hpp:155-162 -> `active`). Expert blocks (bf16, block_bytes
+ * each, a multiple of 2048) live in caller-owned PINNED host memory, raw or in
+ * a K5 code (host_codes 1 = unary, 3 / 4 = window codes; host_bytes = coded
+ * size). Layer l streams into HBM slot l % hbm_slots on the streamer's own
+ * copy-engine stream; the first cache_bytes / block_bytes blocks in (layer,
+ * expert) order are copied to HBM once at create (the hot-expert cache,
+ * MemoryPolicy.expert_cache_bytes) and never streamed. Per layer:
+ *   enqueue_layer (async; waits for the slot's previous release)
+ *   wait_layer(stream)   -- stream waits for the copies; coded blocks are
+ *                           expanded into the slot on `stream`
+ *   expert_ptr           -- device block [W1|W3|W2] of (layer, expert)
+ *   release_layer(stream)-- the slot may be refilled once `stream` gets here
+ * active (nullable, [n_experts]): 0 = not routed to, not streamed.          */
+typedef struct smo_streamer smo_streamer;
+typedef struct {
+  int32_t n_layers, n_experts;
+  uint64_t block_bytes;            /* bf16 bytes of one expert block in HBM */
+  const void* const* host_blocks;  /* [n_layers * n_experts] pinned host pointers */
+  const uint64_t* host_bytes;      /* nullable: link bytes of each coded block */
+  const int32_t* host_codes;       /* nullable: 0 raw, 1 unary, 3 / 4 bits per block */
+  int32_t hbm_slots;               /* >= 2 */
+  int64_t cache_bytes;             /* hot-expert cache in HBM */
+  int32_t device;
+} smo_streamer_args;
+smo_status smo_streamer_create(const smo_streamer_args* args, smo_streamer** out);
+smo_status smo_streamer_destroy(smo_streamer* s);
+smo_status smo_streamer_enqueue_layer(smo_streamer* s, int32_t layer, const uint8_t* active);
+smo_status smo_streamer_expert_ready_event(smo_streamer* s, int32_t layer, void** cuda_event);
+smo_status smo_streamer_wait_layer(smo_streamer* s, int32_t layer, smo_stream stream);
+smo_status smo_streamer_expert_ptr(smo_streamer* s, int32_t layer, int32_t expert, const void** out);
+smo_status smo_streamer_release_layer(smo_streamer* s, int32_t layer, smo_stream stream);
+
 /* ---- support ops of the verify layer (standard Mixtral block, not in the
  *      reference: SURVEY.md §2.3 "support")                                 */
 /* y bf16 [T,h] = x f32 [T,h] * rsqrt(mean(x^2)+eps) * gain bf16 [h] */
@@ -328,6 +363,25 @@ smo_status smo_ep_group_destroy(smo_ep_group* g);
  * slot_bytes >= the largest exchange block: max(T*k*h*2 + 16 + 4*E/P,
  * T*k*h*4) for the engine's T = max_batch * max_verify.                    */
 typedef void (*smo_barrier_fn)(void* ctx);
+/* Standalone dispatch / combine around a caller-run expert shard (the engine
+ * runs the same kernels internally). Rank `rank` of the group owns experts
+ * e % P == rank (local index e / P). dispatch: x bf16 [T,h], ids int32 [T,k]
+ * (global expert ids, router output) -> xl bf16 [P*C,h] rows grouped by local
+ * expert (offsets_l [E/P+1]; src-major inside an expert), back int32 [P*C]
+ * (where each row returns), pos_ep int32 [T*k] (for combine). combine: the
+ * shard's fp32 outputs yl [P*C,h] travel back and x fp32 [T,h] +=
+ * sum_j weights[t,j] * y(t,j) in slot order (the single-GPU combine). C =
+ * rows per destination, the same on every rank, >= T*k. workspace: device,
+ * smo_ep_workspace(P,T,k,h,E,C) bytes, shared by both calls. All ranks call
+ * collectively (same order); async on `stream` (host-synchronising for the
+ * loopback / IPC transports' barriers). */
+size_t smo_ep_workspace(int32_t P, int32_t T, int32_t k, int32_t h, int32_t E, int32_t C);
+smo_status smo_ep_dispatch(smo_ep_group* g, int32_t rank, const void* x, const int32_t* ids, int32_t T, int32_t k,
+                           int32_t h, int32_t E, int32_t C, void* xl, int32_t* offsets_l, int32_t* back,
+                           int32_t* pos_ep, void* workspace, smo_stream stream);
+smo_status smo_ep_combine(smo_ep_group* g, int32_t rank, const float* yl, const int32_t* back,
+                          const int32_t* offsets_l, const int32_t* pos_ep, const float* weights, int32_t T,
+                          int32_t k, int32_t h, int32_t E, int32_t C, float* x, void* workspace, smo_stream stream);
 size_t smo_ep_ipc_handle_bytes(void);
 smo_status smo_ep_ipc_create(int32_t nranks, int32_t rank, uint64_t slot_bytes, smo_ep_group** out,
                              uint8_t* handles);

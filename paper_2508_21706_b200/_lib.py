@@ -63,6 +63,12 @@ class EngineOptions(C.Structure):
                 ("compress_experts", _i32)]
 
 
+class StreamerArgs(C.Structure):
+    _fields_ = [("n_layers", _i32), ("n_experts", _i32), ("block_bytes", _u64), ("host_blocks", _vp),
+                ("host_bytes", _vp), ("host_codes", _vp), ("hbm_slots", _i32), ("cache_bytes", _i64),
+                ("device", _i32)]
+
+
 class VerifyBatch(C.Structure):
     _fields_ = [("b", _i32), ("n", _i32), ("tokens", _vp), ("parent", _vp), ("prefix_len", _vp),
                 ("on_device", _i32)]
@@ -118,6 +124,16 @@ _SIGS = {
     "smo_ep_ipc_connect": (C.c_int, [_vp, _vp, _vp, _vp]),
     "smo_engine_create": (C.c_int, [C.POINTER(ModelConfig), C.POINTER(EngineOptions), C.POINTER(_vp)]),
     "smo_engine_destroy": (C.c_int, [_vp]),
+    "smo_ep_workspace": (_sz, [_i32, _i32, _i32, _i32, _i32, _i32]),
+    "smo_ep_dispatch": (C.c_int, [_vp, _i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "smo_ep_combine": (C.c_int, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp]),
+    "smo_streamer_create": (C.c_int, [_vp, _vp]),
+    "smo_streamer_destroy": (C.c_int, [_vp]),
+    "smo_streamer_enqueue_layer": (C.c_int, [_vp, _i32, _vp]),
+    "smo_streamer_expert_ready_event": (C.c_int, [_vp, _i32, _vp]),
+    "smo_streamer_wait_layer": (C.c_int, [_vp, _i32, _vp]),
+    "smo_streamer_expert_ptr": (C.c_int, [_vp, _i32, _i32, _vp]),
+    "smo_streamer_release_layer": (C.c_int, [_vp, _i32, _vp]),
     "smo_engine_fill_prefix": (C.c_int, [_vp, _vp, _i32]),
     "smo_engine_verify": (C.c_int, [_vp, C.POINTER(VerifyBatch), C.POINTER(VerifyOutput), _vp]),
     "smo_engine_last_times": (C.c_int, [_vp, C.POINTER(StageTimes)]),

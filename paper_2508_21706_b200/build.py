@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libspecmoe.so")
-SOURCES = ["c_api.cu", "ops.cu", "gemm_tc.cu", "moe_tc.cu", "attention.cu", "engine.cu", "decode.cu", "prefill.cu",
+SOURCES = ["c_api.cu", "ops.cu", "gemm_tc.cu", "moe_tc.cu", "attention.cu", "engine.cu", "decode.cu", "prefill.cu", "streamer.cu",
            "ep.cu", "xfer.cu"]
 CXX_SOURCES = ["cpu_attn.cpp"]  # host code (CPU attention placement), g++ with AVX2/FMA
 CXX = os.environ.get("CXX", "g++")

@@ -444,6 +444,10 @@ struct smo_ep_group {
 
 namespace smo {
 smo_status run_guarded(const std::function<void()>& f);
+void permute(const int32_t* ids, int T, int k, int E, const void* x, int h, int32_t* offsets, int32_t* perm,
+             int32_t* pos, void* xp, cudaStream_t st);
+void unpermute_combine(const float* y, const int32_t* pos, const float* w, int T, int k, int h, float* res,
+                       cudaStream_t st, int splits = 1, size_t split_stride = 0);
 EpTransport* ep_transport(void* group) { return group ? reinterpret_cast<smo_ep_group*>(group)->t : nullptr; }
 }  // namespace smo
 
@@ -503,6 +507,84 @@ smo_status smo_ep_ipc_connect(smo_ep_group* g, const uint8_t* all_handles, smo_b
     auto* t = dynamic_cast<smo::IpcTransport*>(g->t);
     SMO_REQUIRE(t, "ep: not an IPC group");
     t->connect(all_handles, barrier, ctx);
+  });
+}
+
+// ---- standalone dispatch / combine (SURVEY.md §8(b) smo_ep_dispatch/combine)
+namespace {
+struct EpWs {  // workspace carve-up, identical for dispatch and combine
+  int32_t *oid, *offsets, *perm, *pos;
+  uint16_t* xp;
+  uint8_t *send, *recv;
+  float *sendback, *recvback;
+  size_t blk_d, bytes;
+};
+EpWs ep_ws(void* base, int P, int T, int k, int h, int E, int C) {
+  const int E_loc = E / P;
+  EpWs w{};
+  w.blk_d = (size_t(C) * h * 2 + size_t(E_loc) * 4 + 15) & ~size_t(15);
+  size_t off = 0;
+  auto take = [&](size_t n) {
+    const size_t at = off;
+    off = (off + n + 255) & ~size_t(255);
+    return reinterpret_cast<uint8_t*>(base) + at;
+  };
+  const size_t PT = size_t(T) * k;
+  w.oid = reinterpret_cast<int32_t*>(take(PT * 4));
+  w.offsets = reinterpret_cast<int32_t*>(take(size_t(E + 1) * 4));
+  w.perm = reinterpret_cast<int32_t*>(take(PT * 4));
+  w.pos = reinterpret_cast<int32_t*>(take(PT * 4));
+  w.xp = reinterpret_cast<uint16_t*>(take(PT * h * 2));
+  w.send = take(size_t(P) * w.blk_d);
+  w.recv = take(size_t(P) * w.blk_d);
+  w.sendback = reinterpret_cast<float*>(take(size_t(P) * C * h * 4));
+  w.recvback = reinterpret_cast<float*>(take(size_t(P) * C * h * 4));
+  w.bytes = off;
+  return w;
+}
+void ep_check(smo_ep_group* g, int rank, int T, int k, int h, int E, int C) {
+  SMO_REQUIRE(g && g->t, "ep: null group");
+  const int P = g->t->P;
+  SMO_REQUIRE(rank >= 0 && rank < P && T >= 0 && k >= 1 && h % 8 == 0 && E % P == 0 && C >= T * k,
+              "ep: bad arguments (E % P == 0, h % 8 == 0, capacity C >= T*k on every rank)");
+}
+}  // namespace
+
+size_t smo_ep_workspace(int32_t P, int32_t T, int32_t k, int32_t h, int32_t E, int32_t C) {
+  if (P < 1 || T < 0 || k < 1 || h < 8 || E < P || C < 1) return 0;
+  return ep_ws(nullptr, P, T, k, h, E, C).bytes;
+}
+
+smo_status smo_ep_dispatch(smo_ep_group* g, int32_t rank, const void* x, const int32_t* ids, int32_t T, int32_t k,
+                           int32_t h, int32_t E, int32_t C, void* xl, int32_t* offsets_l, int32_t* back,
+                           int32_t* pos_ep, void* workspace, smo_stream stream) {
+  return smo::run_guarded([&] {
+    ep_check(g, rank, T, k, h, E, C);
+    SMO_REQUIRE(x && ids && xl && offsets_l && back && pos_ep && workspace, "ep dispatch: null pointer");
+    const int P = g->t->P, E_loc = E / P, PT = T * k;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    EpWs w = ep_ws(workspace, P, T, k, h, E, C);
+    smo::ep_remap(ids, PT, P, E_loc, w.oid, st);
+    smo::permute(w.oid, T, k, E, x, h, w.offsets, w.perm, w.pos, w.xp, st);
+    smo::ep_pack(w.xp, w.offsets, P, E_loc, C, h, w.blk_d, w.send, st, nullptr);
+    smo::ep_pos(w.oid, w.pos, w.offsets, PT, E_loc, C, pos_ep, st);
+    g->t->alltoall(rank, w.send, w.recv, w.blk_d, st);
+    smo::ep_unpack(w.recv, P, E_loc, C, h, w.blk_d, xl, offsets_l, back, st);
+  });
+}
+
+smo_status smo_ep_combine(smo_ep_group* g, int32_t rank, const float* yl, const int32_t* back,
+                          const int32_t* offsets_l, const int32_t* pos_ep, const float* weights, int32_t T,
+                          int32_t k, int32_t h, int32_t E, int32_t C, float* x, void* workspace, smo_stream stream) {
+  return smo::run_guarded([&] {
+    ep_check(g, rank, T, k, h, E, C);
+    SMO_REQUIRE(yl && back && offsets_l && pos_ep && weights && x && workspace, "ep combine: null pointer");
+    const int P = g->t->P, E_loc = E / P;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    EpWs w = ep_ws(workspace, P, T, k, h, E, C);
+    smo::ep_pack_back(yl, back, offsets_l, E_loc, h, w.sendback, st, 1, 0, nullptr, 1);
+    g->t->alltoall(rank, w.sendback, w.recvback, size_t(C) * h * sizeof(float), st);
+    smo::unpermute_combine(w.recvback, pos_ep, weights, T, k, h, x, st);
   });
 }
 

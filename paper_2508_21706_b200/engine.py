@@ -71,14 +71,15 @@ class EpGroup:
     """Expert-parallel transport (smo_ep_group): NCCL across processes, or an
     in-process loopback group for P engines on one device."""
 
-    def __init__(self, handle):
+    def __init__(self, handle, size: int = 0):
         self.handle = handle
+        self.size = size
 
     @staticmethod
     def loopback(ep_size: int) -> "EpGroup":
         h = C.c_void_p()
         L.check(L.load().smo_ep_loopback_create(ep_size, C.byref(h)))
-        return EpGroup(h)
+        return EpGroup(h, ep_size)
 
     @staticmethod
     def nccl_unique_id() -> bytes:
@@ -91,9 +92,39 @@ class EpGroup:
         buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
         h = C.c_void_p()
         L.check(L.load().smo_ep_nccl_create(buf, nranks, rank, C.byref(h)))
-        return EpGroup(h)
+        return EpGroup(h, nranks)
 
     BARRIER_FN = C.CFUNCTYPE(None, C.c_void_p)
+
+    @staticmethod
+    def workspace_bytes(P: int, T: int, k: int, h: int, E: int, C: int) -> int:
+        return int(L.load().smo_ep_workspace(P, T, k, h, E, C))
+
+    def dispatch(self, rank: int, x, ids, n_expert: int, capacity: int, workspace, stream: int = 0):
+        """smo_ep_dispatch: x bf16 [T,h], ids int32 [T,k] (device tensors) ->
+        (xl bf16 [P*C,h], offsets_l int32 [E/P+1], back int32 [P*C],
+        pos_ep int32 [T*k]); collective over the group."""
+        import torch
+        T, h = x.shape
+        k = ids.shape[1]
+        P = self.size
+        xl = torch.empty((P * capacity, h), dtype=torch.bfloat16, device=x.device)
+        offsets_l = torch.empty(n_expert // P + 1, dtype=torch.int32, device=x.device)
+        back = torch.empty(P * capacity, dtype=torch.int32, device=x.device)
+        pos_ep = torch.empty(T * k, dtype=torch.int32, device=x.device)
+        L.check(L.load().smo_ep_dispatch(self.handle, rank, x.data_ptr(), ids.data_ptr(), T, k, h, n_expert, capacity,
+                                         xl.data_ptr(), offsets_l.data_ptr(), back.data_ptr(), pos_ep.data_ptr(),
+                                         workspace.data_ptr(), stream))
+        return xl, offsets_l, back, pos_ep
+
+    def combine(self, rank: int, yl, back, offsets_l, pos_ep, weights, x, n_expert: int, capacity: int, workspace,
+                stream: int = 0):
+        """smo_ep_combine: x fp32 [T,h] += sum_j weights[t,j] * expert output."""
+        T, h = x.shape
+        k = weights.numel() // T
+        L.check(L.load().smo_ep_combine(self.handle, rank, yl.data_ptr(), back.data_ptr(), offsets_l.data_ptr(),
+                                        pos_ep.data_ptr(), weights.data_ptr(), T, k, h, n_expert, capacity,
+                                        x.data_ptr(), workspace.data_ptr(), stream))
 
     @staticmethod
     def ipc(nranks: int, rank: int, slot_bytes: int, all_gather, barrier) -> "EpGroup":
@@ -108,7 +139,7 @@ class EpGroup:
         buf = (C.c_uint8 * len(allb)).from_buffer_copy(allb)
         cb = EpGroup.BARRIER_FN(lambda _ctx: barrier())
         L.check(lib.smo_ep_ipc_connect(h, buf, C.cast(cb, C.c_void_p), None))
-        g = EpGroup(h)
+        g = EpGroup(h, nranks)
         g._keep = cb  # the callback must outlive the group
         return g
 

@@ -281,3 +281,57 @@ def kv_rollback(k_caches, v_caches, prefix_len, acc_len, keep, b, n):
     L.check(L.load().smo_kv_rollback(_p(kp), _p(vp), len(k_caches), _p(prefix_len), _p(acc_len), _p(keep), b, n,
                                      n_kv, d, s_max, _p(kv_len), _stream()))
     return kv_len
+
+
+class ExpertStreamer:
+    """K5 expert streamer handle (smo_streamer_*): blocks in pinned host
+    memory -> double-buffered HBM slots on a copy-engine stream, hot-expert
+    cache, coded blocks expanded on the consumer stream.
+
+    host_blocks: list (layer-major, n_layers * n_experts) of pinned uint8 CPU
+    tensors — raw bf16 blocks of `block_bytes`, or K5 codes (then `codes`
+    gives 1 / 3 / 4 per block). The caller keeps them alive."""
+
+    def __init__(self, host_blocks, n_layers: int, n_experts: int, block_bytes: int, codes=None,
+                 hbm_slots: int = 2, cache_bytes: int = 0, device: int = 0):
+        n = n_layers * n_experts
+        assert len(host_blocks) == n
+        for t in host_blocks:
+            assert t.is_pinned(), "streamer: host blocks must be pinned"
+        self._ptrs = (C.c_void_p * n)(*[t.data_ptr() for t in host_blocks])
+        self._bytes = (C.c_uint64 * n)(*[t.numel() * t.element_size() for t in host_blocks])
+        self._codes = (C.c_int32 * n)(*(codes if codes is not None else [0] * n))
+        a = L.StreamerArgs(n_layers=n_layers, n_experts=n_experts, block_bytes=block_bytes,
+                           host_blocks=C.cast(self._ptrs, C.c_void_p), host_bytes=C.cast(self._bytes, C.c_void_p),
+                           host_codes=C.cast(self._codes, C.c_void_p), hbm_slots=hbm_slots,
+                           cache_bytes=cache_bytes, device=device)
+        self.handle = C.c_void_p()
+        L.check(L.load().smo_streamer_create(C.byref(a), C.byref(self.handle)))
+        self.n_experts, self.block_bytes = n_experts, block_bytes
+
+    def enqueue_layer(self, layer: int, active=None):
+        buf = None
+        if active is not None:
+            buf = (C.c_uint8 * self.n_experts)(*[1 if x else 0 for x in active])
+        L.check(L.load().smo_streamer_enqueue_layer(self.handle, layer, buf))
+
+    def wait_layer(self, layer: int, stream=None):
+        L.check(L.load().smo_streamer_wait_layer(self.handle, layer, stream if stream is not None else _stream()))
+
+    def release_layer(self, layer: int, stream=None):
+        L.check(L.load().smo_streamer_release_layer(self.handle, layer, stream if stream is not None else _stream()))
+
+    def expert_ptr(self, layer: int, expert: int) -> int:
+        p = C.c_void_p()
+        L.check(L.load().smo_streamer_expert_ptr(self.handle, layer, expert, C.byref(p)))
+        return p.value
+
+    def ready_event(self, layer: int) -> int:
+        ev = C.c_void_p()
+        L.check(L.load().smo_streamer_expert_ready_event(self.handle, layer, C.byref(ev)))
+        return ev.value
+
+    def close(self):
+        if getattr(self, "handle", None):
+            L.load().smo_streamer_destroy(self.handle)
+            self.handle = None

@@ -179,3 +179,67 @@ def test_ep_ipc_two_processes_bit_identical(cuda, staged):
         p.join(timeout=120)
     for rank, ok, err in sorted(res):
         assert ok, f"rank {rank}: {err}"
+
+
+def test_ep_dispatch_combine_standalone(cuda):
+    """smo_ep_dispatch / smo_ep_combine (the C-ABI pair SURVEY.md §8(b) names)
+    around a caller-run expert shard, P = 2 ranks on a loopback group (one host
+    thread each): every rank receives exactly the rows routed to its experts,
+    grouped by local expert, and the combined output equals the single-device
+    sum_j w[t,j] * f_{e(t,j)}(x[t]) for its own tokens."""
+    import torch
+    from paper_2508_21706_b200.engine import EpGroup
+    P, E, k, h, T = 2, 8, 2, 256, 12
+    C = T * k
+    g = torch.Generator(device="cuda").manual_seed(7)
+    xs = [(torch.randn((T, h), generator=g, device="cuda") * 0.5).to(torch.bfloat16) for _ in range(P)]
+    ids = [torch.stack([torch.randperm(E, generator=g, device="cuda")[:k] for _ in range(T)]).to(torch.int32)
+           for _ in range(P)]
+    ws_ = [torch.rand((T, k), generator=g, device="cuda") for _ in range(P)]
+    grp = EpGroup.loopback(P)
+    nbytes = EpGroup.workspace_bytes(P, T, k, h, E, C)
+    out, err = [None] * P, [None] * P
+
+    def scale(e):  # the "expert": y = x * (e + 1) / 2
+        return (e + 1) * 0.5
+
+    def rank_fn(r):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+                xl, off, back, pos_ep = grp.dispatch(r, xs[r], ids[r], E, C, ws, st.cuda_stream)
+                st.synchronize()
+                offs = off.cpu().numpy()
+                yl = torch.zeros((P * C, h), dtype=torch.float32, device="cuda")
+                got_rows = []
+                for le in range(E // P):
+                    rows = slice(int(offs[le]), int(offs[le + 1]))
+                    yl[rows] = xl[rows].float() * scale(le * P + r)
+                    got_rows.append(xl[rows].float())
+                x = torch.zeros((T, h), dtype=torch.float32, device="cuda")
+                grp.combine(r, yl, back, off, pos_ep, ws_[r].contiguous(), x, E, C, ws, st.cuda_stream)
+                st.synchronize()
+                out[r] = (x, got_rows)
+        except Exception as ex:  # reported below
+            err[r] = ex
+
+    th = [threading.Thread(target=rank_fn, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert all(e is None for e in err), err
+    for r in range(P):
+        x, got_rows = out[r]
+        want = torch.zeros((T, h), dtype=torch.float32, device="cuda")
+        for j in range(k):
+            f = torch.tensor([scale(int(e)) for e in ids[r][:, j].tolist()], device="cuda")
+            want += ws_[r][:, j:j + 1] * f[:, None] * xs[r].float()
+        assert torch.allclose(x, want, rtol=1e-5, atol=1e-6), (r, (x - want).abs().max())
+        # rank r received exactly the (token, slot) pairs routed to its experts
+        for le in range(E // P):
+            e = le * P + r
+            n_want = sum(int((ids[s] == e).sum()) for s in range(P))
+            assert got_rows[le].shape[0] == n_want, (r, le)
+    grp.close()
