@@ -406,7 +406,7 @@ __device__ __forceinline__ int select_msb(uint32_t x, int k) {
 // builds its 64 output bytes in registers from its 32 lo bytes.
 constexpr int kUDecWarps = 8;
 constexpr int kURun = 3;  // code words per lane per scan round
-__global__ void __launch_bounds__(32 * kUDecWarps) unary_decode_kernel(const __grid_constant__ DecodeJobs jobs,
+__global__ void __launch_bounds__(32 * kUDecWarps, 6) unary_decode_kernel(const __grid_constant__ DecodeJobs jobs,
                                                                        size_t segs) {
   __shared__ uint32_t wbuf[kUDecWarps][kUMaxWords + 8];
   __shared__ int start[kUDecWarps][33];
@@ -422,8 +422,6 @@ __global__ void __launch_bounds__(32 * kUDecWarps) unary_decode_kernel(const __g
     const int base = int(tw.y & 0xffu), nw = int(tw.y >> 16);
     const bool has_esc = (tw.y >> 8) & 1u;
     const uint32_t* codes = reinterpret_cast<const uint32_t*>(sb + kSeg);
-    const uint4 lo0 = reinterpret_cast<const uint4*>(sb)[2 * lane];  // this lane's 32 lo bytes
-    const uint4 lo1 = reinterpret_cast<const uint4*>(sb)[2 * lane + 1];
     // coalesced staging of the stream (words past the end read as ones)
     for (int w = lane; w < nw + 6; w += 32) wb[w] = w < nw ? codes[w] : 0xffffffffu;
     __syncwarp();
@@ -455,36 +453,42 @@ __global__ void __launch_bounds__(32 * kUDecWarps) unary_decode_kernel(const __g
     }
     __syncwarp();
     const int p0 = st[lane];
-    // the lane's codes sit in words k0 .. k0 + 4 when its run is short (the
-    // common case): walk them from registers, shifting a 5-word queue
-    const int k0 = p0 >> 5;
-    const bool fits = st[lane + 1] - 32 * k0 <= 160;
-    uint32_t e4[8];
-    if (__all_sync(0xffffffffu, fits)) {
-      uint32_t q0 = wb[k0], q1 = wb[k0 + 1], q2 = wb[k0 + 2], q3 = wb[k0 + 3], q4 = wb[k0 + 4];
-      int pos = p0 & 31;  // bit offset inside q0
+    // walk the lane's 32 codes: window from shared memory (MIO pipe), one
+    // count-leading-ones per code, code lengths packed per byte with IMAD
+    // (FMA pipe) — the integer ALU pipe is this kernel's limiter
+    uint32_t j4[8];
+    {
+      // two-word register window; a lane loads the next word only when its
+      // codes cross into it (~2 of 32 values), so shared-memory wavefronts
+      // stay few and bank conflicts rare
+      const uint32_t* wp = wb + (p0 >> 5);
+      uint32_t a = wp[0], b = wp[1];
+      wp += 2;
+      int off = p0 & 31;
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        const int j = __clz(~__funnelshift_l(q1, q0, pos));  // <= 15: every code fits the window
-        pos += j + 1;
-        const bool cross = pos >= 32;
-        q0 = cross ? q1 : q0;
-        q1 = cross ? q2 : q1;
-        q2 = cross ? q3 : q2;
-        q3 = cross ? q4 : q3;
-        q4 = cross ? 0xffffffffu : q4;
-        pos &= 31;
-        const uint32_t e = uint32_t(base - j) & 0xffu;
-        e4[i / 4] = (i % 4 == 0) ? e : (e4[i / 4] | (e << (8 * (i % 4))));
+        const int j = __clz(~__funnelshift_l(b, a, off));  // <= 15: every code fits the window
+        off += j + 1;
+        if (off >= 32) {
+          off -= 32;
+          a = b;
+          b = *wp++;
+        }
+        j4[i / 4] = (i % 4 == 0) ? uint32_t(j) : uint32_t(j) * (1u << (8 * (i % 4))) + j4[i / 4];
       }
-    } else {  // long runs (escapes, wide segments): window straight from shared memory
-      int pos = p0;
+    }
+    uint32_t e4[8];
+    if (base >= kUEsc) {  // base - j >= 0 in every byte: one subtraction per 4 values
+      const uint32_t b4 = uint32_t(base) * 0x01010101u;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int j = __clz(~__funnelshift_l(wb[(pos >> 5) + 1], wb[pos >> 5], pos & 31));
-        pos += j + 1;
-        const uint32_t e = uint32_t(base - j) & 0xffu;
-        e4[i / 4] = (i % 4 == 0) ? e : (e4[i / 4] | (e << (8 * (i % 4))));
+      for (int q = 0; q < 8; ++q) e4[q] = b4 - j4[q];
+    } else {  // tiny base (near-zero segments): bytewise
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) v |= (uint32_t(base - int((j4[q] >> (8 * t)) & 0xffu)) & 0xffu) << (8 * t);
+        e4[q] = v;
       }
     }
     if (has_esc) {  // rare: escaped exponents (j = 15), in position order
@@ -509,14 +513,17 @@ __global__ void __launch_bounds__(32 * kUDecWarps) unary_decode_kernel(const __g
       }
     }
     // 32 values -> 64 bytes: two values per word, lo bytes and exponents
-    // spread to 16-bit lanes with PRMT
+    // spread to 16-bit lanes with PRMT (lo loaded late: fewer live registers)
+    const uint4 lo0 = reinterpret_cast<const uint4*>(sb)[2 * lane];  // this lane's 32 lo bytes
+    const uint4 lo1 = reinterpret_cast<const uint4*>(sb)[2 * lane + 1];
     const uint32_t lw[8] = {lo0.x, lo0.y, lo0.z, lo0.w, lo1.x, lo1.y, lo1.z, lo1.w};
     uint32_t out[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
       const uint32_t sel = (k & 1) ? 0x4342u : 0x4140u;
       const uint32_t l16 = __byte_perm(lw[k / 2], 0u, sel), x16 = __byte_perm(e4[k / 2], 0u, sel);
-      out[k] = ((l16 & 0x00800080u) << 8) | (l16 & 0x007f007fu) | (x16 << 7);
+      // disjoint fields: sign * 2^8 + mantissa + exponent * 2^7, as IMADs
+      out[k] = (l16 & 0x00800080u) * 256u + (l16 & 0x007f007fu) + x16 * 128u;
     }
     uint4* d = reinterpret_cast<uint4*>(dst + seg * kSeg + 32 * lane);
 #pragma unroll
