@@ -142,9 +142,20 @@ def dist_init():
     if world > 1:
         import torch.distributed as dist
         import torch
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if SHARE_DEVICE:  # all ranks on cuda:0 (validates the N > 1 path on a 1-GPU box; NCCL refuses)
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     return world, rank, local
+
+
+# SMO_SHARE_DEVICE=1: every rank uses cuda:0 with gloo plumbing and the
+# peer-memory (IPC) transport — a functional check of the expert-parallel
+# bench path on one GPU, not a scaling measurement
+SHARE_DEVICE = os.environ.get("SMO_SHARE_DEVICE", "0") == "1"
 
 
 def barrier(world):
@@ -158,7 +169,7 @@ def max_over_ranks(world, v):
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device="cpu" if SHARE_DEVICE else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -399,7 +410,7 @@ def run_ours(args):
             if b % world or shape.n_expert % world:
                 raise ValueError(f"batch {b} / experts {shape.n_expert} not divisible by {world}")
             grp = None
-            if args.ep_transport == "nccl":
+            if args.ep_transport == "nccl" and not SHARE_DEVICE:
                 try:
                     uid = [EpGroup.nccl_unique_id() if rank == 0 else None]
                     dist.broadcast_object_list(uid, src=0)
