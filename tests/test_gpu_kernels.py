@@ -524,3 +524,33 @@ def test_expert_codec_lossless(cuda, oracle, kind, bits):
     sb = 1040 + 128 * bits + 32
     for sgm in (0, 7, 299):
         assert np.array_equal(_np_decode_segment(c[sgm * sb:(sgm + 1) * sb], bits), xs[sgm * 1024:(sgm + 1) * 1024])
+
+
+@pytest.mark.parametrize("kind", ["procedural", "normal", "wide"])
+def test_expert_codec_unary_matches_numpy_encoder(cuda, oracle, kind):
+    """The GPU unary encoder produces exactly the bytes of the numpy
+    restatement (tests/codec_ref.py: base choice, bit order, escapes, table,
+    padding), and the GPU decoder inverts the numpy encoder's bytes."""
+    import torch
+    import codec_ref
+    from paper_2508_21706_b200 import ops
+    n = 1024 * 40
+    if kind == "procedural":
+        xs = oracle.fill_uniform_bf16(n, 0x5EED, 99, math.sqrt(3.0 / 4096)).view(np.uint16)
+    elif kind == "normal":
+        rng = np.random.default_rng(5)
+        f = rng.normal(0, 0.02, n).astype(np.float32)
+        f[::997] = 0
+        f[::4099] *= 64
+        u = f.view(np.uint32)
+        xs = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    else:
+        xs = np.random.default_rng(6).integers(0, 1 << 16, n).astype(np.uint16)
+    x = torch.from_numpy(xs.view(np.int16).copy()).to(cuda).view(torch.bfloat16)
+    code, _ = ops.expert_encode(x, 1)
+    want = codec_ref.encode(xs)
+    got = code.cpu().numpy().tobytes()
+    assert len(got) == len(want)
+    assert got == want
+    back = ops.expert_decode(torch.frombuffer(bytearray(want), dtype=torch.uint8).to(cuda), n, 1)
+    assert np.array_equal(back.view(torch.int16).cpu().numpy().view(np.uint16), xs)
