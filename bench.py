@@ -57,8 +57,10 @@ def parse():
                     help="LARGE_BATCH (stream whole layers ahead) or BATCH_ONE (stream router-selected experts)")
     ap.add_argument("--no-compress", dest="compress", action="store_false",
                     help="stream raw bf16 experts instead of the lossless code (default: coded, expanded in HBM)")
-    ap.add_argument("--ep-transport", default="nccl", choices=["nccl", "ipc"],
-                    help="N>1 expert-parallel exchange: NCCL send/recv or CUDA-IPC peer mailboxes")
+    ap.add_argument("--ep-transport", default="ipc", choices=["ipc", "nccl"],
+                    help="N>1 expert-parallel exchange: CUDA-IPC peer mailboxes written by the dispatch / "
+                         "combine kernels themselves (default; falls back to NCCL if IPC cannot be set up) "
+                         "or NCCL grouped send/recv (the library baseline)")
     ap.add_argument("--attn-cpu", action="store_true",
                     help="AttentionPlacement::CPU: target K/V in pinned host DRAM, attention on the host pool")
     return ap.parse_args()
@@ -410,22 +412,31 @@ def run_ours(args):
             if b % world or shape.n_expert % world:
                 raise ValueError(f"batch {b} / experts {shape.n_expert} not divisible by {world}")
             grp = None
-            if args.ep_transport == "nccl" and not SHARE_DEVICE:
-                try:
-                    uid = [EpGroup.nccl_unique_id() if rank == 0 else None]
-                    dist.broadcast_object_list(uid, src=0)
-                    grp = EpGroup.nccl(uid[0], world, rank)
-                except Exception as ex:
-                    print(f"[bench] NCCL transport unavailable ({ex}); using the peer-memory transport",
-                          file=sys.stderr)
-            if grp is None:  # CUDA IPC mailboxes over NVLink, no NCCL
+
+            def make_nccl():
+                uid = [EpGroup.nccl_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(uid, src=0)
+                return EpGroup.nccl(uid[0], world, rank)
+
+            def make_ipc():  # peer mailboxes over NVLink, stored into by the EP kernels, no NCCL
                 def all_gather(blob):
                     out = [None] * world
                     dist.all_gather_object(out, blob, group=gloo)
                     return out
-                grp = EpGroup.ipc(world, rank, EpGroup.ipc_slot_bytes(shape, b // world, n), all_gather,
-                                  lambda: dist.barrier(group=gloo))
-                args.ep_transport = "ipc"
+                return EpGroup.ipc(world, rank, EpGroup.ipc_slot_bytes(shape, b // world, n), all_gather,
+                                   lambda: dist.barrier(group=gloo))
+
+            order = ["ipc"] if SHARE_DEVICE else ([args.ep_transport] + [t for t in ("ipc", "nccl")
+                                                                          if t != args.ep_transport])
+            for tname in order:
+                try:
+                    grp = make_ipc() if tname == "ipc" else make_nccl()
+                    args.ep_transport = tname
+                    break
+                except Exception as ex:
+                    print(f"[bench] {tname} transport unavailable ({ex})", file=sys.stderr)
+            if grp is None:
+                raise RuntimeError("no expert-parallel transport")
             ep_rank, ep_size, mode = rank, world, f"ep{world} ({args.ep_transport})"
             b = b // world
         except Exception as ex:  # reported in the line; replicas keep the run measurable
