@@ -425,34 +425,71 @@ __global__ void __launch_bounds__(32 * kUDecWarps, 6) unary_decode_kernel(const 
     // coalesced staging of the stream (words past the end read as ones)
     for (int w = lane; w < nw + 6; w += 32) wb[w] = w < nw ? codes[w] : 0xffffffffu;
     __syncwarp();
-    int cum = 0;
-    for (int c0 = 0; c0 < nw; c0 += 32 * kURun) {
-      const int w0 = c0 + kURun * lane;
+    int p0 = 0;
+    if (nw <= 32 * kURun) {
+      // common case, one run of <= 3 words per lane: zero counts per run,
+      // a warp scan, then each lane binary-searches the run holding zero
+      // 32 L - 1 (shared-memory prefix table) and selects inside its word —
+      // no divergent loops
+      const int w0 = kURun * lane;
       uint32_t z[kURun];
-      int cnt[kURun], n = 0;
+      int n = 0;
 #pragma unroll
       for (int r = 0; r < kURun; ++r) {
         z[r] = w0 + r < nw ? ~wb[w0 + r] : 0u;  // zeros = value ends
-        cnt[r] = __popc(z[r]);
-        n += cnt[r];
+        n += __popc(z[r]);
       }
       int tot = 0;
-      int before = cum + warp_excl_scan(n, lane, &tot);
-      cum += tot;
-      // lanes L whose first value follows zero 32 L - 1 when it lies in this run
+      const int before = warp_excl_scan(n, lane, &tot);
+      st[lane] = before + n;  // zeros up to the end of run `lane`
+      __syncwarp();
+      if (lane > 0) {
+        const int t = 32 * lane - 1;
+        int w = 0;  // first run whose inclusive count exceeds t
 #pragma unroll
-      for (int r = 0; r < kURun; ++r) {
-        for (int L = (before + 32) / 32; L < 32 && 32 * L - 1 < before + cnt[r]; ++L)
-          st[L] = (w0 + r) * 32 + select_msb(z[r], 32 * L - 1 - before) + 1;
-        before += cnt[r];
+        for (int step = 16; step; step >>= 1)
+          if (st[w + step - 1] <= t) w += step;
+        int k = t - (w ? st[w - 1] : 0);
+        int r = 0;
+        uint32_t zw = ~wb[kURun * w];
+#pragma unroll
+        for (int q = 1; q < kURun; ++q) {
+          const int c = __popc(zw);
+          if (k >= c) {
+            k -= c;
+            r = q;
+            zw = kURun * w + q < nw ? ~wb[kURun * w + q] : 0u;
+          }
+        }
+        p0 = (kURun * w + r) * 32 + select_msb(zw, k) + 1;
       }
+    } else {  // long streams (escapes, wide segments): runs over several rounds
+      int cum = 0;
+      for (int c0 = 0; c0 < nw; c0 += 32 * kURun) {
+        const int w0 = c0 + kURun * lane;
+        uint32_t z[kURun];
+        int cnt[kURun], n = 0;
+#pragma unroll
+        for (int r = 0; r < kURun; ++r) {
+          z[r] = w0 + r < nw ? ~wb[w0 + r] : 0u;
+          cnt[r] = __popc(z[r]);
+          n += cnt[r];
+        }
+        int tot = 0;
+        int before = cum + warp_excl_scan(n, lane, &tot);
+        cum += tot;
+        // lanes L whose first value follows zero 32 L - 1 when it lies in this run
+#pragma unroll
+        for (int r = 0; r < kURun; ++r) {
+          for (int L = (before + 32) / 32; L < 32 && 32 * L - 1 < before + cnt[r]; ++L)
+            st[L] = (w0 + r) * 32 + select_msb(z[r], 32 * L - 1 - before) + 1;
+          before += cnt[r];
+        }
+      }
+      if (lane == 0) st[0] = 0;
+      __syncwarp();
+      p0 = st[lane];
     }
-    if (lane == 0) {
-      st[0] = 0;
-      st[32] = 32 * nw;
-    }
-    __syncwarp();
-    const int p0 = st[lane];
     // walk the lane's 32 codes: window from shared memory (MIO pipe), one
     // count-leading-ones per code, code lengths packed per byte with IMAD
     // (FMA pipe) — the integer ALU pipe is this kernel's limiter
