@@ -502,29 +502,33 @@ __global__ void __launch_bounds__(32 * kUDecWarps, 6) unary_decode_kernel(const 
       uint32_t a = wp[0], b = wp[1];
       wp += 2;
       int off = p0 & 31;
+      // f = index of the window's highest zero = 31 - j (16 <= f <= 31):
+      // the code is f-complement long, so off advances by 32 - f
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        const int j = __clz(~__funnelshift_l(b, a, off));  // <= 15: every code fits the window
-        off += j + 1;
+        const int f = 31 - __clz(~__funnelshift_l(b, a, off));  // FLO: every code fits the window
+        off += 32 - f;
         if (off >= 32) {
           off -= 32;
           a = b;
           b = *wp++;
         }
-        j4[i / 4] = (i % 4 == 0) ? uint32_t(j) : uint32_t(j) * (1u << (8 * (i % 4))) + j4[i / 4];
+        j4[i / 4] = (i % 4 == 0) ? uint32_t(f) : uint32_t(f) * (1u << (8 * (i % 4))) + j4[i / 4];
       }
     }
+    // e = base - j = f - (31 - base)
     uint32_t e4[8];
-    if (base >= kUEsc) {  // base - j >= 0 in every byte: one subtraction per 4 values
-      const uint32_t b4 = uint32_t(base) * 0x01010101u;
+    if (base >= kUEsc) {  // f >= 16 >= 31 - base in every byte: one subtraction per 4 values
+      const uint32_t d4 = uint32_t(31 - base) * 0x01010101u;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) e4[q] = b4 - j4[q];
+      for (int q = 0; q < 8; ++q) e4[q] = j4[q] - d4;
     } else {  // tiny base (near-zero segments): bytewise
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         uint32_t v = 0;
 #pragma unroll
-        for (int t = 0; t < 4; ++t) v |= (uint32_t(base - int((j4[q] >> (8 * t)) & 0xffu)) & 0xffu) << (8 * t);
+        for (int t = 0; t < 4; ++t)
+          v |= (uint32_t(int((j4[q] >> (8 * t)) & 0xffu) - 31 + base) & 0xffu) << (8 * t);
         e4[q] = v;
       }
     }
