@@ -19,7 +19,22 @@ namespace smo {
 
 smo_status run_guarded(const std::function<void()>& f);
 
+// makes the streamer's device current for the duration of a call, then
+// restores the caller's (the C-ABI must not change the thread's device)
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    SMO_CUDA_CHECK(cudaGetDevice(&prev));
+    if (prev != dev) SMO_CUDA_CHECK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 struct Streamer {
+  int device = 0;
   int L = 0, E = 0, slots = 2;
   size_t blk = 0;                    // bf16 bytes of one block
   std::vector<const uint8_t*> host;  // [L*E]
@@ -60,9 +75,10 @@ smo_status smo_streamer_create(const smo_streamer_args* a, smo_streamer** out) {
     SMO_REQUIRE(a && out && a->n_layers > 0 && a->n_experts > 0 && a->block_bytes > 0 && a->host_blocks,
                 "streamer: bad arguments");
     SMO_REQUIRE(a->hbm_slots >= 2 && a->block_bytes % 2048 == 0, "streamer: >= 2 slots, block of 1024-value segments");
-    SMO_CUDA_CHECK(cudaSetDevice(a->device));
+    smo::DeviceGuard dg(a->device);
     auto* h = new smo_streamer();
     smo::Streamer& s = h->s;
+    s.device = a->device;
     try {
       s.L = a->n_layers;
       s.E = a->n_experts;
@@ -119,13 +135,18 @@ smo_status smo_streamer_create(const smo_streamer_args* a, smo_streamer** out) {
 }
 
 smo_status smo_streamer_destroy(smo_streamer* h) {
-  return smo::run_guarded([&] { delete h; });
+  return smo::run_guarded([&] {
+    if (!h) return;
+    smo::DeviceGuard dg(h->s.device);
+    delete h;
+  });
 }
 
 smo_status smo_streamer_enqueue_layer(smo_streamer* h, int32_t layer, const uint8_t* active) {
   return smo::run_guarded([&] {
     SMO_REQUIRE(h && layer >= 0 && layer < h->s.L, "streamer: bad layer");
     smo::Streamer& s = h->s;
+    smo::DeviceGuard dg(s.device);
     const int k = s.slot_of(layer);
     // the slot's previous layer must have been released by its consumer
     SMO_CUDA_CHECK(cudaStreamWaitEvent(s.copy, s.freed[size_t(k)], 0));
@@ -159,6 +180,7 @@ smo_status smo_streamer_wait_layer(smo_streamer* h, int32_t layer, smo_stream st
   return smo::run_guarded([&] {
     SMO_REQUIRE(h && layer >= 0 && layer < h->s.L, "streamer: bad layer");
     smo::Streamer& s = h->s;
+    smo::DeviceGuard dg(s.device);
     const int k = s.slot_of(layer);
     SMO_REQUIRE(s.slot_layer[size_t(k)] == layer, "streamer: layer not enqueued");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -196,6 +218,7 @@ smo_status smo_streamer_expert_ptr(smo_streamer* h, int32_t layer, int32_t exper
 smo_status smo_streamer_release_layer(smo_streamer* h, int32_t layer, smo_stream stream) {
   return smo::run_guarded([&] {
     SMO_REQUIRE(h && layer >= 0 && layer < h->s.L, "streamer: bad layer");
+    smo::DeviceGuard dg(h->s.device);
     SMO_CUDA_CHECK(cudaEventRecord(h->s.freed[size_t(h->s.slot_of(layer))], reinterpret_cast<cudaStream_t>(stream)));
   });
 }
