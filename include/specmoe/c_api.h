@@ -316,7 +316,8 @@ typedef struct {
   int32_t hbm_slots;          /* expert-layer staging slots, >= 2 */
   int64_t expert_cache_bytes; /* hot-expert HBM cache (MemoryPolicy.expert_cache_bytes) */
   int32_t host_alias_layers;  /* 0: one pinned expert buffer per layer; A: layer l uses l % A */
-  int32_t device;
+  int32_t device;             /* smo_engine_create makes it current on the calling thread; drive the
+                                 engine from one host thread with that device current */
   int32_t flags;
   int32_t ep_rank, ep_size;   /* expert parallelism: this rank owns experts e % ep_size == ep_rank */
   void* nccl_comm;            /* smo_ep_group* (NCCL or loopback) when ep_size > 1 */
