@@ -562,7 +562,7 @@ def run_ours(args):
     # (profiles/r01h_launches.md): algorithmic bytes = code read + bf16 written
     codec_roof = None
     if args.compress and stages.get("codec", 0) > 0:
-        cb = stages["h2d_bytes"] + stages["h2d_raw_bytes"]
+        cb = stages.get("codec_bytes") or (stages["h2d_bytes"] + stages["h2d_raw_bytes"])
         codec_roof = {"bound": "hbm", "kernel": "K5 expert_decode (coded blocks -> bf16 HBM slot), per step",
                       "achieved": cb / stages["codec"] / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
                       "frac": cb / stages["codec"] / 1e9 / pk["hbm_gbs"], "traffic": codec_traffic_per_block(),

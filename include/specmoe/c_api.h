@@ -428,6 +428,7 @@ typedef struct {
   double draft;        /* drafter time of the last decode step (DRAFT_GPU_STEP total) */
   double h2d_raw_bytes; /* bf16 bytes the streamed blocks carry (= h2d_bytes unless coded) */
   double codec;        /* device time expanding coded expert blocks (compress_experts) */
+  double codec_bytes;  /* their algorithmic bytes: code read + bf16 written (streamed + coded hot cache) */
 } smo_stage_times;
 smo_status smo_engine_last_times(smo_engine* e, smo_stage_times* t);
 /* Measured per-layer timeline of the last verify, 9 doubles per layer (s from

@@ -55,7 +55,7 @@ void Engine::bt_sync(cudaStream_t st) {
 // on the compute stream after slot_ready(l)
 void Engine::decode_slot(int l, cudaStream_t st) {
   const int s = l % slots;
-  if (coded_streamed[size_t(l)].empty()) return;
+  if (coded_streamed[size_t(l)].empty() && coded_cached[size_t(l)].empty()) return;
   SMO_CUDA_CHECK(cudaEventRecord(dec_ev[size_t(2 * l)], st));
   for (int bits : {1, 3, 4}) {  // one launch per code (blocks of a layer share it in practice)
     const void* src[64];
@@ -69,6 +69,18 @@ void Engine::decode_slot(int l, cudaStream_t st) {
       }
       src[n] = cstage + (size_t(s) * E_loc + le) * cblk_bytes;
       dst[n] = pool + (size_t(s) * E_loc + le) * blk_elems;
+      step_codec_bytes += double(blk_csize[size_t(host_layer(l)) * E_loc + size_t(le)] + blk_bytes);
+      ++n;
+    }
+    for (int le : coded_cached[size_t(l)]) {  // hot-cached in their code: source already in HBM
+      if (code_bits(l, le) != bits) continue;
+      if (n == 64) {
+        expert_decode_blocks(src, dst, n, blk_elems, bits, st);
+        n = 0;
+      }
+      src[n] = ccache + ccache_off[size_t(l) * E + size_t(owned[size_t(le)])];
+      dst[n] = pool + (size_t(s) * E_loc + le) * blk_elems;
+      step_codec_bytes += double(blk_csize[size_t(host_layer(l)) * E_loc + size_t(le)] + blk_bytes);
       ++n;
     }
     expert_decode_blocks(src, dst, n, blk_elems, bits, st);
@@ -271,16 +283,52 @@ void Engine::create() {
     }
   }
 
-  // HBM pool: slots x E staging blocks + hot-expert cache
-  const int64_t cache_blocks = opt.expert_cache_bytes > 0 ? int64_t(opt.expert_cache_bytes / int64_t(blk_bytes)) : 0;
+  // HBM pool: slots x E staging blocks + hot-expert cache. With the coded
+  // transfer the cache keeps blocks in their link code (~1.56x more experts
+  // per cache byte) and expands them into the layer's slot each step, like
+  // a streamed block whose bytes are already in HBM (SMO_CODED_CACHE=0: bf16).
   cache_blk.assign(size_t(L) * E, -1);
   int placed = 0;
-  for (int l = 0; l < L && placed < cache_blocks; ++l)
-    for (int e : owned) {
-      if (placed >= cache_blocks) break;
-      cache_blk[size_t(l) * E + e] = slots * E_loc + placed;
-      ++placed;
+  {
+    const char* f = std::getenv("SMO_CODED_CACHE");
+    const bool coded_cache = xcomp && !(f && f[0] == '0');
+    int64_t budget = std::max<int64_t>(opt.expert_cache_bytes, 0);
+    size_t cc_bytes = 0;
+    std::vector<std::pair<size_t, size_t>> cc_src;  // (l*E+e, offset)
+    bool full = false;
+    for (int l = 0; l < L && !full; ++l)
+      for (int e : owned) {
+        const size_t i = size_t(host_layer(l)) * E_loc + size_t(local(e));
+        const bool coded = coded_cache && code_bits(l, local(e)) != 0;
+        const int64_t cost = coded ? int64_t((blk_csize[i] + 255) & ~size_t(255)) : int64_t(blk_bytes);
+        if (cost > budget) {
+          full = true;
+          break;
+        }
+        budget -= cost;
+        if (coded) {
+          cache_blk[size_t(l) * E + e] = kCachedCoded;
+          cc_src.push_back({size_t(l) * E + e, cc_bytes});
+          cc_bytes += size_t(cost);
+        } else {
+          cache_blk[size_t(l) * E + e] = slots * E_loc + placed;
+          ++placed;
+        }
+      }
+    coded_cached.assign(size_t(L), {});
+    ccache_off.assign(size_t(L) * E, 0);
+    if (cc_bytes) {
+      ccache = dalloc<uint8_t>(cc_bytes);
+      for (auto [le_idx, off] : cc_src) {
+        const int l = int(le_idx / E), e = int(le_idx % E);
+        const size_t i = size_t(host_layer(l)) * E_loc + size_t(local(e));
+        SMO_CUDA_CHECK(cudaMemcpy(ccache + off, host_bufs[host_layer(l)] + size_t(local(e)) * blk_elems, blk_csize[i],
+                                  cudaMemcpyHostToDevice));
+        ccache_off[le_idx] = off;
+        coded_cached[size_t(l)].push_back(local(e));
+      }
     }
+  }
   pool_blocks = slots * E_loc + placed;
   pool = dalloc<uint16_t>(size_t(pool_blocks) * blk_elems);
   coded_streamed.assign(size_t(L), {});
@@ -288,7 +336,7 @@ void Engine::create() {
   for (int l = 0; l < L; ++l)
     for (int e : owned) {
       const int cb = cache_blk[size_t(l) * E + e];
-      if (cb < 0) continue;
+      if (cb < 0) continue;  // streamed, or cached in its code (expanded per step)
       const uint16_t* hsrc = host_bufs[host_layer(l)] + size_t(local(e)) * blk_elems;
       if (const int bits = code_bits(l, local(e))) {
         SMO_CUDA_CHECK(cudaMemcpy(cenc, hsrc, blk_csize[size_t(host_layer(l)) * E_loc + size_t(local(e))],
@@ -500,7 +548,7 @@ double Engine::enqueue_h2d(int l, cudaEvent_t t0, cudaEvent_t t1, const uint8_t*
   double bytes = 0;
   const uint16_t* hb = host_bufs[host_layer(l)];
   auto streamed = [&](int le) {
-    return cache_blk[size_t(l) * E + owned[size_t(le)]] < 0 && (!active || active[le]);
+    return cache_blk[size_t(l) * E + owned[size_t(le)]] == -1 && (!active || active[le]);
   };
   coded_streamed[size_t(l)].clear();
   if (xcomp) {
@@ -702,6 +750,7 @@ void Engine::begin_step(cudaStream_t st, bool prefetch) {
   step_h2d_bytes = 0;
   step_h2d_ev.clear();
   step_dec_ev.clear();
+  step_codec_bytes = 0;
   std::fill(layer_bytes.begin(), layer_bytes.end(), 0.0);
   std::fill(layer_raw_bytes.begin(), layer_raw_bytes.end(), 0.0);
   for (int l = 0; prefetch && l < std::min(slots, L); ++l) {
@@ -1009,6 +1058,7 @@ void Engine::times(smo_stage_times* t) {
   r.h2d_transfer = span(pending_h2d);
   r.h2d_bytes = last_h2d_bytes;
   r.codec = span(step_dec_ev);
+  r.codec_bytes = step_codec_bytes;
   for (double v : layer_raw_bytes) r.h2d_raw_bytes += v;
   r.others = std::max(0.0, r.target_total - r.attention - r.gpu_moe);
   *t = r;

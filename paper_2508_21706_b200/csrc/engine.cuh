@@ -169,7 +169,12 @@ struct Engine {
   // expert pool in HBM
   uint16_t* pool = nullptr;
   int slots = 2, pool_blocks = 0;
-  std::vector<int> cache_blk;  // [L*E] pool block of a cached expert, -1 otherwise
+  std::vector<int> cache_blk;  // [L*E] pool block of a cached expert, kCachedCoded, -1 = streamed
+  double step_codec_bytes = 0;                  // code read + bf16 written by this step's expansions
+  static constexpr int kCachedCoded = -2;       // cached in its link code in `ccache`, expanded per step
+  uint8_t* ccache = nullptr;                    // coded hot cache
+  std::vector<size_t> ccache_off;               // [L*E] byte offset in ccache
+  std::vector<std::vector<int>> coded_cached;   // per layer: local experts cached coded
   int32_t* d_w_index = nullptr;  // [L*E]
   std::vector<cudaEvent_t> slot_ready, slot_free;
   // EP: experts owned by this rank
