@@ -144,6 +144,8 @@ void Engine::create() {
     SMO_REQUIRE(!(opt.ep_size > 1 || opt.nccl_comm), "engine: BATCH_ONE streaming is not available with expert parallelism");
     batch_one = true;
     SMO_CUDA_CHECK(cudaEventCreateWithFlags(&route_ev, cudaEventDisableTiming));
+    const char* f = std::getenv("SMO_B1_PREFETCH");
+    b1_prefetch = !(f && f[0] == '0');
   }
   if (opt.attn_cpu) {
     SMO_REQUIRE(!paged, "engine: the CPU attention placement keeps contiguous host K/V (kv_pages = 0)");
@@ -551,32 +553,34 @@ double Engine::enqueue_h2d(int l, cudaEvent_t t0, cudaEvent_t t1, const uint8_t*
     return cache_blk[size_t(l) * E + owned[size_t(le)]] == -1 && (!active || active[le]);
   };
   coded_streamed[size_t(l)].clear();
-  if (xcomp) {
+  // BATCH_ONE link-gap prefetch of this layer: only the remainders are left
+  const bool spec = spec_layer == l;
+  auto staged = [&](int q) { return spec ? spec_done[size_t(q)] : size_t(0); };
+  if (xcomp || spec) {
     // coded blocks into cstage (expanded by decode_slot), raw ones straight into the slot
     for (int q = 0; q < E_loc; ++q) {
-      if (!streamed(q)) continue;
-      if (const int bits = code_bits(l, q)) {
-        (void)bits;
-        const size_t cb = blk_csize[size_t(host_layer(l)) * E_loc + size_t(q)];
-        SMO_CUDA_CHECK(cudaMemcpyAsync(cstage + (size_t(s) * E_loc + q) * cblk_bytes, hb + size_t(q) * blk_elems,
-                                       cb, cudaMemcpyHostToDevice, copy));
-        bytes += double(cb);
-        coded_streamed[size_t(l)].push_back(q);
-      } else {
-        SMO_CUDA_CHECK(cudaMemcpyAsync(pool + (size_t(s) * E_loc + q) * blk_elems, hb + size_t(q) * blk_elems,
-                                       blk_bytes, cudaMemcpyHostToDevice, copy));
-        bytes += double(blk_bytes);
-      }
+      if (!streamed(q) || (!xcomp && staged(q) == 0)) continue;
+      const bool coded = code_bits(l, q) != 0;
+      const size_t full = coded ? blk_csize[size_t(host_layer(l)) * E_loc + size_t(q)] : blk_bytes;
+      const size_t done = staged(q);
+      uint8_t* dstp = coded ? cstage + (size_t(s) * E_loc + q) * cblk_bytes
+                            : reinterpret_cast<uint8_t*>(pool + (size_t(s) * E_loc + q) * blk_elems);
+      if (full > done)
+        SMO_CUDA_CHECK(cudaMemcpyAsync(dstp + done, reinterpret_cast<const uint8_t*>(hb + size_t(q) * blk_elems) + done,
+                                       full - done, cudaMemcpyHostToDevice, copy));
+      bytes += double(full - done);
+      if (coded) coded_streamed[size_t(l)].push_back(q);
     }
   }
+  spec_layer = spec ? -1 : spec_layer;
   int le = xcomp ? E_loc : 0;
   while (le < E_loc) {
-    if (!streamed(le)) {
+    if (!streamed(le) || staged(le) > 0) {  // (partly prefetched raw blocks were completed above)
       ++le;
       continue;
     }
     int le2 = le;
-    while (le2 + 1 < E_loc && streamed(le2 + 1)) ++le2;
+    while (le2 + 1 < E_loc && streamed(le2 + 1) && staged(le2 + 1) == 0) ++le2;
     const size_t nbytes = size_t(le2 - le + 1) * blk_bytes;
     SMO_CUDA_CHECK(cudaMemcpyAsync(pool + (size_t(s) * E_loc + le) * blk_elems, hb + size_t(le) * blk_elems, nbytes,
                                    cudaMemcpyHostToDevice, copy));
@@ -743,7 +747,70 @@ void Engine::verify(const smo_verify_batch& in, smo_verify_output& out, cudaStre
   }
 }
 
+// BATCH_ONE: from the previous step's per-layer copy events, the link idle
+// time between layer l's copies and layer l+1's becomes the prefetch budget
+// after layer l (90 % of the gap). A prefetch longer than the true gap
+// delays layer l+1's copies, so the measured gap is then the prefetch
+// itself and the budget shrinks; a shorter one leaves the true gap visible.
+void Engine::b1_update_budget() {
+  b1_budget.assign(size_t(L), 0.0);
+  if (!b1_prefetch || !b1_measured) return;
+  b1_measured = false;
+  // the previous step's last copies: this step's copies queue behind them on
+  // the same stream anyway, and BATCH_ONE synchronises the host per layer
+  if (cudaEventSynchronize(tev((L - 1) * 8 + 1)) != cudaSuccess) return;
+  double busy = 0, bytes = 0;
+  for (int l = 0; l < L; ++l) {
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, tev(l * 8 + 0), tev(l * 8 + 1)) != cudaSuccess) return;
+    busy += ms * 1e-3;
+    bytes += layer_bytes[size_t(l)];
+  }
+  if (busy <= 0 || bytes <= 0) return;
+  const double bw = bytes / busy;
+  for (int l = 0; l + 1 < L; ++l) {
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, tev(l * 8 + 1), tev((l + 1) * 8 + 0)) != cudaSuccess) continue;
+    b1_budget[size_t(l)] = std::max(0.0, 0.9 * ms * 1e-3 * bw);
+  }
+}
+
+// After layer l's copies (BATCH_ONE): stage prefixes of layer l+1's blocks,
+// the experts most routed at layer l first, up to the budget.
+double Engine::b1_prefetch_step(int l, cudaStream_t copy_st) {
+  spec_layer = -1;
+  if (!b1_prefetch || l + 1 >= L || b1_budget.empty() || b1_budget[size_t(l)] <= 0) return 0;
+  const int ln = l + 1, s = ln % slots;
+  std::vector<int> order;
+  for (int q = 0; q < E_loc; ++q)
+    if (cache_blk[size_t(ln) * E + owned[size_t(q)]] == -1) order.push_back(q);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    const int ea = owned[size_t(a)], eb = owned[size_t(b)];
+    return h_offsets[ea + 1] - h_offsets[ea] > h_offsets[eb + 1] - h_offsets[eb];
+  });
+  SMO_CUDA_CHECK(cudaStreamWaitEvent(copy_st, slot_free[s], 0));
+  spec_done.assign(size_t(E_loc), 0);
+  double left = b1_budget[size_t(l)], bytes = 0;
+  const uint8_t* hb = reinterpret_cast<const uint8_t*>(host_bufs[host_layer(ln)]);
+  for (int q : order) {
+    if (left < 4096) break;
+    const bool coded = code_bits(ln, q) != 0;
+    const size_t full = coded ? blk_csize[size_t(host_layer(ln)) * E_loc + size_t(q)] : blk_bytes;
+    const size_t nb = std::min(full, size_t(left) & ~size_t(4095));
+    uint8_t* dstp = coded ? cstage + (size_t(s) * E_loc + q) * cblk_bytes
+                          : reinterpret_cast<uint8_t*>(pool + (size_t(s) * E_loc + q) * blk_elems);
+    SMO_CUDA_CHECK(cudaMemcpyAsync(dstp, hb + size_t(q) * blk_bytes, nb, cudaMemcpyHostToDevice, copy_st));
+    spec_done[size_t(q)] = nb;
+    left -= double(nb);
+    bytes += double(nb);
+  }
+  spec_layer = ln;
+  return bytes;
+}
+
 void Engine::begin_step(cudaStream_t st, bool prefetch) {
+  if (!prefetch && batch_one) b1_update_budget();
+  spec_layer = -1;
   SMO_CUDA_CHECK(cudaEventRecord(ev[0], st));
   // order the copy stream after the step start (so H2D timing is step-relative)
   SMO_CUDA_CHECK(cudaStreamWaitEvent(copy, ev[0], 0));
@@ -881,6 +948,8 @@ void Engine::verify_core(int b, int n, const int32_t* tokens, const int32_t* par
       for (int e = 0; e < E; ++e) act[size_t(local(e))] = h_offsets[e + 1] > h_offsets[e] ? 1 : 0;
       h2d_bytes += enqueue_h2d(l, tev(l * 8 + 0), tev(l * 8 + 1), act.data());
       h2d_ev.push_back({tev(l * 8 + 0), tev(l * 8 + 1)});
+      const double pf = b1_prefetch_step(l, copy);  // fills the link while layer l+1 is routed
+      h2d_bytes += pf;  // counted in the step's link bytes (wasted when the expert goes unrouted)
     }
     if (cfg.shared_inter > 0) {
       // always-on shared expert (config 4): x += SwiGLU_shared(xn2); its
@@ -1015,6 +1084,7 @@ void Engine::verify_core(int b, int n, const int32_t* tokens, const int32_t* par
   pending_moe = moe_ev;
   pending_h2d = h2d_ev;
   last_h2d_bytes = h2d_bytes;
+  b1_measured = batch_one;
 }
 
 // Per layer: [h2d_start, h2d_end, attn_start, attn_end, moe_start, moe_end,

@@ -150,6 +150,17 @@ struct Engine {
   bool batch_one = false;
   int32_t* h_offsets = nullptr;           // pinned [E+1] routed offsets of the current layer
   cudaEvent_t route_ev = nullptr;
+  // BATCH_ONE link-gap prefetch: while layer l+1's routing is computed the
+  // link would idle; it carries (prefixes of) the experts most routed at
+  // layer l into layer l+1's staging instead, sized from the previous step's
+  // measured gap (SMO_B1_PREFETCH=0 disables)
+  bool b1_prefetch = true;
+  bool b1_measured = false;                // the last step left a gap timeline
+  std::vector<double> b1_budget;          // [L] bytes to prefetch after layer l's copies
+  std::vector<size_t> spec_done;          // [E_loc] bytes of layer spec_layer already staged
+  int spec_layer = -1;
+  double b1_prefetch_step(int l, cudaStream_t copy_st);
+  void b1_update_budget();
   std::vector<double> layer_bytes;        // bytes streamed per layer in the last step
   std::vector<double> layer_raw_bytes;    // their bf16 size (coded blocks expand)
   // lossless expert codec on the link (xfer.cu): coded blocks cross into

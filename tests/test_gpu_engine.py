@@ -245,6 +245,40 @@ def test_batch_one_streams_only_routed_experts(cuda):
     assert 0 < b1 <= s.n_layers * 4 * s.expert_bytes
 
 
+@pytest.mark.parametrize("compress", [False, True])
+def test_batch_one_link_gap_prefetch_bit_identical(cuda, compress, monkeypatch):
+    """BATCH_ONE link-gap prefetch: from the second step on, the engine stages
+    prefixes of layer l+1's likely experts while layer l+1 is routed
+    (budget = the previous step's measured link gap). Results stay
+    bit-identical to LARGE_BATCH and to BATCH_ONE without prefetch, step after
+    step (raw and coded blocks; partly staged blocks are completed)."""
+    from paper_2508_21706_b200.engine import VerifyEngine
+    s = _shape()
+    b, n = 2, 3
+    prefix = np.array([300, 77], np.int32)
+    rng = np.random.default_rng(21)
+    toks = [rng.integers(0, s.vocab, size=(b, n)).astype(np.int32) for _ in range(4)]
+    res = {}
+    for mode in ("large", "one_nopf", "one_pf"):
+        monkeypatch.setenv("SMO_B1_PREFETCH", "0" if mode == "one_nopf" else "1")
+        eng = VerifyEngine(s, max_batch=b, max_verify=n, max_seq=512, batch_one=mode != "large",
+                           compress_experts=compress)
+        eng.fill_prefix(prefix)
+        out = []
+        for t in toks:
+            r = eng.verify(t, prefix)
+            out.append((r, eng.last_times()["h2d_bytes"]))
+        res[mode] = out
+        eng.close()
+    for i in range(len(toks)):
+        for mode in ("one_nopf", "one_pf"):
+            a, c = res["large"][i][0], res[mode][i][0]
+            assert np.array_equal(a.target, c.target), (mode, i)
+            assert np.array_equal(a.acc_len, c.acc_len) and np.array_equal(a.bonus, c.bonus)
+    # the first step has no measured gap yet: identical bytes without / with prefetch
+    assert res["one_pf"][0][1] == res["one_nopf"][0][1]
+
+
 @pytest.mark.parametrize("batch_one,codec", [(False, "unary"), (True, "unary"), (False, "fixed")])
 def test_compressed_expert_stream_bit_identical(cuda, batch_one, codec, monkeypatch):
     """compress_experts: experts cross the link in a lossless code and are
