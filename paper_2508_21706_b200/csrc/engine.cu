@@ -781,6 +781,12 @@ double Engine::b1_prefetch_step(int l, cudaStream_t copy_st) {
   spec_layer = -1;
   if (!b1_prefetch || l + 1 >= L || b1_budget.empty() || b1_budget[size_t(l)] <= 0) return 0;
   const int ln = l + 1, s = ln % slots;
+  // a guessed expert is routed at layer l+1 with probability ~ the fraction
+  // of experts layer l routed to; below one half the wasted prefixes cost
+  // more than the gap buys (measured: DeepSeek-V2-Lite shape at b = 1)
+  int used = 0;
+  for (int q = 0; q < E_loc; ++q) used += h_offsets[owned[size_t(q)] + 1] > h_offsets[owned[size_t(q)]] ? 1 : 0;
+  if (2 * used < E_loc) return 0;
   std::vector<int> order;
   for (int q = 0; q < E_loc; ++q)
     if (cache_blk[size_t(ln) * E + owned[size_t(q)]] == -1) order.push_back(q);
