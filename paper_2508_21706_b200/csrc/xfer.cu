@@ -408,7 +408,7 @@ constexpr int kUDecWarps = 8;
 constexpr int kURun = 3;  // code words per lane per scan round
 __global__ void __launch_bounds__(32 * kUDecWarps, 6) unary_decode_kernel(const __grid_constant__ DecodeJobs jobs,
                                                                        size_t segs) {
-  __shared__ uint32_t wbuf[kUDecWarps][kUMaxWords + 8];
+  __shared__ __align__(16) uint32_t wbuf[kUDecWarps][kUMaxWords + 8];
   __shared__ int start[kUDecWarps][33];
   const uint8_t* __restrict__ src = jobs.src[blockIdx.y];
   uint16_t* __restrict__ dst = jobs.dst[blockIdx.y];
@@ -566,9 +566,21 @@ __global__ void __launch_bounds__(32 * kUDecWarps, 6) unary_decode_kernel(const 
       // disjoint fields: sign * 2^8 + mantissa + exponent * 2^7, as IMADs
       out[k] = (l16 & 0x00800080u) * 256u + (l16 & 0x007f007fu) + x16 * 128u;
     }
-    uint4* d = reinterpret_cast<uint4*>(dst + seg * kSeg + 32 * lane);
+    // through shared memory (the stream buffer is free now) so every global
+    // store instruction writes 512 contiguous bytes
+    __syncwarp();
+    uint4* ob = reinterpret_cast<uint4*>(wb);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) d[k] = make_uint4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
+    for (int k = 0; k < 4; ++k)
+      ob[4 * lane + ((k + lane) & 3)] = make_uint4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
+    __syncwarp();
+    uint4* d = reinterpret_cast<uint4*>(dst + seg * kSeg);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int g = 32 * k + lane;  // 16-byte group g = lane' 4 + k' of lane' = g / 4
+      const int ln = g >> 2, kk = g & 3;
+      d[g] = ob[4 * ln + ((kk + ln) & 3)];
+    }
     __syncwarp();  // wb / st are reused by the next segment
   }
 }
