@@ -43,6 +43,7 @@ struct EngineOptions {
   float router_scale = 1.0f;
   bool drafter = true;                 // build the drafter from ModelSpec.draft (f1) when it has FFN ops
   int kv_pages = 0;                    // K/V layout (f2): 0 contiguous, > 0 paged pool size, -1 paged auto
+  bool compress_experts = true;        // experts cross the host link in the lossless K5 code (xfer.cu)
 };
 
 struct VerifyBatch {
@@ -114,6 +115,7 @@ class VerifyEngine {
     o.ep_rank = 0;
     o.ep_size = 1;
     o.kv_pages = opt.kv_pages;
+    o.compress_experts = opt.compress_experts ? 1 : 0;
     // AttentionPlacement::CPU (the reference's default, config.hpp:110): target
     // K/V in pinned host DRAM, attention on the host pool (f4); GPU_TRANSFER
     // and GPU_RESIDENT run K1 on HBM-resident K/V
