@@ -406,7 +406,7 @@ __device__ __forceinline__ int select_msb(uint32_t x, int k) {
 // builds its 64 output bytes in registers from its 32 lo bytes.
 constexpr int kUDecWarps = 2;
 constexpr int kURun = 3;  // code words per lane per scan round
-__global__ void __launch_bounds__(32 * kUDecWarps, 24) unary_decode_kernel(const __grid_constant__ DecodeJobs jobs,
+__global__ void __launch_bounds__(32 * kUDecWarps, 28) unary_decode_kernel(const __grid_constant__ DecodeJobs jobs,
                                                                        size_t segs) {
   __shared__ __align__(16) uint32_t wbuf[kUDecWarps][kUMaxWords + 8];
   __shared__ int start[kUDecWarps][33];
