@@ -319,7 +319,7 @@ def codec_traffic_per_block(kernel="K5_expert_decode_unary"):
     """dram__bytes_read+write of one expert_decode launch (one Mixtral expert
     block) from the committed ncu capture (profiles/r01h_traffic.json: the
     unary decoder the engine uses; r01f_traffic.json: the 3-bit one)."""
-    for f in ("r01j_traffic.json", "r01i_traffic.json", "r01h_traffic.json", "r01f_traffic.json"):
+    for f in ("r01k_traffic.json", "r01j_traffic.json", "r01i_traffic.json", "r01h_traffic.json", "r01f_traffic.json"):
         try:
             k = json.load(open(os.path.join(ROOT, "profiles", f)))["kernels"][kernel]
             return k["dram_read_bytes"] + k["dram_write_bytes"]
@@ -567,10 +567,10 @@ def run_ours(args):
                       "achieved": cb / stages["codec"] / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
                       "frac": cb / stages["codec"] / 1e9 / pk["hbm_gbs"], "traffic": codec_traffic_per_block(),
                       "traffic_unit": "dram bytes per expert block (one layer's decode launch / its blocks, ncu "
-                      "profiles/r01j_traffic.json); algorithmic per block = "
+                      "profiles/r01k_traffic.json); algorithmic per block = "
                       + str(int(cb / max(1.0, stages["h2d_raw_bytes"]) * shape.expert_bytes)),
-                      "bound_note": "the unary decoder is instruction-issue / latency bound (issue active 75 %, "
-                      "ncu profiles/r01j_launches.md); HBM is not its limiter",
+                      "bound_note": "the unary decoder is instruction-issue / latency bound (issue active 88 %, "
+                      "ncu profiles/r01k_launches.md); HBM is not its limiter",
                       "peak_kind": pk_kind}
     line = {
         "metric": "verified decode tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world,
