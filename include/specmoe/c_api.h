@@ -44,6 +44,14 @@ int smo_device_sm_count(int device);
  * dst[i] = bf16(fl(float(2*u24 - 2^24) * fl(scale*2^-24))),
  * u24 = splitmix64(splitmix64(seed ^ tensor_id*0x9e3779b97f4a7c15 ^ (base+i)))>>40
  * — the reference RNG family (specdec.hpp:34-39).                           */
+/* Trained-weight-like procedural init with the same variance as the uniform
+ * one (std = scale / sqrt(3)): c = sum of the 4 chained splitmix64 draws
+ * u_k = x_k >> 40 of the same stream minus 2^25 (Irwin-Hall, near-gaussian),
+ * times 8 for one value in 1024 (outliers: x_4 & 1023 == 0), out[i] =
+ * bf16(fl(float(c) * fl(scale * 2^-24))) — integer-exact on CPU and GPU
+ * (oracle: orc_fill_normal_bf16).                                           */
+smo_status smo_fill_normal_bf16(void* dst, uint64_t count, uint64_t seed, uint64_t tensor_id, uint64_t base,
+                                float scale, smo_stream stream);
 smo_status smo_fill_uniform_bf16(void* dst, uint64_t count, uint64_t seed, uint64_t tensor_id,
                                  uint64_t base, float scale, smo_stream stream);
 
@@ -305,7 +313,10 @@ typedef struct {
                            Dense decoder layers with the target's attention shape, sharing
                            its embedding and LM head (EAGLE convention), resident in HBM */
   int32_t draft_inter;  /* drafter SwiGLU width: DraftModelSpec.ffn_ops_per_token = 6*h*draft_inter */
+  int32_t expert_init;  /* routed-expert weight distribution: SMO_INIT_UNIFORM (default) or
+                           SMO_INIT_GAUSSIAN (trained-like, smo_fill_normal_bf16); same variance */
 } smo_model_config;
+enum { SMO_INIT_UNIFORM = 0, SMO_INIT_GAUSSIAN = 1 };
 
 enum { SMO_ENGINE_DEBUG = 1 /* keep per-layer intermediates for parity tests */ };
 

@@ -198,6 +198,26 @@ void orc_fill_uniform_bf16(uint16_t* out, size_t count, uint64_t seed,
   }
 }
 
+/* trained-weight-like init (c_api.h smo_fill_normal_bf16 / ops.cu
+ * fill_normal_kernel): Irwin-Hall of 4 chained draws, 1/1024 outliers x8 */
+void orc_fill_normal_bf16(uint16_t* out, size_t count, uint64_t seed,
+                          uint64_t tensor_id, uint64_t base, float scale) {
+  const float s = ldexpf(scale, -24);
+  const uint64_t key = seed ^ (tensor_id * PHI);
+#pragma omp parallel for schedule(static)
+  for (long long i = 0; i < (long long)count; ++i) {
+    uint64_t x = orc_splitmix64(orc_splitmix64(key ^ (base + (uint64_t)i)));
+    int32_t c = (int32_t)(x >> 40);
+    for (int k = 1; k < 4; ++k) {
+      x = orc_splitmix64(x);
+      c += (int32_t)(x >> 40);
+    }
+    c -= 1 << 25;
+    if ((x & 1023u) == 0) c *= 8;
+    out[i] = orc_f32_to_bf16((float)c * s);
+  }
+}
+
 /* ------------------------------------------------------------------------- */
 void orc_rmsnorm(const float* x, const uint16_t* gain, int T, int h, float eps,
                  uint16_t* y) {

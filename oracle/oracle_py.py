@@ -55,6 +55,8 @@ def lib():
         L.orc_random_cases.argtypes = [C.c_uint64, C.c_uint64] + [C.c_void_p] * 5 + [C.POINTER(_sz)] * 3
         L.orc_fill_uniform_bf16.restype = None
         L.orc_fill_uniform_bf16.argtypes = [C.c_void_p, _sz, C.c_uint64, C.c_uint64, C.c_uint64, C.c_float]
+        L.orc_fill_normal_bf16.restype = None
+        L.orc_fill_normal_bf16.argtypes = [C.c_void_p, _sz, C.c_uint64, C.c_uint64, C.c_uint64, C.c_float]
         L.orc_rmsnorm.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_float, C.c_void_p]
         L.orc_gemm_xwt.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
         L.orc_router_logits.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
@@ -181,4 +183,10 @@ def f32_to_bf16(a):
 def fill_uniform_bf16(count, seed, tensor_id, scale, base=0):
     out = np.empty(count, np.uint16)
     lib().orc_fill_uniform_bf16(_ptr(out), count, seed, tensor_id, base, scale)
+    return out
+
+
+def fill_normal_bf16(count, seed, tensor_id, scale, base=0):
+    out = np.empty(count, np.uint16)
+    lib().orc_fill_normal_bf16(_ptr(out), count, seed, tensor_id, base, scale)
     return out

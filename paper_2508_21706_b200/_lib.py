@@ -13,6 +13,7 @@ LIB_PATH = os.environ.get("SPECMOE_LIB", os.path.join(HERE, "libspecmoe.so"))
 
 SMO_OK, SMO_INVALID_ARG, SMO_CAPACITY, SMO_CUDA, SMO_NCCL, SMO_UNSUPPORTED = range(6)
 EPI_BF16, EPI_F32, EPI_F32_ADD, EPI_SWIGLU, EPI_ARGMAX = range(5)
+INIT_UNIFORM, INIT_GAUSSIAN = 0, 1  # smo_model_config.expert_init
 ENGINE_DEBUG = 1
 
 _vp = C.c_void_p
@@ -52,7 +53,8 @@ class ModelConfig(C.Structure):
     _fields_ = [("hidden", _i32), ("inter", _i32), ("n_expert", _i32), ("top_k", _i32), ("n_layers", _i32),
                 ("n_q_heads", _i32), ("n_kv_heads", _i32), ("head_dim", _i32), ("vocab", _i32),
                 ("rope_theta", _f32), ("rms_eps", _f32), ("seed", _u64), ("lm_scale", _f32),
-                ("router_scale", _f32), ("shared_inter", _i32), ("draft_layers", _i32), ("draft_inter", _i32)]
+                ("router_scale", _f32), ("shared_inter", _i32), ("draft_layers", _i32), ("draft_inter", _i32),
+                ("expert_init", _i32)]
 
 
 class EngineOptions(C.Structure):
@@ -91,6 +93,7 @@ _SIGS = {
     "smo_launch_count": (_u64, []),
     "smo_device_sm_count": (C.c_int, [C.c_int]),
     "smo_fill_uniform_bf16": (C.c_int, [_vp, _u64, _u64, _u64, _u64, _f32, _vp]),
+    "smo_fill_normal_bf16": (C.c_int, [_vp, _u64, _u64, _u64, _u64, _f32, _vp]),
     "smo_verify_attention_workspace": (_sz, [C.POINTER(AttnArgs)]),
     "smo_verify_attention": (C.c_int, [C.POINTER(AttnArgs), _vp]),
     "smo_cpu_verify_attention": (C.c_int, [C.POINTER(AttnArgs), _i32]),

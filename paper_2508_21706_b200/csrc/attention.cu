@@ -744,7 +744,8 @@ AttnPlan plan_attention(const smo_attn_args& a, int sms) {
   }();
   if (cost(qa) < cost(qmin)) q = qa;
   pl.Q = std::max(q, (pl.C + 14) / 15);
-  if (const char* fq = std::getenv("SMO_ATTN_Q")) pl.Q = std::max(std::atoi(fq), (pl.C + 14) / 15);  // A/B runs
+  // A/B override: never below qmin (grid <= sms: the workspace holds 2 partial slots per SM)
+  if (const char* fq = std::getenv("SMO_ATTN_Q")) pl.Q = std::max(std::max(std::atoi(fq), qmin), (pl.C + 14) / 15);
   pl.grid = (pl.total + pl.Q - 1) / pl.Q;
   // the layout is sized for the largest tile (128 rows) so that the counter
   // region sits at the same offset for every n: a workspace shared by calls

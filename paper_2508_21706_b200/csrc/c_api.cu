@@ -23,6 +23,8 @@ void gemm_launch(const smo_gemm_args& a, cudaStream_t s);
 size_t gemm_workspace(const smo_gemm_args& a);
 void fill_uniform(void* dst, uint64_t count, uint64_t seed, uint64_t tensor_id, uint64_t base, float scale,
                   cudaStream_t st);
+void fill_normal(void* dst, uint64_t count, uint64_t seed, uint64_t tensor_id, uint64_t base, float scale,
+                 cudaStream_t st);
 void fill_kv_prefix(void* cache, const int32_t* prefix, int b, int n_kv, int d, int s_max, uint64_t seed,
                     uint64_t tensor_id, cudaStream_t st, const int32_t* bt = nullptr, int max_pages = 0);
 void router_topk(const void* x, const void* w, int T, int h, int E, int k, float* logits, int32_t* ids,
@@ -124,6 +126,11 @@ int smo_device_sm_count(int device) {
   int v = 0;
   if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
   return v;
+}
+
+smo_status smo_fill_normal_bf16(void* dst, uint64_t count, uint64_t seed, uint64_t tensor_id, uint64_t base,
+                                float scale, smo_stream stream) {
+  return guard([&] { smo::fill_normal(dst, count, seed, tensor_id, base, scale, S(stream)); });
 }
 
 smo_status smo_fill_uniform_bf16(void* dst, uint64_t count, uint64_t seed, uint64_t tensor_id, uint64_t base,

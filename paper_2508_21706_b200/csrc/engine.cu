@@ -103,6 +103,7 @@ void Engine::create() {
   SMO_REQUIRE(nq > 0 && nkv > 0 && nq % nkv == 0 && (d == 64 || d == 128), "engine: bad attention shape");
   SMO_REQUIRE(h % 256 == 0 && hi % 128 == 0 && V % 128 == 0 && (nq * d) % 128 == 0, "engine: unsupported dims");
   SMO_REQUIRE(cfg.shared_inter >= 0 && cfg.shared_inter % 128 == 0, "engine: shared_inter must be a multiple of 128");
+  SMO_REQUIRE(cfg.expert_init == SMO_INIT_UNIFORM || cfg.expert_init == SMO_INIT_GAUSSIAN, "engine: bad expert_init");
   SMO_REQUIRE(opt.max_batch > 0 && opt.max_verify > 0 && opt.max_verify <= 64, "engine: bad batch options");
   // expert parallelism whenever a transport is given (ep_size 1 with a
   // 1-rank group runs the full dispatch/combine path: a 1-GPU check of it)
@@ -249,9 +250,10 @@ void Engine::create() {
     host_bufs[a] = reinterpret_cast<uint16_t*>(hp);
     for (int e : owned) {
       const uint64_t base = tid::layer(a) + tid::kExpert + 3ull * e;
-      fill_uniform(stage, size_t(hi) * h, cfg.seed, base + 0, 0, std::sqrt(3.0f / h), st);
-      fill_uniform(stage + size_t(hi) * h, size_t(hi) * h, cfg.seed, base + 1, 0, std::sqrt(3.0f / h), st);
-      fill_uniform(stage + 2 * size_t(hi) * h, size_t(h) * hi, cfg.seed, base + 2, 0, std::sqrt(3.0f / hi), st);
+      auto fill = cfg.expert_init == SMO_INIT_GAUSSIAN ? fill_normal : fill_uniform;
+      fill(stage, size_t(hi) * h, cfg.seed, base + 0, 0, std::sqrt(3.0f / h), st);
+      fill(stage + size_t(hi) * h, size_t(hi) * h, cfg.seed, base + 1, 0, std::sqrt(3.0f / h), st);
+      fill(stage + 2 * size_t(hi) * h, size_t(h) * hi, cfg.seed, base + 2, 0, std::sqrt(3.0f / hi), st);
       uint16_t* hdst = host_bufs[a] + size_t(local(e)) * blk_elems;
       bool coded = false;
       // the smallest code that holds the block: unary (variable length) when

@@ -26,6 +26,8 @@ void gemm_launch(const smo_gemm_args& a, cudaStream_t s);
 size_t gemm_workspace(const smo_gemm_args& a);
 void fill_uniform(void* dst, uint64_t count, uint64_t seed, uint64_t tensor_id, uint64_t base, float scale,
                   cudaStream_t st);
+void fill_normal(void* dst, uint64_t count, uint64_t seed, uint64_t tensor_id, uint64_t base, float scale,
+                 cudaStream_t st);
 void fill_kv_prefix(void* cache, const int32_t* prefix, int b, int n_kv, int d, int s_max, uint64_t seed,
                     uint64_t tensor_id, cudaStream_t st, const int32_t* bt = nullptr, int max_pages = 0);
 void router_topk(const void* x, const void* w, int T, int h, int E, int k, float* logits, int32_t* ids,

@@ -25,6 +25,24 @@ __global__ void fill_uniform_kernel(uint16_t* dst, uint64_t count, uint64_t key,
   }
 }
 
+// trained-weight-like init (c_api.h smo_fill_normal_bf16): Irwin-Hall of the
+// four chained draws of the same splitmix64 stream, 1/1024 outliers x8
+__global__ void fill_normal_kernel(uint16_t* dst, uint64_t count, uint64_t key, uint64_t base, float s) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    uint64_t x = splitmix64(splitmix64(key ^ (base + i)));
+    int32_t c = int32_t(x >> 40);
+#pragma unroll
+    for (int k = 1; k < 4; ++k) {
+      x = splitmix64(x);
+      c += int32_t(x >> 40);
+    }
+    c -= 1 << 25;
+    if ((x & 1023u) == 0) c *= 8;
+    dst[i] = f2bf(__fmul_rn(__int2float_rn(c), s));
+  }
+}
+
 __global__ void fill_kv_prefix_kernel(uint16_t* cache, const int32_t* prefix, int n_kv, int d, int s_max,
                                       uint64_t key, float s, const int32_t* bt, int max_pages) {
   const int rh = blockIdx.y;  // r * n_kv + h
@@ -488,6 +506,17 @@ void fill_uniform(void* dst, uint64_t count, uint64_t seed, uint64_t tensor_id, 
   const float s = std::ldexp(scale, -24);
   fill_uniform_kernel<<<grid_for(count, 256), 256, 0, st>>>(reinterpret_cast<uint16_t*>(dst), count,
                                                             seed ^ (tensor_id * 0x9e3779b97f4a7c15ULL), base, s);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+void fill_normal(void* dst, uint64_t count, uint64_t seed, uint64_t tensor_id, uint64_t base, float scale,
+                 cudaStream_t st) {
+  if (!count) return;
+  SMO_REQUIRE(dst, "fill: null pointer");
+  const float s = std::ldexp(scale, -24);
+  fill_normal_kernel<<<grid_for(count, 256), 256, 0, st>>>(reinterpret_cast<uint16_t*>(dst), count,
+                                                           seed ^ (tensor_id * 0x9e3779b97f4a7c15ULL), base, s);
   count_launch();
   SMO_CUDA_CHECK(cudaGetLastError());
 }

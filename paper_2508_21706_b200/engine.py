@@ -38,6 +38,7 @@ class ModelShape:
     shared_inter: int = 0  # always-on shared expert (config 4), resident in HBM
     draft_layers: int = 0  # drafter depth (DraftModelSpec.n_layers); 0: no drafter
     draft_inter: int = 0   # drafter dense SwiGLU width
+    expert_init: int = 0   # 0: uniform (default), 1: gaussian-like trained weights (L.INIT_GAUSSIAN)
 
     @property
     def expert_bytes(self) -> int:
@@ -47,7 +48,7 @@ class ModelShape:
         return L.ModelConfig(self.hidden, self.inter, self.n_expert, self.top_k, self.n_layers, self.n_q_heads,
                              self.n_kv_heads, self.head_dim, self.vocab, self.rope_theta, self.rms_eps, self.seed,
                              self.lm_scale, self.router_scale, self.shared_inter, self.draft_layers,
-                             self.draft_inter)
+                             self.draft_inter, self.expert_init)
 
 
 # BASELINE.json configs
@@ -307,11 +308,16 @@ def geometric_alpha(p: float, k: int) -> float:
 
 
 def step_roofline(shape: ModelShape, b: int, n: int, prefix: int, h2d_gbs: float, hbm_gbs: float,
-                  tflops: float, cached_blocks: int = 0, ep: int = 1, h2d_bytes: Optional[float] = None) -> dict:
+                  tflops: float, cached_blocks: int = 0, ep: int = 1, h2d_bytes: Optional[float] = None,
+                  extra_hbm_bytes: float = 0.0) -> dict:
     """Binding roofline of one verify step: the slower of
     host-link bytes, HBM bytes and tensor peak (roofline.hpp:108-151), per
     GPU. `b` is the global batch; with expert parallelism over `ep` GPUs each
-    streams and reads E/ep experts per layer and attends b/ep requests."""
+    streams and reads E/ep experts per layer and attends b/ep requests.
+    h2d_bytes=None: the algorithmic H2D bytes of SURVEY.md §8(d) (bf16
+    expert blocks, roofline.hpp:61-62); else the bytes actually streamed.
+    extra_hbm_bytes: HBM traffic beyond the algorithmic bytes that the
+    implementation chose to spend (the link codec's code read + bf16 write)."""
     s = shape
     T = b * n
     e_bytes = s.expert_bytes
@@ -321,7 +327,7 @@ def step_roofline(shape: ModelShape, b: int, n: int, prefix: int, h2d_gbs: float
         h2d = h2d_bytes
     kv = 2 * (b / ep) * (prefix + n) * s.n_kv_heads * s.head_dim * 2
     dense = (s.hidden * (s.n_q_heads + 2 * s.n_kv_heads) * s.head_dim + s.n_q_heads * s.head_dim * s.hidden) * 2
-    hbm = s.n_layers * (activated / ep * e_bytes + kv + dense) + s.vocab * s.hidden * 2
+    hbm = s.n_layers * (activated / ep * e_bytes + kv + dense) + s.vocab * s.hidden * 2 + extra_hbm_bytes
     flops = (s.n_layers * (2 * 3 * s.hidden * s.inter * T * s.top_k / ep + 2 * (T / ep) * dense / 2
                            + 4 * (b / ep) * n * (prefix + n) * s.n_q_heads * s.head_dim)
              + 2 * (T / ep) * s.hidden * s.vocab)

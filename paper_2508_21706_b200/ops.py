@@ -40,6 +40,14 @@ def fill_uniform_(t: torch.Tensor, seed: int, tensor_id: int, scale: float, base
     return t
 
 
+def fill_normal_(t: torch.Tensor, seed: int, tensor_id: int, scale: float, base: int = 0) -> torch.Tensor:
+    """Trained-weight-like procedural init (c_api.h smo_fill_normal_bf16),
+    identical to the oracle's orc_fill_normal_bf16."""
+    _req(t, _BF16, "fill_normal_")
+    L.check(L.load().smo_fill_normal_bf16(_p(t), t.numel(), seed, tensor_id, base, scale, _stream()))
+    return t
+
+
 def verify_attention(q, k_cache, v_cache, mask, prefix_len, max_prefix: int, out=None, block_table=None):
     """K1. q [b*n, n_q, d] bf16; caches [b, n_kv, s_max, d] bf16 — or, with
     block_table int32 [b, max_pages], page pools [num_pages, n_kv, 128, d];

@@ -75,9 +75,12 @@ class OracleModel:
         a = l % self.alias
         base = tid_layer(a) + 100 + 3 * e
         h, hi = s.hidden, s.inter
-        w1 = self._fill(hi * h, base, math.sqrt(3.0 / h)).reshape(hi, h)
-        w3 = self._fill(hi * h, base + 1, math.sqrt(3.0 / h)).reshape(hi, h)
-        w2 = self._fill(h * hi, base + 2, math.sqrt(3.0 / hi)).reshape(h, hi)
+        fill = self._fill
+        if getattr(s, "expert_init", 0) == 1:  # gaussian-like trained weights (orc_fill_normal_bf16)
+            fill = lambda count, tid, scale: O.fill_normal_bf16(count, self.s.seed, tid, scale)  # noqa: E731
+        w1 = fill(hi * h, base, math.sqrt(3.0 / h)).reshape(hi, h)
+        w3 = fill(hi * h, base + 1, math.sqrt(3.0 / h)).reshape(hi, h)
+        w2 = fill(h * hi, base + 2, math.sqrt(3.0 / hi)).reshape(h, hi)
         return w1, w3, w2
 
     def kv_prefix(self, l, which, prefix, s_max):
