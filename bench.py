@@ -69,6 +69,9 @@ def parse():
                          "link code's compression ratio")
     ap.add_argument("--no-raw", dest="raw", action="store_false",
                     help="skip the second timed loop with raw bf16 streaming (raw_value)")
+    ap.add_argument("--micro-batches", type=int, default=1,
+                    help="Hyperparameters.m: the batch as m micro-batches, stage-major per layer "
+                         "(pipeline.hpp:147-206); with --attn-cpu the host attends one while the GPU runs the next")
     ap.add_argument("--attn-cpu", action="store_true",
                     help="AttentionPlacement::CPU: target K/V in pinned host DRAM, attention on the host pool")
     return ap.parse_args()
@@ -439,7 +442,8 @@ def raw_pass(shape, args, b, n, prefix, s_max, local, h2d_peak, pk, alias=8):
     from paper_2508_21706_b200.engine import VerifyEngine, step_roofline
     eng = VerifyEngine(shape, max_batch=b, max_verify=n, max_seq=s_max, hbm_slots=args.slots,
                        expert_cache_bytes=int(args.cache_gb * 1e9), host_alias_layers=alias, device=local,
-                       attn_cpu=args.attn_cpu, batch_one=args.moe_batching == "one", compress_experts=False)
+                       attn_cpu=args.attn_cpu, batch_one=args.moe_batching == "one", compress_experts=False,
+                       micro_batches=args.micro_batches)
     dev = torch.device(f"cuda:{local}")
     pre = np.full(b, prefix, np.int32)
     eng.fill_prefix(pre)
@@ -540,7 +544,8 @@ def run_ours(args):
             eng = VerifyEngine(shape, max_batch=b, max_verify=n, max_seq=s_max, hbm_slots=args.slots,
                                expert_cache_bytes=int(args.cache_gb * 1e9), host_alias_layers=a, device=local,
                                ep_rank=ep_rank, ep_size=ep_size, ep_group=grp, attn_cpu=args.attn_cpu,
-                               batch_one=args.moe_batching == "one", compress_experts=args.compress)
+                               batch_one=args.moe_batching == "one", compress_experts=args.compress,
+                               micro_batches=args.micro_batches)
             alias = a
             break
         except _lib.CapacityError as e:
@@ -681,6 +686,7 @@ def run_ours(args):
                    "draft_len": args.k, "verify_rows": b * n, "prefix": prefix, "experts_in": "pinned host DRAM",
                    "expert_cache_gb": args.cache_gb, "hbm_slots": args.slots, "host_alias_layers": alias,
                    "attention_placement": "CPU (host K/V, host thread pool)" if args.attn_cpu else "GPU_RESIDENT (K1)",
+                   "micro_batches": args.micro_batches,
                    "moe_batching": "BATCH_ONE (router-selected experts)" if args.moe_batching == "one"
                    else "LARGE_BATCH (whole layers)",
                    "expert_transfer": f"lossless exponent-coded blocks (xfer.cu, "

@@ -33,7 +33,7 @@
 namespace moeplan {
 
 struct EngineOptions {
-  std::int64_t max_seq = 0;            // KV capacity per request (0: workload total_len + k + 1)
+  std::int64_t max_seq = 0;            // KV capacity per request (0: 2048)
   int hbm_slots = 2;                   // expert staging slots
   int host_alias_layers = 0;           // pinned host buffers shared by layers (0: one per layer)
   int device = 0;
@@ -44,6 +44,12 @@ struct EngineOptions {
   bool drafter = true;                 // build the drafter from ModelSpec.draft (f1) when it has FFN ops
   int kv_pages = 0;                    // K/V layout (f2): 0 contiguous, > 0 paged pool size, -1 paged auto
   bool compress_experts = true;        // experts cross the host link in the lossless K5 code (xfer.cu)
+  // expert parallelism: this rank owns experts e % ep_size ==
+  // ep_rank and streams only those; ep_group = an smo_ep_group (NCCL, CUDA-IPC
+  // peer mailboxes or loopback) of ep_size ranks, owned by the caller
+  int ep_rank = 0;
+  int ep_size = 1;
+  smo_ep_group* ep_group = nullptr;
 };
 
 struct VerifyBatch {
@@ -75,6 +81,10 @@ class VerifyEngine {
   VerifyEngine(const HardwareSpec& hw, const ModelSpec& model, const Hyperparameters& hyper, const MemoryPlan& plan,
                const EngineOptions& opt = {})
       : hw_(hw), model_(model), hyper_(hyper) {
+    if (hyper.exec_strategy.attention_placement == AttentionPlacement::GPU_TRANSFER)
+      throw std::invalid_argument(
+          "VerifyEngine: AttentionPlacement::GPU_TRANSFER (target K/V streamed over the host link every step, "
+          "roofline.hpp:94-103) is not implemented; use GPU_RESIDENT (K/V in HBM) or CPU (host attention)");
     if (!model.arch || model.arch->n_q_heads <= 0 || model.arch->head_dim <= 0 || model.arch->vocab <= 0)
       throw std::invalid_argument("VerifyEngine: ModelSpec.arch (n_q_heads, head_dim, vocab) is required");
     const ModelArch& a = *model.arch;
@@ -107,29 +117,47 @@ class VerifyEngine {
     o.max_batch = std::int32_t(hyper.b);
     o.max_verify = std::int32_t(std::max(1, hyper.k) + 1);
     o.max_seq = std::int32_t(opt.max_seq > 0 ? opt.max_seq : 2048);
-    o.hbm_slots = opt.hbm_slots;
+    // capacity from the MemoryPlan: the hot cache, and (engine-placement
+    // plan, memory.hpp overload) the streamer's staging slots
+    if (hyper.b > plan.b_max) throw CapacityError("VerifyEngine: Hyperparameters.b exceeds MemoryPlan.b_max");
+    const double layer_bytes = 3.0 * double(model.n_expert) * model.expert_size() * double(model.bytes_per_elem);
+    o.hbm_slots = plan.slot_pool_bytes > 0 ? std::max(2, int(std::lround(plan.slot_pool_bytes / layer_bytes)))
+                                           : opt.hbm_slots;
     o.expert_cache_bytes = std::int64_t(plan.expert_cache_bytes);
     o.host_alias_layers = opt.host_alias_layers;
     o.device = opt.device;
     o.flags = opt.debug ? SMO_ENGINE_DEBUG : 0;
-    o.ep_rank = 0;
-    o.ep_size = 1;
+    o.ep_rank = opt.ep_rank;
+    o.ep_size = opt.ep_size;
+    o.nccl_comm = opt.ep_group;
+    if (opt.ep_size > 1 && !opt.ep_group)
+      throw std::invalid_argument("VerifyEngine: ep_size > 1 needs EngineOptions.ep_group");
+    // Hyperparameters.m (config.hpp:118-125): micro-batches, stage-major per
+    // layer like build_target_dag (pipeline.hpp:147-206)
+    o.micro_batches = std::int32_t(std::max<std::int64_t>(1, hyper.m));
     o.kv_pages = opt.kv_pages;
     o.compress_experts = opt.compress_experts ? 1 : 0;
     // AttentionPlacement::CPU (the reference's default, config.hpp:110): target
-    // K/V in pinned host DRAM, attention on the host pool (f4); GPU_TRANSFER
-    // and GPU_RESIDENT run K1 on HBM-resident K/V
+    // K/V in pinned host DRAM, attention on the host pool (f4); GPU_RESIDENT
+    // runs K1 on HBM-resident K/V (GPU_TRANSFER is rejected above)
     o.attn_cpu = hyper.exec_strategy.attention_placement == AttentionPlacement::CPU ? 1 : 0;
     // MoeBatching::BATCH_ONE (config.hpp:111): stream only router-selected experts
     o.moe_batching = hyper.exec_strategy.moe_batching == MoeBatching::BATCH_ONE ? 1 : 0;
     detail::smo_check(smo_engine_create(&c, &o, &h_));
     layers_ = model.n_layers;
     max_verify_ = o.max_verify;
+    max_seq_ = o.max_seq;
+    attn_cpu_ = o.attn_cpu != 0;
   }
   VerifyEngine(const VerifyEngine&) = delete;
   VerifyEngine& operator=(const VerifyEngine&) = delete;
   ~VerifyEngine() {
     if (h_) smo_engine_destroy(h_);
+  }
+
+  // The m of a plan (optimize(), optimizer.hpp:130-175) for the next steps.
+  void set_micro_batches(std::int64_t m) {
+    detail::smo_check(smo_engine_set_micro_batches(h_, std::int32_t(std::max<std::int64_t>(1, m))));
   }
 
   void fill_prefix(const std::vector<std::int32_t>& prefix_len) {
@@ -246,7 +274,7 @@ class VerifyEngine {
   // Committed tokens per request since prefill/decode_begin (accepted drafts
   // + bonus of every step; the prefill's next token is the first root).
   std::vector<std::vector<std::int32_t>> committed() {
-    const std::int32_t b = std::int32_t(kv_len_.size()), cap = 4096;
+    const std::int32_t b = std::int32_t(kv_len_.size()), cap = std::int32_t(max_seq_);  // history capacity
     std::vector<std::int32_t> buf(static_cast<std::size_t>(b) * std::size_t(cap)), n(static_cast<std::size_t>(b));
     detail::smo_check(smo_engine_decode_read(h_, buf.data(), cap, n.data(), nullptr, nullptr));
     std::vector<std::vector<std::int32_t>> out(static_cast<std::size_t>(b));
@@ -266,12 +294,14 @@ class VerifyEngine {
   IterationResult measured(const VerifyBatch& in) {
     smo_stage_times st{};
     detail::smo_check(smo_engine_last_times(h_, &st));
-    std::vector<double> lt(std::size_t(layers_) * 9);
+    std::int32_t m = 1;
+    detail::smo_check(smo_engine_last_micro_batches(h_, &m));
+    const std::size_t stride = 4 + 6 * std::size_t(m);
+    std::vector<double> lt(std::size_t(layers_) * stride);
     detail::smo_check(smo_engine_layer_times(h_, lt.data(), lt.size()));
     IterationResult r;
     EventDag& dag = r.target_dag;
     Schedule& sc = r.target_schedule;
-    int prev_h2d = -1, prev_moe = -1;
     auto add = [&](EventKind k, ExecResource res, double t0, double t1, std::vector<int> deps, std::string lbl) {
       EventNode ev;
       ev.id = int(dag.size());
@@ -287,35 +317,59 @@ class VerifyEngine {
       sc.makespan = std::max(sc.makespan, sc.end.back());
       return ev.id;
     };
-    double attn = 0, moe = 0, h2d = 0, o1 = 0, o2 = 0;
+    // the measured DAG has build_target_dag's structure and id order
+    // (pipeline.hpp:147-206): per layer the transfer, then each stage for
+    // every micro-batch (stage-major); GPU_MOE(l, j) <- {GPU_OTHER2(l, j),
+    // H2D(l)}, GPU_OTHER1(l, j) <- GPU_MOE(l-1, j)
+    const ExecResource attn_res = attn_cpu_ ? ExecResource::CPU : ExecResource::GPU;
+    int prev_h2d = -1;
+    const std::size_t nm = std::size_t(m);
+    std::vector<int> prev_moe(nm, -1), v_o1(nm, -1), v_at(nm, -1), v_o2(nm, -1);
+    double attn = 0, moe = 0, h2d = 0, o1t = 0, o2t = 0;
     for (std::int64_t l = 0; l < layers_; ++l) {
-      const double* t = lt.data() + l * 9;  // h2d0 h2d1 attn0 attn1 moe0 moe1 layer0 premoe bytes
+      const double* t = lt.data() + std::size_t(l) * stride;  // h2d0 h2d1 bytes raw | per mb: o1 a0 a1 pre m0 m1
       const std::string L = "L" + std::to_string(l);
       std::vector<int> hd;
       if (prev_h2d >= 0) hd.push_back(prev_h2d);
       const int eh = add(EventKind::H2D_EXPERTS, ExecResource::H2D, t[0], t[1], hd, L + "/H2D_EXPERTS");
-      std::vector<int> od;
-      if (prev_moe >= 0) od.push_back(prev_moe);
-      const int e1 = add(EventKind::GPU_OTHER1, ExecResource::GPU, t[6], t[2], od, L + "/mb0/GPU_OTHER1");
-      const int ea = add(EventKind::CPU_ATTN, ExecResource::GPU, t[2], t[3], {e1}, L + "/mb0/CPU_ATTN");
-      const int e2 = add(EventKind::GPU_OTHER2, ExecResource::GPU, t[3], t[7], {ea}, L + "/mb0/GPU_OTHER2");
-      prev_moe = add(EventKind::GPU_MOE, ExecResource::GPU, t[4], t[5], {e2, eh}, L + "/mb0/GPU_MOE");
       prev_h2d = eh;
       h2d += t[1] - t[0];
-      attn += t[3] - t[2];
-      moe += t[5] - t[4];
-      o1 += t[2] - t[6];
-      o2 += t[7] - t[3];
+      auto mbt = [&](int j) { return t + 4 + 6 * j; };
+      auto tag = [&](int j, const char* stage) { return L + "/mb" + std::to_string(j) + "/" + stage; };
+      for (int j = 0; j < m; ++j) {
+        std::vector<int> od;
+        if (prev_moe[std::size_t(j)] >= 0) od.push_back(prev_moe[std::size_t(j)]);
+        v_o1[std::size_t(j)] = add(EventKind::GPU_OTHER1, ExecResource::GPU, mbt(j)[0], mbt(j)[1], od,
+                                 tag(j, "GPU_OTHER1"));
+        o1t += mbt(j)[1] - mbt(j)[0];
+      }
+      for (int j = 0; j < m; ++j) {
+        v_at[std::size_t(j)] = add(EventKind::CPU_ATTN, attn_res, mbt(j)[1], mbt(j)[2], {v_o1[std::size_t(j)]},
+                                 tag(j, "CPU_ATTN"));
+        attn += mbt(j)[2] - mbt(j)[1];
+      }
+      for (int j = 0; j < m; ++j) {
+        v_o2[std::size_t(j)] = add(EventKind::GPU_OTHER2, ExecResource::GPU, mbt(j)[2], mbt(j)[3],
+                                 {v_at[std::size_t(j)]}, tag(j, "GPU_OTHER2"));
+        o2t += mbt(j)[3] - mbt(j)[2];
+      }
+      for (int j = 0; j < m; ++j) {
+        prev_moe[std::size_t(j)] = add(EventKind::GPU_MOE, ExecResource::GPU, mbt(j)[4], mbt(j)[5],
+                                       {v_o2[std::size_t(j)], eh}, tag(j, "GPU_MOE"));
+        moe += mbt(j)[5] - mbt(j)[4];
+      }
     }
     IterationBreakdown& bd = r.breakdown;
     bd.target_total = st.target_total;
     bd.cpu_attention = attn;
     bd.gpu_moe = moe;
     bd.h2d_transfer = h2d;
-    bd.others = std::max(0.0, st.target_total - attn - moe - o1 - o2);
+    bd.others = std::max(0.0, st.target_total - attn - moe - o1t - o2t);
     bd.iteration = st.target_total;
     // driving variables as the reference defines them (pipeline.hpp:256-264);
-    // the engine verifies n = k+1 rows, the reference charges k (App. C.2)
+    // the engine verifies n = k+1 rows, the reference charges k (App. C.2).
+    // Per-micro-batch stages are charged per layer for the whole batch, as
+    // iteration_time looks them up before dividing by m (pipeline.hpp:358-372).
     const double b = double(in.b);
     const double k = double(std::max<std::int64_t>(1, in.n - 1));
     double s = 0;
@@ -324,15 +378,17 @@ class VerifyEngine {
     const double nl = double(layers_);
     samples_.push_back({EventKind::CPU_ATTN, b * (s + k) * k, attn / nl});
     samples_.push_back({EventKind::GPU_MOE, b * k, moe / nl});
-    // one transfer sample per layer: bytes actually streamed (hot-cached
-    // experts excluded) -> the copy-engine's affine cost, as the paper's
-    // profiler fits it
+    // one transfer sample per layer. Driving variable: the bf16 bytes of the
+    // experts the layer streamed — the unit iteration_time looks H2D_EXPERTS
+    // up with (3 * n_expert * expert_size * bytes_per_elem, pipeline.hpp:
+    // 361-364) — so the fitted slope absorbs the link code (and a hot cache
+    // shows up as layers with fewer bytes): seconds per bf16 byte carried
     for (std::int64_t l = 0; l < layers_; ++l) {
-      const double* t = lt.data() + l * 9;
-      if (t[8] > 0) samples_.push_back({EventKind::H2D_EXPERTS, t[8], t[1] - t[0]});
+      const double* t = lt.data() + std::size_t(l) * stride;
+      if (t[3] > 0) samples_.push_back({EventKind::H2D_EXPERTS, t[3], t[1] - t[0]});
     }
-    samples_.push_back({EventKind::GPU_OTHER1, b * k, o1 / nl});
-    samples_.push_back({EventKind::GPU_OTHER2, b * k, o2 / nl});
+    samples_.push_back({EventKind::GPU_OTHER1, b * k, o1t / nl});
+    samples_.push_back({EventKind::GPU_OTHER2, b * k, o2t / nl});
     samples_.push_back({EventKind::OVERHEAD, b * (k + 1), bd.others});
     return r;
   }
@@ -343,6 +399,8 @@ class VerifyEngine {
   smo_engine* h_ = nullptr;
   std::int64_t layers_ = 0;
   int max_verify_ = 1;
+  std::int64_t max_seq_ = 2048;
+  bool attn_cpu_ = false;
   std::vector<std::int32_t> kv_len_;  // decode state mirror (host)
   std::vector<int> ks_;
   std::vector<ProfileSample> samples_;

@@ -351,6 +351,13 @@ typedef struct {
                                  else raw; env SMO_CODEC=fixed skips unary) and cross the link
                                  coded; the compute stream expands each layer's blocks into its HBM
                                  slot before the expert kernel. */
+  int32_t micro_batches;      /* Hyperparameters.m (config.hpp:118-125): the batch runs as m micro-
+                                 batches of ~b/m requests, issued stage-major per layer like
+                                 build_target_dag (pipeline.hpp:147-206): GPU_OTHER1 of every
+                                 micro-batch, then their attention, GPU_OTHER2, GPU_MOE (all waiting
+                                 on the layer's one expert transfer). With the CPU placement the host
+                                 attends micro-batch j while the GPU runs j+1's stages. 0/1 = one;
+                                 at most 8; LARGE_BATCH without expert parallelism. */
 } smo_engine_options;
 
 /* ---- expert parallelism ----------------------------------
@@ -403,6 +410,9 @@ typedef struct smo_engine smo_engine;
 
 smo_status smo_engine_create(const smo_model_config* cfg, const smo_engine_options* opt,
                              smo_engine** out);
+/* Change the micro-batch count for subsequent verify / decode steps (the m
+ * that optimize() returns, optimizer.hpp:130-175). Same limits as above.     */
+smo_status smo_engine_set_micro_batches(smo_engine* e, int32_t m);
 smo_status smo_engine_destroy(smo_engine* e);
 /* Fill the synthetic prefix KV of every layer for requests 0..b-1. */
 smo_status smo_engine_fill_prefix(smo_engine* e, const int32_t* prefix_len_host, int32_t b);
@@ -442,11 +452,15 @@ typedef struct {
   double codec_bytes;  /* their algorithmic bytes: code read + bf16 written (streamed + coded hot cache) */
 } smo_stage_times;
 smo_status smo_engine_last_times(smo_engine* e, smo_stage_times* t);
-/* Measured per-layer timeline of the last verify, 9 doubles per layer (s from
- * the step start): H2D_EXPERTS start/end, K1 start/end, GPU_MOE start/end
- * (after the slot wait), layer start, pre-MoE (after permute), and the bytes
- * streamed for that layer (hot-cached experts excluded). n >= 9*L.         */
+/* Measured per-layer timeline of the last verify step with m micro-batches
+ * (smo_engine_last_micro_batches), 4 + 6m doubles per layer, seconds from
+ * the step start: H2D_EXPERTS start, end, the bytes streamed for the layer
+ * (hot-cached experts excluded), their bf16 size; then per micro-batch j:
+ * GPU_OTHER1 start, attention start, attention end (CPU placement: when the
+ * GPU saw the host job finish), pre-MoE (GPU_OTHER2 end), GPU_MOE start
+ * (after the slot wait), GPU_MOE end. n >= (4 + 6m) * L.                    */
 smo_status smo_engine_layer_times(smo_engine* e, double* out, size_t n);
+smo_status smo_engine_last_micro_batches(smo_engine* e, int32_t* m);
 
 /* ---- prefill + decode loop ------------------------------
  * The KV lifecycle around the verify step, all on the engine's device state:

@@ -62,7 +62,7 @@ class EngineOptions(C.Structure):
                 ("expert_cache_bytes", _i64), ("host_alias_layers", _i32), ("device", _i32), ("flags", _i32),
                 ("ep_rank", _i32), ("ep_size", _i32), ("nccl_comm", _vp), ("kv_pages", _i32),
                 ("attn_cpu", _i32), ("moe_batching", _i32),
-                ("compress_experts", _i32)]
+                ("compress_experts", _i32), ("micro_batches", _i32)]
 
 
 class StreamerArgs(C.Structure):
@@ -148,6 +148,8 @@ _SIGS = {
     "smo_engine_decode_read": (C.c_int, [_vp, _vp, _i32, _vp, _vp, _vp]),
     "smo_engine_draft_times": (C.c_int, [_vp, _vp, _sz, _vp]),
     "smo_engine_layer_times": (C.c_int, [_vp, _vp, _sz]),
+    "smo_engine_last_micro_batches": (C.c_int, [_vp, _vp]),
+    "smo_engine_set_micro_batches": (C.c_int, [_vp, _i32]),
     "smo_engine_debug_tensor": (C.c_int, [_vp, C.c_char_p, _i32, _vp, _sz]),
     "smo_engine_tensor_ptr": (C.c_int, [_vp, C.c_char_p, _i32, _i32, C.POINTER(_vp), C.POINTER(_sz)]),
 }

@@ -83,7 +83,7 @@ void Engine::attn_sublayer_cpu(const Scratch& sc, const uint16_t* wqkv, const ui
   job.pool = cpu_pool.get();
   job.job = CpuAttnJob{qh, kc, vc, mask_h, pre_h, ah, b, n, nq, nkv, d, s_max, nch};
   SMO_CUDA_CHECK(cudaLaunchHostFunc(st, host_attn_cb, &job));
-  SMO_CUDA_CHECK(cudaMemcpyAsync(sc.attn, ah, size_t(rows) * nq * d * 2, cudaMemcpyHostToDevice, st));
+  copy_from_mapped(sc.attn, ah, size_t(rows) * nq * d * 2, st);  // not behind the expert stream's H2D copies
   dense_gemm(sc.attn, rows, nq * d, h, wo, nullptr, SMO_EPI_F32_ADD, sc.x, sc.split, st);
 }
 

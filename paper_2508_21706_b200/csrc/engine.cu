@@ -381,7 +381,7 @@ void Engine::create() {
   attn = dalloc<uint16_t>(size_t(maxT) * nq * d);
   ids = dalloc<int32_t>(P);
   rw = dalloc<float>(P);
-  offsets = dalloc<int32_t>(E + 1);
+  offsets = dalloc<int32_t>(size_t(E + 1) * kMaxMb);  // one [E+1] region per micro-batch
   perm = dalloc<int32_t>(P);
   pos = dalloc<int32_t>(P);
   xp = dalloc<uint16_t>(size_t(P) * h);
@@ -474,8 +474,11 @@ void Engine::create() {
     attn_host = halloc_mapped<uint16_t>(size_t(maxT) * nq * d);
     prefix_host = halloc_mapped<int32_t>(maxB);
     mask_host = halloc_mapped<uint64_t>(maxT);
-    host_jobs.resize(size_t(L));
+    host_jobs.resize(size_t(L) * kMaxMb);
+    host_flags = halloc_mapped<uint32_t>(2);
+    async_host.start(host_flags, host_flags + 1);
   }
+  set_micro_batches(opt.micro_batches);
   // drafter + decode-loop state
   if (dL > 0) dh = dalloc<uint16_t>(size_t(maxT) * dI);
   d_dtok = dalloc<int32_t>(maxB);
@@ -505,7 +508,7 @@ void Engine::create() {
   }
   h_stage_elems = size_t(maxT) * 4 + maxB * 4;
   SMO_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_stage), h_stage_elems * 4, cudaHostAllocPortable));
-  ev.resize(8 + size_t(L) * 8);
+  ev.resize(8 + size_t(L) * 8 * kMaxMb);  // per layer: 8 events of micro-batch 0, then 8 per further one
   for (auto& e : ev) SMO_CUDA_CHECK(cudaEventCreate(&e));
   draft_ev.resize(size_t(maxN) + 1);
   for (auto& e : draft_ev) SMO_CUDA_CHECK(cudaEventCreate(&e));
@@ -836,95 +839,120 @@ void Engine::begin_step(cudaStream_t st, bool prefetch) {
 
 // The target verification DAG on device inputs: tokens [b*n], parent
 // [b*n] or null, prefix [b]; results in d_acc / d_bonus / d_keep / target.
+// With m micro-batches (requests [j*b/m, (j+1)*b/m)) every stage of a layer
+// is issued for all micro-batches before the next stage — the stage-major
+// order of build_target_dag (pipeline.hpp:167-170) — and every micro-batch's
+// GPU_MOE waits on the layer's single expert transfer.
 void Engine::verify_core(int b, int n, const int32_t* tokens, const int32_t* parent, const int32_t* prefix, int max_prefix,
                  cudaStream_t st) {
   const int T = b * n;
+  const int M = std::max(1, std::min(mb, b));
+  last_mb = M;
   cudaEvent_t e_end = ev[1];
   double h2d_bytes = step_h2d_bytes;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> h2d_ev = step_h2d_ev, attn_ev, moe_ev;
   build_mask(parent, b, n, d_mask, st);
   embed(tokens, embed_w, T, h, x, st);
-
+  const bool async_cpu = attn_cpu && !capturing;
+  if (attn_cpu) {  // prefix lengths and the mask to the host once per step
+    SMO_CUDA_CHECK(cudaMemcpyAsync(prefix_host, prefix, size_t(b) * 4, cudaMemcpyDeviceToHost, st));
+    SMO_CUDA_CHECK(cudaMemcpyAsync(mask_host, d_mask, size_t(T) * 8, cudaMemcpyDeviceToHost, st));
+  }
+  // micro-batch j: requests [r0, r0 + bj), rows [R0, R0 + Tj)
+  struct Mb {
+    int r0, bj, R0, Tj;
+  };
+  std::vector<Mb> mbs;
+  for (int j = 0; j < M; ++j) {
+    const int r0 = j * b / M, r1 = (j + 1) * b / M;
+    mbs.push_back({r0, r1 - r0, r0 * n, (r1 - r0) * n});
+  }
+  const size_t kv_req = paged ? 0 : size_t(nkv) * s_max * d;  // cache elements per request (contiguous)
   const int PT = T * K;  // (token, slot) pairs
+  std::vector<uint32_t> seq(size_t(M), 0);
   for (int l = 0; l < L; ++l) {
     Layer& ly = layers[l];
-    bool moe_end_recorded = false;
-    SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 6), st));
-    snap("x_in", l, x, size_t(T) * h * 4, st);
-    rmsnorm(x, ones, T, h, cfg.rms_eps, xn, st);
-    snap("xn1", l, xn, size_t(T) * h * 2, st);
-    smo_gemm_args g{};
-    g.x = xn;
-    g.rows = T;
-    g.K = h;
-    g.N = qkv_w;
-    g.groups = 1;
-    g.max_rows_per_group = T;
-    g.w = ly.wqkv;
-    g.w_pool_blocks = 1;
-    g.epilogue = SMO_EPI_BF16;
-    g.out = qkv;
-    g.ldo = qkv_w;
-    g.workspace = gemm_ws;
-    g.workspace_bytes = gemm_ws_bytes;
-    gemm_launch(g, st);
-    uint16_t* q_dst = attn_cpu ? q_host : q;  // CPU placement: q straight into pinned host memory
-    rope_append(qkv, prefix, parent, b, n, nq, nkv, d, s_max, cfg.rope_theta, q_dst, ly.kc, ly.vc, st, bt(),
-                max_pages);
-    snap("q", l, q_dst, size_t(T) * nq * d * 2, st);
-    smo_attn_args a{};
-    a.q = q;
-    a.k_cache = ly.kc;
-    a.v_cache = ly.vc;
-    a.block_table = bt();
-    a.max_pages = max_pages;
-    a.num_pages = num_pages;
-    a.mask = d_mask;
-    a.prefix_len = prefix;
-    a.out = attn;
-    a.b = b;
-    a.n = n;
-    a.n_q = nq;
-    a.n_kv = nkv;
-    a.d = d;
-    a.s_max = s_max;
-    a.max_prefix = max_prefix;
-    a.workspace = attn_ws;
-    a.workspace_bytes = attn_ws_bytes;
-    SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 2), st));
-    if (attn_cpu) {
-      // the paper's CPU attention: prefix lengths and mask to the host, the
-      // host pool attends over the host K/V, the output goes back for O-proj
-      SMO_CUDA_CHECK(cudaMemcpyAsync(prefix_host, prefix, size_t(b) * 4, cudaMemcpyDeviceToHost, st));
-      SMO_CUDA_CHECK(cudaMemcpyAsync(mask_host, d_mask, size_t(T) * 8, cudaMemcpyDeviceToHost, st));
-      HostAttn& hj = host_jobs[size_t(l)];
-      hj.pool = cpu_pool.get();
-      hj.job = CpuAttnJob{q_host, ly.kc, ly.vc, mask_host, prefix_host, attn_host, b, n, nq, nkv, d, s_max, 1};
-      SMO_CUDA_CHECK(cudaLaunchHostFunc(st, host_attn_cb, &hj));
-      SMO_CUDA_CHECK(cudaMemcpyAsync(attn, attn_host, size_t(T) * nq * d * 2, cudaMemcpyHostToDevice, st));
-    } else {
-      attention_launch(a, st);
+    const int32_t* btl = bt();
+    // ---- GPU_OTHER1: RMSNorm -> QKV -> RoPE + K/V append
+    for (int j = 0; j < M; ++j) {
+      const Mb& m = mbs[size_t(j)];
+      SMO_CUDA_CHECK(cudaEventRecord(mev(l, j, 6), st));
+      if (j == 0) snap("x_in", l, x, size_t(T) * h * 4, st);
+      rmsnorm(x + size_t(m.R0) * h, ones, m.Tj, h, cfg.rms_eps, xn + size_t(m.R0) * h, st);
+      if (j == M - 1) snap("xn1", l, xn, size_t(T) * h * 2, st);
+      smo_gemm_args g{};
+      g.x = xn + size_t(m.R0) * h;
+      g.rows = m.Tj;
+      g.K = h;
+      g.N = qkv_w;
+      g.groups = 1;
+      g.max_rows_per_group = m.Tj;
+      g.w = ly.wqkv;
+      g.w_pool_blocks = 1;
+      g.epilogue = SMO_EPI_BF16;
+      g.out = qkv + size_t(m.R0) * qkv_w;
+      g.ldo = qkv_w;
+      g.workspace = gemm_ws;
+      g.workspace_bytes = gemm_ws_bytes;
+      gemm_launch(g, st);
+      uint16_t* q_dst = (attn_cpu ? q_host : q) + size_t(m.R0) * nq * d;
+      rope_append(qkv + size_t(m.R0) * qkv_w, prefix + m.r0, parent ? parent + m.R0 : nullptr, m.bj, n, nq, nkv, d,
+                  s_max, cfg.rope_theta, q_dst, ly.kc + size_t(m.r0) * kv_req, ly.vc + size_t(m.r0) * kv_req, st,
+                  btl ? btl + size_t(m.r0) * max_pages : nullptr, max_pages);
+      if (j == M - 1) snap("q", l, attn_cpu ? q_host : q, size_t(T) * nq * d * 2, st);
+      SMO_CUDA_CHECK(cudaEventRecord(mev(l, j, 2), st));
+      if (attn_cpu) {
+        HostAttn& hj = host_jobs[size_t(l) * kMaxMb + size_t(j)];
+        hj.pool = cpu_pool.get();
+        hj.job = CpuAttnJob{q_host + size_t(m.R0) * nq * d, ly.kc + size_t(m.r0) * kv_req,
+                            ly.vc + size_t(m.r0) * kv_req, mask_host + m.R0, prefix_host + m.r0,
+                            attn_host + size_t(m.R0) * nq * d, m.bj, n, nq, nkv, d, s_max, 1};
+        if (async_cpu) {  // the host starts as soon as this micro-batch's q is written
+          seq[size_t(j)] = ++host_seq;
+          async_host.push({hj.job, hj.pool, seq[size_t(j)]});
+          signal_host_ready(seq[size_t(j)], st);
+        }
+      }
     }
-    SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 3), st));
-    attn_ev.push_back({tev(l * 8 + 2), tev(l * 8 + 3)});
+    // ---- attention (K1 on HBM, or the host job)
+    for (int j = 0; j < M; ++j) {
+      const Mb& m = mbs[size_t(j)];
+      if (attn_cpu) {
+        HostAttn& hj = host_jobs[size_t(l) * kMaxMb + size_t(j)];
+        if (async_cpu) wait_host_flag(seq[size_t(j)], st);
+        else SMO_CUDA_CHECK(cudaLaunchHostFunc(st, host_attn_cb, &hj));
+        // SM loads of the mapped host output, not a copy-engine H2D copy: the
+        // H2D engine is busy with the expert stream (a 1.8 GB layer copy)
+        // and would queue this behind it
+        copy_from_mapped(attn + size_t(m.R0) * nq * d, attn_host + size_t(m.R0) * nq * d, size_t(m.Tj) * nq * d * 2,
+                         st);
+      } else {
+        smo_attn_args a{};
+        a.q = q + size_t(m.R0) * nq * d;
+        a.k_cache = ly.kc + size_t(m.r0) * kv_req;
+        a.v_cache = ly.vc + size_t(m.r0) * kv_req;
+        a.block_table = btl ? btl + size_t(m.r0) * max_pages : nullptr;
+        a.max_pages = max_pages;
+        a.num_pages = num_pages;
+        a.mask = d_mask + m.R0;
+        a.prefix_len = prefix + m.r0;
+        a.out = attn + size_t(m.R0) * nq * d;
+        a.b = m.bj;
+        a.n = n;
+        a.n_q = nq;
+        a.n_kv = nkv;
+        a.d = d;
+        a.s_max = s_max;
+        a.max_prefix = max_prefix;
+        a.workspace = attn_ws;
+        a.workspace_bytes = attn_ws_bytes;
+        attention_launch(a, st);
+      }
+      SMO_CUDA_CHECK(cudaEventRecord(mev(l, j, 3), st));
+      attn_ev.push_back({mev(l, j, 2), mev(l, j, 3)});
+    }
     snap("attn", l, attn, size_t(T) * nq * d * 2, st);
-    g = smo_gemm_args{};
-    g.x = attn;
-    g.rows = T;
-    g.K = nq * d;
-    g.N = h;
-    g.groups = 1;
-    g.max_rows_per_group = T;
-    g.w = ly.wo;
-    g.w_pool_blocks = 1;
-    g.epilogue = SMO_EPI_F32_ADD;
-    g.out = x;
-    g.ldo = h;
-    g.workspace = gemm_ws;
-    g.workspace_bytes = gemm_ws_bytes;
-    gemm_launch(g, st);
-    rmsnorm(x, ones, T, h, cfg.rms_eps, xn, st);
-    snap("xn2", l, xn, size_t(T) * h * 2, st);
+    // ---- GPU_OTHER2: O-proj (+residual) -> RMSNorm -> router -> permute (-> shared expert)
     float* rlog = nullptr;
     if (debug) {
       auto& v = dbg["logits_r"];
@@ -935,119 +963,155 @@ void Engine::verify_core(int b, int n, const int32_t* tokens, const int32_t* par
       }
       rlog = reinterpret_cast<float*>(v[l + 1].p);
     }
-    router_topk(xn, ly.router, T, h, E, K, rlog, ids, rw, st);
-    if (ep_on) {  // owner-major order: rows bound for one rank are contiguous
-      ep_remap(ids, T * K, P, E_loc, oid, st);
-      permute(oid, T, K, E, xn, h, offsets, perm, pos, xp, st);
-    } else {
-      permute(ids, T, K, E, xn, h, offsets, perm, pos, xp, st);
-    }
-    snap("ids", l, ids, size_t(PT) * 4, st);
-    snap("weights", l, rw, size_t(PT) * 4, st);
-    snap("offsets", l, offsets, size_t(E + 1) * 4, st);
-    snap("pos", l, pos, size_t(PT) * 4, st);
-    if (batch_one) {
-      // BATCH_ONE (optimizer.hpp:81-96): wait for this layer's routing, then
-      // stream only the experts its tokens selected
-      SMO_CUDA_CHECK(cudaMemcpyAsync(h_offsets, offsets, size_t(E + 1) * 4, cudaMemcpyDeviceToHost, st));
-      SMO_CUDA_CHECK(cudaEventRecord(route_ev, st));
-      SMO_CUDA_CHECK(cudaEventSynchronize(route_ev));
-      std::vector<uint8_t> act(size_t(E_loc), 0);
-      for (int e = 0; e < E; ++e) act[size_t(local(e))] = h_offsets[e + 1] > h_offsets[e] ? 1 : 0;
-      h2d_bytes += enqueue_h2d(l, tev(l * 8 + 0), tev(l * 8 + 1), act.data());
-      h2d_ev.push_back({tev(l * 8 + 0), tev(l * 8 + 1)});
-      const double pf = b1_prefetch_step(l, copy);  // fills the link while layer l+1 is routed
-      h2d_bytes += pf;  // counted in the step's link bytes (wasted when the expert goes unrouted)
-    }
-    if (cfg.shared_inter > 0) {
-      // always-on shared expert (config 4): x += SwiGLU_shared(xn2); its
-      // weights are resident, so it runs before the wait for streamed experts
-      smo_gemm_args gs{};
-      gs.x = xn;
-      gs.rows = T;
-      gs.K = h;
-      gs.N = cfg.shared_inter;
-      gs.groups = 1;
-      gs.max_rows_per_group = T;
-      gs.w = ly.ws1;
-      gs.w_up = ly.ws3;
-      gs.w_pool_blocks = 1;
-      gs.epilogue = SMO_EPI_SWIGLU;
-      gs.out = hs;
-      gs.ldo = cfg.shared_inter;
-      gemm_launch(gs, st);
-      gs = smo_gemm_args{};
-      gs.x = hs;
-      gs.rows = T;
-      gs.K = cfg.shared_inter;
-      gs.N = h;
-      gs.groups = 1;
-      gs.max_rows_per_group = T;
-      gs.w = ly.ws2;
-      gs.w_pool_blocks = 1;
-      gs.epilogue = SMO_EPI_F32_ADD;
-      gs.out = x;
-      gs.ldo = h;
-      gs.workspace = gemm_ws;
-      gs.workspace_bytes = gemm_ws_bytes;
-      gemm_launch(gs, st);
-    }
-    // ---- MoE: wait for this layer's experts
-    if (ep_on) {
-      moe_ep(l, T, st);
-    } else {
-      SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 7), st));
-      SMO_CUDA_CHECK(cudaStreamWaitEvent(st, slot_ready[l % slots], 0));
-      decode_slot(l, st);  // coded expert blocks -> bf16 slot (compress_experts)
-      SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 4), st));
-      if (moe_fused) {
-        moe_launch(xp, PT, h, hi, E, offsets, pool, blk_bytes, pool_blocks, d_w_index + size_t(l) * E, hbuf, ybuf,
-                   moe_splits, moe_splits, d_done, st);
-        // GPU_MOE = the expert kernel itself (the bench's kernel roofline)
-        SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 5), st));
-        moe_end_recorded = true;
-        SMO_CUDA_CHECK(cudaEventRecord(slot_free[l % slots], st));
-        unpermute_combine(ybuf, pos, rw, T, K, h, x, st, moe_splits, size_t(PT) * h);
-      } else {
-      g = smo_gemm_args{};
-      g.x = xp;
-      g.rows = PT;
-      g.K = h;
-      g.N = hi;
-      g.groups = E;
-      g.row_offsets = offsets;
-      g.max_rows_per_group = T;  // a token selects an expert at most once
-      g.w = pool;
-      g.w_up = pool + size_t(hi) * h;
-      g.w_block_stride = blk_bytes;
-      g.w_pool_blocks = pool_blocks;
-      g.w_index = d_w_index + size_t(l) * E;
-      g.epilogue = SMO_EPI_SWIGLU;
-      g.out = hbuf;
-      g.ldo = hi;
-      gemm_launch(g, st);
-      g = smo_gemm_args{};
-      g.x = hbuf;
-      g.rows = PT;
-      g.K = hi;
+    for (int j = 0; j < M; ++j) {
+      const Mb& m = mbs[size_t(j)];
+      float* xj = x + size_t(m.R0) * h;
+      uint16_t* xnj = xn + size_t(m.R0) * h;
+      smo_gemm_args g{};
+      g.x = attn + size_t(m.R0) * nq * d;
+      g.rows = m.Tj;
+      g.K = nq * d;
       g.N = h;
-      g.groups = E;
-      g.row_offsets = offsets;
-      g.max_rows_per_group = T;
-      g.w = pool + 2 * size_t(hi) * h;
-      g.w_block_stride = blk_bytes;
-      g.w_pool_blocks = pool_blocks;
-      g.w_index = d_w_index + size_t(l) * E;
-      g.epilogue = SMO_EPI_F32;
-      g.out = ybuf;
+      g.groups = 1;
+      g.max_rows_per_group = m.Tj;
+      g.w = ly.wo;
+      g.w_pool_blocks = 1;
+      g.epilogue = SMO_EPI_F32_ADD;
+      g.out = xj;
       g.ldo = h;
+      g.workspace = gemm_ws;
+      g.workspace_bytes = gemm_ws_bytes;
       gemm_launch(g, st);
-      SMO_CUDA_CHECK(cudaEventRecord(slot_free[l % slots], st));
-      unpermute_combine(ybuf, pos, rw, T, K, h, x, st);
+      rmsnorm(xj, ones, m.Tj, h, cfg.rms_eps, xnj, st);
+      if (j == M - 1) snap("xn2", l, xn, size_t(T) * h * 2, st);
+      const size_t p0 = size_t(m.R0) * K;  // first (token, slot) pair of the micro-batch
+      int32_t* offj = offsets + size_t(j) * (E + 1);
+      router_topk(xnj, ly.router, m.Tj, h, E, K, rlog ? rlog + size_t(m.R0) * E : nullptr, ids + p0, rw + p0, st);
+      if (ep_on) {  // owner-major order: rows bound for one rank are contiguous
+        ep_remap(ids, T * K, P, E_loc, oid, st);
+        permute(oid, T, K, E, xn, h, offsets, perm, pos, xp, st);
+      } else {
+        permute(ids + p0, m.Tj, K, E, xnj, h, offj, perm + p0, pos + p0, xp + p0 * h, st);
       }
+      if (j == M - 1) {
+        snap("ids", l, ids, size_t(PT) * 4, st);
+        snap("weights", l, rw, size_t(PT) * 4, st);
+        snap("offsets", l, offsets, size_t(E + 1) * 4, st);
+        snap("pos", l, pos, size_t(PT) * 4, st);
+      }
+      if (batch_one) {
+        // BATCH_ONE (optimizer.hpp:81-96): wait for this layer's routing, then
+        // stream only the experts its tokens selected
+        SMO_CUDA_CHECK(cudaMemcpyAsync(h_offsets, offsets, size_t(E + 1) * 4, cudaMemcpyDeviceToHost, st));
+        SMO_CUDA_CHECK(cudaEventRecord(route_ev, st));
+        SMO_CUDA_CHECK(cudaEventSynchronize(route_ev));
+        std::vector<uint8_t> act(size_t(E_loc), 0);
+        for (int e = 0; e < E; ++e) act[size_t(local(e))] = h_offsets[e + 1] > h_offsets[e] ? 1 : 0;
+        h2d_bytes += enqueue_h2d(l, tev(l * 8 + 0), tev(l * 8 + 1), act.data());
+        h2d_ev.push_back({tev(l * 8 + 0), tev(l * 8 + 1)});
+        const double pf = b1_prefetch_step(l, copy);  // fills the link while layer l+1 is routed
+        h2d_bytes += pf;  // counted in the step's link bytes (wasted when the expert goes unrouted)
+      }
+      if (cfg.shared_inter > 0) {
+        // always-on shared expert (config 4): x += SwiGLU_shared(xn2); its
+        // weights are resident, so it runs before the wait for streamed experts
+        smo_gemm_args gs{};
+        gs.x = xnj;
+        gs.rows = m.Tj;
+        gs.K = h;
+        gs.N = cfg.shared_inter;
+        gs.groups = 1;
+        gs.max_rows_per_group = m.Tj;
+        gs.w = ly.ws1;
+        gs.w_up = ly.ws3;
+        gs.w_pool_blocks = 1;
+        gs.epilogue = SMO_EPI_SWIGLU;
+        gs.out = hs + size_t(m.R0) * cfg.shared_inter;
+        gs.ldo = cfg.shared_inter;
+        gemm_launch(gs, st);
+        gs = smo_gemm_args{};
+        gs.x = hs + size_t(m.R0) * cfg.shared_inter;
+        gs.rows = m.Tj;
+        gs.K = cfg.shared_inter;
+        gs.N = h;
+        gs.groups = 1;
+        gs.max_rows_per_group = m.Tj;
+        gs.w = ly.ws2;
+        gs.w_pool_blocks = 1;
+        gs.epilogue = SMO_EPI_F32_ADD;
+        gs.out = xj;
+        gs.ldo = h;
+        gs.workspace = gemm_ws;
+        gs.workspace_bytes = gemm_ws_bytes;
+        gemm_launch(gs, st);
+      }
+      SMO_CUDA_CHECK(cudaEventRecord(mev(l, j, 7), st));
     }
-    if (!moe_end_recorded) SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 5), st));
-    moe_ev.push_back({tev(l * 8 + 4), tev(l * 8 + 5)});
+    // ---- GPU_MOE: every micro-batch waits on this layer's expert transfer
+    for (int j = 0; j < M; ++j) {
+      const Mb& m = mbs[size_t(j)];
+      if (ep_on) {
+        moe_ep(l, T, st);
+        SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 5), st));
+      } else {
+        if (j == 0) {
+          SMO_CUDA_CHECK(cudaStreamWaitEvent(st, slot_ready[l % slots], 0));
+          decode_slot(l, st);  // coded expert blocks -> bf16 slot (compress_experts)
+        }
+        SMO_CUDA_CHECK(cudaEventRecord(mev(l, j, 4), st));
+        const size_t p0 = size_t(m.R0) * K;
+        const int PTj = m.Tj * K;
+        const int32_t* offj = offsets + size_t(j) * (E + 1);
+        float* yj = ybuf + size_t(moe_splits) * p0 * h;  // this micro-batch's [splits][PTj][h] region
+        if (moe_fused) {
+          moe_launch(xp + p0 * h, PTj, h, hi, E, offj, pool, blk_bytes, pool_blocks, d_w_index + size_t(l) * E,
+                     hbuf + p0 * hi, yj, moe_splits, moe_splits, d_done, st);
+          // GPU_MOE = the expert kernel itself (the bench's kernel roofline)
+          SMO_CUDA_CHECK(cudaEventRecord(mev(l, j, 5), st));
+          if (j == M - 1) SMO_CUDA_CHECK(cudaEventRecord(slot_free[l % slots], st));
+          unpermute_combine(yj, pos + p0, rw + p0, m.Tj, K, h, x + size_t(m.R0) * h, st, moe_splits,
+                            size_t(PTj) * h);
+        } else {
+          smo_gemm_args g{};
+          g.x = xp + p0 * h;
+          g.rows = PTj;
+          g.K = h;
+          g.N = hi;
+          g.groups = E;
+          g.row_offsets = offj;
+          g.max_rows_per_group = m.Tj;  // a token selects an expert at most once
+          g.w = pool;
+          g.w_up = pool + size_t(hi) * h;
+          g.w_block_stride = blk_bytes;
+          g.w_pool_blocks = pool_blocks;
+          g.w_index = d_w_index + size_t(l) * E;
+          g.epilogue = SMO_EPI_SWIGLU;
+          g.out = hbuf + p0 * hi;
+          g.ldo = hi;
+          gemm_launch(g, st);
+          g = smo_gemm_args{};
+          g.x = hbuf + p0 * hi;
+          g.rows = PTj;
+          g.K = hi;
+          g.N = h;
+          g.groups = E;
+          g.row_offsets = offj;
+          g.max_rows_per_group = m.Tj;
+          g.w = pool + 2 * size_t(hi) * h;
+          g.w_block_stride = blk_bytes;
+          g.w_pool_blocks = pool_blocks;
+          g.w_index = d_w_index + size_t(l) * E;
+          g.epilogue = SMO_EPI_F32;
+          g.out = yj;
+          g.ldo = h;
+          gemm_launch(g, st);
+          if (j == M - 1) SMO_CUDA_CHECK(cudaEventRecord(slot_free[l % slots], st));
+          unpermute_combine(yj, pos + p0, rw + p0, m.Tj, K, h, x + size_t(m.R0) * h, st);
+          SMO_CUDA_CHECK(cudaEventRecord(mev(l, j, 5), st));
+        }
+      }
+      moe_ev.push_back({mev(l, j, 4), mev(l, j, 5)});
+    }
     snap("x_out", l, x, size_t(T) * h * 4, st);
     if (!batch_one && l + slots < L) {
       const int ln = l + slots;
@@ -1095,19 +1159,139 @@ void Engine::verify_core(int b, int n, const int32_t* tokens, const int32_t* par
   b1_measured = batch_one;
 }
 
-// Per layer: [h2d_start, h2d_end, attn_start, attn_end, moe_start, moe_end,
-// layer_start, pre_moe] in seconds from the step's start event.
+// Per layer (c_api.h smo_engine_layer_times): [h2d_start, h2d_end, bytes,
+// raw bytes] + per micro-batch [o1_start, attn_start, attn_end, pre_moe,
+// moe_start, moe_end], seconds from the step's start event.
 void Engine::layer_times(double* out, size_t n) {
-  SMO_REQUIRE(n >= size_t(L) * 9, "layer_times: output too small");
+  const int M = last_mb;
+  const size_t stride = 4 + 6 * size_t(M);
+  SMO_REQUIRE(n >= size_t(L) * stride, "layer_times: output too small");
   SMO_CUDA_CHECK(cudaDeviceSynchronize());
+  auto at = [&](cudaEvent_t e) {
+    float ms = 0;
+    SMO_CUDA_CHECK(cudaEventElapsedTime(&ms, ev[0], e));
+    return double(ms) * 1e-3;
+  };
   for (int l = 0; l < L; ++l) {
-    for (int k = 0; k < 8; ++k) {
-      float ms = 0;
-      SMO_CUDA_CHECK(cudaEventElapsedTime(&ms, ev[0], ev[8 + size_t(l) * 8 + k]));
-      out[size_t(l) * 9 + k] = ms * 1e-3;
+    double* o = out + size_t(l) * stride;
+    o[0] = at(tev(l * 8 + 0));
+    o[1] = at(tev(l * 8 + 1));
+    o[2] = layer_bytes[size_t(l)];
+    o[3] = layer_raw_bytes[size_t(l)];
+    for (int j = 0; j < M; ++j) {
+      const int ks[6] = {6, 2, 3, 7, 4, 5};
+      for (int q = 0; q < 6; ++q) o[4 + 6 * j + q] = at(mev(l, j, ks[q]));
     }
-    out[size_t(l) * 9 + 8] = layer_bytes[size_t(l)];
   }
+}
+
+namespace {
+// the compute stream waits here until the host dispatcher has published
+// job `seq` done (the host attention of one micro-batch)
+__global__ void host_flag_wait_kernel(const uint32_t* flag, uint32_t seq) {
+  uint32_t v;
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (int32_t(v - seq) >= 0) break;
+    __nanosleep(2000);
+  }
+}
+// job `seq`'s inputs (written by the preceding kernels) are complete
+__global__ void host_flag_set_kernel(uint32_t* flag, uint32_t seq) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(seq) : "memory");
+}
+}  // namespace
+
+// zero-copy read of pinned mapped host memory by the SMs (16-byte loads)
+__global__ void copy_from_mapped_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, size_t n16) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n16; i += size_t(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+
+void Engine::copy_from_mapped(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  SMO_REQUIRE(bytes % 16 == 0 && (uintptr_t(dst) & 15) == 0 && (uintptr_t(src) & 15) == 0,
+              "copy_from_mapped: 16-byte aligned sizes");
+  const size_t n16 = bytes / 16;
+  const unsigned grid = unsigned(std::min<size_t>((n16 + 255) / 256, 296));
+  copy_from_mapped_kernel<<<std::max(1u, grid), 256, 0, st>>>(reinterpret_cast<uint4*>(dst),
+                                                               reinterpret_cast<const uint4*>(src), n16);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+void Engine::wait_host_flag(uint32_t seq, cudaStream_t st) {
+  host_flag_wait_kernel<<<1, 1, 0, st>>>(host_flags + 1, seq);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+void Engine::signal_host_ready(uint32_t seq, cudaStream_t st) {
+  host_flag_set_kernel<<<1, 1, 0, st>>>(host_flags, seq);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+}
+
+void Engine::set_micro_batches(int m) {
+  SMO_REQUIRE(m >= 0 && m <= kMaxMb, "engine: micro_batches must be in [0, 8]");
+  if (m > 1) {
+    SMO_REQUIRE(!batch_one, "engine: micro-batching needs MoeBatching::LARGE_BATCH");
+    SMO_REQUIRE(!ep_on, "engine: micro-batching is not available with expert parallelism");
+  }
+  mb = std::max(1, m);
+}
+
+void Engine::AsyncHost::start(volatile uint32_t* ready, volatile uint32_t* done) {
+  ready_flag = ready;
+  done_flag = done;
+  th = std::thread([this] {
+    for (;;) {
+      Item it{};
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return stop || head < q.size(); });
+        if (head >= q.size()) return;  // stopping with nothing queued
+        it = q[head++];
+        if (head == q.size()) {
+          q.clear();
+          head = 0;
+        }
+      }
+      // wait until the GPU has written this job's inputs (queued jobs are
+      // finished even when stopping: the stream waits on their results; only
+      // a stream that stopped making progress is abandoned, after 30 s)
+      const auto t0 = std::chrono::steady_clock::now();
+      for (int spins = 0; int32_t(*ready_flag - it.seq) < 0; ++spins) {
+        if (spins > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+        if ((spins & 1023) == 1023) {
+          std::lock_guard<std::mutex> lk(mu);
+          if (stop && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30)) return;
+        }
+      }
+      std::atomic_thread_fence(std::memory_order_acquire);
+      cpu_verify_attention(it.job, *it.pool);
+      std::atomic_thread_fence(std::memory_order_seq_cst);
+      *done_flag = it.seq;  // publish (mapped pinned memory; the GPU polls it)
+    }
+  });
+}
+
+void Engine::AsyncHost::push(const Item& it) {
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    q.push_back(it);
+  }
+  cv.notify_one();
+}
+
+void Engine::AsyncHost::shutdown() {
+  if (!th.joinable()) return;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    stop = true;
+  }
+  cv.notify_one();
+  th.join();
 }
 
 void Engine::times(smo_stage_times* t) {
@@ -1247,6 +1431,20 @@ smo_status smo_engine_layer_times(smo_engine* e, double* out, size_t n) {
   return smo::run_guarded([&] {
     SMO_REQUIRE(e && out, "engine: null argument");
     e->impl.layer_times(out, n);
+  });
+}
+
+smo_status smo_engine_set_micro_batches(smo_engine* e, int32_t m) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(e, "engine: null argument");
+    e->impl.set_micro_batches(m);
+  });
+}
+
+smo_status smo_engine_last_micro_batches(smo_engine* e, int32_t* m) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(e && m, "engine: null argument");
+    *m = e->impl.last_mb;
   });
 }
 

@@ -3,13 +3,17 @@
 // blocks, drafter, decode loop; prefill.cu: layer-major prefill).
 #pragma once
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <functional>
+#include <condition_variable>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <thread>
 #include <string>
 #include <vector>
@@ -147,7 +151,41 @@ struct Engine {
     CpuPool* pool;
     CpuAttnJob job;
   };
-  std::vector<HostAttn> host_jobs;        // one per target layer (enqueued ahead of execution)
+  std::vector<HostAttn> host_jobs;        // [L][kMaxMb] (enqueued ahead of execution)
+  // Asynchronous host attention (verify steps outside graph capture): the
+  // GPU publishes "job seq's q rows are written" in pinned mapped memory
+  // (ready_flag); a dispatcher thread takes the jobs in order, waits for
+  // that, runs the job on the pool, then publishes "job seq done"
+  // (done_flag); the compute stream only waits for done right before the
+  // job's output is consumed (wait_host_flag), so the GPU keeps running the
+  // other micro-batches' stages while the host attends (no stream-blocking
+  // host function). Jobs are queued by value with monotonically increasing
+  // sequence numbers, so steps may be issued ahead without reusing state.
+  struct AsyncHost {
+    struct Item {
+      CpuAttnJob job;
+      CpuPool* pool;
+      uint32_t seq;
+    };
+    std::thread th;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::vector<Item> q;
+    size_t head = 0;
+    bool stop = false;
+    volatile uint32_t* ready_flag = nullptr;  // written by the GPU
+    volatile uint32_t* done_flag = nullptr;   // written by the dispatcher
+    void start(volatile uint32_t* ready, volatile uint32_t* done);
+    void push(const Item& it);
+    void shutdown();
+    ~AsyncHost() { shutdown(); }
+  };
+  AsyncHost async_host;
+  uint32_t* host_flags = nullptr;  // pinned mapped [2]: GPU-ready seq, host-done seq
+  uint32_t host_seq = 0;           // last enqueued host job
+  void signal_host_ready(uint32_t seq, cudaStream_t st);
+  void copy_from_mapped(void* dst, const void* src, size_t bytes, cudaStream_t st);
+  void wait_host_flag(uint32_t seq, cudaStream_t st);
   // BATCH_ONE expert streaming: stream only router-selected experts
   bool batch_one = false;
   int32_t* h_offsets = nullptr;           // pinned [E+1] routed offsets of the current layer
@@ -233,6 +271,7 @@ struct Engine {
   std::map<std::string, std::vector<DevBuf>> dbg;
 
   ~Engine() {
+    async_host.shutdown();  // before the pool and the host buffers it uses go away
     for (auto e : slot_ready) cudaEventDestroy(e);
     for (auto e : slot_free) cudaEventDestroy(e);
     for (auto e : ev) cudaEventDestroy(e);
@@ -422,8 +461,17 @@ struct Engine {
 
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending_attn, pending_moe, pending_h2d;
 
-  // Per layer: [h2d_start, h2d_end, attn_start, attn_end, moe_start, moe_end,
-  // layer_start, pre_moe] in seconds from the step's start event.
+  // micro-batching (Hyperparameters.m, pipeline.hpp:147-206)
+  static constexpr int kMaxMb = 8;
+  int mb = 1;       // micro-batches of the next steps
+  int last_mb = 1;  // of the last step (layer_times layout)
+  // timing event k of micro-batch j of layer l (j = 0: the per-layer events tev)
+  cudaEvent_t mev(int l, int j, int k) const {
+    return j == 0 ? tev(l * 8 + k) : ev[8 + size_t(L) * 8 + (size_t(l) * (kMaxMb - 1) + size_t(j - 1)) * 8 + k];
+  }
+  void set_micro_batches(int m);
+
+    // Per layer (4 + 6 * last_mb doubles, c_api.h smo_engine_layer_times).
   void layer_times(double* out, size_t n);
 
   void times(smo_stage_times* t);

@@ -490,30 +490,33 @@ __global__ void __launch_bounds__(32 * kUDecWarps, 28) unary_decode_kernel(const
       __syncwarp();
       p0 = st[lane];
     }
-    // walk the lane's 32 codes: window from shared memory (MIO pipe), one
-    // count-leading-ones per code, code lengths packed per byte with IMAD
-    // (FMA pipe) — the integer ALU pipe is this kernel's limiter
+    // walk the lane's 32 codes two at a time in a 64-bit window (hi:lo) read
+    // from bit `off` < 32: two codes of <= 16 bits each fit the window, so a
+    // pair needs no bounds check; after each pair one branch-free refill
+    // (SEL) shifts a word in when 32 bits were consumed. Per code: one
+    // 64-bit funnel shift, one find-leading-one of the complement, one add
+    // (the code length is 32 - f for the window's highest zero at f).
     uint32_t j4[8];
     {
-      // two-word register window; a lane loads the next word only when its
-      // codes cross into it (~2 of 32 values), so shared-memory wavefronts
-      // stay few and bank conflicts rare
       const uint32_t* wp = wb + (p0 >> 5);
-      uint32_t a = wp[0], b = wp[1];
+      uint32_t hi = wp[0], lo = wp[1];
       wp += 2;
       int off = p0 & 31;
-      // f = index of the window's highest zero = 31 - j (16 <= f <= 31):
-      // the code is f-complement long, so off advances by 32 - f
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int f = 31 - __clz(~__funnelshift_l(b, a, off));  // FLO: every code fits the window
-        off += 32 - f;
-        if (off >= 32) {
-          off -= 32;
-          a = b;
-          b = *wp++;
-        }
-        j4[i / 4] = (i % 4 == 0) ? uint32_t(f) : uint32_t(f) * (1u << (8 * (i % 4))) + j4[i / 4];
+      for (int i = 0; i < 32; i += 2) {
+        const uint64_t win = (uint64_t(hi) << 32) | lo;
+        const int f1 = 31 - __clz(~uint32_t((win << off) >> 32));
+        const int off2 = off + 32 - f1;  // < 48
+        const int f2 = 31 - __clz(~uint32_t((win << off2) >> 32));
+        off = off2 + 32 - f2;            // < 64
+        const uint32_t nxt = *wp;
+        const bool ge = off >= 32;
+        hi = ge ? lo : hi;
+        lo = ge ? nxt : lo;
+        wp += ge ? 1 : 0;
+        off -= ge ? 32 : 0;
+        const uint32_t pair = uint32_t(f1) | (uint32_t(f2) << 8);
+        j4[i / 4] = (i % 4 == 0) ? pair : j4[i / 4] | (pair << 16);
       }
     }
     // e = base - j = f - (31 - base)
@@ -553,18 +556,19 @@ __global__ void __launch_bounds__(32 * kUDecWarps, 28) unary_decode_kernel(const
         }
       }
     }
-    // 32 values -> 64 bytes: two values per word, lo bytes and exponents
-    // spread to 16-bit lanes with PRMT (lo loaded late: fewer live registers)
+    // 32 values -> 64 bytes: two values per word. PRMT spreads two lo bytes
+    // (sign << 7 | mantissa) to 16-bit lanes with the sign replicated into
+    // the high byte (selector nibbles 8-B), a second PRMT the two exponents;
+    // one LOP3 merges sign, exponent << 7 and mantissa.
     const uint4 lo0 = reinterpret_cast<const uint4*>(sb)[2 * lane];  // this lane's 32 lo bytes
     const uint4 lo1 = reinterpret_cast<const uint4*>(sb)[2 * lane + 1];
     const uint32_t lw[8] = {lo0.x, lo0.y, lo0.z, lo0.w, lo1.x, lo1.y, lo1.z, lo1.w};
     uint32_t out[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
-      const uint32_t sel = (k & 1) ? 0x4342u : 0x4140u;
-      const uint32_t l16 = __byte_perm(lw[k / 2], 0u, sel), x16 = __byte_perm(e4[k / 2], 0u, sel);
-      // disjoint fields: sign * 2^8 + mantissa + exponent * 2^7, as IMADs
-      out[k] = (l16 & 0x00800080u) * 256u + (l16 & 0x007f007fu) + x16 * 128u;
+      const uint32_t t = __byte_perm(lw[k / 2], 0u, (k & 1) ? 0xB3A2u : 0x9180u);
+      const uint32_t x16 = __byte_perm(e4[k / 2], 0u, (k & 1) ? 0x4342u : 0x4140u);
+      out[k] = (t & 0x807F807Fu) | (x16 << 7);
     }
     // through shared memory (the stream buffer is free now) so every global
     // store instruction writes 512 contiguous bytes

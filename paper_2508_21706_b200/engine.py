@@ -172,7 +172,8 @@ class VerifyEngine:
     def __init__(self, shape: ModelShape, *, max_batch: int, max_verify: int, max_seq: int, hbm_slots: int = 2,
                  expert_cache_bytes: int = 0, host_alias_layers: int = 0, device: int = 0, debug: bool = False,
                  ep_rank: int = 0, ep_size: int = 1, ep_group: Optional["EpGroup"] = None, kv_pages: int = 0,
-                 attn_cpu: bool = False, batch_one: bool = False, compress_experts: bool = False):
+                 attn_cpu: bool = False, batch_one: bool = False, compress_experts: bool = False,
+                 micro_batches: int = 1):
         self.shape = shape
         self.max_batch, self.max_verify, self.max_seq = max_batch, max_verify, max_seq
         if ep_size > 1 and ep_group is None:
@@ -183,7 +184,7 @@ class VerifyEngine:
         opt = L.EngineOptions(max_batch, max_verify, max_seq, hbm_slots, int(expert_cache_bytes),
                               host_alias_layers, device, L.ENGINE_DEBUG if debug else 0, ep_rank, ep_size,
                               None if ep_group is None else ep_group.handle, kv_pages, int(attn_cpu),
-                              int(batch_one), int(compress_experts))
+                              int(batch_one), int(compress_experts), int(micro_batches))
         cfg = shape.to_c()
         h = C.c_void_p()
         L.check(L.load().smo_engine_create(C.byref(cfg), C.byref(opt), C.byref(h)))
@@ -199,6 +200,20 @@ class VerifyEngine:
             self.close()
         except Exception:
             pass
+
+    def set_micro_batches(self, m: int) -> None:
+        """Hyperparameters.m for the next steps (stage-major micro-batches)."""
+        L.check(L.load().smo_engine_set_micro_batches(self._h, int(m)))
+
+    def layer_times(self):
+        """Measured per-layer timeline of the last step: (m, array [L, 4 + 6m])
+        (c_api.h smo_engine_layer_times)."""
+        lib = L.load()
+        m = C.c_int32(0)
+        L.check(lib.smo_engine_last_micro_batches(self._h, C.byref(m)))
+        out = np.zeros((self.shape.n_layers, 4 + 6 * m.value))
+        L.check(lib.smo_engine_layer_times(self._h, out.ctypes.data_as(C.c_void_p), out.size))
+        return m.value, out
 
     def fill_prefix(self, prefix_len) -> None:
         p = np.ascontiguousarray(prefix_len, np.int32)

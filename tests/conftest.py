@@ -10,6 +10,7 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and libspecmoe.so")
+    config.addinivalue_line("markers", "sanitizer: compute-sanitizer tier (also gpu)")
 
 
 @pytest.fixture(scope="session")

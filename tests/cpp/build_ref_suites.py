@@ -65,7 +65,7 @@ if __name__ == "__main__":
 
 
 OWN_GPU_SUITES = ["test_verify_engine"]
-OWN_CPU_SUITES = ["test_profile_csv"]
+OWN_CPU_SUITES = ["test_profile_csv", "test_plan_memory"]
 
 
 def build_own() -> list[str]:

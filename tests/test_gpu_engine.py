@@ -27,10 +27,12 @@ def _shape(kind="tiny", seed=0x5EED + 1):
     s = dataclasses.replace(TINY, seed=seed, lm_scale=8.0, router_scale=4.0)
     if kind == "tiny_fg":  # config-4 features at tiny size: 16 experts top-4 + shared expert
         s = dataclasses.replace(s, n_expert=16, top_k=4, shared_inter=512)
+    if kind == "tiny_gauss":  # trained-like gaussian expert weights (smo_fill_normal_bf16)
+        s = dataclasses.replace(s, expert_init=1)
     return s
 
 
-@pytest.fixture(scope="module", params=["tiny", "tiny_fg"])
+@pytest.fixture(scope="module", params=["tiny", "tiny_fg", "tiny_gauss"])
 def setup(cuda, request):
     from paper_2508_21706_b200.engine import VerifyEngine
     import oracle_model
@@ -333,3 +335,67 @@ def test_coded_hot_cache_bit_identical(cuda, batch_one, monkeypatch):
         assert np.array_equal(a.acc_len, c.acc_len) and np.array_equal(a.bonus, c.bonus)
     assert t1["h2d_bytes"] < t0["h2d_bytes"]  # ~7-8 coded blocks cached instead of 5 bf16 ones
     assert t1["codec_bytes"] > 0
+
+
+def test_gaussian_experts_coded_stream_bit_identical(cuda):
+    """Trained-like gaussian expert weights (--init gaussian): the unary link
+    code still round-trips bit for bit through the engine, at more bits per
+    weight than uniform-init blocks (the exponent distribution is wider)."""
+    from paper_2508_21706_b200.engine import VerifyEngine
+    s = dataclasses.replace(_shape(), expert_init=1)
+    b, n = 4, 5
+    prefix = np.array([300, 17, 64, 1], np.int32)
+    tokens = np.random.default_rng(12).integers(0, s.vocab, size=(b, n)).astype(np.int32)
+    out = {}
+    for comp in (False, True):
+        eng = VerifyEngine(s, max_batch=b, max_verify=n, max_seq=512, compress_experts=comp, debug=True)
+        eng.fill_prefix(prefix)
+        r = eng.verify(tokens, prefix)
+        out[comp] = (r, eng.last_times(), eng.debug_tensor("x_out", s.n_layers - 1, (b * n, s.hidden), np.float32))
+        eng.close()
+    (r0, t0, x0), (r1, t1, x1) = out[False], out[True]
+    assert np.array_equal(x0.view(np.uint32), x1.view(np.uint32))
+    assert np.array_equal(r0.target, r1.target)
+    bpw = 16.0 * t1["h2d_bytes"] / t1["h2d_raw_bytes"]
+    assert 10.4 < bpw < 12.5, bpw
+
+
+@pytest.mark.parametrize("attn_cpu", [False, True])
+def test_micro_batches_match_one_batch(cuda, attn_cpu):
+    """Hyperparameters.m (pipeline.hpp:147-206): the batch as m micro-batches
+    issued stage-major gives the same greedy results as m = 1 (margins are
+    wide at lm_scale 8) and residuals within fp32 reordering noise; the host
+    attention of the CPU placement runs asynchronously (dispatcher thread +
+    device-side wait) while the GPU runs the next micro-batch. Several steps
+    are issued back to back without host synchronisation."""
+    import torch
+    from paper_2508_21706_b200.engine import VerifyEngine
+    s = _shape()
+    b, n = 4, 5
+    prefix = np.array([300, 17, 64, 1], np.int32)
+    rng = np.random.default_rng(31)
+    toks = [rng.integers(0, s.vocab, size=(b, n)).astype(np.int32) for _ in range(3)]
+    res = {}
+    for m in (1, 2, 3):
+        eng = VerifyEngine(s, max_batch=b, max_verify=n, max_seq=512, debug=True, attn_cpu=attn_cpu, micro_batches=m)
+        eng.fill_prefix(prefix)
+        stream = torch.cuda.Stream()
+        dev_tok = [torch.from_numpy(t).cuda() for t in toks]
+        pre = torch.from_numpy(prefix).cuda()
+        accs = [torch.zeros(b, dtype=torch.int32, device="cuda") for _ in toks]
+        bons = [torch.zeros(b, dtype=torch.int32, device="cuda") for _ in toks]
+        tgts = [torch.zeros(b * n, dtype=torch.int32, device="cuda") for _ in toks]
+        for t, a, bo, tg in zip(dev_tok, accs, bons, tgts):  # issued back to back
+            eng.verify_device(t, pre, a, bo, target=tg, stream=stream.cuda_stream)
+        stream.synchronize()
+        x = eng.debug_tensor("x_out", s.n_layers - 1, (b * n, s.hidden), np.float32)
+        mm, lt = eng.layer_times()
+        assert mm == m and lt.shape == (s.n_layers, 4 + 6 * m)
+        res[m] = ([a.cpu().numpy() for a in accs], [t.cpu().numpy() for t in tgts], x)
+        eng.close()
+    for m in (2, 3):
+        for i in range(len(toks)):
+            assert np.array_equal(res[m][1][i], res[1][1][i]), (m, i)
+            assert np.array_equal(res[m][0][i], res[1][0][i])
+        x1, xm = res[1][2], res[m][2]
+        assert np.sqrt(np.mean((x1 - xm) ** 2) / np.mean(x1 ** 2)) < 1e-3

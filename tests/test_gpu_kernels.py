@@ -426,6 +426,18 @@ def test_fill_uniform_matches_oracle(cuda, oracle):
     assert np.array_equal(_u16(t), ref)
 
 
+def test_fill_normal_matches_oracle(cuda, oracle):
+    """Gaussian-like procedural init (smo_fill_normal_bf16) is integer-exact:
+    bit-identical to the oracle's orc_fill_normal_bf16; std = scale/sqrt(3)."""
+    import torch
+    from paper_2508_21706_b200 import ops
+    t = torch.empty(1 << 20, dtype=torch.bfloat16, device=cuda)
+    ops.fill_normal_(t, 0x5EED, 777, 0.027, base=5)
+    ref = oracle.fill_normal_bf16(t.numel(), 0x5EED, 777, 0.027, base=5)
+    assert np.array_equal(_u16(t), ref)
+    assert abs(t.float().std().item() - 0.027 / math.sqrt(3)) < 0.03 * 0.027
+
+
 @pytest.mark.parametrize("b,n,nq,nkv,d,prefix", [
     (3, 5, 32, 8, 128, [1024, 131, 7]),     # verify shape, ragged
     (4, 32, 8, 2, 64, [0, 32, 300, 96]),    # prefill chunks

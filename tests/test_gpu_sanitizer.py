@@ -1,0 +1,34 @@
+"""GPU sanitizer tier: compute-sanitizer memcheck, racecheck
+and synccheck over the tiny workloads of tests/sanitize_cases.py — K1's
+split-KV merge, K4-MoE's cross-CTA release/acquire and cooperative launch,
+the unary codec, the verify DAG (2 micro-batches, raw and coded transfer)
+and the expert-parallel loopback exchange. Pass = the tool's ERROR SUMMARY
+reports 0 errors and the workload itself succeeded."""
+import os
+import re
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.sanitizer]
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SAN = "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.parametrize("tool,case", [("memcheck", "kernels"), ("memcheck", "verify"), ("memcheck", "ep"),
+                                       ("racecheck", "kernels"), ("synccheck", "kernels"),
+                                       ("synccheck", "verify")])
+def test_compute_sanitizer_clean(cuda, tool, case):
+    assert os.path.exists(SAN), "compute-sanitizer missing"
+    cmd = [SAN, "--tool", tool, "--error-exitcode", "3", "--print-limit", "20"]
+    if tool == "memcheck":
+        cmd += ["--leak-check", "no"]
+    cmd += [sys.executable, os.path.join(ROOT, "tests", "sanitize_cases.py"), case]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    out = r.stdout + r.stderr
+    m = re.search(r"ERROR SUMMARY: (\d+) error", out)
+    assert m, out[-4000:]
+    assert m.group(1) == "0" and r.returncode == 0, out[-4000:]
+    assert "case ok" in out, out[-4000:]

@@ -80,6 +80,18 @@ def test_cpp_verify_engine_planner_loop(cuda):
     assert r.returncode == 0 and m and m.group(3) == "0", r.stdout + r.stderr
 
 
+def test_cpp_plan_memory_engine_terms():
+    """CPU: the additive plan_memory overload charges GPU_RESIDENT target K/V
+    and the expert streamer's HBM slots; the reference's
+    own plan_memory is unchanged (its suite above still passes)."""
+    B.build_own()
+    path = os.path.join(B.OUT, "test_plan_memory")
+    assert os.path.exists(path), "build/refsuites/test_plan_memory missing"
+    r = subprocess.run([path], capture_output=True, text=True, timeout=300, cwd=os.path.dirname(path))
+    m = SUMMARY.search(r.stdout)
+    assert r.returncode == 0 and m and m.group(3) == "0", r.stdout + r.stderr
+
+
 def test_cpp_profile_csv_ingest():
     """CPU: ProfileSample CSV write/read (the ingest SPEC.md:592 promises) round
     trips exactly and fits the same LatencyModel."""

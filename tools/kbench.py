@@ -40,13 +40,27 @@ def attn(b, n, s, nq=32, nkv=8, d=128, tree=False):
     q = (torch.rand((b * n, nq, d), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
     kc = (torch.rand((b, nkv, s_max, d), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
     vc = (torch.rand((b, nkv, s_max, d), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
-    bits = [(1 << (i + 1)) - 1 for i in range(n)] * b
+    if tree:  # random draft tree per request: ancestor-or-self masks (attention.hpp:41-71)
+        import numpy as np
+        rng = np.random.default_rng(b * 1000 + n)
+        bits = []
+        for _ in range(b):
+            par = [-1] + [int(rng.integers(0, i)) for i in range(1, n)]
+            for i in range(n):
+                m, cur = 0, i
+                while cur >= 0:
+                    m |= 1 << cur
+                    cur = par[cur] if cur > 0 else -1
+                bits.append(m)
+    else:
+        bits = [(1 << (i + 1)) - 1 for i in range(n)] * b
     mask = torch.tensor(bits, dtype=torch.int64, device=dev)
     pre = torch.full((b,), s, dtype=torch.int32, device=dev)
     out = torch.empty_like(q)
     t = timeit(lambda: ops.verify_attention(q, kc, vc, mask, pre, s, out=out))
     byts = 2 * b * (s + n) * nkv * d * 2 + 2 * q.numel() * 2
-    return {"kernel": "K1 verify_attention", "b": b, "n": n, "s": s, "us": t * 1e6, "GBs": byts / t / 1e9,
+    return {"kernel": "K1 verify_attention", "b": b, "n": n, "s": s, "mask": "tree" if tree else "chain",
+            "us": t * 1e6, "GBs": byts / t / 1e9,
             "frac": byts / t / 1e9 / PEAK, "TFLOPs": 4 * b * n * (s + n) * nq * d / t / 1e12}
 
 
@@ -97,10 +111,11 @@ def moe(T=288, h=4096, hi=14336, E=8, k=2, split=0):
     return r
 
 
-def codec(n=3 * 4096 * 14336, bits=3):
-    """K5 codec on one Mixtral expert block: decode reads the code, writes bf16."""
-    g = torch.Generator(device=dev).manual_seed(4)
-    x = ((torch.rand((n,), generator=g, device=dev) * 2 - 1) * 0.027).to(torch.bfloat16)
+def codec(n=3 * 4096 * 14336, bits=3, dist="uniform"):
+    """K5 codec on one Mixtral expert block: decode reads the code, writes bf16.
+    dist: uniform (the engine's procedural init) or gaussian (trained-like)."""
+    x = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    (ops.fill_normal_ if dist == "gaussian" else ops.fill_uniform_)(x, 0x5EED, 1100, math.sqrt(3.0 / 4096))
     code, ovf = ops.expert_encode(x, bits)
     assert not ovf
     out = torch.empty_like(x)
@@ -109,7 +124,7 @@ def codec(n=3 * 4096 * 14336, bits=3):
     assert torch.equal(out.view(torch.int16), x.view(torch.int16))
     byts = code.numel() + 2 * n
     name = "unary" if bits == 1 else f"{bits}-bit"
-    return {"kernel": f"K5 expert_decode ({name})", "N": n, "bits_per_weight": code.numel() * 8 / n,
+    return {"kernel": f"K5 expert_decode ({name})", "dist": dist, "N": n, "bits_per_weight": code.numel() * 8 / n,
             "us": t * 1e6, "GBs": byts / t / 1e9, "frac": byts / t / 1e9 / PEAK, "TFLOPs": 0.0}
 
 
@@ -119,16 +134,20 @@ def main():
     if what in ("attn", "all"):
         res.append(attn(32, 9, 1024))
         res.append(attn(32, 5, 1024))
-        if "--sweep" in sys.argv:
-            for s in (1024, 4096, 16384, 32768):
-                for n in (1, 4, 8, 16):
-                    for b in (1, 16, 64):
-                        if b * n * 4 > 64 * 64 or (b * (s + n) * 8 * 128 * 4 > 20e9):
-                            continue
-                        res.append(attn(b, n, s))
+        if "--sweep" in sys.argv:  # BASELINE config 3 / SURVEY.md §8(d): the full grid, chain and tree
+            for s in (1024, 2048, 4096, 8192, 16384, 32768):
+                for n in (1, 2, 4, 8, 16):
+                    for b in (1, 4, 16, 32, 64):
+                        for tree in ((False, True) if n > 2 else (False,)):
+                            r = attn(b, n, s, tree=tree)
+                            print(json.dumps({k: (round(v, 3) if isinstance(v, float) else v) for k, v in r.items()}),
+                                  flush=True)
+                        torch.cuda.empty_cache()
+            return
     if what in ("codec", "all"):
         res.append(codec(bits=3))
         res.append(codec(bits=1))
+        res.append(codec(bits=1, dist="gaussian"))
     if what in ("gemm", "all"):
         res.append(gemm(288, 4096, 6144, name="qkv"))
         res.append(gemm(288, 4096, 4096, L.EPI_F32_ADD, name="o-proj (+residual)"))
