@@ -43,6 +43,7 @@
 // zero of the stream, so where each lane's run of 32 values starts follows
 // from a warp scan of zero counts per code word.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -405,7 +406,8 @@ __device__ __forceinline__ int select_msb(uint32_t x, int k) {
 // 32-bit window — one count-leading-ones per value, no divergence — and
 // builds its 64 output bytes in registers from its 32 lo bytes.
 constexpr int kUDecWarps = 2;
-constexpr int kURun = 3;  // code words per lane per scan round
+constexpr int kURun = 4;  // code words per lane per scan round (fast path: streams of <= 128 words)
+template <bool kDirect>
 __global__ void __launch_bounds__(32 * kUDecWarps, 28) unary_decode_kernel(const __grid_constant__ DecodeJobs jobs,
                                                                        size_t segs) {
   __shared__ __align__(16) uint32_t wbuf[kUDecWarps][kUMaxWords + 8];
@@ -535,25 +537,25 @@ __global__ void __launch_bounds__(32 * kUDecWarps, 28) unary_decode_kernel(const
         e4[q] = v;
       }
     }
-    if (has_esc) {  // rare: escaped exponents (j = 15), in position order
-      int p = p0, nesc = 0;
-      for (int i = 0; i < 32; ++i) {
-        const int j = __clz(~__funnelshift_l(wb[(p >> 5) + 1], wb[p >> 5], p & 31));
-        p += j + 1;
-        nesc += j == kUEsc;
+    if (has_esc) {  // escaped exponents (code j = 15, i.e. f = 16), in position order:
+      // the walk already holds every f, so the escapes are a byte compare
+      uint32_t emask = 0u;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t m4 = __vcmpeq4(j4[q], 0x10101010u);  // 0xff per escaped byte
+#pragma unroll
+        for (int t = 0; t < 4; ++t) emask |= ((m4 >> (8 * t + 7)) & 1u) << (4 * q + t);
       }
       int etot = 0;
-      int er = warp_excl_scan(nesc, lane, &etot);
+      int er = warp_excl_scan(__popc(emask), lane, &etot);
       const uint8_t* esc = sb + kSeg + 4 * nw;
-      p = p0;
-      for (int i = 0; i < 32 && nesc; ++i) {
-        const int j = __clz(~__funnelshift_l(wb[(p >> 5) + 1], wb[p >> 5], p & 31));
-        p += j + 1;
-        if (j == kUEsc) {
-          const int sh = 8 * (i % 4);
-          e4[i / 4] = (e4[i / 4] & ~(0xffu << sh)) | (uint32_t(esc[er++]) << sh);
-          --nesc;
-        }
+      for (uint32_t m = emask; m; m &= m - 1u) {
+        const int i = __ffs(m) - 1;
+        const int sh = 8 * (i % 4);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q == i / 4) e4[q] = (e4[q] & ~(0xffu << sh)) | (uint32_t(esc[er]) << sh);
+        ++er;
       }
     }
     // 32 values -> 64 bytes: two values per word. PRMT spreads two lo bytes
@@ -570,22 +572,31 @@ __global__ void __launch_bounds__(32 * kUDecWarps, 28) unary_decode_kernel(const
       const uint32_t x16 = __byte_perm(e4[k / 2], 0u, (k & 1) ? 0x4342u : 0x4140u);
       out[k] = (t & 0x807F807Fu) | (x16 << 7);
     }
-    // through shared memory (the stream buffer is free now) so every global
-    // store instruction writes 512 contiguous bytes
-    __syncwarp();
-    uint4* ob = reinterpret_cast<uint4*>(wb);
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      ob[4 * lane + ((k + lane) & 3)] = make_uint4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
-    __syncwarp();
     uint4* d = reinterpret_cast<uint4*>(dst + seg * kSeg);
+    if constexpr (kDirect) {
+      // straight from registers: each lane's 64 bytes are contiguous
+      // (4 x 16 B per lane at a 64 B stride per store instruction)
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int g = 32 * k + lane;  // 16-byte group g = lane' 4 + k' of lane' = g / 4
-      const int ln = g >> 2, kk = g & 3;
-      d[g] = ob[4 * ln + ((kk + ln) & 3)];
+      for (int k = 0; k < 4; ++k)
+        d[4 * lane + k] = make_uint4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
+      __syncwarp();  // wb / st are reused by the next segment
+    } else {
+      // through shared memory (the stream buffer is free now) so every global
+      // store instruction writes 512 contiguous bytes
+      __syncwarp();
+      uint4* ob = reinterpret_cast<uint4*>(wb);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        ob[4 * lane + ((k + lane) & 3)] = make_uint4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int g = 32 * k + lane;  // 16-byte group g = lane' 4 + k' of lane' = g / 4
+        const int ln = g >> 2, kk = g & 3;
+        d[g] = ob[4 * ln + ((kk + ln) & 3)];
+      }
+      __syncwarp();  // wb / st are reused by the next segment
     }
-    __syncwarp();  // wb / st are reused by the next segment
   }
 }
 
@@ -665,7 +676,12 @@ void expert_decode_blocks(const void* const* srcs, void* const* dsts, int n, siz
     const size_t want = (segs + kUDecWarps - 1) / kUDecWarps;
     const size_t cap = want;
     const dim3 ug(unsigned(std::min(want, cap)), unsigned(n));
-    unary_decode_kernel<<<ug, 32 * kUDecWarps, 0, st>>>(jobs, segs);
+    static const bool direct = [] {  // A/B switch: SMO_UNARY_DIRECT=1 stores from registers
+      const char* f = std::getenv("SMO_UNARY_DIRECT");
+      return f && f[0] == '1';
+    }();
+    if (direct) unary_decode_kernel<true><<<ug, 32 * kUDecWarps, 0, st>>>(jobs, segs);
+    else unary_decode_kernel<false><<<ug, 32 * kUDecWarps, 0, st>>>(jobs, segs);
     count_launch();
     SMO_CUDA_CHECK(cudaGetLastError());
     return;

@@ -7,7 +7,7 @@ workspace counters), K4-MoE (cross-CTA release/acquire on per-expert
 counters, cooperative launch), the K5 unary codec, router/permute/combine,
 greedy accept, and the expert-parallel loopback exchange.
 
-    python tests/sanitize_cases.py verify|kernels|ep
+    python tests/sanitize_cases.py verify|kernels|attn|moe|ep
 """
 import dataclasses
 import math
@@ -36,6 +36,11 @@ def case_verify():
 
 
 def case_kernels():
+    case_attn()
+    case_moe()
+
+
+def case_attn():
     from paper_2508_21706_b200 import ops
     dev = torch.device("cuda:0")
     g = torch.Generator(device=dev).manual_seed(3)
@@ -48,6 +53,13 @@ def case_kernels():
     mask = torch.tensor([(1 << (i + 1)) - 1 for i in range(n)], dtype=torch.int64, device=dev)
     pre = torch.tensor([p], dtype=torch.int32, device=dev)
     ops.verify_attention(q, kc, vc, mask, pre, p)
+    torch.cuda.synchronize()
+
+
+def case_moe():
+    from paper_2508_21706_b200 import ops
+    dev = torch.device("cuda:0")
+    g = torch.Generator(device=dev).manual_seed(4)
     # K4-MoE: several token tiles per expert, down split in 2
     T, E, k, h, hi = 300, 4, 2, 256, 256
     x = (torch.rand((T, h), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
@@ -97,5 +109,6 @@ def case_ep():
 
 
 if __name__ == "__main__":
-    {"verify": case_verify, "kernels": case_kernels, "ep": case_ep}[sys.argv[1]]()
+    {"verify": case_verify, "kernels": case_kernels, "attn": case_attn, "moe": case_moe,
+     "ep": case_ep}[sys.argv[1]]()
     print("case ok")
