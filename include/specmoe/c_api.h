@@ -375,10 +375,12 @@ smo_status smo_ep_loopback_create(int32_t ep_size, smo_ep_group** out);
 smo_status smo_ep_group_destroy(smo_ep_group* g);
 /* Peer-memory transport (CUDA IPC; NVLink between GPUs, or several processes
  * on one GPU): each rank owns a mailbox [2][nranks][slot_bytes] peers write
- * into directly, plus interprocess events. create returns this rank's handle
- * blob (smo_ep_ipc_handle_bytes() bytes); the caller all-gathers the blobs
- * (rank order) and connects with a host barrier callback over the same ranks
- * (called once per exchange, from the thread running smo_engine_verify).
+ * into directly, plus a flag area (per-peer round counters written with
+ * release stores and polled with acquire loads by one-thread kernels: the
+ * exchange is device-side only and CUDA-graph capturable). create returns
+ * this rank's handle blob (smo_ep_ipc_handle_bytes() bytes); the caller
+ * all-gathers the blobs (rank order) and connects with a host barrier
+ * callback over the same ranks (called once, at the end of connect).
  * slot_bytes >= the largest exchange block: max(T*k*h*2 + 16 + 4*E/P,
  * T*k*h*4) for the engine's T = max_batch * max_verify.                    */
 typedef void (*smo_barrier_fn)(void* ctx);
@@ -393,7 +395,7 @@ typedef void (*smo_barrier_fn)(void* ctx);
  * rows per destination, the same on every rank, >= T*k. workspace: device,
  * smo_ep_workspace(P,T,k,h,E,C) bytes, shared by both calls. All ranks call
  * collectively (same order); async on `stream` (host-synchronising for the
- * loopback / IPC transports' barriers). */
+ * loopback transport's barriers). */
 size_t smo_ep_workspace(int32_t P, int32_t T, int32_t k, int32_t h, int32_t E, int32_t C);
 smo_status smo_ep_dispatch(smo_ep_group* g, int32_t rank, const void* x, const int32_t* ids, int32_t T, int32_t k,
                            int32_t h, int32_t E, int32_t C, void* xl, int32_t* offsets_l, int32_t* back,

@@ -313,111 +313,156 @@ struct NcclTransport : EpTransport {
 
 // Peer-memory transport (CUDA IPC): every rank owns a mailbox [2][P][slot]
 // that the other ranks write into directly — over NVLink between GPUs, or
-// within one GPU between processes. Round e uses half e % 2: rank r stores
-// its block for p into p's mailbox slot [e%2][r] (after p has consumed the
-// round that last used that half), records its interprocess `sent` event, and
-// after a host barrier (the events' record order is then fixed) waits on
-// every peer's `sent` and reads its own mailbox. No NCCL, no spin.
+// within one GPU between processes — followed by a flag area. Round R uses
+// half R % 2: rank r stores its block for p into p's mailbox slot [R%2][r]
+// (after p has consumed round R-2, which used that half), then a one-thread
+// kernel publishes R into p's arrived[r] (release, system scope) and spins
+// until its own arrived[q] >= R for every peer q (acquire); the consumer
+// kernels then read the local mailbox, and a last one-thread kernel
+// publishes "consumed R" into every peer's consumed_by[r]. The round
+// counter lives in device memory, so the whole exchange is kernels only: no
+// host barrier per exchange, no events, capturable in a CUDA graph (an
+// iteration has an even number of exchanges, so replayed halves repeat).
 // Direct mode: the dispatch / combine kernels store into the peers'
 // mailboxes themselves (dests[half][p] = p's slot [half][r]); the staged
 // alltoall is the same protocol with copies on both sides.
+namespace {
+struct EpFlags {
+  uint32_t* arrived;      // local [P]: round whose block from rank q has landed here
+  uint32_t* consumed_by;  // local [P]: round rank q has finished reading (the blocks this rank wrote)
+  uint32_t* const* peer_arrived;      // device [P]: peer q's arrived array
+  uint32_t* const* peer_consumed_by;  // device [P]: peer q's consumed_by array
+  uint32_t* round;        // local: last completed round
+  int P, rank;
+};
+__device__ __forceinline__ uint32_t ld_acq_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rel_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void spin_geq(const uint32_t* p, uint32_t want) {
+  while (int32_t(ld_acq_sys(p) - want) < 0) __nanosleep(256);
+}
+// before writing round R = round + 1: every peer has consumed round R - 2
+__global__ void ep_flag_begin_kernel(EpFlags f) {
+  const uint32_t R = *f.round + 1;
+  if (R <= 2) return;
+  for (int q = 0; q < f.P; ++q)
+    if (q != f.rank) spin_geq(f.consumed_by + q, R - 2);
+}
+// this rank's blocks for round R are stored: tell every peer, wait for theirs
+__global__ void ep_flag_arrive_kernel(EpFlags f) {
+  const uint32_t R = *f.round + 1;
+  __threadfence_system();
+  for (int q = 0; q < f.P; ++q)
+    if (q != f.rank) st_rel_sys(f.peer_arrived[q] + f.rank, R);
+  for (int q = 0; q < f.P; ++q)
+    if (q != f.rank) spin_geq(f.arrived + q, R);
+  *f.round = R;
+}
+// round R's mailbox half has been read here: peers may overwrite it at R + 2
+__global__ void ep_flag_done_kernel(EpFlags f) {
+  const uint32_t R = *f.round;
+  __threadfence_system();
+  for (int q = 0; q < f.P; ++q)
+    if (q != f.rank) st_rel_sys(f.peer_consumed_by[q] + f.rank, R);
+}
+}  // namespace
+
 struct IpcTransport : EpTransport {
   int rank = 0;
-  size_t slot = 0;
-  uint8_t* mailbox = nullptr;
+  size_t slot = 0, data_bytes = 0;
+  uint8_t* mailbox = nullptr;   // [2][P][slot] + flags: arrived[P], consumed_by[P]
   uint8_t** d_dests = nullptr;  // device [2][P]
-  cudaEvent_t sent = nullptr, consumed = nullptr;
+  uint32_t** d_peer_flags = nullptr;  // device [2][P]: peers' arrived, then consumed_by arrays
+  uint32_t* d_round = nullptr;
   std::vector<uint8_t*> peer_mb;
-  std::vector<cudaEvent_t> peer_sent, peer_consumed;
-  smo_barrier_fn barrier = nullptr;
-  void* barrier_ctx = nullptr;
   int parity = 0;
+  EpFlags flags{};
 
   IpcTransport(int nranks, int r, size_t slot_bytes) {
     P = nranks;
     rank = r;
     slot = (slot_bytes + 255) & ~size_t(255);
-    SMO_CUDA_CHECK(cudaMalloc(&mailbox, 2 * size_t(P) * slot));
+    data_bytes = 2 * size_t(P) * slot;
+    const size_t fb = (2 * size_t(P) * sizeof(uint32_t) + 255) & ~size_t(255);
+    SMO_CUDA_CHECK(cudaMalloc(&mailbox, data_bytes + fb));
+    SMO_CUDA_CHECK(cudaMemset(mailbox + data_bytes, 0, fb));
     SMO_CUDA_CHECK(cudaMalloc(&d_dests, 2 * size_t(P) * sizeof(uint8_t*)));
-    SMO_CUDA_CHECK(cudaEventCreateWithFlags(&sent, cudaEventDisableTiming | cudaEventInterprocess));
-    SMO_CUDA_CHECK(cudaEventCreateWithFlags(&consumed, cudaEventDisableTiming | cudaEventInterprocess));
+    SMO_CUDA_CHECK(cudaMalloc(&d_peer_flags, 2 * size_t(P) * sizeof(uint32_t*)));
+    SMO_CUDA_CHECK(cudaMalloc(&d_round, sizeof(uint32_t)));
+    SMO_CUDA_CHECK(cudaMemset(d_round, 0, sizeof(uint32_t)));
+    SMO_CUDA_CHECK(cudaDeviceSynchronize());
   }
   ~IpcTransport() override {
     for (int p = 0; p < int(peer_mb.size()); ++p)
       if (p != rank && peer_mb[size_t(p)]) cudaIpcCloseMemHandle(peer_mb[size_t(p)]);
-    for (int p = 0; p < int(peer_sent.size()); ++p)
-      if (p != rank) {
-        cudaEventDestroy(peer_sent[size_t(p)]);
-        cudaEventDestroy(peer_consumed[size_t(p)]);
-      }
-    if (sent) cudaEventDestroy(sent);
-    if (consumed) cudaEventDestroy(consumed);
+    if (d_round) cudaFree(d_round);
+    if (d_peer_flags) cudaFree(d_peer_flags);
     if (d_dests) cudaFree(d_dests);
     if (mailbox) cudaFree(mailbox);
   }
-  // handle blob: mailbox memory handle, sent event, consumed event
-  static constexpr size_t kBlob = sizeof(cudaIpcMemHandle_t) + 2 * sizeof(cudaIpcEventHandle_t);
+  uint32_t* flags_of(uint8_t* mb) const { return reinterpret_cast<uint32_t*>(mb + data_bytes); }
+  // handle blob: the mailbox memory handle
+  static constexpr size_t kBlob = sizeof(cudaIpcMemHandle_t);
   void export_handles(uint8_t* out) const {
     cudaIpcMemHandle_t mh;
-    cudaIpcEventHandle_t eh;
     SMO_CUDA_CHECK(cudaIpcGetMemHandle(&mh, mailbox));
     std::memcpy(out, &mh, sizeof(mh));
-    SMO_CUDA_CHECK(cudaIpcGetEventHandle(&eh, sent));
-    std::memcpy(out + sizeof(mh), &eh, sizeof(eh));
-    SMO_CUDA_CHECK(cudaIpcGetEventHandle(&eh, consumed));
-    std::memcpy(out + sizeof(mh) + sizeof(eh), &eh, sizeof(eh));
   }
-  void connect(const uint8_t* all, smo_barrier_fn fn, void* ctx) {
-    barrier = fn;
-    barrier_ctx = ctx;
+  // `barrier` runs once, after every rank has mapped its peers (the flag
+  // areas were zeroed at creation, before the handles were exchanged)
+  void connect(const uint8_t* all, smo_barrier_fn barrier, void* ctx) {
     peer_mb.assign(size_t(P), nullptr);
-    peer_sent.assign(size_t(P), nullptr);
-    peer_consumed.assign(size_t(P), nullptr);
     for (int p = 0; p < P; ++p) {
       if (p == rank) {
         peer_mb[size_t(p)] = mailbox;
-        peer_sent[size_t(p)] = sent;
-        peer_consumed[size_t(p)] = consumed;
         continue;
       }
-      const uint8_t* b = all + size_t(p) * kBlob;
       cudaIpcMemHandle_t mh;
-      cudaIpcEventHandle_t eh;
-      std::memcpy(&mh, b, sizeof(mh));
+      std::memcpy(&mh, all + size_t(p) * kBlob, sizeof(mh));
       void* ptr = nullptr;
       SMO_CUDA_CHECK(cudaIpcOpenMemHandle(&ptr, mh, cudaIpcMemLazyEnablePeerAccess));
       peer_mb[size_t(p)] = reinterpret_cast<uint8_t*>(ptr);
-      std::memcpy(&eh, b + sizeof(mh), sizeof(eh));
-      SMO_CUDA_CHECK(cudaIpcOpenEventHandle(&peer_sent[size_t(p)], eh));
-      std::memcpy(&eh, b + sizeof(mh) + sizeof(eh), sizeof(eh));
-      SMO_CUDA_CHECK(cudaIpcOpenEventHandle(&peer_consumed[size_t(p)], eh));
     }
     std::vector<uint8_t*> dests(2 * size_t(P));
+    std::vector<uint32_t*> pf(2 * size_t(P));
     for (int half = 0; half < 2; ++half)
       for (int p = 0; p < P; ++p)
         dests[size_t(half) * P + p] = peer_mb[size_t(p)] + (size_t(half) * P + rank) * slot;
+    for (int p = 0; p < P; ++p) {
+      pf[size_t(p)] = flags_of(peer_mb[size_t(p)]);          // peer p's arrived[]
+      pf[size_t(P + p)] = flags_of(peer_mb[size_t(p)]) + P;  // peer p's consumed_by[]
+    }
     SMO_CUDA_CHECK(cudaMemcpy(d_dests, dests.data(), dests.size() * sizeof(uint8_t*), cudaMemcpyHostToDevice));
+    SMO_CUDA_CHECK(cudaMemcpy(d_peer_flags, pf.data(), pf.size() * sizeof(uint32_t*), cudaMemcpyHostToDevice));
+    flags = EpFlags{flags_of(mailbox), flags_of(mailbox) + P, d_peer_flags, d_peer_flags + P, d_round, P, rank};
+    if (barrier) barrier(ctx);
   }
   size_t direct_slot() const override { return slot; }
-  // Waiting on a peer's latest `consumed` record is enough: the barrier of the
-  // previous round orders it after the peer's read of the half reused now
-  // (a later record only makes the wait conservative).
   uint8_t* const* direct_begin(cudaStream_t st, const uint8_t** recv) override {
-    SMO_REQUIRE(barrier && !peer_mb.empty(), "ep ipc: transport not connected");
+    SMO_REQUIRE(!peer_mb.empty(), "ep ipc: transport not connected");
     const int half = parity;
     parity ^= 1;
-    for (int p = 0; p < P; ++p)
-      if (p != rank) SMO_CUDA_CHECK(cudaStreamWaitEvent(st, peer_consumed[size_t(p)], 0));
+    ep_flag_begin_kernel<<<1, 1, 0, st>>>(flags);
+    count_launch();
+    SMO_CUDA_CHECK(cudaGetLastError());
     *recv = mailbox + size_t(half) * P * slot;
     return d_dests + size_t(half) * P;
   }
   void direct_exchange(cudaStream_t st) override {
-    SMO_CUDA_CHECK(cudaEventRecord(sent, st));
-    barrier(barrier_ctx);  // every rank has recorded this round's `sent`
-    for (int p = 0; p < P; ++p)
-      if (p != rank) SMO_CUDA_CHECK(cudaStreamWaitEvent(st, peer_sent[size_t(p)], 0));
+    ep_flag_arrive_kernel<<<1, 1, 0, st>>>(flags);
+    count_launch();
+    SMO_CUDA_CHECK(cudaGetLastError());
   }
-  void direct_done(cudaStream_t st) override { SMO_CUDA_CHECK(cudaEventRecord(consumed, st)); }
+  void direct_done(cudaStream_t st) override {
+    ep_flag_done_kernel<<<1, 1, 0, st>>>(flags);
+    count_launch();
+    SMO_CUDA_CHECK(cudaGetLastError());
+  }
   void alltoall(int r, const void* send, void* recv, size_t bytes, cudaStream_t st) override {
     SMO_REQUIRE(r == rank && bytes <= slot, "ep ipc: block larger than the mailbox slot");
     const int half = parity;
