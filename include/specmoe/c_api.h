@@ -208,6 +208,26 @@ smo_status smo_expert_encode(const void* src, uint64_t count, int32_t bits, void
                              smo_stream stream);
 smo_status smo_expert_decode(const void* src, uint64_t count, int32_t bits, void* dst, smo_stream stream);
 
+/* ---- K5 tile code T2 (tcode.cuh; format restated in tests/tcode_ref.py) ----
+ * The link code the fused expert kernel decodes in shared memory: one expert
+ * block [W1 | W3 | W2] (bf16, device; W1/W3 [h_i, h], W2 [h, h_i]) in tiles of
+ * 128 x 64 (= the kernel's k-block), 2-bit level-1 exponent codes + a ranked
+ * escape stream, sign/mantissa verbatim; lossless, ~10.4 bits/weight on
+ * uniform-init and ~10.9 on gaussian-like weights. h, h_i multiples of 128.
+ * smo_tcode_max_bytes is the capacity (every segment raw); encode is
+ * synchronous on `stream` and returns the bytes used; code blocks must be
+ * 16-byte aligned.                                                          */
+size_t smo_tcode_max_bytes(int32_t h, int32_t h_i);
+smo_status smo_tcode_encode(const void* src, int32_t h, int32_t h_i, void* dst, uint64_t* bytes, smo_stream stream);
+smo_status smo_tcode_decode(const void* src, int32_t h, int32_t h_i, void* dst, smo_stream stream);
+/* K4-MoE on T2-coded experts: as smo_moe_experts, but expert e's weights are
+ * the T2 block at w_code[e] (w_code: DEVICE array of E pointers), decoded
+ * tile by tile into shared memory by the kernel itself (no bf16 copy in
+ * HBM). Bit-identical to smo_moe_experts on the decoded weights.            */
+smo_status smo_moe_experts_coded(const void* x_perm, int32_t rows, int32_t h, int32_t h_i, int32_t E,
+                                 const int32_t* offsets, const void* const* w_code, void* h_out, float* y,
+                                 int32_t splits, int32_t* splits_used, int32_t* scratch, smo_stream stream);
+
 /* ---- K5 expert streamer as a standalone handle (streamer.cu) --------------
  * The reference's H2D_EXPERTS(l) stage and the GPU_MOE(l) dependency on it
  * (pipeline.hpp:147-206; transfer bytes roofline.hpp:56-77; LARGE_BATCH vs

@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libspecmoe.so")
 SOURCES = ["c_api.cu", "ops.cu", "gemm_tc.cu", "moe_tc.cu", "attention.cu", "engine.cu", "decode.cu", "prefill.cu", "streamer.cu",
-           "ep.cu", "xfer.cu"]
+           "ep.cu", "xfer.cu", "tcode.cu"]
 CXX_SOURCES = ["cpu_attn.cpp"]  # host code (CPU attention placement), g++ with AVX2/FMA
 CXX = os.environ.get("CXX", "g++")
 CXX_FLAGS = ["-O3", "-mavx2", "-mfma", "-std=c++17", "-fPIC", "-pthread", "-I", CSRC]
@@ -31,7 +31,7 @@ def _stale(out: str, deps: list[str]) -> bool:
 def build(verbose: bool = False, jobs: int = 8) -> str:
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    headers = [os.path.join(CSRC, "common.cuh"), os.path.join(CSRC, "cpu_attn.h"), os.path.join(CSRC, "engine.cuh"),
+    headers = [os.path.join(CSRC, "common.cuh"), os.path.join(CSRC, "cpu_attn.h"), os.path.join(CSRC, "engine.cuh"), os.path.join(CSRC, "tcode.cuh"),
                os.path.join(ROOT, "include", "specmoe", "c_api.h")]
     procs, objs = [], []
     for src in SOURCES:

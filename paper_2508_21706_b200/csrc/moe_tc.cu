@@ -33,6 +33,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "tcode.cuh"
 
 namespace smo {
 
@@ -103,6 +104,89 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// Warps 2..5 of both expert kernels: per unit, wait for the accumulators,
+// then SwiGLU -> H (gate/up units; publish with a release + done[e]) or the
+// fp32 down partial -> y[ks]; hand TMEM back to the MMA warp.
+__device__ __forceinline__ void epilogue_loop(const Schedule& S, const MoeParams& p, uint32_t tmem, int warp, int lane,
+                                              uint64_t& tmem_full, uint64_t& tmem_empty) {
+  const int q = warp & 3;
+  const int row = q * 32 + lane;  // weight row within the 128-row tile
+  const uint32_t trow = tmem + (uint32_t(q * 32) << 16);
+  int it = 0;
+  for (int u = blockIdx.x; u < S.total; u += gridDim.x, ++it) {
+    const Unit x = unit_at(S, u);
+    const int n_pad = (x.cnt + 15) & ~15;
+    mbar_wait(&tmem_full, it & 1);
+    tc_fence_after();
+    if (!x.down) {
+      const int n = x.nb * 128 + row;  // intermediate feature
+      for (int c0 = 0; c0 < n_pad; c0 += 32) {
+        uint32_t g[32], v[32];
+        tmem_ld32(trow + c0, g);
+        tmem_ld32(trow + 256 + c0, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (c0 + j < x.cnt) {
+            const float gv = __uint_as_float(g[j]);
+            p.hbuf[size_t(x.row0 + c0 + j) * p.hi + n] = f2bf(gv / (1.0f + __expf(-gv)) * __uint_as_float(v[j]));
+          }
+      }
+      __threadfence();  // release this unit's H rows before the count
+    } else {
+      const int n = x.nb * 128 + row;  // output feature
+      float* y = p.y + size_t(x.ks) * p.y_stride;
+      for (int c0 = 0; c0 < n_pad; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(trow + c0, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (c0 + j < x.cnt) y[size_t(x.row0 + c0 + j) * p.h + n] = __uint_as_float(r[j]);
+      }
+    }
+    tc_fence_before();
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (warp == 2 && lane == 0) {
+      if (!x.down) {
+        __threadfence();
+        atomicAdd(p.done + x.e, 1);
+      }
+      mbar_arrive(&tmem_empty);
+    }
+  }
+}
+
+// The last CTA to finish zeroes the counters for the next launch (every
+// wait on them is over: all other CTAs have exited their unit loops).
+__device__ __forceinline__ void reset_done(const MoeParams& p) {
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(p.done + kMaxE, 1) == int(gridDim.x) - 1) {
+      for (int e = 0; e < p.E; ++e) atomicExch(p.done + e, 0);
+      atomicExch(p.done + kMaxE, 0);
+    }
+  }
+}
+
+__device__ __forceinline__ void init_schedule(Schedule& S, const MoeParams& p, int tok) {
+  S.nA = p.hi / 128;
+  S.splits = p.splits;
+  S.tok = tok;
+  S.nB = p.splits * (p.h / 128);
+  S.a_base[0] = S.b_base[0] = 0;
+  for (int e = 0; e < p.E; ++e) {
+    S.off[e] = p.offsets[e];
+    const int cnt = p.offsets[e + 1] - p.offsets[e];
+    const int tt = (cnt + tok - 1) / tok;
+    S.a_base[e + 1] = S.a_base[e] + tt * S.nA;
+    S.b_base[e + 1] = S.b_base[e] + tt * S.nB;
+  }
+  S.off[p.E] = p.offsets[p.E];
+  S.totalA = S.a_base[p.E];
+  S.total = S.totalA + S.b_base[p.E];
+}
+
 // kSub k-blocks of 64 per pipeline stage (kSub = 2: each weight row is read
 // 256 contiguous bytes at a time), kTokT-row token tiles, kStagesT stages.
 template <int kSub, int kTokT, int kStagesT>
@@ -122,21 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
-    S.nA = p.hi / 128;
-    S.splits = p.splits;
-    S.tok = kTokT;
-    S.nB = p.splits * (p.h / 128);
-    S.a_base[0] = S.b_base[0] = 0;
-    for (int e = 0; e < p.E; ++e) {
-      S.off[e] = p.offsets[e];
-      const int cnt = p.offsets[e + 1] - p.offsets[e];
-      const int tt = (cnt + kTokT - 1) / kTokT;
-      S.a_base[e + 1] = S.a_base[e] + tt * S.nA;
-      S.b_base[e + 1] = S.b_base[e] + tt * S.nB;
-    }
-    S.off[p.E] = p.offsets[p.E];
-    S.totalA = S.a_base[p.E];
-    S.total = S.totalA + S.b_base[p.E];
+    init_schedule(S, p, kTokT);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
@@ -235,65 +305,186 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int q = warp & 3;
-    const int row = q * 32 + lane;  // weight row within the 128-row tile
-    const uint32_t trow = tmem + (uint32_t(q * 32) << 16);
-    int it = 0;
-    for (int u = blockIdx.x; u < S.total; u += gridDim.x, ++it) {
-      const Unit x = unit_at(S, u);
-      const int n_pad = (x.cnt + 15) & ~15;
-      mbar_wait(&tmem_full, it & 1);
-      tc_fence_after();
-      if (!x.down) {
-        const int n = x.nb * 128 + row;  // intermediate feature
-        for (int c0 = 0; c0 < n_pad; c0 += 32) {
-          uint32_t g[32], v[32];
-          tmem_ld32(trow + c0, g);
-          tmem_ld32(trow + 256 + c0, v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c0 + j < x.cnt) {
-              const float gv = __uint_as_float(g[j]);
-              p.hbuf[size_t(x.row0 + c0 + j) * p.hi + n] = f2bf(gv / (1.0f + __expf(-gv)) * __uint_as_float(v[j]));
-            }
-        }
-        __threadfence();  // release this unit's H rows before the count
-      } else {
-        const int n = x.nb * 128 + row;  // output feature
-        float* y = p.y + size_t(x.ks) * p.y_stride;
-        for (int c0 = 0; c0 < n_pad; c0 += 32) {
-          uint32_t r[32];
-          tmem_ld32(trow + c0, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c0 + j < x.cnt) y[size_t(x.row0 + c0 + j) * p.h + n] = __uint_as_float(r[j]);
+    epilogue_loop(S, p, tmem, warp, lane, tmem_full, tmem_empty);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+  reset_done(p);
+}
+
+// ---------------------------------------------------------------------------
+// K4-MoE on T2-coded experts (tcode.cuh): the same unit schedule, MMA and
+// epilogue, but the weight tiles arrive in their link code and are expanded
+// inside the kernel — no bf16 copy of the expert ever reaches HBM.
+//   w0      code producer: bulk copies (cp.async.bulk) of the k-block's coded
+//           tiles (W1 + W3, or W2) into a code ring of kCS stages
+//   w1      MMA issuer (as above)
+//   w2..w5  epilogue (as above)
+//   w6..    kND decoder warps: warp d decodes segment d (16 rows) of each
+//           coded tile of the stage into the 128B-swizzled A tile, orders its
+//           shared-memory stores for the tensor core (fence.proxy.async) and
+//           arrives on a_full; decoder 0 also issues the stage's token-row
+//           TMA loads (and, for down units, first acquires done[e])
+// The A ring (kAS stages of W1 | W3 | token rows) is released by the MMA
+// commit, the code ring by the kND decoder arrivals.
+constexpr int kCodeSlot = tcode::kTileMax;  // 16416 B: the largest tile code
+
+template <int kND, int kAS, int kCS>
+__global__ void __launch_bounds__(kThreads + 32 * kND, 1)
+    moe_coded_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_h, MoeParams p,
+                     const uint8_t* const* __restrict__ w_code) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  constexpr int kXBytes = kTok * 128;
+  constexpr int kAStage = 2 * kTileA + kXBytes;  // W1 (or W2) | W3 | token rows
+  uint8_t* cring = smem + kAS * kAStage;         // kCS x (2 tile codes)
+  __shared__ __align__(8) uint64_t a_full[kAS], a_empty[kAS], c_full[kCS], c_empty[kCS];
+  __shared__ __align__(8) uint64_t tmem_full, tmem_empty;
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ Schedule S;
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    init_schedule(S, p, kTok);
+    for (int s = 0; s < kAS; ++s) {
+      mbar_init(&a_full[s], kND + 1);  // kND decoder warps + decoder 0's expect_tx for the token rows
+      mbar_init(&a_empty[s], 1);
+    }
+    for (int s = 0; s < kCS; ++s) {
+      mbar_init(&c_full[s], 1);
+      mbar_init(&c_empty[s], kND);
+    }
+    mbar_init(&tmem_full, 1);
+    mbar_init(&tmem_empty, 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_x);
+    tma_prefetch_desc(&tm_h);
+  }
+  if (warp == 1) tmem_alloc<512>(&tmem_base_sh);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  const int KBa = p.h / kBK;                     // gate/up k-blocks per unit
+  const int KBd = (p.hi / kBK) / p.splits;       // k-blocks per down slice
+  const int tiles = (p.h / 128) * (p.hi / kBK);  // tiles per matrix
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ code producer
+    if (elect_one()) {
+      int g = 0;
+      for (int u = blockIdx.x; u < S.total; u += gridDim.x) {
+        const Unit x = unit_at(S, u);
+        const uint8_t* blk = w_code[x.e];
+        const uint32_t* toff = reinterpret_cast<const uint32_t*>(blk);
+        const int KB = x.down ? KBd : KBa;
+        const int kb0 = x.down ? x.ks * KBd : 0;
+        // tile (matrix, row tile, k-block): W1 / W3 rows of h_i (h / 64 k-blocks), W2 rows of h (h_i / 64)
+        const int t0 = x.down ? 2 * tiles + x.nb * (p.hi / kBK) + kb0 : x.nb * (p.h / kBK);
+        for (int kb = 0; kb < KB; ++kb, ++g) {
+          const int s = g % kCS;
+          mbar_wait(&c_empty[s], ((g / kCS) & 1) ^ 1);
+          uint8_t* dst = cring + size_t(s) * 2 * kCodeSlot;
+          const uint32_t a0 = toff[t0 + kb], a1 = toff[t0 + kb + 1];
+          if (x.down) {
+            mbar_arrive_expect_tx(&c_full[s], a1 - a0);
+            bulk_load(dst, blk + a0, a1 - a0, &c_full[s]);
+          } else {
+            const uint32_t b0 = toff[tiles + t0 + kb], b1 = toff[tiles + t0 + kb + 1];
+            mbar_arrive_expect_tx(&c_full[s], (a1 - a0) + (b1 - b0));
+            bulk_load(dst, blk + a0, a1 - a0, &c_full[s]);
+            bulk_load(dst + kCodeSlot, blk + b0, b1 - b0, &c_full[s]);
+          }
         }
       }
-      tc_fence_before();
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (warp == 2 && lane == 0) {
-        if (!x.down) {
-          __threadfence();
-          atomicAdd(p.done + x.e, 1);
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      int g = 0, it = 0;
+      for (int u = blockIdx.x; u < S.total; u += gridDim.x, ++it) {
+        const Unit x = unit_at(S, u);
+        const int n_pad = (x.cnt + 15) & ~15;
+        const uint32_t idesc = make_idesc_bf16(128, n_pad);
+        const int KB = x.down ? KBd : KBa;
+        mbar_wait(&tmem_empty, (it & 1) ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < KB; ++kb, ++g) {
+          const int s = g % kAS;
+          mbar_wait(&a_full[s], (g / kAS) & 1);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + s * kAStage);
+          const uint64_t ad = make_sdesc_sw128(a_addr, 16, 1024);
+          const uint64_t au = make_sdesc_sw128(a_addr + kTileA, 16, 1024);
+          const uint64_t bd = make_sdesc_sw128(a_addr + 2 * kTileA, 16, 1024);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+            const uint64_t ko = uint64_t((k * 32) >> 4);
+            umma_bf16(tmem, ad + ko, bd + ko, idesc, acc);
+            if (!x.down) umma_bf16(tmem + 256, au + ko, bd + ko, idesc, acc);
+          }
+          umma_commit(&a_empty[s]);
         }
-        mbar_arrive(&tmem_empty);
+        umma_commit(&tmem_full);
+      }
+    }
+  } else if (warp < 6) {
+    // ------------------------------------------------------------ epilogue
+    epilogue_loop(S, p, tmem, warp, lane, tmem_full, tmem_empty);
+  } else {
+    // ------------------------------------------------------------ decoders
+    const int d = warp - 6;
+    int g = 0;
+    for (int u = blockIdx.x; u < S.total; u += gridDim.x) {
+      const Unit x = unit_at(S, u);
+      const int n_load = (x.cnt + 31) & ~31;
+      const int KB = x.down ? KBd : KBa;
+      const int kb0 = x.down ? x.ks * KBd : 0;
+      if (d == 0 && x.down && lane == 0) {
+        // every gate/up unit of expert e has published its H rows
+        const int need = ((S.off[x.e + 1] - S.off[x.e] + kTok - 1) / kTok) * S.nA;
+        while (ld_acquire(p.done + x.e) < need) {
+        }
+        fence_proxy_async_global();
+      }
+      for (int kb = 0; kb < KB; ++kb, ++g) {
+        const int sa = g % kAS, sc = g % kCS;
+        uint8_t* st = smem + sa * kAStage;
+        mbar_wait(&a_empty[sa], ((g / kAS) & 1) ^ 1);
+        if (d == 0 && lane == 0) {
+          mbar_arrive_expect_tx(&a_full[sa], uint32_t((n_load / 32) * 4096));
+          const int kc = (kb0 + kb) * kBK;
+          for (int i = 0; i < n_load / 32; ++i)
+            tma_load_2d(st + 2 * kTileA + i * 4096, x.down ? &tm_h : &tm_x, &a_full[sa], kc, x.row0 + i * 32);
+        }
+        mbar_wait(&c_full[sc], (g / kCS) & 1);
+        const uint8_t* code = cring + size_t(sc) * 2 * kCodeSlot;
+#pragma unroll 1
+        for (int m = 0; m < (x.down ? 1 : 2); ++m) {
+          const uint8_t* tc = code + m * kCodeSlot;
+          const uint32_t* hdr = reinterpret_cast<const uint32_t*>(tc);
+#pragma unroll 1
+          for (int sg = d; sg < tcode::kSegs; sg += kND) {
+            uint32_t off = 32;
+            for (int k = 0; k < sg; ++k) off += (hdr[k] >> 16) * 16;
+            tcode::decode_segment(tc + off, hdr[sg], st + m * kTileA, sg, lane);
+          }
+        }
+        fence_proxy_async();  // the stores above feed the tensor core (async proxy)
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&c_empty[sc]);
+          mbar_arrive(&a_full[sa]);
+        }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<512>(tmem);
-  // the last CTA to finish zeroes the counters for the next launch (every
-  // wait on them is over: all other CTAs have exited their unit loops)
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(p.done + kMaxE, 1) == int(gridDim.x) - 1) {
-      for (int e = 0; e < p.E; ++e) atomicExch(p.done + e, 0);
-      atomicExch(p.done + kMaxE, 0);
-    }
-  }
+  reset_done(p);
 }
 
 int sm_count() {
@@ -405,6 +596,66 @@ int moe_launch(const void* x_perm, int rows, int h, int hi, int E, const int32_t
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   SMO_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, t1, t3, t2, tx, th, p));
+  count_launch();
+  return splits;
+}
+
+// The expert block of one layer on T2-coded experts (tcode.cuh): w_code is a
+// DEVICE array of E pointers to each expert's code block (16-B aligned, e.g.
+// the streamed code slots and the coded hot cache). Same unit schedule,
+// split and MMA order as moe_launch, so the outputs are bit-identical to
+// moe_launch on the decoded weights.
+int moe_coded_launch(const void* x_perm, int rows, int h, int hi, int E, const int32_t* offsets,
+                     const void* const* w_code, void* hbuf, float* y, int splits, int max_splits, int* done,
+                     cudaStream_t st) {
+  SMO_REQUIRE(x_perm && offsets && w_code && hbuf && y && done, "moe: null pointer");
+  SMO_REQUIRE(E >= 1 && E <= kMaxE, "moe: 1 <= n_expert <= 64");
+  SMO_REQUIRE(h % 128 == 0 && hi % 128 == 0, "moe: h and h_i must be multiples of 128");
+  SMO_REQUIRE(rows > 0 && max_splits >= 1, "moe: no rows");
+  if (splits <= 0) splits = pick_moe_splits(rows, h, hi, E, max_splits);
+  SMO_REQUIRE(splits <= max_splits && (hi / kBK) % splits == 0, "moe: bad down split");
+  CUtensorMap tx, th;
+  {
+    uint64_t dims[2] = {uint64_t(h), uint64_t(rows)};
+    uint64_t strides[1] = {uint64_t(h) * 2};
+    uint32_t box[2] = {uint32_t(kBK), 32};
+    make_tmap_bf16(&tx, x_perm, 2, dims, strides, box, true);
+  }
+  {
+    uint64_t dims[2] = {uint64_t(hi), uint64_t(rows)};
+    uint64_t strides[1] = {uint64_t(hi) * 2};
+    uint32_t box[2] = {uint32_t(kBK), 32};
+    make_tmap_bf16(&th, hbuf, 2, dims, strides, box, true);
+  }
+  MoeParams p{};
+  p.h = h;
+  p.hi = hi;
+  p.E = E;
+  p.offsets = offsets;
+  p.hbuf = reinterpret_cast<uint16_t*>(hbuf);
+  p.y = y;
+  p.y_stride = size_t(rows) * h;
+  p.splits = splits;
+  p.done = done;
+  constexpr int kND = 8, kAS = 2, kCS = 2;
+  auto kern = moe_coded_kernel<kND, kAS, kCS>;
+  const size_t smem = size_t(kAS) * (2 * kTileA + kTok * 128) + size_t(kCS) * 2 * kCodeSlot + 1024;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SMO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(sm_count()));
+  cfg.blockDim = dim3(kThreads + 32 * kND);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SMO_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, tx, th, p, reinterpret_cast<const uint8_t* const*>(w_code)));
   count_launch();
   return splits;
 }

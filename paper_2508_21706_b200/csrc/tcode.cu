@@ -1,0 +1,309 @@
+// tcode.cu — K5 tile code "T2" (format: tcode.cuh): the GPU encoder of an
+// expert block and a standalone decoder to bf16 (tests, bf16 expansions).
+// The production decoder is tcode::decode_segment inside the fused expert
+// kernel (moe_tc.cu), which never writes the bf16 weights to HBM.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "tcode.cuh"
+
+namespace smo {
+
+namespace {
+
+using namespace tcode;
+
+// the matrices of one expert block, tiles numbered matrix-major
+struct TMats {
+  const uint16_t* src[3];
+  int R[3], C[3];
+  int t0[4];  // first tile of each matrix; t0[3] = tiles
+};
+
+TMats expert_mats(const void* src, int h, int hi) {
+  TMats m{};
+  const size_t n = size_t(h) * hi;
+  for (int i = 0; i < 3; ++i) {
+    m.src[i] = src ? reinterpret_cast<const uint16_t*>(src) + i * n : nullptr;
+    m.R[i] = i < 2 ? hi : h;
+    m.C[i] = i < 2 ? h : hi;
+  }
+  const int per = int(n / (kTileRows * kTileCols));
+  for (int i = 0; i <= 3; ++i) m.t0[i] = i * per;
+  return m;
+}
+
+struct TileAt {
+  int m, nb, kb;
+};
+__device__ __forceinline__ TileAt tile_at(const TMats& M, int t) {
+  const int m = t >= M.t0[2] ? 2 : t >= M.t0[1] ? 1 : 0;
+  const int tl = t - M.t0[m];
+  const int kbs = M.C[m] / kTileCols;
+  return TileAt{m, tl / kbs, tl % kbs};
+}
+
+// level count of a value (5 for literals) for base E
+__device__ __forceinline__ int levels_of(int j) { return (j < 0 || j >= 15) ? 5 : j / 3 + 1; }
+
+constexpr int kEncWarps = 8;
+
+// Pass 1 (write = false): header word of every segment into meta[]. Pass 2:
+// meta[] + the tile table at the head of dst (written by the host between the
+// passes) -> tile headers and segment bodies. One warp per segment, lane L
+// owns values 32 L .. 32 L + 31 (row L / 2 of the segment, half L % 2).
+__global__ void __launch_bounds__(32 * kEncWarps) tcode_encode_kernel(const __grid_constant__ TMats M, int segs,
+                                                                      uint32_t* __restrict__ meta,
+                                                                      uint8_t* __restrict__ dst, bool write) {
+  __shared__ uint32_t fw[kEncWarps][256];  // level fields of the warp's segment (<= 4 x 1024 x 2 bits)
+  const int wib = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int g = blockIdx.x * kEncWarps + wib;
+  if (g >= segs) return;
+  const int t = g / kSegs, s = g % kSegs;
+  const TileAt ta = tile_at(M, t);
+  const int C = M.C[ta.m];
+  const int row = ta.nb * kTileRows + s * kSegRows + (lane >> 1);
+  const int col = ta.kb * kTileCols + 32 * (lane & 1);
+  const uint4* sp = reinterpret_cast<const uint4*>(M.src[ta.m] + size_t(row) * C + col);
+  uint32_t v2[16];  // two values per word, value 2k in the low half
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint4 u = sp[i];
+    v2[4 * i] = u.x;
+    v2[4 * i + 1] = u.y;
+    v2[4 * i + 2] = u.z;
+    v2[4 * i + 3] = u.w;
+  }
+  auto val = [&](int i) -> uint32_t { return (v2[i >> 1] >> (16 * (i & 1))) & 0xffffu; };
+  auto expo = [&](int i) -> int { return int((val(i) >> 7) & 0xffu); };
+  uint32_t hw;
+  if (!write) {
+    int emax = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) emax = max(emax, expo(i));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+    int E = max(emax, 3), best = -1;
+    for (int c = 0; c < 8; ++c) {
+      const int b0 = emax - c;
+      if (b0 < 3) break;  // warp-uniform
+      int cost = 0;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int j = b0 - expo(i);
+        const int n = levels_of(j);
+        cost += 2 * n + ((j < 0 || j >= 15) ? 8 : 0);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) cost += __shfl_xor_sync(0xffffffffu, cost, o);
+      if (best < 0 || cost < best) {
+        best = cost;
+        E = b0;
+      }
+    }
+    int nf = 0, nl = 0, esc = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int j = E - expo(i);
+      const int n = levels_of(j);
+      nf += n - 1;
+      nl += (j < 0 || j >= 15) ? 1 : 0;
+      esc |= n > 1 ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      nf += __shfl_xor_sync(0xffffffffu, nf, o);
+      nl += __shfl_xor_sync(0xffffffffu, nl, o);
+      esc |= __shfl_xor_sync(0xffffffffu, esc, o);
+    }
+    const int bytes = (kLvOff + 4 * ((nf + 15) / 16) + nl + 15) & ~15;
+    hw = bytes >= kRawBytes ? (1u << 8) | (uint32_t(kRawBytes / 16) << 16)
+                            : uint32_t(E) | (uint32_t(esc ? 2 : 0) << 8) | (uint32_t(bytes / 16) << 16);
+    if (lane == 0) meta[g] = hw;
+    return;
+  }
+  hw = meta[g];
+  const uint32_t toff = reinterpret_cast<const uint32_t*>(dst)[t];
+  uint32_t soff = toff + 32;
+  for (int k = 0; k < s; ++k) soff += (meta[t * kSegs + k] >> 16) * 16;
+  uint8_t* sg = dst + soff;
+  if (lane == 0) reinterpret_cast<uint32_t*>(dst + toff)[s] = hw;
+  const int bytes = int(hw >> 16) * 16;
+  if (hw & 0x100u) {
+    uint4* d = reinterpret_cast<uint4*>(sg) + 4 * lane;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) d[i] = make_uint4(v2[4 * i], v2[4 * i + 1], v2[4 * i + 2], v2[4 * i + 3]);
+    return;
+  }
+  const int E = int(hw & 0xffu);
+  // lo bytes and level-1 codes
+  uint32_t lo[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}, l1[2] = {0u, 0u};
+  int cnt[6] = {0, 0, 0, 0, 0, 0};  // values with >= k levels (k = 2..5), literals in [1]
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const uint32_t x = val(i);
+    lo[i >> 2] |= (((x >> 8) & 0x80u) | (x & 0x7fu)) << (8 * (i & 3));
+    const int j = E - expo(i);
+    const int n = levels_of(j);
+    const uint32_t c1 = n > 1 ? 3u : uint32_t(j);
+    const int ii = i & 15;
+    l1[i >> 4] |= c1 << (2 * (ii >> 1) + 16 * (ii & 1));
+#pragma unroll
+    for (int k = 2; k <= 5; ++k) cnt[k] += n >= k ? 1 : 0;
+    cnt[1] += (j < 0 || j >= 15) ? 1 : 0;
+  }
+  reinterpret_cast<uint4*>(sg)[2 * lane] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  reinterpret_cast<uint4*>(sg)[2 * lane + 1] = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+  reinterpret_cast<uint2*>(sg + kL1Off)[lane] = make_uint2(l1[0], l1[1]);
+  uint32_t* wd = fw[wib];
+  for (int k = lane; k < 256; k += 32) wd[k] = 0u;
+  __syncwarp();
+  int base = 0;
+#pragma unroll 1
+  for (int k = 2; k <= 5; ++k) {
+    int tot = 0;
+    int f = base + warp_excl_scan(cnt[k], lane, &tot);
+    for (int i = 0; i < 32; ++i) {
+      const int j = E - expo(i);
+      const int n = levels_of(j);
+      if (n < k) continue;
+      const bool lit = j < 0 || j >= 15;
+      const uint32_t c = (lit || n > k) ? 3u : uint32_t(j - 3 * (k - 1));
+      atomicOr(&wd[f >> 4], c << (2 * (f & 15)));
+      ++f;
+    }
+    base += tot;
+  }
+  __syncwarp();
+  const int nw = (base + 15) / 16;
+  uint32_t* lvp = reinterpret_cast<uint32_t*>(sg + kLvOff);
+  for (int k = lane; k < nw; k += 32) lvp[k] = wd[k];
+  int ltot = 0;
+  int lf = warp_excl_scan(cnt[1], lane, &ltot);
+  uint8_t* lit = sg + kLvOff + 4 * nw;
+  for (int i = 0; i < 32; ++i) {
+    const int e = expo(i);
+    const int j = E - e;
+    if (j < 0 || j >= 15) lit[lf++] = uint8_t(e);
+  }
+  const int used = kLvOff + 4 * nw + ltot;
+  if (lane < bytes - used) sg[used + lane] = 0;  // deterministic padding (< 16 bytes)
+}
+
+// One CTA per tile: stage the tile code in shared memory, eight warps decode
+// one segment each into a swizzled tile (the expert kernel's decoder), then
+// the tile is written back row-major.
+__global__ void __launch_bounds__(256) tcode_decode_kernel(const __grid_constant__ TMats M,
+                                                           const uint8_t* const* __restrict__ srcs,
+                                                           uint16_t* const* __restrict__ dsts) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* tile = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* code = tile + kTileRows * 128;
+  const uint8_t* src = srcs[blockIdx.y];
+  const int t = blockIdx.x;
+  const uint32_t* toff = reinterpret_cast<const uint32_t*>(src);
+  const uint32_t o0 = toff[t], o1 = toff[t + 1];
+  const uint4* g = reinterpret_cast<const uint4*>(src + o0);
+  for (uint32_t i = threadIdx.x; i < (o1 - o0) / 16; i += blockDim.x) reinterpret_cast<uint4*>(code)[i] = g[i];
+  __syncthreads();
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t* hdr = reinterpret_cast<const uint32_t*>(code);
+  uint32_t off = 32;
+  for (int k = 0; k < w; ++k) off += (hdr[k] >> 16) * 16;
+  decode_segment(code + off, hdr[w], tile, w, lane);
+  __syncthreads();
+  const TileAt ta = tile_at(M, t);
+  const int C = M.C[ta.m];
+  uint16_t* dst = dsts[blockIdx.y] + size_t(ta.m) * M.R[0] * M.C[0];
+  for (int i = threadIdx.x; i < kTileRows * 8; i += blockDim.x) {
+    const int r = i >> 3, c = i & 7;
+    const uint4 v = *reinterpret_cast<const uint4*>(tile + r * 128 + ((c ^ (r & 7)) << 4));
+    *reinterpret_cast<uint4*>(dst + size_t(ta.nb * kTileRows + r) * C + ta.kb * kTileCols + 8 * c) = v;
+  }
+}
+
+}  // namespace
+
+size_t tcode_max_bytes(int h, int hi) {
+  const size_t nt = size_t(3) * h * hi / (kTileRows * kTileCols);
+  return ((4 * (nt + 1) + 15) & ~size_t(15)) + nt * size_t(kTileMax);
+}
+
+// [W1 | W3 | W2] (bf16, device) -> T2 code at dst (device, >= tcode_max_bytes).
+// Synchronous on st (host scan of the tile sizes between the passes); returns
+// the code bytes.
+size_t tcode_encode(const void* src, int h, int hi, void* dst, cudaStream_t st) {
+  SMO_REQUIRE(src && dst, "tcode: null pointer");
+  SMO_REQUIRE(h % kTileRows == 0 && hi % kTileRows == 0 && h > 0 && hi > 0, "tcode: h and h_i must be multiples of 128");
+  const TMats M = expert_mats(src, h, hi);
+  const int nt = M.t0[3], segs = nt * kSegs;
+  uint32_t* meta = nullptr;
+  SMO_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&meta), size_t(segs) * 4, st));
+  auto d8 = reinterpret_cast<uint8_t*>(dst);
+  const unsigned grid = unsigned((segs + kEncWarps - 1) / kEncWarps);
+  tcode_encode_kernel<<<grid, 32 * kEncWarps, 0, st>>>(M, segs, meta, d8, false);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+  std::vector<uint32_t> hm(static_cast<size_t>(segs));
+  SMO_CUDA_CHECK(cudaMemcpyAsync(hm.data(), meta, hm.size() * 4, cudaMemcpyDeviceToHost, st));
+  SMO_CUDA_CHECK(cudaStreamSynchronize(st));
+  const size_t tb = (4 * (size_t(nt) + 1) + 15) & ~size_t(15);
+  std::vector<uint32_t> head(tb / 4, 0u);
+  size_t off = tb;
+  for (int t = 0; t < nt; ++t) {
+    head[size_t(t)] = uint32_t(off);
+    off += 32;
+    for (int s = 0; s < kSegs; ++s) off += (hm[size_t(t) * kSegs + s] >> 16) * 16;
+  }
+  SMO_REQUIRE(off < (size_t(1) << 32), "tcode: block too large for 32-bit tile offsets");
+  head[size_t(nt)] = uint32_t(off);
+  SMO_CUDA_CHECK(cudaMemcpyAsync(d8, head.data(), tb, cudaMemcpyHostToDevice, st));
+  tcode_encode_kernel<<<grid, 32 * kEncWarps, 0, st>>>(M, segs, meta, d8, true);
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+  SMO_CUDA_CHECK(cudaFreeAsync(meta, st));
+  SMO_CUDA_CHECK(cudaStreamSynchronize(st));
+  return off;
+}
+
+// Code bytes of a T2 block (reads toff[nt] from the device code).
+size_t tcode_size(const void* code, int h, int hi) {
+  const size_t nt = size_t(3) * h * hi / (kTileRows * kTileCols);
+  uint32_t v = 0;
+  SMO_CUDA_CHECK(cudaMemcpy(&v, reinterpret_cast<const uint8_t*>(code) + 4 * nt, 4, cudaMemcpyDeviceToHost));
+  return v;
+}
+
+// n T2 blocks -> bf16 [W1 | W3 | W2] blocks, one launch.
+void tcode_decode(const void* const* srcs, void* const* dsts, int n, int h, int hi, cudaStream_t st) {
+  SMO_REQUIRE(n >= 0 && n <= 64, "tcode: up to 64 blocks per launch");
+  SMO_REQUIRE(h % kTileRows == 0 && hi % kTileRows == 0 && h > 0 && hi > 0, "tcode: h and h_i must be multiples of 128");
+  if (!n) return;
+  const TMats M = expert_mats(nullptr, h, hi);
+  // pointer tables in device memory (stream-ordered scratch)
+  void** tab = nullptr;
+  SMO_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&tab), size_t(2 * n) * sizeof(void*), st));
+  std::vector<const void*> ht(size_t(2 * n));
+  for (int i = 0; i < n; ++i) {
+    SMO_REQUIRE(srcs[i] && dsts[i], "tcode: null block");
+    ht[size_t(i)] = srcs[i];
+    ht[size_t(n + i)] = dsts[i];
+  }
+  SMO_CUDA_CHECK(cudaMemcpyAsync(tab, ht.data(), ht.size() * sizeof(void*), cudaMemcpyHostToDevice, st));
+  const size_t smem = 1024 + kTileRows * 128 + kTileMax;
+  static bool attr = false;
+  if (!attr) {
+    SMO_CUDA_CHECK(cudaFuncSetAttribute(tcode_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  tcode_decode_kernel<<<dim3(unsigned(M.t0[3]), unsigned(n)), 256, smem, st>>>(
+      M, reinterpret_cast<const uint8_t* const*>(tab), reinterpret_cast<uint16_t* const*>(tab + n));
+  count_launch();
+  SMO_CUDA_CHECK(cudaGetLastError());
+  // the host vector must outlive the async copy
+  SMO_CUDA_CHECK(cudaStreamSynchronize(st));
+  SMO_CUDA_CHECK(cudaFreeAsync(tab, st));
+}
+
+}  // namespace smo

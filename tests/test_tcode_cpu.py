@@ -1,0 +1,91 @@
+"""CPU tier: the K5 tile code T2 restated in numpy (tests/tcode_ref.py) —
+lossless round trips on the data kinds the engine meets, known-answer
+layouts that pin the byte format the GPU encoder must produce
+(tests/test_gpu_tcode.py), and the code sizes the link relies on."""
+import numpy as np
+import pytest
+
+import tcode_ref as T
+import oracle_py as O
+
+
+def _mats(kind: str, h: int, hi: int):
+    n = h * hi
+    if kind == "uniform":  # the engine's expert init (engine.cu, fill_uniform)
+        f = [O.fill_uniform_bf16(n, 7, 1101 + i, np.sqrt(3.0 / (h if i < 2 else hi))) for i in range(3)]
+    elif kind == "gaussian":  # SMO_INIT_GAUSSIAN (fill_normal: Irwin-Hall + 1/1024 outliers x8)
+        f = [O.fill_normal_bf16(n, 7, 1101 + i, np.sqrt(3.0 / (h if i < 2 else hi))) for i in range(3)]
+    else:  # every bit pattern: escapes, literals, raw segments, tiny bases
+        rng = np.random.default_rng(5)
+        f = [rng.integers(0, 1 << 16, n).astype(np.uint16) for _ in range(3)]
+        f[0][::7] = 0  # exact zeros (exponent 0: literals)
+    return np.concatenate(f)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "gaussian", "wide"])
+def test_tcode_round_trip(kind):
+    h, hi = 256, 128
+    x = _mats(kind, h, hi)
+    code = T.encode_expert(x, h, hi)
+    assert len(code) <= T.max_bytes(h, hi)
+    assert np.array_equal(T.decode_expert(code, h, hi), x)
+    bpw = 8 * len(code) / x.size
+    if kind == "uniform":
+        assert 10.2 < bpw < 10.7, bpw  # 8 + ~2.3 exponent bits + headers
+    if kind == "gaussian":
+        assert bpw < 11.1, bpw  # below the unary code on these weights (~11.45)
+
+
+def _segment_tile(seg0: np.ndarray) -> np.ndarray:
+    """A 128 x 64 matrix whose tile (0, 0) has segment 0 = seg0 and 1.0 elsewhere."""
+    W = np.full((128, 64), 0x3F80, np.uint16)
+    W[:16] = seg0.reshape(16, 64)
+    return W
+
+
+def test_tcode_known_answers():
+    # every value 1.0 (exponent 127): E = 127, j = 0 -> all L1 codes 0, no
+    # level fields: 1024 lo bytes + 256 code bytes = 1280 B = 80 x 16
+    W = np.full((128, 64), 0x3F80, np.uint16)
+    code = T.encode([W])
+    toff = np.frombuffer(code[:16], "<u4")
+    assert toff[0] == 16 and toff[1] == len(code) == 16 + 32 + 8 * 1280
+    hdr = np.frombuffer(code[16:48], "<u4")
+    assert np.all(hdr == (127 | (80 << 16)))
+    seg = np.frombuffer(code[48:48 + 1280], np.uint8)
+    assert not np.any(seg)  # lo = 0 (positive, zero mantissa), codes 0
+    # value 3 halved (j = 1) and value 17 at 2^-3 (j = 3: L1 code 3, level-2 code 0)
+    s = np.full(1024, 0x3F80, np.uint16)
+    s[3] = 0x3F00
+    s[17] = 0x3E00
+    code = T.encode([_segment_tile(s)])
+    hw = int(np.frombuffer(code[16:20], "<u4")[0])
+    assert hw & 0xFF == 127 and (hw >> 8) & 0xFF == 2 and (hw >> 16) == 81  # 1280 + 1 level word -> 1296
+    l1 = np.frombuffer(code[48 + 1024:48 + 1280], "<u4")
+    # lane 0 word 0: value 3 = 2 q + 1 with q = 1 -> bits 16 + 2; word 1: value 17 = 16 + 2*0 + 1 -> bits 16
+    assert l1[0] == 1 << 18 and l1[1] == 3 << 16 and not np.any(l1[2:])
+    assert np.frombuffer(code[48 + 1280:48 + 1284], "<u4")[0] == 0  # level-2 code 0
+    assert np.array_equal(T.decode(code, [(128, 64)])[0], _segment_tile(s))
+    # an exact zero (exponent 0, j = 127): five 3s and a literal byte 0
+    z = np.full(1024, 0x3F80, np.uint16)
+    z[0] = 0
+    code = T.encode([_segment_tile(z)])
+    lv = np.frombuffer(code[48 + 1280:48 + 1284], "<u4")[0]
+    assert lv == 0xFF  # levels 2..5 of value 0: fields 0..3 all 3
+    assert np.array_equal(T.decode(code, [(128, 64)])[0], _segment_tile(z))
+    # incompressible segment -> raw (2048 B), flags bit 0
+    r = np.random.default_rng(1).integers(0, 1 << 16, 1024).astype(np.uint16)
+    code = T.encode([_segment_tile(r)])
+    hw = int(np.frombuffer(code[16:20], "<u4")[0])
+    assert (hw >> 8) & 0xFF == 1 and (hw >> 16) == 128
+    assert np.frombuffer(code[48:48 + 2048], "<u2").tolist() == r.tolist()
+
+
+def test_tcode_base_choice_prefers_fewer_bits():
+    # one outlier 2^6 above the rest: E drops to the highest base that keeps
+    # the bulk within level 1 (j = 2; ties prefer the higher E) and the
+    # outlier becomes an 18-bit literal, instead of adding 6 to every j
+    s = np.full(1024, 0x3F80, np.uint16)
+    s[5] = 0x4280  # 64.0
+    E, bits = T.choose_base(((s.astype(np.int64) >> 7) & 0xFF))
+    assert E == 129 and bits == 2 * 1023 + 18

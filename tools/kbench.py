@@ -128,6 +128,59 @@ def codec(n=3 * 4096 * 14336, bits=3, dist="uniform"):
             "us": t * 1e6, "GBs": byts / t / 1e9, "frac": byts / t / 1e9 / PEAK, "TFLOPs": 0.0}
 
 
+def moe_coded(T=288, h=4096, hi=14336, E=8, k=2, dist="uniform"):
+    """K4-MoE on T2-coded experts (decode in shared memory) vs the bf16
+    kernel and vs unary expansion + bf16 kernel (the round-1 pipeline), on
+    the engine's procedural expert init (uniform or gaussian-like)."""
+    g = torch.Generator(device=dev).manual_seed(3)
+    x = (torch.rand((T, h), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
+    blk = 3 * h * hi
+    pool = torch.empty(E * blk, dtype=torch.bfloat16, device=dev)
+    fill = ops.fill_normal_ if dist == "gaussian" else ops.fill_uniform_
+    for e in range(E):
+        b = pool[e * blk:(e + 1) * blk]
+        fill(b[:hi * h], 0x5EED, 1100 + 3 * e, math.sqrt(3.0 / h))
+        fill(b[hi * h:2 * hi * h], 0x5EED, 1101 + 3 * e, math.sqrt(3.0 / h))
+        fill(b[2 * hi * h:], 0x5EED, 1102 + 3 * e, math.sqrt(3.0 / hi))
+    codes = [ops.tcode_encode(pool[e * blk:(e + 1) * blk], h, hi) for e in range(E)]
+    ucodes = [ops.expert_encode(pool[e * blk:(e + 1) * blk], 1)[0] for e in range(E)]
+    w_code = torch.tensor([c.data_ptr() for c in codes], dtype=torch.int64, device=dev)
+    ids = torch.stack([torch.randperm(E, generator=g, device=dev)[:k] for _ in range(T)]).to(torch.int32)
+    off, perm, pos, xp = ops.permute(ids, E, x)
+    hbuf = torch.empty((T * k, hi), dtype=torch.bfloat16, device=dev)
+    y4 = torch.empty((4, T * k, h), dtype=torch.float32, device=dev)
+    scratch = torch.zeros(128, dtype=torch.int32, device=dev)
+    widx = torch.arange(E, dtype=torch.int32, device=dev)
+    st = lambda: torch.cuda.current_stream().cuda_stream  # noqa: E731
+
+    def plain():
+        L.check(L.load().smo_moe_experts(xp.data_ptr(), T * k, h, hi, E, off.data_ptr(), pool.data_ptr(), blk * 2, E,
+                                         widx.data_ptr(), hbuf.data_ptr(), y4.data_ptr(), 0, None,
+                                         scratch.data_ptr(), st()))
+
+    def coded():
+        L.check(L.load().smo_moe_experts_coded(xp.data_ptr(), T * k, h, hi, E, off.data_ptr(), w_code.data_ptr(),
+                                               hbuf.data_ptr(), y4.data_ptr(), 0, None, scratch.data_ptr(), st()))
+
+    def unary_then_plain():
+        for e in range(E):
+            L.check(L.load().smo_expert_decode(ucodes[e].data_ptr(), blk, 1, pool[e * blk:].data_ptr(), st()))
+        plain()
+    cb = sum(c.numel() for c in codes)
+    ub = sum(c.numel() for c in ucodes)
+    act = T * k * h * 2 * 2 + T * k * hi * 2 * 2 + T * k * h * 4  # x rows (gate/up), H write + read, y
+    r = []
+    for nm, fn, byts, wb in (("bf16 weights", plain, E * blk * 2, E * blk * 2),
+                             ("T2-coded weights, decoded in smem", coded, cb, cb),
+                             ("unary expansion (8 launches) + bf16 kernel", unary_then_plain, ub + 2 * E * blk * 2, ub)):
+        t = timeit(fn)
+        r.append({"kernel": f"K4-MoE {nm}", "dist": dist, "T": T, "E": E, "us": t * 1e6,
+                  "weight_bytes": wb, "bits_per_weight": wb * 8 / (E * blk), "GBs": byts / t / 1e9,
+                  "frac": byts / t / 1e9 / PEAK, "GBs_incl_act": (byts + act) / t / 1e9,
+                  "TFLOPs": 3 * 2 * T * k * h * hi / t / 1e12})
+    return r
+
+
 def main():
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
     res = []
@@ -148,6 +201,9 @@ def main():
         res.append(codec(bits=3))
         res.append(codec(bits=1))
         res.append(codec(bits=1, dist="gaussian"))
+    if what in ("moecoded", "all"):
+        res += moe_coded()
+        res += moe_coded(dist="gaussian")
     if what in ("gemm", "all"):
         res.append(gemm(288, 4096, 6144, name="qkv"))
         res.append(gemm(288, 4096, 4096, L.EPI_F32_ADD, name="o-proj (+residual)"))
