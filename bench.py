@@ -59,6 +59,9 @@ def parse():
                     help="LARGE_BATCH (stream whole layers ahead) or BATCH_ONE (stream router-selected experts)")
     ap.add_argument("--no-compress", dest="compress", action="store_false",
                     help="stream raw bf16 experts instead of the lossless code (default: coded, expanded in HBM)")
+    ap.add_argument("--codec", default="unary", choices=["unary", "tile"],
+                    help="link code of the coded transfer: unary (xfer.cu; blocks expanded in HBM by a decode "
+                         "kernel) or tile (tcode.cuh T2; decoded inside the expert kernel, no bf16 expert in HBM)")
     ap.add_argument("--ep-transport", default="ipc", choices=["ipc", "nccl"],
                     help="N>1 expert-parallel exchange: CUDA-IPC peer mailboxes written by the dispatch / "
                          "combine kernels themselves (default; falls back to NCCL if IPC cannot be set up) "
@@ -544,7 +547,8 @@ def run_ours(args):
             eng = VerifyEngine(shape, max_batch=b, max_verify=n, max_seq=s_max, hbm_slots=args.slots,
                                expert_cache_bytes=int(args.cache_gb * 1e9), host_alias_layers=a, device=local,
                                ep_rank=ep_rank, ep_size=ep_size, ep_group=grp, attn_cpu=args.attn_cpu,
-                               batch_one=args.moe_batching == "one", compress_experts=args.compress,
+                               batch_one=args.moe_batching == "one",
+                               compress_experts=(2 if args.codec == "tile" else 1) if args.compress else 0,
                                micro_batches=args.micro_batches)
             alias = a
             break
@@ -658,7 +662,8 @@ def run_ours(args):
                 "per layer; CUDA events around the launch on its stream), per step",
                 "achieved": moe_bytes_step / moe_t / 1e9 if moe_t > 0 else None, "peak": pk["hbm_gbs"],
                 "unit": "GB/s", "frac": (moe_bytes_step / moe_t / 1e9) / pk["hbm_gbs"] if moe_t > 0 else None,
-                "traffic": moe_traffic_per_layer() if (args.model == "mixtral-8x7b" and ep_size == 1) else None,
+                "traffic": moe_traffic_per_layer() if (args.model == "mixtral-8x7b" and ep_size == 1
+                                                       and not (args.compress and args.codec == "tile")) else None,
                 "traffic_unit": "dram bytes per layer (the fused expert launch, ncu profiles/r01c_traffic.json); "
                 "algorithmic per layer = " + str((shape.n_expert // ep_size) * shape.expert_bytes),
                 "peak_kind": pk_kind}
@@ -689,9 +694,14 @@ def run_ours(args):
                    "micro_batches": args.micro_batches,
                    "moe_batching": "BATCH_ONE (router-selected experts)" if args.moe_batching == "one"
                    else "LARGE_BATCH (whole layers)",
-                   "expert_transfer": f"lossless exponent-coded blocks (xfer.cu, "
-                   f"{16.0 * stages['h2d_bytes'] / max(1.0, stages['h2d_raw_bytes']):.2f} bits/weight), expanded in HBM "
-                   "before the expert kernel" if args.compress else "raw bf16",
+                   "expert_transfer": (f"lossless tile-coded blocks (tcode.cuh T2, "
+                                       f"{16.0 * stages['h2d_bytes'] / max(1.0, stages['h2d_raw_bytes']):.2f} "
+                                       "bits/weight), decoded in shared memory by the expert kernel"
+                                       if args.codec == "tile" else
+                                       f"lossless exponent-coded blocks (xfer.cu, "
+                                       f"{16.0 * stages['h2d_bytes'] / max(1.0, stages['h2d_raw_bytes']):.2f} "
+                                       "bits/weight), expanded in HBM before the expert kernel")
+                   if args.compress else "raw bf16",
                    "l2": "inputs larger than L2 (90.2 GB of experts + 4.6 GB KV streamed per step)",
                    "expert_init": args.init,
                    "parallelism": mode},

@@ -370,7 +370,10 @@ typedef struct {
                                  bytes on uniform-init weights; 3-bit window 1.41x; 4-bit 1.29x;
                                  else raw; env SMO_CODEC=fixed skips unary) and cross the link
                                  coded; the compute stream expands each layer's blocks into its HBM
-                                 slot before the expert kernel. */
+                                 slot before the expert kernel. 2 (or env SMO_CODEC=tile): the T2
+                                 tile code (smo_tcode_encode) for every block, streamed and hot-cached
+                                 in that code and decoded by the expert kernel itself in shared memory
+                                 (smo_moe_experts_coded): no expansion launch, no bf16 expert in HBM. */
   int32_t micro_batches;      /* Hyperparameters.m (config.hpp:118-125): the batch runs as m micro-
                                  batches of ~b/m requests, issued stage-major per layer like
                                  build_target_dag (pipeline.hpp:147-206): GPU_OTHER1 of every

@@ -174,6 +174,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   while (!mbar_try_wait(bar, phase)) {
   }
 }
+// For waiters off the critical path (e.g. epilogue warps between units): back
+// off so their polling does not take issue slots from busy warps.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t phase, uint32_t ns) {
+  while (!mbar_try_wait(bar, phase)) __nanosleep(ns);
+}
 
 // 2D / 3D TMA tile loads into CTA shared memory, completion on an mbarrier.
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,

@@ -54,6 +54,7 @@ void Engine::bt_sync(cudaStream_t st) {
 // expand layer l's coded blocks (streamed into cstage) into its pool slot,
 // on the compute stream after slot_ready(l)
 void Engine::decode_slot(int l, cudaStream_t st) {
+  if (tmode) return;  // tile-coded blocks are decoded inside K4-MoE
   const int s = l % slots;
   if (coded_streamed[size_t(l)].empty() && coded_cached[size_t(l)].empty()) return;
   SMO_CUDA_CHECK(cudaEventRecord(dec_ev[size_t(2 * l)], st));
@@ -87,6 +88,14 @@ void Engine::decode_slot(int l, cudaStream_t st) {
   }
   SMO_CUDA_CHECK(cudaEventRecord(dec_ev[size_t(2 * l + 1)], st));
   step_dec_ev.push_back({dec_ev[size_t(2 * l)], dec_ev[size_t(2 * l + 1)]});
+}
+
+int Engine::expert_block(int l, const void* x_perm, int rows, int nexp, const int32_t* offsets, const int32_t* w_index,
+                         const void* const* w_code, void* hb, float* y, int splits, int max_splits, cudaStream_t st) {
+  (void)l;
+  if (tmode) return moe_coded_launch(x_perm, rows, h, hi, nexp, offsets, w_code, hb, y, splits, max_splits, d_done, st);
+  return moe_launch(x_perm, rows, h, hi, nexp, offsets, pool, blk_bytes, pool_blocks, w_index, hb, y, splits,
+                    max_splits, d_done, st);
 }
 
 void Engine::create() {
@@ -236,7 +245,9 @@ void Engine::create() {
     cblk_bytes = expert_code_bytes(blk_elems, 4);  // staging stride: no block is kept coded above it
     const char* f = std::getenv("SMO_CODEC");
     unary = !(f && std::strcmp(f, "fixed") == 0);
-    cenc = dalloc<uint8_t>(unary ? expert_code_bytes(blk_elems, 1) : cblk_bytes);
+    tmode = opt.compress_experts == 2 || (f && std::strcmp(f, "tile") == 0);
+    if (tmode) SMO_REQUIRE(h % 128 == 0 && hi % 128 == 0, "engine: the tile code needs h and h_i multiples of 128");
+    cenc = dalloc<uint8_t>(tmode ? tcode_max_bytes(h, hi) : unary ? expert_code_bytes(blk_elems, 1) : cblk_bytes);
     d_ovf = dalloc<int>(1);
     blk_coded.assign(size_t(host_alias) * E_loc, 0);
     blk_csize.assign(size_t(host_alias) * E_loc, 0);
@@ -260,6 +271,15 @@ void Engine::create() {
       // it beats the 3-bit window, else 3 or 4 bits, else unary if still
       // within the staging stride, else raw bf16 — lossless in every case
       size_t ubytes = 0;
+      if (tmode) {  // T2: always (lossless for any bits; raw tiles inside the code)
+        SMO_CUDA_CHECK(cudaStreamSynchronize(st));
+        const size_t tb = tcode_encode(stage, h, hi, cenc, st);
+        SMO_REQUIRE(tb <= blk_bytes, "engine: tile code of an expert block larger than its bf16 size");
+        SMO_CUDA_CHECK(cudaMemcpy(hdst, cenc, tb, cudaMemcpyDeviceToHost));
+        blk_coded[size_t(a) * E_loc + local(e)] = 2;
+        blk_csize[size_t(a) * E_loc + local(e)] = tb;
+        continue;
+      }
       if (xcomp && unary) {
         SMO_CUDA_CHECK(cudaStreamSynchronize(st));
         expert_encode(stage, blk_elems, 1, cenc, d_ovf, st);
@@ -295,7 +315,7 @@ void Engine::create() {
   int placed = 0;
   {
     const char* f = std::getenv("SMO_CODED_CACHE");
-    const bool coded_cache = xcomp && !(f && f[0] == '0');
+    const bool coded_cache = xcomp && (tmode || !(f && f[0] == '0'));
     int64_t budget = std::max<int64_t>(opt.expert_cache_bytes, 0);
     size_t cc_bytes = 0;
     std::vector<std::pair<size_t, size_t>> cc_src;  // (l*E+e, offset)
@@ -333,7 +353,11 @@ void Engine::create() {
       }
     }
   }
-  pool_blocks = slots * E_loc + placed;
+  if (tmode) {  // staging stride: the largest tile code (16-B multiples), no bf16 slots
+    cblk_bytes = 256;
+    for (size_t b : blk_csize) cblk_bytes = std::max(cblk_bytes, (b + 255) & ~size_t(255));
+  }
+  pool_blocks = (tmode ? 0 : slots * E_loc) + placed;
   pool = dalloc<uint16_t>(size_t(pool_blocks) * blk_elems);
   coded_streamed.assign(size_t(L), {});
   if (xcomp) cstage = dalloc<uint8_t>(size_t(slots) * E_loc * cblk_bytes);
@@ -358,6 +382,25 @@ void Engine::create() {
     }
   d_w_index = dalloc<int32_t>(widx.size());
   SMO_CUDA_CHECK(cudaMemcpy(d_w_index, widx.data(), widx.size() * 4, cudaMemcpyHostToDevice));
+  if (tmode) {  // code block of (layer, expert): its staging slot, or the coded hot cache
+    std::vector<const void*> wc(size_t(L) * E, nullptr);
+    for (int l = 0; l < L; ++l)
+      for (int e : owned) {
+        const size_t i = size_t(l) * E + size_t(e);
+        wc[i] = cache_blk[i] == kCachedCoded ? static_cast<const void*>(ccache + ccache_off[i])
+                                             : static_cast<const void*>(cstage + (size_t(l % slots) * E_loc + local(e)) *
+                                                                                     cblk_bytes);
+      }
+    d_w_code = dalloc<const void*>(wc.size());
+    SMO_CUDA_CHECK(cudaMemcpy(d_w_code, wc.data(), wc.size() * sizeof(void*), cudaMemcpyHostToDevice));
+    if (ep_on) {
+      std::vector<const void*> wl(size_t(L) * E_loc);
+      for (int l = 0; l < L; ++l)
+        for (int le = 0; le < E_loc; ++le) wl[size_t(l) * E_loc + le] = wc[size_t(l) * E + le * P + opt.ep_rank];
+      d_w_code_loc = dalloc<const void*>(wl.size());
+      SMO_CUDA_CHECK(cudaMemcpy(d_w_code_loc, wl.data(), wl.size() * sizeof(void*), cudaMemcpyHostToDevice));
+    }
+  }
   if (ep_on) {  // local expert le of this rank = global expert le*P + rank
     std::vector<int32_t> wl(size_t(L) * E_loc);
     for (int l = 0; l < L; ++l)
@@ -416,7 +459,7 @@ void Engine::create() {
   }
   {
     const char* f = std::getenv("SMO_MOE_FUSED");
-    moe_fused = !(f && f[0] == '0');
+    moe_fused = tmode || !(f && f[0] == '0');  // the tile-coded expert kernel is the fused one
   }
   // fused MoE down splits from the GLOBAL shapes (every EP rank uses the
   // same S, so expert parallelism reproduces one GPU bit for bit)
@@ -637,8 +680,8 @@ void Engine::moe_ep(int l, int T, cudaStream_t st) {
   SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 4), st));
   int splits = 1;
   if (moe_fused) {
-    moe_launch(xl, P * C, h, hi, E_loc, offsets_l, pool, blk_bytes, pool_blocks, d_w_index_loc + size_t(l) * E_loc,
-               hbuf, yl, moe_splits, 4, d_done, st);
+    expert_block(l, xl, P * C, E_loc, offsets_l, d_w_index_loc + size_t(l) * E_loc,
+                 tmode ? d_w_code_loc + size_t(l) * E_loc : nullptr, hbuf, yl, moe_splits, 4, st);
     splits = moe_splits;
   } else {
     smo_gemm_args g{};
@@ -1064,8 +1107,8 @@ void Engine::verify_core(int b, int n, const int32_t* tokens, const int32_t* par
         const int32_t* offj = offsets + size_t(j) * (E + 1);
         float* yj = ybuf + size_t(moe_splits) * p0 * h;  // this micro-batch's [splits][PTj][h] region
         if (moe_fused) {
-          moe_launch(xp + p0 * h, PTj, h, hi, E, offj, pool, blk_bytes, pool_blocks, d_w_index + size_t(l) * E,
-                     hbuf + p0 * hi, yj, moe_splits, moe_splits, d_done, st);
+          expert_block(l, xp + p0 * h, PTj, E, offj, d_w_index + size_t(l) * E,
+                       tmode ? d_w_code + size_t(l) * E : nullptr, hbuf + p0 * hi, yj, moe_splits, moe_splits, st);
           // GPU_MOE = the expert kernel itself (the bench's kernel roofline)
           SMO_CUDA_CHECK(cudaEventRecord(mev(l, j, 5), st));
           if (j == M - 1) SMO_CUDA_CHECK(cudaEventRecord(slot_free[l % slots], st));

@@ -81,6 +81,12 @@ size_t expert_coded_size(const void* code, size_t count, int bits);
 void expert_encode(const void* src, size_t count, int bits, void* dst, int* overflow, cudaStream_t st);
 void expert_decode(const void* src, size_t count, int bits, void* dst, cudaStream_t st);
 void expert_decode_blocks(const void* const* srcs, void* const* dsts, int n, size_t count, int bits, cudaStream_t st);
+size_t tcode_max_bytes(int h, int hi);
+size_t tcode_encode(const void* src, int h, int hi, void* dst, cudaStream_t st);
+void tcode_decode(const void* const* srcs, void* const* dsts, int n, int h, int hi, cudaStream_t st);
+int moe_coded_launch(const void* x_perm, int rows, int h, int hi, int E, const int32_t* offsets,
+                     const void* const* w_code, void* hbuf, float* y, int splits, int max_splits, int* done,
+                     cudaStream_t st);
 
 // Procedural tensor ids; the oracle tests use the same ids.
 namespace tid {
@@ -206,6 +212,13 @@ struct Engine {
   // lossless expert codec on the link (xfer.cu): coded blocks cross into
   // cstage and are expanded into the pool slot on the compute stream
   bool xcomp = false;
+  // T2 tile code (tcode.cuh; compress_experts = 2 or SMO_CODEC=tile): every
+  // block crosses the link and sits in HBM (staging and hot cache) in the
+  // tile code, and K4-MoE decodes it in shared memory (moe_coded_launch):
+  // no expansion launch, no bf16 copy of an expert in HBM
+  bool tmode = false;
+  const void** d_w_code = nullptr;      // [L*E] code block of (layer, expert)
+  const void** d_w_code_loc = nullptr;  // [L*E_loc] (expert parallelism)
   size_t cblk_bytes = 0;                  // coded bytes of one [W1|W3|W2] block at 4 bits (staging stride)
   std::vector<uint8_t> blk_coded;         // [host_alias * E_loc] code of the host block: 0 raw, 1 unary, 3 / 4 bits
   std::vector<size_t> blk_csize;          // [host_alias * E_loc] coded bytes of the host block
@@ -337,6 +350,10 @@ struct Engine {
   // expand layer l's coded blocks (streamed into cstage) into its pool slot,
   // on the compute stream after slot_ready(l)
   void decode_slot(int l, cudaStream_t st);
+  // the expert block of layer l: K4-MoE on the bf16 pool slot, or on the
+  // tile-coded blocks (tmode); returns the down-projection splits
+  int expert_block(int l, const void* x_perm, int rows, int nexp, const int32_t* offsets, const int32_t* w_index,
+                   const void* const* w_code, void* hb, float* y, int splits, int max_splits, cudaStream_t st);
 
   int host_layer(int l) const { return host_alias > 0 ? l % host_alias : l; }
   int expert_owner(int e) const { return opt.ep_size > 1 ? e % opt.ep_size : 0; }

@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "tcode.cuh"
@@ -54,6 +55,7 @@ struct MoeParams {
   size_t y_stride;         // rows * h
   int splits;
   int* done;               // [E] finished gate/up units (zero at launch)
+  int dbg;                 // coded kernel A/B: 1 no decode, 2 no token loads, 4 no code loads
 };
 
 struct Unit {
@@ -107,6 +109,7 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 // Warps 2..5 of both expert kernels: per unit, wait for the accumulators,
 // then SwiGLU -> H (gate/up units; publish with a release + done[e]) or the
 // fp32 down partial -> y[ks]; hand TMEM back to the MMA warp.
+template <int kCols>  // TMEM columns per load (16 under register pressure)
 __device__ __forceinline__ void epilogue_loop(const Schedule& S, const MoeParams& p, uint32_t tmem, int warp, int lane,
                                               uint64_t& tmem_full, uint64_t& tmem_empty) {
   const int q = warp & 3;
@@ -116,17 +119,23 @@ __device__ __forceinline__ void epilogue_loop(const Schedule& S, const MoeParams
   for (int u = blockIdx.x; u < S.total; u += gridDim.x, ++it) {
     const Unit x = unit_at(S, u);
     const int n_pad = (x.cnt + 15) & ~15;
-    mbar_wait(&tmem_full, it & 1);
+    if (kCols == 16) mbar_wait_backoff(&tmem_full, it & 1, 256);  // coded kernel: leave the issue slots to the decoders
+    else mbar_wait(&tmem_full, it & 1);
     tc_fence_after();
     if (!x.down) {
       const int n = x.nb * 128 + row;  // intermediate feature
-      for (int c0 = 0; c0 < n_pad; c0 += 32) {
-        uint32_t g[32], v[32];
-        tmem_ld32(trow + c0, g);
-        tmem_ld32(trow + 256 + c0, v);
+      for (int c0 = 0; c0 < n_pad; c0 += kCols) {
+        uint32_t g[kCols], v[kCols];
+        if constexpr (kCols == 32) {
+          tmem_ld32(trow + c0, g);
+          tmem_ld32(trow + 256 + c0, v);
+        } else {
+          tmem_ld16(trow + c0, g);
+          tmem_ld16(trow + 256 + c0, v);
+        }
         tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
+        for (int j = 0; j < kCols; ++j)
           if (c0 + j < x.cnt) {
             const float gv = __uint_as_float(g[j]);
             p.hbuf[size_t(x.row0 + c0 + j) * p.hi + n] = f2bf(gv / (1.0f + __expf(-gv)) * __uint_as_float(v[j]));
@@ -136,12 +145,13 @@ __device__ __forceinline__ void epilogue_loop(const Schedule& S, const MoeParams
     } else {
       const int n = x.nb * 128 + row;  // output feature
       float* y = p.y + size_t(x.ks) * p.y_stride;
-      for (int c0 = 0; c0 < n_pad; c0 += 32) {
-        uint32_t r[32];
-        tmem_ld32(trow + c0, r);
+      for (int c0 = 0; c0 < n_pad; c0 += kCols) {
+        uint32_t r[kCols];
+        if constexpr (kCols == 32) tmem_ld32(trow + c0, r);
+        else tmem_ld16(trow + c0, r);
         tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
+        for (int j = 0; j < kCols; ++j)
           if (c0 + j < x.cnt) y[size_t(x.row0 + c0 + j) * p.h + n] = __uint_as_float(r[j]);
       }
     }
@@ -305,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    epilogue_loop(S, p, tmem, warp, lane, tmem_full, tmem_empty);
+    epilogue_loop<32>(S, p, tmem, warp, lane, tmem_full, tmem_empty);
   }
   tc_fence_before();
   __syncthreads();
@@ -329,6 +339,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 // The A ring (kAS stages of W1 | W3 | token rows) is released by the MMA
 // commit, the code ring by the kND decoder arrivals.
 constexpr int kCodeSlot = tcode::kTileMax;  // 16416 B: the largest tile code
+
+// Down units with <= 128 token rows take two W2 k-blocks per stage (both code
+// slots and both halves of the token region are free), so all decoder warps
+// have a segment in every stage.
+__device__ __forceinline__ bool down_pair(const Unit& x, int KBd) {
+  return x.down && x.cnt <= 128 && (KBd % 2) == 0;
+}
 
 template <int kND, int kAS, int kCS>
 __global__ void __launch_bounds__(kThreads + 32 * kND, 1)
@@ -372,30 +389,50 @@ __global__ void __launch_bounds__(kThreads + 32 * kND, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ code producer
-    if (elect_one()) {
-      int g = 0;
-      for (int u = blockIdx.x; u < S.total; u += gridDim.x) {
-        const Unit x = unit_at(S, u);
-        const uint8_t* blk = w_code[x.e];
-        const uint32_t* toff = reinterpret_cast<const uint32_t*>(blk);
-        const int KB = x.down ? KBd : KBa;
-        const int kb0 = x.down ? x.ks * KBd : 0;
-        // tile (matrix, row tile, k-block): W1 / W3 rows of h_i (h / 64 k-blocks), W2 rows of h (h_i / 64)
-        const int t0 = x.down ? 2 * tiles + x.nb * (p.hi / kBK) + kb0 : x.nb * (p.h / kBK);
-        for (int kb = 0; kb < KB; ++kb, ++g) {
-          const int s = g % kCS;
-          mbar_wait(&c_empty[s], ((g / kCS) & 1) ^ 1);
-          uint8_t* dst = cring + size_t(s) * 2 * kCodeSlot;
-          const uint32_t a0 = toff[t0 + kb], a1 = toff[t0 + kb + 1];
-          if (x.down) {
-            mbar_arrive_expect_tx(&c_full[s], a1 - a0);
-            bulk_load(dst, blk + a0, a1 - a0, &c_full[s]);
-          } else {
-            const uint32_t b0 = toff[tiles + t0 + kb], b1 = toff[tiles + t0 + kb + 1];
-            mbar_arrive_expect_tx(&c_full[s], (a1 - a0) + (b1 - b0));
-            bulk_load(dst, blk + a0, a1 - a0, &c_full[s]);
-            bulk_load(dst + kCodeSlot, blk + b0, b1 - b0, &c_full[s]);
+    // The whole warp reads the unit's tile offsets 32 tiles at a time
+    // (coalesced; consecutive tiles of a unit are contiguous in the code, so
+    // tile i ends where i + 1 starts) and lane 0 issues the bulk copies: a
+    // stage holds W1 + W3 tile kb (gate/up), W2 tiles kb, kb + 1 (paired down
+    // units) or W2 tile kb.
+    int g = 0;
+    for (int u = blockIdx.x; u < S.total; u += gridDim.x) {
+      const Unit x = unit_at(S, u);
+      const uint8_t* blk = w_code[x.e];
+      const uint32_t* toff = reinterpret_cast<const uint32_t*>(blk);
+      const int KB = x.down ? KBd : KBa;
+      const int kb0 = x.down ? x.ks * KBd : 0;
+      const bool pair = down_pair(x, KBd);
+      // tile (matrix, row tile, k-block): W1 / W3 rows of h_i (h / 64 k-blocks), W2 rows of h (h_i / 64)
+      const int t0 = x.down ? 2 * tiles + x.nb * (p.hi / kBK) + kb0 : x.nb * (p.h / kBK);
+      for (int c0 = 0; c0 < KB; c0 += 32) {
+        const int nc = min(32, KB - c0);
+        const uint32_t a = lane < nc ? toff[t0 + c0 + lane] : 0u, a_end = toff[t0 + c0 + nc];
+        const uint32_t b = (!x.down && lane < nc) ? toff[tiles + t0 + c0 + lane] : 0u;
+        const uint32_t b_end = x.down ? 0u : toff[tiles + t0 + c0 + nc];
+        for (int k = 0; k < nc; k += pair ? 2 : 1, ++g) {
+          auto at = [&](uint32_t v, uint32_t end, int i) {
+            const uint32_t r = __shfl_sync(0xffffffffu, v, i & 31);
+            return i < nc ? r : end;
+          };
+          const uint32_t a0 = at(a, a_end, k), a1 = at(a, a_end, k + 1), a2 = at(a, a_end, k + 2);
+          const uint32_t b0 = at(b, b_end, k), b1 = at(b, b_end, k + 1);
+          if (lane == 0) {
+            const int s = g % kCS;
+            mbar_wait(&c_empty[s], ((g / kCS) & 1) ^ 1);
+            uint8_t* dst = cring + size_t(s) * 2 * kCodeSlot;
+            if (p.dbg & 4) {
+              mbar_arrive(&c_full[s]);
+            } else if (pair) {
+              mbar_arrive_expect_tx(&c_full[s], a2 - a0);
+              bulk_load(dst, blk + a0, a1 - a0, &c_full[s]);
+              bulk_load(dst + kCodeSlot, blk + a1, a2 - a1, &c_full[s]);
+            } else {
+              mbar_arrive_expect_tx(&c_full[s], (a1 - a0) + (x.down ? 0u : b1 - b0));
+              bulk_load(dst, blk + a0, a1 - a0, &c_full[s]);
+              if (!x.down) bulk_load(dst + kCodeSlot, blk + b0, b1 - b0, &c_full[s]);
+            }
           }
+          __syncwarp();
         }
       }
     }
@@ -406,11 +443,13 @@ __global__ void __launch_bounds__(kThreads + 32 * kND, 1)
       for (int u = blockIdx.x; u < S.total; u += gridDim.x, ++it) {
         const Unit x = unit_at(S, u);
         const int n_pad = (x.cnt + 15) & ~15;
+        const uint32_t xb = uint32_t(((x.cnt + 31) & ~31) * 128);  // token rows of one k-block
         const uint32_t idesc = make_idesc_bf16(128, n_pad);
-        const int KB = x.down ? KBd : KBa;
+        const bool pair = down_pair(x, KBd);
+        const int KS = x.down ? (pair ? KBd / 2 : KBd) : KBa;
         mbar_wait(&tmem_empty, (it & 1) ^ 1);
         tc_fence_after();
-        for (int kb = 0; kb < KB; ++kb, ++g) {
+        for (int kb = 0; kb < KS; ++kb, ++g) {
           const int s = g % kAS;
           mbar_wait(&a_full[s], (g / kAS) & 1);
           tc_fence_after();
@@ -418,12 +457,20 @@ __global__ void __launch_bounds__(kThreads + 32 * kND, 1)
           const uint64_t ad = make_sdesc_sw128(a_addr, 16, 1024);
           const uint64_t au = make_sdesc_sw128(a_addr + kTileA, 16, 1024);
           const uint64_t bd = make_sdesc_sw128(a_addr + 2 * kTileA, 16, 1024);
+          const uint64_t bd2 = make_sdesc_sw128(a_addr + 2 * kTileA + xb, 16, 1024);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
             const uint64_t ko = uint64_t((k * 32) >> 4);
             umma_bf16(tmem, ad + ko, bd + ko, idesc, acc);
             if (!x.down) umma_bf16(tmem + 256, au + ko, bd + ko, idesc, acc);
+          }
+          if (pair) {  // second k-block of the stage: W2 tile kb + 1 with its token rows
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint64_t ko = uint64_t((k * 32) >> 4);
+              umma_bf16(tmem, au + ko, bd2 + ko, idesc, 1u);
+            }
           }
           umma_commit(&a_empty[s]);
         }
@@ -432,7 +479,7 @@ __global__ void __launch_bounds__(kThreads + 32 * kND, 1)
     }
   } else if (warp < 6) {
     // ------------------------------------------------------------ epilogue
-    epilogue_loop(S, p, tmem, warp, lane, tmem_full, tmem_empty);
+    epilogue_loop<(kND > 8 ? 16 : 32)>(S, p, tmem, warp, lane, tmem_full, tmem_empty);
   } else {
     // ------------------------------------------------------------ decoders
     const int d = warp - 6;
@@ -440,8 +487,10 @@ __global__ void __launch_bounds__(kThreads + 32 * kND, 1)
     for (int u = blockIdx.x; u < S.total; u += gridDim.x) {
       const Unit x = unit_at(S, u);
       const int n_load = (x.cnt + 31) & ~31;
-      const int KB = x.down ? KBd : KBa;
+      const bool pair = down_pair(x, KBd);
+      const int KS = x.down ? (pair ? KBd / 2 : KBd) : KBa;
       const int kb0 = x.down ? x.ks * KBd : 0;
+      const int ntile = (!x.down || pair) ? 2 : 1;
       if (d == 0 && x.down && lane == 0) {
         // every gate/up unit of expert e has published its H rows
         const int need = ((S.off[x.e + 1] - S.off[x.e] + kTok - 1) / kTok) * S.nA;
@@ -449,28 +498,30 @@ __global__ void __launch_bounds__(kThreads + 32 * kND, 1)
         }
         fence_proxy_async_global();
       }
-      for (int kb = 0; kb < KB; ++kb, ++g) {
+      for (int kb = 0; kb < KS; ++kb, ++g) {
         const int sa = g % kAS, sc = g % kCS;
         uint8_t* st = smem + sa * kAStage;
         mbar_wait(&a_empty[sa], ((g / kAS) & 1) ^ 1);
-        if (d == 0 && lane == 0) {
-          mbar_arrive_expect_tx(&a_full[sa], uint32_t((n_load / 32) * 4096));
-          const int kc = (kb0 + kb) * kBK;
-          for (int i = 0; i < n_load / 32; ++i)
-            tma_load_2d(st + 2 * kTileA + i * 4096, x.down ? &tm_h : &tm_x, &a_full[sa], kc, x.row0 + i * 32);
+        if (d == 0 && lane == 0 && (p.dbg & 2)) {
+          mbar_arrive(&a_full[sa]);
+        } else if (d == 0 && lane == 0) {
+          const int nkb = pair ? 2 : 1;
+          mbar_arrive_expect_tx(&a_full[sa], uint32_t(nkb * (n_load / 32) * 4096));
+          for (int j = 0; j < nkb; ++j) {
+            const int kc = (kb0 + kb * nkb + j) * kBK;
+            for (int i = 0; i < n_load / 32; ++i)
+              tma_load_2d(st + 2 * kTileA + j * n_load * 128 + i * 4096, x.down ? &tm_h : &tm_x, &a_full[sa], kc,
+                          x.row0 + i * 32);
+          }
         }
         mbar_wait(&c_full[sc], (g / kCS) & 1);
         const uint8_t* code = cring + size_t(sc) * 2 * kCodeSlot;
+        if (!(p.dbg & 1)) {
+          // kND = 8: warp d decodes segment d of each tile; kND = 16: warp d
+          // segment d % 8 of tile d / 8 (single-tile stages: warps 0..7)
 #pragma unroll 1
-        for (int m = 0; m < (x.down ? 1 : 2); ++m) {
-          const uint8_t* tc = code + m * kCodeSlot;
-          const uint32_t* hdr = reinterpret_cast<const uint32_t*>(tc);
-#pragma unroll 1
-          for (int sg = d; sg < tcode::kSegs; sg += kND) {
-            uint32_t off = 32;
-            for (int k = 0; k < sg; ++k) off += (hdr[k] >> 16) * 16;
-            tcode::decode_segment(tc + off, hdr[sg], st + m * kTileA, sg, lane);
-          }
+          for (int m = kND > 8 ? d / 8 : 0; m < ntile; m += kND > 8 ? 2 : 1)
+            tcode::decode_segment(code + m * kCodeSlot, st + m * kTileA, d % 8, lane, (p.dbg & 8) ? ~0xe00u : ~0u);
         }
         fence_proxy_async();  // the stores above feed the tensor core (async proxy)
         __syncwarp();
@@ -637,17 +688,32 @@ int moe_coded_launch(const void* x_perm, int rows, int h, int hi, int E, const i
   p.y_stride = size_t(rows) * h;
   p.splits = splits;
   p.done = done;
-  constexpr int kND = 8, kAS = 2, kCS = 2;
-  auto kern = moe_coded_kernel<kND, kAS, kCS>;
-  const size_t smem = size_t(kAS) * (2 * kTileA + kTok * 128) + size_t(kCS) * 2 * kCodeSlot + 1024;
-  static bool attr_set = false;
-  if (!attr_set) {
+  p.dbg = std::getenv("SMO_MOE_CODED_DBG") ? std::atoi(std::getenv("SMO_MOE_CODED_DBG")) : 0;
+  // decoder warps / A stages / code stages (SMO_MOE_CODED=<nd>,<as>,<cs> for A/B runs)
+  static int variant = [] {
+    const char* f = std::getenv("SMO_MOE_CODED");
+    if (f && std::strcmp(f, "8,2,2") == 0) return 1;
+    if (f && std::strcmp(f, "16,2,2") == 0) return 2;
+    if (f && std::strcmp(f, "8,2,3") == 0) return 3;
+    return 0;
+  }();
+  void (*kern)(const CUtensorMap, const CUtensorMap, MoeParams, const uint8_t* const*) = nullptr;
+  int nd = 0, as = 0, cs = 0;
+  switch (variant) {
+    case 1: kern = moe_coded_kernel<8, 2, 2>, nd = 8, as = 2, cs = 2; break;
+    case 2: kern = moe_coded_kernel<16, 2, 2>, nd = 16, as = 2, cs = 2; break;
+    case 3: kern = moe_coded_kernel<8, 2, 3>, nd = 8, as = 2, cs = 3; break;
+    default: kern = moe_coded_kernel<16, 2, 2>, nd = 16, as = 2, cs = 2; break;
+  }
+  const size_t smem = size_t(as) * (2 * kTileA + kTok * 128) + size_t(cs) * 2 * kCodeSlot + 1024;
+  static bool attr_set[4] = {false, false, false, false};
+  if (!attr_set[variant]) {
     SMO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr_set = true;
+    attr_set[variant] = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(unsigned(sm_count()));
-  cfg.blockDim = dim3(kThreads + 32 * kND);
+  cfg.blockDim = dim3(unsigned(kThreads + 32 * nd));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];

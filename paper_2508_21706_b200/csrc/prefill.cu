@@ -170,8 +170,8 @@ void Engine::prefill(const int32_t* tok_h, const int32_t* len_h, int b, int Lmax
     SMO_CUDA_CHECK(cudaStreamWaitEvent(st, slot_ready[l % slots], 0));
     decode_slot(l, st);
     if (moe_fused) {
-      moe_launch(p_xp, PT, h, hi, E, p_off, pool, blk_bytes, pool_blocks, d_w_index + size_t(l) * E, p_hb, p_y,
-                 pf_splits, pf_splits, d_done, st);
+      expert_block(l, p_xp, PT, E, p_off, d_w_index + size_t(l) * E, tmode ? d_w_code + size_t(l) * E : nullptr, p_hb,
+                   p_y, pf_splits, pf_splits, st);
     } else {
     smo_gemm_args g2{};
     g2.x = p_xp;

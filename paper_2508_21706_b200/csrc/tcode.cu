@@ -44,19 +44,23 @@ __device__ __forceinline__ TileAt tile_at(const TMats& M, int t) {
   return TileAt{m, tl / kbs, tl % kbs};
 }
 
-// level count of a value (5 for literals) for base E
-__device__ __forceinline__ int levels_of(int j) { return (j < 0 || j >= 15) ? 5 : j / 3 + 1; }
+// code class of an exponent offset j: 0 level 1 (j <= 2), 1 level 2
+// (3..5), 2 nibble (6..20), 3 literal; bits 2, 4, 8, 16
+__device__ __forceinline__ int class_of(int j) {
+  return (j >= 0 && j <= 2) ? 0 : (j >= 3 && j <= 5) ? 1 : (j >= 6 && j <= 20) ? 2 : 3;
+}
 
 constexpr int kEncWarps = 8;
 
-// Pass 1 (write = false): header word of every segment into meta[]. Pass 2:
-// meta[] + the tile table at the head of dst (written by the host between the
-// passes) -> tile headers and segment bodies. One warp per segment, lane L
-// owns values 32 L .. 32 L + 31 (row L / 2 of the segment, half L % 2).
+// Pass 1 (write = false): per segment E | flags << 8 | (stream bytes / 4)
+// << 12 into meta[]. The host then turns stream sizes into offsets (and
+// marks incompressible tiles raw) and rewrites meta[] with the final header
+// words. Pass 2 writes the tiles. One warp per segment, lane L owns values
+// 32 L .. 32 L + 31 (row L / 2 of the segment, half L % 2).
 __global__ void __launch_bounds__(32 * kEncWarps) tcode_encode_kernel(const __grid_constant__ TMats M, int segs,
                                                                       uint32_t* __restrict__ meta,
                                                                       uint8_t* __restrict__ dst, bool write) {
-  __shared__ uint32_t fw[kEncWarps][256];  // level fields of the warp's segment (<= 4 x 1024 x 2 bits)
+  __shared__ uint32_t fw[kEncWarps][64 + 128];  // L2 (<= 1024 x 2 bits) and L3 (<= 1024 x 4 bits) words
   const int wib = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int g = blockIdx.x * kEncWarps + wib;
   if (g >= segs) return;
@@ -77,24 +81,19 @@ __global__ void __launch_bounds__(32 * kEncWarps) tcode_encode_kernel(const __gr
   }
   auto val = [&](int i) -> uint32_t { return (v2[i >> 1] >> (16 * (i & 1))) & 0xffffu; };
   auto expo = [&](int i) -> int { return int((val(i) >> 7) & 0xffu); };
-  uint32_t hw;
   if (!write) {
     int emax = 0;
 #pragma unroll
     for (int i = 0; i < 32; ++i) emax = max(emax, expo(i));
 #pragma unroll
     for (int o = 16; o; o >>= 1) emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
-    int E = max(emax, 3), best = -1;
+    int E = max(emax, 6), best = -1;
     for (int c = 0; c < 8; ++c) {
       const int b0 = emax - c;
-      if (b0 < 3) break;  // warp-uniform
+      if (b0 < 6) break;  // warp-uniform (E >= 6: no borrow in the decoder's E - c1 - c2)
       int cost = 0;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int j = b0 - expo(i);
-        const int n = levels_of(j);
-        cost += 2 * n + ((j < 0 || j >= 15) ? 8 : 0);
-      }
+      for (int i = 0; i < 32; ++i) cost += 2 << class_of(b0 - expo(i));
 #pragma unroll
       for (int o = 16; o; o >>= 1) cost += __shfl_xor_sync(0xffffffffu, cost, o);
       if (best < 0 || cost < best) {
@@ -102,93 +101,88 @@ __global__ void __launch_bounds__(32 * kEncWarps) tcode_encode_kernel(const __gr
         E = b0;
       }
     }
-    int nf = 0, nl = 0, esc = 0;
+    int n2 = 0, n3 = 0, nl = 0;
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-      const int j = E - expo(i);
-      const int n = levels_of(j);
-      nf += n - 1;
-      nl += (j < 0 || j >= 15) ? 1 : 0;
-      esc |= n > 1 ? 1 : 0;
+      const int k = class_of(E - expo(i));
+      n2 += k >= 1;
+      n3 += k >= 2;
+      nl += k == 3;
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
-      nf += __shfl_xor_sync(0xffffffffu, nf, o);
+      n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+      n3 += __shfl_xor_sync(0xffffffffu, n3, o);
       nl += __shfl_xor_sync(0xffffffffu, nl, o);
-      esc |= __shfl_xor_sync(0xffffffffu, esc, o);
     }
-    const int bytes = (kLvOff + 4 * ((nf + 15) / 16) + nl + 15) & ~15;
-    hw = bytes >= kRawBytes ? (1u << 8) | (uint32_t(kRawBytes / 16) << 16)
-                            : uint32_t(E) | (uint32_t(esc ? 2 : 0) << 8) | (uint32_t(bytes / 16) << 16);
-    if (lane == 0) meta[g] = hw;
+    const uint32_t words = uint32_t((n2 + 15) / 16 + (n3 + 7) / 8 + (nl + 3) / 4);
+    const uint32_t flags = (n2 ? 2u : 0u) | (n3 ? 4u : 0u) | (nl ? 8u : 0u);
+    if (lane == 0) meta[g] = uint32_t(E) | (flags << 8) | (words << 12);
     return;
   }
-  hw = meta[g];
-  const uint32_t toff = reinterpret_cast<const uint32_t*>(dst)[t];
-  uint32_t soff = toff + 32;
-  for (int k = 0; k < s; ++k) soff += (meta[t * kSegs + k] >> 16) * 16;
-  uint8_t* sg = dst + soff;
-  if (lane == 0) reinterpret_cast<uint32_t*>(dst + toff)[s] = hw;
-  const int bytes = int(hw >> 16) * 16;
-  if (hw & 0x100u) {
-    uint4* d = reinterpret_cast<uint4*>(sg) + 4 * lane;
+  const uint32_t hw = meta[g];
+  uint8_t* tb = dst + reinterpret_cast<const uint32_t*>(dst)[t];
+  if (hw & 0x100u) {  // raw tile: the header, then the segment's 16 rows verbatim
+    uint4* d = reinterpret_cast<uint4*>(tb + 32 + 2 * kSeg * s) + 4 * lane;
 #pragma unroll
     for (int i = 0; i < 4; ++i) d[i] = make_uint4(v2[4 * i], v2[4 * i + 1], v2[4 * i + 2], v2[4 * i + 3]);
+    if (lane == 0) reinterpret_cast<uint32_t*>(tb)[s] = s == 0 ? 0x100u : 0u;
     return;
   }
+  if (lane == 0) reinterpret_cast<uint32_t*>(tb)[s] = hw;
   const int E = int(hw & 0xffu);
-  // lo bytes and level-1 codes
   uint32_t lo[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}, l1[2] = {0u, 0u};
-  int cnt[6] = {0, 0, 0, 0, 0, 0};  // values with >= k levels (k = 2..5), literals in [1]
+  int n2 = 0, n3 = 0, nl = 0;
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
     const uint32_t x = val(i);
     lo[i >> 2] |= (((x >> 8) & 0x80u) | (x & 0x7fu)) << (8 * (i & 3));
     const int j = E - expo(i);
-    const int n = levels_of(j);
-    const uint32_t c1 = n > 1 ? 3u : uint32_t(j);
+    const int k = class_of(j);
+    const uint32_t c1 = k ? 3u : uint32_t(j);
     const int ii = i & 15;
     l1[i >> 4] |= c1 << (2 * (ii >> 1) + 16 * (ii & 1));
-#pragma unroll
-    for (int k = 2; k <= 5; ++k) cnt[k] += n >= k ? 1 : 0;
-    cnt[1] += (j < 0 || j >= 15) ? 1 : 0;
+    n2 += k >= 1;
+    n3 += k >= 2;
+    nl += k == 3;
   }
-  reinterpret_cast<uint4*>(sg)[2 * lane] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-  reinterpret_cast<uint4*>(sg)[2 * lane + 1] = make_uint4(lo[4], lo[5], lo[6], lo[7]);
-  reinterpret_cast<uint2*>(sg + kL1Off)[lane] = make_uint2(l1[0], l1[1]);
-  uint32_t* wd = fw[wib];
-  for (int k = lane; k < 256; k += 32) wd[k] = 0u;
+  reinterpret_cast<uint4*>(tb + kLoOff + kSeg * s)[2 * lane] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  reinterpret_cast<uint4*>(tb + kLoOff + kSeg * s)[2 * lane + 1] = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+  reinterpret_cast<uint2*>(tb + kL1Off + 256 * s)[lane] = make_uint2(l1[0], l1[1]);
+  uint32_t* w2 = fw[wib];
+  uint32_t* w3 = fw[wib] + 64;
+  for (int k = lane; k < 64 + 128; k += 32) fw[wib][k] = 0u;
   __syncwarp();
-  int base = 0;
-#pragma unroll 1
-  for (int k = 2; k <= 5; ++k) {
-    int tot = 0;
-    int f = base + warp_excl_scan(cnt[k], lane, &tot);
-    for (int i = 0; i < 32; ++i) {
-      const int j = E - expo(i);
-      const int n = levels_of(j);
-      if (n < k) continue;
-      const bool lit = j < 0 || j >= 15;
-      const uint32_t c = (lit || n > k) ? 3u : uint32_t(j - 3 * (k - 1));
-      atomicOr(&wd[f >> 4], c << (2 * (f & 15)));
-      ++f;
-    }
-    base += tot;
-  }
-  __syncwarp();
-  const int nw = (base + 15) / 16;
-  uint32_t* lvp = reinterpret_cast<uint32_t*>(sg + kLvOff);
-  for (int k = lane; k < nw; k += 32) lvp[k] = wd[k];
-  int ltot = 0;
-  int lf = warp_excl_scan(cnt[1], lane, &ltot);
-  uint8_t* lit = sg + kLvOff + 4 * nw;
+  int t2 = 0, t3 = 0, tl = 0;
+  int f2 = warp_excl_scan(n2, lane, &t2), f3 = warp_excl_scan(n3, lane, &t3), fl = warp_excl_scan(nl, lane, &tl);
+  uint8_t* stp = tb + 4 * (hw >> 12);
+  const int nw2 = (t2 + 15) / 16, nw3 = (t3 + 7) / 8;
+  uint8_t* lit = stp + 4 * (nw2 + nw3);
   for (int i = 0; i < 32; ++i) {
     const int e = expo(i);
     const int j = E - e;
-    if (j < 0 || j >= 15) lit[lf++] = uint8_t(e);
+    const int k = class_of(j);
+    if (k >= 1) {
+      atomicOr(&w2[f2 >> 4], (k == 1 ? uint32_t(j - 3) : 3u) << (2 * (f2 & 15)));
+      ++f2;
+    }
+    if (k >= 2) {
+      atomicOr(&w3[f3 >> 3], (k == 2 ? uint32_t(j - 6) : 15u) << (4 * (f3 & 7)));
+      ++f3;
+    }
+    if (k == 3) lit[fl++] = uint8_t(e);
   }
-  const int used = kLvOff + 4 * nw + ltot;
-  if (lane < bytes - used) sg[used + lane] = 0;  // deterministic padding (< 16 bytes)
+  __syncwarp();
+  uint32_t* sw = reinterpret_cast<uint32_t*>(stp);
+  for (int k = lane; k < nw2; k += 32) sw[k] = w2[k];
+  for (int k = lane; k < nw3; k += 32) sw[nw2 + k] = w3[k];
+  const int lpad = ((tl + 3) & ~3) - tl;
+  if (lane < lpad) lit[tl + lane] = 0;
+  if (s == kSegs - 1) {  // tile padding to 16 bytes
+    const uint8_t* end = lit + tl + lpad;
+    const uint8_t* tend = dst + reinterpret_cast<const uint32_t*>(dst)[t + 1];
+    if (lane < int(tend - end)) const_cast<uint8_t*>(end)[lane] = 0;
+  }
 }
 
 // One CTA per tile: stage the tile code in shared memory, eight warps decode
@@ -208,10 +202,7 @@ __global__ void __launch_bounds__(256) tcode_decode_kernel(const __grid_constant
   for (uint32_t i = threadIdx.x; i < (o1 - o0) / 16; i += blockDim.x) reinterpret_cast<uint4*>(code)[i] = g[i];
   __syncthreads();
   const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t* hdr = reinterpret_cast<const uint32_t*>(code);
-  uint32_t off = 32;
-  for (int k = 0; k < w; ++k) off += (hdr[k] >> 16) * 16;
-  decode_segment(code + off, hdr[w], tile, w, lane);
+  decode_segment(code, tile, w, lane);
   __syncthreads();
   const TileAt ta = tile_at(M, t);
   const int C = M.C[ta.m];
@@ -253,12 +244,27 @@ size_t tcode_encode(const void* src, int h, int hi, void* dst, cudaStream_t st) 
   size_t off = tb;
   for (int t = 0; t < nt; ++t) {
     head[size_t(t)] = uint32_t(off);
-    off += 32;
-    for (int s = 0; s < kSegs; ++s) off += (hm[size_t(t) * kSegs + s] >> 16) * 16;
+    uint32_t* mt = hm.data() + size_t(t) * kSegs;
+    size_t sz = kStreamOff;
+    for (int s = 0; s < kSegs; ++s) sz += 4 * size_t(mt[s] >> 12);
+    sz = (sz + 15) & ~size_t(15);
+    if (sz >= size_t(kTileMax)) {  // incompressible: the whole tile raw
+      for (int s = 0; s < kSegs; ++s) mt[s] = 0x100u;
+      sz = kTileMax;
+    } else {
+      uint32_t so = kStreamOff / 4;
+      for (int s = 0; s < kSegs; ++s) {
+        const uint32_t words = mt[s] >> 12;
+        mt[s] = (mt[s] & 0xfffu) | (so << 12);
+        so += words;
+      }
+    }
+    off += sz;
   }
   SMO_REQUIRE(off < (size_t(1) << 32), "tcode: block too large for 32-bit tile offsets");
   head[size_t(nt)] = uint32_t(off);
   SMO_CUDA_CHECK(cudaMemcpyAsync(d8, head.data(), tb, cudaMemcpyHostToDevice, st));
+  SMO_CUDA_CHECK(cudaMemcpyAsync(meta, hm.data(), hm.size() * 4, cudaMemcpyHostToDevice, st));
   tcode_encode_kernel<<<grid, 32 * kEncWarps, 0, st>>>(M, segs, meta, d8, true);
   count_launch();
   SMO_CUDA_CHECK(cudaGetLastError());

@@ -9,26 +9,29 @@
 //           one k-block of the expert kernel's A operand. u32 toff[nt + 1]
 //           (tile byte offsets from the block start; toff[nt] = total),
 //           zero-padded to 16 B, then the tiles (16-B aligned).
-//   tile    u32 hdr[8] (E | flags << 8 | size16 << 16; flags bit 0 raw,
-//           bit 1 some value escapes level 1; size16 = segment bytes / 16),
-//           then 8 segments of 16 rows x 64 columns.
-//   segment value order v = 64 r + c; "lane" L owns values 32 L .. 32 L + 31
-//           (row L / 2, columns 32 (L % 2) ..). Raw: 1024 bf16. Coded:
-//           lo[1024] (sign << 7 | mantissa), L1[256] (2-bit level-1 codes:
-//           lane L's word w at byte 8 L + 4 w holds value 16 w + 2 q at bits
-//           2 q and value 16 w + 2 q + 1 at bits 16 + 2 q), the level stream
-//           (2-bit fields LSB first: level-2 codes of the values whose level-1
-//           code is 3, in value order, then level 3, ... 5), literal exponent
-//           bytes (values whose five codes are all 3), zero padding to 16 B.
-//   value   j = E - e; 0 <= j <= 14: j // 3 + 1 levels (3 on all but the
-//           last, j - 3 (levels - 1) on the last); otherwise five 3s and a
-//           literal. E (>= 3) = the segment maximum or up to 7 below it with
-//           the fewest code bits; >= 2048 coded bytes -> raw.
+//   tile    8 segments of 16 rows x 64 columns. u32 hdr[8] (E | flags << 8
+//           | soff4 << 12; flags 1 raw tile, 2 some value leaves level 1,
+//           4 nibble level reached, 8 literals; soff4 = the segment's stream
+//           offset / 4), lo[8][1024] (sign << 7 | mantissa), L1[8][256]
+//           (2-bit level-1 codes: "lane" L of a segment owns values 32 L ..
+//           32 L + 31 = row L / 2, columns 32 (L % 2) ..; its word w at byte
+//           8 L + 4 w holds value 16 w + 2 q at bits 2 q and value
+//           16 w + 2 q + 1 at bits 16 + 2 q), then per segment a 4-B aligned
+//           stream: L2 (2-bit fields, LSB first, for the values whose level-1
+//           code is 3, value order), L3 (4-bit nibbles for the values whose
+//           level-2 code is 3), literal exponent bytes (nibble 15), zero
+//           padding to 4; the tile is padded to 16 B. A raw tile (hdr[0] =
+//           1 << 8, other words 0) is the header + 128 x 64 bf16 row-major.
+//   value   j = E - e: j <= 2 is its level-1 code; 3..5 codes 3, j - 3;
+//           6..20 codes 3, 3, nibble j - 6; otherwise 3, 3, 15 + literal
+//           (2, 4, 8, 16 bits). E (>= 6) = the segment maximum or up to 7
+//           below it with the fewest code bits.
 // Uniform-init weights: ~10.4 bits per weight (the unary code of xfer.cu:
-// 10.25), gaussian-like: ~10.9 (unary: 11.45). What it buys is the decoder:
-// level 1 is a fixed 2-bit field per value, so 30 of every 32 values decode
-// with 5 integer ops per pair and no serial dependence; only the ~1/8 of
-// values that escape level 1 take a short ranked walk.
+// 10.25), gaussian-like: ~11.0 (unary: 11.45). What it buys is the decoder:
+// level 1 is a fixed 2-bit field per value, so every value decodes with 5
+// integer ops per pair and no serial dependence; the ~1/7 of values that
+// leave level 1 are ranked with one ballot scan per level and rewritten
+// from registers.
 #pragma once
 
 #include <stdint.h>
@@ -38,11 +41,11 @@ namespace smo {
 namespace tcode {
 
 constexpr int kTileRows = 128, kTileCols = 64, kSegRows = 16, kSegs = 8;
-constexpr int kSeg = kSegRows * kTileCols;         // 1024 values
-constexpr int kRawBytes = 2 * kSeg;                // 2048
-constexpr int kL1Off = kSeg;                       // L1 codes after lo
-constexpr int kLvOff = kSeg + 256;                 // level stream
-constexpr int kTileMax = 32 + kSegs * kRawBytes;   // 16416: the largest tile code
+constexpr int kSeg = kSegRows * kTileCols;        // 1024 values
+constexpr int kLoOff = 32;                        // lo[8][1024] after the header
+constexpr int kL1Off = kLoOff + kSegs * kSeg;     // L1[8][256]
+constexpr int kStreamOff = kL1Off + kSegs * 256;  // 10272: first segment stream
+constexpr int kTileMax = 32 + 2 * kTileRows * kTileCols;  // 16416: a raw tile, the largest
 
 __device__ __forceinline__ int warp_excl_scan(int v, int lane, int* total) {
   int x = v;
@@ -55,86 +58,141 @@ __device__ __forceinline__ int warp_excl_scan(int v, int lane, int* total) {
   return x - v;
 }
 
-// Decode segment s of a tile (code in shared memory at `seg`, header word hw)
-// into the 128B-swizzled bf16 tile at `tile` (128 rows of 128 B, 1024-B
-// aligned; 16-B chunk c of row r at (c ^ (r & 7)) — what TMA SWIZZLE_128B
-// writes and the UMMA descriptors read). One warp; every lane writes its
-// half-row with four 16-B stores, escaped values are then patched in place.
-__device__ __forceinline__ void decode_segment(const uint8_t* __restrict__ seg, uint32_t hw, uint8_t* tile, int s,
-                                               int lane) {
+// Exclusive warp prefix sum of v in [0, 63] from six bit-plane ballots: no
+// shuffle chain, so its latency is one ballot + popcounts.
+__device__ __forceinline__ int warp_excl_scan_small(int v, int lane, int* total) {
+  const uint32_t lt = (1u << lane) - 1u;
+  int pre = 0, tot = 0;
+#pragma unroll
+  for (int b = 0; b < 6; ++b) {
+    const uint32_t bal = __ballot_sync(0xffffffffu, (v >> b) & 1);
+    pre += __popc(bal & lt) << b;
+    tot += __popc(bal) << b;
+  }
+  *total = tot;
+  return pre;
+}
+
+// Decode segment s of a tile whose code sits in shared memory at `tc` into
+// the 128B-swizzled bf16 tile at `tile` (128 rows of 128 B, 1024-B aligned;
+// 16-B chunk c of row r at (c ^ (r & 7)) — what TMA SWIZZLE_128B writes and
+// the UMMA descriptors read). One warp; every lane writes its half-row with
+// four 16-B stores, then rewrites the values that left level 1 (one warp scan
+// per level ranks the lanes' fields; each lane walks its own from a register
+// window).
+__device__ __forceinline__ void decode_segment(const uint8_t* __restrict__ tc, uint8_t* tile, int s, int lane,
+                                               uint32_t hw_mask = 0xffffffffu) {
   const int r = kSegRows * s + (lane >> 1);
   const int half = lane & 1;
   uint8_t* rowp = tile + r * 128;
   const int x = r & 7;
-  if (hw & 0x100u) {  // raw segment: lane L's 64 bytes are its half-row
-    const uint4* src = reinterpret_cast<const uint4*>(seg) + 4 * lane;
+  const uint32_t* hdr = reinterpret_cast<const uint32_t*>(tc);
+  if (hdr[0] & 0x100u) {  // raw tile: lane L's 64 bytes are its half-row
+    const uint4* src = reinterpret_cast<const uint4*>(tc + 32 + 2 * kSeg * s) + 4 * lane;
 #pragma unroll
     for (int k = 0; k < 4; ++k) *reinterpret_cast<uint4*>(rowp + (((4 * half + k) ^ x) << 4)) = src[k];
     return;
   }
+  const uint32_t hw = hdr[s] & hw_mask;
   const uint32_t E = hw & 0xffu;
-  const uint4 lo0 = reinterpret_cast<const uint4*>(seg)[2 * lane];
-  const uint4 lo1 = reinterpret_cast<const uint4*>(seg)[2 * lane + 1];
-  const uint2 cw = reinterpret_cast<const uint2*>(seg + kL1Off)[lane];
+  const uint8_t* lob = tc + kLoOff + kSeg * s;
+  const uint4 lo0 = reinterpret_cast<const uint4*>(lob)[2 * lane];
+  const uint4 lo1 = reinterpret_cast<const uint4*>(lob)[2 * lane + 1];
+  const uint2 cw = reinterpret_cast<const uint2*>(tc + kL1Off + 256 * s)[lane];
   const uint32_t lw[8] = {lo0.x, lo0.y, lo0.z, lo0.w, lo1.x, lo1.y, lo1.z, lo1.w};
   const uint32_t e2 = (E << 7) | (E << 23);
+  const uint32_t* st = reinterpret_cast<const uint32_t*>(tc + 4 * (hw >> 12));
+  // Level 2 first, into registers: the values whose level-1 code is 3 (bit i
+  // = value i of the lane) take their 2-bit code c2 from the lane's run of
+  // fields (consecutive from its rank; <= 16 sit in one register window) and
+  // deposit it in d0 / d1, laid out like the level-1 words, so the pair
+  // compose below subtracts both codes at once: e = E - c1 - c2 (E >= 6, so
+  // E - 6 never borrows). Per escape this is ALU work only.
+  uint32_t d0 = 0u, d1 = 0u, m3 = 0u;
+  int tot2 = 0;
+  if (hw & 0x200u) {  // warp-uniform
+    const uint32_t m0 = cw.x & (cw.x >> 1), m1 = cw.y & (cw.y >> 1);
+    const uint32_t m2 = ((m0 & 0x5555u) | ((m0 >> 15) & 0xAAAAu)) | (((m1 & 0x5555u) | ((m1 >> 15) & 0xAAAAu)) << 16);
+    const int n2 = __popc(m2);
+    const int r2 = warp_excl_scan(n2, lane, &tot2);
+    auto dep = [&](int i, uint32_t c) {
+      const uint32_t v = c << ((i & 14) | ((i & 1) << 4));
+      if (i < 16) d0 |= v;
+      else d1 |= v;
+      m3 |= (c == 3u ? 1u : 0u) << i;
+    };
+    if (__all_sync(0xffffffffu, n2 <= 16)) {
+      const int nw = (tot2 + 15) >> 4, wi = r2 >> 4;
+      const uint32_t w0 = wi < nw ? st[wi] : 0u, w1 = wi + 1 < nw ? st[wi + 1] : 0u;
+      uint32_t win = uint32_t(((uint64_t(w1) << 32) | w0) >> (2 * (r2 & 15)));
+      for (uint32_t mm = m2; mm; mm &= mm - 1u) {
+        dep(__ffs(mm) - 1, win & 3u);
+        win >>= 2;
+      }
+    } else {  // > 16 in some lane (wide-range data): fields from shared memory
+      int f = r2;
+      for (uint32_t mm = m2; mm; mm &= mm - 1u, ++f) dep(__ffs(mm) - 1, (st[f >> 4] >> (2 * (f & 15))) & 3u);
+    }
+  }
   uint32_t out[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
     // pair k = values 2k, 2k+1: codes at bits 2q and 16 + 2q of word k / 8,
     // moved to the exponent fields (bits 7-8 and 23-24) and subtracted from E
-    const uint32_t w = k < 8 ? cw.x : cw.y;
     const int q = k & 7;
+    const uint32_t w = k < 8 ? cw.x : cw.y, dw = k < 8 ? d0 : d1;
     const uint32_t cc = (q <= 3 ? (w << (7 - 2 * q)) : (w >> (2 * q - 7))) & 0x01800180u;
+    const uint32_t dd = (q <= 3 ? (dw << (7 - 2 * q)) : (dw >> (2 * q - 7))) & 0x01800180u;
     // two lo bytes -> 16-bit lanes with the sign replicated into the high byte
     const uint32_t t = __byte_perm(lw[k >> 1], 0u, (k & 1) ? 0xB3A2u : 0x9180u);
-    out[k] = (t & 0x807F807Fu) | (e2 - cc);
+    out[k] = (t & 0x807F807Fu) | (e2 - cc - dd);
   }
 #pragma unroll
   for (int k = 0; k < 4; ++k)
     *reinterpret_cast<uint4*>(rowp + (((4 * half + k) ^ x) << 4)) =
         make_uint4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
-  if (!(hw & 0x200u)) return;  // no value escapes level 1 (warp-uniform)
-  // values whose level-1 code is 3, as a value-indexed mask (bit i = value i)
-  const uint32_t m0 = cw.x & (cw.x >> 1), m1 = cw.y & (cw.y >> 1);
-  uint32_t m = ((m0 & 0x5555u) | ((m0 >> 15) & 0xAAAAu)) | (((m1 & 0x5555u) | ((m1 >> 15) & 0xAAAAu)) << 16);
-  const uint32_t* lv = reinterpret_cast<const uint32_t*>(seg + kLvOff);
-  auto at = [&](int i) -> uint16_t* {
-    return reinterpret_cast<uint16_t*>(rowp + (((4 * half + (i >> 3)) ^ x) << 4) + ((i & 7) << 1));
+  // value i of this lane rewritten whole with exponent e: its sign /
+  // mantissa byte from lo, at 16-B chunk (4 half + i / 8) ^ x of the row,
+  // i.e. byte ((hx << 3) ^ i) << 1 of the row with hx = 4 half ^ x
+  const uint8_t* mylo = lob + 32 * lane;
+  const int hx3 = ((4 * half) ^ x) << 3;
+  auto put = [&](int i, uint32_t e) {
+    const uint32_t lo = mylo[i];
+    *reinterpret_cast<uint16_t*>(rowp + ((hx3 ^ i) << 1)) = uint16_t(((lo & 0x80u) << 8) | (e << 7) | (lo & 0x7fu));
   };
-  int base = 0;  // fields of the earlier levels
-#pragma unroll 1
-  for (int lev = 2; lev <= 5; ++lev) {
-    int tot = 0;
-    int f = base + warp_excl_scan(__popc(m), lane, &tot);
-    if (tot == 0) break;
-    uint32_t next = 0u;
-    for (uint32_t mm = m; mm; mm &= mm - 1u) {
+  if (!(hw & 0x400u)) return;  // no value reaches the nibble level
+  // level 3: nibbles j - 6 of the values whose level-2 code is 3
+  const uint32_t* st3 = st + ((tot2 + 15) >> 4);
+  int tot3 = 0;
+  const int n3 = __popc(m3);
+  const int r3 = warp_excl_scan(n3, lane, &tot3);
+  uint32_t ml = 0u;
+  if (__all_sync(0xffffffffu, n3 <= 8)) {
+    const int nw = (tot3 + 7) >> 3, wi = r3 >> 3;
+    const uint32_t w0 = wi < nw ? st3[wi] : 0u, w1 = wi + 1 < nw ? st3[wi + 1] : 0u;
+    uint32_t win = uint32_t(((uint64_t(w1) << 32) | w0) >> (4 * (r3 & 7)));
+    for (uint32_t mm = m3; mm; mm &= mm - 1u) {
       const int i = __ffs(mm) - 1;
-      const uint32_t c = (lv[f >> 4] >> (2 * (f & 15))) & 3u;
-      ++f;
-      // the value ends here: j = 3 (lev - 1) + c, stored as E - 3 so far
-      // (e >= 0, so the subtraction never borrows into the sign)
-      const uint32_t dj = 3u * uint32_t(lev - 2) + c;
-      if (c != 3u && dj) {
-        uint16_t* p = at(i);
-        *p = uint16_t(*p - (dj << 7));
-      }
-      next |= (c == 3u ? 1u : 0u) << i;
+      const uint32_t c = win & 15u;
+      win >>= 4;
+      if (c == 15u) ml |= 1u << i;
+      else put(i, E - 6u - c);
     }
-    base += tot;
-    m = next;
-  }
-  // values whose five codes are all 3: literal exponent bytes, in value order
-  int tot = 0;
-  int f = warp_excl_scan(__popc(m), lane, &tot);
-  if (tot) {
-    const uint8_t* lit = reinterpret_cast<const uint8_t*>(lv + ((base + 15) >> 4));
-    for (uint32_t mm = m; mm; mm &= mm - 1u) {
-      uint16_t* p = at(__ffs(mm) - 1);
-      *p = uint16_t((*p & 0x807Fu) | (uint32_t(lit[f++]) << 7));
+  } else {
+    int f = r3;
+    for (uint32_t mm = m3; mm; mm &= mm - 1u, ++f) {
+      const int i = __ffs(mm) - 1;
+      const uint32_t c = (st3[f >> 3] >> (4 * (f & 7))) & 15u;
+      if (c == 15u) ml |= 1u << i;
+      else put(i, E - 6u - c);
     }
   }
+  if (!(hw & 0x800u)) return;
+  // literal exponent bytes, in value order
+  const uint8_t* lit = reinterpret_cast<const uint8_t*>(st3 + ((tot3 + 7) >> 3));
+  int totl = 0;
+  int f = warp_excl_scan(__popc(ml), lane, &totl);
+  for (uint32_t mm = ml; mm; mm &= mm - 1u) put(__ffs(mm) - 1, lit[f++]);
 }
 
 }  // namespace tcode

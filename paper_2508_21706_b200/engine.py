@@ -172,7 +172,7 @@ class VerifyEngine:
     def __init__(self, shape: ModelShape, *, max_batch: int, max_verify: int, max_seq: int, hbm_slots: int = 2,
                  expert_cache_bytes: int = 0, host_alias_layers: int = 0, device: int = 0, debug: bool = False,
                  ep_rank: int = 0, ep_size: int = 1, ep_group: Optional["EpGroup"] = None, kv_pages: int = 0,
-                 attn_cpu: bool = False, batch_one: bool = False, compress_experts: bool = False,
+                 attn_cpu: bool = False, batch_one: bool = False, compress_experts: int = 0,
                  micro_batches: int = 1):
         self.shape = shape
         self.max_batch, self.max_verify, self.max_seq = max_batch, max_verify, max_seq

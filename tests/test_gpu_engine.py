@@ -281,7 +281,8 @@ def test_batch_one_link_gap_prefetch_bit_identical(cuda, compress, monkeypatch):
     assert res["one_pf"][0][1] == res["one_nopf"][0][1]
 
 
-@pytest.mark.parametrize("batch_one,codec", [(False, "unary"), (True, "unary"), (False, "fixed")])
+@pytest.mark.parametrize("batch_one,codec", [(False, "unary"), (True, "unary"), (False, "fixed"), (False, "tile"),
+                                             (True, "tile")])
 def test_compressed_expert_stream_bit_identical(cuda, batch_one, codec, monkeypatch):
     """compress_experts: experts cross the link in a lossless code and are
     expanded in HBM — verify results bit-identical to raw streaming. Default:
@@ -306,8 +307,37 @@ def test_compressed_expert_stream_bit_identical(cuda, batch_one, codec, monkeypa
     assert np.array_equal(r0.acc_len, r1.acc_len) and np.array_equal(r0.bonus, r1.bonus)
     if codec == "fixed":
         assert b1 > 0 and b1 / b0 <= 1456 / 2048 + 1e-9  # (the coded hot cache holds more blocks)
+    elif codec == "tile":  # T2 decoded inside the expert kernel
+        assert b1 > 0 and b1 / b0 < 11.0 / 16, 16 * b1 / b0
     else:
         assert b1 > 0 and b1 / b0 < 11.0 / 16, 16 * b1 / b0  # below the 3-bit code
+
+
+@pytest.mark.parametrize("kind", ["tiny", "tiny_fg", "tiny_gauss"])
+def test_tile_code_engine_bit_identical(cuda, kind, monkeypatch):
+    """compress_experts = 2: every expert block streams and is hot-cached in
+    the T2 tile code and K4-MoE decodes it in shared memory — no expansion
+    launch, no bf16 expert in HBM. Two steps (the slots cycle) with a hot
+    cache: bit-identical to raw bf16 streaming."""
+    from paper_2508_21706_b200.engine import VerifyEngine
+    s = _shape(kind)
+    b, n = 4, 5
+    prefix = np.array([300, 17, 64, 1], np.int32)
+    rng = np.random.default_rng(10)
+    toks = [rng.integers(0, s.vocab, size=(b, n)).astype(np.int32) for _ in range(2)]
+    out = {}
+    for comp in (0, 2):
+        eng = VerifyEngine(s, max_batch=b, max_verify=n, max_seq=512, compress_experts=comp,
+                           expert_cache_bytes=3 * s.expert_bytes if comp else 0)
+        eng.fill_prefix(prefix)
+        out[comp] = ([eng.verify(t, prefix) for t in toks], eng.last_times())
+        eng.close()
+    for r0, r1 in zip(out[0][0], out[2][0]):
+        assert np.array_equal(r0.target, r1.target)
+        assert np.array_equal(r0.acc_len, r1.acc_len) and np.array_equal(r0.bonus, r1.bonus)
+    t2 = out[2][1]
+    assert t2["codec"] == 0.0  # nothing expanded
+    assert 0 < t2["h2d_bytes"] < t2["h2d_raw_bytes"] * 11.5 / 16
 
 
 @pytest.mark.parametrize("batch_one", [False, True])

@@ -101,8 +101,8 @@ def _coded_vs_plain(torch, cuda, h, hi, E, rows_per, kind, splits=0):
     assert torch.equal(y0.view(torch.int32), y1.view(torch.int32))
     if kind == "wide":  # NaN / Inf bit patterns: bit identity is the whole check
         return
-    # and the plain kernel itself against fp32 torch on one expert
-    e = 1
+    # and the plain kernel itself against fp32 torch on the first non-empty expert
+    e = int(np.flatnonzero(np.asarray(rows_per) > 0)[0])
     a, b = int(off[e]), int(off[e + 1])
     w1 = pool[e * blk:e * blk + hi * h].view(hi, h).float()
     w3 = pool[e * blk + hi * h:e * blk + 2 * hi * h].view(hi, h).float()

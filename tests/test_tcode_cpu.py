@@ -31,7 +31,7 @@ def test_tcode_round_trip(kind):
     assert np.array_equal(T.decode_expert(code, h, hi), x)
     bpw = 8 * len(code) / x.size
     if kind == "uniform":
-        assert 10.2 < bpw < 10.7, bpw  # 8 + ~2.3 exponent bits + headers
+        assert 10.2 < bpw < 10.7, bpw  # 8 + ~2.35 exponent bits + headers
     if kind == "gaussian":
         assert bpw < 11.1, bpw  # below the unary code on these weights (~11.45)
 
@@ -45,47 +45,48 @@ def _segment_tile(seg0: np.ndarray) -> np.ndarray:
 
 def test_tcode_known_answers():
     # every value 1.0 (exponent 127): E = 127, j = 0 -> all L1 codes 0, no
-    # level fields: 1024 lo bytes + 256 code bytes = 1280 B = 80 x 16
+    # streams: header 32 + lo 8 x 1024 + L1 8 x 256 = 10272 bytes
     W = np.full((128, 64), 0x3F80, np.uint16)
     code = T.encode([W])
     toff = np.frombuffer(code[:16], "<u4")
-    assert toff[0] == 16 and toff[1] == len(code) == 16 + 32 + 8 * 1280
+    assert toff[0] == 16 and toff[1] == len(code) == 16 + 10272
     hdr = np.frombuffer(code[16:48], "<u4")
-    assert np.all(hdr == (127 | (80 << 16)))
-    seg = np.frombuffer(code[48:48 + 1280], np.uint8)
-    assert not np.any(seg)  # lo = 0 (positive, zero mantissa), codes 0
-    # value 3 halved (j = 1) and value 17 at 2^-3 (j = 3: L1 code 3, level-2 code 0)
+    assert np.all(hdr == (127 | ((10272 // 4) << 12)))
+    assert not np.any(np.frombuffer(code[48:], np.uint8))  # lo = 0 (positive, zero mantissa), codes 0
+    # segment 0: value 3 halved (j = 1) and value 17 at 2^-3 (j = 3: L1 code 3, level-2 code 0)
     s = np.full(1024, 0x3F80, np.uint16)
     s[3] = 0x3F00
     s[17] = 0x3E00
     code = T.encode([_segment_tile(s)])
-    hw = int(np.frombuffer(code[16:20], "<u4")[0])
-    assert hw & 0xFF == 127 and (hw >> 8) & 0xFF == 2 and (hw >> 16) == 81  # 1280 + 1 level word -> 1296
-    l1 = np.frombuffer(code[48 + 1024:48 + 1280], "<u4")
+    hdr = np.frombuffer(code[16:48], "<u4")
+    assert hdr[0] == 127 | (2 << 8) | (2568 << 12) and hdr[1] == 127 | (2569 << 12)
+    l1 = np.frombuffer(code[16 + 32 + 8192:16 + 32 + 8192 + 256], "<u4")
     # lane 0 word 0: value 3 = 2 q + 1 with q = 1 -> bits 16 + 2; word 1: value 17 = 16 + 2*0 + 1 -> bits 16
     assert l1[0] == 1 << 18 and l1[1] == 3 << 16 and not np.any(l1[2:])
-    assert np.frombuffer(code[48 + 1280:48 + 1284], "<u4")[0] == 0  # level-2 code 0
+    assert np.frombuffer(code[16 + 10272:16 + 10276], "<u4")[0] == 0  # level-2 code 0
+    assert len(code) == 16 + 10288  # one stream word, padded to 16 B
     assert np.array_equal(T.decode(code, [(128, 64)])[0], _segment_tile(s))
-    # an exact zero (exponent 0, j = 127): five 3s and a literal byte 0
+    # an exact zero (exponent 0, j = 127): 3, 3, nibble 15 and a literal byte 0
     z = np.full(1024, 0x3F80, np.uint16)
     z[0] = 0
     code = T.encode([_segment_tile(z)])
-    lv = np.frombuffer(code[48 + 1280:48 + 1284], "<u4")[0]
-    assert lv == 0xFF  # levels 2..5 of value 0: fields 0..3 all 3
+    assert (int(np.frombuffer(code[16:20], "<u4")[0]) >> 8) & 0xF == 2 | 4 | 8
+    st = np.frombuffer(code[16 + 10272:16 + 10284], "<u4")
+    assert st.tolist() == [3, 15, 0]  # L2 word, L3 word, literal 0 padded to 4 bytes
     assert np.array_equal(T.decode(code, [(128, 64)])[0], _segment_tile(z))
-    # incompressible segment -> raw (2048 B), flags bit 0
-    r = np.random.default_rng(1).integers(0, 1 << 16, 1024).astype(np.uint16)
-    code = T.encode([_segment_tile(r)])
-    hw = int(np.frombuffer(code[16:20], "<u4")[0])
-    assert (hw >> 8) & 0xFF == 1 and (hw >> 16) == 128
-    assert np.frombuffer(code[48:48 + 2048], "<u2").tolist() == r.tolist()
+    # incompressible tile -> raw: header word 0 = flags 1, the tile verbatim
+    r = np.random.default_rng(1).integers(0, 1 << 16, (128, 64)).astype(np.uint16)
+    code = T.encode([r])
+    assert np.frombuffer(code[16:48], "<u4").tolist() == [1 << 8] + [0] * 7
+    assert len(code) == 16 + 32 + 16384 and np.frombuffer(code[48:], "<u2").tolist() == r.ravel().tolist()
+    assert np.array_equal(T.decode(code, [(128, 64)])[0], r)
 
 
 def test_tcode_base_choice_prefers_fewer_bits():
     # one outlier 2^6 above the rest: E drops to the highest base that keeps
     # the bulk within level 1 (j = 2; ties prefer the higher E) and the
-    # outlier becomes an 18-bit literal, instead of adding 6 to every j
+    # outlier becomes a 16-bit literal, instead of adding 6 to every j
     s = np.full(1024, 0x3F80, np.uint16)
     s[5] = 0x4280  # 64.0
     E, bits = T.choose_base(((s.astype(np.int64) >> 7) & 0xFF))
-    assert E == 129 and bits == 2 * 1023 + 18
+    assert E == 129 and bits == 2 * 1023 + 16

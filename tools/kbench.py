@@ -181,6 +181,25 @@ def moe_coded(T=288, h=4096, hi=14336, E=8, k=2, dist="uniform"):
     return r
 
 
+def tcode_dec(h=4096, hi=14336, dist="uniform"):
+    """K5 tile code (T2) standalone expansion of one Mixtral expert block to bf16."""
+    n = 3 * h * hi
+    x = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    fill = ops.fill_normal_ if dist == "gaussian" else ops.fill_uniform_
+    fill(x[:hi * h], 0x5EED, 1100, math.sqrt(3.0 / h))
+    fill(x[hi * h:2 * hi * h], 0x5EED, 1101, math.sqrt(3.0 / h))
+    fill(x[2 * hi * h:], 0x5EED, 1102, math.sqrt(3.0 / hi))
+    code = ops.tcode_encode(x, h, hi)
+    out = torch.empty_like(x)
+    t = timeit(lambda: L.check(L.load().smo_tcode_decode(code.data_ptr(), h, hi, out.data_ptr(),
+                                                         torch.cuda.current_stream().cuda_stream)))
+    assert torch.equal(out.view(torch.int16), x.view(torch.int16))
+    byts = code.numel() + 2 * n
+    return {"kernel": "K5 tcode_decode (T2 tile code -> bf16)", "dist": dist, "N": n,
+            "bits_per_weight": code.numel() * 8 / n, "us": t * 1e6, "GBs": byts / t / 1e9, "frac": byts / t / 1e9 / PEAK,
+            "TFLOPs": 0.0}
+
+
 def main():
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
     res = []
@@ -201,6 +220,10 @@ def main():
         res.append(codec(bits=3))
         res.append(codec(bits=1))
         res.append(codec(bits=1, dist="gaussian"))
+    if what in ("tcode", "all"):
+        res.append(tcode_dec())
+        res.append(tcode_dec(dist="gaussian"))
+        res.append(codec(bits=1))
     if what in ("moecoded", "all"):
         res += moe_coded()
         res += moe_coded(dist="gaussian")
