@@ -205,6 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   TR_INIT();
   if (warp == 0 && lane == 0) {
+    TR(0, 9);  // kernel entry (trace builds)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
@@ -236,6 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (warp == 0 && lane == 0) TR(0, 8);  // setup done (barriers, TMEM, V zero-fill)
   const uint32_t tmem = tmem_base_sh;
   const int f_begin = blockIdx.x * p.Q, f_end = min(p.total, f_begin + p.Q);
 
@@ -628,49 +630,69 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
           if (stid < cur.npieces) slot_of[stid] = partial_slot(p, cur.first_cta + stid, cur.pair);
           asm volatile("bar.sync 5, 256;" ::: "memory");
           const int np = cur.npieces;
+          // the np (<= 16) partial (m, l) of a row, 4 loads in flight at a time
+          // (one L2 round trip per 4 pieces instead of one per piece); l is
+          // parked in shared memory until the row maximum is known
+          float* wl = slots + 16 * 128 + 64;
           for (int rr = stid; rr < p.rows; rr += 32 * kSoftWarps) {
             float Mx = -INFINITY, Lx = 0.f;
-#pragma unroll 4
-            for (int j = 0; j < np; ++j) Mx = fmaxf(Mx, __ldcg(&p.ws_ml[size_t(slot_of[j]) * p.rows + rr]).x);
-#pragma unroll 4
+            for (int j0 = 0; j0 < np; j0 += 4) {
+              float2 v[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                if (j0 + j < np) v[j] = __ldcg(&p.ws_ml[size_t(slot_of[j0 + j]) * p.rows + rr]);
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                if (j0 + j < np) {
+                  Mx = fmaxf(Mx, v[j].x);
+                  w[(j0 + j) * 128 + rr] = v[j].x;
+                  wl[(j0 + j) * 128 + rr] = v[j].y;
+                }
+            }
             for (int j = 0; j < np; ++j) {
-              const float2 v = __ldcg(&p.ws_ml[size_t(slot_of[j]) * p.rows + rr]);
-              const float e2 = v.x == -INFINITY ? 0.f : ex2_approx(v.x - Mx);
+              const float m = w[j * 128 + rr];
+              const float e2 = m == -INFINITY ? 0.f : ex2_approx(m - Mx);
               w[j * 128 + rr] = e2;
-              Lx += v.y * e2;
+              Lx += wl[j * 128 + rr] * e2;
             }
             const float inv = Lx > 0.f ? 1.f / Lx : 0.f;
             for (int j = 0; j < np; ++j) w[j * 128 + rr] *= inv;
           }
           if (warp == 4 && lane == 0) TR(2, 32);
           asm volatile("bar.sync 5, 256;" ::: "memory");
-          // every thread keeps kE independent partial loads in flight (the
-          // L2 round trip, not bandwidth, bounds this loop)
-          constexpr int kE = 4;
+          // every thread keeps kJ pieces x kE elements of partial loads in
+          // flight (the L2 round trip, not bandwidth, bounds this loop)
+          constexpr int kE = 1, kJ = 8;
           const int n_e = p.rows * (D / 4);
           for (int e0 = stid; e0 < n_e; e0 += 32 * kSoftWarps * kE) {
             float4 acc[kE];
 #pragma unroll
             for (int u = 0; u < kE; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int j = 0; j < np; ++j) {
-              const float4* src = reinterpret_cast<const float4*>(p.ws_o + size_t(slot_of[j]) * p.rows * D);
-              float4 v[kE];
+            for (int j0 = 0; j0 < np; j0 += kJ) {
+              float4 v[kJ][kE];
 #pragma unroll
-              for (int u = 0; u < kE; ++u) {
-                const int e = e0 + u * 32 * kSoftWarps;
-                if (e < n_e) v[u] = __ldcg(src + e);
-              }
+              for (int jj = 0; jj < kJ; ++jj) {
+                const float4* src = reinterpret_cast<const float4*>(
+                    p.ws_o + size_t(slot_of[j0 + jj < np ? j0 + jj : 0]) * p.rows * D);
 #pragma unroll
-              for (int u = 0; u < kE; ++u) {
-                const int e = e0 + u * 32 * kSoftWarps;
-                if (e < n_e) {
-                  const float wj = w[j * 128 + e / (D / 4)];
-                  acc[u].x += v[u].x * wj;
-                  acc[u].y += v[u].y * wj;
-                  acc[u].z += v[u].z * wj;
-                  acc[u].w += v[u].w * wj;
+                for (int u = 0; u < kE; ++u) {
+                  const int e = e0 + u * 32 * kSoftWarps;
+                  if (j0 + jj < np && e < n_e) v[jj][u] = __ldcg(src + e);
                 }
               }
+#pragma unroll
+              for (int jj = 0; jj < kJ; ++jj)
+#pragma unroll
+                for (int u = 0; u < kE; ++u) {
+                  const int e = e0 + u * 32 * kSoftWarps;
+                  if (j0 + jj < np && e < n_e) {
+                    const float wj = w[(j0 + jj) * 128 + e / (D / 4)];
+                    acc[u].x += v[jj][u].x * wj;
+                    acc[u].y += v[jj][u].y * wj;
+                    acc[u].z += v[jj][u].z * wj;
+                    acc[u].w += v[jj][u].w * wj;
+                  }
+                }
             }
 #pragma unroll
             for (int u = 0; u < kE; ++u) {

@@ -8,11 +8,12 @@ import torch
 import kbench
 from paper_2508_21706_b200 import _lib as L, ops
 lib = L.load()
-print(kbench.attn(32, 9, 1024))
+b, n, s = (int(v) for v in sys.argv[1:4]) if len(sys.argv) >= 4 else (32, 9, 1024)
+nq, nkv, d = 32, 8, 128
+print(kbench.attn(b, n, s))
 buf = np.zeros((3, 4096), np.uint64); cnt = np.zeros(3, np.int32)
 lib.smo_debug_attn_trace(buf.ctypes.data_as(C.c_void_p), cnt.ctypes.data_as(C.c_void_p))  # clear
 dev = torch.device("cuda:0")
-b, n, s, nq, nkv, d = 32, 9, 1024, 32, 8, 128
 q = torch.randn((b * n, nq, d), device=dev).to(torch.bfloat16)
 kc = torch.randn((b, nkv, s + 80, d), device=dev).to(torch.bfloat16)
 vc = torch.randn((b, nkv, s + 80, d), device=dev).to(torch.bfloat16)

@@ -5,7 +5,7 @@ set -e
 OUT=$1; shift
 TMP=$(mktemp -d)
 cd "$(dirname "$0")/.."
-for f in c_api ops gemm_tc moe_tc attention engine decode prefill ep xfer; do
+for f in c_api ops gemm_tc moe_tc attention engine decode prefill streamer ep xfer tcode; do
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -std=c++17 -Xcompiler -fPIC \
     --expt-relaxed-constexpr -I include -I paper_2508_21706_b200/csrc "$@" -c paper_2508_21706_b200/csrc/$f.cu -o $TMP/$f.o &
 done
