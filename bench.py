@@ -59,9 +59,11 @@ def parse():
                     help="LARGE_BATCH (stream whole layers ahead) or BATCH_ONE (stream router-selected experts)")
     ap.add_argument("--no-compress", dest="compress", action="store_false",
                     help="stream raw bf16 experts instead of the lossless code (default: coded, expanded in HBM)")
-    ap.add_argument("--codec", default="unary", choices=["unary", "tile"],
-                    help="link code of the coded transfer: unary (xfer.cu; blocks expanded in HBM by a decode "
-                         "kernel) or tile (tcode.cuh T2; decoded inside the expert kernel, no bf16 expert in HBM)")
+    ap.add_argument("--codec", default="auto", choices=["auto", "unary", "tile"],
+                    help="link code of the coded transfer: auto (the engine probes the first expert block and "
+                         "keeps the smaller: unary for uniform-init, tile for gaussian-like weights), unary (xfer.cu; "
+                         "blocks expanded in HBM by a decode kernel) or tile (tcode.cuh T2; decoded inside the "
+                         "expert kernel, no bf16 expert in HBM)")
     ap.add_argument("--ep-transport", default="ipc", choices=["ipc", "nccl"],
                     help="N>1 expert-parallel exchange: CUDA-IPC peer mailboxes written by the dispatch / "
                          "combine kernels themselves (default; falls back to NCCL if IPC cannot be set up) "
@@ -542,6 +544,8 @@ def run_ours(args):
         except Exception as ex:  # fail loudly: a replica run would not measure the EP path
             raise RuntimeError(f"expert parallelism over {world} ranks could not be set up: {ex}") from ex
     eng = None
+    if args.codec == "unary":  # pin the unary code (no probe)
+        os.environ["SMO_CODEC"] = "unary"
     for a in (alias, 8, 4, 2):
         try:
             eng = VerifyEngine(shape, max_batch=b, max_verify=n, max_seq=s_max, hbm_slots=args.slots,
@@ -663,7 +667,7 @@ def run_ours(args):
                 "achieved": moe_bytes_step / moe_t / 1e9 if moe_t > 0 else None, "peak": pk["hbm_gbs"],
                 "unit": "GB/s", "frac": (moe_bytes_step / moe_t / 1e9) / pk["hbm_gbs"] if moe_t > 0 else None,
                 "traffic": moe_traffic_per_layer() if (args.model == "mixtral-8x7b" and ep_size == 1
-                                                       and not (args.compress and args.codec == "tile")) else None,
+                                                       and stages.get("link_code", 0) != 2) else None,
                 "traffic_unit": "dram bytes per layer (the fused expert launch, ncu profiles/r01c_traffic.json); "
                 "algorithmic per layer = " + str((shape.n_expert // ep_size) * shape.expert_bytes),
                 "peak_kind": pk_kind}
@@ -697,7 +701,7 @@ def run_ours(args):
                    "expert_transfer": (f"lossless tile-coded blocks (tcode.cuh T2, "
                                        f"{16.0 * stages['h2d_bytes'] / max(1.0, stages['h2d_raw_bytes']):.2f} "
                                        "bits/weight), decoded in shared memory by the expert kernel"
-                                       if args.codec == "tile" else
+                                       if stages.get("link_code", 0) == 2 else
                                        f"lossless exponent-coded blocks (xfer.cu, "
                                        f"{16.0 * stages['h2d_bytes'] / max(1.0, stages['h2d_raw_bytes']):.2f} "
                                        "bits/weight), expanded in HBM before the expert kernel")

@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -50,6 +51,14 @@ struct EngineOptions {
   int ep_rank = 0;
   int ep_size = 1;
   smo_ep_group* ep_group = nullptr;
+  // drafter GPU-part / CPU-part split (build_draft_dag
+  // pipeline.hpp:217-253): with draft_cpu_kv every decode step first sets how
+  // many requests keep the drafter on the GPU — dynamic_split_ratio(hw, model,
+  // *draft_split_policy, current length, b) (memory.hpp:93-106) when a policy
+  // is given, else draft_gpu_requests (-1: all); the rest attend on the host
+  bool draft_cpu_kv = false;
+  std::optional<MemoryPolicy> draft_split_policy;
+  std::int64_t draft_gpu_requests = -1;
 };
 
 struct VerifyBatch {
@@ -137,6 +146,7 @@ class VerifyEngine {
     o.micro_batches = std::int32_t(std::max<std::int64_t>(1, hyper.m));
     o.kv_pages = opt.kv_pages;
     o.compress_experts = opt.compress_experts ? 1 : 0;
+    o.draft_cpu_kv = opt.draft_cpu_kv ? 1 : 0;
     // AttentionPlacement::CPU (the reference's default, config.hpp:110): target
     // K/V in pinned host DRAM, attention on the host pool (f4); GPU_RESIDENT
     // runs K1 on HBM-resident K/V (GPU_TRANSFER is rejected above)
@@ -148,6 +158,9 @@ class VerifyEngine {
     max_verify_ = o.max_verify;
     max_seq_ = o.max_seq;
     attn_cpu_ = o.attn_cpu != 0;
+    draft_cpu_kv_ = opt.draft_cpu_kv;
+    draft_split_policy_ = opt.draft_split_policy;
+    draft_gpu_requests_ = opt.draft_gpu_requests;
   }
   VerifyEngine(const VerifyEngine&) = delete;
   VerifyEngine& operator=(const VerifyEngine&) = delete;
@@ -220,33 +233,71 @@ class VerifyEngine {
     vb.b = std::int64_t(kv_len_.size());
     vb.n = k + 1;
     vb.prefix_len = kv_len_;
-    detail::smo_check(smo_engine_decode_step(h_, k, planted ? planted->data() : nullptr, nullptr));
-    IterationResult r = measured(vb);
-    std::vector<double> dt(std::size_t(k) + 2, 0.0);
-    std::int32_t steps = 0;
-    detail::smo_check(smo_engine_draft_times(h_, dt.data(), dt.size(), &steps));
     double s = 0;
     for (auto p : kv_len_) s += double(p);
     s /= double(kv_len_.size());
+    // the drafter split of this step (f1): GPU-part requests from the memory
+    // policy at the current length (memory.hpp:93-106) or the fixed count
+    std::int64_t g = vb.b;
+    if (draft_cpu_kv_) {
+      g = draft_split_policy_
+              ? dynamic_split_ratio(hw_, model_, *draft_split_policy_, std::max<std::int64_t>(1, std::llround(s) + k + 1),
+                                    vb.b)
+              : (draft_gpu_requests_ < 0 ? vb.b : std::min(draft_gpu_requests_, vb.b));
+      detail::smo_check(smo_engine_set_draft_split(h_, g >= vb.b ? -1 : std::int32_t(g)));
+      split_gpu_.push_back(g);
+    }
+    detail::smo_check(smo_engine_decode_step(h_, k, planted ? planted->data() : nullptr, nullptr));
+    IterationResult r = measured(vb);
+    std::vector<double> dt(std::size_t(k) + 2, 0.0), sp(3 * (std::size_t(k) + 2), 0.0);
+    std::int32_t steps = 0, ssteps = 0;
+    detail::smo_check(smo_engine_draft_times(h_, dt.data(), dt.size(), &steps));
+    if (g < vb.b) detail::smo_check(smo_engine_draft_split_times(h_, sp.data(), sp.size(), &ssteps));
     double t0 = 0;
-    for (int t = 0; t < steps; ++t) {
+    std::vector<int> prev;
+    auto add = [&](EventKind kind, ExecResource res, double start, double dur, std::vector<int> deps,
+                   const std::string& label) {
       EventNode ev;
-      ev.id = t;
-      ev.kind = EventKind::DRAFT_GPU_STEP;
-      ev.resource = ExecResource::GPU;
-      ev.duration = dt[std::size_t(t)];
-      if (t > 0) ev.deps.push_back(t - 1);
-      ev.label = "draft/step" + std::to_string(t) + "/GPU_STEP";
+      ev.id = int(r.draft_dag.size());
+      ev.kind = kind;
+      ev.resource = res;
+      ev.duration = dur;
+      ev.deps = std::move(deps);
+      ev.label = label;
       r.draft_dag.push_back(ev);
-      r.draft_schedule.start.push_back(t0);
-      r.draft_schedule.end.push_back(t0 + ev.duration);
-      r.draft_schedule.busy[std::size_t(ExecResource::GPU)] += ev.duration;
-      t0 += ev.duration;
-      samples_.push_back({EventKind::DRAFT_GPU_STEP, double(vb.b) * s, ev.duration});
+      r.draft_schedule.start.push_back(start);
+      r.draft_schedule.end.push_back(start + dur);
+      r.draft_schedule.busy[std::size_t(res)] += dur;
+      return ev.id;
+    };
+    for (int t = 0; t < steps; ++t) {
+      const std::string tag = "draft/step" + std::to_string(t) + "/";
+      std::vector<int> ends;
+      if (ssteps > t) {  // build_draft_dag (pipeline.hpp:217-253): GPU_STEP || CPU_ATTN -> GPU_FFN
+        const double a = sp[3 * std::size_t(t)], host = sp[3 * std::size_t(t) + 1], after = sp[3 * std::size_t(t) + 2];
+        const double end = t0 + a + after, ffn0 = t0 + std::max(a, host);
+        if (g > 0) {
+          ends.push_back(add(EventKind::DRAFT_GPU_STEP, ExecResource::GPU, t0, a, prev, tag + "GPU_STEP"));
+          samples_.push_back({EventKind::DRAFT_GPU_STEP, double(g) * s, a});
+          r.breakdown.draft_gpu_part += a;
+        }
+        const int at = add(EventKind::DRAFT_CPU_ATTN, ExecResource::CPU, t0, host, prev, tag + "CPU_ATTN");
+        samples_.push_back({EventKind::DRAFT_CPU_ATTN, double(vb.b - g) * s, host});
+        const double ffn = std::max(0.0, end - ffn0);
+        ends.push_back(add(EventKind::DRAFT_GPU_FFN, ExecResource::GPU, ffn0, ffn, {at}, tag + "GPU_FFN"));
+        r.breakdown.draft_cpu_part += host + ffn;  // the breakdown's convention (pipeline.hpp:407-411)
+        t0 = end;
+      } else {
+        ends.push_back(add(EventKind::DRAFT_GPU_STEP, ExecResource::GPU, t0, dt[std::size_t(t)], prev,
+                           tag + "GPU_STEP"));
+        samples_.push_back({EventKind::DRAFT_GPU_STEP, double(vb.b) * s, dt[std::size_t(t)]});
+        r.breakdown.draft_gpu_part += dt[std::size_t(t)];
+        t0 += dt[std::size_t(t)];
+      }
+      prev = std::move(ends);
     }
     r.draft_schedule.makespan = t0;
     r.breakdown.draft_total = t0;
-    r.breakdown.draft_gpu_part = t0;
     r.breakdown.iteration = r.breakdown.target_total + t0;
     std::vector<std::int32_t> kv(kv_len_.size());
     detail::smo_check(smo_engine_decode_read(h_, nullptr, 0, nullptr, kv.data(), nullptr));
@@ -285,6 +336,8 @@ class VerifyEngine {
   }
   const std::vector<std::int32_t>& kv_len() const { return kv_len_; }
   const std::vector<int>& chosen_k() const { return ks_; }
+  // GPU-part request count the drafter split used at each decode step
+  const std::vector<std::int64_t>& draft_split_history() const { return split_gpu_; }
 
   // Accumulated measured samples (one per stage kind and verify call).
   const std::vector<ProfileSample>& profile() const { return samples_; }
@@ -401,6 +454,10 @@ class VerifyEngine {
   int max_verify_ = 1;
   std::int64_t max_seq_ = 2048;
   bool attn_cpu_ = false;
+  bool draft_cpu_kv_ = false;
+  std::optional<MemoryPolicy> draft_split_policy_;
+  std::int64_t draft_gpu_requests_ = -1;
+  std::vector<std::int64_t> split_gpu_;
   std::vector<std::int32_t> kv_len_;  // decode state mirror (host)
   std::vector<int> ks_;
   std::vector<ProfileSample> samples_;

@@ -381,6 +381,11 @@ typedef struct {
                                  on the layer's one expert transfer). With the CPU placement the host
                                  attends micro-batch j while the GPU runs j+1's stages. 0/1 = one;
                                  at most 8; LARGE_BATCH without expert parallelism. */
+  int32_t draft_cpu_kv;       /* 1: also keep a pinned host copy slot for every request's drafter K/V,
+                                 so smo_engine_set_draft_split can move requests' drafter attention
+                                 to the host thread pool (the paper's draft CPU part, build_draft_dag
+                                 pipeline.hpp:217-253; split from dynamic_split_ratio memory.hpp:93-106).
+                                 Contiguous K/V only (kv_pages = 0). */
 } smo_engine_options;
 
 /* ---- expert parallelism ----------------------------------
@@ -475,6 +480,8 @@ typedef struct {
   double h2d_raw_bytes; /* bf16 bytes the streamed blocks carry (= h2d_bytes unless coded) */
   double codec;        /* device time expanding coded expert blocks (compress_experts) */
   double codec_bytes;  /* their algorithmic bytes: code read + bf16 written (streamed + coded hot cache) */
+  double link_code;    /* the engine's expert link code: 0 raw bf16, 1 unary / window codes expanded in HBM,
+                          2 T2 tile code decoded inside the expert kernel */
 } smo_stage_times;
 smo_status smo_engine_last_times(smo_engine* e, smo_stage_times* t);
 /* Measured per-layer timeline of the last verify step with m micro-batches
@@ -530,6 +537,20 @@ smo_status smo_engine_decode_run(smo_engine* e, int32_t k, int32_t steps, int32_
 /* Measured duration (s) of each drafter step of the last decode step
  * (DRAFT_GPU_STEP events, pipeline.hpp:208-253); *steps = k+1 (0: no drafter). */
 smo_status smo_engine_draft_times(smo_engine* e, double* out, size_t n, int32_t* steps);
+/* Drafter GPU-part / CPU-part split (engine created with draft_cpu_kv):
+ * requests [0, gpu_requests) keep their drafter K/V in HBM and attend with K1
+ * (DRAFT_GPU_STEP); requests [gpu_requests, b) keep it in pinned host memory
+ * and attend on the host thread pool (DRAFT_CPU_ATTN), whose output feeds the
+ * drafter's GPU projections / FFN (DRAFT_GPU_FFN) — the two parts of a step
+ * run concurrently. Moves the affected requests' drafter K/V rows (call after
+ * prefill / decode_begin, between steps). -1: every request on the GPU. Chain
+ * decode steps only (no tree steps or decode graphs while split).          */
+smo_status smo_engine_set_draft_split(smo_engine* e, int32_t gpu_requests);
+/* Per drafter step of the last decode step with a split: out[3t..3t+2] =
+ * (GPU part up to the host join, host attention wall time summed over the
+ * drafter layers, GPU work after the join) in seconds; *steps = k+1, or 0
+ * when the last step ran without a split.                                   */
+smo_status smo_engine_draft_split_times(smo_engine* e, double* out, size_t n, int32_t* steps);
 smo_status smo_engine_decode_read(smo_engine* e, int32_t* committed, int32_t cap, int32_t* n_committed,
                                   int32_t* kv_len, int32_t* root);
 

@@ -62,7 +62,7 @@ class EngineOptions(C.Structure):
                 ("expert_cache_bytes", _i64), ("host_alias_layers", _i32), ("device", _i32), ("flags", _i32),
                 ("ep_rank", _i32), ("ep_size", _i32), ("nccl_comm", _vp), ("kv_pages", _i32),
                 ("attn_cpu", _i32), ("moe_batching", _i32),
-                ("compress_experts", _i32), ("micro_batches", _i32)]
+                ("compress_experts", _i32), ("micro_batches", _i32), ("draft_cpu_kv", _i32)]
 
 
 class StreamerArgs(C.Structure):
@@ -84,7 +84,7 @@ class StageTimes(C.Structure):
     _fields_ = [("target_total", C.c_double), ("attention", C.c_double), ("gpu_moe", C.c_double),
                 ("h2d_transfer", C.c_double), ("others", C.c_double), ("h2d_bytes", C.c_double),
                 ("launches", C.c_double), ("draft", C.c_double), ("h2d_raw_bytes", C.c_double),
-                ("codec", C.c_double), ("codec_bytes", C.c_double)]
+                ("codec", C.c_double), ("codec_bytes", C.c_double), ("link_code", C.c_double)]
 
 
 _SIGS = {
@@ -102,6 +102,8 @@ _SIGS = {
     "smo_expert_encode": (C.c_int, [_vp, _u64, _i32, _vp, _vp, _vp]),
     "smo_expert_decode": (C.c_int, [_vp, _u64, _i32, _vp, _vp]),
     "smo_tcode_max_bytes": (_sz, [_i32, _i32]),
+    "smo_engine_set_draft_split": (C.c_int, [_vp, _i32]),
+    "smo_engine_draft_split_times": (C.c_int, [_vp, _vp, _sz, _vp]),
     "smo_tcode_encode": (C.c_int, [_vp, _i32, _i32, _vp, _vp, _vp]),
     "smo_tcode_decode": (C.c_int, [_vp, _i32, _i32, _vp, _vp]),
     "smo_moe_experts_coded": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),

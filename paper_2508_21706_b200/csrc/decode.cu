@@ -115,14 +115,65 @@ void Engine::lm_argmax(const float* xr, int rows, int32_t* out, cudaStream_t st)
 }
 
 // One drafter step for b requests: token tok_in[r] at position pos[r]
-// (its K/V appended there), greedy next token into out_tok[r].
+// (its K/V appended there), greedy next token into out_tok[r]. With the
+// draft split (draft_g = g < b) the projections, FFN and LM head still run
+// batched over all b rows on the GPU, but the attention of rows [g, b) runs
+// on the host pool over their host-resident drafter K/V (DRAFT_CPU_ATTN,
+// started as soon as their q is written, joined before O-proj =
+// DRAFT_GPU_FFN) while K1 attends rows [0, g) (DRAFT_GPU_STEP).
 void Engine::draft_forward(int b, const int32_t* tok_in, const int32_t* pos, int max_pos, int32_t* out_tok,
-                   cudaStream_t st) {
+                   cudaStream_t st, int step) {
   const Scratch sc{x, xn, qkv, q, attn, attn_ws, attn_ws_bytes, 0};
   embed(tok_in, embed_w, b, h, x, st);
   const std::vector<int> mp{max_pos};
-  for (auto& dl : dlayers) {
-    attn_sublayer(sc, dl.wqkv, dl.wo, dl.kc, dl.vc, b, 1, 1, pos, mp, d_mask1, st);
+  const int g = draft_g < 0 ? b : std::min(draft_g, b);
+  if (g == b) {
+    for (auto& dl : dlayers) {
+      attn_sublayer(sc, dl.wqkv, dl.wo, dl.kc, dl.vc, b, 1, 1, pos, mp, d_mask1, st);
+      ffn_dense(sc, dh, b, dl.w1, dl.w3, dl.w2, dI, st);
+    }
+    lm_argmax(x, b, out_tok, st);
+    return;
+  }
+  const size_t kv_req = size_t(nkv) * s_max * d;
+  for (int li = 0; li < dL; ++li) {
+    DLayer& dl = dlayers[size_t(li)];
+    rmsnorm(x, ones, b, h, cfg.rms_eps, xn, st);
+    dense_gemm(xn, b, h, qkv_w, dl.wqkv, nullptr, SMO_EPI_BF16, qkv, 0, st);
+    // CPU part first: its q / K / V rows to host memory, then the host starts
+    rope_append(qkv + size_t(g) * qkv_w, pos + g, nullptr, b - g, 1, nq, nkv, d, s_max, cfg.rope_theta, dq_h,
+                dkc_h[size_t(li)] + size_t(g) * kv_req, dvc_h[size_t(li)] + size_t(g) * kv_req, st);
+    SMO_CUDA_CHECK(cudaMemcpyAsync(dpos_h, pos + g, size_t(b - g) * 4, cudaMemcpyDeviceToDevice, st));
+    const uint32_t seq = ++host_seq;
+    async_host.push({CpuAttnJob{dq_h, dkc_h[size_t(li)] + size_t(g) * kv_req, dvc_h[size_t(li)] + size_t(g) * kv_req,
+                                dmask_h, dpos_h, da_h, b - g, 1, nq, nkv, d, s_max, 1},
+                     cpu_pool.get(), seq});
+    signal_host_ready(seq, st);
+    if (step >= 0) step_seqs[size_t(step)].push_back(seq);
+    if (g > 0) {  // GPU part: K1 over its HBM drafter K/V
+      rope_append(qkv, pos, nullptr, g, 1, nq, nkv, d, s_max, cfg.rope_theta, q, dl.kc, dl.vc, st);
+      smo_attn_args a{};
+      a.q = q;
+      a.k_cache = dl.kc;
+      a.v_cache = dl.vc;
+      a.mask = d_mask1;
+      a.prefix_len = pos;
+      a.out = attn;
+      a.b = g;
+      a.n = 1;
+      a.n_q = nq;
+      a.n_kv = nkv;
+      a.d = d;
+      a.s_max = s_max;
+      a.max_prefix = max_pos;
+      a.workspace = attn_ws;
+      a.workspace_bytes = attn_ws_bytes;
+      attention_launch(a, st);
+    }
+    if (step >= 0 && li == dL - 1) SMO_CUDA_CHECK(cudaEventRecord(join_ev[size_t(step)], st));
+    wait_host_flag(seq, st);
+    copy_from_mapped(attn + size_t(g) * nq * d, da_h, size_t(b - g) * nq * d * 2, st);
+    dense_gemm(attn, b, nq * d, h, dl.wo, nullptr, SMO_EPI_F32_ADD, x, 0, st);
     ffn_dense(sc, dh, b, dl.w1, dl.w3, dl.w2, dI, st);
   }
   lm_argmax(x, b, out_tok, st);
@@ -137,6 +188,8 @@ void Engine::decode_begin(const int32_t* root_h, const int32_t* kv_h, int b) {
     SMO_REQUIRE(root_h[r] >= 0 && root_h[r] < V, "decode_begin: root token out of range");
     mx = std::max<int64_t>(mx, kv_h[r]);
   }
+  if (draft_g >= 0 && dec_b > 0) set_draft_split(-1);  // the drafter K/V back in HBM
+  draft_g = -1;
   SMO_CUDA_CHECK(cudaDeviceSynchronize());
   SMO_CUDA_CHECK(cudaMemcpy(d_root, root_h, size_t(b) * 4, cudaMemcpyHostToDevice));
   SMO_CUDA_CHECK(cudaMemcpy(d_kvlen, kv_h, size_t(b) * 4, cudaMemcpyHostToDevice));
@@ -195,6 +248,8 @@ void Engine::decode_device(int k, bool planted, int bound, cudaStream_t st, bool
   begin_step(st, !batch_one);  // the first layers' experts stream while the drafter runs
   decode_prep(d_root, planted ? d_drafts : nullptr, b, n, d_dec_tok, st);
   if (tree) {
+    SMO_REQUIRE(draft_g < 0 || draft_g >= b, "decode: tree steps need every request's drafter on the GPU");
+    last_split = false;
     // planted draft tree: the drafter runs its layers over all n nodes at
     // once (tree positions and mask) so its K/V covers every node; verify
     // with the tree mask; the accepted root path's K/V rows of every target
@@ -224,10 +279,12 @@ void Engine::decode_device(int k, bool planted, int bound, cudaStream_t st, bool
   // proposes d_{t+1}; the extra step t = k only appends d_k's draft K/V so
   // that a fully accepted chain leaves no hole in the drafter's cache
   last_draft_steps = dL > 0 ? k + 1 : 0;
+  last_split = dL > 0 && draft_g >= 0 && draft_g < b;
+  step_seqs.assign(size_t(k) + 1, {});
   for (int t = 0; dL > 0 && t <= k; ++t) {
     SMO_CUDA_CHECK(cudaEventRecord(draft_ev[size_t(t)], st));
     draft_io(d_dec_tok, d_kvlen, t, b, n, d_dtok, d_dpos, st);
-    draft_forward(b, d_dtok, d_dpos, bound + t, d_dout, st);
+    draft_forward(b, d_dtok, d_dpos, bound + t, d_dout, st, t);
     if (!planted && t < k) draft_scatter(d_dout, b, n, t, d_dec_tok, st);
   }
   SMO_CUDA_CHECK(cudaEventRecord(ev[3], st));
@@ -245,8 +302,8 @@ void Engine::decode_run(int k, int steps, bool graph, cudaStream_t st) {
   SMO_REQUIRE(b > 0, "decode: call smo_engine_prefill or smo_engine_decode_begin first");
   SMO_REQUIRE(k >= 0 && n <= maxN, "decode: k + 1 exceeds max_verify");
   SMO_REQUIRE(k == 0 || dL > 0, "decode: k > 0 needs a drafter (draft_layers)");
-  SMO_REQUIRE(!batch_one && !attn_cpu && !ep_on && !debug,
-              "decode graph: not with BATCH_ONE, CPU attention, expert parallelism or debug snapshots");
+  SMO_REQUIRE(!batch_one && !attn_cpu && !ep_on && !debug && (draft_g < 0 || draft_g >= b),
+              "decode graph: not with BATCH_ONE, CPU attention, expert parallelism, debug snapshots or a draft split");
   SMO_REQUIRE(st != nullptr, "decode graph: needs a non-default stream");
   const int64_t end = kv_bound + int64_t(steps) * n;  // kv bound after the last iteration
   SMO_REQUIRE(end <= s_max, "decode: KV capacity (max_seq) exhausted");

@@ -246,9 +246,27 @@ void Engine::create() {
     const char* f = std::getenv("SMO_CODEC");
     unary = !(f && std::strcmp(f, "fixed") == 0);
     tmode = opt.compress_experts == 2 || (f && std::strcmp(f, "tile") == 0);
-    if (tmode) SMO_REQUIRE(h % 128 == 0 && hi % 128 == 0, "engine: the tile code needs h and h_i multiples of 128");
-    cenc = dalloc<uint8_t>(tmode ? tcode_max_bytes(h, hi) : unary ? expert_code_bytes(blk_elems, 1) : cblk_bytes);
-    d_ovf = dalloc<int>(1);
+    const bool tile_ok = h % 128 == 0 && hi % 128 == 0;
+    if (tmode) SMO_REQUIRE(tile_ok, "engine: the tile code needs h and h_i multiples of 128");
+    cenc = dalloc<uint8_t>(std::max(tile_ok ? tcode_max_bytes(h, hi) : size_t(0),
+                                    unary ? expert_code_bytes(blk_elems, 1) : cblk_bytes));
+    // compress_experts = 1 without SMO_CODEC: the link code with fewer bytes on
+    // this model's weights, probed on the first expert block — unary (the
+    // geometric exponents of uniform-init blocks: 10.25 vs 10.42 bits/weight)
+    // or the tile code (gaussian-like blocks: 11.0 vs 11.46)
+    if (opt.compress_experts == 1 && !f && tile_ok && !owned.empty()) {
+      const uint64_t base = tid::layer(0) + tid::kExpert + 3ull * owned[0];
+      auto fill = cfg.expert_init == SMO_INIT_GAUSSIAN ? fill_normal : fill_uniform;
+      fill(stage, size_t(hi) * h, cfg.seed, base + 0, 0, std::sqrt(3.0f / h), st);
+      fill(stage + size_t(hi) * h, size_t(hi) * h, cfg.seed, base + 1, 0, std::sqrt(3.0f / h), st);
+      fill(stage + 2 * size_t(hi) * h, size_t(h) * hi, cfg.seed, base + 2, 0, std::sqrt(3.0f / hi), st);
+      SMO_CUDA_CHECK(cudaStreamSynchronize(st));
+      const size_t tb = tcode_encode(stage, h, hi, cenc, st);
+      expert_encode(stage, blk_elems, 1, cenc, d_ovf ? d_ovf : (d_ovf = dalloc<int>(1)), st);
+      const size_t ub = expert_coded_size(cenc, blk_elems, 1);
+      tmode = double(tb) < 0.99 * double(ub);
+    }
+    if (!d_ovf) d_ovf = dalloc<int>(1);
     blk_coded.assign(size_t(host_alias) * E_loc, 0);
     blk_csize.assign(size_t(host_alias) * E_loc, 0);
   }
@@ -291,8 +309,9 @@ void Engine::create() {
         blk_csize[size_t(a) * E_loc + local(e)] = cb;
         coded = true;
       };
-      if (ubytes && ubytes <= expert_code_bytes(blk_elems, 3)) keep(1, ubytes);
+      // a fixed window code only where it is smaller than unary (and holds the block)
       for (int bits = 3; xcomp && !coded && bits <= 4; ++bits) {
+        if (ubytes && expert_code_bytes(blk_elems, bits) >= ubytes) continue;
         SMO_CUDA_CHECK(cudaMemset(d_ovf, 0, sizeof(int)));
         expert_encode(stage, blk_elems, bits, cenc, d_ovf, st);
         int ovf = 0;
@@ -518,8 +537,23 @@ void Engine::create() {
     prefix_host = halloc_mapped<int32_t>(maxB);
     mask_host = halloc_mapped<uint64_t>(maxT);
     host_jobs.resize(size_t(L) * kMaxMb);
-    host_flags = halloc_mapped<uint32_t>(2);
-    async_host.start(host_flags, host_flags + 1);
+    ensure_async_host();
+  }
+  if (opt.draft_cpu_kv) {  // drafter CPU part (f1): host drafter K/V, q / attention staging
+    SMO_REQUIRE(dL > 0, "engine: draft_cpu_kv needs a drafter (draft_layers)");
+    SMO_REQUIRE(!paged, "engine: draft_cpu_kv needs contiguous K/V (kv_pages = 0)");
+    draft_cpu = true;
+    for (int l = 0; l < dL; ++l) {
+      dkc_h.push_back(halloc_mapped<uint16_t>(kv_elems()));
+      dvc_h.push_back(halloc_mapped<uint16_t>(kv_elems()));
+    }
+    dq_h = halloc_mapped<uint16_t>(size_t(maxB) * nq * d);
+    da_h = halloc_mapped<uint16_t>(size_t(maxB) * nq * d);
+    dpos_h = halloc_mapped<int32_t>(maxB);
+    dmask_h = halloc_mapped<uint64_t>(maxB);
+    for (int r = 0; r < maxB; ++r) dmask_h[r] = 1;
+    if (!cpu_pool) cpu_pool.reset(new CpuPool(int(std::max(1u, std::thread::hardware_concurrency()))));
+    ensure_async_host();
   }
   set_micro_batches(opt.micro_batches);
   // drafter + decode-loop state
@@ -555,6 +589,8 @@ void Engine::create() {
   for (auto& e : ev) SMO_CUDA_CHECK(cudaEventCreate(&e));
   draft_ev.resize(size_t(maxN) + 1);
   for (auto& e : draft_ev) SMO_CUDA_CHECK(cudaEventCreate(&e));
+  join_ev.resize(size_t(maxN));
+  for (auto& e : join_ev) SMO_CUDA_CHECK(cudaEventCreate(&e));
   dec_ev.resize(size_t(2) * L);
   for (auto& e : dec_ev) SMO_CUDA_CHECK(cudaEventCreate(&e));
   SMO_CUDA_CHECK(cudaDeviceSynchronize());
@@ -1263,6 +1299,59 @@ void Engine::copy_from_mapped(void* dst, const void* src, size_t bytes, cudaStre
   SMO_CUDA_CHECK(cudaGetLastError());
 }
 
+void Engine::ensure_async_host() {
+  if (host_flags) return;
+  host_flags = halloc_mapped<uint32_t>(2);
+  async_host.start(host_flags, host_flags + 1);
+}
+
+// Move requests between the drafter's GPU part (HBM K/V, K1) and CPU part
+// (pinned host K/V, host pool): their drafter K/V rows follow them.
+void Engine::set_draft_split(int g) {
+  SMO_REQUIRE(draft_cpu, "engine: the draft split needs draft_cpu_kv");
+  SMO_REQUIRE(dec_b > 0, "engine: set the draft split after prefill / decode_begin");
+  SMO_REQUIRE(g >= -1 && g <= dec_b, "engine: draft split out of range");
+  const int old_g = draft_g < 0 ? dec_b : draft_g;
+  const int new_g = g < 0 ? dec_b : g;
+  if (new_g == old_g) {
+    draft_g = g;
+    return;
+  }
+  SMO_CUDA_CHECK(cudaDeviceSynchronize());
+  const size_t kv_req = size_t(nkv) * s_max * d;  // elements per request (contiguous)
+  const int lo = std::min(old_g, new_g), hi_r = std::max(old_g, new_g);
+  const bool to_host = new_g < old_g;
+  for (int l = 0; l < dL; ++l) {
+    const size_t off = size_t(lo) * kv_req, bytes = size_t(hi_r - lo) * kv_req * 2;
+    if (to_host) {
+      SMO_CUDA_CHECK(cudaMemcpy(dkc_h[size_t(l)] + off, dlayers[size_t(l)].kc + off, bytes, cudaMemcpyDeviceToHost));
+      SMO_CUDA_CHECK(cudaMemcpy(dvc_h[size_t(l)] + off, dlayers[size_t(l)].vc + off, bytes, cudaMemcpyDeviceToHost));
+    } else {
+      SMO_CUDA_CHECK(cudaMemcpy(dlayers[size_t(l)].kc + off, dkc_h[size_t(l)] + off, bytes, cudaMemcpyHostToDevice));
+      SMO_CUDA_CHECK(cudaMemcpy(dlayers[size_t(l)].vc + off, dvc_h[size_t(l)] + off, bytes, cudaMemcpyHostToDevice));
+    }
+  }
+  draft_g = g;
+}
+
+int Engine::draft_split_times(double* out, size_t n) {
+  SMO_CUDA_CHECK(cudaDeviceSynchronize());
+  if (!last_was_decode || !last_split) return 0;
+  const int m = last_draft_steps;
+  SMO_REQUIRE(n >= size_t(3) * m, "draft_split_times: output too small");
+  for (int t = 0; t < m; ++t) {
+    float a = 0, b = 0;
+    SMO_CUDA_CHECK(cudaEventElapsedTime(&a, draft_ev[size_t(t)], join_ev[size_t(t)]));
+    SMO_CUDA_CHECK(cudaEventElapsedTime(&b, join_ev[size_t(t)], draft_ev[size_t(t) + 1]));
+    double host = 0;
+    for (uint32_t sq : step_seqs[size_t(t)]) host += double(async_host.dur_ns[sq & 255u].load(std::memory_order_acquire)) * 1e-9;
+    out[3 * t] = a * 1e-3;
+    out[3 * t + 1] = host;
+    out[3 * t + 2] = b * 1e-3;
+  }
+  return m;
+}
+
 void Engine::wait_host_flag(uint32_t seq, cudaStream_t st) {
   host_flag_wait_kernel<<<1, 1, 0, st>>>(host_flags + 1, seq);
   count_launch();
@@ -1312,7 +1401,11 @@ void Engine::AsyncHost::start(volatile uint32_t* ready, volatile uint32_t* done)
         }
       }
       std::atomic_thread_fence(std::memory_order_acquire);
+      const auto ts = std::chrono::steady_clock::now();
       cpu_verify_attention(it.job, *it.pool);
+      dur_ns[it.seq & 255u].store(
+          uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - ts).count()),
+          std::memory_order_release);
       std::atomic_thread_fence(std::memory_order_seq_cst);
       *done_flag = it.seq;  // publish (mapped pinned memory; the GPU polls it)
     }
@@ -1364,6 +1457,7 @@ void Engine::times(smo_stage_times* t) {
   r.h2d_bytes = last_h2d_bytes;
   r.codec = span(step_dec_ev);
   r.codec_bytes = step_codec_bytes;
+  r.link_code = tmode ? 2.0 : xcomp ? 1.0 : 0.0;
   for (double v : layer_raw_bytes) r.h2d_raw_bytes += v;
   r.others = std::max(0.0, r.target_total - r.attention - r.gpu_moe);
   *t = r;
@@ -1460,6 +1554,20 @@ smo_status smo_engine_draft_times(smo_engine* e, double* out, size_t n, int32_t*
   return smo::run_guarded([&] {
     SMO_REQUIRE(e && out && steps, "engine: null argument");
     *steps = e->impl.draft_times(out, n);
+  });
+}
+
+smo_status smo_engine_set_draft_split(smo_engine* e, int32_t gpu_requests) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(e, "engine: null argument");
+    e->impl.set_draft_split(gpu_requests);
+  });
+}
+
+smo_status smo_engine_draft_split_times(smo_engine* e, double* out, size_t n, int32_t* steps) {
+  return smo::run_guarded([&] {
+    SMO_REQUIRE(e && out && steps, "engine: null argument");
+    *steps = e->impl.draft_split_times(out, n);
   });
 }
 

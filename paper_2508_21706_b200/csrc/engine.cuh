@@ -127,6 +127,21 @@ struct Engine {
   };
   std::vector<DLayer> dlayers;
   int dL = 0, dI = 0;
+  // drafter GPU-part / CPU-part split (build_draft_dag
+  // pipeline.hpp:217-253): requests [draft_g, dec_b) keep their drafter K/V
+  // in pinned host memory (dkc_h / dvc_h, contiguous [maxB][n_kv][s_max][d])
+  // and attend on the host pool while the GPU part runs K1
+  bool draft_cpu = false;
+  int draft_g = -1;  // GPU-part requests; -1: all
+  std::vector<uint16_t*> dkc_h, dvc_h;
+  uint16_t *dq_h = nullptr, *da_h = nullptr;  // pinned mapped [maxB, n_q, d]: CPU-part q / attention out
+  int32_t* dpos_h = nullptr;                  // pinned mapped [maxB]: CPU-part positions (= prefix)
+  uint64_t* dmask_h = nullptr;                // pinned [maxB]: bit 0 (the row sees itself)
+  std::vector<cudaEvent_t> join_ev;           // [maxN]: host join of each drafter step
+  std::vector<std::vector<uint32_t>> step_seqs;  // host job sequence numbers of each drafter step
+  bool last_split = false;
+  void set_draft_split(int g);
+  int draft_split_times(double* out, size_t n);
   uint16_t* dh = nullptr;  // drafter SwiGLU activations [maxT, dI]
   int32_t *d_dtok = nullptr, *d_dpos = nullptr, *d_dout = nullptr;
   uint64_t* d_mask1 = nullptr;  // single-row chain mask (bit 0) per request
@@ -175,6 +190,7 @@ struct Engine {
     };
     std::thread th;
     std::mutex mu;
+    std::atomic<uint64_t> dur_ns[256];  // wall time of job seq (ring by seq & 255)
     std::condition_variable cv;
     std::vector<Item> q;
     size_t head = 0;
@@ -432,8 +448,8 @@ struct Engine {
 
   // One drafter step for b requests: token tok_in[r] at position pos[r]
   // (its K/V appended there), greedy next token into out_tok[r].
-  void draft_forward(int b, const int32_t* tok_in, const int32_t* pos, int max_pos, int32_t* out_tok,
-                     cudaStream_t st);
+  void draft_forward(int b, const int32_t* tok_in, const int32_t* pos, int max_pos, int32_t* out_tok, cudaStream_t st,
+                     int step = -1);
 
   // ------------------------------------------------------------------ decode
   void decode_begin(const int32_t* root_h, const int32_t* kv_h, int b);
@@ -460,6 +476,7 @@ struct Engine {
 
   // durations (s) of the drafter steps of the last decode step; returns count
   int draft_times(double* out, size_t n);
+  void ensure_async_host();
 
   void decode_read(int32_t* committed, int cap, int32_t* n_committed, int32_t* kv_len, int32_t* root);
 

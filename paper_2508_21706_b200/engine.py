@@ -173,7 +173,7 @@ class VerifyEngine:
                  expert_cache_bytes: int = 0, host_alias_layers: int = 0, device: int = 0, debug: bool = False,
                  ep_rank: int = 0, ep_size: int = 1, ep_group: Optional["EpGroup"] = None, kv_pages: int = 0,
                  attn_cpu: bool = False, batch_one: bool = False, compress_experts: int = 0,
-                 micro_batches: int = 1):
+                 micro_batches: int = 1, draft_cpu_kv: bool = False):
         self.shape = shape
         self.max_batch, self.max_verify, self.max_seq = max_batch, max_verify, max_seq
         if ep_size > 1 and ep_group is None:
@@ -184,7 +184,7 @@ class VerifyEngine:
         opt = L.EngineOptions(max_batch, max_verify, max_seq, hbm_slots, int(expert_cache_bytes),
                               host_alias_layers, device, L.ENGINE_DEBUG if debug else 0, ep_rank, ep_size,
                               None if ep_group is None else ep_group.handle, kv_pages, int(attn_cpu),
-                              int(batch_one), int(compress_experts), int(micro_batches))
+                              int(batch_one), int(compress_experts), int(micro_batches), int(draft_cpu_kv))
         cfg = shape.to_c()
         h = C.c_void_p()
         L.check(L.load().smo_engine_create(C.byref(cfg), C.byref(opt), C.byref(h)))
@@ -289,6 +289,19 @@ class VerifyEngine:
         """`steps` drafter-driven iterations (asynchronous); graph=True replays
         one captured CUDA graph per iteration (needs a non-default stream)."""
         L.check(L.load().smo_engine_decode_run(self._h, k, steps, int(graph), C.c_void_p(stream or 0)))
+
+    def set_draft_split(self, gpu_requests: int) -> None:
+        """Drafter GPU part = requests [0, gpu_requests), CPU part (host K/V,
+        host-pool attention) = the rest; -1: all on the GPU (draft_cpu_kv)."""
+        L.check(L.load().smo_engine_set_draft_split(self._h, int(gpu_requests)))
+
+    def draft_split_times(self, max_steps: int = 64) -> np.ndarray:
+        """[steps, 3] (GPU part, host attention, GPU after the join) seconds of
+        the last decode step's drafter steps; empty if it ran without a split."""
+        out = np.zeros(3 * max_steps, np.float64)
+        n = C.c_int32(0)
+        L.check(L.load().smo_engine_draft_split_times(self._h, out.ctypes.data_as(C.c_void_p), out.size, C.byref(n)))
+        return out[:3 * n.value].reshape(n.value, 3)
 
     def decode_read(self, b: int, cap: int):
         """(committed [b, cap] -1 padded, n_committed [b], kv_len [b], root [b])"""

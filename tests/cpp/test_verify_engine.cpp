@@ -277,3 +277,92 @@ TEST_CASE("closed loop: prefill -> measured fit -> controller picks k -> decode 
     CHECK(std::vector<std::int32_t>(ref[r].begin(), ref[r].begin() + std::ptrdiff_t(spec[r].size())) == spec[r]);
   }
 }
+
+TEST_CASE("drafter split: dynamic_split_ratio moves requests to the host part, build_draft_dag structure, greedy") {
+  HardwareSpec hw = b200();
+  ModelSpec m = tiny();
+  WorkloadSpec w = apps();
+  Hyperparameters hp;
+  hp.b = 3;
+  hp.k = 4;
+  MemoryPlan plan = plan_memory(hw, m, w, hp.b, hp.mem_policy);
+  EngineOptions opt;
+  opt.max_seq = 512;
+  opt.seed = 0x5EED + 7;
+  opt.lm_scale = 8.0f;
+  opt.router_scale = 4.0f;
+  std::vector<std::vector<std::int32_t>> prompts(3);
+  std::uint64_t lcg = 777;
+  const int lens[3] = {40, 17, 9};
+  for (int r = 0; r < 3; ++r)
+    for (int i = 0; i < lens[r]; ++i) {
+      lcg = lcg * 6364136223846793005ull + 1442695040888963407ull;
+      prompts[std::size_t(r)].push_back(std::int32_t((lcg >> 33) % 32000));
+    }
+  // an HBM budget that holds the draft K/V of ~500 / (16 B x current length)
+  // requests: 1 of 3 at the start, none once the mean length passes 31
+  HardwareSpec tight = hw;
+  tight.gpu_mem = m.draft.param_bytes + 500.0;
+  EngineOptions so = opt;
+  so.draft_cpu_kv = true;
+  MemoryPolicy pol;
+  pol.activation_bytes = 0;
+  so.draft_split_policy = pol;
+  VerifyEngine eng(tight, m, hp, plan, so);
+  eng.prefill(prompts);
+  bool partial = false, all_cpu = false;
+  for (int it = 0; it < 8; ++it) {
+    const int k = 2 + it % 2;  // two driving values per stage for the fit below
+    IterationResult r = eng.decode_step(k);
+    const std::int64_t g = eng.draft_split_history().back();
+    if (g >= 3) {
+      CHECK(r.draft_dag.size() == std::size_t(k + 1));
+      continue;
+    }
+    partial = partial || g > 0;
+    all_cpu = all_cpu || g == 0;
+    std::size_t n_gpu = 0, n_cpu = 0, n_ffn = 0;
+    for (const auto& ev : r.draft_dag) {
+      if (ev.kind == EventKind::DRAFT_GPU_STEP) ++n_gpu;
+      if (ev.kind == EventKind::DRAFT_CPU_ATTN) {
+        ++n_cpu;
+        CHECK(ev.resource == ExecResource::CPU);
+        CHECK(ev.duration > 0);
+      }
+      if (ev.kind == EventKind::DRAFT_GPU_FFN) {
+        ++n_ffn;
+        REQUIRE(ev.deps.size() == 1);
+        CHECK(r.draft_dag[std::size_t(ev.deps[0])].kind == EventKind::DRAFT_CPU_ATTN);
+      }
+    }
+    CHECK(n_cpu == std::size_t(k + 1));
+    CHECK(n_ffn == std::size_t(k + 1));
+    CHECK(n_gpu == (g > 0 ? std::size_t(k + 1) : 0u));
+    CHECK(r.breakdown.draft_cpu_part > 0);
+    // the same structure as the reference's DAG for these splits
+    CHECK(build_draft_dag(DraftStepDurations{}, k + 1, g, 3 - g).size() == r.draft_dag.size());
+  }
+  const auto& hist = eng.draft_split_history();
+  for (std::size_t i = 1; i < hist.size(); ++i) CHECK(hist[i] <= hist[i - 1]);  // nonincreasing in length
+  CHECK(partial);
+  CHECK(all_cpu);
+  // DRAFT_CPU_ATTN samples on the reference's driving variable (cpu requests x
+  // prefix, pipeline.hpp:262) for fit_latency_models
+  std::vector<double> xs;
+  for (const auto& sm : eng.profile())
+    if (sm.kind == EventKind::DRAFT_CPU_ATTN) xs.push_back(sm.driving);
+  CHECK(xs.size() >= 8);
+  CHECK(*std::max_element(xs.begin(), xs.end()) > *std::min_element(xs.begin(), xs.end()));
+  const auto split = eng.committed();
+  // greedy invariance: the split only moves where the drafter attends
+  VerifyEngine plain(hw, m, hp, plan, opt);
+  plain.prefill(prompts);
+  for (int it = 0; it < 8; ++it) plain.decode_step(2 + it % 2);
+  const auto ref = plain.committed();
+  for (std::size_t r = 0; r < split.size(); ++r) {
+    const std::size_t nn = std::min(ref[r].size(), split[r].size());
+    CHECK(nn >= 8);
+    CHECK(std::vector<std::int32_t>(ref[r].begin(), ref[r].begin() + std::ptrdiff_t(nn)) ==
+          std::vector<std::int32_t>(split[r].begin(), split[r].begin() + std::ptrdiff_t(nn)));
+  }
+}

@@ -378,3 +378,37 @@ def test_paged_graph_decode_matches_paged_eager(ref):
         eng.close()
     for a, c in zip(out[0], out[1]):
         assert np.array_equal(a, c)
+
+
+@pytest.mark.parametrize("g", [1, 0])
+def test_drafter_cpu_split_commits_greedy_sequence(ref, g):
+    """Drafter CPU part: requests [g, b) keep their drafter
+    K/V in pinned host memory and attend on the host pool while K1 attends
+    the GPU part. Greedy verification makes the committed tokens independent
+    of where the drafter attended: identical to an all-GPU engine; the split
+    measures a host attention time per drafter step."""
+    from paper_2508_21706_b200.engine import VerifyEngine as _VE
+    s, om, _ = ref
+    b, steps, k = len(PROMPTS), 8, 3
+    prompts = _prompts(s)
+    out = {}
+    for split in (False, True):
+        eng = _VE(s, max_batch=b, max_verify=6, max_seq=256, draft_cpu_kv=split)
+        nxt = eng.prefill(prompts)
+        if split:
+            eng.set_draft_split(g)
+        times = []
+        for _ in range(steps):
+            eng.decode_step(k)
+            if split:
+                times.append(eng.draft_split_times())
+        out[split] = (nxt, eng.decode_read(b, 128))
+        eng.close()
+        if split:
+            for t in times:
+                assert t.shape == (k + 1, 3) and np.all(t[:, 1] > 0) and np.all(t >= 0)
+    (n0, (c0, m0, kv0, _)), (n1, (c1, m1, kv1, _)) = out[False], out[True]
+    assert np.array_equal(n0, n1)
+    for r in range(b):
+        m = min(m0[r], m1[r])
+        assert m >= steps and np.array_equal(c0[r, :m], c1[r, :m]), r

@@ -346,6 +346,7 @@ def test_coded_hot_cache_bit_identical(cuda, batch_one, monkeypatch):
     them into the layer's slot every step: bit-identical to a bf16 cache of
     the same byte budget, with more experts cached (fewer bytes streamed)."""
     from paper_2508_21706_b200.engine import VerifyEngine
+    monkeypatch.setenv("SMO_CODEC", "unary")  # the expansion path (the tile code always caches coded)
     s = _shape()
     b, n = 4, 5
     prefix = np.array([300, 17, 64, 1], np.int32)
