@@ -364,7 +364,9 @@ typedef struct {
                                  0 = LARGE_BATCH: stream whole layers ahead (layer l+S during l);
                                  1 = BATCH_ONE: after layer l's router, stream only the experts its
                                  tokens selected (host waits for the routing, then issues the copies).
-                                 Prefill always streams whole layers. Not with expert parallelism. */
+                                 Prefill always streams whole layers. With expert parallelism each
+                                 owner streams its local experts that received rows, once the
+                                 dispatch exchange has landed (no link-gap prefetch). */
   int32_t compress_experts;   /* 1: experts sit in pinned host DRAM in the smallest lossless code of
                                  smo_expert_encode that holds the block (unary exponents: 1.56x fewer
                                  bytes on uniform-init weights; 3-bit window 1.41x; 4-bit 1.29x;

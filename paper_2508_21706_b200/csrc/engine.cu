@@ -151,11 +151,10 @@ void Engine::create() {
   }
   kv_known.assign(size_t(maxB), 0);
   if (opt.moe_batching) {
-    SMO_REQUIRE(!(opt.ep_size > 1 || opt.nccl_comm), "engine: BATCH_ONE streaming is not available with expert parallelism");
     batch_one = true;
     SMO_CUDA_CHECK(cudaEventCreateWithFlags(&route_ev, cudaEventDisableTiming));
     const char* f = std::getenv("SMO_B1_PREFETCH");
-    b1_prefetch = !(f && f[0] == '0');
+    b1_prefetch = !(f && f[0] == '0') && !(opt.ep_size > 1 || opt.nccl_comm);  // (1 GPU: global routing on host)
   }
   if (opt.attn_cpu) {
     SMO_REQUIRE(!paged, "engine: the CPU attention placement keeps contiguous host K/V (kv_pages = 0)");
@@ -694,7 +693,8 @@ void Engine::snap(const char* name, int layer, const void* src, size_t bytes, cu
 }
 
 // Expert-parallel MoE of layer l (ep.cu): dispatch, local shard, combine.
-void Engine::moe_ep(int l, int T, cudaStream_t st) {
+double Engine::moe_ep(int l, int T, cudaStream_t st, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* h2d_ev) {
+  double streamed = 0;
   const int PT = T * K;
   const int rank = opt.ep_rank;
   ep_pos(oid, pos, offsets, PT, E_loc, ep_rows, pos_ep, st);
@@ -709,6 +709,18 @@ void Engine::moe_ep(int l, int T, cudaStream_t st) {
     ep_pack(xp, offsets, P, E_loc, C, h, blk_d, ep_send, st);
     ept->alltoall(rank, ep_send, ep_recv, blk_d, st);
     ep_unpack(ep_recv, P, E_loc, C, h, blk_d, xl, offsets_l, back, st);
+  }
+  if (batch_one) {
+    // BATCH_ONE with expert parallelism: the rows every rank routed to this
+    // rank's experts are known once the dispatch exchange landed; stream
+    // only the local experts that received any (optimizer.hpp:81-96)
+    SMO_CUDA_CHECK(cudaMemcpyAsync(h_offsets, offsets_l, size_t(E_loc + 1) * 4, cudaMemcpyDeviceToHost, st));
+    SMO_CUDA_CHECK(cudaEventRecord(route_ev, st));
+    SMO_CUDA_CHECK(cudaEventSynchronize(route_ev));
+    std::vector<uint8_t> act(size_t(E_loc), 0);
+    for (int le = 0; le < E_loc; ++le) act[size_t(le)] = h_offsets[le + 1] > h_offsets[le] ? 1 : 0;
+    streamed += enqueue_h2d(l, tev(l * 8 + 0), tev(l * 8 + 1), act.data());
+    if (h2d_ev) h2d_ev->push_back({tev(l * 8 + 0), tev(l * 8 + 1)});
   }
   SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 7), st));
   SMO_CUDA_CHECK(cudaStreamWaitEvent(st, slot_ready[l % slots], 0));
@@ -767,6 +779,7 @@ void Engine::moe_ep(int l, int T, cudaStream_t st) {
     ept->alltoall(rank, ep_sendback, ep_recvback, size_t(C) * h * sizeof(float), st);
     unpermute_combine(ep_recvback, pos_ep, rw, T, K, h, x, st);
   }
+  return streamed;
 }
 
 void Engine::verify(const smo_verify_batch& in, smo_verify_output& out, cudaStream_t st) {
@@ -1078,7 +1091,7 @@ void Engine::verify_core(int b, int n, const int32_t* tokens, const int32_t* par
         snap("offsets", l, offsets, size_t(E + 1) * 4, st);
         snap("pos", l, pos, size_t(PT) * 4, st);
       }
-      if (batch_one) {
+      if (batch_one && !ep_on) {
         // BATCH_ONE (optimizer.hpp:81-96): wait for this layer's routing, then
         // stream only the experts its tokens selected
         SMO_CUDA_CHECK(cudaMemcpyAsync(h_offsets, offsets, size_t(E + 1) * 4, cudaMemcpyDeviceToHost, st));
@@ -1130,7 +1143,7 @@ void Engine::verify_core(int b, int n, const int32_t* tokens, const int32_t* par
     for (int j = 0; j < M; ++j) {
       const Mb& m = mbs[size_t(j)];
       if (ep_on) {
-        moe_ep(l, T, st);
+        h2d_bytes += moe_ep(l, T, st, &h2d_ev);
         SMO_CUDA_CHECK(cudaEventRecord(tev(l * 8 + 5), st));
       } else {
         if (j == 0) {

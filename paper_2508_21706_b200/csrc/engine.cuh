@@ -392,7 +392,7 @@ struct Engine {
   void snap(const char* name, int layer, const void* src, size_t bytes, cudaStream_t st);
 
   // Expert-parallel MoE of layer l (ep.cu): dispatch, local shard, combine.
-  void moe_ep(int l, int T, cudaStream_t st);
+  double moe_ep(int l, int T, cudaStream_t st, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* h2d_ev = nullptr);
 
   cudaEvent_t tev(int i) const { return ev[8 + size_t(i)]; }
 

@@ -42,19 +42,21 @@ def _run_ep(shape, P, tokens, prefix, s_max, debug=True, **kw):
     return engines, results, grp
 
 
-@pytest.mark.parametrize("P,compress", [(2, False), (4, False), (2, True)])
-def test_ep_loopback_bit_identical_to_single_gpu(cuda, P, compress):
+@pytest.mark.parametrize("P,compress,batch_one", [(2, False, False), (4, False, False), (2, True, False),
+                                                 (2, False, True), (4, True, True)])
+def test_ep_loopback_bit_identical_to_single_gpu(cuda, P, compress, batch_one):
     """Rank r's tokens go to every owner and come back; each token's result
     depends only on its own request, so rank r's EP outputs must equal a
     single-GPU engine run on rank r's requests alone, bit for bit (the
-    procedural prefix KV is indexed by the engine-local request)."""
+    procedural prefix KV is indexed by the engine-local request). BATCH_ONE:
+    each owner streams only its local experts that received rows."""
     from paper_2508_21706_b200.engine import TINY, VerifyEngine
     shape = dataclasses.replace(TINY, seed=0x5EED + 3, lm_scale=8.0, router_scale=4.0)
     s_max = PREFIX + N + 64
     rng = np.random.default_rng(11)
     tokens = rng.integers(0, shape.vocab, size=(B, N)).astype(np.int32)
     prefix = np.array([PREFIX, PREFIX - 3, 200, 1], np.int32)
-    engines, results, grp = _run_ep(shape, P, tokens, prefix, s_max, compress_experts=compress)
+    engines, results, grp = _run_ep(shape, P, tokens, prefix, s_max, compress_experts=compress, batch_one=batch_one)
     bl = B // P
     for r in range(P):
         ref = VerifyEngine(shape, max_batch=bl, max_verify=N, max_seq=s_max, debug=True)
@@ -71,8 +73,11 @@ def test_ep_loopback_bit_identical_to_single_gpu(cuda, P, compress):
     # each rank streamed only its shard of the experts
     t0 = engines[0].last_times()
     raw = shape.n_layers * (shape.n_expert // P) * shape.expert_bytes
+    if batch_one:  # only the routed local experts
+        assert 0 < t0["h2d_raw_bytes"] <= raw and t0["h2d_raw_bytes"] % shape.expert_bytes == 0
+        raw = t0["h2d_raw_bytes"]
     assert t0["h2d_raw_bytes"] == raw
-    if compress:  # coded blocks: the unary code, below the 3-bit window's 1456 B per 1024 weights
+    if compress:  # coded blocks (unary or tile code), below the 3-bit window's 1456 B per 1024 weights
         assert 0 < t0["h2d_bytes"] <= raw * 1456 // 2048
     else:
         assert t0["h2d_bytes"] == raw
