@@ -708,6 +708,7 @@ def run_ours(args):
                    if args.compress else "raw bf16",
                    "l2": "inputs larger than L2 (90.2 GB of experts + 4.6 GB KV streamed per step)",
                    "expert_init": args.init,
+                   "host_numa_node": int(stages.get("host_numa", -1)),
                    "parallelism": mode},
         "committed_tokens_per_s_model": world * b * geometric_alpha(0.8, args.k) / t_step,
         "h2d": {"achieved_gbs": h2d_bytes / t_step / 1e9, "link_peak_gbs": h2d_peak,

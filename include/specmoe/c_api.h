@@ -484,6 +484,8 @@ typedef struct {
   double codec_bytes;  /* their algorithmic bytes: code read + bf16 written (streamed + coded hot cache) */
   double link_code;    /* the engine's expert link code: 0 raw bf16, 1 unary / window codes expanded in HBM,
                           2 T2 tile code decoded inside the expert kernel */
+  double host_numa;    /* NUMA node the pinned expert blocks were bound to (the GPU's own; -1: default
+                          placement, e.g. a single-node host or SMO_HOST_NUMA=-1) */
 } smo_stage_times;
 smo_status smo_engine_last_times(smo_engine* e, smo_stage_times* t);
 /* Measured per-layer timeline of the last verify step with m micro-batches

@@ -17,6 +17,14 @@
 // layouts: W1,W3 [h_i, h], W2 [h, h_i]); the HBM pool holds S staging slots of
 // E blocks each plus the hot-expert cache (MemoryPolicy.expert_cache_bytes,
 // config.hpp:103-108), filled once at creation.
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <cctype>
+#include <cstdio>
+
 #include "engine.cuh"
 
 namespace smo {
@@ -49,6 +57,58 @@ void Engine::bt_sync(cudaStream_t st) {
   if (!paged || !bt_dirty) return;
   SMO_CUDA_CHECK(cudaMemcpyAsync(d_bt, h_bt, size_t(maxB) * max_pages * 4, cudaMemcpyHostToDevice, st));
   bt_dirty = false;
+}
+
+int device_numa_node(int device) {
+  if (const char* f = std::getenv("SMO_HOST_NUMA")) return std::atoi(f);  // -1: no placement
+  struct stat sb {};
+  if (stat("/sys/devices/system/node/node1", &sb) != 0) return -1;  // single-node host
+  char bus[32] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof(bus), device) != cudaSuccess) return -1;
+  for (char* c = bus; *c; ++c) *c = char(std::tolower(*c));
+  std::string path = std::string("/sys/bus/pci/devices/") + bus + "/numa_node";
+  FILE* f = std::fopen(path.c_str(), "r");
+  if (!f) {  // sysfs uses a 4-hex-digit domain; CUDA prints 8
+    if (std::strlen(bus) > 12) f = std::fopen((std::string("/sys/bus/pci/devices/") + (bus + 4) + "/numa_node").c_str(), "r");
+    if (!f) return -1;
+  }
+  int node = -1;
+  if (std::fscanf(f, "%d", &node) != 1) node = -1;
+  std::fclose(f);
+  return node;
+}
+
+void* pinned_alloc(size_t bytes, int node, size_t* bytes_out) {
+  *bytes_out = 0;
+  if (node >= 0 && node < 64) {
+    void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
+    if (p != MAP_FAILED) {
+      unsigned long mask = 1ul << node;
+      const long rc = syscall(SYS_mbind, p, bytes, 2 /* MPOL_BIND */, &mask, 64ul, 0u);
+      if (rc == 0 && cudaHostRegister(p, bytes, cudaHostRegisterPortable) == cudaSuccess) {
+        *bytes_out = bytes;
+        return p;
+      }
+      cudaGetLastError();
+      munmap(p, bytes);
+    }
+  }
+  void* hp = nullptr;
+  if (cudaHostAlloc(&hp, bytes, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return hp;
+}
+
+void pinned_free(void* p, size_t numa_bytes) {
+  if (!p) return;
+  if (numa_bytes) {
+    cudaHostUnregister(p);
+    munmap(p, numa_bytes);
+  } else {
+    cudaFreeHost(p);
+  }
 }
 
 // expand layer l's coded blocks (streamed into cstage) into its pool slot,
@@ -235,6 +295,7 @@ void Engine::create() {
   for (int e = 0; e < E; ++e)
     if (owns(e)) owned.push_back(e);
   host_bufs.assign(host_alias, nullptr);
+  host_numa = device_numa_node(opt.device);
   uint16_t* stage = dalloc<uint16_t>(blk_elems);
   xcomp = opt.compress_experts != 0;
   uint8_t* cenc = nullptr;
@@ -270,12 +331,13 @@ void Engine::create() {
     blk_csize.assign(size_t(host_alias) * E_loc, 0);
   }
   for (int a = 0; a < host_alias; ++a) {
-    void* hp = nullptr;
-    cudaError_t err = cudaHostAlloc(&hp, blk_bytes * E_loc, cudaHostAllocPortable);
-    if (err != cudaSuccess)
-      throw Error(SMO_CAPACITY, "engine: pinned host allocation of " + std::to_string(blk_bytes * E) +
-                                    " bytes failed (" + cudaGetErrorString(err) + "); set host_alias_layers");
+    size_t nb = 0;
+    void* hp = pinned_alloc(blk_bytes * E_loc, host_numa, &nb);
+    if (!hp)
+      throw Error(SMO_CAPACITY, "engine: pinned host allocation of " + std::to_string(blk_bytes * E_loc) +
+                                    " bytes failed; set host_alias_layers");
     host_bufs[a] = reinterpret_cast<uint16_t*>(hp);
+    host_numa_bytes.push_back(nb);
     for (int e : owned) {
       const uint64_t base = tid::layer(a) + tid::kExpert + 3ull * e;
       auto fill = cfg.expert_init == SMO_INIT_GAUSSIAN ? fill_normal : fill_uniform;
@@ -1471,6 +1533,9 @@ void Engine::times(smo_stage_times* t) {
   r.codec = span(step_dec_ev);
   r.codec_bytes = step_codec_bytes;
   r.link_code = tmode ? 2.0 : xcomp ? 1.0 : 0.0;
+  bool bound = !host_numa_bytes.empty();
+  for (size_t b : host_numa_bytes) bound = bound && b > 0;
+  r.host_numa = bound ? double(host_numa) : -1.0;
   for (double v : layer_raw_bytes) r.h2d_raw_bytes += v;
   r.others = std::max(0.0, r.target_total - r.attention - r.gpu_moe);
   *t = r;

@@ -104,6 +104,14 @@ struct DevBuf {
   size_t bytes = 0;
 };
 
+// Pinned host memory for the expert blocks, placed on a NUMA node (the
+// GPU's own, so each rank's shard crosses only its local root complex):
+// mmap + mbind(MPOL_BIND) + cudaHostRegister; bytes_out = 0 when it fell
+// back to cudaHostAlloc (single-node hosts, SMO_HOST_NUMA=-1, any failure).
+int device_numa_node(int device);
+void* pinned_alloc(size_t bytes, int node, size_t* bytes_out);
+void pinned_free(void* p, size_t numa_bytes);
+
 struct Engine {
   smo_model_config cfg{};
   smo_engine_options opt{};
@@ -245,6 +253,8 @@ struct Engine {
   std::vector<cudaEvent_t> draft_ev;  // [maxN + 1]: boundaries of the drafter steps
   int last_draft_steps = 0;
   std::vector<uint16_t*> host_bufs;  // pinned, E blocks each
+  std::vector<size_t> host_numa_bytes;  // > 0: placed on the GPU's NUMA node (mmap + mbind + cudaHostRegister)
+  int host_numa = -1;                   // NUMA node of the expert buffers (-1: default placement)
   int host_alias = 0;
   // expert pool in HBM
   uint16_t* pool = nullptr;
@@ -308,7 +318,7 @@ struct Engine {
     for (auto e : dec_ev) cudaEventDestroy(e);
     if (route_ev) cudaEventDestroy(route_ev);
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
-    for (auto hb : host_bufs) cudaFreeHost(hb);
+    for (size_t i = 0; i < host_bufs.size(); ++i) pinned_free(host_bufs[i], i < host_numa_bytes.size() ? host_numa_bytes[i] : 0);
     if (h_stage) cudaFreeHost(h_stage);
     if (h_bt) cudaFreeHost(h_bt);
     cpu_pool.reset();

@@ -430,3 +430,23 @@ def test_micro_batches_match_one_batch(cuda, attn_cpu):
             assert np.array_equal(res[m][0][i], res[1][0][i])
         x1, xm = res[1][2], res[m][2]
         assert np.sqrt(np.mean((x1 - xm) ** 2) / np.mean(x1 ** 2)) < 1e-3
+
+
+def test_numa_bound_expert_buffers(cuda, monkeypatch):
+    """SMO_HOST_NUMA=<node>: the pinned expert blocks are mmap'd, mbind'ed to
+    the node and registered with CUDA (the path a multi-socket box takes for
+    each rank's shard, on the GPU's own node); results bit-identical."""
+    from paper_2508_21706_b200.engine import VerifyEngine
+    s = _shape()
+    b, n = 2, 3
+    prefix = np.array([40, 7], np.int32)
+    tokens = np.random.default_rng(12).integers(0, s.vocab, size=(b, n)).astype(np.int32)
+    out = {}
+    for node in ("-1", "0"):
+        monkeypatch.setenv("SMO_HOST_NUMA", node)
+        eng = VerifyEngine(s, max_batch=b, max_verify=n, max_seq=128)
+        eng.fill_prefix(prefix)
+        out[node] = (eng.verify(tokens, prefix), eng.last_times())
+        eng.close()
+    assert out["-1"][1]["host_numa"] == -1 and out["0"][1]["host_numa"] == 0
+    assert np.array_equal(out["-1"][0].target, out["0"][0].target)
