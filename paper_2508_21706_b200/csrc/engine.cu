@@ -538,6 +538,8 @@ void Engine::create() {
     hbuf = dalloc<uint16_t>(size_t(P) * hi);
   }
   {
+    const char* sp = std::getenv("SMO_STEP_PREFETCH");
+    step_pf = !(sp && sp[0] == '0');
     const char* f = std::getenv("SMO_MOE_FUSED");
     moe_fused = tmode || !(f && f[0] == '0');  // the tile-coded expert kernel is the fused one
   }
@@ -985,10 +987,40 @@ void Engine::begin_step(cudaStream_t st, bool prefetch) {
   step_codec_bytes = 0;
   std::fill(layer_bytes.begin(), layer_bytes.end(), 0.0);
   std::fill(layer_raw_bytes.begin(), layer_raw_bytes.end(), 0.0);
+  const bool have_pf = next_pf && !capturing;  // (a graph must contain its own copies)
+  next_pf = false;
   for (int l = 0; prefetch && l < std::min(slots, L); ++l) {
+    if (have_pf) {  // already streaming since the previous step's end
+      step_h2d_bytes += pf_bytes[size_t(l)];
+      layer_bytes[size_t(l)] = pf_bytes[size_t(l)];
+      layer_raw_bytes[size_t(l)] = pf_raw[size_t(l)];
+      step_h2d_ev.push_back({pf_ev[size_t(2 * l)], pf_ev[size_t(2 * l + 1)]});
+      continue;
+    }
     step_h2d_bytes += enqueue_h2d(l, tev(l * 8 + 0), tev(l * 8 + 1));
     step_h2d_ev.push_back({tev(l * 8 + 0), tev(l * 8 + 1)});
   }
+}
+
+void Engine::prefetch_next_step() {
+  if (!step_pf || batch_one || capturing || L <= slots) return;
+  const int n = std::min(slots, L);
+  if (pf_ev.empty()) {
+    pf_ev.resize(size_t(2 * slots));
+    for (auto& e : pf_ev) SMO_CUDA_CHECK(cudaEventCreate(&e));
+    pf_bytes.assign(size_t(slots), 0.0);
+    pf_raw.assign(size_t(slots), 0.0);
+  }
+  // this step's per-layer byte accounting of layers [0, n) stays as measured
+  std::vector<double> lb(layer_bytes.begin(), layer_bytes.begin() + n), lr(layer_raw_bytes.begin(),
+                                                                            layer_raw_bytes.begin() + n);
+  for (int l = 0; l < n; ++l) {
+    pf_bytes[size_t(l)] = enqueue_h2d(l, pf_ev[size_t(2 * l)], pf_ev[size_t(2 * l + 1)]);
+    pf_raw[size_t(l)] = layer_raw_bytes[size_t(l)];
+  }
+  std::copy(lb.begin(), lb.end(), layer_bytes.begin());
+  std::copy(lr.begin(), lr.end(), layer_raw_bytes.begin());
+  next_pf = true;
 }
 
 // The target verification DAG on device inputs: tokens [b*n], parent
@@ -1273,6 +1305,7 @@ void Engine::verify_core(int b, int n, const int32_t* tokens, const int32_t* par
       h2d_ev.push_back({tev(ln * 8 + 0), tev(ln * 8 + 1)});
     }
   }
+  prefetch_next_step();  // the next step's first layers, into the slots this step just freed
   // ---- LM head with fused argmax partials, then K6
   rmsnorm(x, final_norm, T, h, cfg.rms_eps, xn, st);
   snap("xf", -1, xn, size_t(T) * h * 2, st);

@@ -316,6 +316,8 @@ struct Engine {
     for (auto e : ev) cudaEventDestroy(e);
     for (auto e : draft_ev) cudaEventDestroy(e);
     for (auto e : dec_ev) cudaEventDestroy(e);
+    for (auto e : pf_ev) cudaEventDestroy(e);
+    for (auto e : join_ev) cudaEventDestroy(e);
     if (route_ev) cudaEventDestroy(route_ev);
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     for (size_t i = 0; i < host_bufs.size(); ++i) pinned_free(host_bufs[i], i < host_numa_bytes.size() ? host_numa_bytes[i] : 0);
@@ -482,6 +484,16 @@ struct Engine {
   int64_t graph_bound = -1;
   uint64_t graph_launches = 0;
   bool capturing = false;
+  // Cross-step prefetch (LARGE_BATCH): the experts are the same every step,
+  // so once a step has enqueued its last layer's copy, layers [0, slots) of
+  // the NEXT step start streaming into their freed slots — the link does not
+  // idle through the step's tail (last layer, LM head, accept) and the host
+  // round trip of a synchronous API call. SMO_STEP_PREFETCH=0 disables.
+  bool step_pf = true;
+  bool next_pf = false;
+  std::vector<cudaEvent_t> pf_ev;           // [2*slots] copy start / end per prefetched layer
+  std::vector<double> pf_bytes, pf_raw;     // [slots]
+  void prefetch_next_step();
   void decode_run(int k, int steps, bool graph, cudaStream_t st);
 
   // durations (s) of the drafter steps of the last decode step; returns count

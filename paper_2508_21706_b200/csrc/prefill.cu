@@ -37,6 +37,7 @@ void Engine::prefill(const int32_t* tok_h, const int32_t* len_h, int b, int Lmax
   SMO_REQUIRE(int64_t(nch) * C + maxN <= s_max, "prefill: prompt exceeds max_seq");
   for (int r = 0; r < b; ++r) SMO_REQUIRE(len_h[r] >= 1 && len_h[r] <= Lmax, "prefill: len out of range");
   draft_g = -1;  // the prefill writes every request's drafter K/V in HBM
+  next_pf = false;  // (a pending cross-step prefetch only duplicates the prefill's own copies)
   const int Tp = b * nch * C;
   std::vector<int32_t> tok(size_t(Tp), 0), pre(size_t(nch) * b);
   for (int c = 0; c < nch; ++c)

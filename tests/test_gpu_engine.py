@@ -450,3 +450,32 @@ def test_numa_bound_expert_buffers(cuda, monkeypatch):
         eng.close()
     assert out["-1"][1]["host_numa"] == -1 and out["0"][1]["host_numa"] == 0
     assert np.array_equal(out["-1"][0].target, out["0"][0].target)
+
+
+@pytest.mark.parametrize("compress", [0, 1])
+def test_cross_step_prefetch_bit_identical(cuda, compress, monkeypatch):
+    """The next step's first layers stream into their slots at the end of a
+    step (SMO_STEP_PREFETCH, default on): consecutive verify steps give the
+    same results and the same per-step link bytes as without it."""
+    from paper_2508_21706_b200.engine import VerifyEngine
+    s = _shape()
+    b, n = 4, 5
+    prefix = np.array([300, 17, 64, 1], np.int32)
+    rng = np.random.default_rng(13)
+    toks = [rng.integers(0, s.vocab, size=(b, n)).astype(np.int32) for _ in range(3)]
+    out = {}
+    for pf in ("0", "1"):
+        monkeypatch.setenv("SMO_STEP_PREFETCH", pf)
+        eng = VerifyEngine(s, max_batch=b, max_verify=n, max_seq=512, compress_experts=compress,
+                           expert_cache_bytes=s.expert_bytes)
+        eng.fill_prefix(prefix)
+        res = []
+        for t in toks:
+            r = eng.verify(t, prefix)
+            res.append((r, eng.last_times()["h2d_bytes"]))
+        out[pf] = res
+        eng.close()
+    for (r0, b0), (r1, b1) in zip(out["0"], out["1"]):
+        assert np.array_equal(r0.target, r1.target)
+        assert np.array_equal(r0.acc_len, r1.acc_len) and np.array_equal(r0.bonus, r1.bonus)
+        assert b0 == b1
