@@ -69,7 +69,7 @@ def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     go = os.path.join(ROOT, "gpurun_out")
     parts = [f"# ncu summary — {tag}", "",
-             "Captured with `tools/prof_{}.sh` under gpurun on one B200 (`--clock-control none`).".format(tag),
+             "Captured with `tools/gpu.sh {} launches` under gpurun on one B200 (`--clock-control none`).".format(tag),
              "Launch-list times are cold-cache and serialised: compare shares, not absolutes.", ""]
     lp = os.path.join(go, f"launches_{tag}.csv")
     if os.path.exists(lp):
