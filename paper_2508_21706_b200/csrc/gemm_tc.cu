@@ -13,6 +13,7 @@
 //   FLOPs = 2 * rows * N * K (x2 for SwiGLU), HBM bytes ~= weight bytes
 //   (N*K*2 per group, x2 for SwiGLU) + activations.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -42,6 +43,7 @@ struct GemmParams {
   int kb_per_split;
   int token_tiles;
   float* partial;    // [split_k][rows][N] fp32 when split_k > 1
+  int cluster;       // CTAs along the weight tiles sharing each token-row box by TMA multicast (1: none)
 };
 
 __device__ __forceinline__ void tmem_alloc_dyn(uint32_t cols, uint32_t* dst) {
@@ -93,10 +95,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // cluster of p.cluster CTAs over consecutive weight tiles (same group, token
+  // tile and K slice): each loads 1/cluster of the token-row boxes of a stage
+  // and multicasts them to all, and a stage is reused only once every CTA's
+  // MMA released it (the commit arrives on every CTA's empty barrier)
+  const int cs = p.cluster;
+  const uint32_t crank = cs > 1 ? cluster_ctarank() : 0u;
+  const uint16_t cmask = uint16_t((1u << cs) - 1u);
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], uint32_t(cs));
     }
     mbar_init(&tmem_full_bar, 1);
     fence_barrier_init();
@@ -107,6 +116,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_alloc_dyn(tmem_cols, &tmem_base_sh);
   tc_fence_before();
   __syncthreads();
+  if (cs > 1) cluster_sync_all();  // every CTA's barriers are initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
 
@@ -122,8 +132,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_3d(sa, &tm_w, &full_bar[s], kc, nb * 128, wblk);
         if (swiglu) tma_load_3d(sa + kTileBytesA, &tm_u, &full_bar[s], kc, nb * 128, wblk);
         uint8_t* sb = sa + a_bytes;
-        for (int i = 0; i < n_load / 32; ++i)
-          tma_load_2d(sb + i * 4096, &tm_x, &full_bar[s], kc, row0 + i * 32);
+        if (cs > 1) {
+          for (int i = int(crank); i < n_load / 32; i += cs)
+            tma_load_2d_mc(sb + i * 4096, &tm_x, &full_bar[s], kc, row0 + i * 32, cmask);
+        } else {
+          for (int i = 0; i < n_load / 32; ++i) tma_load_2d(sb + i * 4096, &tm_x, &full_bar[s], kc, row0 + i * 32);
+        }
       }
     }
   } else if (warp == 1) {
@@ -153,7 +167,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (nc1 > 0) umma_bf16(tmem + 256, ad + ko, bd1 + ko, id1, acc);
           if (swiglu) umma_bf16(tmem + 256, au + ko, bd0 + ko, id0, acc);
         }
-        umma_commit(&empty_bar[s]);
+        if (cs > 1) umma_commit_mc(&empty_bar[s], cmask);
+        else umma_commit(&empty_bar[s]);
       }
       umma_commit(&tmem_full_bar);
     }
@@ -242,6 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc_dyn(tmem_cols, tmem);
+  if (cs > 1) cluster_sync_all();  // peers' last commits may still arrive on our barriers
 }
 
 // Fixed-order split-K reduction fused with the epilogue: out = epi(sum_s P_s).
@@ -288,7 +304,7 @@ int device_sm_count() {
 }
 
 struct GemmPlan {
-  int tile, token_tiles, stages, split;
+  int tile, token_tiles, stages, split, cluster;
   uint32_t cols;
 };
 
@@ -306,12 +322,29 @@ GemmPlan plan_gemm(const smo_gemm_args& a) {
   while (int(pl.cols) < need) pl.cols <<= 1;
   // split K so that a dense GEMM with few weight tiles still covers the SMs;
   // only for plain fp32/bf16/residual epilogues (argmax/SwiGLU need full sums)
+  pl.cluster = 1;
   pl.split = 1;
   const bool splittable = a.epilogue == SMO_EPI_BF16 || a.epilogue == SMO_EPI_F32 || a.epilogue == SMO_EPI_F32_ADD;
   const int tiles = (a.N / 128) * a.groups * pl.token_tiles;
   if (splittable && a.groups == 1 && a.split_k != 1 && (a.N % 512) == 0) {
     const int want = a.split_k > 1 ? a.split_k : device_sm_count() / std::max(1, tiles);
     pl.split = std::max(1, std::min({want, a.K / kBK / 8, 8}));
+  }
+  // dense GEMMs: CTAs of consecutive weight tiles share the token rows by
+  // TMA multicast (the rows are re-read by every weight tile otherwise: for
+  // 288 tokens they are 2.25x the weight bytes per stage). SMO_GEMM_CLUSTER=1
+  // disables (A/B).
+  static const int env_cluster = [] {
+    const char* f = std::getenv("SMO_GEMM_CLUSTER");
+    return f ? std::atoi(f) : 0;
+  }();
+  if (a.groups == 1 && !a.row_offsets && env_cluster != 1) {
+    const int nt = a.N / 128;
+    for (int c : {4, 2})
+      if ((env_cluster == 0 || env_cluster == c) && nt % c == 0 && (pl.tile / 32) >= c) {
+        pl.cluster = c;
+        break;
+      }
   }
   return pl;
 }
@@ -383,8 +416,25 @@ void gemm_launch(const smo_gemm_args& a, cudaStream_t stream) {
                                         kSmemBudget + 4096));
     attr_set = true;
   }
+  p.cluster = pl.cluster;
   dim3 grid(a.N / 128, a.groups, token_tiles * pl.split);
-  gemm_tc_kernel<<<grid, kThreads, smem, stream>>>(tw, tu, tx, p, cols);
+  if (pl.cluster > 1) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(pl.cluster);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SMO_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_tc_kernel, tw, tu, tx, p, cols));
+  } else {
+    gemm_tc_kernel<<<grid, kThreads, smem, stream>>>(tw, tu, tx, p, cols);
+  }
   count_launch();
   SMO_CUDA_CHECK(cudaGetLastError());
   if (pl.split > 1) {

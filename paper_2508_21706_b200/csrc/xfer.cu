@@ -423,9 +423,24 @@ __global__ void __launch_bounds__(32 * kUDecWarps, 28) unary_decode_kernel(const
     const uint8_t* sb = src + tw.x;
     const int base = int(tw.y & 0xffu), nw = int(tw.y >> 16);
     const bool has_esc = (tw.y >> 8) & 1u;
-    const uint32_t* codes = reinterpret_cast<const uint32_t*>(sb + kSeg);
-    // coalesced staging of the stream (words past the end read as ones)
-    for (int w = lane; w < nw + 6; w += 32) wb[w] = w < nw ? codes[w] : 0xffffffffu;
+    // coalesced 16-B staging of the stream (it starts 16-B aligned and the
+    // segment is padded to 16 B, so whole chunks stay inside it); words past
+    // the end read as ones, 6 of them at least
+    {
+      const uint4* c4 = reinterpret_cast<const uint4*>(sb + kSeg);
+      const int nc = (nw + 3) >> 2;
+      for (int c = lane; c < nc + 2; c += 32) {
+        uint4 v = c < nc ? c4[c] : make_uint4(~0u, ~0u, ~0u, ~0u);
+        const int w0 = 4 * c;
+        if (w0 + 3 >= nw) {
+          v.x = w0 < nw ? v.x : ~0u;
+          v.y = w0 + 1 < nw ? v.y : ~0u;
+          v.z = w0 + 2 < nw ? v.z : ~0u;
+          v.w = ~0u;
+        }
+        reinterpret_cast<uint4*>(wb)[c] = v;
+      }
+    }
     __syncwarp();
     int p0 = 0;
     if (nw <= 32 * kURun) {
