@@ -330,18 +330,20 @@ GemmPlan plan_gemm(const smo_gemm_args& a) {
     const int want = a.split_k > 1 ? a.split_k : device_sm_count() / std::max(1, tiles);
     pl.split = std::max(1, std::min({want, a.K / kBK / 8, 8}));
   }
-  // dense GEMMs: CTAs of consecutive weight tiles share the token rows by
-  // TMA multicast (the rows are re-read by every weight tile otherwise: for
-  // 288 tokens they are 2.25x the weight bytes per stage). SMO_GEMM_CLUSTER=1
-  // disables (A/B).
+  // Dense GEMMs can run as clusters of 2 or 4 weight tiles that share the
+  // token rows by TMA multicast (SMO_GEMM_CLUSTER=2|4; the rows are otherwise
+  // re-read from L2 by every weight tile: 2.25x the weight bytes per stage at
+  // 288 tokens). Measured and left off: QKV 42 -> 65 us, O-proj 38 -> 40 us,
+  // LM head unchanged (tools/kbench.py gemm) — the lockstep of the cluster's
+  // stage release costs more than the L2 reads it saves.
   static const int env_cluster = [] {
     const char* f = std::getenv("SMO_GEMM_CLUSTER");
-    return f ? std::atoi(f) : 0;
+    return f ? std::atoi(f) : 1;
   }();
-  if (a.groups == 1 && !a.row_offsets && env_cluster != 1) {
+  if (a.groups == 1 && !a.row_offsets && env_cluster > 1) {
     const int nt = a.N / 128;
     for (int c : {4, 2})
-      if ((env_cluster == 0 || env_cluster == c) && nt % c == 0 && (pl.tile / 32) >= c) {
+      if (env_cluster == c && nt % c == 0 && (pl.tile / 32) >= c) {
         pl.cluster = c;
         break;
       }
