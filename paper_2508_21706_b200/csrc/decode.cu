@@ -305,6 +305,10 @@ void Engine::decode_run(int k, int steps, bool graph, cudaStream_t st) {
   SMO_REQUIRE(!batch_one && !attn_cpu && !ep_on && !debug && (draft_g < 0 || draft_g >= b),
               "decode graph: not with BATCH_ONE, CPU attention, expert parallelism, debug snapshots or a draft split");
   SMO_REQUIRE(st != nullptr, "decode graph: needs a non-default stream");
+  if (next_pf) {  // a cross-step prefetch from an eager step: let it land (the graph streams its own)
+    SMO_CUDA_CHECK(cudaStreamSynchronize(copy));
+    next_pf = false;
+  }
   const int64_t end = kv_bound + int64_t(steps) * n;  // kv bound after the last iteration
   SMO_REQUIRE(end <= s_max, "decode: KV capacity (max_seq) exhausted");
   for (int r = 0; r < b; ++r) {  // pages for every iteration of the run, outside the graph
