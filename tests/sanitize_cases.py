@@ -7,7 +7,7 @@ workspace counters), K4-MoE (cross-CTA release/acquire on per-expert
 counters, cooperative launch), the K5 unary codec, router/permute/combine,
 greedy accept, and the expert-parallel loopback exchange.
 
-    python tests/sanitize_cases.py verify|kernels|attn|moe|ep
+    python tests/sanitize_cases.py verify|kernels|attn|moe|ep|coded|draft
 """
 import dataclasses
 import math
@@ -76,6 +76,49 @@ def case_moe():
     torch.cuda.synchronize()
 
 
+def case_coded():
+    """T2 tile code: GPU encoder + decoder round trip, and K4-MoE decoding it in
+    shared memory (bulk copies into a code ring, 16 decoder warps,
+    fence.proxy.async + mbarriers, paired down stages) on ragged groups."""
+    from paper_2508_21706_b200 import ops
+    dev = torch.device("cuda:0")
+    g = torch.Generator(device=dev).manual_seed(5)
+    T, E, k, h, hi = 150, 4, 2, 256, 384
+    blk = 3 * h * hi
+    blks = []
+    for e in range(E):
+        b = torch.empty(blk, dtype=torch.bfloat16, device=dev)
+        ops.fill_uniform_(b, 0x5EED, 500 + e, math.sqrt(3.0 / h))
+        blks.append(b)
+    codes = [ops.tcode_encode(b, h, hi) for b in blks]
+    assert torch.equal(ops.tcode_decode(codes[0], h, hi).view(torch.int16), blks[0].view(torch.int16))
+    w_code = torch.tensor([c.data_ptr() for c in codes], dtype=torch.int64, device=dev)
+    x = (torch.rand((T, h), generator=g, device=dev) * 2 - 1).to(torch.bfloat16)
+    ids = torch.topk(torch.randn((T, E), generator=g, device=dev), k, dim=1).indices.to(torch.int32).contiguous()
+    off, perm, pos, xp = ops.permute(ids, E, x)
+    h1, y1 = ops.moe_experts_coded(xp, off, w_code, h=h, h_i=hi, n_expert=E)
+    h0, y0 = ops.moe_experts(xp, off, torch.cat(blks), h=h, h_i=hi, n_expert=E, w_block_stride=blk * 2,
+                             w_pool_blocks=E, splits=y1.shape[0])
+    assert torch.equal(y0.view(torch.int32), y1.view(torch.int32))
+    torch.cuda.synchronize()
+
+
+def case_draft():
+    """Drafter CPU part: host-resident drafter K/V, host-pool attention released
+    and awaited through device-polled flags in mapped memory."""
+    from paper_2508_21706_b200.engine import TINY, VerifyEngine
+    s = dataclasses.replace(TINY, seed=0x5EED + 5, draft_layers=1, draft_inter=512)
+    rng = np.random.default_rng(2)
+    prompts = [list(rng.integers(0, s.vocab, size=L)) for L in (40, 17, 9)]
+    eng = VerifyEngine(s, max_batch=3, max_verify=4, max_seq=128, draft_cpu_kv=True)
+    eng.prefill(prompts)
+    eng.set_draft_split(1)
+    for _ in range(2):
+        eng.decode_step(3)
+    eng.decode_read(3, 32)
+    eng.close()
+
+
 def case_ep():
     from paper_2508_21706_b200.engine import TINY, EpGroup, VerifyEngine
     s = dataclasses.replace(TINY, seed=0x5EED + 3)
@@ -110,5 +153,5 @@ def case_ep():
 
 if __name__ == "__main__":
     {"verify": case_verify, "kernels": case_kernels, "attn": case_attn, "moe": case_moe,
-     "ep": case_ep}[sys.argv[1]]()
+     "ep": case_ep, "coded": case_coded, "draft": case_draft}[sys.argv[1]]()
     print("case ok")
