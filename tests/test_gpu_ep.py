@@ -248,3 +248,59 @@ def test_ep_dispatch_combine_standalone(cuda):
             n_want = sum(int((ids[s] == e).sum()) for s in range(P))
             assert got_rows[le].shape[0] == n_want, (r, le)
     grp.close()
+
+
+def test_ep_loopback_decode_loop_matches_single_gpu(cuda):
+    """The decode loop under expert parallelism: each rank drafts (on-device
+    drafter) and commits its own requests; the verify step dispatches their
+    rows to the expert owners. Committed histories equal single-GPU engines
+    run on each rank's requests, bit for bit."""
+    import torch
+    from paper_2508_21706_b200.engine import TINY, EpGroup, VerifyEngine
+    shape = dataclasses.replace(TINY, seed=0x5EED + 6, lm_scale=8.0, router_scale=4.0, draft_layers=1,
+                                draft_inter=512)
+    P, k, steps = 2, 3, 3
+    s_max = PREFIX + (k + 1) * steps + 64
+    rng = np.random.default_rng(21)
+    kv = np.array([PREFIX, PREFIX - 3, 200, 9], np.int32)
+    root = rng.integers(0, shape.vocab, size=B).astype(np.int32)
+    grp = EpGroup.loopback(P)
+    bl = B // P
+    engines = [VerifyEngine(shape, max_batch=bl, max_verify=k + 1, max_seq=s_max, ep_rank=r, ep_size=P,
+                            ep_group=grp) for r in range(P)]
+    for r, e in enumerate(engines):
+        e.fill_prefix(kv[r * bl:(r + 1) * bl])
+        e.decode_begin(root[r * bl:(r + 1) * bl], kv[r * bl:(r + 1) * bl])
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    errors = []
+
+    def work(r):
+        try:
+            for _ in range(steps):
+                engines[r].decode_step(k, stream=streams[r].cuda_stream)
+            streams[r].synchronize()
+        except Exception as ex:
+            errors.append(ex)
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errors, errors
+    for r in range(P):
+        mine = slice(r * bl, (r + 1) * bl)
+        got = engines[r].decode_read(bl, 64)
+        ref = VerifyEngine(shape, max_batch=bl, max_verify=k + 1, max_seq=s_max)
+        ref.fill_prefix(kv[mine])
+        ref.decode_begin(root[mine], kv[mine])
+        for _ in range(steps):
+            ref.decode_step(k)
+        want = ref.decode_read(bl, 64)
+        ref.close()
+        for a, b in zip(got, want):
+            assert np.array_equal(a, b), r
+        assert np.all(got[1] >= steps)
+    for e in engines:
+        e.close()
+    grp.close()
