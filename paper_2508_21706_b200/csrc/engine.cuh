@@ -310,6 +310,7 @@ struct Engine {
   std::map<std::string, std::vector<DevBuf>> dbg;
 
   ~Engine() {
+    cudaDeviceSynchronize();  // in-flight copies (e.g. a cross-step prefetch) read the host buffers freed below
     async_host.shutdown();  // before the pool and the host buffers it uses go away
     for (auto e : slot_ready) cudaEventDestroy(e);
     for (auto e : slot_free) cudaEventDestroy(e);
