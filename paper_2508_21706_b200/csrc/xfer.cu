@@ -429,16 +429,19 @@ __global__ void __launch_bounds__(32 * kUDecWarps, 28) unary_decode_kernel(const
     {
       const uint4* c4 = reinterpret_cast<const uint4*>(sb + kSeg);
       const int nc = (nw + 3) >> 2;
-      for (int c = lane; c < nc + 2; c += 32) {
+      auto chunk = [&](int c) {
         uint4 v = c < nc ? c4[c] : make_uint4(~0u, ~0u, ~0u, ~0u);
         const int w0 = 4 * c;
-        if (w0 + 3 >= nw) {
-          v.x = w0 < nw ? v.x : ~0u;
-          v.y = w0 + 1 < nw ? v.y : ~0u;
-          v.z = w0 + 2 < nw ? v.z : ~0u;
-          v.w = ~0u;
-        }
+        v.x = w0 < nw ? v.x : ~0u;
+        v.y = w0 + 1 < nw ? v.y : ~0u;
+        v.z = w0 + 2 < nw ? v.z : ~0u;
+        v.w = w0 + 3 < nw ? v.w : ~0u;
         reinterpret_cast<uint4*>(wb)[c] = v;
+      };
+      if (nc + 2 <= 32) {  // common case (<= 120 words): one chunk per lane
+        if (lane < nc + 2) chunk(lane);
+      } else {
+        for (int c = lane; c < nc + 2; c += 32) chunk(c);
       }
     }
     __syncwarp();
@@ -518,23 +521,32 @@ __global__ void __launch_bounds__(32 * kUDecWarps, 28) unary_decode_kernel(const
       const uint32_t* wp = wb + (p0 >> 5);
       uint32_t hi = wp[0], lo = wp[1];
       wp += 2;
-      int off = p0 & 31;
+      uint32_t off = uint32_t(p0 & 31);
+      uint32_t fs[32];
 #pragma unroll
       for (int i = 0; i < 32; i += 2) {
+        // f = bfind(~window) (position of the window's highest zero), and the
+        // code is 32 - f bits long: one SHF, one FLO, one IADD3 per code
         const uint64_t win = (uint64_t(hi) << 32) | lo;
-        const int f1 = 31 - __clz(~uint32_t((win << off) >> 32));
-        const int off2 = off + 32 - f1;  // < 48
-        const int f2 = 31 - __clz(~uint32_t((win << off2) >> 32));
-        off = off2 + 32 - f2;            // < 64
+        uint32_t f1, f2;
+        asm("bfind.u32 %0, %1;" : "=r"(f1) : "r"(~uint32_t((win << off) >> 32)));
+        const uint32_t off2 = off + 32u - f1;  // < 48
+        asm("bfind.u32 %0, %1;" : "=r"(f2) : "r"(~uint32_t((win << off2) >> 32)));
+        off = off2 + 32u - f2;                 // < 64
+        // refill: shift a word in once 32 bits were consumed (off >> 5 is 0 or 1)
         const uint32_t nxt = *wp;
-        const bool ge = off >= 32;
+        const bool ge = off >= 32u;
         hi = ge ? lo : hi;
         lo = ge ? nxt : lo;
-        wp += ge ? 1 : 0;
-        off -= ge ? 32 : 0;
-        const uint32_t pair = uint32_t(f1) | (uint32_t(f2) << 8);
-        j4[i / 4] = (i % 4 == 0) ? pair : j4[i / 4] | (pair << 16);
+        wp += off >> 5;
+        off &= 31u;
+        fs[i] = f1;
+        fs[i + 1] = f2;
       }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)  // four f (16..31) per word, bytewise
+        j4[q] = __byte_perm(__byte_perm(fs[4 * q], fs[4 * q + 1], 0x0040u), __byte_perm(fs[4 * q + 2], fs[4 * q + 3], 0x0040u),
+                            0x5410u);
     }
     // e = base - j = f - (31 - base)
     uint32_t e4[8];
@@ -688,7 +700,13 @@ void expert_decode_blocks(const void* const* srcs, void* const* dsts, int n, siz
     // one warp per segment (the kernel's grid-stride loop then runs once):
     // measured faster than a one-wave persistent grid (238 vs 212 us per
     // Mixtral block) — warps finish unevenly and fresh blocks refill the SMs
-    const size_t want = (segs + kUDecWarps - 1) / kUDecWarps;
+    // segments per warp (SMO_UNARY_SPW, A/B): the per-warp prologue is
+    // amortised over that many segments of the grid-stride loop
+    static const size_t spw = [] {
+      const char* f = std::getenv("SMO_UNARY_SPW");
+      return size_t(std::max(1, f ? std::atoi(f) : 1));
+    }();
+    const size_t want = (segs + kUDecWarps * spw - 1) / (kUDecWarps * spw);
     const size_t cap = want;
     const dim3 ug(unsigned(std::min(want, cap)), unsigned(n));
     static const bool direct = [] {  // A/B switch: SMO_UNARY_DIRECT=1 stores from registers
