@@ -24,6 +24,7 @@
 //    Q/O; FLOPs = 4*n*(s+n)*n_q*d per request.
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -91,8 +92,9 @@ __device__ __forceinline__ void trace_ev(int role, int code) {
 // Flat ("stream-K") schedule: the (pair, chunk) slots of all requests and KV
 // heads are laid end to end and CTA i processes slots [i*Q, (i+1)*Q). The
 // run of slots a CTA holds for one pair is a piece; a piece covering a whole
-// pair writes the output, otherwise it leaves a partial (O, m, l) and the
-// pair's last finishing piece merges them (in-kernel split-KV combine).
+// pair writes the output, otherwise it leaves a partial (O, m, l) and, once
+// all of the pair's pieces are published, each of them merges one slice of
+// the output (in-kernel split-KV combine, after the CTA's last item).
 struct Piece {
   int pair, r, h, c0, c1, keys;  // chunks [c0, c1) of pair (r, h); keys = prefix + n
   int first_cta, npieces;        // CTAs holding the pair's non-empty pieces
@@ -200,10 +202,15 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
   // PV). Softmax warps skip o_full phases (lazy rescale), so the epilogue
   // waits on o_last, which every warp observes once per item.
   __shared__ __align__(8) uint64_t s_full[kSP], s_empty[kSP], o_full, o_last, p_full;
+  __shared__ __align__(8) uint64_t mrg_full;  // split-KV merge: bulk copies of partials landed
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   TR_INIT();
+  // the producer's first piece needs its request's prefix length: issue the
+  // load before the setup below so its latency hides under it
+  const int pre0 = warp == 0 && int(blockIdx.x) * p.Q < p.total
+                       ? __ldg(p.prefix + piece_request(p, int(blockIdx.x) * p.Q)) : 0;
   if (warp == 0 && lane == 0) {
     TR(0, 9);  // kernel entry (trace builds)
     for (int i = 0; i < 2; ++i) {
@@ -221,6 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
     mbar_init(&o_full, 1);
     mbar_init(&o_last, 1);
     mbar_init(&p_full, kSoftWarps);
+    mbar_init(&mrg_full, 1);
     fence_barrier_init();
     tma_prefetch_desc(&tm_q);
     tma_prefetch_desc(&tm_kv_k);
@@ -246,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
     if (elect_one()) {
       int used = 0, gc = 0;
       for (int f = f_begin; f < f_end;) {
-        const Piece pc = piece_at(p, f, f_end);
+        const Piece pc = f == f_begin ? piece_make(p, f, f_end, pre0) : piece_at(p, f, f_end);
         f = pc.next_f;
         if (pc.c1 <= pc.c0) continue;
         const int qb = used % L::kQBufs;
@@ -394,8 +402,10 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
     const int col0 = rep * kW + half * kCols;   // this thread's key columns in a chunk
     const int oc0 = half * kOCols;              // this thread's O columns
     const uint32_t pair_bar = 1 + q4;           // named barrier of the two warps of a quadrant
-    __shared__ int last_sh;
     int gc = 0, items_done = 0;
+    Piece sp0{}, sp1{};  // this CTA's split pieces (at most its first and last)
+    int n_split = 0;
+    const uint32_t mrg_phase = 0;  // mrg_full completes once per launch (the merge pass)
     // per-row output offsets (query i, head hh of the KV group) in rows of D
     __shared__ int row_off_sh[128];
     for (int rr = stid; rr < p.rows; rr += 32 * kSoftWarps) row_off_sh[rr] = (rr / p.g) * p.n_q + rr % p.g;
@@ -614,113 +624,143 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
       }
       if (warp == 4 && lane == 0) TR(2, 9);
       if (!whole) {
-        // publish the partial; the pair's last piece merges all of them
-        __threadfence();
+        // publish the partial (bar.sync orders the CTA's partial stores
+        // before thread 0's release add; release is cumulative); the pair is
+        // merged after this CTA's last item, a slice by each of its pieces
         asm volatile("bar.sync 5, 256;" ::: "memory");
         if (warp == 4 && lane == 0) TR(2, 30);
-        if (stid == 0) last_sh = atomicAdd(p.ws_cnt + cur.pair, 1) == cur.npieces - 1;
-        asm volatile("bar.sync 5, 256;" ::: "memory");
-        if (warp == 4 && lane == 0) TR(2, 31);
-        if (last_sh) {
-          __threadfence();
-          // merge weights w[j][row] = 2^(m_j - M) / L into the stage, slot
-          // indices of the pair's pieces first (npieces <= 16)
-          float* w = slots;
-          int* slot_of = reinterpret_cast<int*>(slots + 16 * 128);
-          if (stid < cur.npieces) slot_of[stid] = partial_slot(p, cur.first_cta + stid, cur.pair);
-          asm volatile("bar.sync 5, 256;" ::: "memory");
-          const int np = cur.npieces;
-          // the np (<= 16) partial (m, l) of a row, 4 loads in flight at a time
-          // (one L2 round trip per 4 pieces instead of one per piece); l is
-          // parked in shared memory until the row maximum is known
-          float* wl = slots + 16 * 128 + 64;
-          for (int rr = stid; rr < p.rows; rr += 32 * kSoftWarps) {
-            float Mx = -INFINITY, Lx = 0.f;
-            for (int j0 = 0; j0 < np; j0 += 4) {
-              float2 v[4];
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                if (j0 + j < np) v[j] = __ldcg(&p.ws_ml[size_t(slot_of[j0 + j]) * p.rows + rr]);
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                if (j0 + j < np) {
-                  Mx = fmaxf(Mx, v[j].x);
-                  w[(j0 + j) * 128 + rr] = v[j].x;
-                  wl[(j0 + j) * 128 + rr] = v[j].y;
-                }
-            }
-            for (int j = 0; j < np; ++j) {
-              const float m = w[j * 128 + rr];
-              const float e2 = m == -INFINITY ? 0.f : ex2_approx(m - Mx);
-              w[j * 128 + rr] = e2;
-              Lx += wl[j * 128 + rr] * e2;
-            }
-            const float inv = Lx > 0.f ? 1.f / Lx : 0.f;
-            for (int j = 0; j < np; ++j) w[j * 128 + rr] *= inv;
-          }
-          if (warp == 4 && lane == 0) TR(2, 32);
-          asm volatile("bar.sync 5, 256;" ::: "memory");
-          // every thread keeps kJ pieces x kE elements of partial loads in
-          // flight (the L2 round trip, not bandwidth, bounds this loop)
-          constexpr int kE = 1, kJ = 8;
-          const int n_e = p.rows * (D / 4);
-          for (int e0 = stid; e0 < n_e; e0 += 32 * kSoftWarps * kE) {
-            float4 acc[kE];
-#pragma unroll
-            for (int u = 0; u < kE; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int j0 = 0; j0 < np; j0 += kJ) {
-              float4 v[kJ][kE];
-#pragma unroll
-              for (int jj = 0; jj < kJ; ++jj) {
-                const float4* src = reinterpret_cast<const float4*>(
-                    p.ws_o + size_t(slot_of[j0 + jj < np ? j0 + jj : 0]) * p.rows * D);
-#pragma unroll
-                for (int u = 0; u < kE; ++u) {
-                  const int e = e0 + u * 32 * kSoftWarps;
-                  if (j0 + jj < np && e < n_e) v[jj][u] = __ldcg(src + e);
-                }
-              }
-#pragma unroll
-              for (int jj = 0; jj < kJ; ++jj)
-#pragma unroll
-                for (int u = 0; u < kE; ++u) {
-                  const int e = e0 + u * 32 * kSoftWarps;
-                  if (j0 + jj < np && e < n_e) {
-                    const float wj = w[(j0 + jj) * 128 + e / (D / 4)];
-                    acc[u].x += v[jj][u].x * wj;
-                    acc[u].y += v[jj][u].y * wj;
-                    acc[u].z += v[jj][u].z * wj;
-                    acc[u].w += v[jj][u].w * wj;
-                  }
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kE; ++u) {
-              const int e = e0 + u * 32 * kSoftWarps;
-              if (e < n_e) {
-                const int rr = e / (D / 4), c4 = e % (D / 4);
-                uint16_t* dst = p.out + (size_t(cur.r) * p.n * p.n_q + size_t(cur.h) * p.g + row_off_sh[rr]) * D;
-                *reinterpret_cast<uint2*>(dst + 4 * c4) =
-                    make_uint2(pack_bf16x2(acc[u].x, acc[u].y), pack_bf16x2(acc[u].z, acc[u].w));
-              }
-            }
-          }
-          if (warp == 4 && lane == 0) TR(2, 33);
-          if (stid == 0) p.ws_cnt[cur.pair] = 0;  // ready for the next launch
-        }
+        if (stid == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p.ws_cnt + cur.pair) : "memory");
+        if (n_split == 0)
+          sp0 = cur;
+        else
+          sp1 = cur;
+        ++n_split;
       }
       // all stage reads done -> restore the V tile to zeros and hand the
       // stage back to the producer. The epilogue scratch above left fp32 bit
       // patterns in it; a later partial last chunk only loads V rows up to its
       // end and keeps the rest, whose P is zero — but 0 * (a bf16 NaN/Inf
       // pattern) is not zero in the PV MMA.
+      // (after the CTA's last item no chunk loads follow: no zero-fill)
       asm volatile("bar.sync 5, 256;" ::: "memory");
-      for (int i = stid; i < L::kKvBytes / 16; i += 32 * kSoftWarps)
-        reinterpret_cast<uint4*>(stage + L::kKvBytes)[i] = make_uint4(0, 0, 0, 0);
-      fence_proxy_async();
-      asm volatile("bar.sync 5, 256;" ::: "memory");
+      if (have) {
+        for (int i = stid; i < L::kKvBytes / 16; i += 32 * kSoftWarps)
+          reinterpret_cast<uint4*>(stage + L::kKvBytes)[i] = make_uint4(0, 0, 0, 0);
+        fence_proxy_async();
+        asm volatile("bar.sync 5, 256;" ::: "memory");
+      }
       if (stid == 0) mbar_arrive(&kv_empty[s_last]);
       if (warp == 4 && lane == 0) TR(2, 10);
+    }
+    // ---- split-KV merge (deferred). A CTA's first and last pieces may be
+    // parts of a pair (its middle pieces are whole pairs). Every piece of a
+    // split pair merges one slice of the pair's output, out = sum_j w_j O_j
+    // with w_j[row] = 2^(m_j - M) / L, once all np pieces are published:
+    // the merge reads np x slice instead of one CTA reading np x the whole
+    // pair, in parallel on np SMs (the grid is cooperative, so the pieces are
+    // co-resident and the wait resolves). The slice's partial runs are
+    // contiguous, so one thread stages them with np bulk copies into the
+    // now idle K/V stages; the sums run in piece order (deterministic).
+    // Both split pieces are merged in one pass (one set of barriers and
+    // round trips): region k of the stages holds pair k's weights, (m, l)
+    // rows and staged partials.
+    if (n_split > 0) {
+      constexpr int kRegion = 16 * 128 + 64 + 16 * 128 * 2 + 16 * 128 * 4 + 64;  // floats: w, slots, (m, l), partials (+1 float4 slack)
+      static_assert(2 * kRegion * 4 <= L::kStages * 2 * L::kKvBytes, "merge regions exceed the K/V stages");
+      // per-pair slice geometry in shared memory (indexed by pair k below)
+      __shared__ int np[2], e_lo[2], ne[2], r_lo[2], nr[2];
+      if (stid < 2) {
+        const int k = stid;
+        const Piece& sp = k == 0 ? sp0 : sp1;
+        const int jme = int(blockIdx.x) - sp.first_cta, n_e = p.rows * (D / 4);
+        const int npk = k < n_split ? sp.npieces : 0;
+        const int lo = k < n_split ? jme * n_e / npk : 0;
+        const int nek = k < n_split ? (jme + 1) * n_e / npk - lo : 0;  // float4, >= 2
+        np[k] = npk;
+        e_lo[k] = lo;
+        ne[k] = nek;
+        r_lo[k] = lo / (D / 4);
+        nr[k] = k < n_split ? (lo + nek - 1) / (D / 4) + 1 - lo / (D / 4) : 0;
+      }
+      asm volatile("bar.sync 5, 256;" ::: "memory");
+      float* const mbase = reinterpret_cast<float*>(smem + L::kKvOff);
+      auto w = [&](int k) { return mbase + k * kRegion; };
+      auto slot_of = [&](int k) { return reinterpret_cast<int*>(mbase + k * kRegion + 16 * 128); };
+      auto mls = [&](int k) { return reinterpret_cast<float2*>(mbase + k * kRegion + 16 * 128 + 64); };
+      auto stg = [&](int k) { return reinterpret_cast<float4*>(mbase + k * kRegion + 16 * 128 + 64 + 16 * 128 * 2); };
+      if (warp == 4 && lane == 0) TR(2, 31);
+      if (stid == 0) {
+        for (int k = 0; k < n_split; ++k) {
+          const int* cnt = p.ws_cnt + (k == 0 ? sp0.pair : sp1.pair);
+          int v;
+          for (;;) {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+            if (v >= np[k]) break;
+            __nanosleep(32);
+          }
+        }
+      }
+      if (stid < 32 && stid < np[0]) slot_of(0)[stid] = partial_slot(p, sp0.first_cta + stid, sp0.pair);
+      if (stid >= 32 && stid - 32 < np[1]) slot_of(1)[stid - 32] = partial_slot(p, sp1.first_cta + stid - 32, sp1.pair);
+      fence_proxy_async();  // generic accesses of the stages before the bulk copies
+      asm volatile("bar.sync 5, 256;" ::: "memory");
+      if (stid == 0) {
+        mbar_arrive_expect_tx(&mrg_full, uint32_t((np[0] * ne[0] + np[1] * ne[1]) * 16));
+        for (int k = 0; k < n_split; ++k)
+          for (int j = 0; j < np[k]; ++j)
+            bulk_load(stg(k) + j * ne[k],
+                      reinterpret_cast<const float4*>(p.ws_o + size_t(slot_of(k)[j]) * p.rows * D) + e_lo[k],
+                      uint32_t(ne[k] * 16), &mrg_full);
+      }
+      // (m, l) of the slices' rows, both pairs in one round trip
+      for (int t = stid; t < np[0] * nr[0] + np[1] * nr[1]; t += 32 * kSoftWarps) {
+        const int k = t >= np[0] * nr[0], tt = t - (k ? np[0] * nr[0] : 0);
+        const int j = tt / nr[k], rl = tt - j * nr[k];
+        mls(k)[j * 128 + rl] = __ldcg(&p.ws_ml[size_t(slot_of(k)[j]) * p.rows + r_lo[k] + rl]);
+      }
+      asm volatile("bar.sync 5, 256;" ::: "memory");
+      for (int t = stid; t < nr[0] + nr[1]; t += 32 * kSoftWarps) {
+        const int k = t >= nr[0], rl = t - (k ? nr[0] : 0);
+        float Mx = -INFINITY, Lx = 0.f;
+        for (int j = 0; j < np[k]; ++j) Mx = fmaxf(Mx, mls(k)[j * 128 + rl].x);
+        for (int j = 0; j < np[k]; ++j) {
+          const float2 ml = mls(k)[j * 128 + rl];
+          const float e2 = ml.x == -INFINITY ? 0.f : ex2_approx(ml.x - Mx);
+          w(k)[j * 128 + rl] = e2;
+          Lx += ml.y * e2;
+        }
+        const float inv = Lx > 0.f ? 1.f / Lx : 0.f;
+        for (int j = 0; j < np[k]; ++j) w(k)[j * 128 + rl] *= inv;
+      }
+      asm volatile("bar.sync 5, 256;" ::: "memory");
+      if (warp == 4 && lane == 0) TR(2, 32);
+      mbar_wait(&mrg_full, mrg_phase);
+      for (int t = stid; t < ne[0] + ne[1]; t += 32 * kSoftWarps) {
+        const int k = t >= ne[0], e = t - (k ? ne[0] : 0);
+        const Piece& sp = k ? sp1 : sp0;
+        const int E = e_lo[k] + e, rr = E / (D / 4), c4 = E % (D / 4);
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int j = 0; j < np[k]; ++j) {
+          const float4 v = stg(k)[j * ne[k] + e];
+          const float wj = w(k)[j * 128 + rr - r_lo[k]];
+          acc.x += v.x * wj;
+          acc.y += v.y * wj;
+          acc.z += v.z * wj;
+          acc.w += v.w * wj;
+        }
+        uint16_t* obase = p.out + (size_t(sp.r) * p.n * p.n_q + size_t(sp.h) * p.g) * D;
+        *reinterpret_cast<uint2*>(obase + size_t(row_off_sh[rr]) * D + 4 * c4) =
+            make_uint2(pack_bf16x2(acc.x, acc.y), pack_bf16x2(acc.z, acc.w));
+      }
+      if (warp == 4 && lane == 0) TR(2, 33);
+      if (stid == 0) {  // a pair's last merge re-arms its counter for the next launch
+        for (int k = 0; k < n_split; ++k) {
+          int* cnt = p.ws_cnt + (k == 0 ? sp0.pair : sp1.pair);
+          int old;
+          asm volatile("atom.relaxed.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
+          if (old == 2 * np[k] - 1) *cnt = 0;
+        }
+      }
     }
   }
   tc_fence_before();
@@ -738,7 +778,7 @@ constexpr size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // Flat schedule: C chunk slots per (request, KV head), Q consecutive slots per
 // CTA so that the grid fills the SMs once; Q >= C/15 keeps a pair's pieces
-// (the in-kernel merge reads all of them from one CTA) within 16. Workspace: two partial slots per CTA
+// within 16 (the merge's weight table). Workspace: two partial slots per CTA
 // (sized for a full grid, so it does not depend on the prefix lengths) and
 // one counter per pair.
 AttnPlan plan_attention(const smo_attn_args& a, int sms) {
@@ -802,7 +842,19 @@ void launch_k1(int grid, cudaStream_t stream, const CUtensorMap& tq, const CUten
                                         int(smem)));
     set = true;
   }
-  verify_attention_kernel<D, R><<<grid, kThreads, smem, stream>>>(tq, tk, tv, tv8, p);
+  // cooperative: the pieces of a split pair wait for each other before the
+  // merge (grid <= SMs at one CTA per SM)
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SMO_CUDA_CHECK(cudaLaunchKernelEx(&cfg, verify_attention_kernel<D, R>, tq, tk, tv, tv8, p));
 }
 
 void check_attn_args(const smo_attn_args& a) {

@@ -72,6 +72,8 @@ def attn(b, n, s, nq=32, nkv=8, d=128, tree=False):
     def run():
         L.check(L.load().smo_verify_attention(ctypes.byref(a), torch.cuda.current_stream().cuda_stream))
     t = timeit(run)
+    if os.environ.get("KBENCH_B2B"):  # A/B: mean of 20 back-to-back launches (warm L2, no carve-out switch)
+        t = timeit(lambda: [run() for _ in range(20)]) / 20
     byts = 2 * b * (s + n) * nkv * d * 2 + 2 * q.numel() * 2
     return {"kernel": "K1 verify_attention", "b": b, "n": n, "s": s, "mask": "tree" if tree else "chain",
             "us": t * 1e6, "GBs": byts / t / 1e9,
@@ -230,6 +232,10 @@ def main():
                                   flush=True)
                         torch.cuda.empty_cache()
             return
+    if what == "attnsmall":  # latency end of config 3 (split-KV merge, launch floor)
+        for b, n, s in ((1, 1, 1024), (1, 9, 1024), (4, 9, 1024), (1, 9, 4096), (1, 1, 32768), (16, 9, 1024),
+                        (32, 9, 1024), (64, 16, 1024)):
+            res.append(attn(b, n, s))
     if what in ("codec", "all"):
         res.append(codec(bits=3))
         res.append(codec(bits=1))
