@@ -681,9 +681,9 @@ def run_ours(args):
                       "frac": cb / stages["codec"] / 1e9 / pk["hbm_gbs"], "traffic": codec_traffic_per_block(),
                       "traffic_unit": "dram bytes per expert block (one layer's decode launch / its blocks, ncu "
                       "profiles/r01k_traffic.json); algorithmic per block = "
-                      + str(int(cb / max(1.0, stages["h2d_raw_bytes"]) * shape.expert_bytes)),
-                      "bound_note": "the unary decoder is instruction-issue / latency bound (issue active 88 %, "
-                      "ncu profiles/r01k_launches.md); HBM is not its limiter",
+                      + str(int((stages["code_bits"] / 16.0 + 1.0) * shape.expert_bytes)),
+                      "bound_note": "the unary decoder is integer-pipe bound (ALU pipe 81 % of peak, issue slots "
+                      "78 % busy, ncu profiles/r02e_unary_decode.md); HBM is not its limiter",
                       "peak_kind": pk_kind}
     line = {
         "metric": "verified decode tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world,
@@ -699,11 +699,11 @@ def run_ours(args):
                    "moe_batching": "BATCH_ONE (router-selected experts)" if args.moe_batching == "one"
                    else "LARGE_BATCH (whole layers)",
                    "expert_transfer": (f"lossless tile-coded blocks (tcode.cuh T2, "
-                                       f"{16.0 * stages['h2d_bytes'] / max(1.0, stages['h2d_raw_bytes']):.2f} "
+                                       f"{stages['code_bits']:.2f} "
                                        "bits/weight), decoded in shared memory by the expert kernel"
                                        if stages.get("link_code", 0) == 2 else
                                        f"lossless exponent-coded blocks (xfer.cu, "
-                                       f"{16.0 * stages['h2d_bytes'] / max(1.0, stages['h2d_raw_bytes']):.2f} "
+                                       f"{stages['code_bits']:.2f} "
                                        "bits/weight), expanded in HBM before the expert kernel")
                    if args.compress else "raw bf16",
                    "l2": "inputs larger than L2 (90.2 GB of experts + 4.6 GB KV streamed per step)",
@@ -727,8 +727,9 @@ def run_ours(args):
                                          "note": "the same rule on the bytes that actually crossed the link"},
                           "h2d_peak_gbs": h2d_peak, "hbm_peak_gbs": pk["hbm_gbs"],
                           "hbm_term_includes_codec_bytes": codec_hbm},
-        "codec_bits_per_weight": (16.0 * stages["h2d_bytes"] / stages["h2d_raw_bytes"]
-                                  if args.compress and stages["h2d_raw_bytes"] > 0 else 16.0),
+        "codec_bits_per_weight": stages["code_bits"],  # the blocks as stored (host + coded cache)
+        "link_bits_per_weight": (16.0 * stages["h2d_bytes"] / stages["h2d_raw_bytes"]
+                                 if stages["h2d_raw_bytes"] > 0 else None),  # what crossed the link this step
         "expert_tflops": (shape.n_layers * 2 * 3 * shape.hidden * shape.inter * b * n * shape.top_k / moe_t / 1e12
                           if moe_t > 0 else None),
         "attention_roofline": {"bound": "hbm", "achieved": attn_bytes_step / stages["attention"] / 1e9

@@ -486,6 +486,9 @@ typedef struct {
                           2 T2 tile code decoded inside the expert kernel */
   double host_numa;    /* NUMA node the pinned expert blocks were bound to (the GPU's own; -1: default
                           placement, e.g. a single-node host or SMO_HOST_NUMA=-1) */
+  double code_bits;    /* mean bits per weight of the engine's expert blocks as stored in host memory
+                          and the coded hot cache (16: raw bf16) — defined even when no block crossed
+                          the link in the last step (everything cached) */
 } smo_stage_times;
 smo_status smo_engine_last_times(smo_engine* e, smo_stage_times* t);
 /* Measured per-layer timeline of the last verify step with m micro-batches

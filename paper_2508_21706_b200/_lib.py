@@ -85,7 +85,7 @@ class StageTimes(C.Structure):
                 ("h2d_transfer", C.c_double), ("others", C.c_double), ("h2d_bytes", C.c_double),
                 ("launches", C.c_double), ("draft", C.c_double), ("h2d_raw_bytes", C.c_double),
                 ("codec", C.c_double), ("codec_bytes", C.c_double), ("link_code", C.c_double),
-                ("host_numa", C.c_double)]
+                ("host_numa", C.c_double), ("code_bits", C.c_double)]
 
 
 _SIGS = {
