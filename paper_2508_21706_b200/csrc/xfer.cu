@@ -411,6 +411,7 @@ template <bool kDirect>
 __global__ void __launch_bounds__(32 * kUDecWarps, 28) unary_decode_kernel(const __grid_constant__ DecodeJobs jobs,
                                                                        size_t segs) {
   __shared__ __align__(16) uint32_t wbuf[kUDecWarps][kUMaxWords + 8];
+  __shared__ __align__(16) uint4 lobuf[kUDecWarps][64];  // the segment's lo bytes, copied ahead (cp.async)
   __shared__ int start[kUDecWarps][33];
   const uint8_t* __restrict__ src = jobs.src[blockIdx.y];
   uint16_t* __restrict__ dst = jobs.dst[blockIdx.y];
@@ -423,6 +424,12 @@ __global__ void __launch_bounds__(32 * kUDecWarps, 28) unary_decode_kernel(const
     const uint8_t* sb = src + tw.x;
     const int base = int(tw.y & 0xffu), nw = int(tw.y >> 16);
     const bool has_esc = (tw.y >> 8) & 1u;
+    // the lane's 32 lo bytes go to shared memory by cp.async now (no
+    // registers held), so their latency hides under the search and the walk
+    const uint32_t lo_s = smem_u32(&lobuf[wib][2 * lane]);
+    cp_async_16(lo_s, sb + 32 * lane);
+    cp_async_16(lo_s + 16, sb + 32 * lane + 16);
+    asm volatile("cp.async.commit_group;" ::: "memory");
     // coalesced 16-B staging of the stream (it starts 16-B aligned and the
     // segment is padded to 16 B, so whole chunks stay inside it); words past
     // the end read as ones, 6 of them at least
@@ -589,8 +596,9 @@ __global__ void __launch_bounds__(32 * kUDecWarps, 28) unary_decode_kernel(const
     // (sign << 7 | mantissa) to 16-bit lanes with the sign replicated into
     // the high byte (selector nibbles 8-B), a second PRMT the two exponents;
     // one LOP3 merges sign, exponent << 7 and mantissa.
-    const uint4 lo0 = reinterpret_cast<const uint4*>(sb)[2 * lane];  // this lane's 32 lo bytes
-    const uint4 lo1 = reinterpret_cast<const uint4*>(sb)[2 * lane + 1];
+    asm volatile("cp.async.wait_group 0;" ::: "memory");  // this lane's own copies
+    const uint4 lo0 = lobuf[wib][2 * lane];  // this lane's 32 lo bytes
+    const uint4 lo1 = lobuf[wib][2 * lane + 1];
     const uint32_t lw[8] = {lo0.x, lo0.y, lo0.z, lo0.w, lo1.x, lo1.y, lo1.z, lo1.w};
     uint32_t out[16];
 #pragma unroll
