@@ -665,7 +665,9 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
     // round trips): region k of the stages holds pair k's weights, (m, l)
     // rows and staged partials.
     if (n_split > 0) {
-      constexpr int kRegion = 16 * 128 + 64 + 16 * 128 * 2 + 16 * 128 * 4 + 64;  // floats: w, slots, (m, l), partials (+1 float4 slack)
+      // floats: w [16][128], slot_of [64], (m, l) [16][128], then the staged
+      // partials: np slices of ne float4 with np * ne <= rows * D / 4 + np
+      constexpr int kRegion = 16 * 128 + 64 + 16 * 128 * 2 + (128 * (D / 4) + 16) * 4;
       static_assert(2 * kRegion * 4 <= L::kStages * 2 * L::kKvBytes, "merge regions exceed the K/V stages");
       // per-pair slice geometry in shared memory (indexed by pair k below)
       __shared__ int np[2], e_lo[2], ne[2], r_lo[2], nr[2];

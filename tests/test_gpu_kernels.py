@@ -228,6 +228,10 @@ def _attn_case(torch, cuda, b, n, nq, nkv, d, prefix, s_max, tree, seed):
     (32, 9, 32, 8, 128, [1024] * 32, False),           # BASELINE config 2 verify shape
     (32, 32, 32, 8, 128, [256] * 32, False),           # Mixtral prefill chunk 8, b=32
     (64, 1, 32, 8, 128, [4096] * 64, False),           # plain decode, long prefix
+    # 128 rows with long prefixes: CTAs hold two split pairs, each merging a
+    # slice of both (the merge staging sized for rows * D / 4 float4)
+    (8, 32, 32, 8, 128, [4096] * 8, False),            # Mixtral prefill chunk, s = 4k
+    (4, 32, 16, 4, 64, [3000, 2900, 3100, 2000], True),  # d = 64, 128 rows, ragged
 ])
 def test_verify_attention_vs_oracle(cuda, oracle, b, n, nq, nkv, d, prefix, tree):
     import torch
