@@ -58,21 +58,6 @@ __device__ __forceinline__ int warp_excl_scan(int v, int lane, int* total) {
   return x - v;
 }
 
-// Exclusive warp prefix sum of v in [0, 63] from six bit-plane ballots: no
-// shuffle chain, so its latency is one ballot + popcounts.
-__device__ __forceinline__ int warp_excl_scan_small(int v, int lane, int* total) {
-  const uint32_t lt = (1u << lane) - 1u;
-  int pre = 0, tot = 0;
-#pragma unroll
-  for (int b = 0; b < 6; ++b) {
-    const uint32_t bal = __ballot_sync(0xffffffffu, (v >> b) & 1);
-    pre += __popc(bal & lt) << b;
-    tot += __popc(bal) << b;
-  }
-  *total = tot;
-  return pre;
-}
-
 // Decode segment s of a tile whose code sits in shared memory at `tc` into
 // the 128B-swizzled bf16 tile at `tile` (128 rows of 128 B, 1024-B aligned;
 // 16-B chunk c of row r at (c ^ (r & 7)) — what TMA SWIZZLE_128B writes and
