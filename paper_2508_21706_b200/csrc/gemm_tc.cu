@@ -44,6 +44,7 @@ struct GemmParams {
   int token_tiles;
   float* partial;    // [split_k][rows][N] fp32 when split_k > 1
   int cluster;       // CTAs along the weight tiles sharing each token-row box by TMA multicast (1: none)
+  int csplit;        // split-K reduced inside a (1, 1, split_k) cluster through DSMEM (no partials in HBM)
 };
 
 __device__ __forceinline__ void tmem_alloc_dyn(uint32_t cols, uint32_t* dst) {
@@ -68,7 +69,9 @@ __device__ __forceinline__ void tmem_dealloc_dyn(uint32_t cols, uint32_t taddr) 
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_u,
                    const __grid_constant__ CUtensorMap tm_x, GemmParams p, uint32_t tmem_cols) {
-  const int nb = blockIdx.x, g = blockIdx.y, tt = blockIdx.z % p.token_tiles, ks = blockIdx.z / p.token_tiles;
+  // z = token tile * split_k + K slice: the K slices of one output tile are
+  // consecutive, i.e. one (1, 1, split_k) cluster in the DSMEM-reduce mode
+  const int nb = blockIdx.x, g = blockIdx.y, tt = blockIdx.z / p.split_k, ks = blockIdx.z % p.split_k;
   const int g_begin = p.row_offsets ? p.row_offsets[g] : 0;
   const int g_end = p.row_offsets ? p.row_offsets[g + 1] : p.rows;
   const int row0 = g_begin + tt * p.tile_tokens;
@@ -224,7 +227,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else {
           tmem_ld_wait();
-          if (p.split_k > 1) {  // fp32 partial of this K slice; reduced in fixed order later
+          if (p.csplit) {  // fp32 partial of this K slice into this CTA's smem, token-major [cnt][128]
+            float* P = reinterpret_cast<float*>(smem);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (c0 + j < cnt) P[(c0 + j) * 128 + row] = __uint_as_float(r[j]);
+          } else if (p.split_k > 1) {  // fp32 partial of this K slice; reduced in fixed order later
             float* part = p.partial + size_t(ks) * p.rows * p.N;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
@@ -258,6 +266,64 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) tmem_dealloc_dyn(tmem_cols, tmem);
   if (cs > 1) cluster_sync_all();  // peers' last commits may still arrive on our barriers
+  if (p.csplit) {
+    // Split-K reduce through distributed shared memory: every CTA of the
+    // cluster holds its K slice's fp32 tile [cnt][128] in its (now idle)
+    // smem ring; after one cluster barrier CTA ks reduces tokens
+    // [ks cnt / S, (ks + 1) cnt / S) over the S slices in slice order
+    // (deterministic, = the partial-buffer path's sum) and applies the
+    // epilogue; a second barrier keeps every slice alive until read.
+    const int S = p.split_k;
+    cluster_sync_all();
+    const int t0 = ks * cnt / S, t1 = (ks + 1) * cnt / S;
+    const uint32_t pbase = smem_u32(smem);
+    const bool vec = (reinterpret_cast<uintptr_t>(p.out) & 15) == 0 && (p.ldo & 3) == 0;  // 16-B rows of 4
+    for (int idx = threadIdx.x; idx < (t1 - t0) * 32; idx += kThreads) {
+      const int t = t0 + idx / 32, c4 = idx % 32;
+      const uint32_t off = uint32_t((t * 128 + 4 * c4) * 4);
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int j = 0; j < S; ++j) {
+        uint32_t ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(pbase + off), "r"(j));
+        float4 v;
+        asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(ra) : "memory");
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+      }
+      const size_t o = size_t(row0 + t) * p.ldo + size_t(nb) * 128 + 4 * c4;
+      if (p.epilogue == SMO_EPI_BF16) {
+        uint16_t* dst = reinterpret_cast<uint16_t*>(p.out) + o;
+        if (vec) {
+          *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16x2(acc.x, acc.y), pack_bf16x2(acc.z, acc.w));
+        } else {
+          dst[0] = f2bf(acc.x);
+          dst[1] = f2bf(acc.y);
+          dst[2] = f2bf(acc.z);
+          dst[3] = f2bf(acc.w);
+        }
+      } else {
+        float* dst = reinterpret_cast<float*>(p.out) + o;
+        if (p.epilogue == SMO_EPI_F32_ADD) {
+          acc.x += dst[0];
+          acc.y += dst[1];
+          acc.z += dst[2];
+          acc.w += dst[3];
+        }
+        if (vec) {
+          *reinterpret_cast<float4*>(dst) = acc;
+        } else {
+          dst[0] = acc.x;
+          dst[1] = acc.y;
+          dst[2] = acc.z;
+          dst[3] = acc.w;
+        }
+      }
+    }
+    cluster_sync_all();
+  }
 }
 
 // Fixed-order split-K reduction fused with the epilogue: out = epi(sum_s P_s).
@@ -292,6 +358,15 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits,
   }
 }
 
+void set_gemm_smem_attr() {
+  static bool attr_set = false;
+  if (!attr_set) {
+    SMO_CUDA_CHECK(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kSmemBudget + 4096));
+    attr_set = true;
+  }
+}
+
 int device_sm_count() {
   static int sms = 0;
   if (!sms) {
@@ -305,6 +380,7 @@ int device_sm_count() {
 
 struct GemmPlan {
   int tile, token_tiles, stages, split, cluster;
+  bool csplit;  // split-K reduced through DSMEM inside a (1, 1, split) cluster
   uint32_t cols;
 };
 
@@ -340,6 +416,50 @@ GemmPlan plan_gemm(const smo_gemm_args& a) {
     const char* f = std::getenv("SMO_GEMM_CLUSTER");
     return f ? std::atoi(f) : 1;
   }();
+  static const int env_csplit = [] {
+    const char* f = std::getenv("SMO_GEMM_CSPLIT");
+    return f ? std::atoi(f) : 1;
+  }();
+  // the split-K partials reduce through DSMEM (SMO_GEMM_CSPLIT=0: fp32
+  // partials in a workspace + a reduce launch) when a cluster of `split`
+  // CTAs is portable, the [tile][128] fp32 slice fits the smem ring, and
+  // every cluster is resident in one wave (a GPC holds a whole number of
+  // clusters: 148 SMs do not take 48 clusters of 3). The automatic split
+  // steps down until the clusters fit (QKV at 288 tokens: split 2 in
+  // clusters, 38.9 us, beats split 3 with partials, 42.0 us).
+  pl.csplit = false;
+  const bool cs_ok = env_csplit && env_cluster <= 1 && pl.tile * 128 * 4 <= pl.stages * stage_bytes;
+  auto fits = [&](int sp) {
+    static int fit[9][kMaxStages + 1] = {};
+    int& nfit = fit[sp][pl.stages];
+    if (nfit == 0) {
+      set_gemm_smem_attr();
+      cudaLaunchConfig_t q{};
+      q.gridDim = dim3(a.N / 128, 1, sp);
+      q.blockDim = dim3(kThreads);
+      q.dynamicSmemBytes = size_t(pl.stages) * stage_bytes + 1024;
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = 1;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = unsigned(sp);
+      q.attrs = qa;
+      q.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&nfit, gemm_tc_kernel, &q) != cudaSuccess || nfit <= 0) {
+        cudaGetLastError();
+        nfit = -1;
+      }
+    }
+    return nfit > 0 && long(a.N / 128) * a.groups * pl.token_tiles <= nfit;
+  };
+  if (cs_ok && pl.split > 1 && pl.split <= 8) {
+    for (int sp = pl.split; sp >= (a.split_k > 1 ? pl.split : 2); --sp)
+      if (fits(sp)) {
+        pl.split = sp;
+        pl.csplit = true;
+        break;
+      }
+  }
   if (a.groups == 1 && !a.row_offsets && env_cluster > 1) {
     const int nt = a.N / 128;
     for (int c : {4, 2})
@@ -355,7 +475,7 @@ GemmPlan plan_gemm(const smo_gemm_args& a) {
 
 size_t gemm_workspace(const smo_gemm_args& a) {
   const GemmPlan pl = plan_gemm(a);
-  return pl.split > 1 ? size_t(pl.split) * a.rows * a.N * sizeof(float) : 0;
+  return pl.split > 1 && !pl.csplit ? size_t(pl.split) * a.rows * a.N * sizeof(float) : 0;
 }
 
 void gemm_launch(const smo_gemm_args& a, cudaStream_t stream) {
@@ -372,7 +492,7 @@ void gemm_launch(const smo_gemm_args& a, cudaStream_t stream) {
   const int tile = pl.tile, token_tiles = pl.token_tiles, stages = pl.stages;
   const uint32_t cols = pl.cols;
   SMO_REQUIRE(stages >= 2, "gemm: token tile too large for the smem ring");
-  const size_t ws_need = pl.split > 1 ? size_t(pl.split) * a.rows * a.N * sizeof(float) : 0;
+  const size_t ws_need = pl.split > 1 && !pl.csplit ? size_t(pl.split) * a.rows * a.N * sizeof(float) : 0;
   SMO_REQUIRE(ws_need == 0 || (a.workspace && a.workspace_bytes >= ws_need),
               "gemm: split-K workspace too small (smo_gemm_workspace)");
 
@@ -412,15 +532,25 @@ void gemm_launch(const smo_gemm_args& a, cudaStream_t stream) {
   p.partial = reinterpret_cast<float*>(a.workspace);
   const int stage_bytes = kTileBytesA * (swiglu ? 2 : 1) + tile * 128;
   const size_t smem = size_t(stages) * stage_bytes + 1024;
-  static bool attr_set = false;
-  if (!attr_set) {
-    SMO_CUDA_CHECK(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        kSmemBudget + 4096));
-    attr_set = true;
-  }
+  set_gemm_smem_attr();
   p.cluster = pl.cluster;
+  p.csplit = pl.csplit ? 1 : 0;
   dim3 grid(a.N / 128, a.groups, token_tiles * pl.split);
-  if (pl.cluster > 1) {
+  if (pl.csplit) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = unsigned(pl.split);
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SMO_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_tc_kernel, tw, tu, tx, p, cols));
+  } else if (pl.cluster > 1) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(kThreads);
@@ -439,7 +569,7 @@ void gemm_launch(const smo_gemm_args& a, cudaStream_t stream) {
   }
   count_launch();
   SMO_CUDA_CHECK(cudaGetLastError());
-  if (pl.split > 1) {
+  if (pl.split > 1 && !pl.csplit) {
     const size_t total4 = size_t(a.rows) * a.N / 4;
     const int blocks = int(std::min<size_t>((total4 + 255) / 256, size_t(device_sm_count()) * 8));
     splitk_reduce_kernel<<<blocks, 256, 0, stream>>>(p.partial, pl.split, a.rows, a.N, a.epilogue, a.out, p.ldo);

@@ -20,7 +20,9 @@ def _u16(t):
 
 # ---------------------------------------------------------------- K4 GEMM
 @pytest.mark.parametrize("T,K,N", [(1, 512, 128), (20, 512, 768), (160, 4096, 1024), (288, 4096, 768),
-                                   (300, 1024, 256), (520, 512, 384), (37, 14336, 256), (4100, 512, 384)])
+                                   (300, 1024, 256), (520, 512, 384), (37, 14336, 256), (4100, 512, 384),
+                                   # the verify step's projections (split K reduced in clusters)
+                                   (288, 4096, 6144), (288, 4096, 4096), (32, 4096, 6144)])
 def test_gemm_dense_f32_vs_torch(cuda, T, K, N):
     import torch
     from paper_2508_21706_b200 import ops, _lib as L
@@ -38,6 +40,49 @@ def test_gemm_dense_f32_vs_torch(cuda, T, K, N):
     ops.gemm(x, w, epilogue=L.EPI_F32_ADD, out=acc)
     assert (acc - 1.0 - ref).abs().max().item() <= 1e-4 * max(1.0, ref.abs().max().item())
     torch.cuda.synchronize()
+
+
+_CSPLIT_SHAPES = [(288, 4096, 6144), (288, 4096, 4096), (32, 4096, 6144), (160, 4096, 1024), (288, 14336, 4096)]
+_CSPLIT_SCRIPT = r'''
+import sys, math, torch, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2508_21706_b200 import ops, _lib as L
+outs = []
+for T, K, N in %r:
+    g = torch.Generator(device="cuda").manual_seed(T + K + N)
+    x = (torch.rand((T, K), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    w = ((torch.rand((N, K), generator=g, device="cuda") * 2 - 1) * math.sqrt(3.0 / K)).to(torch.bfloat16)
+    for sk in (2, 4):  # the same K slicing in both modes (the automatic split differs)
+        acc = torch.ones((T, N), dtype=torch.float32, device="cuda")
+        ops.gemm(x, w, epilogue=L.EPI_F32_ADD, out=acc, split_k=sk)
+        outs += [ops.gemm(x, w, epilogue=L.EPI_F32, split_k=sk).cpu().numpy(),
+                 ops.gemm(x, w, epilogue=L.EPI_BF16, split_k=sk).float().cpu().numpy(), acc.cpu().numpy()]
+np.savez(sys.argv[2], *outs)
+''' % (_CSPLIT_SHAPES,)
+
+
+def test_gemm_cluster_splitk_bit_identical(cuda, tmp_path):
+    """Split-K reduced through DSMEM inside (1, 1, split) clusters sums the
+    K slices in the same order as the partial-buffer path (SMO_GEMM_CSPLIT=0,
+    fp32 partials + reduce launch): fp32, bf16 and residual-add epilogues are
+    bit-identical at the verify step's projection shapes, for the same split
+    (the automatic split differs between the modes: clusters must fit one
+    wave)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for mode in ("0", "1"):
+        env = dict(os.environ, SMO_GEMM_CSPLIT=mode)
+        f = str(tmp_path / f"g{mode}.npz")
+        r = subprocess.run([sys.executable, "-c", _CSPLIT_SCRIPT, root, f], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        z = np.load(f)
+        res[mode] = [z[k] for k in sorted(z.files, key=lambda n: int(n.split("_")[1]))]
+    for a, b in zip(res["0"], res["1"]):
+        assert np.array_equal(a, b)
 
 
 @pytest.mark.parametrize("T,V", [(20, 32000), (288, 32000), (5, 1024)])
