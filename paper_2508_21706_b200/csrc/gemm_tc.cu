@@ -13,6 +13,7 @@
 //   FLOPs = 2 * rows * N * K (x2 for SwiGLU), HBM bytes ~= weight bytes
 //   (N*K*2 per group, x2 for SwiGLU) + activations.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -66,6 +67,33 @@ __device__ __forceinline__ void tmem_dealloc_dyn(uint32_t cols, uint32_t taddr) 
   }
 }
 
+__device__ __forceinline__ void tmem_alloc_pair_dyn(uint32_t cols, uint32_t* dst) {
+  switch (cols) {
+    case 32: tmem_alloc_pair<32>(dst); break;
+    case 64: tmem_alloc_pair<64>(dst); break;
+    case 128: tmem_alloc_pair<128>(dst); break;
+    case 256: tmem_alloc_pair<256>(dst); break;
+    default: tmem_alloc_pair<512>(dst); break;
+  }
+}
+__device__ __forceinline__ void tmem_dealloc_pair_dyn(uint32_t cols, uint32_t taddr) {
+  switch (cols) {
+    case 32: tmem_dealloc_pair<32>(taddr); break;
+    case 64: tmem_dealloc_pair<64>(taddr); break;
+    case 128: tmem_dealloc_pair<128>(taddr); break;
+    case 256: tmem_dealloc_pair<256>(taddr); break;
+    default: tmem_dealloc_pair<512>(taddr); break;
+  }
+}
+
+// kPair: CTA pairs (tcgen05 cta_group::2, cluster x = 2): the pair's two
+// 128-row weight tiles form one M = 256 MMA issued by the even CTA; each CTA
+// loads its own weight rows and HALF of the token rows (N split across the
+// pair), so every token row crosses into shared memory once per 256 weight
+// rows instead of once per 128 — the token operand is 2.25x the weight bytes
+// per stage at 288 tokens. Each CTA's TMEM holds its 128 rows x all tokens,
+// so the epilogues are the single-CTA ones.
+template <bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_u,
                    const __grid_constant__ CUtensorMap tm_x, GemmParams p, uint32_t tmem_cols) {
@@ -80,10 +108,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const bool swiglu = p.epilogue == SMO_EPI_SWIGLU;
   const int wblk = p.w_index ? p.w_index[g] : g;
-  const int n_pad = (cnt + 15) & ~15;
-  const int n_load = (cnt + 31) & ~31;
+  // pair: tokens padded to 64 so each instruction's N (n1 <= 256, n2) splits
+  // into two halves of whole 32-row boxes; CTA r loads rows [r n1/2, ..) and
+  // [n1 + r n2/2, ..) of the tile (rows past the batch load as zeros)
+  const int n_pad = kPair ? (cnt + 63) & ~63 : (cnt + 15) & ~15;
+  const int n_load = kPair ? n_pad / 2 : (cnt + 31) & ~31;  // token rows this CTA loads per stage
   const int a_bytes = kTileBytesA * (swiglu ? 2 : 1);
-  const int stage_bytes = a_bytes + p.tile_tokens * 128;
+  const int stage_bytes = a_bytes + (kPair ? p.tile_tokens / 2 : p.tile_tokens) * 128;
   const uint32_t tx_bytes = uint32_t(a_bytes + (n_load / 32) * 4096);
   const int kb0 = ks * p.kb_per_split;
   const int KB = min(p.K / kBK - kb0, p.kb_per_split);  // k-blocks of this CTA's K slice
@@ -103,8 +134,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   // and multicasts them to all, and a stage is reused only once every CTA's
   // MMA released it (the commit arrives on every CTA's empty barrier)
   const int cs = p.cluster;
-  const uint32_t crank = cs > 1 ? cluster_ctarank() : 0u;
+  const uint32_t crank = (cs > 1 || kPair || p.csplit) ? cluster_ctarank() : 0u;
   const uint16_t cmask = uint16_t((1u << cs) - 1u);
+  const uint32_t pr = kPair ? (crank & 1u) : 0u;          // rank within the CTA pair
+  const uint32_t lead = crank & ~1u;                       // the pair's even (MMA-issuing) CTA
+  const uint16_t pmask = uint16_t(3u << lead);             // both CTAs of the pair
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -116,10 +150,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tm_x);
     if (swiglu) tma_prefetch_desc(&tm_u);
   }
-  if (warp == 1) tmem_alloc_dyn(tmem_cols, &tmem_base_sh);
+  if (warp == 1) {
+    if constexpr (kPair) tmem_alloc_pair_dyn(tmem_cols, &tmem_base_sh);
+    else tmem_alloc_dyn(tmem_cols, &tmem_base_sh);
+  }
   tc_fence_before();
   __syncthreads();
-  if (cs > 1) cluster_sync_all();  // every CTA's barriers are initialised before any multicast
+  if (cs > 1 || kPair) cluster_sync_all();  // every CTA's barriers are initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
 
@@ -129,12 +166,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = kb % p.stages;
         const uint32_t ph = (kb / p.stages) & 1;
         mbar_wait(&empty_bar[s], ph ^ 1);
-        mbar_arrive_expect_tx(&full_bar[s], tx_bytes);
         uint8_t* sa = smem + s * stage_bytes;
         const int kc = (kb0 + kb) * kBK;
+        uint8_t* sb = sa + a_bytes;
+        if constexpr (kPair) {
+          // own weight rows + own half of the token rows, completing on the
+          // leader's full barrier; the leader alone arrives, expecting both
+          // CTAs' bytes (the tx count may run ahead of the expectation: the
+          // peer refills stage s only after the leader's commit released it)
+          const uint32_t fb = mapa_u32(smem_u32(&full_bar[s]), lead);
+          if (pr == 0) mbar_arrive_expect_tx(&full_bar[s], 2 * tx_bytes);
+          tma_load_3d_pair(sa, &tm_w, fb, kc, nb * 128, wblk);
+          const int n1 = min(n_pad, 256), n2 = n_pad - n1;
+          for (int i = 0; i < n1 / 64; ++i)
+            tma_load_2d_pair(sb + i * 4096, &tm_x, fb, kc, row0 + int(pr) * (n1 / 2) + i * 32);
+          for (int i = 0; i < n2 / 64; ++i)
+            tma_load_2d_pair(sb + (n1 / 64 + i) * 4096, &tm_x, fb, kc, row0 + n1 + int(pr) * (n2 / 2) + i * 32);
+          continue;
+        }
+        mbar_arrive_expect_tx(&full_bar[s], tx_bytes);
         tma_load_3d(sa, &tm_w, &full_bar[s], kc, nb * 128, wblk);
         if (swiglu) tma_load_3d(sa + kTileBytesA, &tm_u, &full_bar[s], kc, nb * 128, wblk);
-        uint8_t* sb = sa + a_bytes;
         if (cs > 1) {
           for (int i = int(crank); i < n_load / 32; i += cs)
             tma_load_2d_mc(sb + i * 4096, &tm_x, &full_bar[s], kc, row0 + i * 32, cmask);
@@ -144,7 +196,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (elect_one()) {
+    if (kPair && pr != 0) {
+      // the pair's MMAs are issued by the even CTA
+    } else if (kPair) {
+      if (elect_one()) {
+        const int n1 = min(n_pad, 256), n2 = n_pad - n1;
+        const uint32_t id0 = make_idesc_bf16(256, n1);
+        const uint32_t id1 = n2 > 0 ? make_idesc_bf16(256, n2) : 0u;
+        for (int kb = 0; kb < KB; ++kb) {
+          const int s = kb % p.stages;
+          const uint32_t ph = (kb / p.stages) & 1;
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + s * stage_bytes);
+          const uint64_t ad = make_sdesc_sw128(a_addr, 16, 1024);
+          const uint64_t bd0 = make_sdesc_sw128(a_addr + a_bytes, 16, 1024);
+          const uint64_t bd1 = bd0 + uint64_t(((n1 / 2) * 128) >> 4);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+            const uint64_t ko = uint64_t((k * 32) >> 4);
+            umma_bf16_pair(tmem, ad + ko, bd0 + ko, id0, acc);
+            if (n2 > 0) umma_bf16_pair(tmem + uint32_t(n1), ad + ko, bd1 + ko, id1, acc);
+          }
+          umma_commit_pair_mc(&empty_bar[s], pmask);
+        }
+        umma_commit_pair_mc(&tmem_full_bar, pmask);
+      }
+    } else if (elect_one()) {
       const int nc0 = min(n_pad, 256);
       const int nc1 = n_pad - nc0;
       const uint32_t id0 = make_idesc_bf16(128, nc0);
@@ -264,7 +343,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc_dyn(tmem_cols, tmem);
+  if constexpr (kPair) cluster_sync_all();  // both CTAs done with the pair's TMEM
+  if (warp == 1) {
+    if constexpr (kPair) tmem_dealloc_pair_dyn(tmem_cols, tmem);
+    else tmem_dealloc_dyn(tmem_cols, tmem);
+  }
   if (cs > 1) cluster_sync_all();  // peers' last commits may still arrive on our barriers
   if (p.csplit) {
     // Split-K reduce through distributed shared memory: every CTA of the
@@ -284,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int j = 0; j < S; ++j) {
         uint32_t ra;
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(pbase + off), "r"(j));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(pbase + off), "r"(kPair ? int(pr) + 2 * j : j));
         float4 v;
         asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
                      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(ra) : "memory");
@@ -361,10 +444,35 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ part, int splits,
 void set_gemm_smem_attr() {
   static bool attr_set = false;
   if (!attr_set) {
-    SMO_CUDA_CHECK(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SMO_CUDA_CHECK(cudaFuncSetAttribute(gemm_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kSmemBudget + 4096));
+    SMO_CUDA_CHECK(cudaFuncSetAttribute(gemm_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         kSmemBudget + 4096));
     attr_set = true;
   }
+}
+
+// clusters of (cx, 1, cz) CTAs of gemm_tc_kernel<kPair> resident at once (-1: none / error)
+template <bool kPair>
+int gemm_cluster_fit(int cx, int cz, int smem_bytes) {
+  set_gemm_smem_attr();
+  cudaLaunchConfig_t q{};
+  q.gridDim = dim3(unsigned(cx), 1, unsigned(cz));
+  q.blockDim = dim3(kThreads);
+  q.dynamicSmemBytes = size_t(smem_bytes);
+  cudaLaunchAttribute qa[1];
+  qa[0].id = cudaLaunchAttributeClusterDimension;
+  qa[0].val.clusterDim.x = unsigned(cx);
+  qa[0].val.clusterDim.y = 1;
+  qa[0].val.clusterDim.z = unsigned(cz);
+  q.attrs = qa;
+  q.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<kPair>, &q) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    return -1;
+  }
+  return n;
 }
 
 int device_sm_count() {
@@ -380,11 +488,74 @@ int device_sm_count() {
 
 struct GemmPlan {
   int tile, token_tiles, stages, split, cluster;
-  bool csplit;  // split-K reduced through DSMEM inside a (1, 1, split) cluster
+  bool csplit;  // split-K reduced through DSMEM inside a (pair ? 2 : 1, 1, split) cluster
+  bool pair;    // CTA pairs (cta_group::2, M = 256)
   uint32_t cols;
 };
 
+// Dense projections as CTA pairs (see the kernel): tokens in tiles of up to
+// 512 rounded to 64, each CTA stages half of them; K split over clusters of
+// (2, 1, split) reduced through DSMEM when the clusters fit one wave.
+bool plan_pair(const smo_gemm_args& a, GemmPlan& pl) {
+  const bool swiglu = a.epilogue == SMO_EPI_SWIGLU;
+  const int per_group = a.max_rows_per_group > 0 ? std::min(a.max_rows_per_group, a.rows) : a.rows;
+  pl = GemmPlan{};
+  if (a.groups == 1 && !a.row_offsets && !a.w_index && !swiglu && a.N % 256 == 0 &&
+      !std::getenv("SMO_GEMM_CLUSTER")) {
+    pl.pair = true;
+    pl.cluster = 1;
+    pl.tile = std::min(512, (per_group + 63) & ~63);
+    pl.token_tiles = (per_group + pl.tile - 1) / pl.tile;
+    const int sb = kTileBytesA + (pl.tile / 2) * 128;
+    pl.stages = std::min(kMaxStages, kSmemBudget / sb);
+    pl.cols = 32;
+    while (int(pl.cols) < pl.tile) pl.cols <<= 1;
+    const int pairs = (a.N / 256) * pl.token_tiles;
+    pl.split = 1;
+    pl.csplit = false;
+    const bool splittable = a.epilogue == SMO_EPI_BF16 || a.epilogue == SMO_EPI_F32 || a.epilogue == SMO_EPI_F32_ADD;
+    if (splittable && a.split_k != 1 && pl.tile * 128 * 4 <= pl.stages * sb) {
+      const int want = a.split_k > 1 ? a.split_k : device_sm_count() / std::max(1, 2 * pairs);
+      const int top = std::max(1, std::min({want, a.K / kBK / 8, 4}));
+      for (int sp = top; sp >= (a.split_k > 1 ? top : 2); --sp) {
+        const int n = gemm_cluster_fit<true>(2, sp, pl.stages * sb + 1024);
+        if (n > 0 && pairs <= n) {
+          pl.split = sp;
+          pl.csplit = true;
+          break;
+        }
+      }
+    }
+    // an explicit split the pair clusters cannot hold: the single-CTA plan
+    if (a.split_k > 1 && pl.split != a.split_k) return false;
+    return true;
+  }
+  return false;
+}
+
+GemmPlan plan_single(const smo_gemm_args& a);
+
+// The pair plan where it launches at least as many CTAs as the single-CTA
+// plan (same-box A/B, tools/gemm_ab.py: QKV 38.4 -> 35.8 us, LM head + argmax
+// 117 -> 103 us; O-proj and the K = 14336 projection keep the single-CTA
+// plan, whose split 4 fills more SMs than the pair's clusters of 6 or 8 can).
+// SMO_GEMM_PAIR=0: never, =2: always when eligible.
 GemmPlan plan_gemm(const smo_gemm_args& a) {
+  static const int env_pair = [] {
+    const char* f = std::getenv("SMO_GEMM_PAIR");
+    return f ? std::atoi(f) : 1;
+  }();
+  const GemmPlan single = plan_single(a);
+  GemmPlan pair;
+  if (env_pair && plan_pair(a, pair)) {
+    const long ps = 2L * (a.N / 256) * pair.token_tiles * pair.split;
+    const long ss = long(a.N / 128) * a.groups * single.token_tiles * single.split;
+    if (env_pair == 2 || ps >= ss) return pair;
+  }
+  return single;
+}
+
+GemmPlan plan_single(const smo_gemm_args& a) {
   const bool swiglu = a.epilogue == SMO_EPI_SWIGLU;
   const int per_group = a.max_rows_per_group > 0 ? std::min(a.max_rows_per_group, a.rows) : a.rows;
   GemmPlan pl{};
@@ -432,24 +603,7 @@ GemmPlan plan_gemm(const smo_gemm_args& a) {
   auto fits = [&](int sp) {
     static int fit[9][kMaxStages + 1] = {};
     int& nfit = fit[sp][pl.stages];
-    if (nfit == 0) {
-      set_gemm_smem_attr();
-      cudaLaunchConfig_t q{};
-      q.gridDim = dim3(a.N / 128, 1, sp);
-      q.blockDim = dim3(kThreads);
-      q.dynamicSmemBytes = size_t(pl.stages) * stage_bytes + 1024;
-      cudaLaunchAttribute qa[1];
-      qa[0].id = cudaLaunchAttributeClusterDimension;
-      qa[0].val.clusterDim.x = 1;
-      qa[0].val.clusterDim.y = 1;
-      qa[0].val.clusterDim.z = unsigned(sp);
-      q.attrs = qa;
-      q.numAttrs = 1;
-      if (cudaOccupancyMaxActiveClusters(&nfit, gemm_tc_kernel, &q) != cudaSuccess || nfit <= 0) {
-        cudaGetLastError();
-        nfit = -1;
-      }
-    }
+    if (nfit == 0) nfit = gemm_cluster_fit<false>(1, sp, pl.stages * stage_bytes + 1024);
     return nfit > 0 && long(a.N / 128) * a.groups * pl.token_tiles <= nfit;
   };
   if (cs_ok && pl.split > 1 && pl.split <= 8) {
@@ -489,6 +643,9 @@ void gemm_launch(const smo_gemm_args& a, cudaStream_t stream) {
   SMO_REQUIRE(a.epilogue != SMO_EPI_ARGMAX || (a.argmax_val && a.argmax_idx), "gemm: ARGMAX needs partial buffers");
   SMO_REQUIRE(a.epilogue == SMO_EPI_ARGMAX || a.out, "gemm: null output");
   const GemmPlan pl = plan_gemm(a);
+  if (std::getenv("SMO_GEMM_DEBUG"))
+    std::fprintf(stderr, "gemm rows=%d K=%d N=%d: pair=%d tile=%d tt=%d stages=%d split=%d csplit=%d\n", a.rows, a.K,
+                 a.N, int(pl.pair), pl.tile, pl.token_tiles, pl.stages, pl.split, int(pl.csplit));
   const int tile = pl.tile, token_tiles = pl.token_tiles, stages = pl.stages;
   const uint32_t cols = pl.cols;
   SMO_REQUIRE(stages >= 2, "gemm: token tile too large for the smem ring");
@@ -530,13 +687,27 @@ void gemm_launch(const smo_gemm_args& a, cudaStream_t stream) {
   p.kb_per_split = (a.K / kBK + pl.split - 1) / pl.split;
   p.token_tiles = token_tiles;
   p.partial = reinterpret_cast<float*>(a.workspace);
-  const int stage_bytes = kTileBytesA * (swiglu ? 2 : 1) + tile * 128;
+  const int stage_bytes = kTileBytesA * (swiglu ? 2 : 1) + (pl.pair ? tile / 2 : tile) * 128;
   const size_t smem = size_t(stages) * stage_bytes + 1024;
   set_gemm_smem_attr();
   p.cluster = pl.cluster;
   p.csplit = pl.csplit ? 1 : 0;
   dim3 grid(a.N / 128, a.groups, token_tiles * pl.split);
-  if (pl.csplit) {
+  if (pl.pair) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = pl.csplit ? unsigned(pl.split) : 1u;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SMO_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<true>, tw, tu, tx, p, cols));
+  } else if (pl.csplit) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(kThreads);
@@ -549,7 +720,7 @@ void gemm_launch(const smo_gemm_args& a, cudaStream_t stream) {
     attr[0].val.clusterDim.z = unsigned(pl.split);
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    SMO_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_tc_kernel, tw, tu, tx, p, cols));
+    SMO_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<false>, tw, tu, tx, p, cols));
   } else if (pl.cluster > 1) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
@@ -563,9 +734,9 @@ void gemm_launch(const smo_gemm_args& a, cudaStream_t stream) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    SMO_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_tc_kernel, tw, tu, tx, p, cols));
+    SMO_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<false>, tw, tu, tx, p, cols));
   } else {
-    gemm_tc_kernel<<<grid, kThreads, smem, stream>>>(tw, tu, tx, p, cols);
+    gemm_tc_kernel<false><<<grid, kThreads, smem, stream>>>(tw, tu, tx, p, cols);
   }
   count_launch();
   SMO_CUDA_CHECK(cudaGetLastError());

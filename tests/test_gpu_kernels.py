@@ -62,7 +62,8 @@ np.savez(sys.argv[2], *outs)
 
 
 def test_gemm_cluster_splitk_bit_identical(cuda, tmp_path):
-    """Split-K reduced through DSMEM inside (1, 1, split) clusters sums the
+    """Split-K reduced through DSMEM inside (1, 1, split) clusters — and the
+    CTA-pair (cta_group::2) kernel in (2, 1, split) clusters — sum the
     K slices in the same order as the partial-buffer path (SMO_GEMM_CSPLIT=0,
     fp32 partials + reduce launch): fp32, bf16 and residual-add epilogues are
     bit-identical at the verify step's projection shapes, for the same split
@@ -73,16 +74,20 @@ def test_gemm_cluster_splitk_bit_identical(cuda, tmp_path):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = {}
-    for mode in ("0", "1"):
-        env = dict(os.environ, SMO_GEMM_CSPLIT=mode)
+    modes = {"0": dict(SMO_GEMM_CSPLIT="0", SMO_GEMM_PAIR="0"), "1": dict(SMO_GEMM_CSPLIT="1", SMO_GEMM_PAIR="0"),
+             "pair": dict(SMO_GEMM_PAIR="2")}  # CTA pairs (cta_group::2, M = 256) wherever eligible
+    for mode, extra in modes.items():
+        env = dict(os.environ, **extra)
         f = str(tmp_path / f"g{mode}.npz")
         r = subprocess.run([sys.executable, "-c", _CSPLIT_SCRIPT, root, f], env=env, capture_output=True, text=True,
                            timeout=600)
         assert r.returncode == 0, r.stderr[-3000:]
         z = np.load(f)
         res[mode] = [z[k] for k in sorted(z.files, key=lambda n: int(n.split("_")[1]))]
-    for a, b in zip(res["0"], res["1"]):
-        assert np.array_equal(a, b)
+    for other in ("1", "pair"):
+        for i, (a, b) in enumerate(zip(res["0"], res[other])):
+            assert np.array_equal(a, b), (other, _CSPLIT_SHAPES[i // 6], (2, 4)[(i // 3) % 2], i % 3,
+                                          float(np.abs(a - b).max()))
 
 
 @pytest.mark.parametrize("T,V", [(20, 32000), (288, 32000), (5, 1024)])

@@ -15,4 +15,9 @@ for (T, K, N, epi, nm) in ((288, 4096, 6144, L.EPI_BF16, "qkv"), (288, 4096, 409
     out = torch.zeros((T, N), dtype=torch.float32 if epi in (L.EPI_F32_ADD, L.EPI_F32) else torch.bfloat16, device=dev)
     t = kbench.timeit(lambda: ops.gemm(x, w, epilogue=epi, out=out))
     res.append(f"{nm}:{t*1e6:.1f}")
+T, K, V = 288, 4096, 32000
+x = (torch.rand((T, K), device=dev) * 2 - 1).to(torch.bfloat16)
+w = (torch.rand((V, K), device=dev) * 2 - 1).to(torch.bfloat16)
+t = kbench.timeit(lambda: ops.gemm(x, w, epilogue=L.EPI_ARGMAX))
+res.append(f"lmhead:{t*1e6:.1f}")
 print(tag, " ".join(res), flush=True)
