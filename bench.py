@@ -377,9 +377,9 @@ def run_reference(args):
 
 def codec_traffic_per_block(kernel="K5_expert_decode_unary"):
     """dram__bytes_read+write of one expert_decode launch (one Mixtral expert
-    block) from the committed ncu capture (profiles/r01h_traffic.json: the
-    unary decoder the engine uses; r01f_traffic.json: the 3-bit one)."""
-    for f in ("r01k_traffic.json", "r01j_traffic.json", "r01i_traffic.json", "r01h_traffic.json", "r01f_traffic.json"):
+    block) from the newest committed ncu capture (profiles/r02e_traffic.json:
+    the unary decoder the engine uses; r01f_traffic.json: the 3-bit one)."""
+    for f in ("r02e_traffic.json", "r01k_traffic.json", "r01j_traffic.json", "r01i_traffic.json", "r01h_traffic.json", "r01f_traffic.json"):
         try:
             k = json.load(open(os.path.join(ROOT, "profiles", f)))["kernels"][kernel]
             return k["dram_read_bytes"] + k["dram_write_bytes"]
@@ -680,7 +680,7 @@ def run_ours(args):
                       "achieved": cb / stages["codec"] / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
                       "frac": cb / stages["codec"] / 1e9 / pk["hbm_gbs"], "traffic": codec_traffic_per_block(),
                       "traffic_unit": "dram bytes per expert block (one layer's decode launch / its blocks, ncu "
-                      "profiles/r01k_traffic.json); algorithmic per block = "
+                      "profiles/r02e_traffic.json); algorithmic per block = "
                       + str(int((stages["code_bits"] / 16.0 + 1.0) * shape.expert_bytes)),
                       "bound_note": "the unary decoder is integer-pipe bound (ALU pipe 81 % of peak, issue slots "
                       "78 % busy, ncu profiles/r02e_unary_decode.md); HBM is not its limiter",
