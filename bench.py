@@ -59,11 +59,12 @@ def parse():
                     help="LARGE_BATCH (stream whole layers ahead) or BATCH_ONE (stream router-selected experts)")
     ap.add_argument("--no-compress", dest="compress", action="store_false",
                     help="stream raw bf16 experts instead of the lossless code (default: coded, expanded in HBM)")
-    ap.add_argument("--codec", default="auto", choices=["auto", "unary", "tile"],
-                    help="link code of the coded transfer: auto (the engine probes the first expert block and "
-                         "keeps the smaller: unary for uniform-init, tile for gaussian-like weights), unary (xfer.cu; "
-                         "blocks expanded in HBM by a decode kernel) or tile (tcode.cuh T2; decoded inside the "
-                         "expert kernel, no bf16 expert in HBM)")
+    ap.add_argument("--codec", default="auto", choices=["auto", "unary", "tile", "tile3"],
+                    help="link code of the coded transfer: auto (the engine probes the first expert block: T3 "
+                         "when the hot cache holds every block, else the smaller of unary and T2 — unary for "
+                         "uniform-init, T2 for gaussian-like weights), unary (xfer.cu; blocks expanded in HBM by a "
+                         "decode kernel), tile (tcode.cuh T2) or tile3 (T3, fixed 3-bit exponents; both decoded "
+                         "inside the expert kernel, no bf16 expert in HBM)")
     ap.add_argument("--ep-transport", default="ipc", choices=["ipc", "nccl"],
                     help="N>1 expert-parallel exchange: CUDA-IPC peer mailboxes written by the dispatch / "
                          "combine kernels themselves (default; falls back to NCCL if IPC cannot be set up) "
@@ -552,7 +553,7 @@ def run_ours(args):
                                expert_cache_bytes=int(args.cache_gb * 1e9), host_alias_layers=a, device=local,
                                ep_rank=ep_rank, ep_size=ep_size, ep_group=grp, attn_cpu=args.attn_cpu,
                                batch_one=args.moe_batching == "one",
-                               compress_experts=(2 if args.codec == "tile" else 1) if args.compress else 0,
+                               compress_experts=({"tile": 2, "tile3": 3}.get(args.codec, 1)) if args.compress else 0,
                                micro_batches=args.micro_batches)
             alias = a
             break
@@ -667,7 +668,7 @@ def run_ours(args):
                 "achieved": moe_bytes_step / moe_t / 1e9 if moe_t > 0 else None, "peak": pk["hbm_gbs"],
                 "unit": "GB/s", "frac": (moe_bytes_step / moe_t / 1e9) / pk["hbm_gbs"] if moe_t > 0 else None,
                 "traffic": moe_traffic_per_layer() if (args.model == "mixtral-8x7b" and ep_size == 1
-                                                       and stages.get("link_code", 0) != 2) else None,
+                                                       and stages.get("link_code", 0) < 2) else None,
                 "traffic_unit": "dram bytes per layer (the fused expert launch, ncu profiles/r01c_traffic.json); "
                 "algorithmic per layer = " + str((shape.n_expert // ep_size) * shape.expert_bytes),
                 "peak_kind": pk_kind}
@@ -698,10 +699,10 @@ def run_ours(args):
                    "micro_batches": args.micro_batches,
                    "moe_batching": "BATCH_ONE (router-selected experts)" if args.moe_batching == "one"
                    else "LARGE_BATCH (whole layers)",
-                   "expert_transfer": (f"lossless tile-coded blocks (tcode.cuh T2, "
+                   "expert_transfer": (f"lossless tile-coded blocks (tcode.cuh T{int(stages['link_code'])}, "
                                        f"{stages['code_bits']:.2f} "
                                        "bits/weight), decoded in shared memory by the expert kernel"
-                                       if stages.get("link_code", 0) == 2 else
+                                       if stages.get("link_code", 0) >= 2 else
                                        f"lossless exponent-coded blocks (xfer.cu, "
                                        f"{stages['code_bits']:.2f} "
                                        "bits/weight), expanded in HBM before the expert kernel")

@@ -227,6 +227,18 @@ smo_status smo_tcode_decode(const void* src, int32_t h, int32_t h_i, void* dst, 
 smo_status smo_moe_experts_coded(const void* x_perm, int32_t rows, int32_t h, int32_t h_i, int32_t E,
                                  const int32_t* offsets, const void* const* w_code, void* h_out, float* y,
                                  int32_t splits, int32_t* splits_used, int32_t* scratch, smo_stream stream);
+/* ---- K5 tile code T3 (tcode.cuh; format restated in tests/tcode3_ref.py) ----
+ * The same tiles with every exponent a fixed 3-bit code (escapes, ~1/128 of
+ * uniform-init values, as a per-segment (position, exponent) list): ~11.2
+ * bits/weight, a decoder without per-lane loops — the code for a
+ * device-bound step (every block resident in the coded hot cache). Capacity
+ * smo_tcode_max_bytes; the expert kernel on T3 blocks is
+ * smo_moe_experts_coded3 (same contract as smo_moe_experts_coded).         */
+smo_status smo_tcode3_encode(const void* src, int32_t h, int32_t h_i, void* dst, uint64_t* bytes, smo_stream stream);
+smo_status smo_tcode3_decode(const void* src, int32_t h, int32_t h_i, void* dst, smo_stream stream);
+smo_status smo_moe_experts_coded3(const void* x_perm, int32_t rows, int32_t h, int32_t h_i, int32_t E,
+                                  const int32_t* offsets, const void* const* w_code, void* h_out, float* y,
+                                  int32_t splits, int32_t* splits_used, int32_t* scratch, smo_stream stream);
 
 /* ---- K5 expert streamer as a standalone handle (streamer.cu) --------------
  * The reference's H2D_EXPERTS(l) stage and the GPU_MOE(l) dependency on it
@@ -375,7 +387,11 @@ typedef struct {
                                  slot before the expert kernel. 2 (or env SMO_CODEC=tile): the T2
                                  tile code (smo_tcode_encode) for every block, streamed and hot-cached
                                  in that code and decoded by the expert kernel itself in shared memory
-                                 (smo_moe_experts_coded): no expansion launch, no bf16 expert in HBM. */
+                                 (smo_moe_experts_coded): no expansion launch, no bf16 expert in HBM.
+                                 3 (or SMO_CODEC=tile3): the T3 tile code (smo_tcode3_encode). With 1
+                                 and no SMO_CODEC the engine probes the first block: T3 when the hot
+                                 cache holds every block (device-bound step), else T2 when smaller
+                                 than the unary code, else unary. */
   int32_t micro_batches;      /* Hyperparameters.m (config.hpp:118-125): the batch runs as m micro-
                                  batches of ~b/m requests, issued stage-major per layer like
                                  build_target_dag (pipeline.hpp:147-206): GPU_OTHER1 of every

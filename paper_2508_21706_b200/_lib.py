@@ -108,6 +108,9 @@ _SIGS = {
     "smo_tcode_encode": (C.c_int, [_vp, _i32, _i32, _vp, _vp, _vp]),
     "smo_tcode_decode": (C.c_int, [_vp, _i32, _i32, _vp, _vp]),
     "smo_moe_experts_coded": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
+    "smo_tcode3_encode": (C.c_int, [_vp, _i32, _i32, _vp, _vp, _vp]),
+    "smo_tcode3_decode": (C.c_int, [_vp, _i32, _i32, _vp, _vp]),
+    "smo_moe_experts_coded3": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp]),
     "smo_chunked_attention_f64": (C.c_int, [_sz, _sz, _sz, _vp, _vp, _vp, _sz, _vp, _vp]),
     "smo_router_topk": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "smo_permute": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp]),

@@ -41,11 +41,11 @@ size_t expert_coded_size(const void* code, size_t count, int bits);
 void expert_encode(const void* src, size_t count, int bits, void* dst, int* overflow, cudaStream_t st);
 void expert_decode(const void* src, size_t count, int bits, void* dst, cudaStream_t st);
 size_t tcode_max_bytes(int h, int hi);
-size_t tcode_encode(const void* src, int h, int hi, void* dst, cudaStream_t st);
-void tcode_decode(const void* const* srcs, void* const* dsts, int n, int h, int hi, cudaStream_t st);
+size_t tcode_encode(const void* src, int h, int hi, void* dst, cudaStream_t st, int fmt = 2);
+void tcode_decode(const void* const* srcs, void* const* dsts, int n, int h, int hi, cudaStream_t st, int fmt = 2);
 int moe_coded_launch(const void* x_perm, int rows, int h, int hi, int E, const int32_t* offsets,
                      const void* const* w_code, void* hbuf, float* y, int splits, int max_splits, int* done,
-                     cudaStream_t st);
+                     cudaStream_t st, int fmt = 2);
 void rmsnorm(const float* x, const void* gain, int T, int h, float eps, void* y, cudaStream_t st);
 void embed(const int32_t* tok, const void* emb, int T, int h, float* x, cudaStream_t st);
 void rope_append(const void* qkv, const int32_t* prefix, const int32_t* parent, int b, int n, int n_q, int n_kv,
@@ -227,6 +227,15 @@ smo_status smo_tcode_encode(const void* src, int32_t h, int32_t h_i, void* dst, 
 smo_status smo_tcode_decode(const void* src, int32_t h, int32_t h_i, void* dst, smo_stream stream) {
   return guard([&] { smo::tcode_decode(&src, &dst, 1, h, h_i, S(stream)); });
 }
+smo_status smo_tcode3_encode(const void* src, int32_t h, int32_t h_i, void* dst, uint64_t* bytes, smo_stream stream) {
+  return guard([&] {
+    const size_t n = smo::tcode_encode(src, h, h_i, dst, S(stream), 3);
+    if (bytes) *bytes = n;
+  });
+}
+smo_status smo_tcode3_decode(const void* src, int32_t h, int32_t h_i, void* dst, smo_stream stream) {
+  return guard([&] { smo::tcode_decode(&src, &dst, 1, h, h_i, S(stream), 3); });
+}
 
 smo_status smo_unpermute_combine_split(const float* y, int32_t splits, uint64_t split_stride, const int32_t* pos,
                                        const float* w, int32_t T, int32_t k, int32_t h, float* residual,
@@ -254,6 +263,15 @@ smo_status smo_moe_experts_coded(const void* x_perm, int32_t rows, int32_t h, in
   return guard([&] {
     const int sp = smo::moe_coded_launch(x_perm, rows, h, h_i, E, offsets, w_code, h_out, y, splits, 4, scratch,
                                          S(stream));
+    if (splits_used) *splits_used = sp;
+  });
+}
+smo_status smo_moe_experts_coded3(const void* x_perm, int32_t rows, int32_t h, int32_t h_i, int32_t E,
+                                  const int32_t* offsets, const void* const* w_code, void* h_out, float* y,
+                                  int32_t splits, int32_t* splits_used, int32_t* scratch, smo_stream stream) {
+  return guard([&] {
+    const int sp = smo::moe_coded_launch(x_perm, rows, h, h_i, E, offsets, w_code, h_out, y, splits, 4, scratch,
+                                         S(stream), 3);
     if (splits_used) *splits_used = sp;
   });
 }

@@ -153,7 +153,8 @@ void Engine::decode_slot(int l, cudaStream_t st) {
 int Engine::expert_block(int l, const void* x_perm, int rows, int nexp, const int32_t* offsets, const int32_t* w_index,
                          const void* const* w_code, void* hb, float* y, int splits, int max_splits, cudaStream_t st) {
   (void)l;
-  if (tmode) return moe_coded_launch(x_perm, rows, h, hi, nexp, offsets, w_code, hb, y, splits, max_splits, d_done, st);
+  if (tmode)
+    return moe_coded_launch(x_perm, rows, h, hi, nexp, offsets, w_code, hb, y, splits, max_splits, d_done, st, tfmt);
   return moe_launch(x_perm, rows, h, hi, nexp, offsets, pool, blk_bytes, pool_blocks, w_index, hb, y, splits,
                     max_splits, d_done, st);
 }
@@ -305,7 +306,8 @@ void Engine::create() {
     cblk_bytes = expert_code_bytes(blk_elems, 4);  // staging stride: no block is kept coded above it
     const char* f = std::getenv("SMO_CODEC");
     unary = !(f && std::strcmp(f, "fixed") == 0);
-    tmode = opt.compress_experts == 2 || (f && std::strcmp(f, "tile") == 0);
+    tmode = opt.compress_experts == 2 || opt.compress_experts == 3 || (f && std::strncmp(f, "tile", 4) == 0);
+    tfmt = (opt.compress_experts == 3 || (f && std::strcmp(f, "tile3") == 0)) ? 3 : 2;
     const bool tile_ok = h % 128 == 0 && hi % 128 == 0;
     if (tmode) SMO_REQUIRE(tile_ok, "engine: the tile code needs h and h_i multiples of 128");
     cenc = dalloc<uint8_t>(std::max(tile_ok ? tcode_max_bytes(h, hi) : size_t(0),
@@ -322,14 +324,27 @@ void Engine::create() {
       fill(stage + 2 * size_t(hi) * h, size_t(h) * hi, cfg.seed, base + 2, 0, std::sqrt(3.0f / hi), st);
       SMO_CUDA_CHECK(cudaStreamSynchronize(st));
       const size_t tb = tcode_encode(stage, h, hi, cenc, st);
+      const size_t t3b = tcode_encode(stage, h, hi, cenc, st, 3);
       expert_encode(stage, blk_elems, 1, cenc, d_ovf ? d_ovf : (d_ovf = dalloc<int>(1)), st);
       const size_t ub = expert_coded_size(cenc, blk_elems, 1);
-      // the tile code also when the hot cache holds every block in it: no
-      // block then crosses the link, the step is device-bound, and decoding
-      // inside the expert kernel skips the per-step expansion (config 2 with
-      // a 64 GB cache: 5391 vs 5049 verified tok/s)
-      const double all_tile = double(L) * double(owned.size()) * double((tb + 255) & ~size_t(255));
-      tmode = double(tb) < 0.99 * double(ub) || double(opt.expert_cache_bytes) >= all_tile;
+      // When the hot cache holds every block, no block crosses the link and
+      // the step is device-bound: a tile code decoded inside the expert
+      // kernel, T3 (fixed 3-bit exponents, the fastest decode) if every block
+      // fits in it, else T2 (profiles/r02h_t3.md). Otherwise the link binds:
+      // the smaller code (unary for uniform-init, T2 for gaussian-like).
+      auto all = [&](size_t per) {
+        return 1.005 * double(L) * double(owned.size()) * double((per + 255) & ~size_t(255));
+      };
+      const double cache = double(opt.expert_cache_bytes);
+      tmode = true;
+      if (cache >= all(t3b)) {
+        tfmt = 3;
+      } else if (cache >= all(tb)) {
+        tfmt = 2;
+      } else {
+        tmode = double(tb) < 0.99 * double(ub);
+        tfmt = 2;
+      }
     }
     if (!d_ovf) d_ovf = dalloc<int>(1);
     blk_coded.assign(size_t(host_alias) * E_loc, 0);
@@ -357,7 +372,7 @@ void Engine::create() {
       size_t ubytes = 0;
       if (tmode) {  // T2: always (lossless for any bits; raw tiles inside the code)
         SMO_CUDA_CHECK(cudaStreamSynchronize(st));
-        const size_t tb = tcode_encode(stage, h, hi, cenc, st);
+        const size_t tb = tcode_encode(stage, h, hi, cenc, st, tfmt);
         SMO_REQUIRE(tb <= blk_bytes, "engine: tile code of an expert block larger than its bf16 size");
         SMO_CUDA_CHECK(cudaMemcpy(hdst, cenc, tb, cudaMemcpyDeviceToHost));
         blk_coded[size_t(a) * E_loc + local(e)] = 2;
@@ -1570,7 +1585,7 @@ void Engine::times(smo_stage_times* t) {
   r.h2d_bytes = last_h2d_bytes;
   r.codec = span(step_dec_ev);
   r.codec_bytes = step_codec_bytes;
-  r.link_code = tmode ? 2.0 : xcomp ? 1.0 : 0.0;
+  r.link_code = tmode ? double(tfmt) : xcomp ? 1.0 : 0.0;
   bool bound = !host_numa_bytes.empty();
   for (size_t b : host_numa_bytes) bound = bound && b > 0;
   r.host_numa = bound ? double(host_numa) : -1.0;

@@ -82,11 +82,11 @@ void expert_encode(const void* src, size_t count, int bits, void* dst, int* over
 void expert_decode(const void* src, size_t count, int bits, void* dst, cudaStream_t st);
 void expert_decode_blocks(const void* const* srcs, void* const* dsts, int n, size_t count, int bits, cudaStream_t st);
 size_t tcode_max_bytes(int h, int hi);
-size_t tcode_encode(const void* src, int h, int hi, void* dst, cudaStream_t st);
-void tcode_decode(const void* const* srcs, void* const* dsts, int n, int h, int hi, cudaStream_t st);
+size_t tcode_encode(const void* src, int h, int hi, void* dst, cudaStream_t st, int fmt = 2);
+void tcode_decode(const void* const* srcs, void* const* dsts, int n, int h, int hi, cudaStream_t st, int fmt = 2);
 int moe_coded_launch(const void* x_perm, int rows, int h, int hi, int E, const int32_t* offsets,
                      const void* const* w_code, void* hbuf, float* y, int splits, int max_splits, int* done,
-                     cudaStream_t st);
+                     cudaStream_t st, int fmt = 2);
 
 // Procedural tensor ids; the oracle tests use the same ids.
 namespace tid {
@@ -241,6 +241,7 @@ struct Engine {
   // tile code, and K4-MoE decodes it in shared memory (moe_coded_launch):
   // no expansion launch, no bf16 copy of an expert in HBM
   bool tmode = false;
+  int tfmt = 2;  // the tile code: 2 (T2) or 3 (T3, fixed 3-bit exponents)
   const void** d_w_code = nullptr;      // [L*E] code block of (layer, expert)
   const void** d_w_code_loc = nullptr;  // [L*E_loc] (expert parallelism)
   size_t cblk_bytes = 0;                  // coded bytes of one [W1|W3|W2] block at 4 bits (staging stride)

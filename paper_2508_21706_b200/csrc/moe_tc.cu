@@ -347,7 +347,7 @@ __device__ __forceinline__ bool down_pair(const Unit& x, int KBd) {
   return x.down && x.cnt <= 128 && (KBd % 2) == 0;
 }
 
-template <int kND, int kAS, int kCS>
+template <int kND, int kAS, int kCS, int kFmt = 2>  // kFmt: the tile code, T2 or T3 (tcode.cuh)
 __global__ void __launch_bounds__(kThreads + 32 * kND, 1)
     moe_coded_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_h, MoeParams p,
                      const uint8_t* const* __restrict__ w_code) {
@@ -521,7 +521,10 @@ __global__ void __launch_bounds__(kThreads + 32 * kND, 1)
           // segment d % 8 of tile d / 8 (single-tile stages: warps 0..7)
 #pragma unroll 1
           for (int m = kND > 8 ? d / 8 : 0; m < ntile; m += kND > 8 ? 2 : 1)
-            tcode::decode_segment(code + m * kCodeSlot, st + m * kTileA, d % 8, lane, (p.dbg & 8) ? ~0xe00u : ~0u);
+            if constexpr (kFmt == 3)
+              tcode::decode_segment3(code + m * kCodeSlot, st + m * kTileA, d % 8, lane);
+            else
+              tcode::decode_segment(code + m * kCodeSlot, st + m * kTileA, d % 8, lane, (p.dbg & 8) ? ~0xe00u : ~0u);
         }
         fence_proxy_async();  // the stores above feed the tensor core (async proxy)
         __syncwarp();
@@ -658,7 +661,8 @@ int moe_launch(const void* x_perm, int rows, int h, int hi, int E, const int32_t
 // moe_launch on the decoded weights.
 int moe_coded_launch(const void* x_perm, int rows, int h, int hi, int E, const int32_t* offsets,
                      const void* const* w_code, void* hbuf, float* y, int splits, int max_splits, int* done,
-                     cudaStream_t st) {
+                     cudaStream_t st, int fmt) {
+  SMO_REQUIRE(fmt == 2 || fmt == 3, "moe: tile code format must be 2 (T2) or 3 (T3)");
   SMO_REQUIRE(x_perm && offsets && w_code && hbuf && y && done, "moe: null pointer");
   SMO_REQUIRE(E >= 1 && E <= kMaxE, "moe: 1 <= n_expert <= 64");
   SMO_REQUIRE(h % 128 == 0 && hi % 128 == 0, "moe: h and h_i must be multiples of 128");
@@ -705,11 +709,16 @@ int moe_coded_launch(const void* x_perm, int rows, int h, int hi, int E, const i
     case 3: kern = moe_coded_kernel<8, 2, 3>, nd = 8, as = 2, cs = 3; break;
     default: kern = moe_coded_kernel<16, 2, 2>, nd = 16, as = 2, cs = 2; break;
   }
+  int slot = variant;
+  if (fmt == 3) {  // T3: 16 decoder warps, 2 A / 2 code stages
+    kern = moe_coded_kernel<16, 2, 2, 3>, nd = 16, as = 2, cs = 2;
+    slot = 4;
+  }
   const size_t smem = size_t(as) * (2 * kTileA + kTok * 128) + size_t(cs) * 2 * kCodeSlot + 1024;
-  static bool attr_set[4] = {false, false, false, false};
-  if (!attr_set[variant]) {
+  static bool attr_set[5] = {false, false, false, false, false};
+  if (!attr_set[slot]) {
     SMO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr_set[variant] = true;
+    attr_set[slot] = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(unsigned(sm_count()));

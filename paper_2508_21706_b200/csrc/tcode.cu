@@ -185,9 +185,119 @@ __global__ void __launch_bounds__(32 * kEncWarps) tcode_encode_kernel(const __gr
   }
 }
 
+// T3 encoder (format: tcode.cuh / tests/tcode3_ref.py), the same two passes:
+// pass 1 writes E | nesc << 9 per segment (0xffffffff: the segment forces a
+// raw tile — its maximum exponent is below 7 or it has > 1023 escapes), the
+// host lays out the escape lists and raw tiles, pass 2 writes the tiles.
+__global__ void __launch_bounds__(32 * kEncWarps) tcode3_encode_kernel(const __grid_constant__ TMats M, int segs,
+                                                                       uint32_t* __restrict__ meta,
+                                                                       uint8_t* __restrict__ dst, bool write) {
+  const int wib = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int g = blockIdx.x * kEncWarps + wib;
+  if (g >= segs) return;
+  const int t = g / kSegs, s = g % kSegs;
+  const TileAt ta = tile_at(M, t);
+  const int C = M.C[ta.m];
+  const int row = ta.nb * kTileRows + s * kSegRows + (lane >> 1);
+  const int col = ta.kb * kTileCols + 32 * (lane & 1);
+  const uint4* sp = reinterpret_cast<const uint4*>(M.src[ta.m] + size_t(row) * C + col);
+  uint32_t v2[16];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint4 u = sp[i];
+    v2[4 * i] = u.x;
+    v2[4 * i + 1] = u.y;
+    v2[4 * i + 2] = u.z;
+    v2[4 * i + 3] = u.w;
+  }
+  auto val = [&](int i) -> uint32_t { return (v2[i >> 1] >> (16 * (i & 1))) & 0xffffu; };
+  auto expo = [&](int i) -> int { return int((val(i) >> 7) & 0xffu); };
+  if (!write) {
+    int emax = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) emax = max(emax, expo(i));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+    int E = -1, best = -1;
+    for (int c = 0; c < 8; ++c) {
+      const int b0 = emax - c;
+      if (b0 < 7) break;  // warp-uniform
+      int n = 0;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int j = b0 - expo(i);
+        n += (j < 0 || j > 6) ? 1 : 0;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+      if (best < 0 || n < best) {
+        best = n;
+        E = b0;
+      }
+    }
+    if (lane == 0) meta[g] = (E < 0 || best > 1023) ? 0xffffffffu : (uint32_t(E) | (uint32_t(best) << 9));
+    return;
+  }
+  const uint32_t hw = meta[g];
+  uint8_t* tb = dst + reinterpret_cast<const uint32_t*>(dst)[t];
+  if (hw & 0x100u) {  // raw tile
+    uint4* d = reinterpret_cast<uint4*>(tb + 32 + 2 * kSeg * s) + 4 * lane;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) d[i] = make_uint4(v2[4 * i], v2[4 * i + 1], v2[4 * i + 2], v2[4 * i + 3]);
+    if (lane == 0) reinterpret_cast<uint32_t*>(tb)[s] = s == 0 ? 0x100u : 0u;
+    return;
+  }
+  if (lane == 0) reinterpret_cast<uint32_t*>(tb)[s] = hw;
+  const int E = int(hw & 0xffu), nesc = int((hw >> 9) & 0x7ffu);
+  uint32_t lo[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}, w[3] = {0u, 0u, 0u};
+  int ne = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const uint32_t x = val(i);
+    lo[i >> 2] |= (((x >> 8) & 0x80u) | (x & 0x7fu)) << (8 * (i & 3));
+    const int j = E - expo(i);
+    const bool esc = j < 0 || j > 6;
+    const uint32_t c = esc ? 7u : uint32_t(j);
+    ne += esc ? 1 : 0;
+    const int k = i >> 1, odd = i & 1;
+    if (k < 15) {
+      w[k / 5] |= c << (3 * (k % 5) + 16 * odd);
+    } else {
+#pragma unroll
+      for (int b = 0; b < 3; ++b) w[b] |= ((c >> b) & 1u) << (15 + 16 * odd);
+    }
+  }
+  reinterpret_cast<uint4*>(tb + kLoOff + kSeg * s)[2 * lane] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  reinterpret_cast<uint4*>(tb + kLoOff + kSeg * s)[2 * lane + 1] = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+  uint32_t* cwp = reinterpret_cast<uint32_t*>(tb + kC3Off + 384 * s) + 3 * lane;
+  cwp[0] = w[0];
+  cwp[1] = w[1];
+  cwp[2] = w[2];
+  // escape list: this lane's escapes at its rank, in value order
+  int tot = 0;
+  int f = warp_excl_scan(ne, lane, &tot);
+  uint8_t* el = tb + 4 * (hw >> 20);
+  for (int i = 0; i < 32; ++i) {
+    const int j = E - expo(i);
+    if (j < 0 || j > 6) {
+      reinterpret_cast<uint16_t*>(el)[f] = uint16_t(32 * lane + i);
+      el[2 * nesc + f] = uint8_t(expo(i));
+      ++f;
+    }
+  }
+  const int used = 3 * nesc, pad = ((used + 3) & ~3) - used;
+  if (lane < pad) el[used + lane] = 0;
+  if (s == kSegs - 1) {  // tile padding to 16 bytes
+    const uint8_t* end = el + used + pad;
+    const uint8_t* tend = dst + reinterpret_cast<const uint32_t*>(dst)[t + 1];
+    if (lane < int(tend - end)) const_cast<uint8_t*>(end)[lane] = 0;
+  }
+}
+
 // One CTA per tile: stage the tile code in shared memory, eight warps decode
 // one segment each into a swizzled tile (the expert kernel's decoder), then
 // the tile is written back row-major.
+template <int kFmt>
 __global__ void __launch_bounds__(256) tcode_decode_kernel(const __grid_constant__ TMats M,
                                                            const uint8_t* const* __restrict__ srcs,
                                                            uint16_t* const* __restrict__ dsts) {
@@ -202,7 +312,8 @@ __global__ void __launch_bounds__(256) tcode_decode_kernel(const __grid_constant
   for (uint32_t i = threadIdx.x; i < (o1 - o0) / 16; i += blockDim.x) reinterpret_cast<uint4*>(code)[i] = g[i];
   __syncthreads();
   const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
-  decode_segment(code, tile, w, lane);
+  if constexpr (kFmt == 3) decode_segment3(code, tile, w, lane);
+  else decode_segment(code, tile, w, lane);
   __syncthreads();
   const TileAt ta = tile_at(M, t);
   const int C = M.C[ta.m];
@@ -221,10 +332,11 @@ size_t tcode_max_bytes(int h, int hi) {
   return ((4 * (nt + 1) + 15) & ~size_t(15)) + nt * size_t(kTileMax);
 }
 
-// [W1 | W3 | W2] (bf16, device) -> T2 code at dst (device, >= tcode_max_bytes).
-// Synchronous on st (host scan of the tile sizes between the passes); returns
-// the code bytes.
-size_t tcode_encode(const void* src, int h, int hi, void* dst, cudaStream_t st) {
+// [W1 | W3 | W2] (bf16, device) -> T2 (fmt 2) or T3 (fmt 3) code at dst
+// (device, >= tcode_max_bytes). Synchronous on st (host scan of the tile
+// sizes between the passes); returns the code bytes.
+size_t tcode_encode(const void* src, int h, int hi, void* dst, cudaStream_t st, int fmt) {
+  SMO_REQUIRE(fmt == 2 || fmt == 3, "tcode: format must be 2 (T2) or 3 (T3)");
   SMO_REQUIRE(src && dst, "tcode: null pointer");
   SMO_REQUIRE(h % kTileRows == 0 && hi % kTileRows == 0 && h > 0 && hi > 0, "tcode: h and h_i must be multiples of 128");
   const TMats M = expert_mats(src, h, hi);
@@ -233,9 +345,13 @@ size_t tcode_encode(const void* src, int h, int hi, void* dst, cudaStream_t st) 
   SMO_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&meta), size_t(segs) * 4, st));
   auto d8 = reinterpret_cast<uint8_t*>(dst);
   const unsigned grid = unsigned((segs + kEncWarps - 1) / kEncWarps);
-  tcode_encode_kernel<<<grid, 32 * kEncWarps, 0, st>>>(M, segs, meta, d8, false);
-  count_launch();
-  SMO_CUDA_CHECK(cudaGetLastError());
+  auto pass = [&](bool write) {
+    if (fmt == 3) tcode3_encode_kernel<<<grid, 32 * kEncWarps, 0, st>>>(M, segs, meta, d8, write);
+    else tcode_encode_kernel<<<grid, 32 * kEncWarps, 0, st>>>(M, segs, meta, d8, write);
+    count_launch();
+    SMO_CUDA_CHECK(cudaGetLastError());
+  };
+  pass(false);
   std::vector<uint32_t> hm(static_cast<size_t>(segs));
   SMO_CUDA_CHECK(cudaMemcpyAsync(hm.data(), meta, hm.size() * 4, cudaMemcpyDeviceToHost, st));
   SMO_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -245,6 +361,29 @@ size_t tcode_encode(const void* src, int h, int hi, void* dst, cudaStream_t st) 
   for (int t = 0; t < nt; ++t) {
     head[size_t(t)] = uint32_t(off);
     uint32_t* mt = hm.data() + size_t(t) * kSegs;
+    if (fmt == 3) {  // escape lists after the codes; raw if a segment asks or nothing is saved
+      bool raw = false;
+      size_t sz = kEsc3Off;
+      for (int s = 0; s < kSegs; ++s) {
+        if (mt[s] == 0xffffffffu) raw = true;
+        else sz += (3 * size_t((mt[s] >> 9) & 0x7ffu) + 3) & ~size_t(3);
+      }
+      const size_t end = sz;
+      sz = (sz + 15) & ~size_t(15);
+      if (raw || sz >= size_t(kTileMax) || end / 4 >= 4096) {
+        for (int s = 0; s < kSegs; ++s) mt[s] = 0x100u;
+        sz = kTileMax;
+      } else {
+        uint32_t eo = kEsc3Off;
+        for (int s = 0; s < kSegs; ++s) {
+          const uint32_t n = (mt[s] >> 9) & 0x7ffu;
+          mt[s] = (mt[s] & 0xfffffu) | ((eo / 4) << 20);
+          eo += (3 * n + 3) & ~3u;
+        }
+      }
+      off += sz;
+      continue;
+    }
     size_t sz = kStreamOff;
     for (int s = 0; s < kSegs; ++s) sz += 4 * size_t(mt[s] >> 12);
     sz = (sz + 15) & ~size_t(15);
@@ -265,9 +404,7 @@ size_t tcode_encode(const void* src, int h, int hi, void* dst, cudaStream_t st) 
   head[size_t(nt)] = uint32_t(off);
   SMO_CUDA_CHECK(cudaMemcpyAsync(d8, head.data(), tb, cudaMemcpyHostToDevice, st));
   SMO_CUDA_CHECK(cudaMemcpyAsync(meta, hm.data(), hm.size() * 4, cudaMemcpyHostToDevice, st));
-  tcode_encode_kernel<<<grid, 32 * kEncWarps, 0, st>>>(M, segs, meta, d8, true);
-  count_launch();
-  SMO_CUDA_CHECK(cudaGetLastError());
+  pass(true);
   SMO_CUDA_CHECK(cudaFreeAsync(meta, st));
   SMO_CUDA_CHECK(cudaStreamSynchronize(st));
   return off;
@@ -281,8 +418,9 @@ size_t tcode_size(const void* code, int h, int hi) {
   return v;
 }
 
-// n T2 blocks -> bf16 [W1 | W3 | W2] blocks, one launch.
-void tcode_decode(const void* const* srcs, void* const* dsts, int n, int h, int hi, cudaStream_t st) {
+// n T2 / T3 blocks -> bf16 [W1 | W3 | W2] blocks, one launch.
+void tcode_decode(const void* const* srcs, void* const* dsts, int n, int h, int hi, cudaStream_t st, int fmt) {
+  SMO_REQUIRE(fmt == 2 || fmt == 3, "tcode: format must be 2 (T2) or 3 (T3)");
   SMO_REQUIRE(n >= 0 && n <= 64, "tcode: up to 64 blocks per launch");
   SMO_REQUIRE(h % kTileRows == 0 && hi % kTileRows == 0 && h > 0 && hi > 0, "tcode: h and h_i must be multiples of 128");
   if (!n) return;
@@ -300,11 +438,17 @@ void tcode_decode(const void* const* srcs, void* const* dsts, int n, int h, int 
   const size_t smem = 1024 + kTileRows * 128 + kTileMax;
   static bool attr = false;
   if (!attr) {
-    SMO_CUDA_CHECK(cudaFuncSetAttribute(tcode_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    SMO_CUDA_CHECK(cudaFuncSetAttribute(tcode_decode_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    SMO_CUDA_CHECK(cudaFuncSetAttribute(tcode_decode_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr = true;
   }
-  tcode_decode_kernel<<<dim3(unsigned(M.t0[3]), unsigned(n)), 256, smem, st>>>(
-      M, reinterpret_cast<const uint8_t* const*>(tab), reinterpret_cast<uint16_t* const*>(tab + n));
+  const dim3 grid(unsigned(M.t0[3]), unsigned(n));
+  if (fmt == 3)
+    tcode_decode_kernel<3><<<grid, 256, smem, st>>>(M, reinterpret_cast<const uint8_t* const*>(tab),
+                                                     reinterpret_cast<uint16_t* const*>(tab + n));
+  else
+    tcode_decode_kernel<2><<<grid, 256, smem, st>>>(M, reinterpret_cast<const uint8_t* const*>(tab),
+                                                     reinterpret_cast<uint16_t* const*>(tab + n));
   count_launch();
   SMO_CUDA_CHECK(cudaGetLastError());
   // the host vector must outlive the async copy

@@ -46,6 +46,11 @@ constexpr int kLoOff = 32;                        // lo[8][1024] after the heade
 constexpr int kL1Off = kLoOff + kSegs * kSeg;     // L1[8][256]
 constexpr int kStreamOff = kL1Off + kSegs * 256;  // 10272: first segment stream
 constexpr int kTileMax = 32 + 2 * kTileRows * kTileCols;  // 16416: a raw tile, the largest
+// T3 (tests/tcode3_ref.py): hdr[8] = E | nesc << 9 | eoff4 << 20 (bit 8 of
+// hdr[0]: raw tile), lo[8][1024], 3-bit codes C3[8][32 lanes][3 words], per
+// segment an escape list (u16 positions, then u8 exponents, padded to 4 B)
+constexpr int kC3Off = kLoOff + kSegs * kSeg;     // 8224
+constexpr int kEsc3Off = kC3Off + kSegs * 384;    // 11296: first escape list
 
 __device__ __forceinline__ int warp_excl_scan(int v, int lane, int* total) {
   int x = v;
@@ -178,6 +183,68 @@ __device__ __forceinline__ void decode_segment(const uint8_t* __restrict__ tc, u
   int totl = 0;
   int f = warp_excl_scan(__popc(ml), lane, &totl);
   for (uint32_t mm = ml; mm; mm &= mm - 1u) put(__ffs(mm) - 1, lit[f++]);
+}
+
+// T3: decode segment s into the swizzled tile (one warp). Every value is a
+// fixed 3-bit code j = E - e (7: escape); pair k < 15 of lane L sits at bits
+// 3 (k % 5) (even) and 16 + 3 (k % 5) (odd) of word k / 5, so one shift and
+// mask place both codes under the bf16 pair's exponent fields (E >= 7: no
+// borrow) — five integer ops per pair and no per-lane loop. The escapes
+// (code 7) are rewritten afterwards from the segment's (position, exponent)
+// list, the warp's lanes taking consecutive entries.
+__device__ __forceinline__ void decode_segment3(const uint8_t* __restrict__ tc, uint8_t* tile, int s, int lane) {
+  const int r = kSegRows * s + (lane >> 1);
+  const int half = lane & 1;
+  uint8_t* rowp = tile + r * 128;
+  const int x = r & 7;
+  const uint32_t* hdr = reinterpret_cast<const uint32_t*>(tc);
+  if (hdr[0] & 0x100u) {  // raw tile: lane L's 64 bytes are its half-row
+    const uint4* src = reinterpret_cast<const uint4*>(tc + 32 + 2 * kSeg * s) + 4 * lane;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) *reinterpret_cast<uint4*>(rowp + (((4 * half + k) ^ x) << 4)) = src[k];
+    return;
+  }
+  const uint32_t hw = hdr[s];
+  const uint32_t E = hw & 0xffu;
+  const uint8_t* lob = tc + kLoOff + kSeg * s;
+  const uint4 lo0 = reinterpret_cast<const uint4*>(lob)[2 * lane];
+  const uint4 lo1 = reinterpret_cast<const uint4*>(lob)[2 * lane + 1];
+  const uint32_t* cw = reinterpret_cast<const uint32_t*>(tc + kC3Off + 384 * s) + 3 * lane;
+  const uint32_t w0 = cw[0], w1 = cw[1], w2 = cw[2];
+  const uint32_t lw[8] = {lo0.x, lo0.y, lo0.z, lo0.w, lo1.x, lo1.y, lo1.z, lo1.w};
+  const uint32_t e2 = (E << 7) | (E << 23);
+  uint32_t out[16];
+#pragma unroll
+  for (int k = 0; k < 15; ++k) {
+    const int j = k % 5;
+    const uint32_t w = k < 5 ? w0 : k < 10 ? w1 : w2;
+    const uint32_t cc = (3 * j <= 7 ? (w << (7 - 3 * j)) : (w >> (3 * j - 7))) & 0x03800380u;
+    const uint32_t t = __byte_perm(lw[k >> 1], 0u, (k & 1) ? 0xB3A2u : 0x9180u);
+    out[k] = (t & 0x807F807Fu) | (e2 - cc);
+  }
+  {  // pair 15: code bit b of the even / odd value at bit 15 / 31 of word b
+    const uint32_t ce = ((w0 >> 15) & 1u) | ((w1 >> 14) & 2u) | ((w2 >> 13) & 4u);
+    const uint32_t co = (w0 >> 31) | ((w1 >> 30) & 2u) | ((w2 >> 29) & 4u);
+    const uint32_t t = __byte_perm(lw[7], 0u, 0xB3A2u);
+    out[15] = (t & 0x807F807Fu) | (e2 - ((ce << 7) | (co << 23)));
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    *reinterpret_cast<uint4*>(rowp + (((4 * half + k) ^ x) << 4)) =
+        make_uint4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
+  const int nesc = int((hw >> 9) & 0x7ffu);
+  if (nesc) {  // warp-uniform
+    __syncwarp();  // the escape's row may belong to another lane's stores
+    const uint8_t* el = tc + 4 * (hw >> 20);
+    for (int q = lane; q < nesc; q += 32) {
+      const int pos = reinterpret_cast<const uint16_t*>(el)[q];
+      const uint32_t e = el[2 * nesc + q];
+      const int r2 = kSegRows * s + (pos >> 6), c = pos & 63;
+      const uint32_t lo = lob[pos];
+      *reinterpret_cast<uint16_t*>(tile + r2 * 128 + ((((c >> 3) ^ (r2 & 7)) << 4) | ((c & 7) << 1))) =
+          uint16_t(((lo & 0x80u) << 8) | (e << 7) | (lo & 0x7fu));
+    }
+  }
 }
 
 }  // namespace tcode

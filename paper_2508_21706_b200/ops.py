@@ -129,9 +129,10 @@ def moe_experts(x_perm, offsets, pool, *, h: int, h_i: int, n_expert: int, w_blo
     return hout, y[:used.value]
 
 
-def moe_experts_coded(x_perm, offsets, w_code, *, h: int, h_i: int, n_expert: int, splits: int = 0):
-    """K4-MoE on T2-coded experts: w_code = int64 device tensor [E] of code
-    block addresses (tcode_encode outputs). Same returns as moe_experts."""
+def moe_experts_coded(x_perm, offsets, w_code, *, h: int, h_i: int, n_expert: int, splits: int = 0, fmt: int = 2):
+    """K4-MoE on tile-coded experts (fmt 2: T2, 3: T3): w_code = int64 device
+    tensor [E] of code block addresses (tcode_encode outputs of that format).
+    Same returns as moe_experts."""
     _req(x_perm, _BF16, "x_perm")
     rows = x_perm.shape[0]
     dev = x_perm.device
@@ -139,26 +140,30 @@ def moe_experts_coded(x_perm, offsets, w_code, *, h: int, h_i: int, n_expert: in
     y = torch.empty((splits or 4, rows, h), dtype=torch.float32, device=dev)
     scratch = torch.zeros(80, dtype=torch.int32, device=dev)
     used = C.c_int32(0)
-    L.check(L.load().smo_moe_experts_coded(_p(x_perm), rows, h, h_i, n_expert, _p(offsets), _p(w_code), _p(hout),
-                                           _p(y), splits, C.byref(used), _p(scratch), _stream()))
+    fn = L.load().smo_moe_experts_coded3 if fmt == 3 else L.load().smo_moe_experts_coded
+    L.check(fn(_p(x_perm), rows, h, h_i, n_expert, _p(offsets), _p(w_code), _p(hout), _p(y), splits, C.byref(used),
+               _p(scratch), _stream()))
     return hout, y[:used.value]
 
 
-def tcode_encode(block, h: int, h_i: int):
-    """T2 tile code of one expert block [W1 | W3 | W2] (bf16, device):
-    uint8 device tensor trimmed to the bytes used (16-B aligned storage)."""
+def tcode_encode(block, h: int, h_i: int, fmt: int = 2):
+    """T2 (fmt 2) or T3 (fmt 3) tile code of one expert block [W1 | W3 | W2]
+    (bf16, device): uint8 device tensor trimmed to the bytes used (16-B
+    aligned storage)."""
     _req(block, _BF16, "block")
-    assert block.numel() == 3 * h * h_i
+    assert block.numel() == 3 * h * h_i and fmt in (2, 3)
     code = torch.empty(int(L.load().smo_tcode_max_bytes(h, h_i)), dtype=torch.uint8, device=block.device)
     n = C.c_uint64(0)
-    L.check(L.load().smo_tcode_encode(_p(block), h, h_i, _p(code), C.byref(n), _stream()))
+    fn = L.load().smo_tcode3_encode if fmt == 3 else L.load().smo_tcode_encode
+    L.check(fn(_p(block), h, h_i, _p(code), C.byref(n), _stream()))
     return code[:n.value]
 
 
-def tcode_decode(code, h: int, h_i: int):
+def tcode_decode(code, h: int, h_i: int, fmt: int = 2):
     """Inverse of tcode_encode: the bf16 block [W1 | W3 | W2] (3 h h_i values)."""
     out = torch.empty(3 * h * h_i, dtype=_BF16, device=code.device)
-    L.check(L.load().smo_tcode_decode(_p(code), h, h_i, _p(out), _stream()))
+    fn = L.load().smo_tcode3_decode if fmt == 3 else L.load().smo_tcode_decode
+    L.check(fn(_p(code), h, h_i, _p(out), _stream()))
     return out
 
 

@@ -315,8 +315,8 @@ def test_compressed_expert_stream_bit_identical(cuda, batch_one, codec, monkeypa
 
 @pytest.mark.parametrize("kind", ["tiny", "tiny_fg", "tiny_gauss"])
 def test_tile_code_engine_bit_identical(cuda, kind, monkeypatch):
-    """compress_experts = 2: every expert block streams and is hot-cached in
-    the T2 tile code and K4-MoE decodes it in shared memory — no expansion
+    """compress_experts = 2 / 3: every expert block streams and is hot-cached in
+    the T2 / T3 tile code and K4-MoE decodes it in shared memory — no expansion
     launch, no bf16 expert in HBM. Two steps (the slots cycle) with a hot
     cache: bit-identical to raw bf16 streaming."""
     from paper_2508_21706_b200.engine import VerifyEngine
@@ -326,18 +326,19 @@ def test_tile_code_engine_bit_identical(cuda, kind, monkeypatch):
     rng = np.random.default_rng(10)
     toks = [rng.integers(0, s.vocab, size=(b, n)).astype(np.int32) for _ in range(2)]
     out = {}
-    for comp in (0, 2):
+    for comp in (0, 2, 3):  # raw, T2, T3
         eng = VerifyEngine(s, max_batch=b, max_verify=n, max_seq=512, compress_experts=comp,
                            expert_cache_bytes=3 * s.expert_bytes if comp else 0)
         eng.fill_prefix(prefix)
         out[comp] = ([eng.verify(t, prefix) for t in toks], eng.last_times())
         eng.close()
-    for r0, r1 in zip(out[0][0], out[2][0]):
-        assert np.array_equal(r0.target, r1.target)
-        assert np.array_equal(r0.acc_len, r1.acc_len) and np.array_equal(r0.bonus, r1.bonus)
-    t2 = out[2][1]
-    assert t2["codec"] == 0.0  # nothing expanded
-    assert 0 < t2["h2d_bytes"] < t2["h2d_raw_bytes"] * 11.5 / 16
+    for comp in (2, 3):
+        for r0, r1 in zip(out[0][0], out[comp][0]):
+            assert np.array_equal(r0.target, r1.target)
+            assert np.array_equal(r0.acc_len, r1.acc_len) and np.array_equal(r0.bonus, r1.bonus)
+        t2 = out[comp][1]
+        assert t2["codec"] == 0.0 and t2["link_code"] == comp  # nothing expanded
+        assert 0 < t2["h2d_bytes"] < t2["h2d_raw_bytes"] * (11.5 if comp == 2 else 12.0) / 16
 
 
 @pytest.mark.parametrize("batch_one", [False, True])

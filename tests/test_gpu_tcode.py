@@ -78,12 +78,12 @@ def test_tcode_full_mixtral_block(cuda):
         assert np.array_equal(tile, W[nb * 128:(nb + 1) * 128, kb * 64:(kb + 1) * 64]), t
 
 
-def _coded_vs_plain(torch, cuda, h, hi, E, rows_per, kind, splits=0):
+def _coded_vs_plain(torch, cuda, h, hi, E, rows_per, kind, splits=0, fmt=2):
     from paper_2508_21706_b200 import ops
     g = torch.Generator(device=cuda).manual_seed(7)
     blks = [_block(torch, cuda, kind, h, hi, base=2000 + 3 * e) for e in range(E)]
     pool = torch.cat(blks)
-    codes = [ops.tcode_encode(b, h, hi) for b in blks]
+    codes = [ops.tcode_encode(b, h, hi, fmt=fmt) for b in blks]
     w_code = torch.tensor([c.data_ptr() for c in codes], dtype=torch.int64, device=cuda)
     counts = torch.tensor(rows_per, dtype=torch.int32)
     off = torch.zeros(E + 1, dtype=torch.int32)
@@ -94,7 +94,7 @@ def _coded_vs_plain(torch, cuda, h, hi, E, rows_per, kind, splits=0):
     blk = 3 * h * hi
     h0, y0 = ops.moe_experts(x, off, pool, h=h, h_i=hi, n_expert=E, w_block_stride=blk * 2, w_pool_blocks=E,
                              splits=splits)
-    h1, y1 = ops.moe_experts_coded(x, off, w_code, h=h, h_i=hi, n_expert=E, splits=splits)
+    h1, y1 = ops.moe_experts_coded(x, off, w_code, h=h, h_i=hi, n_expert=E, splits=splits, fmt=fmt)
     torch.cuda.synchronize()
     assert y0.shape == y1.shape
     assert torch.equal(h0.view(torch.int16), h1.view(torch.int16))
@@ -130,3 +130,48 @@ def test_moe_coded_bit_identical_mixtral_dims(cuda):
     import torch
     rows = [70, 75, 68, 80, 71, 69, 72, 71]
     _coded_vs_plain(torch, cuda, 4096, 14336, 8, rows, "uniform")
+
+
+# ---------------------------------------------------------------- T3
+import tcode3_ref as T3  # noqa: E402
+
+
+@pytest.mark.parametrize("kind", ["uniform", "gaussian", "wide"])
+def test_tcode3_gpu_encoder_matches_numpy(cuda, kind):
+    """T3: the GPU encoder writes exactly the numpy restatement's bytes
+    (tests/tcode3_ref.py) and the GPU decoder inverts it bit for bit."""
+    import torch
+    from paper_2508_21706_b200 import ops
+    h, hi = 256, 384
+    blk = _block(torch, cuda, kind, h, hi)
+    code = ops.tcode_encode(blk, h, hi, fmt=3)
+    ref = T3.encode_expert(_u16(torch, blk), h, hi)
+    assert code.numel() == len(ref)
+    assert bytes(code.cpu().numpy().tobytes()) == ref
+    out = ops.tcode_decode(code, h, hi, fmt=3)
+    assert torch.equal(out.view(torch.int16), blk.view(torch.int16))
+
+
+def test_tcode3_full_mixtral_block(cuda):
+    """A whole Mixtral expert block through T3: bit-exact, ~11.2 bits/weight."""
+    import torch
+    from paper_2508_21706_b200 import ops
+    h, hi = 4096, 14336
+    blk = _block(torch, cuda, "uniform", h, hi, base=1100)
+    code = ops.tcode_encode(blk, h, hi, fmt=3)
+    bpw = code.numel() * 8 / blk.numel()
+    assert 11.0 < bpw < 11.4, bpw
+    out = ops.tcode_decode(code, h, hi, fmt=3)
+    assert torch.equal(out.view(torch.int16), blk.view(torch.int16))
+
+
+@pytest.mark.parametrize("kind", ["uniform", "gaussian", "wide"])
+def test_moe_coded3_bit_identical_small(cuda, kind):
+    import torch
+    _coded_vs_plain(torch, cuda, 512, 768, 6, [5, 0, 33, 130, 1, 64], kind, fmt=3)
+
+
+def test_moe_coded3_bit_identical_mixtral_dims(cuda):
+    import torch
+    rows = [70, 75, 68, 80, 71, 69, 72, 71]
+    _coded_vs_plain(torch, cuda, 4096, 14336, 8, rows, "uniform", fmt=3)

@@ -90,3 +90,51 @@ def test_tcode_base_choice_prefers_fewer_bits():
     s[5] = 0x4280  # 64.0
     E, bits = T.choose_base(((s.astype(np.int64) >> 7) & 0xFF))
     assert E == 129 and bits == 2 * 1023 + 16
+
+
+# ---------------------------------------------------------------- T3
+import tcode3_ref as T3  # noqa: E402
+
+
+@pytest.mark.parametrize("kind", ["uniform", "gaussian", "wide"])
+def test_tcode3_round_trip(kind):
+    h, hi = 256, 128
+    x = _mats(kind, h, hi)
+    code = T3.encode_expert(x, h, hi)
+    assert len(code) <= T.max_bytes(h, hi)
+    assert np.array_equal(T3.decode_expert(code, h, hi), x)
+    bpw = 8 * len(code) / x.size
+    if kind == "uniform":
+        assert 11.0 < bpw < 11.4, bpw  # 8 + 3 + escapes (~1/128 x 24 bits) + headers
+
+
+def test_tcode3_known_answers():
+    # every value 1.0: E = 127, codes 0, no escapes: 32 + 8192 + 3072 = 11296 bytes
+    W = np.full((128, 64), 0x3F80, np.uint16)
+    code = T3.encode([W])
+    assert np.frombuffer(code[:16], "<u4")[1] == len(code) == 16 + 11296
+    assert np.all(np.frombuffer(code[16:48], "<u4") == (127 | ((11296 // 4) << 20)))
+    # segment 0: value 3 halved (j = 1), value 30 at 2^-6 (j = 6, pair 15 even),
+    # value 33 at 2^-7 (j = 7: escape, lane 1 pair 0 odd)
+    s = np.full(1024, 0x3F80, np.uint16)
+    s[3], s[30], s[33] = 0x3F00, 0x3C80, 0x3C00
+    code = T3.encode([_segment_tile(s)])
+    hdr = np.frombuffer(code[16:48], "<u4")
+    assert hdr[0] == 127 | (1 << 9) | ((11296 // 4) << 20) and hdr[1] == 127 | ((11300 // 4) << 20)
+    c3 = np.frombuffer(code[16 + 8224:16 + 8224 + 384], "<u4")
+    # lane 0: pair 1 (values 2, 3) odd code 1 at bits 16 + 3; pair 15 even code 6 = 0b110: bits 15 of words 1, 2
+    assert c3[0] == 1 << 19 and c3[1] == 1 << 15 and c3[2] == 1 << 15
+    assert c3[3] == 7 << 16  # lane 1, pair 0 odd: the escape code
+    assert np.frombuffer(code[16 + 11296:16 + 11298], "<u2")[0] == 33 and code[16 + 11298] == 120
+    assert np.array_equal(T3.decode(code, [(128, 64)])[0], _segment_tile(s))
+    # an exact zero: the segment maximum stays the base, the zero escapes
+    z = np.full(1024, 0x3F80, np.uint16)
+    z[0] = 0
+    code = T3.encode([_segment_tile(z)])
+    assert (int(np.frombuffer(code[16:20], "<u4")[0]) >> 9) & 0x7FF == 1
+    assert np.array_equal(T3.decode(code, [(128, 64)])[0], _segment_tile(z))
+    # a segment whose maximum exponent is below 7 (near-zero values) -> raw tile
+    t = np.full(1024, 0x0080, np.uint16)  # exponent 1
+    code = T3.encode([_segment_tile(t)])
+    assert np.frombuffer(code[16:48], "<u4").tolist() == [1 << 8] + [0] * 7
+    assert np.array_equal(T3.decode(code, [(128, 64)])[0], _segment_tile(t))

@@ -159,6 +159,8 @@ def moe_coded(T=288, h=4096, hi=14336, E=8, k=2, dist="uniform"):
         fill(b[hi * h:2 * hi * h], 0x5EED, 1101 + 3 * e, math.sqrt(3.0 / h))
         fill(b[2 * hi * h:], 0x5EED, 1102 + 3 * e, math.sqrt(3.0 / hi))
     codes = [ops.tcode_encode(pool[e * blk:(e + 1) * blk], h, hi) for e in range(E)]
+    codes3 = [ops.tcode_encode(pool[e * blk:(e + 1) * blk], h, hi, fmt=3) for e in range(E)]
+    w_code3 = torch.tensor([c.data_ptr() for c in codes3], dtype=torch.int64, device=dev)
     ucodes = [ops.expert_encode(pool[e * blk:(e + 1) * blk], 1)[0] for e in range(E)]
     w_code = torch.tensor([c.data_ptr() for c in codes], dtype=torch.int64, device=dev)
     ids = torch.stack([torch.randperm(E, generator=g, device=dev)[:k] for _ in range(T)]).to(torch.int32)
@@ -178,16 +180,22 @@ def moe_coded(T=288, h=4096, hi=14336, E=8, k=2, dist="uniform"):
         L.check(L.load().smo_moe_experts_coded(xp.data_ptr(), T * k, h, hi, E, off.data_ptr(), w_code.data_ptr(),
                                                hbuf.data_ptr(), y4.data_ptr(), 0, None, scratch.data_ptr(), st()))
 
+    def coded3():
+        L.check(L.load().smo_moe_experts_coded3(xp.data_ptr(), T * k, h, hi, E, off.data_ptr(), w_code3.data_ptr(),
+                                                hbuf.data_ptr(), y4.data_ptr(), 0, None, scratch.data_ptr(), st()))
+
     def unary_then_plain():
         for e in range(E):
             L.check(L.load().smo_expert_decode(ucodes[e].data_ptr(), blk, 1, pool[e * blk:].data_ptr(), st()))
         plain()
     cb = sum(c.numel() for c in codes)
+    cb3 = sum(c.numel() for c in codes3)
     ub = sum(c.numel() for c in ucodes)
     act = T * k * h * 2 * 2 + T * k * hi * 2 * 2 + T * k * h * 4  # x rows (gate/up), H write + read, y
     r = []
     for nm, fn, byts, wb in (("bf16 weights", plain, E * blk * 2, E * blk * 2),
                              ("T2-coded weights, decoded in smem", coded, cb, cb),
+                             ("T3-coded weights, decoded in smem", coded3, cb3, cb3),
                              ("unary expansion (8 launches) + bf16 kernel", unary_then_plain, ub + 2 * E * blk * 2, ub)):
         t = timeit(fn)
         r.append({"kernel": f"K4-MoE {nm}", "dist": dist, "T": T, "E": E, "us": t * 1e6,
