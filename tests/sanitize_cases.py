@@ -77,7 +77,7 @@ def case_moe():
 
 
 def case_coded():
-    """T2 tile code: GPU encoder + decoder round trip, and K4-MoE decoding it in
+    """T2 / T3 tile codes: GPU encoder + decoder round trip, and K4-MoE decoding them in
     shared memory (bulk copies into a code ring, 16 decoder warps,
     fence.proxy.async + mbarriers, paired down stages) on ragged groups."""
     from paper_2508_21706_b200 import ops
@@ -100,6 +100,12 @@ def case_coded():
     h0, y0 = ops.moe_experts(xp, off, torch.cat(blks), h=h, h_i=hi, n_expert=E, w_block_stride=blk * 2,
                              w_pool_blocks=E, splits=y1.shape[0])
     assert torch.equal(y0.view(torch.int32), y1.view(torch.int32))
+    # T3: encoder + decoder, and K4-MoE decoding it (escape lists patched after a __syncwarp)
+    codes3 = [ops.tcode_encode(b, h, hi, fmt=3) for b in blks]
+    assert torch.equal(ops.tcode_decode(codes3[1], h, hi, fmt=3).view(torch.int16), blks[1].view(torch.int16))
+    w_code3 = torch.tensor([c.data_ptr() for c in codes3], dtype=torch.int64, device=dev)
+    h3, y3 = ops.moe_experts_coded(xp, off, w_code3, h=h, h_i=hi, n_expert=E, fmt=3)
+    assert torch.equal(y0.view(torch.int32), y3.view(torch.int32))
     torch.cuda.synchronize()
 
 
