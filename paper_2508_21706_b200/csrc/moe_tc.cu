@@ -710,12 +710,13 @@ int moe_coded_launch(const void* x_perm, int rows, int h, int hi, int E, const i
     default: kern = moe_coded_kernel<16, 2, 2>, nd = 16, as = 2, cs = 2; break;
   }
   int slot = variant;
-  if (fmt == 3) {  // T3: 16 decoder warps, 2 A / 2 code stages
-    kern = moe_coded_kernel<16, 2, 2, 3>, nd = 16, as = 2, cs = 2;
-    slot = 4;
+  if (fmt == 3) {  // T3: 16 decoder warps, 2 A / 2 code stages (SMO_MOE_CODED=8,2,2: 8 decoder warps)
+    if (variant == 1) kern = moe_coded_kernel<8, 2, 2, 3>, nd = 8, as = 2, cs = 2;
+    else kern = moe_coded_kernel<16, 2, 2, 3>, nd = 16, as = 2, cs = 2;
+    slot = variant == 1 ? 5 : 4;
   }
   const size_t smem = size_t(as) * (2 * kTileA + kTok * 128) + size_t(cs) * 2 * kCodeSlot + 1024;
-  static bool attr_set[5] = {false, false, false, false, false};
+  static bool attr_set[6] = {false, false, false, false, false, false};
   if (!attr_set[slot]) {
     SMO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr_set[slot] = true;
