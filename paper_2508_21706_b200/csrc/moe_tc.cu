@@ -347,16 +347,20 @@ __device__ __forceinline__ bool down_pair(const Unit& x, int KBd) {
   return x.down && x.cnt <= 128 && (KBd % 2) == 0;
 }
 
-template <int kND, int kAS, int kCS, int kFmt = 2>  // kFmt: the tile code, T2 or T3 (tcode.cuh)
-__global__ void __launch_bounds__(kThreads + 32 * kND, 1)
+// kTS: stages of the token-row ring, fed by its own TMA warp (w6) so the
+// token loads run kTS stages ahead of the MMA instead of waiting for the
+// decoded weight stage to be released (decoder warps are w7..).
+template <int kND, int kAS, int kCS, int kFmt = 2, int kTS = 2>  // kFmt: the tile code, T2 or T3 (tcode.cuh)
+__global__ void __launch_bounds__(kThreads + 32 + 32 * kND, 1)
     moe_coded_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_h, MoeParams p,
                      const uint8_t* const* __restrict__ w_code) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr int kXBytes = kTok * 128;
-  constexpr int kAStage = 2 * kTileA + kXBytes;  // W1 (or W2) | W3 | token rows
-  uint8_t* cring = smem + kAS * kAStage;         // kCS x (2 tile codes)
-  __shared__ __align__(8) uint64_t a_full[kAS], a_empty[kAS], c_full[kCS], c_empty[kCS];
+  constexpr int kAStage = 2 * kTileA;            // W1 (or W2) | W3, decoded
+  uint8_t* tring = smem + kAS * kAStage;         // kTS x token rows
+  uint8_t* cring = tring + kTS * kXBytes;        // kCS x (2 tile codes)
+  __shared__ __align__(8) uint64_t a_full[kAS], a_empty[kAS], c_full[kCS], c_empty[kCS], t_full[kTS], t_empty[kTS];
   __shared__ __align__(8) uint64_t tmem_full, tmem_empty;
   __shared__ uint32_t tmem_base_sh;
   __shared__ Schedule S;
@@ -365,8 +369,12 @@ __global__ void __launch_bounds__(kThreads + 32 * kND, 1)
   if (threadIdx.x == 0) {
     init_schedule(S, p, kTok);
     for (int s = 0; s < kAS; ++s) {
-      mbar_init(&a_full[s], kND + 1);  // kND decoder warps + decoder 0's expect_tx for the token rows
+      mbar_init(&a_full[s], kND);  // the kND decoder warps
       mbar_init(&a_empty[s], 1);
+    }
+    for (int s = 0; s < kTS; ++s) {
+      mbar_init(&t_full[s], 1);  // the token warp's expect_tx
+      mbar_init(&t_empty[s], 1);
     }
     for (int s = 0; s < kCS; ++s) {
       mbar_init(&c_full[s], 1);
@@ -450,14 +458,16 @@ __global__ void __launch_bounds__(kThreads + 32 * kND, 1)
         mbar_wait(&tmem_empty, (it & 1) ^ 1);
         tc_fence_after();
         for (int kb = 0; kb < KS; ++kb, ++g) {
-          const int s = g % kAS;
+          const int s = g % kAS, ts = g % kTS;
+          mbar_wait(&t_full[ts], (g / kTS) & 1);
           mbar_wait(&a_full[s], (g / kAS) & 1);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + s * kAStage);
+          const uint32_t t_addr = smem_u32(tring + ts * kXBytes);
           const uint64_t ad = make_sdesc_sw128(a_addr, 16, 1024);
           const uint64_t au = make_sdesc_sw128(a_addr + kTileA, 16, 1024);
-          const uint64_t bd = make_sdesc_sw128(a_addr + 2 * kTileA, 16, 1024);
-          const uint64_t bd2 = make_sdesc_sw128(a_addr + 2 * kTileA + xb, 16, 1024);
+          const uint64_t bd = make_sdesc_sw128(t_addr, 16, 1024);
+          const uint64_t bd2 = make_sdesc_sw128(t_addr + xb, 16, 1024);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
@@ -473,6 +483,7 @@ __global__ void __launch_bounds__(kThreads + 32 * kND, 1)
             }
           }
           umma_commit(&a_empty[s]);
+          umma_commit(&t_empty[ts]);
         }
         umma_commit(&tmem_full);
       }
@@ -480,40 +491,55 @@ __global__ void __launch_bounds__(kThreads + 32 * kND, 1)
   } else if (warp < 6) {
     // ------------------------------------------------------------ epilogue
     epilogue_loop<(kND > 8 ? 16 : 32)>(S, p, tmem, warp, lane, tmem_full, tmem_empty);
+  } else if (warp == 6) {
+    // ------------------------------------------------------------ token rows
+    // x rows (gate/up units) or H rows (down units, after every gate/up unit
+    // of the expert published them) of each stage's k-block(s), kTS stages ahead
+    if (lane == 0) {
+      int g = 0;
+      for (int u = blockIdx.x; u < S.total; u += gridDim.x) {
+        const Unit x = unit_at(S, u);
+        const int n_load = (x.cnt + 31) & ~31;
+        const bool pair = down_pair(x, KBd);
+        const int KS = x.down ? (pair ? KBd / 2 : KBd) : KBa;
+        const int kb0 = x.down ? x.ks * KBd : 0;
+        if (x.down) {
+          const int need = ((S.off[x.e + 1] - S.off[x.e] + kTok - 1) / kTok) * S.nA;
+          while (ld_acquire(p.done + x.e) < need) {
+          }
+          fence_proxy_async_global();
+        }
+        for (int kb = 0; kb < KS; ++kb, ++g) {
+          const int ts = g % kTS;
+          mbar_wait(&t_empty[ts], ((g / kTS) & 1) ^ 1);
+          uint8_t* tt = tring + ts * kXBytes;
+          if (p.dbg & 2) {
+            mbar_arrive(&t_full[ts]);
+            continue;
+          }
+          const int nkb = pair ? 2 : 1;
+          mbar_arrive_expect_tx(&t_full[ts], uint32_t(nkb * (n_load / 32) * 4096));
+          for (int j = 0; j < nkb; ++j) {
+            const int kc = (kb0 + kb * nkb + j) * kBK;
+            for (int i = 0; i < n_load / 32; ++i)
+              tma_load_2d(tt + j * n_load * 128 + i * 4096, x.down ? &tm_h : &tm_x, &t_full[ts], kc, x.row0 + i * 32);
+          }
+        }
+      }
+    }
   } else {
     // ------------------------------------------------------------ decoders
-    const int d = warp - 6;
+    const int d = warp - 7;
     int g = 0;
     for (int u = blockIdx.x; u < S.total; u += gridDim.x) {
       const Unit x = unit_at(S, u);
-      const int n_load = (x.cnt + 31) & ~31;
       const bool pair = down_pair(x, KBd);
       const int KS = x.down ? (pair ? KBd / 2 : KBd) : KBa;
-      const int kb0 = x.down ? x.ks * KBd : 0;
       const int ntile = (!x.down || pair) ? 2 : 1;
-      if (d == 0 && x.down && lane == 0) {
-        // every gate/up unit of expert e has published its H rows
-        const int need = ((S.off[x.e + 1] - S.off[x.e] + kTok - 1) / kTok) * S.nA;
-        while (ld_acquire(p.done + x.e) < need) {
-        }
-        fence_proxy_async_global();
-      }
       for (int kb = 0; kb < KS; ++kb, ++g) {
         const int sa = g % kAS, sc = g % kCS;
         uint8_t* st = smem + sa * kAStage;
         mbar_wait(&a_empty[sa], ((g / kAS) & 1) ^ 1);
-        if (d == 0 && lane == 0 && (p.dbg & 2)) {
-          mbar_arrive(&a_full[sa]);
-        } else if (d == 0 && lane == 0) {
-          const int nkb = pair ? 2 : 1;
-          mbar_arrive_expect_tx(&a_full[sa], uint32_t(nkb * (n_load / 32) * 4096));
-          for (int j = 0; j < nkb; ++j) {
-            const int kc = (kb0 + kb * nkb + j) * kBK;
-            for (int i = 0; i < n_load / 32; ++i)
-              tma_load_2d(st + 2 * kTileA + j * n_load * 128 + i * 4096, x.down ? &tm_h : &tm_x, &a_full[sa], kc,
-                          x.row0 + i * 32);
-          }
-        }
         mbar_wait(&c_full[sc], (g / kCS) & 1);
         const uint8_t* code = cring + size_t(sc) * 2 * kCodeSlot;
         if (!(p.dbg & 1)) {
@@ -709,21 +735,26 @@ int moe_coded_launch(const void* x_perm, int rows, int h, int hi, int E, const i
     case 3: kern = moe_coded_kernel<8, 2, 3>, nd = 8, as = 2, cs = 3; break;
     default: kern = moe_coded_kernel<16, 2, 2>, nd = 16, as = 2, cs = 2; break;
   }
-  int slot = variant;
-  if (fmt == 3) {  // T3: 16 decoder warps, 2 A / 2 code stages (SMO_MOE_CODED=8,2,2: 8 decoder warps)
-    if (variant == 1) kern = moe_coded_kernel<8, 2, 2, 3>, nd = 8, as = 2, cs = 2;
-    else kern = moe_coded_kernel<16, 2, 2, 3>, nd = 16, as = 2, cs = 2;
-    slot = variant == 1 ? 5 : 4;
+  int slot = variant, ts = 2;
+  if (fmt == 3) {  // T3: 16 decoder warps, 2 weight / 3 token / 2 code stages (SMO_MOE_CODED=8,2,2: 8 decoders)
+    static const int t3v = [] {
+      const char* f = std::getenv("SMO_MOE_CODED3");
+      return f ? std::atoi(f) : 0;
+    }();
+    if (variant == 1) kern = moe_coded_kernel<8, 2, 2, 3, 3>, nd = 8, as = 2, cs = 2, ts = 3;
+    else if (t3v == 1) kern = moe_coded_kernel<16, 3, 2, 3, 2>, nd = 16, as = 3, cs = 2, ts = 2;
+    else kern = moe_coded_kernel<16, 2, 2, 3, 3>, nd = 16, as = 2, cs = 2, ts = 3;
+    slot = variant == 1 ? 5 : t3v == 1 ? 6 : 4;
   }
-  const size_t smem = size_t(as) * (2 * kTileA + kTok * 128) + size_t(cs) * 2 * kCodeSlot + 1024;
-  static bool attr_set[6] = {false, false, false, false, false, false};
+  const size_t smem = size_t(as) * 2 * kTileA + size_t(ts) * kTok * 128 + size_t(cs) * 2 * kCodeSlot + 1024;
+  static bool attr_set[7] = {false, false, false, false, false, false, false};
   if (!attr_set[slot]) {
     SMO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr_set[slot] = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(unsigned(sm_count()));
-  cfg.blockDim = dim3(unsigned(kThreads + 32 * nd));
+  cfg.blockDim = dim3(unsigned(kThreads + 32 + 32 * nd));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
