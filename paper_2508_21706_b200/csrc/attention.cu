@@ -197,11 +197,14 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
   // the compiler: LDS/STS instead of generic LD/ST)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ __align__(8) uint64_t q_full[2], q_empty[2];
-  __shared__ __align__(8) uint64_t kv_full[kStages], kv_empty[kStages];
+  // K and V of a chunk stage have separate rings: a K tile is free once S
+  // is in TMEM and the softmax warps have used it for the max exchange, a V
+  // tile only after PV — so K loads run up to a stage ahead of V loads
+  __shared__ __align__(8) uint64_t k_full[kStages], k_empty[kStages], v_full[kStages], v_empty[kStages];
   // o_full: one phase per PV (chunk); o_last: one phase per item (its last
   // PV). Softmax warps skip o_full phases (lazy rescale), so the epilogue
   // waits on o_last, which every warp observes once per item.
-  __shared__ __align__(8) uint64_t s_full[kSP], s_empty[kSP], o_full, o_last, p_full;
+  __shared__ __align__(8) uint64_t s_full[kSP], s_empty[kSP], o_full, o_last, p_full[2];
   __shared__ __align__(8) uint64_t mrg_full;  // split-KV merge: bulk copies of partials landed
   __shared__ uint32_t tmem_base_sh;
 
@@ -222,12 +225,15 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
       mbar_init(&s_empty[i], 1);
     }
     for (int i = 0; i < kStages; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], kSoftWarps);  // every softmax warp, after the max exchange
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);           // PV commit (or the epilogue, for a piece's last chunk)
     }
     mbar_init(&o_full, 1);
     mbar_init(&o_last, 1);
-    mbar_init(&p_full, kSoftWarps);
+    mbar_init(&p_full[0], kSoftWarps);  // P of even / odd chunks: the softmax warps may finish
+    mbar_init(&p_full[1], kSoftWarps);  // chunk c+1 before the MMA thread has seen P(c)
     mbar_init(&mrg_full, 1);
     fence_barrier_init();
     tma_prefetch_desc(&tm_q);
@@ -251,44 +257,92 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
+    // Two cursors over the same chunk sequence: the K cursor (which also
+    // loads each piece's Q tile) and the V cursor, polled round robin so a
+    // K load never waits behind a V stage that PV still holds.
     if (elect_one()) {
-      int used = 0, gc = 0;
-      for (int f = f_begin; f < f_end;) {
-        const Piece pc = f == f_begin ? piece_make(p, f, f_end, pre0) : piece_at(p, f, f_end);
-        f = pc.next_f;
-        if (pc.c1 <= pc.c0) continue;
-        const int qb = used % L::kQBufs;
-        mbar_wait(&q_empty[qb], ((used / L::kQBufs) & 1) ^ 1);
-        ++used;
-        mbar_arrive_expect_tx(&q_full[qb], uint32_t(R * L::kKBlocks * 64 * p.g * p.n * 2));
-        for (int kb = 0; kb < L::kKBlocks; ++kb)
-          for (int k = 0; k < R; ++k)
-            tma_load_3d(smem + L::kQOff + qb * L::kQBytes + kb * 16384 + k * kLanes * 128, &tm_q, &q_full[qb],
-                        kb * 64, pc.h * p.g, pc.r * p.n);
-        const int row_base = (pc.r * p.n_kv + pc.h) * p.s_max;
-        for (int c = pc.c0; c < pc.c1; ++c, ++gc) {
-          // first cache row of chunk c: contiguous, or its page (one page = one chunk)
-          const int crow = p.bt ? (p.bt[pc.r * p.max_pages + c] * p.n_kv + pc.h) * kChunk : row_base + c * kChunk;
-          const int s = gc % kStages;
-          TR(0, 1);
-          mbar_wait(&kv_empty[s], ((gc / kStages) & 1) ^ 1);
-          TR(0, 2);
-          uint8_t* kdst = smem + L::kKvOff + s * 2 * L::kKvBytes;
-          uint8_t* vdst = kdst + L::kKvBytes;
-          // a request's last chunk: V rows past its end (rounded up to 8) are
-          // not loaded, the tile keeps finite older rows there (P is zero)
-          const int vrows = min(kChunk, (pc.keys - c * kChunk + 7) & ~7);
-          mbar_arrive_expect_tx(&kv_full[s], uint32_t(L::kKvBytes + vrows * L::kKBlocks * 128));
-          for (int kb = 0; kb < L::kKBlocks; ++kb) {
-            tma_load_2d(kdst + kb * 16384, &tm_kv_k, &kv_full[s], kb * 64, crow);
-            if (vrows == kChunk) {
-              tma_load_2d(vdst + kb * 16384, &tm_kv_v, &kv_full[s], kb * 64, crow);
-            } else {
-              for (int r8 = 0; r8 < vrows; r8 += 8)
-                tma_load_2d(vdst + kb * 16384 + r8 * 128, &tm_v8, &kv_full[s], kb * 64, crow + r8);
-            }
+      struct Cursor {
+        int f, c, g;
+        bool first, more;
+        Piece pc;
+      };
+      auto next_piece = [&](Cursor& u) {
+        while (u.f < f_end) {
+          u.pc = u.first ? piece_make(p, u.f, f_end, pre0) : piece_at(p, u.f, f_end);
+          u.first = false;
+          u.f = u.pc.next_f;
+          if (u.pc.c1 > u.pc.c0) {
+            u.c = u.pc.c0;
+            return true;
           }
         }
+        return false;
+      };
+      // first cache row of chunk c: contiguous, or its page (one page = one chunk)
+      auto chunk_row = [&](const Piece& pc, int c) {
+        return p.bt ? (p.bt[pc.r * p.max_pages + c] * p.n_kv + pc.h) * kChunk
+                    : (pc.r * p.n_kv + pc.h) * p.s_max + c * kChunk;
+      };
+      Cursor ku{f_begin, 0, 0, true, false, {}}, vu{f_begin, 0, 0, true, false, {}};
+      ku.more = next_piece(ku);
+      vu.more = next_piece(vu);
+      int used = 0;
+      bool q_in = false;  // the K cursor's piece has its Q tile issued
+      while (ku.more || vu.more) {
+        bool progress = false;
+        if (ku.more && !q_in) {
+          const int qb = used % L::kQBufs;
+          if (mbar_test_wait(&q_empty[qb], ((used / L::kQBufs) & 1) ^ 1)) {
+            ++used;
+            mbar_arrive_expect_tx(&q_full[qb], uint32_t(R * L::kKBlocks * 64 * p.g * p.n * 2));
+            for (int kb = 0; kb < L::kKBlocks; ++kb)
+              for (int k = 0; k < R; ++k)
+                tma_load_3d(smem + L::kQOff + qb * L::kQBytes + kb * 16384 + k * kLanes * 128, &tm_q, &q_full[qb],
+                            kb * 64, ku.pc.h * p.g, ku.pc.r * p.n);
+            q_in = true;
+            progress = true;
+          }
+        }
+        if (ku.more && q_in) {
+          const int s = ku.g % kStages;
+          if (mbar_test_wait(&k_empty[s], ((ku.g / kStages) & 1) ^ 1)) {
+            TR(0, 2);
+            const int crow = chunk_row(ku.pc, ku.c);
+            uint8_t* kdst = smem + L::kKvOff + s * 2 * L::kKvBytes;
+            mbar_arrive_expect_tx(&k_full[s], uint32_t(L::kKvBytes));
+            for (int kb = 0; kb < L::kKBlocks; ++kb) tma_load_2d(kdst + kb * 16384, &tm_kv_k, &k_full[s], kb * 64, crow);
+            ++ku.g;
+            if (++ku.c >= ku.pc.c1) {
+              ku.more = next_piece(ku);
+              q_in = false;
+            }
+            progress = true;
+          }
+        }
+        if (vu.more && vu.g < ku.g) {
+          const int s = vu.g % kStages;
+          if (mbar_test_wait(&v_empty[s], ((vu.g / kStages) & 1) ^ 1)) {
+            TR(0, 3);
+            const int crow = chunk_row(vu.pc, vu.c);
+            uint8_t* vdst = smem + L::kKvOff + s * 2 * L::kKvBytes + L::kKvBytes;
+            // a request's last chunk: V rows past its end (rounded up to 8) are
+            // not loaded, the tile keeps finite older rows there (P is zero)
+            const int vrows = min(kChunk, (vu.pc.keys - vu.c * kChunk + 7) & ~7);
+            mbar_arrive_expect_tx(&v_full[s], uint32_t(vrows * L::kKBlocks * 128));
+            for (int kb = 0; kb < L::kKBlocks; ++kb) {
+              if (vrows == kChunk) {
+                tma_load_2d(vdst + kb * 16384, &tm_kv_v, &v_full[s], kb * 64, crow);
+              } else {
+                for (int r8 = 0; r8 < vrows; r8 += 8)
+                  tma_load_2d(vdst + kb * 16384 + r8 * 128, &tm_v8, &v_full[s], kb * 64, crow + r8);
+              }
+            }
+            ++vu.g;
+            if (++vu.c >= vu.pc.c1) vu.more = next_piece(vu);
+            progress = true;
+          }
+        }
+        if (!progress) __nanosleep(20);
       }
     }
   } else if (warp == 1) {
@@ -297,7 +351,6 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
       const uint32_t id_s = make_idesc_bf16(128, kChunk);
       const uint32_t id_o = make_idesc_bf16(128, D, /*b_mn_major=*/1);
       int used = 0, gc = 0;
-      uint32_t p_phase = 0;
       for (int f = f_begin; f < f_end;) {
         const Piece pc = piece_at(p, f, f_end);
         f = pc.next_f;
@@ -311,14 +364,14 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
         // was consumed by PV two chunks earlier
         auto s_ready = [&](int ci) {
           const int g2 = gc + ci;
-          return mbar_test_wait(&kv_full[g2 % kStages], (g2 / kStages) & 1) &&
+          return mbar_test_wait(&k_full[g2 % kStages], (g2 / kStages) & 1) &&
                  mbar_test_wait(&s_empty[g2 % kSP], ((g2 / kSP) & 1) ^ 1);
         };
         auto issue_s = [&](int ci) {
           const int g2 = gc + ci;
           const int s = g2 % kStages, sb = g2 % kSP;
           TR(1, 1);
-          mbar_wait(&kv_full[s], (g2 / kStages) & 1);
+          mbar_wait(&k_full[s], (g2 / kStages) & 1);
           mbar_wait(&s_empty[sb], ((g2 / kSP) & 1) ^ 1);
           tc_fence_after();
           // descriptors are built once and advanced by constants: the single
@@ -338,10 +391,40 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
           const int g2 = gc + ci;
           const int s = g2 % kStages, sb = g2 % kSP;
           uint8_t* vbuf = smem + L::kKvOff + s * 2 * L::kKvBytes + L::kKvBytes;
+          // Wait for V(ci) and P(ci); meanwhile issue S(ci+1) as soon as its K
+          // landed and its S/P buffer is free (never blocking: PV(ci) must not
+          // queue behind the next chunk's K load). S(j) is thus issued after
+          // PV(j-2), so S(j) complete implies PV(j-2) complete (the softmax
+          // warps' o_full parity wait relies on it).
+          bool next_issued = ci + 1 >= nch, v_in = false;
+#ifdef SMO_ATTN_TRACE
+          bool tk = false, ts = false, tv = false;
+#endif
+          for (;;) {
+#ifdef SMO_ATTN_TRACE
+            if (!next_issued && !tk && mbar_test_wait(&k_full[(g2 + 1) % kStages], ((g2 + 1) / kStages) & 1)) {
+              tk = true;
+              TR(1, 7);
+            }
+            if (!next_issued && !ts && mbar_test_wait(&s_empty[(g2 + 1) % kSP], (((g2 + 1) / kSP) & 1) ^ 1)) {
+              ts = true;
+              TR(1, 8);
+            }
+            if (!tv && mbar_test_wait(&v_full[s], (g2 / kStages) & 1)) {
+              tv = true;
+              TR(1, 9);
+            }
+#endif
+            if (!next_issued && s_ready(ci + 1)) {
+              issue_s(ci + 1);
+              next_issued = true;
+            }
+            v_in = v_in || mbar_test_wait(&v_full[s], (g2 / kStages) & 1);
+            if (v_in && mbar_test_wait(&p_full[g2 & 1], (g2 >> 1) & 1)) break;
+          }
           // last chunk: the producer loaded V only up to the request's end
           // rounded up to 8 rows; zero the loaded rows past the end (their P
-          // is zero, stale cache contents may be non-finite). The stage
-          // landed: S(ci) was issued after kv_full.
+          // is zero, stale cache contents may be non-finite)
           const int valid = pc.keys - (pc.c0 + ci) * kChunk;
           if (valid < kChunk && (valid & 7)) {
             for (int rr = valid; rr < ((valid + 7) & ~7); ++rr)
@@ -353,18 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
             fence_proxy_async();
           }
           TR(1, 4);
-          // PV(ci) must not queue behind the next chunk's K/V load (it frees
-          // that load's stage): issue S(ci+1) early only if it is ready
-          bool next_issued = ci + 1 >= nch;
-          while (!next_issued && !mbar_test_wait(&p_full, p_phase)) {
-            if (s_ready(ci + 1)) {
-              issue_s(ci + 1);
-              next_issued = true;
-            }
-          }
-          mbar_wait(&p_full, p_phase);
           TR(1, 5);
-          p_phase ^= 1;
           tc_fence_after();
           const uint64_t vd = make_sdesc_sw128(smem_u32(vbuf), 16384, 1024);
           const uint32_t pt = tmem + sb * 128;
@@ -373,14 +445,16 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
 #pragma unroll
           for (int kk = 0; kk < kChunk / 16; ++kk) {
             umma_bf16_ts(tmem + kOAcc, pt + kk * 8, vd + uint64_t(kk * 128), id_o, (ci > 0 || kk > 0) ? 1u : 0u);
+#ifndef SMO_K1_AB_NO_LO  // timing A/B only (drops the P lo plane: wrong numerics)
             umma_bf16_ts(tmem + kOAcc, pt + 64 + kk * 8, vd + uint64_t(kk * 128), id_o, 1u);
+#endif
           }
           umma_commit(&o_full);
           if (ci + 1 == nch) umma_commit(&o_last);
           umma_commit(&s_empty[sb]);
           // the last chunk's stage is released by the softmax warps after the
           // epilogue (they use it as scratch)
-          if (ci + 1 < nch) umma_commit(&kv_empty[s]);
+          if (ci + 1 < nch) umma_commit(&v_empty[s]);
           TR(1, 6);
           if (!next_issued) issue_s(ci + 1);
         }
@@ -396,7 +470,11 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
     const int row = lrow % kLanes;              // query row (i*g + hh)
     const int stid = threadIdx.x - 64;          // 0..255 over the softmax warps
     const uint32_t tlane = uint32_t(q4 * 32) << 16;
+#ifdef SMO_K1_AB_NOSOFT  // timing A/B only: no softmax math (wrong results)
+    const bool warp_live = false;
+#else
     const bool warp_live = (q4 * 32) % kLanes < p.rows;
+#endif
     const bool live = row < p.rows;
     const int qi = live ? row / p.g : 0;
     const int col0 = rep * kW + half * kCols;   // this thread's key columns in a chunk
@@ -478,6 +556,12 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
         // overwrite the S buffer
         asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
         cmax = fmaxf(cmax, xchg[(half ^ 1) * 128 + lrow]) * p.scale_log2;
+        // K tile (and exchange) done: hand it to the producer, except a
+        // piece's last chunk, whose stage is the epilogue's scratch
+        if (ci + 1 < nch) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&k_empty[g2 % kStages]);
+        }
         const bool grow = cmax > m_ref + 8.f;  // also true for the first visible score
         const float m_new = grow ? cmax : m_ref;
         const float alpha = grow ? (m_ref == -INFINITY ? 0.f : ex2_approx(m_ref - m_new)) : 1.f;
@@ -539,7 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full);
+        if (lane == 0) mbar_arrive(&p_full[g2 & 1]);
         if (warp == 4 && lane == 0) TR(2, 5);
       }
       mbar_wait(&o_last, items_done & 1);
@@ -649,7 +733,8 @@ __global__ void __launch_bounds__(kThreads, 1)  // 168 regs: 3 warps share an SM
         fence_proxy_async();
         asm volatile("bar.sync 5, 256;" ::: "memory");
       }
-      if (stid == 0) mbar_arrive(&kv_empty[s_last]);
+      if (lane == 0) mbar_arrive(&k_empty[s_last]);
+      if (stid == 0) mbar_arrive(&v_empty[s_last]);
       if (warp == 4 && lane == 0) TR(2, 10);
     }
     // ---- split-KV merge (deferred). A CTA's first and last pieces may be
