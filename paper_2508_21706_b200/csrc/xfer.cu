@@ -585,10 +585,12 @@ __global__ void __launch_bounds__(32 * kUDecWarps, 28) unary_decode_kernel(const
       const uint8_t* esc = sb + kSeg + 4 * nw;
       for (uint32_t m = emask; m; m &= m - 1u) {
         const int i = __ffs(m) - 1;
-        const int sh = 8 * (i % 4);
+        const uint32_t sh = 8u * uint32_t(i % 4), wq = uint32_t(i / 4);
+        const uint32_t eb = uint32_t(esc[er]) << sh, keep = ~(0xffu << sh);
+        // select-based patch over all eight words (no dynamic index: e4
+        // stays in registers instead of local memory on every segment)
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (q == i / 4) e4[q] = (e4[q] & ~(0xffu << sh)) | (uint32_t(esc[er]) << sh);
+        for (int q = 0; q < 8; ++q) e4[q] = uint32_t(q) == wq ? ((e4[q] & keep) | eb) : e4[q];
         ++er;
       }
     }
