@@ -408,7 +408,10 @@ __device__ __forceinline__ int select_msb(uint32_t x, int k) {
 constexpr int kUDecWarps = 2;
 constexpr int kURun = 4;  // code words per lane per scan round (fast path: streams of <= 128 words)
 template <bool kDirect>
-__global__ void __launch_bounds__(32 * kUDecWarps, 28) unary_decode_kernel(const __grid_constant__ DecodeJobs jobs,
+#ifndef SMO_UDEC_MINB  // resident blocks per SM the register budget is sized for (A/B: -DSMO_UDEC_MINB=n)
+#define SMO_UDEC_MINB 28
+#endif
+__global__ void __launch_bounds__(32 * kUDecWarps, SMO_UDEC_MINB) unary_decode_kernel(const __grid_constant__ DecodeJobs jobs,
                                                                        size_t segs) {
   __shared__ __align__(16) uint32_t wbuf[kUDecWarps][kUMaxWords + 8];
   __shared__ __align__(16) uint4 lobuf[kUDecWarps][64];  // the segment's lo bytes, copied ahead (cp.async)
