@@ -184,6 +184,37 @@ def test_fused_moe_kernel_vs_torch(cuda, T, E, k, h, hi, splits):
         assert dy <= 1e-4 * max(1.0, Y.abs().max().item()), (e, dy)
 
 
+@pytest.mark.parametrize("T,E,k,h,hi,splits", [(288, 8, 2, 1024, 512, 4), (48, 64, 6, 512, 384, 2),
+                                                (576, 8, 2, 512, 1792, 0)])
+def test_fused_moe_kernel_repeat_bit_identical(cuda, T, E, k, h, hi, splits):
+    """Race detector for K4-MoE's cross-CTA hand-off (a down unit's producer
+    acquires its expert's gate/up counter) in place of the pool-closed
+    compute-sanitizer: many launches, with foreign kernels in between, give
+    bit-identical H and y."""
+    import torch
+    from paper_2508_21706_b200 import ops
+    g = torch.Generator(device=cuda).manual_seed(E * 100 + T + 7)
+    x = _bf16_rand(torch, (T, h), g)
+    blk = 3 * h * hi
+    pool = _bf16_rand(torch, (E * blk,), g, scale=math.sqrt(3.0 / h))
+    logits = torch.randn((T, E), generator=g, device=cuda)
+    ids = torch.topk(logits, k, dim=1).indices.to(torch.int32).contiguous()
+    off, perm, pos, xp = ops.permute(ids, E, x)
+    widx = torch.arange(E, dtype=torch.int32, device=cuda)
+    run = lambda: ops.moe_experts(xp, off, pool, h=h, h_i=hi, n_expert=E, w_block_stride=blk * 2,
+                                  w_pool_blocks=E, w_index=widx, splits=splits)
+    h0, y0 = run()
+    junk = torch.empty(1 << 22, device=cuda)
+    outs = []
+    for i in range(40):
+        if i % 2 == 0:
+            junk.normal_()
+        outs.append(run())
+    torch.cuda.synchronize()
+    for i, (hh, yy) in enumerate(outs):
+        assert torch.equal(hh, h0) and torch.equal(yy, y0), f"launch {i} differs from the first"
+
+
 # ---------------------------------------------------------------- K2 / K3
 @pytest.mark.parametrize("T,h,E,k", [(20, 512, 8, 2), (288, 4096, 8, 2), (64, 2048, 64, 6)])
 def test_router_bit_exact_vs_oracle(cuda, oracle, T, h, E, k):
@@ -518,6 +549,67 @@ def test_verify_attention_paged_bit_identical(cuda, b, n, nq, nkv, d, prefix):
     vp[bt.long().view(-1)] = vf.reshape(b * max_pages, nkv, 128, d)
     got = ops.verify_attention(q, kp, vp, mask, pre, max(prefix), block_table=bt)
     assert torch.equal(got, ref)
+
+
+@pytest.mark.parametrize("b,n,nq,nkv,d,prefix,paged", [
+    (32, 9, 32, 8, 128, [1024] * 32, False),                # BASELINE config 2: two whole pairs per CTA
+    (16, 9, 32, 8, 128, [1024 - 37 * i for i in range(16)], True),  # ragged + paged: split pairs, merges
+    (1, 9, 32, 8, 128, [1024], False),                      # b = 1: every pair split over 9 CTAs
+    (8, 32, 16, 4, 64, [3000, 17, 2048, 129, 1, 900, 4095, 640], False),  # d = 64 (6 stages), 128 rows
+])
+def test_verify_attention_repeat_bit_identical(cuda, b, n, nq, nkv, d, prefix, paged):
+    """Race detector standing in for compute-sanitizer (closed on the GPU
+    pool): K1's producer / MMA / softmax hand-offs (separate K and V rings,
+    P barriers by chunk parity, cross-CTA partial merges) must give
+    bit-identical outputs over many back-to-back launches on one workspace,
+    with a foreign kernel between some launches to vary the timing."""
+    import torch
+    from paper_2508_21706_b200 import ops
+    s_max = max(prefix) + n + 64
+    q, kc, vc, mask, pre, _ = _attn_case(torch, cuda, b, n, nq, nkv, d, prefix, s_max, False, seed=b * 13 + n)
+    kw = {}
+    if paged:
+        max_pages = (s_max + 127) // 128
+        bt = torch.arange(b * max_pages, dtype=torch.int32, device=cuda).flip(0).view(b, max_pages).contiguous()
+        pad = max_pages * 128 - s_max
+        kp = torch.empty((b * max_pages, nkv, 128, d), dtype=torch.bfloat16, device=cuda)
+        vp = torch.empty_like(kp)
+        kf = torch.nn.functional.pad(kc, (0, 0, 0, pad)).view(b, nkv, max_pages, 128, d).transpose(1, 2)
+        vf = torch.nn.functional.pad(vc, (0, 0, 0, pad)).view(b, nkv, max_pages, 128, d).transpose(1, 2)
+        kp[bt.long().view(-1)] = kf.reshape(b * max_pages, nkv, 128, d)
+        vp[bt.long().view(-1)] = vf.reshape(b * max_pages, nkv, 128, d)
+        kc, vc, kw = kp, vp, {"block_table": bt}
+    ref = ops.verify_attention(q, kc, vc, mask, pre, max(prefix), **kw)
+    # one persistent workspace, as the engine keeps it: the pair counters must
+    # be re-armed to zero by every launch
+    import ctypes
+    from paper_2508_21706_b200 import _lib as L
+    lib = L.load()
+    if paged:
+        bt = kw["block_table"]
+        mp, npg, smx = bt.shape[1], kc.shape[0], 128 * bt.shape[1]
+    else:
+        mp, npg, smx = 0, 0, s_max
+    outs = [torch.empty_like(q) for _ in range(160)]
+    args = []
+    for o in outs:
+        a = L.AttnArgs(q=q.data_ptr(), k_cache=kc.data_ptr(), v_cache=vc.data_ptr(), mask=mask.data_ptr(),
+                       prefix_len=pre.data_ptr(), out=o.data_ptr(), b=b, n=n, n_q=nq, n_kv=nkv, d=d, s_max=smx,
+                       max_prefix=max(prefix), workspace=None, workspace_bytes=0,
+                       block_table=bt.data_ptr() if paged else None, max_pages=mp, num_pages=npg)
+        args.append(a)
+    wsb = lib.smo_verify_attention_workspace(ctypes.byref(args[0]))
+    ws = torch.zeros(max(16, wsb), dtype=torch.uint8, device=cuda)
+    junk = torch.empty(1 << 22, device=cuda)
+    st = torch.cuda.current_stream().cuda_stream
+    for i, a in enumerate(args):
+        a.workspace, a.workspace_bytes = ws.data_ptr(), wsb
+        if i % 3 == 0:
+            junk.normal_()  # a foreign kernel between launches shifts the CTAs' relative timing
+        L.check(lib.smo_verify_attention(ctypes.byref(a), st))
+    torch.cuda.synchronize()
+    for i, o in enumerate(outs):
+        assert torch.equal(o, ref), f"launch {i} differs from the first"
 
 
 # ---------------------------------------------------------------- K5 codec
