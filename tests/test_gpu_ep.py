@@ -143,7 +143,8 @@ def _ipc_rank(rank, world, port, out_q, staged=False):
         mine = slice(rank * bl, (rank + 1) * bl)
         eng.fill_prefix(prefix[mine])
         stream = torch.cuda.Stream()
-        got = [eng.verify(tokens[mine], prefix[mine], stream=stream.cuda_stream) for _ in range(2)]
+        # 12 steps: the device-side round flags of the mailbox exchange cycle many times
+        got = [eng.verify(tokens[mine], prefix[mine], stream=stream.cuda_stream) for _ in range(12)]
         stream.synchronize()
         eng.close()
         dist.barrier()

@@ -175,3 +175,34 @@ def test_moe_coded3_bit_identical_mixtral_dims(cuda):
     import torch
     rows = [70, 75, 68, 80, 71, 69, 72, 71]
     _coded_vs_plain(torch, cuda, 4096, 14336, 8, rows, "uniform", fmt=3)
+
+
+@pytest.mark.parametrize("fmt", [2, 3])
+def test_moe_coded_repeat_bit_identical(cuda, fmt):
+    """Race detector for the coded expert kernel's decoder-warp / token-ring /
+    MMA hand-offs (compute-sanitizer is closed on the GPU pool): repeated
+    launches, foreign kernels in between, bit-identical H and y."""
+    import torch
+    from paper_2508_21706_b200 import ops
+    h, hi, E = 512, 768, 6
+    rows_per = [5, 0, 33, 130, 1, 64]
+    g = torch.Generator(device=cuda).manual_seed(11)
+    blks = [_block(torch, cuda, "uniform", h, hi, base=3000 + 3 * e) for e in range(E)]
+    codes = [ops.tcode_encode(b, h, hi, fmt=fmt) for b in blks]
+    w_code = torch.tensor([c.data_ptr() for c in codes], dtype=torch.int64, device=cuda)
+    off = torch.zeros(E + 1, dtype=torch.int32)
+    off[1:] = torch.cumsum(torch.tensor(rows_per, dtype=torch.int32), 0)
+    rows = int(off[-1])
+    off = off.to(cuda)
+    x = (torch.rand((rows, h), generator=g, device=cuda) * 2 - 1).to(torch.bfloat16)
+    h0, y0 = ops.moe_experts_coded(x, off, w_code, h=h, h_i=hi, n_expert=E, splits=2, fmt=fmt)
+    junk = torch.empty(1 << 22, device=cuda)
+    outs = []
+    for i in range(40):
+        if i % 2 == 0:
+            junk.normal_()
+        outs.append(ops.moe_experts_coded(x, off, w_code, h=h, h_i=hi, n_expert=E, splits=2, fmt=fmt))
+    torch.cuda.synchronize()
+    for i, (hh, yy) in enumerate(outs):
+        assert torch.equal(hh.view(torch.int16), h0.view(torch.int16)), f"launch {i}: H differs"
+        assert torch.equal(yy.view(torch.int32), y0.view(torch.int32)), f"launch {i}: y differs"
