@@ -589,15 +589,94 @@ void embed(const int32_t* tok, const void* emb, int T, int h, float* x, cudaStre
   SMO_CUDA_CHECK(cudaGetLastError());
 }
 
+// RoPE + K/V append with the inverse frequencies theta^(-2j/d) computed once
+// on the host in double (the oracle's own pow, oracle/oracle.c) and passed by
+// value: a row only evaluates its 64 fp64 sincos, and the rotation / copies
+// move bf16 pairs and 16-byte chunks instead of single values.
+struct RopeInv {
+  double inv[64];
+};
+__global__ void rope_append_v2_kernel(const uint16_t* __restrict__ qkv, const int32_t* __restrict__ prefix,
+                                      const int32_t* __restrict__ parent, int n, int n_q, int n_kv, int d, int s_max,
+                                      const __grid_constant__ RopeInv ri, uint16_t* __restrict__ q_out,
+                                      uint16_t* __restrict__ kc, uint16_t* __restrict__ vc,
+                                      const int32_t* __restrict__ bt, int max_pages) {
+  const int row = blockIdx.x;
+  const int r = row / n, i = row % n;
+  int depth = i;
+  if (parent) {
+    depth = 0;
+    int cur = i;
+    while (cur > 0 && depth <= n) {
+      cur = parent[size_t(r) * n + cur];
+      ++depth;
+    }
+  }
+  const int pos = prefix[r] + depth;
+  const int slot = prefix[r] + i;
+  const int half = d / 2;
+  const int width = (n_q + 2 * n_kv) * d;
+  const uint16_t* src = qkv + size_t(row) * width;
+  __shared__ float cs_sh[64], sn_sh[64];
+  for (int j = threadIdx.x; j < half; j += blockDim.x) {
+    double sn, cs;
+    sincos(double(pos) * ri.inv[j], &sn, &cs);
+    cs_sh[j] = float(cs);
+    sn_sh[j] = float(sn);
+  }
+  __syncthreads();
+  const int hp = half / 2;  // bf16 pairs per half head
+  for (int e = threadIdx.x; e < (n_q + n_kv) * hp; e += blockDim.x) {
+    const int head = e / hp, j = 2 * (e % hp);
+    const uint32_t a2 = *reinterpret_cast<const uint32_t*>(src + head * d + j);
+    const uint32_t b2 = *reinterpret_cast<const uint32_t*>(src + head * d + j + half);
+    const float a0 = __uint_as_float(a2 << 16), a1 = __uint_as_float(a2 & 0xffff0000u);
+    const float b0 = __uint_as_float(b2 << 16), b1 = __uint_as_float(b2 & 0xffff0000u);
+    const float c0 = cs_sh[j], s0 = sn_sh[j], c1 = cs_sh[j + 1], s1 = sn_sh[j + 1];
+    const uint32_t o0 = uint32_t(f2bf(a0 * c0 - b0 * s0)) | (uint32_t(f2bf(a1 * c1 - b1 * s1)) << 16);
+    const uint32_t o1 = uint32_t(f2bf(b0 * c0 + a0 * s0)) | (uint32_t(f2bf(b1 * c1 + a1 * s1)) << 16);
+    uint16_t* dst;
+    if (head < n_q) {
+      dst = q_out + (size_t(row) * n_q + head) * d;
+    } else {
+      const long long kr = kv_row(bt, max_pages, r, head - n_q, slot, n_kv, s_max);
+      if (kr < 0) continue;
+      dst = kc + size_t(kr) * d;
+    }
+    *reinterpret_cast<uint32_t*>(dst + j) = o0;
+    *reinterpret_cast<uint32_t*>(dst + j + half) = o1;
+  }
+  for (int e = threadIdx.x; e < n_kv * (d / 8); e += blockDim.x) {  // V rows: 16-byte chunks
+    const int hk = e / (d / 8), c = 8 * (e % (d / 8));
+    const long long vr = kv_row(bt, max_pages, r, hk, slot, n_kv, s_max);
+    if (vr >= 0)
+      *reinterpret_cast<uint4*>(vc + size_t(vr) * d + c) =
+          *reinterpret_cast<const uint4*>(src + (n_q + n_kv) * d + hk * d + c);
+  }
+}
+
 void rope_append(const void* qkv, const int32_t* prefix, const int32_t* parent, int b, int n, int n_q, int n_kv,
                  int d, int s_max, float theta, void* q_out, void* kc, void* vc, cudaStream_t st, const int32_t* bt,
                  int max_pages) {
   SMO_REQUIRE(qkv && prefix && q_out && kc && vc, "rope_append: null pointer");
   SMO_REQUIRE(d % 2 == 0 && d <= 128, "rope_append: head_dim must be even and <= 128");
-  rope_append_kernel<<<b * n, 256, 0, st>>>(reinterpret_cast<const uint16_t*>(qkv), prefix, parent, n, n_q, n_kv,
-                                            d, s_max, double(theta), reinterpret_cast<uint16_t*>(q_out),
-                                            reinterpret_cast<uint16_t*>(kc), reinterpret_cast<uint16_t*>(vc), bt,
-                                            max_pages);
+  static const bool v1 = [] {  // A/B: SMO_ROPE_V1=1 -> the per-row fp64 pow kernel
+    const char* f = std::getenv("SMO_ROPE_V1");
+    return f && f[0] == '1';
+  }();
+  if (v1 || d % 4 != 0) {
+    rope_append_kernel<<<b * n, 256, 0, st>>>(reinterpret_cast<const uint16_t*>(qkv), prefix, parent, n, n_q, n_kv,
+                                              d, s_max, double(theta), reinterpret_cast<uint16_t*>(q_out),
+                                              reinterpret_cast<uint16_t*>(kc), reinterpret_cast<uint16_t*>(vc), bt,
+                                              max_pages);
+  } else {
+    RopeInv ri{};
+    for (int j = 0; j < d / 2; ++j) ri.inv[j] = std::pow(double(theta), -2.0 * j / double(d));
+    rope_append_v2_kernel<<<b * n, 256, 0, st>>>(reinterpret_cast<const uint16_t*>(qkv), prefix, parent, n, n_q,
+                                                 n_kv, d, s_max, ri, reinterpret_cast<uint16_t*>(q_out),
+                                                 reinterpret_cast<uint16_t*>(kc), reinterpret_cast<uint16_t*>(vc), bt,
+                                                 max_pages);
+  }
   count_launch();
   SMO_CUDA_CHECK(cudaGetLastError());
 }
