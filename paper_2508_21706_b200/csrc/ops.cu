@@ -75,15 +75,27 @@ __global__ void router_topk_kernel(const uint16_t* __restrict__ x, const uint16_
   for (int e = wid; e < E; e += nw) {
     const uint16_t* wr = w + size_t(e) * h;
     float a = 0.f;
-    for (int base = lane * 8; base < h; base += 256) {
-      const uint4 xv = *reinterpret_cast<const uint4*>(xr + base);
-      const uint4 wv = *reinterpret_cast<const uint4*>(wr + base);
-      const uint32_t xs[4] = {xv.x, xv.y, xv.z, xv.w};
-      const uint32_t ws[4] = {wv.x, wv.y, wv.z, wv.w};
+    // the 16-byte loads of kU chunks are issued together, then the FMA chain
+    // on `a` runs in the fixed order (bit-identical to one chunk at a time)
+    constexpr int kU = 8;
+    for (int b0 = lane * 8; b0 < h; b0 += 256 * kU) {
+      uint4 xv[kU], wv[kU];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        a = __fmaf_rn(__uint_as_float(xs[q] << 16), __uint_as_float(ws[q] << 16), a);
-        a = __fmaf_rn(__uint_as_float(xs[q] & 0xffff0000u), __uint_as_float(ws[q] & 0xffff0000u), a);
+      for (int u = 0; u < kU; ++u) {
+        const int base = b0 + 256 * u;
+        xv[u] = base < h ? *reinterpret_cast<const uint4*>(xr + base) : make_uint4(0, 0, 0, 0);
+        wv[u] = base < h ? *reinterpret_cast<const uint4*>(wr + base) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (b0 + 256 * u >= h) break;
+        const uint32_t xs[4] = {xv[u].x, xv[u].y, xv[u].z, xv[u].w};
+        const uint32_t ws[4] = {wv[u].x, wv[u].y, wv[u].z, wv[u].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          a = __fmaf_rn(__uint_as_float(xs[q] << 16), __uint_as_float(ws[q] << 16), a);
+          a = __fmaf_rn(__uint_as_float(xs[q] & 0xffff0000u), __uint_as_float(ws[q] & 0xffff0000u), a);
+        }
       }
     }
 #pragma unroll
