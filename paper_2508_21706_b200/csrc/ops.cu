@@ -214,34 +214,48 @@ __global__ void combine_kernel(const float* __restrict__ y, const int32_t* __res
 }
 
 // ---------------------------------------------------------------- norm / embed
+// One block of 256 threads per row; the row's float4 chunks (h <= 8192) are
+// loaded once, together, and kept in registers for the scaling pass. The
+// per-thread sum of squares runs over the thread's chunks in increasing
+// column order, as before (bit-identical).
+constexpr int kRmsMaxV = 8;
 __global__ void rmsnorm_kernel(const float* __restrict__ x, const uint16_t* __restrict__ gain, int h, float eps,
                                uint16_t* __restrict__ y) {
   const int t = blockIdx.x;
   const float* xr = x + size_t(t) * h;
-  float ss = 0.f;
-  for (int c = threadIdx.x * 4; c < h; c += blockDim.x * 4) {
-    const float4 v = *reinterpret_cast<const float4*>(xr + c);
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  const int stride = blockDim.x * 4;
+  float4 v[kRmsMaxV];
+  uint2 gv[kRmsMaxV];
+#pragma unroll
+  for (int u = 0; u < kRmsMaxV; ++u) {
+    const int c = threadIdx.x * 4 + u * stride;
+    v[u] = c < h ? *reinterpret_cast<const float4*>(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    gv[u] = c < h ? *reinterpret_cast<const uint2*>(gain + c) : make_uint2(0u, 0u);
   }
+  float ss = 0.f;
+#pragma unroll
+  for (int u = 0; u < kRmsMaxV; ++u)
+    if (threadIdx.x * 4 + u * stride < h) ss += v[u].x * v[u].x + v[u].y * v[u].y + v[u].z * v[u].z + v[u].w * v[u].w;
   __shared__ float red[32];
   ss = warp_sum(ss);
   if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = ss;
   __syncthreads();
   if (threadIdx.x < 32) {
-    float v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
-    v = warp_sum(v);
-    if (threadIdx.x == 0) red[0] = v;
+    float r = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+    r = warp_sum(r);
+    if (threadIdx.x == 0) red[0] = r;
   }
   __syncthreads();
   const float inv = rsqrtf(red[0] / float(h) + eps);
-  for (int c = threadIdx.x * 4; c < h; c += blockDim.x * 4) {
-    const float4 v = *reinterpret_cast<const float4*>(xr + c);
-    const uint2 gv = *reinterpret_cast<const uint2*>(gain + c);
-    const float g0 = __uint_as_float(gv.x << 16), g1 = __uint_as_float(gv.x & 0xffff0000u);
-    const float g2 = __uint_as_float(gv.y << 16), g3 = __uint_as_float(gv.y & 0xffff0000u);
+#pragma unroll
+  for (int u = 0; u < kRmsMaxV; ++u) {
+    const int c = threadIdx.x * 4 + u * stride;
+    if (c >= h) break;
+    const float g0 = __uint_as_float(gv[u].x << 16), g1 = __uint_as_float(gv[u].x & 0xffff0000u);
+    const float g2 = __uint_as_float(gv[u].y << 16), g3 = __uint_as_float(gv[u].y & 0xffff0000u);
     uint2 o;
-    o.x = uint32_t(f2bf(v.x * inv * g0)) | (uint32_t(f2bf(v.y * inv * g1)) << 16);
-    o.y = uint32_t(f2bf(v.z * inv * g2)) | (uint32_t(f2bf(v.w * inv * g3)) << 16);
+    o.x = uint32_t(f2bf(v[u].x * inv * g0)) | (uint32_t(f2bf(v[u].y * inv * g1)) << 16);
+    o.y = uint32_t(f2bf(v[u].z * inv * g2)) | (uint32_t(f2bf(v[u].w * inv * g3)) << 16);
     *reinterpret_cast<uint2*>(y + size_t(t) * h + c) = o;
   }
 }
@@ -585,7 +599,7 @@ void unpermute_combine(const float* y, const int32_t* pos, const float* w, int T
 }
 
 void rmsnorm(const float* x, const void* gain, int T, int h, float eps, void* y, cudaStream_t st) {
-  SMO_REQUIRE(x && gain && y && h % 4 == 0, "rmsnorm: bad arguments");
+  SMO_REQUIRE(x && gain && y && h % 4 == 0 && h <= 256 * 4 * kRmsMaxV, "rmsnorm: bad arguments (h % 4 == 0, h <= 8192)");
   if (T <= 0) return;
   rmsnorm_kernel<<<T, 256, 0, st>>>(x, reinterpret_cast<const uint16_t*>(gain), h, eps,
                                     reinterpret_cast<uint16_t*>(y));

@@ -1,0 +1,15 @@
+"""Per-layer small kernels at the verify shape (T=288, h=4096): RMSNorm and the
+router, device time via kbench.timeit (L2 flushed) — same-box A/B with SPECMOE_LIB."""
+import sys, json
+sys.path.insert(0, "tools")
+import torch, kbench
+from paper_2508_21706_b200 import ops
+dev = torch.device("cuda:0")
+T, h = 288, 4096
+x = torch.randn((T, h), device=dev)
+gain = torch.ones(h, dtype=torch.bfloat16, device=dev)
+res = {"rmsnorm": round(kbench.timeit(lambda: ops.rmsnorm(x, gain, 1e-5)) * 1e6, 2)}
+xb = x.to(torch.bfloat16)
+w = (torch.rand((8, h), device=dev) * 0.02).to(torch.bfloat16)
+res["router"] = round(kbench.timeit(lambda: ops.router_topk(xb, w, 2)) * 1e6, 2)
+print(json.dumps(res))
