@@ -12,4 +12,10 @@ res = {"rmsnorm": round(kbench.timeit(lambda: ops.rmsnorm(x, gain, 1e-5)) * 1e6,
 xb = x.to(torch.bfloat16)
 w = (torch.rand((8, h), device=dev) * 0.02).to(torch.bfloat16)
 res["router"] = round(kbench.timeit(lambda: ops.router_topk(xb, w, 2)) * 1e6, 2)
+k = 2
+y = torch.randn((T * k, h), device=dev)
+pos = torch.randperm(T * k, device=dev).to(torch.int32)
+wts = torch.rand((T, k), device=dev)
+resid = torch.randn((T, h), device=dev)
+res["combine"] = round(kbench.timeit(lambda: ops.unpermute_combine_(resid, y, pos, wts)) * 1e6, 2)
 print(json.dumps(res))
