@@ -130,10 +130,21 @@ __global__ void router_topk_kernel(const uint16_t* __restrict__ x, const uint16_
 // ---------------------------------------------------------------- K3 permute
 // Single CTA, one warp per expert (strided): ballot + popc gives each pair's
 // rank among the earlier pairs of its expert -> a stable counting sort.
-__global__ void permute_kernel(const int32_t* __restrict__ ids, int P, int E, int32_t* offsets, int32_t* perm,
+// The ids are staged in shared memory first (one coalesced pass by all
+// threads) when they fit: the per-expert ballot loops then read shared memory
+// instead of making a global round trip per 32 pairs.
+constexpr int kPermuteSmemIds = 12288;  // 48 KB of dynamic shared memory
+__global__ void permute_kernel(const int32_t* __restrict__ ids_g, int P, int E, int32_t* offsets, int32_t* perm,
                                int32_t* pos) {
   __shared__ int cnt[kMaxExperts + 1];
+  extern __shared__ int ids_sh[];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  const bool staged = P <= kPermuteSmemIds;
+  if (staged) {
+    for (int i = threadIdx.x; i < P; i += blockDim.x) ids_sh[i] = ids_g[i];
+    __syncthreads();
+  }
+  const int32_t* ids = staged ? ids_sh : ids_g;
   for (int e = warp; e < E; e += nw) {
     int c = 0;
     for (int i0 = 0; i0 < P; i0 += 32) {
@@ -576,7 +587,7 @@ void permute(const int32_t* ids, int T, int k, int E, const void* x, int h, int3
   SMO_REQUIRE(ids && offsets && perm && pos, "permute: null pointer");
   SMO_REQUIRE(E >= 1 && E <= kMaxExperts, "permute: bad E");
   const int P = T * k;
-  permute_kernel<<<1, 1024, 0, st>>>(ids, P, E, offsets, perm, pos);
+  permute_kernel<<<1, 1024, P <= kPermuteSmemIds ? size_t(P) * 4 : 0, st>>>(ids, P, E, offsets, perm, pos);
   count_launch();
   SMO_CUDA_CHECK(cudaGetLastError());
   if (x && xp && P > 0) {

@@ -18,4 +18,6 @@ pos = torch.randperm(T * k, device=dev).to(torch.int32)
 wts = torch.rand((T, k), device=dev)
 resid = torch.randn((T, h), device=dev)
 res["combine"] = round(kbench.timeit(lambda: ops.unpermute_combine_(resid, y, pos, wts)) * 1e6, 2)
+ids = torch.randint(0, 8, (T, 2), device=dev, dtype=torch.int32)
+res["permute"] = round(kbench.timeit(lambda: ops.permute(ids, 8)) * 1e6, 2)
 print(json.dumps(res))
