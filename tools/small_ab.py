@@ -20,4 +20,5 @@ resid = torch.randn((T, h), device=dev)
 res["combine"] = round(kbench.timeit(lambda: ops.unpermute_combine_(resid, y, pos, wts)) * 1e6, 2)
 ids = torch.randint(0, 8, (T, 2), device=dev, dtype=torch.int32)
 res["permute"] = round(kbench.timeit(lambda: ops.permute(ids, 8)) * 1e6, 2)
+res["permute+gather"] = round(kbench.timeit(lambda: ops.permute(ids, 8, xb)) * 1e6, 2)
 print(json.dumps(res))
